@@ -1,0 +1,211 @@
+/*
+ * ss_abi.h -- C ABI of the B200-native 3DSS surface-splatting hot path.
+ *
+ * libss_b200.so (built from paper_2605_05876_b200/csrc/) exports these entry
+ * points.  They are the seams of the reference package's Python hot path
+ * (surfsplat 0.1.0, a CPU numpy/numba package with no native ABI of its own):
+ * each function replaces one reference routine, cited per entry below, and the
+ * Python host mirror (paper_2605_05876_b200/) binds them with ctypes the way a
+ * maintainer would bind them from the reference.
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer owned by the caller (the torch
+ *    allocator in the host mirror); the library never allocates.  Scratch
+ *    buffers are sized by the caller from the formulas documented per entry.
+ *    Exceptions, passed by value from the HOST: the struct arguments
+ *    (SsCamera/SsCloud/SsEnv/... themselves, whose members are device
+ *    pointers), `background` (3 floats) and `origin3` (3 floats).
+ *  - `stream` is a cudaStream_t passed as void*.  All work is stream-ordered,
+ *    asynchronous and CUDA-graph capturable (no host synchronisation inside).
+ *  - Return value: SS_OK, SS_ERR_INVALID (bad argument, checked on the host
+ *    before any launch), or SS_ERR_CUDA (launch error; see ss_last_error()).
+ *  - Surfel parameters are float32 struct-of-arrays (surfels.py:80-105).
+ *    Per-view records are indexed by SOURCE surfel index (culled rows carry
+ *    rect = 0 and emit no pairs); the reference compacts kept rows in
+ *    ascending source order (preprocess.py:296), which is order-isomorphic,
+ *    so sort orders and tile lists are identical after the host re-indexes.
+ */
+#ifndef SS_ABI_H
+#define SS_ABI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SS_OK = 0, SS_ERR_INVALID = 1, SS_ERR_CUDA = 2 };
+
+#define SS_REC_FLOATS 24  /* 96-byte record, see SsRecord in csrc/ss_common.cuh */
+#define SS_ACC_FLOATS 20  /* per-record backward accumulator: 17 grads + ss + touch + pad */
+#define SS_KMAX_CAP 16    /* largest k_max the kernels accept (= reference default K_MAX) */
+
+typedef struct SsCamera {
+    double view[16];   /* row-major world->view (camera.py:28-48) */
+    double proj[16];   /* row-major view->clip, GL style (camera.py:17-25) */
+    int width, height;
+} SsCamera;
+
+typedef struct SsCloud {
+    const float *centers;       /* (n,3) */
+    const float *quats;         /* (n,4) wxyz */
+    const float *log_scales;    /* (n,2) */
+    const float *albedo_raw;    /* (n,3) pre-sigmoid */
+    const float *metallic_raw;  /* (n,)  */
+    const float *roughness_raw; /* (n,)  */
+    int n;
+} SsCloud;
+
+/* Prefiltered environment (shading.py:334-379) as consumed by shading. */
+typedef struct SsEnv {
+    const float *diffuse;   /* (He,We,3) */
+    const float *specular;  /* (L,He,We,3) */
+    const float *lut;       /* (R,R,2) BRDF LUT, row = roughness (shading.py:118-156) */
+    int he, we, levels, lut_res;
+} SsEnv;
+
+typedef struct SsPreprocessOpts {
+    float r_cut;       /* preprocess.py:19 */
+    float mip_sigma;   /* preprocess.py:34 */
+    int mip_enabled;
+    int tile;          /* rasterizer.py:22 */
+} SsPreprocessOpts;
+
+/* Colour sources of render() (rasterizer.py:341-350). */
+enum { SS_COLOR_EXPLICIT = 0, SS_COLOR_IBL = 1, SS_COLOR_ALBEDO = 2 };
+
+/* Optional per-surfel outputs of preprocess (ProjectedSurfels fields,
+ * preprocess.py:195-228), all (n, ...) and nullable. */
+typedef struct SsProjAux {
+    float *c_cam, *tu_cam, *tv_cam;   /* (n,3) */
+    float *eps_z;                     /* (n,)  */
+    float *center_ndc;                /* (n,2) */
+    float *jac;                       /* (n,2,2) */
+    uint8_t *jac_ok;                  /* (n,)  */
+    float *colors;                    /* (n,3) the per-surfel colours used */
+    int32_t *cells;                   /* (n,15) shading branch signature (shading.py:490-497) */
+} SsProjAux;
+
+/* ---- preprocess + shade + tile count --------------------------------------
+ * Replaces preprocess() (preprocess.py:231-309), shade_surfels()
+ * (shading.py:447-503) and the count half of bin_and_sort()
+ * (rasterizer.py:92-106).  Writes one 96-byte record per surfel, the cull code
+ * (0-4, preprocess.py:23-27), the per-record pair count and accumulates the
+ * per-tile pair histogram `tile_counts` (ntiles ints, zeroed by the caller).
+ * color_source: SS_COLOR_EXPLICIT reads `colors_in` (n,3); SS_COLOR_IBL shades
+ * against `env`; SS_COLOR_ALBEDO uses sigmoid(albedo_raw).  `flags` (int[4],
+ * zeroed by caller) receives [0] zero-norm quaternion seen, [1] non-finite
+ * colour seen. */
+int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                  int color_source, const float *colors_in, const SsEnv *env,
+                  float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
+                  const SsProjAux *aux, int32_t *flags, void *stream);
+
+/* ---- tile binning with deterministic order ---------------------------------
+ * Replaces the rest of bin_and_sort() (rasterizer.py:106-116): exclusive scan
+ * of tile_counts into tile_offsets (ntiles+1 int32), bucket scatter of
+ * (z_start, record) keys, and a per-tile sort by (z_start, record index) so
+ * the result equals np.lexsort((rec, z_start, tile)) bit for bit.
+ * pair_capacity bounds pair_rec/keys; flags[2] is set when it overflowed.
+ * keys: uint64 scratch of pair_capacity entries; cursors: ntiles ints scratch. */
+int ss_bin_sort(int n, const float *records, const int8_t *cull, int width, int height, int tile,
+                const int32_t *tile_counts, int32_t *tile_offsets, int32_t *cursors,
+                uint64_t *keys, int32_t *pair_rec, int64_t pair_capacity, int32_t *flags,
+                void *stream);
+
+/* ---- raster forward -------------------------------------------------------
+ * Replaces _forward_kernel (rasterizer.py:119-249), interval depth mode.
+ * rgb (H,W,3), alpha/depth (H,W) float32, nlayers (H,W) int32 are written for
+ * every pixel.  Nullable extras: pair_cover (per pair int32, with_cover_counts),
+ * stacks (collect_stacks; st_w/st_z/st_z2 (H,W,k), st_c (H,W,k,3), st_n (H,W,k)),
+ * discarded (1 int64, the discarded_overflow statistic). */
+typedef struct SsStacks { float *w, *c, *z, *z2; int32_t *n; } SsStacks;
+int ss_raster_forward(int width, int height, int tile, const int32_t *tile_offsets,
+                      const int32_t *pair_rec, const float *records, const float *background,
+                      int k_max, float *rgb, float *alpha, float *depth, int32_t *nlayers,
+                      int32_t *pair_cover, const SsStacks *stacks, unsigned long long *discarded,
+                      void *stream);
+
+/* ---- raster backward ------------------------------------------------------
+ * Replaces _backward_kernel (backward.py:48-321) and the pair reduction
+ * (backward.py:382-396).  g_rgb (H,W,3) / g_alpha (H,W) float32 upstream
+ * gradients (g_alpha nullable).  Accumulates into rec_acc (n x 20 float,
+ * zeroed by the caller): [0:3] dt1, [3:6] dt2, [6:9] dt4, [9:12] dSigma^-1,
+ * [12] dn_f, [13:16] dcolour, [16] dview_z, [17] screen-space |g| sum,
+ * [18] covering-pixel count (as float bits of an int32 counter).  cons_loss
+ * (1 double, zeroed) receives the consolidation penalty value. */
+int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offsets,
+                       const int32_t *pair_rec, const float *records, const float *background,
+                       int k_max, const float *g_rgb, const float *g_alpha, float cons_scale,
+                       float *rec_acc, double *cons_loss, void *stream);
+
+/* ---- chain backward -------------------------------------------------------
+ * Replaces the per-surfel tail of backward_image() (backward.py:398-461,
+ * 473-548), shade_backward() (shading.py:525-616) and quat_frame_backward()
+ * (surfels.py:54-77).  Reads rec_acc and ADDS into the parameter gradients
+ * (so multi-view steps accumulate in place): g_centers (n,3), g_quats (n,4),
+ * g_log_scales (n,2), g_albedo_raw (n,3), g_metallic_raw, g_roughness_raw,
+ * g_colors (n,3, nullable), ss_grad (n), touched (n int32 counts).  With
+ * SS_COLOR_IBL it also scatters the derived-map gradients into d_diffuse
+ * (He,We,3) and d_specular (L,He,We,3) (float, accumulated). */
+typedef struct SsGrads {
+    float *centers, *quats, *log_scales, *albedo_raw, *metallic_raw, *roughness_raw;
+    float *colors;     /* nullable */
+    float *ss_grad;
+    int32_t *touched;
+    float *d_diffuse, *d_specular;   /* nullable unless SS_COLOR_IBL */
+} SsGrads;
+int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                      int color_source, const SsEnv *env, const int8_t *cull,
+                      const float *rec_acc, const SsGrads *grads, void *stream);
+
+/* ---- environment ----------------------------------------------------------
+ * ss_brdf_lut: brdf_lut() (shading.py:118-156) -> lut (res,res,2) float.
+ * ss_env_refresh: EnvironmentLight.refresh (shading.py:369-379): base_log
+ *   (He,We,3) -> base, diffuse (He,We,3), specular (L,He,We,3).
+ * ss_env_adjoint: env_gradient (shading.py:381-394): d_diffuse, d_specular
+ *   -> d_base_log (He,We,3) (and d_base when non-null).
+ * Both need the diffuse row sums: ss_env_rowsums fills rowsum (He*We floats). */
+int ss_brdf_lut(int res, int samples, float *lut, void *stream);
+int ss_env_rowsums(int he, int we, float *rowsum, void *stream);
+int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log,
+                   const float *rowsum, float *base, float *diffuse, float *specular, void *stream);
+int ss_env_adjoint(int he, int we, int levels, int samples, const float *base,
+                   const float *rowsum, const float *d_diffuse, const float *d_specular,
+                   float *d_base, float *d_base_log, void *stream);
+
+/* ---- optimiser ------------------------------------------------------------
+ * Adam.step (adam.py:21-41) fused over one parameter tensor of `count`
+ * floats; m, v float32 state; bias corrections from step t (>= 1). */
+int ss_adam_step(int64_t count, float *param, const float *grad, float *m, float *v,
+                 int t, float lr, float beta1, float beta2, float eps, void *stream);
+/* q <- q / |q| after the step (train.py:246). */
+int ss_normalize_quats(int n, float *quats, void *stream);
+
+/* ---- refinement scan (densify.py:101-202) ---------------------------------
+ * Isolation prune (densify.py:118-123): isolated[i] = 1 iff no other centre
+ * lies within 3 * max(exp(log_scales[i])).  Fixed-radius existence query on a
+ * uniform grid: ss_grid_cells writes each centre's linear cell id
+ * ((x*dim + y)*dim + z, axes clamped to [0, dim), dim <= 1024); the caller
+ * sorts the ids (sorted_cells, with the permutation `order`); ss_isolation
+ * visits the cells overlapping each query ball by binary search. */
+int ss_grid_cells(int n, const float *centers, const float *origin3, float cell, int dim,
+                  int32_t *cell_of, void *stream);
+int ss_isolation(int n, const float *centers, const float *log_scales, const int32_t *order,
+                 const int32_t *sorted_cells, const float *origin3, float cell, int dim,
+                 uint8_t *isolated, void *stream);
+/* Split children (densify.py:60-98): parent rows `parents` (nsplit) produce
+ * the (+) child at out row plus_row0+k and the (-) child at minus_row0+k;
+ * only centres and log-scales differ from the parent (the caller copies the
+ * other attributes). `origin3` is a HOST pointer. */
+int ss_split_children(int nsplit, const int32_t *parents, const float *centers, const float *quats,
+                      const float *log_scales, float *out_centers, float *out_log_scales,
+                      int64_t plus_row0, int64_t minus_row0, void *stream);
+
+const char *ss_last_error(void);
+int ss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_ABI_H */

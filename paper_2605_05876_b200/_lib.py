@@ -1,0 +1,158 @@
+"""ctypes binding of libss_b200.so (include/ss_abi.h).
+
+This is the only place the host mirror touches native code.  It fails loudly:
+there is no CPU path, so a missing library or a missing CUDA device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "libss_b200.so")
+
+SS_OK, SS_ERR_INVALID, SS_ERR_CUDA = 0, 1, 2
+SS_COLOR_EXPLICIT, SS_COLOR_IBL, SS_COLOR_ALBEDO = 0, 1, 2
+REC_FLOATS = 24
+ACC_FLOATS = 20
+KMAX_CAP = 16
+
+c_p = ctypes.c_void_p
+
+
+class SsCamera(ctypes.Structure):
+    _fields_ = [("view", ctypes.c_double * 16), ("proj", ctypes.c_double * 16),
+                ("width", ctypes.c_int), ("height", ctypes.c_int)]
+
+
+class SsCloud(ctypes.Structure):
+    _fields_ = [("centers", c_p), ("quats", c_p), ("log_scales", c_p), ("albedo_raw", c_p),
+                ("metallic_raw", c_p), ("roughness_raw", c_p), ("n", ctypes.c_int)]
+
+
+class SsEnv(ctypes.Structure):
+    _fields_ = [("diffuse", c_p), ("specular", c_p), ("lut", c_p), ("he", ctypes.c_int),
+                ("we", ctypes.c_int), ("levels", ctypes.c_int), ("lut_res", ctypes.c_int)]
+
+
+class SsPreprocessOpts(ctypes.Structure):
+    _fields_ = [("r_cut", ctypes.c_float), ("mip_sigma", ctypes.c_float),
+                ("mip_enabled", ctypes.c_int), ("tile", ctypes.c_int)]
+
+
+class SsProjAux(ctypes.Structure):
+    _fields_ = [("c_cam", c_p), ("tu_cam", c_p), ("tv_cam", c_p), ("eps_z", c_p),
+                ("center_ndc", c_p), ("jac", c_p), ("jac_ok", c_p), ("colors", c_p), ("cells", c_p)]
+
+
+class SsStacks(ctypes.Structure):
+    _fields_ = [("w", c_p), ("c", c_p), ("z", c_p), ("z2", c_p), ("n", c_p)]
+
+
+class SsGrads(ctypes.Structure):
+    _fields_ = [("centers", c_p), ("quats", c_p), ("log_scales", c_p), ("albedo_raw", c_p),
+                ("metallic_raw", c_p), ("roughness_raw", c_p), ("colors", c_p), ("ss_grad", c_p),
+                ("touched", c_p), ("d_diffuse", c_p), ("d_specular", c_p)]
+
+
+_lib = None
+
+_SIGNATURES = {
+    "ss_preprocess": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_bin_sort": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
+                    c_p, c_p, ctypes.c_int64, c_p, c_p],
+    "ss_raster_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
+                          ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_raster_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
+                           ctypes.POINTER(ctypes.c_float), ctypes.c_int, c_p, c_p, ctypes.c_float, c_p, c_p, c_p],
+    "ss_chain_backward": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p],
+    "ss_brdf_lut": [ctypes.c_int, ctypes.c_int, c_p, c_p],
+    "ss_env_rowsums": [ctypes.c_int, ctypes.c_int, c_p, c_p],
+    "ss_env_refresh": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_env_adjoint": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_adam_step": [ctypes.c_int64, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_float, ctypes.c_float,
+                     ctypes.c_float, ctypes.c_float, c_p],
+    "ss_normalize_quats": [ctypes.c_int, c_p, c_p],
+    "ss_grid_cells": [ctypes.c_int, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_int, c_p, c_p],
+    "ss_isolation": [ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float,
+                     ctypes.c_int, c_p, c_p],
+    "ss_split_children": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64, c_p],
+}
+
+EXPORTED = [k for k in _SIGNATURES] + ["ss_last_error", "ss_version"]
+
+
+def load(require_cuda=True):
+    """Load the library (does not need a GPU); with require_cuda, also insist
+    on a CUDA device since every entry point launches kernels."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libss_b200.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, argt in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            if argt is not None:
+                fn.argtypes = argt
+            fn.restype = ctypes.c_int
+        lib.ss_last_error.restype = ctypes.c_char_p
+        lib.ss_version.restype = ctypes.c_int
+        _lib = lib
+    if require_cuda and not torch.cuda.is_available():
+        raise RuntimeError("paper_2605_05876_b200 needs a CUDA (sm_100a) device; there is no CPU path")
+    return _lib
+
+
+def check(rc, what):
+    if rc == SS_OK:
+        return
+    if rc == SS_ERR_INVALID:
+        raise ValueError(f"{what}: invalid argument")
+    msg = _lib.ss_last_error().decode() if _lib is not None else "?"
+    raise RuntimeError(f"{what}: CUDA error: {msg}")
+
+
+def ptr(t):
+    """Device pointer of a contiguous tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return c_p(t.data_ptr())
+
+
+def stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return c_p(s.cuda_stream)
+
+
+def fvec(vals):
+    arr = (ctypes.c_float * len(vals))(*[float(v) for v in vals])
+    return ctypes.cast(arr, ctypes.POINTER(ctypes.c_float)), arr
+
+
+def make_camera(cam):
+    c = SsCamera()
+    v = np.ascontiguousarray(cam.view, dtype=np.float64).reshape(16)
+    p = np.ascontiguousarray(cam.proj, dtype=np.float64).reshape(16)
+    for k in range(16):
+        c.view[k] = float(v[k])
+        c.proj[k] = float(p[k])
+    c.width, c.height = int(cam.width), int(cam.height)
+    return c
+
+
+def make_cloud(cloud):
+    return SsCloud(ptr(cloud.centers), ptr(cloud.quats), ptr(cloud.log_scales), ptr(cloud.albedo_raw),
+                   ptr(cloud.metallic_raw), ptr(cloud.roughness_raw), len(cloud))
+
+
+def make_env(env):
+    if env is None:
+        return None
+    he, we = env.shape
+    return SsEnv(ptr(env.diffuse), ptr(env.specular), ptr(env.lut), he, we, env.levels, env.lut.shape[0])

@@ -1,0 +1,102 @@
+"""backward_image() API (mirror of surfsplat.backward, backward.py:29-470).
+
+Two native launches per view: the tile-CTA raster backward (pixel replays,
+per-layer suffix recursion, consolidation, warp-reduced per-record atomics)
+and the per-surfel chain kernel (MIP chain, rows -> world, shading adjoint
+with the derived-map scatter, quaternion adjoint).  With IBL colours the env
+adjoint kernel finishes the environment gradient.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .preprocess import make_opts
+
+
+@dataclass
+class BackwardResult:
+    centers: torch.Tensor
+    quats: torch.Tensor
+    log_scales: torch.Tensor
+    albedo_raw: torch.Tensor
+    metallic_raw: torch.Tensor
+    roughness_raw: torch.Tensor
+    colors: torch.Tensor
+    env_base_log: torch.Tensor | None
+    background: torch.Tensor
+    ss_grad: torch.Tensor
+    touched: torch.Tensor
+    cons_loss: float
+    touch_count: torch.Tensor | None = None
+    d_diffuse: torch.Tensor | None = None
+    d_specular: torch.Tensor | None = None
+
+
+def zero_grads(n, dev):
+    z = lambda *s: torch.zeros(s, device=dev, dtype=torch.float32)
+    return {"centers": z(n, 3), "quats": z(n, 4), "log_scales": z(n, 2), "albedo_raw": z(n, 3),
+            "metallic_raw": z(n), "roughness_raw": z(n), "colors": z(n, 3), "ss_grad": z(n),
+            "touched": torch.zeros(n, device=dev, dtype=torch.int32)}
+
+
+def grads_struct(g, d_diffuse=None, d_specular=None):
+    return _lib.SsGrads(*(_lib.ptr(g[k]) for k in ("centers", "quats", "log_scales", "albedo_raw", "metallic_raw",
+                                                   "roughness_raw")),
+                        _lib.ptr(g.get("colors")), _lib.ptr(g["ss_grad"]), _lib.ptr(g["touched"]),
+                        _lib.ptr(d_diffuse), _lib.ptr(d_specular))
+
+
+def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0) -> BackwardResult:
+    opt = result.options
+    if opt.depth_mode != "interval":
+        raise ValueError("backward requires depth_mode='interval'")
+    if result.state is None:
+        raise ValueError("result was not produced by paper_2605_05876_b200.render")
+    lib = _lib.load()
+    st = result.state
+    dev = st.records.device
+    cam = result.camera
+    H, W = int(cam.height), int(cam.width)
+    n = len(cloud)
+    g_rgb = torch.zeros((H, W, 3), device=dev) if g_rgb is None else torch.as_tensor(g_rgb, device=dev)
+    g_rgb = g_rgb.to(torch.float32).contiguous()
+    ga = None if g_alpha is None else torch.as_tensor(g_alpha, device=dev).to(torch.float32).contiguous()
+    acc = torch.zeros((n, _lib.ACC_FLOATS), device=dev, dtype=torch.float32)
+    cons = torch.zeros(1, device=dev, dtype=torch.float64)
+    bgp, _keep = _lib.fvec(opt.background)
+    rc = lib.ss_raster_backward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
+                                _lib.ptr(st.records), bgp, int(opt.k_max), _lib.ptr(g_rgb), _lib.ptr(ga),
+                                float(cons_scale), _lib.ptr(acc), _lib.ptr(cons), _lib.stream_ptr())
+    _lib.check(rc, "ss_raster_backward")
+    g = zero_grads(n, dev)
+    env = result.env
+    ibl = result.color_source == "ibl"
+    d_diff = d_spec = None
+    if ibl:
+        d_diff = torch.zeros_like(env.base)
+        d_spec = torch.zeros_like(env.specular)
+    source = {"explicit": _lib.SS_COLOR_EXPLICIT, "ibl": _lib.SS_COLOR_IBL, "albedo": _lib.SS_COLOR_ALBEDO}[result.color_source]
+    cl = _lib.make_cloud(cloud)
+    camst = _lib.make_camera(cam)
+    po = make_opts(opt.preprocess_options(), int(opt.tile))
+    envs = _lib.make_env(env) if ibl else None
+    gs = grads_struct(g, d_diff, d_spec)
+    rc = lib.ss_chain_backward(ctypes.byref(cl), ctypes.byref(camst), ctypes.byref(po), source,
+                               ctypes.byref(envs) if envs is not None else None, _lib.ptr(st.cull), _lib.ptr(acc),
+                               ctypes.byref(gs), _lib.stream_ptr())
+    _lib.check(rc, "ss_chain_backward")
+    g_env = None
+    if ibl:
+        _, g_env = env.env_gradient(d_diff, d_spec)
+    g_bg = (g_rgb * (1.0 - result.alpha)[..., None]).sum(dim=(0, 1))
+    return BackwardResult(centers=g["centers"], quats=g["quats"], log_scales=g["log_scales"],
+                          albedo_raw=g["albedo_raw"], metallic_raw=g["metallic_raw"],
+                          roughness_raw=g["roughness_raw"], colors=g["colors"], env_base_log=g_env,
+                          background=g_bg, ss_grad=g["ss_grad"], touched=g["touched"] > 0,
+                          cons_loss=float(cons.item()), touch_count=g["touched"], d_diffuse=d_diff,
+                          d_specular=d_spec)

@@ -1,0 +1,176 @@
+// binning.cu -- tile binning with a deterministic (tile, z_start, record)
+// order, sync-free (all counts stay on the device).
+//
+// Reference: bin_and_sort (rasterizer.py:92-116) = emit pairs, np.lexsort by
+// (tile, z_start[rec], rec), offsets by bincount.  B200 design:
+//   1. the preprocess kernel already built the per-tile histogram;
+//   2. tile_scan: one CTA scans it into tile_offsets (the output) and checks
+//      the pair capacity;
+//   3. scatter: each record drops a 64-bit key (orderable z_start << 32 | rec)
+//      into every tile bucket of its rect (unordered, atomics);
+//   4. tile_sort: one CTA per tile sorts its bucket in shared memory with a
+//      padding-free bitonic network.  Keys are unique (rec in the low bits),
+//      so the order is total and equals lexsort's stable tie-break exactly.
+#include "ss_common.cuh"
+
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kSortThreads = 512;
+constexpr int kSortCap = 8192;  // keys per tile sorted in shared memory (64 KB)
+
+__device__ __forceinline__ uint32_t orderable(float z) {
+    uint32_t u = __float_as_uint(z == 0.0f ? 0.0f : z);  // -0.0 == +0.0 like lexsort
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
+    const int32_t *__restrict__ counts, int ntiles, int32_t *__restrict__ offsets,
+    int32_t *__restrict__ cursors, int64_t capacity, int32_t *__restrict__ flags)
+{
+    __shared__ int32_t warp_sums[kScanThreads / 32];
+    __shared__ int32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int base = 0; base < ntiles; base += kScanThreads) {
+        int t = base + threadIdx.x;
+        int v = t < ntiles ? counts[t] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int s = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        int excl = carry + (wid > 0 ? warp_sums[wid - 1] : 0) + x - v;
+        if (t < ntiles) {
+            offsets[t] = excl;
+            cursors[t] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == kScanThreads - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        offsets[ntiles] = carry;
+        if ((int64_t)carry > capacity) atomicOr(&flags[2], 1);
+    }
+}
+
+__global__ void __launch_bounds__(256) scatter_kernel(
+    int n, const SsRecord *__restrict__ records, const int8_t *__restrict__ cull, int ntx, int tile,
+    const int32_t *__restrict__ offsets, int32_t *__restrict__ cursors, uint64_t *__restrict__ keys,
+    int64_t capacity)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || cull[i] != 0) return;
+    const int4 r = records[i].r;
+    const float zs = records[i].d.z;
+    const uint64_t key = ((uint64_t)orderable(zs) << 32) | (uint32_t)i;
+    int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            int t = ty * ntx + tx;
+            int64_t at = (int64_t)offsets[t] + atomicAdd(&cursors[t], 1);
+            if (at < capacity) keys[at] = key;
+        }
+}
+
+// Ascending bitonic network on n elements padded (virtually) with +inf up to
+// a power of two: every comparator is ascending, so a pair whose upper index
+// is past the end never exchanges and the padding never has to exist.
+template <typename Load, typename Swap>
+__device__ __forceinline__ void bitonic_sort(int n, Load ld, Swap sw) {
+    int N = 1;
+    while (N < n) N <<= 1;
+    for (int k = 2; k <= N; k <<= 1) {
+        const int hk = k >> 1;
+        for (int p = threadIdx.x; p < (N >> 1); p += blockDim.x) {
+            int blk = p / hk, off = p % hk;
+            int lo = blk * k + off, hi = blk * k + k - 1 - off;
+            if (hi < n) sw(lo, hi);
+        }
+        __syncthreads();
+        for (int j = hk >> 1; j >= 1; j >>= 1) {
+            for (int p = threadIdx.x; p < (N >> 1); p += blockDim.x) {
+                int lo = (p / j) * 2 * j + (p % j), hi = lo + j;
+                if (hi < n) sw(lo, hi);
+            }
+            __syncthreads();
+        }
+    }
+    (void)ld;
+}
+
+__global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(
+    const int32_t *__restrict__ offsets, uint64_t *__restrict__ keys, int32_t *__restrict__ pair_rec,
+    int64_t capacity)
+{
+    extern __shared__ uint64_t skeys[];
+    const int t = blockIdx.x;
+    const int64_t o0 = offsets[t];
+    int64_t o1 = offsets[t + 1];
+    if (o1 > capacity) o1 = capacity;
+    if (o0 >= o1) return;
+    const int n = (int)(o1 - o0);
+    uint64_t *g = keys + o0;
+    if (n <= kSortCap) {
+        for (int k = threadIdx.x; k < n; k += blockDim.x) skeys[k] = g[k];
+        __syncthreads();
+        bitonic_sort(n, 0, [&](int a, int b) {
+            uint64_t x = skeys[a], y = skeys[b];
+            if (x > y) { skeys[a] = y; skeys[b] = x; }
+        });
+        for (int k = threadIdx.x; k < n; k += blockDim.x) pair_rec[o0 + k] = (int32_t)(uint32_t)skeys[k];
+    } else {
+        // rare oversized tile: same network directly in global memory
+        bitonic_sort(n, 0, [&](int a, int b) {
+            uint64_t x = g[a], y = g[b];
+            if (x > y) { g[a] = y; g[b] = x; }
+        });
+        for (int k = threadIdx.x; k < n; k += blockDim.x) pair_rec[o0 + k] = (int32_t)(uint32_t)g[k];
+    }
+}
+
+}  // namespace
+
+extern "C" int ss_bin_sort(int n, const float *records, const int8_t *cull, int width, int height, int tile,
+                           const int32_t *tile_counts, int32_t *tile_offsets, int32_t *cursors,
+                           uint64_t *keys, int32_t *pair_rec, int64_t pair_capacity, int32_t *flags,
+                           void *stream)
+{
+    if (width <= 0 || height <= 0 || tile <= 0 || !tile_counts || !tile_offsets || !cursors || !flags)
+        return SS_ERR_INVALID;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSortCap * (int)sizeof(uint64_t));
+        attr_set = true;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int ntx = (width + tile - 1) / tile, nty = (height + tile - 1) / tile;
+    const int ntiles = ntx * nty;
+    tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tile_counts, ntiles, tile_offsets, cursors, pair_capacity, flags);
+    SS_CUDA_CHECK_LAUNCH();
+    if (n > 0) {
+        scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, reinterpret_cast<const SsRecord *>(records), cull,
+                                                        ntx, tile, tile_offsets, cursors, keys, pair_capacity);
+        SS_CUDA_CHECK_LAUNCH();
+    }
+    tile_sort_kernel<<<ntiles, kSortThreads, kSortCap * sizeof(uint64_t), st>>>(tile_offsets, keys, pair_rec,
+                                                                               pair_capacity);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}

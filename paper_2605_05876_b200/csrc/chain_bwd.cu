@@ -1,0 +1,277 @@
+// chain_bwd.cu -- per-surfel tail of the backward pass, float64 like the
+// reference: MIP-filter chain (backward.py:473-548), T rows -> camera ->
+// world (backward.py:398-441), shading adjoint (shading.py:525-615) with the
+// derived-map scatter, activations, and the quaternion adjoint
+// (surfels.py:54-77).  One thread per surfel; the projection state is
+// recomputed from the 56 B of parameters (cheaper than storing it), so the
+// kernel streams params + the 80 B record accumulator and ADDS 14 parameter
+// gradients + stats (multi-view steps accumulate in place, no extra pass).
+#include "ss_common.cuh"
+#include "shading.cuh"
+
+namespace {
+
+struct ChainParams {
+    SsCloud cloud;
+    double view[16], proj[16], cam_pos[3];
+    float viewf[16], projf[16];
+    int W, H, mip, color_source;
+    double sigma;
+    float r_cut, sigma_f;
+    SsEnv env;
+    const int8_t *cull;
+    const float *acc;
+    SsGrads g;
+};
+
+__device__ __forceinline__ float dot_gemm(float a0, float a1, float a2, float b0, float b1, float b2) {
+    return __fmaf_rn(a2, b2, __fmaf_rn(a1, b1, fm(a0, b0)));
+}
+__device__ __forceinline__ float dot_gemv(float a0, float a1, float a2, float v0, float v1, float v2) {
+    return __fmaf_rn(a2, v2, __fmaf_rn(a0, v0, fm(a1, v1)));
+}
+
+// T rows of surfel i, bit-identical to the preprocess kernel (explicit
+// round-to-nearest ops so this file's FMA contraction cannot change them).
+__device__ __forceinline__ void rows_of(const ChainParams &P, int i, float t1[3], float t2[3], float t4[3]) {
+    const SsCloud &c = P.cloud;
+    const float c0 = c.centers[3 * i], c1 = c.centers[3 * i + 1], c2 = c.centers[3 * i + 2];
+    const float4 q = reinterpret_cast<const float4 *>(c.quats)[i];
+    const float2 ls = reinterpret_cast<const float2 *>(c.log_scales)[i];
+    const float nrm = __fsqrt_rn(fa(fa(fa(fm(q.x, q.x), fm(q.y, q.y)), fm(q.z, q.z)), fm(q.w, q.w)));
+    const float w = fd(q.x, nrm), x = fd(q.y, nrm), y = fd(q.z, nrm), z = fd(q.w, nrm);
+    const float uh0 = fs(1.f, fm(2.f, fa(fm(y, y), fm(z, z)))), uh1 = fm(2.f, fa(fm(x, y), fm(w, z))),
+                uh2 = fm(2.f, fs(fm(x, z), fm(w, y)));
+    const float vh0 = fm(2.f, fs(fm(x, y), fm(w, z))), vh1 = fs(1.f, fm(2.f, fa(fm(x, x), fm(z, z)))),
+                vh2 = fm(2.f, fa(fm(y, z), fm(w, x)));
+    const float su = (float)exp((double)ls.x), sv = (float)exp((double)ls.y);
+    const float su0 = fm(su, uh0), su1 = fm(su, uh1), su2 = fm(su, uh2);
+    const float sv0 = fm(sv, vh0), sv1 = fm(sv, vh1), sv2 = fm(sv, vh2);
+    float cc[3], tu[3], tv[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const float R0 = P.viewf[4 * r], R1 = P.viewf[4 * r + 1], R2 = P.viewf[4 * r + 2];
+        cc[r] = fa(dot_gemm(c0, c1, c2, R0, R1, R2), P.viewf[4 * r + 3]);
+        tu[r] = dot_gemm(su0, su1, su2, R0, R1, R2);
+        tv[r] = dot_gemm(sv0, sv1, sv2, R0, R1, R2);
+    }
+    const int irs[3] = {0, 1, 3};
+    float *rows[3] = {t1, t2, t4};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float *Pr = P.projf + 4 * irs[k];
+        rows[k][0] = dot_gemv(tu[0], tu[1], tu[2], Pr[0], Pr[1], Pr[2]);
+        rows[k][1] = dot_gemv(tv[0], tv[1], tv[2], Pr[0], Pr[1], Pr[2]);
+        rows[k][2] = fa(dot_gemv(cc[0], cc[1], cc[2], Pr[0], Pr[1], Pr[2]), Pr[3]);
+    }
+}
+
+__global__ void __launch_bounds__(128) chain_kernel(ChainParams P)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.cloud.n || P.cull[i] != 0) return;
+    const float *a = P.acc + (size_t)i * SS_ACC_FLOATS;
+    const float4 a0 = reinterpret_cast<const float4 *>(a)[0];
+    const float4 a1 = reinterpret_cast<const float4 *>(a)[1];
+    const float4 a2 = reinterpret_cast<const float4 *>(a)[2];
+    const float4 a3 = reinterpret_cast<const float4 *>(a)[3];
+    const float4 a4 = reinterpret_cast<const float4 *>(a)[4];
+    double G1[3] = {a0.x, a0.y, a0.z}, G2[3] = {a0.w, a1.x, a1.y}, G4[3] = {a1.z, a1.w, a2.x};
+    const double gs0 = a2.y, gs1 = a2.z, gs2 = a2.w, gnf = a3.x;
+    const double gcol[3] = {a3.y, a3.z, a3.w};
+    const double gz = a4.x;
+    const float ss = a4.y;
+    const int touch = __float_as_int(a4.z);
+
+    float t1f[3], t2f[3], t4f[3];
+    rows_of(P, i, t1f, t2f, t4f);
+    if (P.mip) {
+        // _mip_chain_backward (backward.py:473-548)
+        float jf[4];
+        const bool ok = ss_center_jacobian(t1f, t2f, t4f, P.W, P.H, jf);
+        const double j00 = jf[0], j01 = jf[1], j10 = jf[2], j11 = jf[3];
+        const double sg = P.sigma;
+        const double s00 = 1.0 + sg * (j00 * j00 + j01 * j01);
+        const double s01 = sg * (j00 * j10 + j01 * j11);
+        const double s11 = 1.0 + sg * (j10 * j10 + j11 * j11);
+        const double det = s00 * s11 - s01 * s01;
+        const double b00 = s11 / det, b01 = -s01 / det, b11 = s00 / det;
+        const double nf = 1.0 / sqrt(det);
+        const double g00 = gs0, g01 = 0.5 * gs1, g11 = gs2;
+        const double bg00 = b00 * g00 + b01 * g01, bg01 = b00 * g01 + b01 * g11;
+        const double bg10 = b01 * g00 + b11 * g01, bg11 = b01 * g01 + b11 * g11;
+        const double ga00 = -(bg00 * b00 + bg01 * b01) - 0.5 * gnf * nf * b00;
+        const double ga01 = -(bg00 * b01 + bg01 * b11) - 0.5 * gnf * nf * b01;
+        const double ga11 = -(bg10 * b01 + bg11 * b11) - 0.5 * gnf * nf * b11;
+        if (ok) {
+            const double ts = 2.0 * sg;
+            const double gj00 = ts * (ga00 * j00 + ga01 * j10), gj01 = ts * (ga00 * j01 + ga01 * j11);
+            const double gj10 = ts * (ga01 * j00 + ga11 * j10), gj11 = ts * (ga01 * j01 + ga11 * j11);
+            const double T1[3] = {t1f[0], t1f[1], t1f[2]}, T2[3] = {t2f[0], t2f[1], t2f[2]}, T4[3] = {t4f[0], t4f[1], t4f[2]};
+            const double d4 = T4[2], cx = T1[2] / d4, cy = T2[2] / d4;
+            const double dx = 1.0 / P.W, dy = 1.0 / P.H;
+            const double pr[4][4] = {{cx + dx, cy, gj00, gj10}, {cx - dx, cy, -gj00, -gj10},
+                                     {cx, cy + dy, gj01, gj11}, {cx, cy - dy, -gj01, -gj11}};
+            double gcx = 0.0, gcy = 0.0;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const double px = pr[p][0], py = pr[p][1];
+                double k[3], l[3];
+                for (int c = 0; c < 3; ++c) { k[c] = px * T4[c] - T1[c]; l[c] = py * T4[c] - T2[c]; }
+                const double p0 = k[1] * l[2] - k[2] * l[1];
+                const double p1 = k[2] * l[0] - k[0] * l[2];
+                const double den = k[0] * l[1] - k[1] * l[0];
+                if (!(fabs(den) >= SS_DENOM_EPS)) continue;
+                const double u = p0 / den, v = p1 / den;
+                const double gu = pr[p][2], gv = pr[p][3];
+                const double gp[3] = {gu / den, gv / den, -(gu * u + gv * v) / den};
+                const double gk[3] = {l[1] * gp[2] - l[2] * gp[1], l[2] * gp[0] - l[0] * gp[2], l[0] * gp[1] - l[1] * gp[0]};
+                const double gl[3] = {gp[1] * k[2] - gp[2] * k[1], gp[2] * k[0] - gp[0] * k[2], gp[0] * k[1] - gp[1] * k[0]};
+                for (int c = 0; c < 3; ++c) {
+                    G1[c] -= gk[c];
+                    G2[c] -= gl[c];
+                    G4[c] += px * gk[c] + py * gl[c];
+                }
+                gcx += (gk[0] * T4[0] + gk[1] * T4[1]) + gk[2] * T4[2];
+                gcy += (gl[0] * T4[0] + gl[1] * T4[1]) + gl[2] * T4[2];
+            }
+            G1[2] += gcx / d4;
+            G4[2] -= gcx * cx / d4;
+            G2[2] += gcy / d4;
+            G4[2] -= gcy * cy / d4;
+        }
+    }
+    // T rows -> camera (backward.py:405-410)
+    const double *pm = P.proj;
+    double gtu[3], gtv[3], gcc[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        gtu[c] = G1[0] * pm[c] + G2[0] * pm[4 + c] + G4[0] * pm[12 + c];
+        gtv[c] = G1[1] * pm[c] + G2[1] * pm[4 + c] + G4[1] * pm[12 + c];
+        gcc[c] = G1[2] * pm[c] + G2[2] * pm[4 + c] + G4[2] * pm[12 + c];
+    }
+    gcc[2] -= gz;
+    // camera -> world (backward.py:412-441)
+    double gw[3], guw[3], gvw[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        gw[k] = (gcc[0] * P.view[k] + gcc[1] * P.view[4 + k]) + gcc[2] * P.view[8 + k];
+        guw[k] = (gtu[0] * P.view[k] + gtu[1] * P.view[4 + k]) + gtu[2] * P.view[8 + k];
+        gvw[k] = (gtv[0] * P.view[k] + gtv[1] * P.view[4 + k]) + gtv[2] * P.view[8 + k];
+    }
+    const SsCloud &cl = P.cloud;
+    const double q0 = cl.quats[4 * i], q1 = cl.quats[4 * i + 1], q2 = cl.quats[4 * i + 2], q3 = cl.quats[4 * i + 3];
+    const double qn = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
+    const double w = q0 / qn, x = q1 / qn, y = q2 / qn, z = q3 / qn;
+    const double uh[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
+    const double vh[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
+    const double su = exp((double)cl.log_scales[2 * i]), sv = exp((double)cl.log_scales[2 * i + 1]);
+    const double gsu = (guw[0] * uh[0] + guw[1] * uh[1]) + guw[2] * uh[2];
+    const double gsv = (gvw[0] * vh[0] + gvw[1] * vh[1]) + gvw[2] * vh[2];
+    double gU[3], gV[3], gN[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < 3; ++k) { gU[k] = su * guw[k]; gV[k] = sv * gvw[k]; }
+    double gcent[3] = {gw[0], gw[1], gw[2]};
+    double galb[3] = {0.0, 0.0, 0.0}, gmet = 0.0, grough = 0.0;
+
+    if (P.color_source == SS_COLOR_IBL) {
+        ShadeIn in;
+        ss_shade_inputs(cl, i, P.cam_pos, in);
+        ShadeState st;
+        double col[3];
+        ss_shade_forward(in, P.env, st, col);
+        ShadeGrads sg;
+        ss_shade_backward(in, st, P.env, gcol, sg);
+        for (int c = 0; c < 3; ++c) { gcent[c] += sg.center[c]; gN[c] = sg.normal[c]; galb[c] = sg.albedo_raw[c]; }
+        gmet = sg.metallic_raw;
+        grough = sg.roughness_raw;
+        // derived-map scatter (bilinear_scatter, shading.py:248-260, 583-597)
+        const int we = P.env.we;
+        const size_t lstride = (size_t)P.env.he * we * 3;
+        const double wts[2] = {1.0 - st.frac, st.frac};
+        const int lvs[2] = {st.lvl0, st.lvl1};
+        const SsBil &bs = st.bs;
+        const int sidx[4] = {bs.j0 * we + bs.i0, bs.j0 * we + bs.i1, bs.j1 * we + bs.i0, bs.j1 * we + bs.i1};
+        const double scw[4] = {(1 - bs.tu) * (1 - bs.tv), bs.tu * (1 - bs.tv), (1 - bs.tu) * bs.tv, bs.tu * bs.tv};
+        for (int h = 0; h < 2; ++h) {
+            if (wts[h] == 0.0) continue;
+            float *dst = P.g.d_specular + lstride * lvs[h];
+            for (int k = 0; k < 4; ++k)
+                for (int c = 0; c < 3; ++c) {
+                    const float val = (float)(sg.g_ls[c] * wts[h] * scw[k]);
+                    if (val != 0.f) atomicAdd(dst + 3 * sidx[k] + c, val);
+                }
+        }
+        const SsBil &bd = st.bd;
+        const int didx[4] = {bd.j0 * we + bd.i0, bd.j0 * we + bd.i1, bd.j1 * we + bd.i0, bd.j1 * we + bd.i1};
+        const double dcw[4] = {(1 - bd.tu) * (1 - bd.tv), bd.tu * (1 - bd.tv), (1 - bd.tu) * bd.tv, bd.tu * bd.tv};
+        for (int k = 0; k < 4; ++k)
+            for (int c = 0; c < 3; ++c) {
+                const float val = (float)(sg.g_ld[c] * dcw[k]);
+                if (val != 0.f) atomicAdd(P.g.d_diffuse + 3 * didx[k] + c, val);
+            }
+    } else if (P.color_source == SS_COLOR_ALBEDO) {
+        for (int c = 0; c < 3; ++c) {
+            const double al = (double)ss_sigmoid_f32(cl.albedo_raw[3 * i + c]);
+            galb[c] = gcol[c] * al * (1.0 - al);
+        }
+    }
+    // quat_frame_backward (surfels.py:54-77)
+#define D3(g, a0, a1, a2) ((g)[0] * (a0) + (g)[1] * (a1) + (g)[2] * (a2))
+    const double gqw = D3(gU, 0.0, 2 * z, -2 * y) + D3(gV, -2 * z, 0.0, 2 * x) + D3(gN, 2 * y, -2 * x, 0.0);
+    const double gqx = D3(gU, 0.0, 2 * y, 2 * z) + D3(gV, 2 * y, -4 * x, 2 * w) + D3(gN, 2 * z, -2 * w, -4 * x);
+    const double gqy = D3(gU, -4 * y, 2 * x, -2 * w) + D3(gV, 2 * x, 0.0, 2 * z) + D3(gN, 2 * w, 2 * z, -4 * y);
+    const double gqz = D3(gU, -4 * z, 2 * w, 2 * x) + D3(gV, -2 * w, -4 * z, 2 * y) + D3(gN, 2 * x, 2 * y, 0.0);
+#undef D3
+    const double radial = ((gqw * w + gqx * x) + gqy * y) + gqz * z;
+
+    SsGrads &g = P.g;
+    for (int c = 0; c < 3; ++c) {
+        g.centers[3 * i + c] += (float)gcent[c];
+        g.albedo_raw[3 * i + c] += (float)galb[c];
+    }
+    float4 gq = reinterpret_cast<float4 *>(g.quats)[i];
+    gq.x += (float)((gqw - radial * w) / qn);
+    gq.y += (float)((gqx - radial * x) / qn);
+    gq.z += (float)((gqy - radial * y) / qn);
+    gq.w += (float)((gqz - radial * z) / qn);
+    reinterpret_cast<float4 *>(g.quats)[i] = gq;
+    float2 gl = reinterpret_cast<float2 *>(g.log_scales)[i];
+    gl.x += (float)(gsu * su);
+    gl.y += (float)(gsv * sv);
+    reinterpret_cast<float2 *>(g.log_scales)[i] = gl;
+    g.metallic_raw[i] += (float)gmet;
+    g.roughness_raw[i] += (float)grough;
+    if (g.colors)
+        for (int c = 0; c < 3; ++c) g.colors[3 * i + c] += (float)gcol[c];
+    g.ss_grad[i] += ss;
+    g.touched[i] += touch;
+}
+
+}  // namespace
+
+extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                                 int color_source, const SsEnv *env, const int8_t *cull,
+                                 const float *rec_acc, const SsGrads *grads, void *stream)
+{
+    if (!cloud || !cam || !opt || !grads) return SS_ERR_INVALID;
+    if (cloud->n == 0) return SS_OK;
+    if (!cull || !rec_acc) return SS_ERR_INVALID;
+    if (color_source == SS_COLOR_IBL && (!env || !grads->d_diffuse || !grads->d_specular)) return SS_ERR_INVALID;
+    if (cloud->n == 0) return SS_OK;
+    ChainParams P;
+    P.cloud = *cloud;
+    for (int k = 0; k < 16; ++k) {
+        P.view[k] = cam->view[k]; P.proj[k] = cam->proj[k];
+        P.viewf[k] = (float)cam->view[k]; P.projf[k] = (float)cam->proj[k];
+    }
+    for (int k = 0; k < 3; ++k)
+        P.cam_pos[k] = -(cam->view[k] * cam->view[3] + cam->view[4 + k] * cam->view[7] + cam->view[8 + k] * cam->view[11]);
+    P.W = cam->width; P.H = cam->height; P.mip = opt->mip_enabled; P.color_source = color_source;
+    P.sigma = (double)opt->mip_sigma;
+    P.r_cut = opt->r_cut; P.sigma_f = opt->mip_sigma;
+    P.env = env ? *env : SsEnv{};
+    P.cull = cull; P.acc = rec_acc; P.g = *grads;
+    chain_kernel<<<(cloud->n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}

@@ -1,0 +1,295 @@
+// env.cu -- environment prefilter operators applied on the fly, their
+// adjoint, and the preintegrated BRDF LUT.
+//
+// Reference: EnvironmentLight.refresh / env_gradient (shading.py:369-394),
+// build_diffuse_operator (:275-282, a DENSE T x T float64 matrix),
+// build_specular_operator (:285-331), brdf_lut (:118-156).  The reference
+// materialises T x T operators (51.5 GB at 128x256, 825 GB at 256x512); here
+// the diffuse operator is regenerated per (row, column) tile from separable
+// sin/cos tables in shared memory (an O(T^2) FP32 N-body pass, gather form in
+// both directions so no atomics), and the specular operator is regenerated
+// per output texel from the same Hammersley/GGX samples.
+#include "ss_common.cuh"
+#include "shading.cuh"
+
+namespace {
+
+__device__ __forceinline__ double radical_inverse(uint32_t i) {
+    return (double)__brev(i) * 2.3283064365386963e-10;
+}
+
+__device__ __forceinline__ void ggx_h(double xi0, double xi1, double alpha, double h[3]) {
+    const double phi = 2.0 * SS_PI * xi0;
+    const double cos_t = sqrt((1.0 - xi1) / (1.0 + (alpha * alpha - 1.0) * xi1));
+    const double sin_t = sqrt(ss_npmax(1.0 - cos_t * cos_t, 0.0));
+    h[0] = sin_t * cos(phi); h[1] = sin_t * sin(phi); h[2] = cos_t;
+}
+
+__device__ __forceinline__ double smith_g1(double c, double k) { return c / (c * (1.0 - k) + k); }
+
+__global__ void lut_kernel(int res, int samples, float *lut) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= res * res) return;
+    const int j = id / res, i = id % res;
+    const double r = ((double)j + 0.5) / res, alpha = r * r, k = alpha / 2.0;
+    const double cv = ((double)i + 0.5) / res;
+    const double vx = sqrt(1.0 - cv * cv), vz = cv;
+    double s1 = 0.0, s2 = 0.0;
+    for (int s = 0; s < samples; ++s) {
+        double h[3];
+        ggx_h(((double)s + 0.5) / samples, radical_inverse((uint32_t)s), alpha, h);
+        const double vh = vx * h[0] + vz * h[2];
+        const double l2 = 2.0 * vh * h[2] - vz;
+        const bool good = l2 > 0.0 && vh > 0.0;
+        const double g = smith_g1(cv, k) * smith_g1(ss_npmax(l2, 1e-8), k);
+        const double gv = good ? g * vh / ss_npmax(h[2] * cv, 1e-8) : 0.0;
+        const double fc = pow(1.0 - ss_clip(vh, 0.0, 1.0), 5.0);
+        s1 += gv * (1.0 - fc);
+        s2 += gv * fc;
+    }
+    lut[2 * id] = (float)(s1 / samples);
+    lut[2 * id + 1] = (float)(s2 / samples);
+}
+
+// Texel direction tables (latlong_texel_dirs, shading.py:162-169).
+struct DirTab {
+    float *st, *ct, *cp, *sp, *om;  // sin/cos theta per row, cos/sin phi per column, solid angle per row
+};
+
+__device__ __forceinline__ void load_tables(int he, int we, DirTab t) {
+    for (int r = threadIdx.x; r < he; r += blockDim.x) {
+        const double th = ((double)r + 0.5) * (SS_PI / he);
+        t.st[r] = (float)sin(th);
+        t.ct[r] = (float)cos(th);
+        t.om[r] = (float)(sin(th) * (SS_PI / he) * (2.0 * SS_PI / we));
+    }
+    for (int c = threadIdx.x; c < we; c += blockDim.x) {
+        const double ph = ((double)c + 0.5) * (2.0 * SS_PI / we) - SS_PI;
+        t.cp[c] = (float)cos(ph);
+        t.sp[c] = (float)sin(ph);
+    }
+}
+
+// mode 0: rowsum_i = sum_j max(d_i.d_j,0) om_j
+// mode 1: out_i   = sum_j max(d_i.d_j,0) om_j x_j / rowsum_i        (refresh)
+// mode 2: out_j   = om_j sum_i max(d_i.d_j,0) x_i / rowsum_i        (adjoint)
+template <int MODE>
+__global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const float *__restrict__ x,
+                                                      const float *__restrict__ rowsum, float *__restrict__ out) {
+    extern __shared__ float sm[];
+    DirTab tab{sm, sm + he, sm + 2 * he, sm + 2 * he + we, sm + 2 * he + 2 * we};
+    load_tables(he, we, tab);
+    __syncthreads();
+    const int T = he * we;
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= T) return;
+    const int ar = a / we, ac = a % we;
+    const float sta = tab.st[ar], cta = tab.ct[ar], cpa = tab.cp[ac], spa = tab.sp[ac];
+    double tot0 = 0.0, tot1 = 0.0, tot2 = 0.0;
+    for (int r = 0; r < he; ++r) {
+        const float sr = tab.st[r] * sta, cr = tab.ct[r] * cta;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        for (int c = 0; c < we; ++c) {
+            const float dot = sr * (cpa * tab.cp[c] + spa * tab.sp[c]) + cr;
+            if (dot <= 0.f) continue;
+            const int b = r * we + c;
+            if (MODE == 0) {
+                s0 += dot;
+            } else if (MODE == 1) {
+                s0 += dot * x[3 * b]; s1 += dot * x[3 * b + 1]; s2 += dot * x[3 * b + 2];
+            } else {
+                const float inv = 1.f / rowsum[b];
+                s0 += dot * x[3 * b] * inv; s1 += dot * x[3 * b + 1] * inv; s2 += dot * x[3 * b + 2] * inv;
+            }
+        }
+        const double om = MODE == 2 ? 1.0 : (double)tab.om[r];
+        tot0 += om * s0; tot1 += om * s1; tot2 += om * s2;
+    }
+    if (MODE == 0) {
+        out[a] = (float)tot0;
+    } else if (MODE == 1) {
+        const double inv = 1.0 / (double)rowsum[a];
+        out[3 * a] = (float)(tot0 * inv); out[3 * a + 1] = (float)(tot1 * inv); out[3 * a + 2] = (float)(tot2 * inv);
+    } else {
+        const double om = tab.om[ar];
+        out[3 * a] += (float)(tot0 * om); out[3 * a + 1] += (float)(tot1 * om); out[3 * a + 2] += (float)(tot2 * om);
+    }
+}
+
+struct SpecSample {
+    int idx[4];
+    double w[4];
+};
+
+// One GGX sample of a specular operator row (shading.py:306-323).
+__device__ __forceinline__ bool spec_sample(const double d[3], const double tx[3], const double ty[3], int s,
+                                            int samples, double alpha, int he, int we, SpecSample &o, double &wgt) {
+    double h[3];
+    ggx_h(((double)s + 0.5) / samples, radical_inverse((uint32_t)s), alpha, h);
+    double hv[3];
+    for (int c = 0; c < 3; ++c) hv[c] = h[0] * tx[c] + h[1] * ty[c] + h[2] * d[c];
+    const double vh = (d[0] * hv[0] + d[1] * hv[1]) + d[2] * hv[2];
+    double l[3];
+    for (int c = 0; c < 3; ++c) l[c] = 2.0 * vh * hv[c] - d[c];
+    const double nl = (d[0] * l[0] + d[1] * l[1]) + d[2] * l[2];
+    wgt = ss_npmax(nl, 0.0);
+    if (!(wgt > 0.0)) return false;
+    double fu, fv;
+    ss_dir_coords(l, he, we, fu, fv);
+    const SsBil b = ss_bil_prepare(he, we, fu, fv, true);
+    o.idx[0] = b.j0 * we + b.i0; o.idx[1] = b.j0 * we + b.i1; o.idx[2] = b.j1 * we + b.i0; o.idx[3] = b.j1 * we + b.i1;
+    o.w[0] = wgt * (1 - b.tu) * (1 - b.tv); o.w[1] = wgt * b.tu * (1 - b.tv);
+    o.w[2] = wgt * (1 - b.tu) * b.tv; o.w[3] = wgt * b.tu * b.tv;
+    return true;
+}
+
+__device__ __forceinline__ void texel_frame(int a, int he, int we, double d[3], double tx[3], double ty[3]) {
+    const int r = a / we, c = a % we;
+    const double th = ((double)r + 0.5) * (SS_PI / he);
+    const double ph = ((double)c + 0.5) * (2.0 * SS_PI / we) - SS_PI;
+    d[0] = sin(th) * cos(ph); d[1] = sin(th) * sin(ph); d[2] = cos(th);
+    double up[3] = {0.0, 0.0, 1.0};
+    if (!(fabs(d[2]) < 0.999)) { up[0] = 1.0; up[2] = 0.0; }
+    tx[0] = up[1] * d[2] - up[2] * d[1]; tx[1] = up[2] * d[0] - up[0] * d[2]; tx[2] = up[0] * d[1] - up[1] * d[0];
+    const double tn = sqrt((tx[0] * tx[0] + tx[1] * tx[1]) + tx[2] * tx[2]);
+    for (int k = 0; k < 3; ++k) tx[k] /= tn;
+    ty[0] = d[1] * tx[2] - d[2] * tx[1]; ty[1] = d[2] * tx[0] - d[0] * tx[2]; ty[2] = d[0] * tx[1] - d[1] * tx[0];
+}
+
+// specular[l] = S_l base (l >= 1); level 0 is the identity (shading.py:287-289)
+__global__ void __launch_bounds__(128) spec_refresh_kernel(int he, int we, int levels, int samples,
+                                                           const float *__restrict__ base, float *__restrict__ spec) {
+    const int T = he * we;
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lv = blockIdx.y + 1;
+    if (a >= T) return;
+    const double rough = lv / (levels - 1.0), alpha = rough * rough;
+    double d[3], tx[3], ty[3];
+    texel_frame(a, he, we, d, tx, ty);
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, ws = 0.0;
+    for (int s = 0; s < samples; ++s) {
+        SpecSample o;
+        double wgt;
+        if (!spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt)) continue;
+        ws += wgt;
+        for (int k = 0; k < 4; ++k) {
+            acc0 += o.w[k] * base[3 * o.idx[k]];
+            acc1 += o.w[k] * base[3 * o.idx[k] + 1];
+            acc2 += o.w[k] * base[3 * o.idx[k] + 2];
+        }
+    }
+    float *out = spec + (size_t)lv * T * 3 + 3 * a;
+    if (ws <= 0.0) {
+        out[0] = base[3 * a]; out[1] = base[3 * a + 1]; out[2] = base[3 * a + 2];
+    } else {
+        out[0] = (float)(acc0 / ws); out[1] = (float)(acc1 / ws); out[2] = (float)(acc2 / ws);
+    }
+}
+
+// d_base += S_l^T g_l (scatter form; atomics), l >= 1
+__global__ void __launch_bounds__(128) spec_adjoint_kernel(int he, int we, int levels, int samples,
+                                                           const float *__restrict__ g, float *__restrict__ d_base) {
+    const int T = he * we;
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lv = blockIdx.y + 1;
+    if (a >= T) return;
+    const float *gl = g + (size_t)lv * T * 3;
+    const double g0 = gl[3 * a], g1 = gl[3 * a + 1], g2 = gl[3 * a + 2];
+    if (g0 == 0.0 && g1 == 0.0 && g2 == 0.0) return;
+    const double rough = lv / (levels - 1.0), alpha = rough * rough;
+    double d[3], tx[3], ty[3];
+    texel_frame(a, he, we, d, tx, ty);
+    double ws = 0.0;
+    for (int s = 0; s < samples; ++s) {
+        SpecSample o;
+        double wgt;
+        if (spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt)) ws += wgt;
+    }
+    if (ws <= 0.0) {
+        atomicAdd(d_base + 3 * a, (float)g0); atomicAdd(d_base + 3 * a + 1, (float)g1); atomicAdd(d_base + 3 * a + 2, (float)g2);
+        return;
+    }
+    const double inv = 1.0 / ws;
+    for (int s = 0; s < samples; ++s) {
+        SpecSample o;
+        double wgt;
+        if (!spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt)) continue;
+        for (int k = 0; k < 4; ++k) {
+            const double f = o.w[k] * inv;
+            atomicAdd(d_base + 3 * o.idx[k], (float)(f * g0));
+            atomicAdd(d_base + 3 * o.idx[k] + 1, (float)(f * g1));
+            atomicAdd(d_base + 3 * o.idx[k] + 2, (float)(f * g2));
+        }
+    }
+}
+
+__global__ void exp_kernel(int n, const float *__restrict__ lg, float *__restrict__ base, float *__restrict__ spec0) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const float b = (float)exp((double)lg[k]);
+    base[k] = b;
+    spec0[k] = b;
+}
+
+__global__ void adjoint_finish_kernel(int n, const float *__restrict__ g0, const float *__restrict__ base,
+                                      float *__restrict__ d_base, float *__restrict__ d_log) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const float db = d_base[k] + g0[k];
+    d_base[k] = db;
+    d_log[k] = db * base[k];
+}
+
+size_t tab_bytes(int he, int we) { return (size_t)(3 * he + 2 * we) * sizeof(float); }
+
+}  // namespace
+
+extern "C" int ss_brdf_lut(int res, int samples, float *lut, void *stream) {
+    if (res < 2 || samples < 1 || !lut) return SS_ERR_INVALID;
+    lut_kernel<<<(res * res + 127) / 128, 128, 0, (cudaStream_t)stream>>>(res, samples, lut);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_env_rowsums(int he, int we, float *rowsum, void *stream) {
+    if (he < 2 || we < 2 || !rowsum) return SS_ERR_INVALID;
+    const int T = he * we;
+    diffuse_kernel<0><<<(T + 255) / 256, 256, tab_bytes(he, we), (cudaStream_t)stream>>>(he, we, nullptr, nullptr, rowsum);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log,
+                              const float *rowsum, float *base, float *diffuse, float *specular, void *stream) {
+    if (he < 2 || we < 2 || levels < 1 || !base_log || !rowsum || !base || !diffuse || !specular) return SS_ERR_INVALID;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int T = he * we;
+    exp_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular);
+    SS_CUDA_CHECK_LAUNCH();
+    diffuse_kernel<1><<<(T + 255) / 256, 256, tab_bytes(he, we), st>>>(he, we, base, rowsum, diffuse);
+    SS_CUDA_CHECK_LAUNCH();
+    if (levels > 1) {
+        spec_refresh_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, base, specular);
+        SS_CUDA_CHECK_LAUNCH();
+    }
+    return SS_OK;
+}
+
+extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, const float *rowsum,
+                              const float *d_diffuse, const float *d_specular, float *d_base, float *d_base_log,
+                              void *stream) {
+    if (he < 2 || we < 2 || levels < 1 || !base || !rowsum || !d_diffuse || !d_specular || !d_base || !d_base_log)
+        return SS_ERR_INVALID;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int T = he * we;
+    cudaMemsetAsync(d_base, 0, sizeof(float) * 3 * T, st);
+    diffuse_kernel<2><<<(T + 255) / 256, 256, tab_bytes(he, we), st>>>(he, we, d_diffuse, rowsum, d_base);
+    SS_CUDA_CHECK_LAUNCH();
+    if (levels > 1) {
+        spec_adjoint_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, d_specular, d_base);
+        SS_CUDA_CHECK_LAUNCH();
+    }
+    adjoint_finish_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, d_specular, base, d_base, d_base_log);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}

@@ -1,0 +1,163 @@
+// optim.cu -- fused Adam step, quaternion renormalisation and the refinement
+// scan helpers (isolation query on a uniform grid, split children).
+//
+// Reference: Adam.step (adam.py:21-41), normalize_quats after the step
+// (train.py:246), prune_keep_mask isolation test (densify.py:118-123, scipy
+// cKDTree k=2), split_cloud (densify.py:60-98).  All HBM-streaming kernels.
+#include "ss_common.cuh"
+
+namespace {
+
+__global__ void adam_kernel(int64_t count, float *__restrict__ p, const float *__restrict__ g,
+                            float *__restrict__ m, float *__restrict__ v, double lr, double b1, double b2,
+                            double eps, double c1, double c2) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < count; k += (int64_t)gridDim.x * blockDim.x) {
+        const double gg = g[k];
+        const double mm = b1 * (double)m[k] + (1.0 - b1) * gg;
+        const double vv = b2 * (double)v[k] + (1.0 - b2) * gg * gg;
+        m[k] = (float)mm;
+        v[k] = (float)vv;
+        const double mh = mm / c1, vh = vv / c2;
+        p[k] = p[k] - (float)(lr * mh / (sqrt(vh) + eps));
+    }
+}
+
+__global__ void normalize_quats_kernel(int n, float4 *__restrict__ q) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 a = q[i];
+    const float nrm = sqrtf(((a.x * a.x + a.y * a.y) + a.z * a.z) + a.w * a.w);
+    if (nrm > 0.f) { a.x /= nrm; a.y /= nrm; a.z /= nrm; a.w /= nrm; }
+    q[i] = a;
+}
+
+struct Grid { float ox, oy, oz, cell; int dim; };
+
+__device__ __forceinline__ int axis_cell(float c, float o, float cell, int dim) {
+    int k = (int)floorf((c - o) / cell);
+    return k < 0 ? 0 : (k >= dim ? dim - 1 : k);
+}
+
+__global__ void grid_cells_kernel(int n, const float *__restrict__ c, Grid g, int32_t *__restrict__ cell_of) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = axis_cell(c[3 * i], g.ox, g.cell, g.dim), y = axis_cell(c[3 * i + 1], g.oy, g.cell, g.dim),
+              z = axis_cell(c[3 * i + 2], g.oz, g.cell, g.dim);
+    cell_of[i] = (x * g.dim + y) * g.dim + z;
+}
+
+__device__ __forceinline__ int lower_bound(const int32_t *a, int n, int key) {
+    int lo = 0, hi = n;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if (a[mid] < key) lo = mid + 1; else hi = mid; }
+    return lo;
+}
+
+__global__ void isolation_kernel(int n, const float *__restrict__ c, const float *__restrict__ ls,
+                                 const int32_t *__restrict__ order, const int32_t *__restrict__ sorted_cells, Grid g,
+                                 uint8_t *__restrict__ isolated) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (n <= 1) { isolated[i] = 0; return; }
+    // support = R_CUT * max(scales) with numpy's float32 scales (densify.py:122)
+    const float s0 = (float)exp((double)ls[2 * i]), s1 = (float)exp((double)ls[2 * i + 1]);
+    const double sup = (double)(3.0f * (s0 > s1 ? s0 : s1));  // float32 like the reference
+    const double sup2 = sup * sup;
+    const double px = c[3 * i], py = c[3 * i + 1], pz = c[3 * i + 2];
+    const int x0 = axis_cell((float)(px - sup), g.ox, g.cell, g.dim), x1 = axis_cell((float)(px + sup), g.ox, g.cell, g.dim);
+    const int y0 = axis_cell((float)(py - sup), g.oy, g.cell, g.dim), y1 = axis_cell((float)(py + sup), g.oy, g.cell, g.dim);
+    const int z0 = axis_cell((float)(pz - sup), g.oz, g.cell, g.dim), z1 = axis_cell((float)(pz + sup), g.oz, g.cell, g.dim);
+    for (int x = x0; x <= x1; ++x)
+        for (int y = y0; y <= y1; ++y) {
+            const int key0 = (x * g.dim + y) * g.dim + z0, key1 = (x * g.dim + y) * g.dim + z1;
+            int k = lower_bound(sorted_cells, n, key0);
+            for (; k < n && sorted_cells[k] <= key1; ++k) {
+                const int j = order[k];
+                if (j == i) continue;
+                const double dx = px - c[3 * j], dy = py - c[3 * j + 1], dz = pz - c[3 * j + 2];
+                if (sqrt(dx * dx + dy * dy + dz * dz) <= sup) { isolated[i] = 0; return; }
+            }
+        }
+    (void)sup2;
+    isolated[i] = 1;
+}
+
+__global__ void split_kernel(int ns, const int32_t *__restrict__ parents, const float *__restrict__ centers,
+                             const float *__restrict__ quats, const float *__restrict__ ls, float *__restrict__ oc,
+                             float *__restrict__ ols, int64_t plus0, int64_t minus0) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ns) return;
+    const int p = parents[k];
+    const double q0 = quats[4 * p], q1 = quats[4 * p + 1], q2 = quats[4 * p + 2], q3 = quats[4 * p + 3];
+    const double qn = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
+    const double w = q0 / qn, x = q1 / qn, y = q2 / qn, z = q3 / qn;
+    const double u[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
+    const double v[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
+    double s0 = (double)(float)exp((double)ls[2 * p]), s1 = (double)(float)exp((double)ls[2 * p + 1]);
+    const bool axis_u = s0 >= s1;
+    const double smax = axis_u ? s0 : s1;
+    if (axis_u) s0 *= 0.7; else s1 *= 0.7;
+    const float l0 = (float)log(s0), l1 = (float)log(s1);
+    for (int c = 0; c < 3; ++c) {
+        const double off = (smax / 2.0) * (axis_u ? u[c] : v[c]);
+        const double cc = centers[3 * p + c];
+        oc[3 * (plus0 + k) + c] = (float)(cc + off);
+        oc[3 * (minus0 + k) + c] = (float)(cc - off);
+    }
+    ols[2 * (plus0 + k)] = l0; ols[2 * (plus0 + k) + 1] = l1;
+    ols[2 * (minus0 + k)] = l0; ols[2 * (minus0 + k) + 1] = l1;
+}
+
+}  // namespace
+
+extern "C" int ss_adam_step(int64_t count, float *param, const float *grad, float *m, float *v, int t, float lr,
+                            float beta1, float beta2, float eps, void *stream) {
+    if (count < 0 || t < 1 || (count > 0 && (!param || !grad || !m || !v))) return SS_ERR_INVALID;
+    if (count == 0) return SS_OK;
+    const double c1 = 1.0 - pow((double)beta1, t), c2 = 1.0 - pow((double)beta2, t);
+    const int blocks = (int)((count + 255) / 256 < 148 * 16 ? (count + 255) / 256 : 148 * 16);
+    adam_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(count, param, grad, m, v, lr, beta1, beta2, eps, c1, c2);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_normalize_quats(int n, float *quats, void *stream) {
+    if (n < 0 || (n > 0 && !quats)) return SS_ERR_INVALID;
+    if (n == 0) return SS_OK;
+    normalize_quats_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, reinterpret_cast<float4 *>(quats));
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_grid_cells(int n, const float *centers, const float *origin3, float cell, int dim,
+                             int32_t *cell_of, void *stream) {
+    if (n < 0 || !origin3 || cell <= 0.f || dim < 1 || dim > 1024) return SS_ERR_INVALID;
+    if (n == 0) return SS_OK;
+    Grid g{origin3[0], origin3[1], origin3[2], cell, dim};
+    grid_cells_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n, centers, g, cell_of);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_isolation(int n, const float *centers, const float *log_scales, const int32_t *order,
+                            const int32_t *sorted_cells, const float *origin3, float cell, int dim,
+                            uint8_t *isolated, void *stream) {
+    if (n < 0 || !origin3 || cell <= 0.f || dim < 1 || dim > 1024) return SS_ERR_INVALID;
+    if (n == 0) return SS_OK;
+    Grid g{origin3[0], origin3[1], origin3[2], cell, dim};
+    isolation_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(n, centers, log_scales, order, sorted_cells, g,
+                                                                         isolated);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_split_children(int nsplit, const int32_t *parents, const float *centers, const float *quats,
+                                 const float *log_scales, float *out_centers, float *out_log_scales,
+                                 int64_t plus_row0, int64_t minus_row0, void *stream) {
+    if (nsplit < 0) return SS_ERR_INVALID;
+    if (nsplit == 0) return SS_OK;
+    split_kernel<<<(nsplit + 127) / 128, 128, 0, (cudaStream_t)stream>>>(nsplit, parents, centers, quats, log_scales,
+                                                                         out_centers, out_log_scales, plus_row0,
+                                                                         minus_row0);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}

@@ -1,0 +1,230 @@
+// preprocess.cu -- per-surfel projection, filter setup, bounding, shading and
+// tile counting in ONE pass over the surfel parameters.
+//
+// Reference: preprocess.py:38-309 (float32 throughout), shading.py:447-503
+// (float64), rasterizer.py:92-106 (tile spans).  Compiled with -fmad=false:
+// every float32 expression below rounds each operation like numpy does; the
+// two BLAS inner products are written as the explicit fmaf chains numpy's
+// OpenBLAS kernels evaluate (hard part 1).
+//
+// HBM: reads 56 B of parameters per surfel (plus a few KB of env/LUT texels
+// that stay in L1/L2), writes one 96 B record + 1 B cull + 4 B pair count.
+#include "ss_common.cuh"
+#include "shading.cuh"
+
+namespace {
+
+__device__ __forceinline__ float dot_gemm(float a0, float a1, float a2, float b0, float b1, float b2) {
+    return __fmaf_rn(a2, b2, __fmaf_rn(a1, b1, a0 * b0));
+}
+__device__ __forceinline__ float dot_gemv(float a0, float a1, float a2, float v0, float v1, float v2) {
+    return __fmaf_rn(a2, v2, __fmaf_rn(a0, v0, a1 * v1));
+}
+__device__ __forceinline__ float npmaxf(float a, float b) { return (a != a) ? a : (a > b ? a : b); }
+__device__ __forceinline__ float npclipf(float a, float lo, float hi) {
+    if (a != a) return a;
+    return a < lo ? lo : (a > hi ? hi : a);
+}
+
+struct CamF {
+    float view[16], proj[16];
+    double cam_pos[3];
+    int W, H;
+};
+
+__global__ void __launch_bounds__(256) preprocess_kernel(
+    SsCloud cloud, CamF cam, SsPreprocessOpts opt, int color_source, const float *__restrict__ colors_in,
+    SsEnv env, SsRecord *__restrict__ records, int8_t *__restrict__ cull_out,
+    int32_t *__restrict__ pair_count, int32_t *__restrict__ tile_counts, SsProjAux aux,
+    int32_t *__restrict__ flags)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cloud.n) return;
+    const float c0 = cloud.centers[3 * i], c1 = cloud.centers[3 * i + 1], c2 = cloud.centers[3 * i + 2];
+    const float4 q = reinterpret_cast<const float4 *>(cloud.quats)[i];
+    const float2 ls = reinterpret_cast<const float2 *>(cloud.log_scales)[i];
+    const float ar0 = cloud.albedo_raw[3 * i], ar1 = cloud.albedo_raw[3 * i + 1], ar2 = cloud.albedo_raw[3 * i + 2];
+    const float mr = cloud.metallic_raw[i], rr = cloud.roughness_raw[i];
+
+    bool finite = isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(q.x) && isfinite(q.y) &&
+                  isfinite(q.z) && isfinite(q.w) && isfinite(ls.x) && isfinite(ls.y) && isfinite(ar0) &&
+                  isfinite(ar1) && isfinite(ar2) && isfinite(mr) && isfinite(rr);
+    int code = finite ? 0 : 1;
+
+    // quat_to_frame in float32 (surfels.py:40-51)
+    float nrm = sqrtf(((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w);
+    if (nrm == 0.0f) atomicOr(&flags[0], 1);
+    float w = q.x / nrm, x = q.y / nrm, y = q.z / nrm, z = q.w / nrm;
+    float uh0 = 1.0f - 2.0f * (y * y + z * z), uh1 = 2.0f * (x * y + w * z), uh2 = 2.0f * (x * z - w * y);
+    float vh0 = 2.0f * (x * y - w * z), vh1 = 1.0f - 2.0f * (x * x + z * z), vh2 = 2.0f * (y * z + w * x);
+    // numpy's float32 exp is a SIMD kernel; the correctly rounded value is the
+    // documented stand-in (oracle/ss_oracle.c does the same).
+    float su = (float)exp((double)ls.x), sv = (float)exp((double)ls.y);
+    float su0 = su * uh0, su1 = su * uh1, su2 = su * uh2;
+    float sv0 = sv * vh0, sv1 = sv * vh1, sv2 = sv * vh2;
+    float cc[3], tu[3], tv[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const float R0 = cam.view[4 * r], R1 = cam.view[4 * r + 1], R2 = cam.view[4 * r + 2];
+        cc[r] = dot_gemm(c0, c1, c2, R0, R1, R2) + cam.view[4 * r + 3];
+        tu[r] = dot_gemm(su0, su1, su2, R0, R1, R2);
+        tv[r] = dot_gemm(sv0, sv1, sv2, R0, R1, R2);
+    }
+    const float vz = -cc[2];
+    float t[3][3];
+    const int irs[3] = {0, 1, 3};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float *P = cam.proj + 4 * irs[k];
+        t[k][0] = dot_gemv(tu[0], tu[1], tu[2], P[0], P[1], P[2]);
+        t[k][1] = dot_gemv(tv[0], tv[1], tv[2], P[0], P[1], P[2]);
+        t[k][2] = dot_gemv(cc[0], cc[1], cc[2], P[0], P[1], P[2]) + P[3];
+    }
+    const float *t1 = t[0], *t2 = t[1], *t4 = t[2];
+    if (code == 0 && !(vz >= SS_VIEW_Z_EPS)) code = 2;
+    bool alive = code == 0;
+    const float ez = opt.r_cut * sqrtf(tu[2] * tu[2] + tv[2] * tv[2]);
+    const float sd4 = alive ? t4[2] : 1.0f;
+    const float cnx = t1[2] / sd4, cny = t2[2] / sd4;
+
+    float j00 = 0.f, j01 = 0.f, j10 = 0.f, j11 = 0.f;
+    bool ok = false;
+    float m00 = 1.f, m01 = 0.f, m11 = 1.f, nf = 1.f;
+    float tb[3][3];
+    if (opt.mip_enabled) {
+        float jj[4];
+        ok = ss_center_jacobian(t1, t2, t4, cam.W, cam.H, jj);
+        if (ok && alive) { j00 = jj[0]; j01 = jj[1]; j10 = jj[2]; j11 = jj[3]; }
+        const float s = opt.mip_sigma;
+        float jjt00 = j00 * j00 + j01 * j01;
+        float jjt01 = j00 * j10 + j01 * j11;
+        float jjt11 = j10 * j10 + j11 * j11;
+        float s00 = 1.0f + s * jjt00, s01 = s * jjt01, s11 = 1.0f + s * jjt11;
+        float det = s00 * s11 - s01 * s01;
+        float inv_det = 1.0f / det;
+        m00 = s11 * inv_det; m01 = -s01 * inv_det; m11 = s00 * inv_det;
+        nf = sqrtf(inv_det);
+        float la = sqrtf(1.0f + s * jjt00);
+        float lb = s * jjt01 / la;
+        float lc = sqrtf(npmaxf(1.0f + s * jjt11 - lb * lb, 1.17549435e-38f));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            tb[k][0] = la * t[k][0] + lb * t[k][1];
+            tb[k][1] = lc * t[k][1];
+            tb[k][2] = t[k][2];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) { tb[k][0] = t[k][0]; tb[k][1] = t[k][1]; tb[k][2] = t[k][2]; }
+    }
+    // bounding_rect (preprocess.py:77-105)
+    const float rr2 = opt.r_cut * opt.r_cut;
+    const float *b4 = tb[2];
+    float f44 = b4[2] * b4[2] - rr2 * (b4[0] * b4[0] + b4[1] * b4[1]);
+    bool valid = f44 > 0.0f;
+    float f44s = valid ? f44 : 1.0f;
+    float ctr[2], half[2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        const float *tr = tb[a];
+        float fi4 = tr[2] * b4[2] - rr2 * (tr[0] * b4[0] + tr[1] * b4[1]);
+        float fii = tr[2] * tr[2] - rr2 * (tr[0] * tr[0] + tr[1] * tr[1]);
+        float disc = npmaxf(fi4 * fi4 - f44 * fii, 0.0f);
+        ctr[a] = fi4 / f44s;
+        half[a] = sqrtf(disc) / f44s;
+    }
+    if (alive && !valid) code = 3;
+    alive = code == 0;
+    const float fw = (float)cam.W, fh = (float)cam.H;
+    float lo_x = ctr[0] - half[0], hi_x = ctr[0] + half[0];
+    float lo_y = ctr[1] - half[1], hi_y = ctr[1] + half[1];
+    float x0 = ceilf((lo_x + 1.0f) * 0.5f * fw - 0.5f - 9.99999975e-05f);
+    float x1 = floorf((hi_x + 1.0f) * 0.5f * fw - 0.5f + 9.99999975e-05f) + 1.0f;
+    float y0 = ceilf((1.0f - hi_y) * 0.5f * fh - 0.5f - 9.99999975e-05f);
+    float y1 = floorf((1.0f - lo_y) * 0.5f * fh - 0.5f + 9.99999975e-05f) + 1.0f;
+    x0 = npclipf(x0, 0.f, fw); x1 = npclipf(x1, 0.f, fw);
+    y0 = npclipf(y0, 0.f, fh); y1 = npclipf(y1, 0.f, fh);
+    if (alive && (x0 >= x1 || y0 >= y1)) code = 4;
+    alive = code == 0;
+
+    // colour (rasterizer.py:341-353)
+    float col[3] = {0.f, 0.f, 0.f};
+    if (color_source == SS_COLOR_EXPLICIT) {
+        col[0] = colors_in[3 * i]; col[1] = colors_in[3 * i + 1]; col[2] = colors_in[3 * i + 2];
+    } else if (color_source == SS_COLOR_ALBEDO) {
+        col[0] = ss_sigmoid_f32(ar0); col[1] = ss_sigmoid_f32(ar1); col[2] = ss_sigmoid_f32(ar2);
+    } else {
+        ShadeIn in;
+        ss_shade_inputs(cloud, i, cam.cam_pos, in);
+        ShadeState st;
+        double out[3];
+        ss_shade_forward(in, env, st, out);
+        col[0] = (float)out[0]; col[1] = (float)out[1]; col[2] = (float)out[2];
+        if (aux.cells) ss_shade_cells(st, env, aux.cells + 15 * i);
+    }
+    if (!(isfinite(col[0]) && isfinite(col[1]) && isfinite(col[2]))) atomicOr(&flags[1], 1);
+
+    const float zs = vz - ez, ze = vz + ez;
+    SsRecord rec;
+    rec.a = make_float4(t1[0], t1[1], t1[2], t2[0]);
+    rec.b = make_float4(t2[1], t2[2], t4[0], t4[1]);
+    rec.c = make_float4(t4[2], m00, m01, m11);
+    rec.d = make_float4(nf, vz, zs, ze);
+    rec.e = make_float4(col[0], col[1], col[2], ez);
+    int count = 0;
+    if (alive) {
+        int ix0 = (int)x0, iy0 = (int)y0, ix1 = (int)x1, iy1 = (int)y1;
+        rec.r = make_int4(ix0, iy0, ix1, iy1);
+        const int tile = opt.tile;
+        const int ntx = (cam.W + tile - 1) / tile;
+        int tx0 = ix0 / tile, ty0 = iy0 / tile, tx1 = (ix1 - 1) / tile, ty1 = (iy1 - 1) / tile;
+        count = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&tile_counts[ty * ntx + tx], 1);
+    } else {
+        rec.r = make_int4(0, 0, 0, 0);
+    }
+    records[i] = rec;
+    cull_out[i] = (int8_t)code;
+    if (pair_count) pair_count[i] = count;
+    if (aux.c_cam) {
+        for (int k = 0; k < 3; ++k) { aux.c_cam[3 * i + k] = cc[k]; aux.tu_cam[3 * i + k] = tu[k]; aux.tv_cam[3 * i + k] = tv[k]; }
+    }
+    if (aux.eps_z) aux.eps_z[i] = ez;
+    if (aux.center_ndc) { aux.center_ndc[2 * i] = cnx; aux.center_ndc[2 * i + 1] = cny; }
+    if (aux.jac) {
+        aux.jac[4 * i] = j00; aux.jac[4 * i + 1] = j01; aux.jac[4 * i + 2] = j10; aux.jac[4 * i + 3] = j11;
+        aux.jac_ok[i] = ok ? 1 : 0;
+    }
+    if (aux.colors) { aux.colors[3 * i] = col[0]; aux.colors[3 * i + 1] = col[1]; aux.colors[3 * i + 2] = col[2]; }
+}
+
+}  // namespace
+
+extern "C" int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                             int color_source, const float *colors_in, const SsEnv *env,
+                             float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
+                             const SsProjAux *aux, int32_t *flags, void *stream)
+{
+    if (!cloud || !cam || !opt || !tile_counts || !flags) return SS_ERR_INVALID;
+    if (cam->width <= 0 || cam->height <= 0 || opt->tile <= 0) return SS_ERR_INVALID;
+    if (cloud->n == 0) return SS_OK;
+    if (!records || !cull) return SS_ERR_INVALID;
+    if (color_source == SS_COLOR_EXPLICIT && !colors_in) return SS_ERR_INVALID;
+    if (color_source == SS_COLOR_IBL && (!env || !env->diffuse || !env->specular || !env->lut)) return SS_ERR_INVALID;
+    if (cloud->n == 0) return SS_OK;
+    CamF cf;
+    for (int k = 0; k < 16; ++k) { cf.view[k] = (float)cam->view[k]; cf.proj[k] = (float)cam->proj[k]; }
+    // camera.py:69-72: position = -R^T t (float64)
+    for (int k = 0; k < 3; ++k)
+        cf.cam_pos[k] = -(cam->view[k] * cam->view[3] + cam->view[4 + k] * cam->view[7] + cam->view[8 + k] * cam->view[11]);
+    cf.W = cam->width; cf.H = cam->height;
+    SsEnv e = env ? *env : SsEnv{};
+    SsProjAux a = aux ? *aux : SsProjAux{};
+    int blocks = (cloud->n + 255) / 256;
+    preprocess_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        *cloud, cf, *opt, color_source, colors_in, e, reinterpret_cast<SsRecord *>(records), cull,
+        pair_count, tile_counts, a, flags);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}

@@ -1,0 +1,153 @@
+"""Environment light and split-sum shading API (mirror of surfsplat.shading).
+
+EnvironmentLight keeps the learnable log radiance (He, We, 3) and the derived
+maps (irradiance, GGX roughness chain, BRDF LUT) as float32 CUDA tensors.
+refresh() and env_gradient() run the on-the-fly operator kernels of
+csrc/env.cu (shading.py:369-394); nothing T x T is ever materialised.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+DEFAULT_ENV_SHAPE = (16, 32)
+DEFAULT_LEVELS = 6
+DEFAULT_LUT_RES = 64
+DEFAULT_LUT_SAMPLES = 128
+DEFAULT_SPEC_SAMPLES = 128
+
+_LUT_CACHE = {}
+_ROWSUM_CACHE = {}
+
+
+def brdf_lut(res=DEFAULT_LUT_RES, samples=DEFAULT_LUT_SAMPLES):
+    """(res, res, 2) float32 device LUT, row = roughness (shading.py:118-156)."""
+    key = (res, samples, torch.cuda.current_device())
+    if key not in _LUT_CACHE:
+        lib = _lib.load()
+        lut = torch.empty((res, res, 2), device="cuda", dtype=torch.float32)
+        _lib.check(lib.ss_brdf_lut(res, samples, _lib.ptr(lut), _lib.stream_ptr()), "ss_brdf_lut")
+        _LUT_CACHE[key] = lut
+    return _LUT_CACHE[key]
+
+
+def diffuse_rowsums(he, we):
+    key = (he, we, torch.cuda.current_device())
+    if key not in _ROWSUM_CACHE:
+        lib = _lib.load()
+        rs = torch.empty(he * we, device="cuda", dtype=torch.float32)
+        _lib.check(lib.ss_env_rowsums(he, we, _lib.ptr(rs), _lib.stream_ptr()), "ss_env_rowsums")
+        _ROWSUM_CACHE[key] = rs
+    return _ROWSUM_CACHE[key]
+
+
+class EnvironmentLight:
+    """Learnable lat-long environment (shading.py:334-409)."""
+
+    def __init__(self, base_log, levels=DEFAULT_LEVELS, lut_res=DEFAULT_LUT_RES,
+                 lut_samples=DEFAULT_LUT_SAMPLES, spec_samples=DEFAULT_SPEC_SAMPLES):
+        t = base_log if isinstance(base_log, torch.Tensor) else torch.from_numpy(np.asarray(base_log, dtype=np.float64))
+        t = t.to(device="cuda", dtype=torch.float32).contiguous()
+        if t.dim() != 3 or t.shape[2] != 3 or min(t.shape[:2]) < 2:
+            raise ValueError("base_log must be (He >= 2, We >= 2, 3)")
+        if levels < 1:
+            raise ValueError("at least one roughness level")
+        self.base_log = t
+        self.levels, self.lut_res, self.lut_samples, self.spec_samples = int(levels), int(lut_res), int(lut_samples), int(spec_samples)
+        he, we = self.shape
+        self.base = torch.empty_like(t)
+        self.diffuse = torch.empty_like(t)
+        self.specular = torch.empty((self.levels, he, we, 3), device="cuda", dtype=torch.float32)
+        self.refresh()
+
+    @property
+    def shape(self):
+        return tuple(self.base_log.shape[:2])
+
+    @property
+    def lut(self):
+        return brdf_lut(self.lut_res, self.lut_samples)
+
+    def level_roughness(self):
+        if self.levels == 1:
+            return np.zeros(1)
+        return np.arange(self.levels) / (self.levels - 1.0)
+
+    def refresh(self):
+        lib = _lib.load()
+        he, we = self.shape
+        rs = diffuse_rowsums(he, we)
+        _lib.check(lib.ss_env_refresh(he, we, self.levels, self.spec_samples, _lib.ptr(self.base_log), _lib.ptr(rs),
+                                      _lib.ptr(self.base), _lib.ptr(self.diffuse), _lib.ptr(self.specular),
+                                      _lib.stream_ptr()), "ss_env_refresh")
+
+    def env_gradient(self, d_diffuse, d_specular):
+        """Derived-map gradients -> (d_base, d_base_log) (shading.py:381-394)."""
+        lib = _lib.load()
+        he, we = self.shape
+        dd = torch.as_tensor(d_diffuse, device="cuda", dtype=torch.float32).contiguous() if d_diffuse is not None \
+            else torch.zeros_like(self.base)
+        ds = torch.as_tensor(d_specular, device="cuda", dtype=torch.float32).contiguous() if d_specular is not None \
+            else torch.zeros_like(self.specular)
+        d_base = torch.empty_like(self.base)
+        d_log = torch.empty_like(self.base)
+        _lib.check(lib.ss_env_adjoint(he, we, self.levels, self.spec_samples, _lib.ptr(self.base),
+                                      _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(dd), _lib.ptr(ds),
+                                      _lib.ptr(d_base), _lib.ptr(d_log), _lib.stream_ptr()), "ss_env_adjoint")
+        return d_base, d_log
+
+    @staticmethod
+    def uniform(value=0.5, shape=DEFAULT_ENV_SHAPE, levels=DEFAULT_LEVELS):
+        return EnvironmentLight(np.log(np.full(tuple(shape) + (3,), float(value))), levels=levels)
+
+    @staticmethod
+    def from_base(base, levels=DEFAULT_LEVELS):
+        return EnvironmentLight(np.log(np.maximum(np.asarray(base, dtype=np.float64), 1e-8)), levels=levels)
+
+    def copy(self):
+        return EnvironmentLight(self.base_log.clone(), self.levels, self.lut_res, self.lut_samples, self.spec_samples)
+
+
+SRGB_LIN_BOUND = 0.0031308
+
+
+def _srgb(t):
+    return torch.where(t <= SRGB_LIN_BOUND, t * 12.92,
+                       1.055 * torch.pow(torch.clamp(t, min=SRGB_LIN_BOUND), 1.0 / 2.4) - 0.055)
+
+
+def _srgb_grad(t):
+    return torch.where(t <= SRGB_LIN_BOUND, torch.full_like(t, 12.92),
+                       (1.055 / 2.4) * torch.pow(torch.clamp(t, min=SRGB_LIN_BOUND), 1.0 / 2.4 - 1.0))
+
+
+def tone_map(img, mode="ldr"):
+    """shading.py:54-65 on device tensors."""
+    if mode == "ldr":
+        return _srgb(torch.clamp(img, 0.0, 1.0))
+    if mode == "hdr-loss":
+        return _srgb(torch.log1p(torch.clamp(img, min=0.0)))
+    raise ValueError(f"unknown tone map mode {mode!r}")
+
+
+def tone_map_backward(img, mode, g_out):
+    """shading.py:68-79 on device tensors."""
+    if mode == "ldr":
+        inside = (img > 0.0) & (img < 1.0)
+        return torch.where(inside, g_out * _srgb_grad(torch.clamp(img, 0.0, 1.0)), torch.zeros_like(img))
+    if mode == "hdr-loss":
+        x = torch.clamp(img, min=0.0)
+        return torch.where(img > 0.0, g_out * _srgb_grad(torch.log1p(x)) / (1.0 + x), torch.zeros_like(img))
+    raise ValueError(f"unknown tone map mode {mode!r}")
+
+
+def shade_surfels(cloud, env, camera):
+    """Per-surfel IBL colours (shading.py:447-503) via the preprocess kernel's
+    shading stage.  Returns (colors (N,3) float32, cells (N,15) int32)."""
+    from .preprocess import PreprocessOptions, run_preprocess
+    st = run_preprocess(cloud, camera, PreprocessOptions(), color_source=_lib.SS_COLOR_IBL, env=env,
+                        want_aux=True)
+    return st.aux["colors"], st.aux["cells"]

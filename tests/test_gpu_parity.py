@@ -1,0 +1,156 @@
+"""CUDA path vs oracle / reference golden fixtures (needs a B200).
+
+Every call goes through the package API, i.e. through the C ABI of
+libss_b200.so.  Tolerances: tile lists, sort orders, cull codes, rects,
+nlayers and touched counts bit-exact; images 1e-4 relative (+1e-6 abs);
+gradients 1e-3 relative with an array-scaled floor (tests/parity.py).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_io import SCENES, camera_of, cloud_of, load, proj_of
+from parity import grad_close, host, image_close
+
+pytestmark = pytest.mark.gpu
+
+import paper_2605_05876_b200 as ss  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def _render(d, **over):
+    cloud = ss.SurfelCloud.from_host(cloud_of(d))
+    cam = ss.Camera(**vars(camera_of(d)))
+    env = None
+    colors = None
+    src = str(d["color_source"])
+    if src == "explicit":
+        colors = d["colors_in"]
+    if "env_base_log" in d:
+        env = ss.EnvironmentLight(d["env_base_log"], levels=int(d["env_levels"]))
+    opt = ss.RenderOptions(background=tuple(float(v) for v in d["background"]),
+                           mip_enabled=bool(d["mip_enabled"]), k_max=int(d["k_max"]), **over)
+    return cloud, cam, env, ss.render(cloud, cam, opt, env=env, colors=colors)
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_preprocess_matches_oracle_bit_exact(name):
+    d = load(name)
+    cloud, cam, env, res = _render(d)
+    ref = O.preprocess(cloud_of(d), camera_of(d), mip_enabled=bool(d["mip_enabled"]))
+    got = res.proj
+    np.testing.assert_array_equal(host(got.cull_code), ref["cull_code"])
+    np.testing.assert_array_equal(host(got.source_index), ref["source_index"])
+    np.testing.assert_array_equal(host(got.rect), ref["rect"])
+    for k in ("t1", "t2", "t4", "view_z", "eps_z", "sinv", "n_f", "c_cam", "tu_cam", "tv_cam", "jac"):
+        np.testing.assert_array_equal(host(getattr(got, k)), ref[k], err_msg=k)
+    np.testing.assert_array_equal(host(got.jac_ok), ref["jac_ok"])
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_tile_lists_bit_exact(name):
+    """Tile offsets and sort order equal np.lexsort's on the same records, and
+    the reference's own lists whenever the records' rects agree."""
+    d = load(name)
+    _, _, _, res = _render(d)
+    proj = res.proj
+    to, pr = O.bin_and_sort(host(proj.rect), host(proj.z_start), proj.width, proj.height)
+    np.testing.assert_array_equal(host(res.tile_offsets), to)
+    np.testing.assert_array_equal(host(res.pair_rec), pr)
+    if np.array_equal(host(proj.rect), d["proj_rect"]):
+        np.testing.assert_array_equal(host(res.tile_offsets), d["tile_offsets"])
+        np.testing.assert_array_equal(host(res.pair_rec), d["pair_rec"])
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_forward_images_match_reference(name):
+    d = load(name)
+    _, _, _, res = _render(d)
+    for k in ("rgb", "alpha", "depth"):
+        bad, err = image_close(getattr(res, k), d[k])
+        assert bad == 0, f"{k}: {bad} pixels off, max abs err {err}"
+    np.testing.assert_array_equal(host(res.nlayers), d["nlayers"])
+    assert res.stats["discarded_overflow"] == int(d["discarded"])
+
+
+def test_stacks_and_cover_counts():
+    d = load("explicit_cons")
+    _, _, _, res = _render(d, collect_stacks=True, with_cover_counts=True)
+    np.testing.assert_array_equal(host(res.cover_counts), d["cover_counts"])
+    np.testing.assert_array_equal(host(res.stacks["member_count"]), d["stack_member_count"])
+    for k in ("weight_sum", "color_sum"):
+        bad, err = image_close(res.stacks[k], d[f"stack_{k}"], rel=1e-4, abs_=1e-6)
+        assert bad == 0, (k, err)
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_backward_matches_reference(name):
+    d = load(name)
+    cloud, cam, env, res = _render(d)
+    back = ss.backward_image(cloud, res, g_rgb=d["g_rgb_in"], g_alpha=d.get("g_alpha_in"),
+                             cons_scale=float(d["cons_scale"]))
+    for k in ("centers", "quats", "log_scales", "albedo_raw", "metallic_raw", "roughness_raw", "colors",
+              "ss_grad", "env_base_log"):
+        if f"g_{k}" not in d:
+            continue
+        bad, err = grad_close(getattr(back, k), d[f"g_{k}"])
+        assert bad == 0, f"{k}: {bad} entries off, max err/scale {err}"
+    np.testing.assert_array_equal(host(back.touched), d["g_touched"])
+    bad, _ = grad_close(back.background, d["g_background"], rel=1e-4)
+    assert bad == 0
+    assert back.cons_loss == pytest.approx(float(d["g_cons_loss"]), rel=1e-4, abs=1e-12)
+
+
+def test_env_refresh_and_adjoint_match_reference():
+    d = load("env_ops")
+    env = ss.EnvironmentLight(d["base_log"], levels=int(d["levels"]))
+    for k in ("base", "diffuse", "specular"):
+        bad, err = image_close(getattr(env, k), d[k], rel=1e-5)
+        assert bad == 0, (k, err)
+    db, dl = env.env_gradient(d["d_diffuse"], d["d_specular"])
+    assert grad_close(db, d["d_base"], rel=1e-4)[0] == 0
+    assert grad_close(dl, d["d_base_log"], rel=1e-4)[0] == 0
+    bad, err = image_close(env.lut, d["lut"], rel=1e-5, abs_=1e-7)
+    assert bad == 0, err
+
+
+def test_empty_and_all_culled():
+    cam = ss.Camera.perspective(16, 16, 45.0, (0.0, -3.0, 0.0), (0.0, 0.0, 0.0))
+    empty = ss.SurfelCloud(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 2)), np.zeros((0, 3)),
+                           np.zeros(0), np.zeros(0))
+    opt = ss.RenderOptions(background=(0.4, 0.5, 0.6))
+    res = ss.render(empty, cam, opt)
+    assert float(res.alpha.abs().max()) == 0.0 and res.stats["pairs"] == 0
+    back = ss.backward_image(empty, res, g_rgb=np.ones((16, 16, 3)))
+    assert back.centers.shape == (0, 3)
+    q = np.array([[1.0, 0.0, 0.0, 0.0]])
+    behind = ss.SurfelCloud([[0.0, -10.0, 0.0]], q, np.log([[0.3, 0.3]]), np.zeros((1, 3)), [0.0], [0.0])
+    res = ss.render(behind, cam, opt)
+    assert int(res.nlayers.max()) == 0
+    np.testing.assert_allclose(host(res.rgb), np.broadcast_to(np.float32([0.4, 0.5, 0.6]), (16, 16, 3)))
+
+
+def test_errors_are_loud():
+    d = load("explicit_cons")
+    cloud = ss.SurfelCloud.from_host(cloud_of(d))
+    cam = ss.Camera(**vars(camera_of(d)))
+    bad_colors = d["colors_in"].copy()
+    bad_colors[3, 1] = np.nan
+    with pytest.raises(ValueError):
+        ss.render(cloud, cam, colors=bad_colors)
+    with pytest.raises(ValueError):
+        ss.render(cloud, cam, ss.RenderOptions(depth_mode="ternary"))
+    q = cloud.quats.clone()
+    q[0] = 0.0
+    zc = ss.SurfelCloud(cloud.centers, q, cloud.log_scales, cloud.albedo_raw, cloud.metallic_raw,
+                        cloud.roughness_raw)
+    with pytest.raises(ValueError):
+        ss.render(zc, cam)
+
+
+def test_repeat_is_deterministic_forward():
+    d = load("config0_small")
+    _, _, _, a = _render(d)
+    _, _, _, b = _render(d)
+    assert torch.equal(a.rgb, b.rgb) and torch.equal(a.pair_rec, b.pair_rec)
