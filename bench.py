@@ -1,0 +1,322 @@
+"""Headline benchmark: fwd+bwd views/sec, 1M surfels @ 800^2 (BASELINE config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one inverse-rendering step over 64 views (sharded 64/N per rank),
+i.e. per view preprocess+shade, binning/sort, fused forward+L1 loss, backward,
+per-surfel chain; then env adjoint, NCCL all-reduce (N>1), Adam, quaternion
+renorm and env refresh (paper_2605_05876_b200.step.TrainStep).  Synthetic
+seeded data of the config's shape (no dataset ships with the reference):
+ground-truth surfels on a noise-displaced unit sphere, targets rendered from
+them, optimised parameters = truth + perturbation.  Prints ONE JSON line.
+
+`value` times the step with inputs resident in HBM; `e2e` times the public
+TrainStep.step() with the step's target images copied from pinned host memory
+every step (overlapped on a copy stream) and the loss read back.  The working
+set (56 MB params + 64 x 7.7 MB targets + ~0.3 GB/view of records and pairs)
+exceeds the 126 MB L2, so no explicit L2 flush is done between steps.
+
+--impl reference times the CPU oracle (oracle/, the restatement of the
+reference's numba/numpy path) on this host's cores for one view of the same
+workload (env reduced to 64x128 as BASELINE.md prescribes for config 2).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+N_SURFELS = 1_000_000
+RES = 800
+VIEWS_PER_STEP = 64
+ENV_SHAPE = (128, 256)
+METRIC = "fwd+bwd views/sec, 1M surfels @800², at 1/2/4/8 B200; ncu HBM GB/s vs peak"
+UNIT = "views/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def _config(extra=None):
+    cfg = {"workload": "config2: 1M surfels, 800x800, 64 views/step sharded by view, env 128x256x3, "
+                       "L1 loss in linear space, Adam + env refresh per step",
+           "surfels": N_SURFELS, "image": [RES, RES], "views_per_step": VIEWS_PER_STEP,
+           "env": list(ENV_SHAPE), "cameras": "Fibonacci sphere r=3.5, FOV 45 deg (assumed)",
+           "l2": "inputs larger than L2 (no flush)"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (reference arm and cpu_baseline)
+
+
+def cpu_oracle_view(n=N_SURFELS, env_shape=(64, 128), seed=0):
+    """One fwd+bwd view of the config-2 workload on the CPU oracle.  Returns
+    (seconds, threads, sample description)."""
+    from types import SimpleNamespace
+
+    from oracle import oracle as O
+    from paper_2605_05876_b200 import scenes
+    from paper_2605_05876_b200.camera import fibonacci_cameras
+
+    gt = scenes.config2(seed, n)
+    opt = scenes.perturb(gt, seed + 1)
+    cam = fibonacci_cameras(VIEWS_PER_STEP, 3.5, RES, RES)[0]
+    env = O.EnvOracle(np.log(scenes.env_lognormal(*env_shape, seed + 2)))
+    cg, co = SimpleNamespace(**gt), SimpleNamespace(**opt)
+    target = O.render(cg, cam, env=env).rgb
+    t0 = time.perf_counter()
+    res = O.render(co, cam, env=env)
+    _, g = O.photometric_l1(res.rgb, target)
+    O.backward_image(co, res, g, None, 0.0, env=env)
+    dt = time.perf_counter() - t0
+    return dt, O.num_threads(), (f"1 view of config 2 ({n} surfels, {RES}x{RES}) fwd+L1+bwd on the C oracle, "
+                                 f"env reduced to {env_shape[0]}x{env_shape[1]} (BASELINE.md)")
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    for _ in range(max(args.warmup, 0) and 1):
+        cpu_oracle_view(n=100_000)
+    times = []
+    for _ in range(args.steps):
+        dt, cores, sample = cpu_oracle_view()
+        times.append(dt)
+    v = 1.0 / float(np.mean(times))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+            "data": "synthetic", "config": _config({"sample": sample}),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index):
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, nm in enumerate(names):
+                if r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_05876_b200 as ss
+    from paper_2605_05876_b200 import scenes
+    from paper_2605_05876_b200.step import TrainStep
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    views_per_rank = VIEWS_PER_STEP // world
+    my_views = list(range(rank * views_per_rank, (rank + 1) * views_per_rank))
+
+    gt = scenes.config2(0, N_SURFELS)
+    init = scenes.perturb(gt, 1)
+    env_base = scenes.env_lognormal(*ENV_SHAPE, 2)
+    cams_all = ss.fibonacci_cameras(VIEWS_PER_STEP, 3.5, RES, RES)
+    cams = [cams_all[i] for i in my_views]
+
+    # targets rendered from ground truth (linear HDR), then kept resident
+    gt_cloud = ss.SurfelCloud(**gt)
+    gt_env = ss.EnvironmentLight.from_base(env_base)
+    targets = [ss.render(gt_cloud, c, ss.RenderOptions(), env=gt_env).rgb.contiguous() for c in cams]
+    del gt_cloud
+    torch.cuda.synchronize()
+
+    cloud = ss.SurfelCloud(**init)
+    env = ss.EnvironmentLight(np.log(env_base) + np.random.default_rng(3).normal(0, 0.1, env_base.shape))
+    ts = TrainStep(cloud, env, RES, RES)
+    ts.size_pairs(cams[:4])
+    stream = torch.cuda.current_stream()
+
+    def one_step():
+        return ts.step(cams, targets)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if ts.check_overflow():
+        ts.size_pairs(cams, slack=1.3)
+        one_step()
+
+    # ---- timed region: inputs resident in HBM ----
+    clocks = Clocks(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # dominant-kernel timing: events around every train_backward launch
+    ts.kernel_events = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    kev = ts.kernel_events
+    ts.kernel_events = None
+    clk = clocks.stop() if clocks else None
+    t = torch.tensor([step_ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms = float(t.item())
+    value = VIEWS_PER_STEP / (step_ms / 1e3)
+
+    # dominant kernel (raster backward) share and roofline, live CUDA events
+    per_kernel = {}
+    for name, a, b in kev:
+        per_kernel.setdefault(name, []).append(a.elapsed_time(b))
+    ts.collect_stats = True
+    one_step()
+    ts.collect_stats = False
+    stats = ts.last_stats()
+
+    # ---- e2e: public API with host-resident targets ----
+    host_targets = [tg.cpu().pin_memory() for tg in targets]
+    for _ in range(2):
+        ts.step_host(cams, host_targets).item()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = time.perf_counter()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    for _ in range(args.steps):
+        ts.step_host(cams, host_targets).item()
+    eb.record(stream)
+    torch.cuda.synchronize()
+    e_ms = ea.elapsed_time(eb) / args.steps
+    et = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e_ms = float(et.item())
+    h2d = sum(h.numel() * h.element_size() for h in host_targets) * world
+    e2e = {"value": VIEWS_PER_STEP / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": 4 * world, "wall_ms_per_step": 1e3 * (time.perf_counter() - e0) / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = _peaks()
+    P, Nk = stats["pairs_mean"], stats["kept_mean"]
+    HW = RES * RES
+    bwd_ms = float(np.mean(per_kernel.get("train_backward", [float("nan")])))
+    fwd_ms = float(np.mean(per_kernel.get("train_forward", [float("nan")])))
+    # algorithmic bytes per launch: raster bwd gathers 96 B/pair
+    # + 4 B list entry, reads its per-pixel upstream (16 B/px) and writes the
+    # 80 B record accumulator of every kept record
+    bwd_bytes = 100.0 * P + 16.0 * HW + 80.0 * Nk
+    achieved = bwd_bytes / (bwd_ms / 1e3) / 1e9
+    view_bytes = 176.0 * N_SURFELS + 352.0 * Nk + 236.0 * P + 40.0 * HW
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        dt, cores, sample = cpu_oracle_view()
+        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    launches = ts.launches_per_step * args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": _config({"parallelism": f"dp{world} over views", "pairs_per_view": P, "kept_per_view": Nk}),
+        "e2e": e2e,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "raster backward (ss_train_backward)",
+                     "algorithmic_bytes_per_launch": bwd_bytes, "avg_launch_ms": bwd_ms,
+                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)"},
+        "view_roofline": {"bytes_per_view": view_bytes,
+                          "achieved_gbs": view_bytes * VIEWS_PER_STEP / world / (step_ms / 1e3) / 1e9,
+                          "frac": view_bytes * VIEWS_PER_STEP / world / (step_ms / 1e3) / 1e9 / peak},
+        "kernel_ms": {k: float(np.mean(v)) for k, v in per_kernel.items()},
+        "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
+        "loss": float(ts.loss_f.item()),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

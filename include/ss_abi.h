@@ -139,6 +139,22 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
                        int k_max, const float *g_rgb, const float *g_alpha, float cons_scale,
                        float *rec_acc, double *cons_loss, void *stream);
 
+/* ---- fused training step (SURVEY §8d "fwd+bwd view") ----------------------
+ * ss_train_forward: the forward walk fused with the L1 photometric loss
+ * (losses.py:94-108, lambda_ssim=0) against `target` (H,W,3) and with the
+ * per-pixel suffix recursion of backward.py:201-238.  Writes per pixel and
+ * layer the float4 (A, dL/dC_raw rgb) into `coef` (k_max*H*W*4 floats, layer-
+ * major planes) and adds sum|rgb - target| into loss_sum (1 double).  rgb is
+ * nullable.  ss_train_backward: pass 2 of backward.py:240-320 only, reading
+ * `coef`; accumulates into rec_acc exactly like ss_raster_backward. */
+int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
+                     const int32_t *pair_rec, const float *records, const float *background,
+                     int k_max, const float *target, float *coef, double *loss_sum, float *rgb,
+                     void *stream);
+int ss_train_backward(int width, int height, int tile, const int32_t *tile_offsets,
+                      const int32_t *pair_rec, const float *records, int k_max, const float *coef,
+                      float *rec_acc, void *stream);
+
 /* ---- chain backward -------------------------------------------------------
  * Replaces the per-surfel tail of backward_image() (backward.py:398-461,
  * 473-548), shade_backward() (shading.py:525-616) and quat_frame_backward()

@@ -80,6 +80,9 @@ _SIGNATURES = {
     "ss_grid_cells": [ctypes.c_int, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_int, c_p, c_p],
     "ss_isolation": [ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float,
                      ctypes.c_int, c_p, c_p],
+    "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
+                         ctypes.c_int, c_p, c_p, c_p, c_p, c_p],
+    "ss_train_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p],
     "ss_split_children": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64, c_p],
 }
 

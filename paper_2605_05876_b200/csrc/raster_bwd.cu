@@ -29,6 +29,7 @@ constexpr int KC = SS_KMAX_CAP;
 constexpr int NCH = 18;  // reduced channels: t1(3) t2(3) t4(3) sinv(3) nf col(3) vz ss
 
 struct BwdParams {
+    const float4 *coef;  // kCoef: per-layer (A, dL/dC_raw) from ss_train_forward
     int W, H, tile, ntx, k_max;
     float bg0, bg1, bg2, cons_scale;
     const int32_t *offsets;
@@ -46,6 +47,7 @@ __device__ __forceinline__ void stage_record(SsRecord *dst, const SsRecord *__re
     for (int k = 0; k < 6; ++k) d[k] = __ldg(s + k);
 }
 
+template <bool kCoef>
 __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
 {
     extern __shared__ SsRecord srec[];
@@ -69,9 +71,10 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
     const int nthreads = blockDim.x;
 
     // ---------------- pass 1: layer sums (rasterizer walk replay) ----------
-    float lw[KC], lc0[KC], lc1[KC], lc2[KC], lzs[KC], lz2s[KC], lz0[KC];
+    constexpr int KP = kCoef ? 1 : KC;
+    float lw[KP], lc0[KP], lc1[KP], lc2[KP], lzs[KP], lz2s[KP], lz0[KP];
     int nl = 0;
-    {
+    if constexpr (!kCoef) {
         float Wg = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Zs = 0.f, Z2s = 0.f, z0 = 0.f, zmax = 0.f;
         bool stopped = false;
         for (int base = p0; base < p1; base += nthreads) {
@@ -127,9 +130,9 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
     // ------- per-pixel layer gradients (float64, backward.py:160-238) -------
     // Stored per layer: A (weight term), gC (3), B (depth), Cq (variance),
     // zb (layer mean depth), vr (raw variance): g_w = A + gC.c + B dz + Cq (dz^2 - vr)
-    float cA[KC], cC0[KC], cC1[KC], cC2[KC], cB[KC], cQ[KC], cZb[KC], cV[KC];
+    float cA[KP], cC0[KP], cC1[KP], cC2[KP], cB[KP], cQ[KP], cZb[KP], cV[KP];
     double cons_pix = 0.0;
-    if (nl > 0) {
+    if (!kCoef && nl > 0) {
         double a[KC], tb[KC], zb[KC], vr[KC], gw_c[KC], gz_c[KC], gv_c[KC];
         double trans = 1.0;
         for (int m = 0; m < nl; ++m) {
@@ -194,9 +197,15 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
     {
         int m_cur = 0, group_n = 0;
         float zmax = 0.f;
-        bool stopped = nl == 0;
+        bool stopped = kCoef ? !live : nl == 0;
+        const int m_end = kCoef ? P.k_max : nl;
+        const size_t HW = (size_t)P.W * P.H;
         float A = 0.f, G0 = 0.f, G1 = 0.f, G2 = 0.f, Bz = 0.f, Qv = 0.f, Zb = 0.f, Vr = 0.f;
-        if (nl > 0) { A = cA[0]; G0 = cC0[0]; G1 = cC1[0]; G2 = cC2[0]; Bz = cB[0]; Qv = cQ[0]; Zb = cZb[0]; Vr = cV[0]; }
+        if (kCoef) {
+            if (live) { const float4 c = P.coef[pix]; A = c.x; G0 = c.y; G1 = c.z; G2 = c.w; }
+        } else if (nl > 0) {
+            A = cA[0]; G0 = cC0[0]; G1 = cC1[0]; G2 = cC2[0]; Bz = cB[0]; Qv = cQ[0]; Zb = cZb[0]; Vr = cV[0];
+        }
         for (int base = p0; base < p1; base += nthreads) {
             const int cn = min(nthreads, p1 - base);
             __syncthreads();
@@ -224,9 +233,12 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
                             ++m_cur;
                             group_n = 0;
                             zmax = 0.f;
-                            if (m_cur >= P.k_max || m_cur >= nl) {
+                            if (m_cur >= P.k_max || m_cur >= m_end) {
                                 stopped = true;
                                 go = false;
+                            } else if (kCoef) {
+                                const float4 c = P.coef[(size_t)m_cur * HW + pix];
+                                A = c.x; G0 = c.y; G1 = c.z; G2 = c.w;
                             } else {
                                 A = cA[m_cur]; G0 = cC0[m_cur]; G1 = cC1[m_cur]; G2 = cC2[m_cur];
                                 Bz = cB[m_cur]; Qv = cQ[m_cur]; Zb = cZb[m_cur]; Vr = cV[m_cur];
@@ -284,6 +296,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
         }
     }
 
+    if (kCoef) return;
     // consolidation value: block reduce, one double atomic per CTA
     double cp = cons_pix;
 #pragma unroll
@@ -315,7 +328,27 @@ extern "C" int ss_raster_backward(int width, int height, int tile, const int32_t
     P.g_rgb = g_rgb; P.g_alpha = g_alpha; P.acc = rec_acc; P.cons_loss = cons_loss;
     const int nty = (height + tile - 1) / tile;
     const int threads = tile * tile;
-    raster_bwd_kernel<<<P.ntx * nty, threads, threads * sizeof(SsRecord), (cudaStream_t)stream>>>(P);
+    P.coef = nullptr;
+    raster_bwd_kernel<false><<<P.ntx * nty, threads, threads * sizeof(SsRecord), (cudaStream_t)stream>>>(P);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_train_backward(int width, int height, int tile, const int32_t *tile_offsets,
+                                 const int32_t *pair_rec, const float *records, int k_max, const float *coef,
+                                 float *rec_acc, void *stream)
+{
+    if (width <= 0 || height <= 0 || tile != 16 || k_max < 1 || k_max > SS_KMAX_CAP) return SS_ERR_INVALID;
+    if (!tile_offsets || !coef) return SS_ERR_INVALID;
+    BwdParams P{};
+    P.W = width; P.H = height; P.tile = tile; P.ntx = (width + tile - 1) / tile; P.k_max = k_max;
+    P.offsets = tile_offsets; P.pair_rec = pair_rec;
+    P.records = reinterpret_cast<const SsRecord *>(records);
+    P.acc = rec_acc;
+    P.coef = reinterpret_cast<const float4 *>(coef);
+    const int nty = (height + tile - 1) / tile;
+    const int threads = tile * tile;
+    raster_bwd_kernel<true><<<P.ntx * nty, threads, threads * sizeof(SsRecord), (cudaStream_t)stream>>>(P);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

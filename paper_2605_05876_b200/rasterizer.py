@@ -51,8 +51,8 @@ class RenderOptions:
             raise ValueError("only the default coverage rate gamma = 2*pi is implemented")
         if not 1 <= int(self.k_max) <= _lib.KMAX_CAP:
             raise ValueError(f"k_max must be in [1, {_lib.KMAX_CAP}]")
-        if int(self.tile) not in (8, 16, 24, 32):
-            raise ValueError("tile must be 8, 16, 24 or 32")
+        if int(self.tile) not in (8, 16):
+            raise ValueError("tile must be 8 or 16 (one 8x4-pixel warp block per tile quadrant)")
 
 
 @dataclass

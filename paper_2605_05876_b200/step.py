@@ -1,0 +1,257 @@
+"""Batched inverse-rendering step: the BASELINE "fwd+bwd view" workload.
+
+One step = for every view of the batch: preprocess+shade, device binning and
+per-tile sort, fused forward + L1 loss + per-pixel suffix recursion, pass-2
+backward, per-surfel chain (accumulating into the step's gradient buffer);
+then the environment adjoint once for the batch, an NCCL all-reduce of the
+packed gradients when running data-parallel (views sharded across ranks,
+surfels/env replicated), Adam on every parameter tensor, quaternion
+renormalisation and the environment refresh.  This is the reference's
+`fit` step body (train.py:188-248) with the loss of BASELINE config 0 (L1 in
+linear space) and a batch of views instead of one (gradients summed over
+views, the batching SURVEY.md §7 hard part 7 defines).
+
+Everything inside step() is asynchronous: no host synchronisation until the
+caller reads the loss, so the whole step can also be captured in a CUDA graph.
+Pair buffers are sized once from a measured view (x1.5); an overflow (flag
+set by the binning kernel) is reported by check_overflow() so the caller can
+grow the buffers and re-run.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .adam import Adam
+from .preprocess import PreprocessOptions, make_opts
+
+PARAMS = ("centers", "quats", "log_scales", "albedo_raw", "metallic_raw", "roughness_raw")
+_WIDTH = {"centers": 3, "quats": 4, "log_scales": 2, "albedo_raw": 3, "metallic_raw": 1, "roughness_raw": 1}
+
+
+class TrainStep:
+    def __init__(self, cloud, env, width, height, k_max=16, tile=16, background=(0.0, 0.0, 0.0),
+                 lrs=None, pair_capacity=None, process_group=None, options=None):
+        self.lib = _lib.load()
+        self.cloud, self.env = cloud, env
+        self.W, self.H, self.k_max, self.tile = int(width), int(height), int(k_max), int(tile)
+        self.bg = tuple(float(b) for b in background)
+        self.opts = options or PreprocessOptions()
+        self.pg = process_group
+        self.lrs = lrs or {"centers": 1.6e-4, "quats": 1e-3, "log_scales": 5e-3, "albedo_raw": 5e-3,
+                           "metallic_raw": 5e-3, "roughness_raw": 5e-3, "env_base_log": 1e-2}
+        n = len(cloud)
+        dev = cloud.centers.device
+        self.n = n
+        self.ntx = (self.W + tile - 1) // tile
+        self.ntiles = self.ntx * ((self.H + tile - 1) // tile)
+        f32 = dict(device=dev, dtype=torch.float32)
+        i32 = dict(device=dev, dtype=torch.int32)
+        self.records = torch.empty((n, _lib.REC_FLOATS), **f32)
+        self.cull = torch.empty(n, device=dev, dtype=torch.int8)
+        self.tile_counts = torch.zeros(self.ntiles, **i32)
+        self.flags = torch.zeros(4, **i32)
+        self.offsets = torch.empty(self.ntiles + 1, **i32)
+        self.cursors = torch.empty(self.ntiles, **i32)
+        self.coef = torch.empty((self.k_max, self.H * self.W, 4), **f32)
+        self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
+        he, we = env.shape
+        self.T = he * we
+        # packed gradient buffer: params, ss_grad, env d_base_log, loss -- one all-reduce
+        sizes = [n * _WIDTH[k] for k in PARAMS] + [n, 3 * self.T, 1]
+        self.flat = torch.zeros(sum(sizes), **f32)
+        views, off = [], 0
+        for s in sizes:
+            views.append(self.flat[off:off + s])
+            off += s
+        self.grads = {k: views[i].view(n, _WIDTH[k]) if _WIDTH[k] > 1 else views[i] for i, k in enumerate(PARAMS)}
+        self.grads["ss_grad"] = views[len(PARAMS)]
+        self.g_env_log = views[len(PARAMS) + 1].view(he, we, 3)
+        self.loss_f = views[len(PARAMS) + 2]
+        self.touched = torch.zeros(n, **i32)
+        self.loss = torch.zeros(1, device=dev, dtype=torch.float64)
+        self.d_diffuse = torch.zeros_like(env.base)
+        self.d_spec = torch.zeros_like(env.specular)
+        self.d_base = torch.empty_like(env.base)
+        self.adam = Adam()
+        self._cl = _lib.make_cloud(cloud)
+        self._po = make_opts(self.opts, tile)
+        self._envs = _lib.make_env(env)
+        self._gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
+                                _lib.ptr(self.touched), _lib.ptr(self.d_diffuse), _lib.ptr(self.d_spec))
+        self._bg = _lib.fvec(self.bg)
+        self.capacity = 0
+        self.keys = self.pair = None
+        if pair_capacity:
+            self._alloc_pairs(pair_capacity)
+        self.collect_stats = False
+        self._pairs, self._kept, self._nviews = [], [], 0
+        self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
+        self._stage = None
+        self.launches_per_view = 7     # preprocess, scan, scatter, tile sort, train fwd, train bwd, chain
+        self.launches_per_step_fixed = 3 + 7 + 1 + 3  # env adjoint, Adam x7, quat renorm, env refresh
+
+    # -- buffers -----------------------------------------------------------
+    def _alloc_pairs(self, cap):
+        cap = int(cap)
+        dev = self.records.device
+        self.keys = torch.empty(cap, device=dev, dtype=torch.int64)
+        self.pair = torch.empty(cap, device=dev, dtype=torch.int32)
+        self.capacity = cap
+
+    def size_pairs(self, cameras, slack=1.5):
+        """Measure the pair count of a few views (host sync) and size buffers."""
+        worst = 0
+        for cam in cameras:
+            self._preprocess(cam)
+            worst = max(worst, int(self.tile_counts.sum().item()))
+        self._alloc_pairs(max(int(worst * slack), 1024))
+        return worst
+
+    def check_overflow(self):
+        return bool(self.flags[2].item())
+
+    # -- per-view stages ----------------------------------------------------
+    def _preprocess(self, cam):
+        self.tile_counts.zero_()
+        camst = _lib.make_camera(cam)
+        rc = self.lib.ss_preprocess(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
+                                    _lib.SS_COLOR_IBL, None, ctypes.byref(self._envs), _lib.ptr(self.records),
+                                    _lib.ptr(self.cull), None, _lib.ptr(self.tile_counts), None,
+                                    _lib.ptr(self.flags), _lib.stream_ptr())
+        _lib.check(rc, "ss_preprocess")
+        return camst
+
+    def view(self, cam, target):
+        """Forward + backward of one view; gradients accumulate into self.grads."""
+        lib = self.lib
+        s = _lib.stream_ptr()
+        camst = self._preprocess(cam)
+        _lib.check(lib.ss_bin_sort(self.n, _lib.ptr(self.records), _lib.ptr(self.cull), self.W, self.H, self.tile,
+                                   _lib.ptr(self.tile_counts), _lib.ptr(self.offsets), _lib.ptr(self.cursors),
+                                   _lib.ptr(self.keys), _lib.ptr(self.pair), self.capacity, _lib.ptr(self.flags), s),
+                   "ss_bin_sort")
+        ev = self._ev_begin("train_forward")
+        _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(self.offsets), _lib.ptr(self.pair),
+                                        _lib.ptr(self.records), self._bg[0], self.k_max, _lib.ptr(target),
+                                        _lib.ptr(self.coef), _lib.ptr(self.loss), None, s), "ss_train_forward")
+        self._ev_end(ev)
+        self.acc.zero_()
+        ev = self._ev_begin("train_backward")
+        _lib.check(lib.ss_train_backward(self.W, self.H, self.tile, _lib.ptr(self.offsets), _lib.ptr(self.pair),
+                                         _lib.ptr(self.records), self.k_max, _lib.ptr(self.coef),
+                                         _lib.ptr(self.acc), s), "ss_train_backward")
+        self._ev_end(ev)
+        _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
+                                         _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(self.cull),
+                                         _lib.ptr(self.acc), ctypes.byref(self._gs), s), "ss_chain_backward")
+
+    def _ev_begin(self, name):
+        if self.kernel_events is None:
+            return None
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        return (name, a, b)
+
+    def _ev_end(self, ev):
+        if ev is not None:
+            ev[2].record()
+            self.kernel_events.append(ev)
+
+    @property
+    def launches_per_step(self):
+        return self.launches_per_view * self._nviews + self.launches_per_step_fixed
+
+    def last_stats(self):
+        """Pair and kept-record counts of the last step's views (host sync)."""
+        return {"pairs_mean": float(np.mean(self._pairs)) if self._pairs else 0.0,
+                "kept_mean": float(np.mean(self._kept)) if self._kept else 0.0}
+
+    def zero(self):
+        self.flat.zero_()
+        self.touched.zero_()
+        self.d_diffuse.zero_()
+        self.d_spec.zero_()
+        self.loss.zero_()
+        self.flags.zero_()
+
+    def gradients(self, cameras, targets):
+        """Sum of per-view gradients over this rank's views (+ env adjoint)."""
+        if self.capacity == 0:
+            self.size_pairs(cameras[:2])
+        self.zero()
+        self._nviews = len(cameras)
+        self._pairs, self._kept = [], []
+        for cam, tgt in zip(cameras, targets):
+            self.view(cam, tgt)
+            if self.collect_stats:
+                self._pairs.append(int(self.offsets[-1].item()))
+                self._kept.append(int((self.cull == 0).sum().item()))
+        self._finish()
+
+    def _finish(self):
+        he, we = self.env.shape
+        from .shading import diffuse_rowsums
+        _lib.check(self.lib.ss_env_adjoint(he, we, self.env.levels, self.env.spec_samples, _lib.ptr(self.env.base),
+                                           _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(self.d_diffuse),
+                                           _lib.ptr(self.d_spec), _lib.ptr(self.d_base), _lib.ptr(self.g_env_log),
+                                           _lib.stream_ptr()), "ss_env_adjoint")
+        self.loss_f.copy_(self.loss)
+        if self.pg is not None or (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+            dist.all_reduce(self.flat, group=self.pg)
+            dist.all_reduce(self.touched, group=self.pg)
+
+    def apply(self, lr_scale=1.0):
+        """Adam on all tensors, quaternion renorm, env refresh (train.py:241-248)."""
+        for k in PARAMS:
+            p = getattr(self.cloud, k)
+            self.adam.step(k, p, self.grads[k], self.lrs[k] * lr_scale)
+        _lib.check(self.lib.ss_normalize_quats(self.n, _lib.ptr(self.cloud.quats), _lib.stream_ptr()),
+                   "ss_normalize_quats")
+        self.adam.step("env_base_log", self.env.base_log, self.g_env_log, self.lrs["env_base_log"] * lr_scale)
+        self.env.refresh()
+
+    def step(self, cameras, targets):
+        self.gradients(cameras, targets)
+        self.apply()
+        return self.loss_f  # device scalar: sum over views of sum|rgb - target|
+
+    def step_host(self, cameras, host_targets):
+        """step() with the targets in pinned HOST memory: each view's target is
+        copied on a side stream into a double buffer, overlapped with the
+        previous view's kernels."""
+        if self.capacity == 0:
+            self.size_pairs(cameras[:2])
+        compute = torch.cuda.current_stream()
+        if self._stage is None:
+            self._stage = [torch.empty((self.H, self.W, 3), device=self.records.device, dtype=torch.float32)
+                           for _ in range(2)]
+            self._copy = torch.cuda.Stream()
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def issue(i):
+            b = i % 2
+            with torch.cuda.stream(self._copy):
+                if i >= 2:
+                    self._copy.wait_event(free[b])
+                self._stage[b].copy_(host_targets[i], non_blocking=True)
+                ready[b].record(self._copy)
+
+        self.zero()
+        self._nviews = len(cameras)
+        issue(0)
+        for i, cam in enumerate(cameras):
+            if i + 1 < len(cameras):
+                issue(i + 1)
+            compute.wait_event(ready[i % 2])
+            self.view(cam, self._stage[i % 2])
+            free[i % 2].record(compute)
+        self._finish()
+        self.apply()
+        return self.loss_f
