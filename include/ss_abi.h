@@ -107,11 +107,13 @@ int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessO
  * (z_start, record) keys, and a per-tile sort by (z_start, record index) so
  * the result equals np.lexsort((rec, z_start, tile)) bit for bit.
  * pair_capacity bounds pair_rec/keys; flags[2] is set when it overflowed.
- * keys: uint64 scratch of pair_capacity entries; cursors: ntiles ints scratch. */
+ * keys: uint64 scratch of pair_capacity entries; cursors: ntiles ints scratch.
+ * pair_rect (2 uint32 per pair) receives each pair's record rect packed as
+ * (x0 | y0 << 16, x1 | y1 << 16), the rasterisers' cull input. */
 int ss_bin_sort(int n, const float *records, const int8_t *cull, int width, int height, int tile,
                 const int32_t *tile_counts, int32_t *tile_offsets, int32_t *cursors,
-                uint64_t *keys, int32_t *pair_rec, int64_t pair_capacity, int32_t *flags,
-                void *stream);
+                uint64_t *keys, int32_t *pair_rec, uint32_t *pair_rect, int64_t pair_capacity,
+                int32_t *flags, void *stream);
 
 /* ---- raster forward -------------------------------------------------------
  * Replaces _forward_kernel (rasterizer.py:119-249), interval depth mode.
@@ -121,7 +123,7 @@ int ss_bin_sort(int n, const float *records, const int8_t *cull, int width, int 
  * discarded (1 int64, the discarded_overflow statistic). */
 typedef struct SsStacks { float *w, *c, *z, *z2; int32_t *n; } SsStacks;
 int ss_raster_forward(int width, int height, int tile, const int32_t *tile_offsets,
-                      const int32_t *pair_rec, const float *records, const float *background,
+                      const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
                       int k_max, float *rgb, float *alpha, float *depth, int32_t *nlayers,
                       int32_t *pair_cover, const SsStacks *stacks, unsigned long long *discarded,
                       void *stream);
@@ -135,7 +137,7 @@ int ss_raster_forward(int width, int height, int tile, const int32_t *tile_offse
  * [18] covering-pixel count (as float bits of an int32 counter).  cons_loss
  * (1 double, zeroed) receives the consolidation penalty value. */
 int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offsets,
-                       const int32_t *pair_rec, const float *records, const float *background,
+                       const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
                        int k_max, const float *g_rgb, const float *g_alpha, float cons_scale,
                        float *rec_acc, double *cons_loss, void *stream);
 
@@ -143,17 +145,21 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
  * ss_train_forward: the forward walk fused with the L1 photometric loss
  * (losses.py:94-108, lambda_ssim=0) against `target` (H,W,3) and with the
  * per-pixel suffix recursion of backward.py:201-238.  Writes per pixel and
- * layer the float4 (A, dL/dC_raw rgb) into `coef` (k_max*H*W*4 floats, layer-
- * major planes) and adds sum|rgb - target| into loss_sum (1 double).  rgb is
- * nullable.  ss_train_backward: pass 2 of backward.py:240-320 only, reading
- * `coef`; accumulates into rec_acc exactly like ss_raster_backward. */
+ * layer the float4 (A, dL/dC_raw rgb) into `coef` (k_max*H*W*4 floats,
+ * layer-major planes), the depth at which each layer closed into `thr`
+ * (k_max*H*W floats) and the number of closed layers into `ncl` (H*W int32),
+ * and adds sum|rgb - target| into loss_sum (1 double).  rgb is nullable.
+ * ss_train_backward: pass 2 of backward.py:240-320 without the walk: layer
+ * membership from `thr`/`ncl`, one thread per (record, tile) pair; accumulates
+ * into rec_acc exactly like ss_raster_backward (channel 16 stays 0: no
+ * consolidation term in this loss).  pair_rect is accepted for symmetry. */
 int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
-                     const int32_t *pair_rec, const float *records, const float *background,
-                     int k_max, const float *target, float *coef, double *loss_sum, float *rgb,
-                     void *stream);
+                     const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
+                     const float *background, int k_max, const float *target, float *coef, float *thr,
+                     int32_t *ncl, double *loss_sum, float *rgb, void *stream);
 int ss_train_backward(int width, int height, int tile, const int32_t *tile_offsets,
-                      const int32_t *pair_rec, const float *records, int k_max, const float *coef,
-                      float *rec_acc, void *stream);
+                      const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, int k_max,
+                      const float *coef, const float *thr, const int32_t *ncl, float *rec_acc, void *stream);
 
 /* ---- chain backward -------------------------------------------------------
  * Replaces the per-surfel tail of backward_image() (backward.py:398-461,
@@ -217,6 +223,14 @@ int ss_isolation(int n, const float *centers, const float *log_scales, const int
 int ss_split_children(int nsplit, const int32_t *parents, const float *centers, const float *quats,
                       const float *log_scales, float *out_centers, float *out_log_scales,
                       int64_t plus_row0, int64_t minus_row0, void *stream);
+
+/* Diagnostic for the rasterisers' fast coverage test: counts[0] (pixel,
+ * in-rect record) evaluations, counts[1] decisions differing from the exact
+ * reference arithmetic (0 by construction), counts[2] exact fallbacks taken.
+ * counts: 3 uint64, zeroed by the caller. */
+int ss_debug_cover_check(int width, int height, int tile, const int32_t *tile_offsets,
+                         const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
+                         unsigned long long *counts, void *stream);
 
 const char *ss_last_error(void);
 int ss_version(void);

@@ -64,10 +64,10 @@ _lib = None
 _SIGNATURES = {
     "ss_preprocess": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_bin_sort": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
-                    c_p, c_p, ctypes.c_int64, c_p, c_p],
-    "ss_raster_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
+                    c_p, c_p, c_p, ctypes.c_int64, c_p, c_p],
+    "ss_raster_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
                           ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
-    "ss_raster_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
+    "ss_raster_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p,
                            ctypes.POINTER(ctypes.c_float), ctypes.c_int, c_p, c_p, ctypes.c_float, c_p, c_p, c_p],
     "ss_chain_backward": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p],
     "ss_brdf_lut": [ctypes.c_int, ctypes.c_int, c_p, c_p],
@@ -80,9 +80,11 @@ _SIGNATURES = {
     "ss_grid_cells": [ctypes.c_int, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_int, c_p, c_p],
     "ss_isolation": [ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float,
                      ctypes.c_int, c_p, c_p],
-    "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
-                         ctypes.c_int, c_p, c_p, c_p, c_p, c_p],
-    "ss_train_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p],
+    "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
+                         ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_train_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p,
+                          c_p, c_p],
+    "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_split_children": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64, c_p],
 }
 

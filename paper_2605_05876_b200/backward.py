@@ -70,7 +70,7 @@ def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0) -> B
     cons = torch.zeros(1, device=dev, dtype=torch.float64)
     bgp, _keep = _lib.fvec(opt.background)
     rc = lib.ss_raster_backward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
-                                _lib.ptr(st.records), bgp, int(opt.k_max), _lib.ptr(g_rgb), _lib.ptr(ga),
+                                _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, int(opt.k_max), _lib.ptr(g_rgb), _lib.ptr(ga),
                                 float(cons_scale), _lib.ptr(acc), _lib.ptr(cons), _lib.stream_ptr())
     _lib.check(rc, "ss_raster_backward")
     g = zero_grads(n, dev)

@@ -69,23 +69,49 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
     }
 }
 
+// Tile s of a record's span, row-major (rasterizer.py:84-89).
+__device__ __forceinline__ int span_tile(const int4 r, int tile, int ntx, int s) {
+    const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile;
+    const int sx = tx1 - tx0 + 1;
+    return (ty0 + s / sx) * ntx + tx0 + s % sx;
+}
+
+// Each record drops its key into every tile bucket of its rect.  Lanes walk
+// their spans in lock step so that lanes hitting the same tile (spatially
+// coherent record order) share one atomic: __match_any_sync groups them, the
+// leader reserves popc slots and every lane takes its rank inside the group.
 __global__ void __launch_bounds__(256) scatter_kernel(
     int n, const SsRecord *__restrict__ records, const int8_t *__restrict__ cull, int ntx, int tile,
     const int32_t *__restrict__ offsets, int32_t *__restrict__ cursors, uint64_t *__restrict__ keys,
     int64_t capacity)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || cull[i] != 0) return;
-    const int4 r = records[i].r;
-    const float zs = records[i].d.z;
-    const uint64_t key = ((uint64_t)orderable(zs) << 32) | (uint32_t)i;
-    int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
-            int t = ty * ntx + tx;
-            int64_t at = (int64_t)offsets[t] + atomicAdd(&cursors[t], 1);
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool alive = i < n && cull[i] == 0;
+    int4 r = make_int4(0, 0, 1, 1);
+    int cnt = 0;
+    uint64_t key = 0;
+    if (alive) {
+        r = records[i].r;
+        const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
+        cnt = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+        key = ((uint64_t)orderable(records[i].d.z) << 32) | (uint32_t)i;
+    }
+    const int maxc = __reduce_max_sync(0xffffffffu, cnt);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int s = 0; s < maxc; ++s) {
+        const bool act = s < cnt;
+        const int t = act ? span_tile(r, tile, ntx, s) : -1 - lane;  // unique dummies never match
+        const unsigned grp = __match_any_sync(0xffffffffu, t);
+        const int leader = __ffs(grp) - 1;
+        int base = 0;
+        if (act && lane == leader) base = atomicAdd(&cursors[t], __popc(grp));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (act) {
+            const int64_t at = (int64_t)offsets[t] + base + __popc(grp & lt);
             if (at < capacity) keys[at] = key;
         }
+    }
 }
 
 // Ascending bitonic network on n elements padded (virtually) with +inf up to
@@ -114,9 +140,15 @@ __device__ __forceinline__ void bitonic_sort(int n, Load ld, Swap sw) {
     (void)ld;
 }
 
+// packed pixel rect of a record, in pair order, for the rasterisers' warp cull
+__device__ __forceinline__ uint2 pack_rect(const SsRecord *__restrict__ recs, int rec) {
+    const int4 r = recs[rec].r;
+    return make_uint2((uint32_t)r.x | ((uint32_t)r.y << 16), (uint32_t)r.z | ((uint32_t)r.w << 16));
+}
+
 __global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(
     const int32_t *__restrict__ offsets, uint64_t *__restrict__ keys, int32_t *__restrict__ pair_rec,
-    int64_t capacity)
+    uint2 *__restrict__ pair_rect, const SsRecord *__restrict__ recs, int64_t capacity)
 {
     extern __shared__ uint64_t skeys[];
     const int t = blockIdx.x;
@@ -133,14 +165,22 @@ __global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(
             uint64_t x = skeys[a], y = skeys[b];
             if (x > y) { skeys[a] = y; skeys[b] = x; }
         });
-        for (int k = threadIdx.x; k < n; k += blockDim.x) pair_rec[o0 + k] = (int32_t)(uint32_t)skeys[k];
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+            const int rec = (int32_t)(uint32_t)skeys[k];
+            pair_rec[o0 + k] = rec;
+            pair_rect[o0 + k] = pack_rect(recs, rec);
+        }
     } else {
         // rare oversized tile: same network directly in global memory
         bitonic_sort(n, 0, [&](int a, int b) {
             uint64_t x = g[a], y = g[b];
             if (x > y) { g[a] = y; g[b] = x; }
         });
-        for (int k = threadIdx.x; k < n; k += blockDim.x) pair_rec[o0 + k] = (int32_t)(uint32_t)g[k];
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+            const int rec = (int32_t)(uint32_t)g[k];
+            pair_rec[o0 + k] = rec;
+            pair_rect[o0 + k] = pack_rect(recs, rec);
+        }
     }
 }
 
@@ -148,11 +188,12 @@ __global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(
 
 extern "C" int ss_bin_sort(int n, const float *records, const int8_t *cull, int width, int height, int tile,
                            const int32_t *tile_counts, int32_t *tile_offsets, int32_t *cursors,
-                           uint64_t *keys, int32_t *pair_rec, int64_t pair_capacity, int32_t *flags,
-                           void *stream)
+                           uint64_t *keys, int32_t *pair_rec, uint32_t *pair_rect, int64_t pair_capacity,
+                           int32_t *flags, void *stream)
 {
     if (width <= 0 || height <= 0 || tile <= 0 || !tile_counts || !tile_offsets || !cursors || !flags)
         return SS_ERR_INVALID;
+    if (width > 65535 || height > 65535) return SS_ERR_INVALID;  // rects are packed as uint16
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -169,8 +210,9 @@ extern "C" int ss_bin_sort(int n, const float *records, const int8_t *cull, int 
                                                         ntx, tile, tile_offsets, cursors, keys, pair_capacity);
         SS_CUDA_CHECK_LAUNCH();
     }
-    tile_sort_kernel<<<ntiles, kSortThreads, kSortCap * sizeof(uint64_t), st>>>(tile_offsets, keys, pair_rec,
-                                                                               pair_capacity);
+    tile_sort_kernel<<<ntiles, kSortThreads, kSortCap * sizeof(uint64_t), st>>>(
+        tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const SsRecord *>(records),
+        pair_capacity);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

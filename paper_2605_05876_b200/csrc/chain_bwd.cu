@@ -66,7 +66,7 @@ __device__ __forceinline__ void rows_of(const ChainParams &P, int i, float t1[3]
     }
 }
 
-__global__ void __launch_bounds__(128) chain_kernel(ChainParams P)
+__global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.cloud.n || P.cull[i] != 0) return;

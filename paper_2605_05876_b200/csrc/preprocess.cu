@@ -38,22 +38,23 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     int32_t *__restrict__ pair_count, int32_t *__restrict__ tile_counts, SsProjAux aux,
     int32_t *__restrict__ flags)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= cloud.n) return;
+    const int i_raw = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in_range = i_raw < cloud.n;
+    const int i = in_range ? i_raw : cloud.n - 1;  // tail lanes recompute the last row, write nothing
     const float c0 = cloud.centers[3 * i], c1 = cloud.centers[3 * i + 1], c2 = cloud.centers[3 * i + 2];
     const float4 q = reinterpret_cast<const float4 *>(cloud.quats)[i];
     const float2 ls = reinterpret_cast<const float2 *>(cloud.log_scales)[i];
     const float ar0 = cloud.albedo_raw[3 * i], ar1 = cloud.albedo_raw[3 * i + 1], ar2 = cloud.albedo_raw[3 * i + 2];
     const float mr = cloud.metallic_raw[i], rr = cloud.roughness_raw[i];
 
-    bool finite = isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(q.x) && isfinite(q.y) &&
+    bool finite = in_range && isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(q.x) && isfinite(q.y) &&
                   isfinite(q.z) && isfinite(q.w) && isfinite(ls.x) && isfinite(ls.y) && isfinite(ar0) &&
                   isfinite(ar1) && isfinite(ar2) && isfinite(mr) && isfinite(rr);
     int code = finite ? 0 : 1;
 
     // quat_to_frame in float32 (surfels.py:40-51)
     float nrm = sqrtf(((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w);
-    if (nrm == 0.0f) atomicOr(&flags[0], 1);
+    if (in_range && nrm == 0.0f) atomicOr(&flags[0], 1);
     float w = q.x / nrm, x = q.y / nrm, y = q.z / nrm, z = q.w / nrm;
     float uh0 = 1.0f - 2.0f * (y * y + z * z), uh1 = 2.0f * (x * y + w * z), uh2 = 2.0f * (x * z - w * y);
     float vh0 = 2.0f * (x * y - w * z), vh1 = 1.0f - 2.0f * (x * x + z * z), vh2 = 2.0f * (y * z + w * x);
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         col[0] = (float)out[0]; col[1] = (float)out[1]; col[2] = (float)out[2];
         if (aux.cells) ss_shade_cells(st, env, aux.cells + 15 * i);
     }
-    if (!(isfinite(col[0]) && isfinite(col[1]) && isfinite(col[2]))) atomicOr(&flags[1], 1);
+    if (in_range && !(isfinite(col[0]) && isfinite(col[1]) && isfinite(col[2]))) atomicOr(&flags[1], 1);
 
     const float zs = vz - ez, ze = vz + ez;
     SsRecord rec;
@@ -172,18 +173,33 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     rec.d = make_float4(nf, vz, zs, ze);
     rec.e = make_float4(col[0], col[1], col[2], ez);
     int count = 0;
+    const int tile = opt.tile;
+    const int ntx = (cam.W + tile - 1) / tile;
+    int tx0 = 0, ty0 = 0, sx = 1;
     if (alive) {
         int ix0 = (int)x0, iy0 = (int)y0, ix1 = (int)x1, iy1 = (int)y1;
         rec.r = make_int4(ix0, iy0, ix1, iy1);
-        const int tile = opt.tile;
-        const int ntx = (cam.W + tile - 1) / tile;
-        int tx0 = ix0 / tile, ty0 = iy0 / tile, tx1 = (ix1 - 1) / tile, ty1 = (iy1 - 1) / tile;
-        count = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
-        for (int ty = ty0; ty <= ty1; ++ty)
-            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&tile_counts[ty * ntx + tx], 1);
+        tx0 = ix0 / tile; ty0 = iy0 / tile;
+        const int tx1 = (ix1 - 1) / tile, ty1 = (iy1 - 1) / tile;
+        sx = tx1 - tx0 + 1;
+        count = sx * (ty1 - ty0 + 1);
     } else {
         rec.r = make_int4(0, 0, 0, 0);
     }
+    // per-tile histogram; lanes in lock step share atomics for equal tiles
+    {
+        __syncwarp();
+        const unsigned full = 0xffffffffu;
+        const int lane = threadIdx.x & 31;
+        const int maxc = __reduce_max_sync(full, count);
+        for (int s = 0; s < maxc; ++s) {
+            const bool act = s < count;
+            const int t = act ? (ty0 + s / sx) * ntx + tx0 + s % sx : -1 - lane;
+            const unsigned grp = __match_any_sync(full, t);
+            if (act && lane == __ffs(grp) - 1) atomicAdd(&tile_counts[t], __popc(grp));
+        }
+    }
+    if (!in_range) return;
     records[i] = rec;
     cull_out[i] = (int8_t)code;
     if (pair_count) pair_count[i] = count;

@@ -22,6 +22,7 @@
 // form of backward.py:278-286.
 #include "ss_common.cuh"
 #include "warp_reduce.cuh"
+#include "raster_walk.cuh"
 
 namespace {
 
@@ -34,33 +35,25 @@ struct BwdParams {
     float bg0, bg1, bg2, cons_scale;
     const int32_t *offsets;
     const int32_t *pair_rec;
+    const uint2 *pair_rect;
     const SsRecord *records;
     const float *g_rgb, *g_alpha;
     float *acc;
     double *cons_loss;
 };
 
-__device__ __forceinline__ void stage_record(SsRecord *dst, const SsRecord *__restrict__ src) {
-    const float4 *s = reinterpret_cast<const float4 *>(src);
-    float4 *d = reinterpret_cast<float4 *>(dst);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) d[k] = __ldg(s + k);
-}
-
 template <bool kCoef>
 __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
 {
-    extern __shared__ SsRecord srec[];
+    __shared__ SsRecord wbuf_all[8][32];
     __shared__ double cons_red[32];
     const int t = blockIdx.x;
-    const int tx = t % P.ntx, ty = t / P.ntx;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int wpr = P.tile >> 3;
-    const int bx = tx * P.tile + (wid % wpr) * 8, by = ty * P.tile + (wid / wpr) * 4;
-    const int px = bx + (lane & 7), py = by + (lane >> 3);
-    const bool live = px < P.W && py < P.H;
-    const float x = ss_ndc_x(px, P.W), y = ss_ndc_y(py, P.H);
-    const size_t pix = live ? (size_t)py * P.W + px : 0;
+    const WarpPix wp = warp_pixels(t, P.ntx, P.tile, P.W, P.H);
+    const int lane = wp.lane, wid = wp.wid;
+    const bool live = wp.live;
+    const size_t pix = wp.pix;
+    const float x = wp.x, y = wp.y;
+    SsRecord *wbuf = wbuf_all[wid];
 
     // owner lane / channel of the transposed warp reduction
     const int my_ch = warp_tr_index<NCH>(lane);
@@ -68,7 +61,6 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
     const bool owner = (__ffs(same) - 1) == lane;
 
     const int p0 = P.offsets[t], p1 = P.offsets[t + 1];
-    const int nthreads = blockDim.x;
 
     // ---------------- pass 1: layer sums (rasterizer walk replay) ----------
     constexpr int KP = kCoef ? 1 : KC;
@@ -76,50 +68,27 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
     int nl = 0;
     if constexpr (!kCoef) {
         float Wg = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Zs = 0.f, Z2s = 0.f, z0 = 0.f, zmax = 0.f;
-        bool stopped = false;
-        for (int base = p0; base < p1; base += nthreads) {
-            const int cn = min(nthreads, p1 - base);
-            __syncthreads();
-            if ((int)threadIdx.x < cn) stage_record(&srec[threadIdx.x], P.records + P.pair_rec[base + threadIdx.x]);
-            __syncthreads();
-            for (int sub = 0; sub < cn; sub += 32) {
-                bool ov = false;
-                if (sub + lane < cn) {
-                    const int4 r = srec[sub + lane].r;
-                    ov = r.x < bx + 8 && r.z > bx && r.y < by + 4 && r.w > by;
-                }
-                unsigned mask = __ballot_sync(0xffffffffu, ov);
-                while (mask) {
-                    const int j = sub + __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    const SsRecord &R = srec[j];
-                    const int4 r = R.r;
-                    if (!(live && !stopped && px >= r.x && px < r.z && py >= r.y && py < r.w)) continue;
-                    if (Wg > 0.f && R.d.z > zmax) {
-                        lw[nl] = Wg; lc0[nl] = C0; lc1[nl] = C1; lc2[nl] = C2;
-                        lzs[nl] = Zs; lz2s[nl] = Z2s; lz0[nl] = z0;
-                        ++nl;
-                        Wg = C0 = C1 = C2 = Zs = Z2s = zmax = 0.f;
-                        if (nl >= P.k_max) { stopped = true; continue; }
-                    }
-                    const float t1[3] = {R.a.x, R.a.y, R.a.z};
-                    const float t2[3] = {R.a.w, R.b.x, R.b.y};
-                    const float t4[3] = {R.b.z, R.b.w, R.c.x};
-                    SsHit h;
-                    if (!ss_intersect(x, y, t1, t2, t4, h)) continue;
-                    const double rho2 = ss_rho2(R.c.y, R.c.z, R.c.w, h.u, h.v);
-                    if (rho2 >= 9.0) continue;
-                    const float w = R.d.x * __expf(-0.5f * (float)rho2);
-                    const float z = R.d.y;
-                    if (Wg == 0.f) z0 = z;
-                    const float dz = z - z0;
-                    Wg += w;
-                    C0 += w * R.e.x; C1 += w * R.e.y; C2 += w * R.e.z;
-                    Zs += w * dz; Z2s += w * dz * dz;
-                    if (R.d.w > zmax) zmax = R.d.w;
-                }
+        bool stopped = !live;
+        walk_tile(wp, p0, p1, P.pair_rec, P.pair_rect, P.records, wbuf, [&](const SsRecord &R, int, int) {
+            if (stopped || !in_rect(wp, R.r)) return;
+            if (Wg > 0.f && R.d.z > zmax) {
+                lw[nl] = Wg; lc0[nl] = C0; lc1[nl] = C1; lc2[nl] = C2;
+                lzs[nl] = Zs; lz2s[nl] = Z2s; lz0[nl] = z0;
+                ++nl;
+                Wg = C0 = C1 = C2 = Zs = Z2s = zmax = 0.f;
+                if (nl >= P.k_max) { stopped = true; return; }
             }
-        }
+            Cover c;
+            if (!ss_cover(x, y, R, c)) return;
+            const float w = R.d.x * __expf(-0.5f * c.rho2);
+            const float z = R.d.y;
+            if (Wg == 0.f) z0 = z;
+            const float dz = z - z0;
+            Wg += w;
+            C0 += w * R.e.x; C1 += w * R.e.y; C2 += w * R.e.z;
+            Zs += w * dz; Z2s += w * dz * dz;
+            if (R.d.w > zmax) zmax = R.d.w;
+        });
         if (live && Wg > 0.f) {
             lw[nl] = Wg; lc0[nl] = C0; lc1[nl] = C1; lc2[nl] = C2;
             lzs[nl] = Zs; lz2s[nl] = Z2s; lz0[nl] = z0;
@@ -206,93 +175,70 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
         } else if (nl > 0) {
             A = cA[0]; G0 = cC0[0]; G1 = cC1[0]; G2 = cC2[0]; Bz = cB[0]; Qv = cQ[0]; Zb = cZb[0]; Vr = cV[0];
         }
-        for (int base = p0; base < p1; base += nthreads) {
-            const int cn = min(nthreads, p1 - base);
-            __syncthreads();
-            if ((int)threadIdx.x < cn) stage_record(&srec[threadIdx.x], P.records + P.pair_rec[base + threadIdx.x]);
-            __syncthreads();
-            for (int sub = 0; sub < cn; sub += 32) {
-                bool ov = false;
-                if (sub + lane < cn) {
-                    const int4 r = srec[sub + lane].r;
-                    ov = r.x < bx + 8 && r.z > bx && r.y < by + 4 && r.w > by;
-                }
-                unsigned mask = __ballot_sync(0xffffffffu, ov);
-                while (mask) {
-                    const int j = sub + __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    const SsRecord &R = srec[j];
-                    const int4 r = R.r;
-                    float v[NCH];
+        for (int cb = p0; cb < p1; cb += 32 * 8) {
+            if (__all_sync(0xffffffffu, stopped)) break;
+            const int ce = min(p1, cb + 32 * 8);
+            walk_tile(wp, cb, ce, P.pair_rec, P.pair_rect, P.records, wbuf, [&](const SsRecord &R, int, int rec) {
+                float v[NCH];
 #pragma unroll
-                    for (int c = 0; c < NCH; ++c) v[c] = 0.f;
-                    bool cov = false;
-                    if (live && !stopped && px >= r.x && px < r.z && py >= r.y && py < r.w) {
-                        bool go = true;
-                        if (group_n > 0 && R.d.z > zmax) {
-                            ++m_cur;
-                            group_n = 0;
-                            zmax = 0.f;
-                            if (m_cur >= P.k_max || m_cur >= m_end) {
-                                stopped = true;
-                                go = false;
-                            } else if (kCoef) {
-                                const float4 c = P.coef[(size_t)m_cur * HW + pix];
-                                A = c.x; G0 = c.y; G1 = c.z; G2 = c.w;
-                            } else {
-                                A = cA[m_cur]; G0 = cC0[m_cur]; G1 = cC1[m_cur]; G2 = cC2[m_cur];
-                                Bz = cB[m_cur]; Qv = cQ[m_cur]; Zb = cZb[m_cur]; Vr = cV[m_cur];
-                            }
-                        }
-                        if (go) {
-                            const float t1[3] = {R.a.x, R.a.y, R.a.z};
-                            const float t2[3] = {R.a.w, R.b.x, R.b.y};
-                            const float t4[3] = {R.b.z, R.b.w, R.c.x};
-                            SsHit h;
-                            if (ss_intersect(x, y, t1, t2, t4, h)) {
-                                const double rho2 = ss_rho2(R.c.y, R.c.z, R.c.w, h.u, h.v);
-                                if (rho2 < 9.0) {
-                                    cov = true;
-                                    ++group_n;
-                                    if (R.d.w > zmax) zmax = R.d.w;
-                                    const float e = __expf(-0.5f * (float)rho2);
-                                    const float w = R.d.x * e;
-                                    const float dz = R.d.y - Zb;
-                                    const float gw = A + G0 * R.e.x + G1 * R.e.y + G2 * R.e.z + Bz * dz + Qv * (dz * dz - Vr);
-                                    v[13] = w * G0; v[14] = w * G1; v[15] = w * G2;
-                                    v[16] = w * (Bz + 2.f * Qv * dz);
-                                    const float gr = -0.5f * w * gw;
-                                    v[12] = e * gw;
-                                    const float u = h.u, vv = h.v;
-                                    v[9] = gr * u * u; v[10] = gr * 2.f * u * vv; v[11] = gr * vv * vv;
-                                    const float gu = 2.f * gr * (R.c.y * u + R.c.z * vv);
-                                    const float gv = 2.f * gr * (R.c.z * u + R.c.w * vv);
-                                    const float inv_den = 1.f / h.den;
-                                    const float gp0 = gu * inv_den, gp1 = gv * inv_den, gp2 = -(gu * u + gv * vv) * inv_den;
-                                    const float gk0 = h.l1 * gp2 - h.l2 * gp1;
-                                    const float gk1 = h.l2 * gp0 - h.l0 * gp2;
-                                    const float gk2 = h.l0 * gp1 - h.l1 * gp0;
-                                    const float gl0 = gp1 * h.k2 - gp2 * h.k1;
-                                    const float gl1 = gp2 * h.k0 - gp0 * h.k2;
-                                    const float gl2 = gp0 * h.k1 - gp1 * h.k0;
-                                    v[0] = -gk0; v[1] = -gk1; v[2] = -gk2;
-                                    v[3] = -gl0; v[4] = -gl1; v[5] = -gl2;
-                                    v[6] = x * gk0 + y * gl0; v[7] = x * gk1 + y * gl1; v[8] = x * gk2 + y * gl2;
-                                    v[17] = fabsf(t4[2]) * sqrtf(gk2 * gk2 + gl2 * gl2);
-                                }
-                            }
+                for (int k = 0; k < NCH; ++k) v[k] = 0.f;
+                bool cov = false;
+                if (!stopped && in_rect(wp, R.r)) {
+                    bool go = true;
+                    if (group_n > 0 && R.d.z > zmax) {
+                        ++m_cur;
+                        group_n = 0;
+                        zmax = 0.f;
+                        if (m_cur >= P.k_max || m_cur >= m_end) {
+                            stopped = true;
+                            go = false;
+                        } else if (kCoef) {
+                            const float4 c = P.coef[(size_t)m_cur * HW + pix];
+                            A = c.x; G0 = c.y; G1 = c.z; G2 = c.w;
+                        } else {
+                            A = cA[m_cur]; G0 = cC0[m_cur]; G1 = cC1[m_cur]; G2 = cC2[m_cur];
+                            Bz = cB[m_cur]; Qv = cQ[m_cur]; Zb = cZb[m_cur]; Vr = cV[m_cur];
                         }
                     }
-                    const unsigned cm = __ballot_sync(0xffffffffu, cov);
-                    if (cm) {
-                        warp_tr_reduce<NCH>(v, lane);
-                        const int rec = P.pair_rec[base + j];
-                        float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
-                        if (owner) atomicAdd(dst + my_ch, v[0]);
-                        if (lane == 0) atomicAdd(reinterpret_cast<int *>(dst + 18), __popc(cm));
+                    Cover c;
+                    if (go && ss_cover(x, y, R, c)) {
+                        // backward.py:272-320 in the centred depth form
+                        cov = true;
+                        ++group_n;
+                        if (R.d.w > zmax) zmax = R.d.w;
+                        const float e = __expf(-0.5f * c.rho2);
+                        const float w = R.d.x * e;
+                        const float dz = R.d.y - Zb;
+                        const float gw = A + G0 * R.e.x + G1 * R.e.y + G2 * R.e.z + Bz * dz + Qv * (dz * dz - Vr);
+                        v[13] = w * G0; v[14] = w * G1; v[15] = w * G2;
+                        v[16] = w * (Bz + 2.f * Qv * dz);
+                        const float gr = -0.5f * w * gw;
+                        v[12] = e * gw;
+                        const float u = c.u, vv = c.v;
+                        v[9] = gr * u * u; v[10] = gr * 2.f * u * vv; v[11] = gr * vv * vv;
+                        const float gu = 2.f * gr * (R.c.y * u + R.c.z * vv);
+                        const float gv = 2.f * gr * (R.c.z * u + R.c.w * vv);
+                        const float gp0 = gu * c.inv_den, gp1 = gv * c.inv_den, gp2 = -(gu * u + gv * vv) * c.inv_den;
+                        const float gk0 = c.l1 * gp2 - c.l2 * gp1;
+                        const float gk1 = c.l2 * gp0 - c.l0 * gp2;
+                        const float gk2 = c.l0 * gp1 - c.l1 * gp0;
+                        const float gl0 = gp1 * c.k2 - gp2 * c.k1;
+                        const float gl1 = gp2 * c.k0 - gp0 * c.k2;
+                        const float gl2 = gp0 * c.k1 - gp1 * c.k0;
+                        v[0] = -gk0; v[1] = -gk1; v[2] = -gk2;
+                        v[3] = -gl0; v[4] = -gl1; v[5] = -gl2;
+                        v[6] = x * gk0 + y * gl0; v[7] = x * gk1 + y * gl1; v[8] = x * gk2 + y * gl2;
+                        v[17] = fabsf(R.c.x) * sqrtf(gk2 * gk2 + gl2 * gl2);
                     }
                 }
-            }
+                const unsigned cm = __ballot_sync(0xffffffffu, cov);
+                if (cm) {
+                    warp_tr_reduce<NCH>(v, lane);
+                    float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
+                    if (owner) atomicAdd(dst + my_ch, v[0]);
+                    if (lane == 0) atomicAdd(reinterpret_cast<int *>(dst + 18), __popc(cm));
+                }
+            });
         }
     }
 
@@ -313,7 +259,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
 }  // namespace
 
 extern "C" int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offsets,
-                                  const int32_t *pair_rec, const float *records, const float *background,
+                                  const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
                                   int k_max, const float *g_rgb, const float *g_alpha, float cons_scale,
                                   float *rec_acc, double *cons_loss, void *stream)
 {
@@ -324,31 +270,13 @@ extern "C" int ss_raster_backward(int width, int height, int tile, const int32_t
     P.bg0 = background[0]; P.bg1 = background[1]; P.bg2 = background[2];
     P.cons_scale = cons_scale;
     P.offsets = tile_offsets; P.pair_rec = pair_rec;
+    P.pair_rect = reinterpret_cast<const uint2 *>(pair_rect);
     P.records = reinterpret_cast<const SsRecord *>(records);
     P.g_rgb = g_rgb; P.g_alpha = g_alpha; P.acc = rec_acc; P.cons_loss = cons_loss;
     const int nty = (height + tile - 1) / tile;
     const int threads = tile * tile;
     P.coef = nullptr;
-    raster_bwd_kernel<false><<<P.ntx * nty, threads, threads * sizeof(SsRecord), (cudaStream_t)stream>>>(P);
-    SS_CUDA_CHECK_LAUNCH();
-    return SS_OK;
-}
-
-extern "C" int ss_train_backward(int width, int height, int tile, const int32_t *tile_offsets,
-                                 const int32_t *pair_rec, const float *records, int k_max, const float *coef,
-                                 float *rec_acc, void *stream)
-{
-    if (width <= 0 || height <= 0 || tile != 16 || k_max < 1 || k_max > SS_KMAX_CAP) return SS_ERR_INVALID;
-    if (!tile_offsets || !coef) return SS_ERR_INVALID;
-    BwdParams P{};
-    P.W = width; P.H = height; P.tile = tile; P.ntx = (width + tile - 1) / tile; P.k_max = k_max;
-    P.offsets = tile_offsets; P.pair_rec = pair_rec;
-    P.records = reinterpret_cast<const SsRecord *>(records);
-    P.acc = rec_acc;
-    P.coef = reinterpret_cast<const float4 *>(coef);
-    const int nty = (height + tile - 1) / tile;
-    const int threads = tile * tile;
-    raster_bwd_kernel<true><<<P.ntx * nty, threads, threads * sizeof(SsRecord), (cudaStream_t)stream>>>(P);
+    raster_bwd_kernel<false><<<P.ntx * nty, threads, 0, (cudaStream_t)stream>>>(P);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

@@ -22,6 +22,7 @@
 // (A, dL/dC_raw rgb) that the pass-2-only backward kernel consumes, so the
 // backward never replays the walk a second time.
 #include "ss_common.cuh"
+#include "raster_walk.cuh"
 
 namespace {
 
@@ -30,6 +31,7 @@ struct FwdParams {
     float bg0, bg1, bg2;
     const int32_t *offsets;
     const int32_t *pair_rec;
+    const uint2 *pair_rect;
     const SsRecord *records;
     float *rgb, *alpha, *depth;
     int32_t *nlayers;
@@ -40,39 +42,32 @@ struct FwdParams {
     const float *target;   // (H,W,3)
     float inv_count;       // 1 / (3 H W): mean over all image entries
     float4 *coef;          // (k_max, H*W) float4
+    float *thr;            // (k_max, H*W) depth at which each layer closed
+    int32_t *ncl;          // (H*W) number of closed layers
     double *loss;          // sum of |rgb - target| (1 double)
 };
-
-__device__ __forceinline__ void stage_record(SsRecord *dst, const SsRecord *__restrict__ src) {
-    const float4 *s = reinterpret_cast<const float4 *>(src);
-    float4 *d = reinterpret_cast<float4 *>(dst);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) d[k] = __ldg(s + k);
-}
 
 template <bool kExtras, bool kTrain>
 __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
 {
-    extern __shared__ SsRecord srec[];
+    __shared__ SsRecord wbuf_all[8][32];
     __shared__ double loss_red[32];
     const int t = blockIdx.x;
-    const int tx = t % P.ntx, ty = t / P.ntx;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int wpr = P.tile >> 3;  // warps per tile row (8 px wide each)
-    const int bx = tx * P.tile + (wid % wpr) * 8, by = ty * P.tile + (wid / wpr) * 4;
-    const int px = bx + (lane & 7), py = by + (lane >> 3);
-    const bool live = px < P.W && py < P.H;
-    const float x = ss_ndc_x(px, P.W), y = ss_ndc_y(py, P.H);
+    const WarpPix wp = warp_pixels(t, P.ntx, P.tile, P.W, P.H);
+    const int lane = wp.lane, wid = wp.wid;
+    const bool live = wp.live;
+    const size_t pix = wp.pix;
+    SsRecord *wbuf = wbuf_all[wid];
 
     float Wg = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Zg = 0.f, Z2g = 0.f, zmax = 0.f;
     float T = 1.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, dnum = 0.f, dden = 0.f;
     int layers = 0, members = 0;
-    bool stopped = false;
+    bool stopped = !live;
     unsigned discarded = 0;
-    const size_t pix = live ? (size_t)py * P.W + px : 0;
     // training: per-layer raw sums for the suffix recursion
     constexpr int KL = kTrain ? SS_KMAX_CAP : 1;
     float lw[KL], lc0[KL], lc1[KL], lc2[KL];
+    int ncl = 0;
 
     auto close_layer = [&]() {
         const float a_k = -expm1f(-Wg);
@@ -93,63 +88,42 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
     };
 
     const int p0 = P.offsets[t], p1 = P.offsets[t + 1];
-    const int nthreads = blockDim.x;
-    for (int base = p0; base < p1; base += nthreads) {
-        const int cn = min(nthreads, p1 - base);
-        __syncthreads();
-        if ((int)threadIdx.x < cn) stage_record(&srec[threadIdx.x], P.records + P.pair_rec[base + threadIdx.x]);
-        __syncthreads();
-        for (int sub = 0; sub < cn; sub += 32) {
-            // warp-level cull: which of these 32 records touch my 8x4 block?
-            bool ov = false;
-            if (sub + lane < cn) {
-                const int4 r = srec[sub + lane].r;
-                ov = r.x < bx + 8 && r.z > bx && r.y < by + 4 && r.w > by;
-            }
-            unsigned mask = __ballot_sync(0xffffffffu, ov);
-            while (mask) {
-                const int j = sub + __ffs(mask) - 1;
-                mask &= mask - 1;
-                const SsRecord &R = srec[j];
-                const int4 r = R.r;
-                const bool inr = live && px >= r.x && px < r.z && py >= r.y && py < r.w;
-                bool cov = false;
-                if (inr) {
-                    if (stopped) {
-                        ++discarded;
-                    } else {
-                        bool go = true;
-                        if (Wg > 0.f && R.d.z > zmax) {
-                            close_layer();  // rasterizer.py:168-196
-                            if (layers >= P.k_max) { stopped = true; ++discarded; go = false; }
-                        }
-                        if (go) {
-                            const float t1[3] = {R.a.x, R.a.y, R.a.z};
-                            const float t2[3] = {R.a.w, R.b.x, R.b.y};
-                            const float t4[3] = {R.b.z, R.b.w, R.c.x};
-                            SsHit h;
-                            if (ss_intersect(x, y, t1, t2, t4, h)) {
-                                const double rho2 = ss_rho2(R.c.y, R.c.z, R.c.w, h.u, h.v);
-                                if (rho2 < 9.0) {
-                                    cov = true;
-                                    const float w = R.d.x * __expf(-0.5f * (float)rho2);
-                                    const float z = R.d.y;
-                                    Wg += w;
-                                    C0 += w * R.e.x; C1 += w * R.e.y; C2 += w * R.e.z;
-                                    if (!kTrain) { Zg += w * z; Z2g += w * z * z; }
-                                    ++members;
-                                    if (R.d.w > zmax) zmax = R.d.w;
-                                }
-                            }
-                        }
+    // per 32-pair chunk early exit once every lane of the warp stopped
+    // (only when the discard statistic is not requested)
+    for (int cb = p0; cb < p1; cb += 32 * 8) {
+        if (!kExtras && __all_sync(0xffffffffu, stopped)) break;
+        const int ce = min(p1, cb + 32 * 8);
+        walk_tile(wp, cb, ce, P.pair_rec, P.pair_rect, P.records, wbuf, [&](const SsRecord &R, int pidx, int) {
+            bool cov = false;
+            if (in_rect(wp, R.r)) {
+                if (stopped) {
+                    ++discarded;
+                } else {
+                    bool go = true;
+                    if (Wg > 0.f && R.d.z > zmax) {
+                        if (kTrain) P.thr[(size_t)ncl * P.W * P.H + pix] = zmax;
+                        ++ncl;
+                        close_layer();  // rasterizer.py:168-196
+                        if (layers >= P.k_max) { stopped = true; ++discarded; go = false; }
+                    }
+                    Cover c;
+                    if (go && ss_cover(wp.x, wp.y, R, c)) {
+                        cov = true;
+                        const float w = R.d.x * __expf(-0.5f * c.rho2);
+                        const float z = R.d.y;
+                        Wg += w;
+                        C0 += w * R.e.x; C1 += w * R.e.y; C2 += w * R.e.z;
+                        if (!kTrain) { Zg += w * z; Z2g += w * z * z; }
+                        ++members;
+                        if (R.d.w > zmax) zmax = R.d.w;
                     }
                 }
-                if (kExtras && P.pair_cover) {
-                    const unsigned cm = __ballot_sync(0xffffffffu, cov);
-                    if (cm && lane == 0) atomicAdd(&P.pair_cover[base + j], __popc(cm));
-                }
             }
-        }
+            if (kExtras && P.pair_cover) {
+                const unsigned cm = __ballot_sync(0xffffffffu, cov);
+                if (cm && lane == 0) atomicAdd(&P.pair_cover[pidx], __popc(cm));
+            }
+        });
     }
     double lsum = 0.0;
     if (live) {
@@ -163,6 +137,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
             P.depth[pix] = dden > 0.f ? dnum / dden : 0.f;
             P.nlayers[pix] = layers;
         } else {
+            P.ncl[pix] = ncl;
             // L1 loss and its image gradient (losses.py:100-104)
             const float d0 = r0 - P.target[3 * pix], d1 = r1 - P.target[3 * pix + 1], d2 = r2 - P.target[3 * pix + 2];
             lsum = (double)fabsf(d0) + (double)fabsf(d1) + (double)fabsf(d2);
@@ -219,11 +194,12 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
 
 template <bool kExtras, bool kTrain>
 void launch(const FwdParams &P, int ntiles, int threads, cudaStream_t st) {
-    raster_fwd_kernel<kExtras, kTrain><<<ntiles, threads, threads * sizeof(SsRecord), st>>>(P);
+    raster_fwd_kernel<kExtras, kTrain><<<ntiles, threads, 0, st>>>(P);
 }
 
 bool fill_common(FwdParams &P, int width, int height, int tile, const int32_t *tile_offsets,
-                 const int32_t *pair_rec, const float *records, const float *background, int k_max) {
+                 const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
+                 int k_max) {
     if (width <= 0 || height <= 0 || tile < 8 || tile > 16 || (tile & 7) || k_max < 1 || k_max > SS_KMAX_CAP)
         return false;
     if (!tile_offsets || !background) return false;
@@ -231,6 +207,7 @@ bool fill_common(FwdParams &P, int width, int height, int tile, const int32_t *t
     P.W = width; P.H = height; P.tile = tile; P.ntx = (width + tile - 1) / tile; P.k_max = k_max;
     P.bg0 = background[0]; P.bg1 = background[1]; P.bg2 = background[2];
     P.offsets = tile_offsets; P.pair_rec = pair_rec;
+    P.pair_rect = reinterpret_cast<const uint2 *>(pair_rect);
     P.records = reinterpret_cast<const SsRecord *>(records);
     return true;
 }
@@ -238,13 +215,13 @@ bool fill_common(FwdParams &P, int width, int height, int tile, const int32_t *t
 }  // namespace
 
 extern "C" int ss_raster_forward(int width, int height, int tile, const int32_t *tile_offsets,
-                                 const int32_t *pair_rec, const float *records, const float *background,
+                                 const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
                                  int k_max, float *rgb, float *alpha, float *depth, int32_t *nlayers,
                                  int32_t *pair_cover, const SsStacks *stacks, unsigned long long *discarded,
                                  void *stream)
 {
     FwdParams P;
-    if (!fill_common(P, width, height, tile, tile_offsets, pair_rec, records, background, k_max)) return SS_ERR_INVALID;
+    if (!fill_common(P, width, height, tile, tile_offsets, pair_rec, pair_rect, records, background, k_max)) return SS_ERR_INVALID;
     if (!rgb || !alpha || !depth || !nlayers) return SS_ERR_INVALID;
     P.rgb = rgb; P.alpha = alpha; P.depth = depth; P.nlayers = nlayers;
     P.pair_cover = pair_cover;
@@ -259,20 +236,68 @@ extern "C" int ss_raster_forward(int width, int height, int tile, const int32_t 
 }
 
 extern "C" int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
-                                const int32_t *pair_rec, const float *records, const float *background,
-                                int k_max, const float *target, float *coef, double *loss_sum, float *rgb,
-                                void *stream)
+                                const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
+                                int k_max, const float *target, float *coef, float *thr, int32_t *ncl,
+                                double *loss_sum, float *rgb, void *stream)
 {
     FwdParams P;
-    if (!fill_common(P, width, height, tile, tile_offsets, pair_rec, records, background, k_max)) return SS_ERR_INVALID;
-    if (!target || !coef || !loss_sum) return SS_ERR_INVALID;
+    if (!fill_common(P, width, height, tile, tile_offsets, pair_rec, pair_rect, records, background, k_max)) return SS_ERR_INVALID;
+    if (!target || !coef || !thr || !ncl || !loss_sum) return SS_ERR_INVALID;
     P.target = target;
+    P.thr = thr;
+    P.ncl = ncl;
     P.inv_count = (float)(1.0 / (3.0 * (double)width * (double)height));
     P.coef = reinterpret_cast<float4 *>(coef);
     P.loss = loss_sum;
     P.rgb = rgb;
     const int ntiles = P.ntx * ((height + tile - 1) / tile);
     launch<false, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Diagnostic: every (pixel, in-rect record) of a view is tested with the fast
+// coverage path (ss_cover) and the exact reference evaluation; counts[0] =
+// evaluations, counts[1] = decisions that differ (must be 0), counts[2] =
+// evaluations that took the exact fallback.
+namespace {
+__global__ void __launch_bounds__(256) cover_check_kernel(int W, int H, int tile, int ntx, const int32_t *offsets,
+                                                          const int32_t *pair_rec, const uint2 *pair_rect,
+                                                          const SsRecord *recs, unsigned long long *counts)
+{
+    __shared__ SsRecord wbuf_all[8][32];
+    const int t = blockIdx.x;
+    const WarpPix wp = warp_pixels(t, ntx, tile, W, H);
+    unsigned long long n = 0, bad = 0, slow = 0;
+    walk_tile(wp, offsets[t], offsets[t + 1], pair_rec, pair_rect, recs, wbuf_all[wp.wid],
+              [&](const SsRecord &R, int, int) {
+                  if (!in_rect(wp, R.r)) return;
+                  ++n;
+                  Cover c;
+                  const bool fast = ss_cover(wp.x, wp.y, R, c);
+                  const float t1[3] = {R.a.x, R.a.y, R.a.z}, t2[3] = {R.a.w, R.b.x, R.b.y}, t4[3] = {R.b.z, R.b.w, R.c.x};
+                  SsHit h;
+                  const bool exact = ss_intersect(wp.x, wp.y, t1, t2, t4, h) && ss_rho2(R.c.y, R.c.z, R.c.w, h.u, h.v) < 9.0;
+                  bad += fast != exact;
+                  const float a = c.k0 * c.l1, b = c.k1 * c.l0;
+                  slow += !(fabsf(c.den) > 1e-5f * (fabsf(a) + fabsf(b)) + 1e-8f) || fabsf(c.rho2 - 9.f) < 0.09f;
+              });
+    atomicAdd(&counts[0], n);
+    atomicAdd(&counts[1], bad);
+    atomicAdd(&counts[2], slow);
+}
+}  // namespace
+
+extern "C" int ss_debug_cover_check(int width, int height, int tile, const int32_t *tile_offsets,
+                                    const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
+                                    unsigned long long *counts, void *stream)
+{
+    if (width <= 0 || height <= 0 || tile != 16 || !tile_offsets || !counts) return SS_ERR_INVALID;
+    const int ntx = (width + tile - 1) / tile, nty = (height + tile - 1) / tile;
+    cover_check_kernel<<<ntx * nty, 256, 0, (cudaStream_t)stream>>>(width, height, tile, ntx, tile_offsets, pair_rec,
+                                                                    reinterpret_cast<const uint2 *>(pair_rect),
+                                                                    reinterpret_cast<const SsRecord *>(records), counts);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

@@ -41,6 +41,7 @@ class ViewState:
     options: PreprocessOptions
     color_source: int
     aux: dict = field(default_factory=dict)
+    pair_rect: torch.Tensor | None = None  # (P, 2) int32 packed rects in pair order (after binning)
 
     @property
     def ntx(self):

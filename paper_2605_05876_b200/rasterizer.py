@@ -88,10 +88,12 @@ def bin_state(state: ViewState):
     cursors = torch.empty(state.ntiles, device=dev, dtype=torch.int32)
     keys = torch.empty(max(total, 1), device=dev, dtype=torch.int64)
     pair = torch.empty(max(total, 1), device=dev, dtype=torch.int32)
+    rects = torch.empty((max(total, 1), 2), device=dev, dtype=torch.int32)
     rc = lib.ss_bin_sort(len(state.cull), _lib.ptr(state.records), _lib.ptr(state.cull), state.width, state.height,
                          state.tile, _lib.ptr(state.tile_counts), _lib.ptr(offsets), _lib.ptr(cursors), _lib.ptr(keys),
-                         _lib.ptr(pair), total, _lib.ptr(state.flags), _lib.stream_ptr())
+                         _lib.ptr(pair), _lib.ptr(rects), total, _lib.ptr(state.flags), _lib.stream_ptr())
     _lib.check(rc, "ss_bin_sort")
+    state.pair_rect = rects
     return offsets, pair[:total]
 
 
@@ -154,7 +156,8 @@ def render(cloud, camera, options: RenderOptions | None = None, env=None, colors
                                                                    "depth_sq_sum", "member_count")))
     discarded = torch.zeros(1, device=dev, dtype=torch.int64)
     bgp, _keep = _lib.fvec(opt.background)
-    rc = lib.ss_raster_forward(W, H, int(opt.tile), _lib.ptr(offsets), _lib.ptr(pair_src), _lib.ptr(state.records),
+    rc = lib.ss_raster_forward(W, H, int(opt.tile), _lib.ptr(offsets), _lib.ptr(pair_src), _lib.ptr(state.pair_rect),
+                               _lib.ptr(state.records),
                                bgp, K, _lib.ptr(rgb), _lib.ptr(alpha), _lib.ptr(depth), _lib.ptr(nlayers),
                                _lib.ptr(pair_cover), ctypes.byref(st_struct) if st_struct is not None else None,
                                _lib.ptr(discarded), _lib.stream_ptr())

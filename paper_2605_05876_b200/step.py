@@ -59,6 +59,8 @@ class TrainStep:
         self.offsets = torch.empty(self.ntiles + 1, **i32)
         self.cursors = torch.empty(self.ntiles, **i32)
         self.coef = torch.empty((self.k_max, self.H * self.W, 4), **f32)
+        self.thr = torch.empty((self.k_max, self.H * self.W), **f32)
+        self.ncl = torch.empty(self.H * self.W, **i32)
         self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
         he, we = env.shape
         self.T = he * we
@@ -102,6 +104,7 @@ class TrainStep:
         dev = self.records.device
         self.keys = torch.empty(cap, device=dev, dtype=torch.int64)
         self.pair = torch.empty(cap, device=dev, dtype=torch.int32)
+        self.pair_rect = torch.empty((cap, 2), device=dev, dtype=torch.int32)
         self.capacity = cap
 
     def size_pairs(self, cameras, slack=1.5):
@@ -134,18 +137,21 @@ class TrainStep:
         camst = self._preprocess(cam)
         _lib.check(lib.ss_bin_sort(self.n, _lib.ptr(self.records), _lib.ptr(self.cull), self.W, self.H, self.tile,
                                    _lib.ptr(self.tile_counts), _lib.ptr(self.offsets), _lib.ptr(self.cursors),
-                                   _lib.ptr(self.keys), _lib.ptr(self.pair), self.capacity, _lib.ptr(self.flags), s),
+                                   _lib.ptr(self.keys), _lib.ptr(self.pair), _lib.ptr(self.pair_rect), self.capacity,
+                                   _lib.ptr(self.flags), s),
                    "ss_bin_sort")
         ev = self._ev_begin("train_forward")
         _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(self.offsets), _lib.ptr(self.pair),
-                                        _lib.ptr(self.records), self._bg[0], self.k_max, _lib.ptr(target),
-                                        _lib.ptr(self.coef), _lib.ptr(self.loss), None, s), "ss_train_forward")
+                                        _lib.ptr(self.pair_rect), _lib.ptr(self.records), self._bg[0], self.k_max,
+                                        _lib.ptr(target), _lib.ptr(self.coef), _lib.ptr(self.thr), _lib.ptr(self.ncl),
+                                        _lib.ptr(self.loss), None, s), "ss_train_forward")
         self._ev_end(ev)
         self.acc.zero_()
         ev = self._ev_begin("train_backward")
         _lib.check(lib.ss_train_backward(self.W, self.H, self.tile, _lib.ptr(self.offsets), _lib.ptr(self.pair),
-                                         _lib.ptr(self.records), self.k_max, _lib.ptr(self.coef),
-                                         _lib.ptr(self.acc), s), "ss_train_backward")
+                                         _lib.ptr(self.pair_rect), _lib.ptr(self.records), self.k_max, _lib.ptr(self.coef),
+                                         _lib.ptr(self.thr), _lib.ptr(self.ncl), _lib.ptr(self.acc), s),
+                   "ss_train_backward")
         self._ev_end(ev)
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                          _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(self.cull),

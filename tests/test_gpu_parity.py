@@ -154,3 +154,27 @@ def test_repeat_is_deterministic_forward():
     _, _, _, a = _render(d)
     _, _, _, b = _render(d)
     assert torch.equal(a.rgb, b.rgb) and torch.equal(a.pair_rec, b.pair_rec)
+
+
+def test_fast_coverage_path_is_exact_at_scale():
+    """The rasterisers' fast coverage test (FMA + approximate reciprocal with
+    an exact fallback near the cut-off) must take the same decision as the
+    reference arithmetic for every (pixel, in-rect record) of a config-2 view."""
+    import ctypes
+    from paper_2605_05876_b200 import _lib, scenes
+    from paper_2605_05876_b200.preprocess import run_preprocess
+    from paper_2605_05876_b200.rasterizer import bin_state
+    cloud = ss.SurfelCloud(**scenes.config2(0, 300_000))
+    env = ss.EnvironmentLight.from_base(scenes.env_lognormal(16, 32, 2))
+    lib = _lib.load()
+    for cam in ss.fibonacci_cameras(3, 3.5, 800, 800):
+        st = run_preprocess(cloud, cam, ss.PreprocessOptions(), _lib.SS_COLOR_IBL, env=env)
+        offsets, pair = bin_state(st)
+        counts = torch.zeros(3, device="cuda", dtype=torch.int64)
+        rc = lib.ss_debug_cover_check(800, 800, 16, _lib.ptr(offsets), _lib.ptr(pair), _lib.ptr(st.pair_rect),
+                                      _lib.ptr(st.records), _lib.ptr(counts), _lib.stream_ptr())
+        _lib.check(rc, "ss_debug_cover_check")
+        n, bad, slow = (int(v) for v in counts.cpu())
+        assert n > 1_000_000
+        assert bad == 0, f"{bad} coverage decisions differ from the reference arithmetic"
+        assert slow < 0.05 * n
