@@ -69,49 +69,25 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
     }
 }
 
-// Tile s of a record's span, row-major (rasterizer.py:84-89).
-__device__ __forceinline__ int span_tile(const int4 r, int tile, int ntx, int s) {
-    const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile;
-    const int sx = tx1 - tx0 + 1;
-    return (ty0 + s / sx) * ntx + tx0 + s % sx;
-}
-
-// Each record drops its key into every tile bucket of its rect.  Lanes walk
-// their spans in lock step so that lanes hitting the same tile (spatially
-// coherent record order) share one atomic: __match_any_sync groups them, the
-// leader reserves popc slots and every lane takes its rank inside the group.
+// Each record drops its key into every tile bucket of its rect; the slot
+// inside a bucket comes from the tile's cursor (order inside a bucket is
+// arbitrary: the per-tile sort that follows keys on (z_start, record)).
 __global__ void __launch_bounds__(256) scatter_kernel(
     int n, const SsRecord *__restrict__ records, const int8_t *__restrict__ cull, int ntx, int tile,
     const int32_t *__restrict__ offsets, int32_t *__restrict__ cursors, uint64_t *__restrict__ keys,
     int64_t capacity)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const bool alive = i < n && cull[i] == 0;
-    int4 r = make_int4(0, 0, 1, 1);
-    int cnt = 0;
-    uint64_t key = 0;
-    if (alive) {
-        r = records[i].r;
-        const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
-        cnt = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
-        key = ((uint64_t)orderable(records[i].d.z) << 32) | (uint32_t)i;
-    }
-    const int maxc = __reduce_max_sync(0xffffffffu, cnt);
-    const unsigned lt = (1u << lane) - 1u;
-    for (int s = 0; s < maxc; ++s) {
-        const bool act = s < cnt;
-        const int t = act ? span_tile(r, tile, ntx, s) : -1 - lane;  // unique dummies never match
-        const unsigned grp = __match_any_sync(0xffffffffu, t);
-        const int leader = __ffs(grp) - 1;
-        int base = 0;
-        if (act && lane == leader) base = atomicAdd(&cursors[t], __popc(grp));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (act) {
-            const int64_t at = (int64_t)offsets[t] + base + __popc(grp & lt);
+    if (i >= n || cull[i] != 0) return;
+    const int4 r = records[i].r;
+    const uint64_t key = ((uint64_t)orderable(records[i].d.z) << 32) | (uint32_t)i;
+    const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            const int t = ty * ntx + tx;
+            const int64_t at = (int64_t)offsets[t] + atomicAdd(&cursors[t], 1);
             if (at < capacity) keys[at] = key;
         }
-    }
 }
 
 // Ascending bitonic network on n elements padded (virtually) with +inf up to

@@ -5,10 +5,11 @@
 // build_diffuse_operator (:275-282, a DENSE T x T float64 matrix),
 // build_specular_operator (:285-331), brdf_lut (:118-156).  The reference
 // materialises T x T operators (51.5 GB at 128x256, 825 GB at 256x512); here
-// the diffuse operator is regenerated per (row, column) tile from separable
-// sin/cos tables in shared memory (an O(T^2) FP32 N-body pass, gather form in
-// both directions so no atomics), and the specular operator is regenerated
-// per output texel from the same Hammersley/GGX samples.
+// the diffuse operator is regenerated on the fly as an O(T^2) FP32 N-body
+// pass (column texels staged through shared memory, gather form in both
+// directions so no atomics, float64 chunk accumulation), and the specular
+// operator is regenerated per output texel from the same Hammersley/GGX
+// samples (refresh: gather; adjoint: scatter with float atomics).
 #include "ss_common.cuh"
 #include "shading.cuh"
 
@@ -51,68 +52,76 @@ __global__ void lut_kernel(int res, int samples, float *lut) {
     lut[2 * id + 1] = (float)(s2 / samples);
 }
 
-// Texel direction tables (latlong_texel_dirs, shading.py:162-169).
-struct DirTab {
-    float *st, *ct, *cp, *sp, *om;  // sin/cos theta per row, cos/sin phi per column, solid angle per row
-};
-
-__device__ __forceinline__ void load_tables(int he, int we, DirTab t) {
-    for (int r = threadIdx.x; r < he; r += blockDim.x) {
-        const double th = ((double)r + 0.5) * (SS_PI / he);
-        t.st[r] = (float)sin(th);
-        t.ct[r] = (float)cos(th);
-        t.om[r] = (float)(sin(th) * (SS_PI / he) * (2.0 * SS_PI / we));
-    }
-    for (int c = threadIdx.x; c < we; c += blockDim.x) {
-        const double ph = ((double)c + 0.5) * (2.0 * SS_PI / we) - SS_PI;
-        t.cp[c] = (float)cos(ph);
-        t.sp[c] = (float)sin(ph);
-    }
+// Texel direction and solid angle (latlong_texel_dirs, shading.py:162-169).
+__device__ __forceinline__ void texel(int b, int he, int we, float d[3], float &om) {
+    const int r = b / we, c = b % we;
+    const double th = ((double)r + 0.5) * (SS_PI / he);
+    const double ph = ((double)c + 0.5) * (2.0 * SS_PI / we) - SS_PI;
+    const double st = sin(th);
+    d[0] = (float)(st * cos(ph)); d[1] = (float)(st * sin(ph)); d[2] = (float)cos(th);
+    om = (float)(st * (SS_PI / he) * (2.0 * SS_PI / we));
 }
 
-// mode 0: rowsum_i = sum_j max(d_i.d_j,0) om_j
-// mode 1: out_i   = sum_j max(d_i.d_j,0) om_j x_j / rowsum_i        (refresh)
-// mode 2: out_j   = om_j sum_i max(d_i.d_j,0) x_i / rowsum_i        (adjoint)
+// The clamped-cosine quadrature as an on-the-fly T x T product (N-body form).
+// Column texels are staged CHUNK at a time in shared memory as (dir, value)
+// with the per-column factor folded into the value, so the inner loop is
+// 3 FFMA (dot) + max + 3 FFMA (accumulate):
+// mode 0: rowsum_a = sum_b max(d_a.d_b,0) om_b
+// mode 1: out_a    = sum_b max(d_a.d_b,0) om_b x_b / rowsum_a          (refresh)
+// mode 2: out_b   += om_b sum_a max(d_a.d_b,0) x_a / rowsum_a          (adjoint; roles swapped)
+constexpr int kChunk = 1024;
+
 template <int MODE>
 __global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const float *__restrict__ x,
                                                       const float *__restrict__ rowsum, float *__restrict__ out) {
-    extern __shared__ float sm[];
-    DirTab tab{sm, sm + he, sm + 2 * he, sm + 2 * he + we, sm + 2 * he + 2 * we};
-    load_tables(he, we, tab);
-    __syncthreads();
+    __shared__ float4 sd[kChunk];   // column direction (xyz, w unused)
+    __shared__ float4 sv[kChunk];   // column value rgb with its factor folded in (w unused)
     const int T = he * we;
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= T) return;
-    const int ar = a / we, ac = a % we;
-    const float sta = tab.st[ar], cta = tab.ct[ar], cpa = tab.cp[ac], spa = tab.sp[ac];
-    double tot0 = 0.0, tot1 = 0.0, tot2 = 0.0;
-    for (int r = 0; r < he; ++r) {
-        const float sr = tab.st[r] * sta, cr = tab.ct[r] * cta;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-        for (int c = 0; c < we; ++c) {
-            const float dot = sr * (cpa * tab.cp[c] + spa * tab.sp[c]) + cr;
-            if (dot <= 0.f) continue;
-            const int b = r * we + c;
+    float da[3] = {0.f, 0.f, 0.f}, oma = 0.f;
+    if (a < T) texel(a, he, we, da, oma);
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    for (int base = 0; base < T; base += kChunk) {
+        const int cn = min(kChunk, T - base);
+        __syncthreads();
+        for (int k = threadIdx.x; k < cn; k += blockDim.x) {
+            const int b = base + k;
+            float db[3], omb;
+            texel(b, he, we, db, omb);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (MODE == 0) {
-                s0 += dot;
+                v.x = omb;
             } else if (MODE == 1) {
-                s0 += dot * x[3 * b]; s1 += dot * x[3 * b + 1]; s2 += dot * x[3 * b + 2];
+                v = make_float4(omb * x[3 * b], omb * x[3 * b + 1], omb * x[3 * b + 2], 0.f);
             } else {
                 const float inv = 1.f / rowsum[b];
-                s0 += dot * x[3 * b] * inv; s1 += dot * x[3 * b + 1] * inv; s2 += dot * x[3 * b + 2] * inv;
+                v = make_float4(x[3 * b] * inv, x[3 * b + 1] * inv, x[3 * b + 2] * inv, 0.f);
             }
+            sd[k] = make_float4(db[0], db[1], db[2], 0.f);
+            sv[k] = v;
         }
-        const double om = MODE == 2 ? 1.0 : (double)tab.om[r];
-        tot0 += om * s0; tot1 += om * s1; tot2 += om * s2;
+        __syncthreads();
+#pragma unroll 4
+        for (int k = 0; k < cn; ++k) {
+            const float4 d = sd[k];
+            const float c = fmaxf(da[0] * d.x + da[1] * d.y + da[2] * d.z, 0.f);
+            const float4 v = sv[k];
+            s0 = fmaf(c, v.x, s0);
+            if (MODE != 0) { s1 = fmaf(c, v.y, s1); s2 = fmaf(c, v.z, s2); }
+        }
+        // flush the chunk partial into float64 (keeps the 32k-term sum accurate)
+        t0 += s0; t1 += s1; t2 += s2;
+        s0 = s1 = s2 = 0.f;
     }
+    if (a >= T) return;
     if (MODE == 0) {
-        out[a] = (float)tot0;
+        out[a] = (float)t0;
     } else if (MODE == 1) {
         const double inv = 1.0 / (double)rowsum[a];
-        out[3 * a] = (float)(tot0 * inv); out[3 * a + 1] = (float)(tot1 * inv); out[3 * a + 2] = (float)(tot2 * inv);
+        out[3 * a] = (float)(t0 * inv); out[3 * a + 1] = (float)(t1 * inv); out[3 * a + 2] = (float)(t2 * inv);
     } else {
-        const double om = tab.om[ar];
-        out[3 * a] += (float)(tot0 * om); out[3 * a + 1] += (float)(tot1 * om); out[3 * a + 2] += (float)(tot2 * om);
+        out[3 * a] += (float)(t0 * oma); out[3 * a + 1] += (float)(t1 * oma); out[3 * a + 2] += (float)(t2 * oma);
     }
 }
 
@@ -240,7 +249,6 @@ __global__ void adjoint_finish_kernel(int n, const float *__restrict__ g0, const
     d_log[k] = db * base[k];
 }
 
-size_t tab_bytes(int he, int we) { return (size_t)(3 * he + 2 * we) * sizeof(float); }
 
 }  // namespace
 
@@ -254,7 +262,7 @@ extern "C" int ss_brdf_lut(int res, int samples, float *lut, void *stream) {
 extern "C" int ss_env_rowsums(int he, int we, float *rowsum, void *stream) {
     if (he < 2 || we < 2 || !rowsum) return SS_ERR_INVALID;
     const int T = he * we;
-    diffuse_kernel<0><<<(T + 255) / 256, 256, tab_bytes(he, we), (cudaStream_t)stream>>>(he, we, nullptr, nullptr, rowsum);
+    diffuse_kernel<0><<<(T + 255) / 256, 256, 0, (cudaStream_t)stream>>>(he, we, nullptr, nullptr, rowsum);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
@@ -266,7 +274,7 @@ extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const flo
     const int T = he * we;
     exp_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular);
     SS_CUDA_CHECK_LAUNCH();
-    diffuse_kernel<1><<<(T + 255) / 256, 256, tab_bytes(he, we), st>>>(he, we, base, rowsum, diffuse);
+    diffuse_kernel<1><<<(T + 255) / 256, 256, 0, st>>>(he, we, base, rowsum, diffuse);
     SS_CUDA_CHECK_LAUNCH();
     if (levels > 1) {
         spec_refresh_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, base, specular);
@@ -283,7 +291,7 @@ extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const flo
     cudaStream_t st = (cudaStream_t)stream;
     const int T = he * we;
     cudaMemsetAsync(d_base, 0, sizeof(float) * 3 * T, st);
-    diffuse_kernel<2><<<(T + 255) / 256, 256, tab_bytes(he, we), st>>>(he, we, d_diffuse, rowsum, d_base);
+    diffuse_kernel<2><<<(T + 255) / 256, 256, 0, st>>>(he, we, d_diffuse, rowsum, d_base);
     SS_CUDA_CHECK_LAUNCH();
     if (levels > 1) {
         spec_adjoint_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, d_specular, d_base);

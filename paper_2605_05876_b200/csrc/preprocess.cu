@@ -186,19 +186,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     } else {
         rec.r = make_int4(0, 0, 0, 0);
     }
-    // per-tile histogram; lanes in lock step share atomics for equal tiles
-    {
-        __syncwarp();
-        const unsigned full = 0xffffffffu;
-        const int lane = threadIdx.x & 31;
-        const int maxc = __reduce_max_sync(full, count);
-        for (int s = 0; s < maxc; ++s) {
-            const bool act = s < count;
-            const int t = act ? (ty0 + s / sx) * ntx + tx0 + s % sx : -1 - lane;
-            const unsigned grp = __match_any_sync(full, t);
-            if (act && lane == __ffs(grp) - 1) atomicAdd(&tile_counts[t], __popc(grp));
-        }
-    }
+    // per-tile histogram (one global atomic per (record, tile); records in
+    // source order spread over the image, so the counters see little contention)
+    for (int s = 0; s < count; ++s) atomicAdd(&tile_counts[(ty0 + s / sx) * ntx + tx0 + s % sx], 1);
     if (!in_range) return;
     records[i] = rec;
     cull_out[i] = (int8_t)code;

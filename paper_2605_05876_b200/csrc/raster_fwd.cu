@@ -4,16 +4,16 @@
 // per-pixel semantics rasterize_pixel/composite_layers (reference.py:133-182).
 //
 // B200 mapping: one CTA per screen tile (tile*tile threads, one pixel each);
-// warps own 8x4 pixel blocks.  The tile's sorted record list is streamed
-// through shared memory in CTA-sized chunks (one 96 B record gathered per
-// thread with 16-byte loads); each warp then culls 32 staged records at a
-// time against its 8x4 block with one ballot and walks only the overlapping
-// ones, in list order, all 32 lanes on the same record (shared-memory
-// broadcast).  The ray/plane intersection reproduces the reference's float32
-// arithmetic exactly (ss_intersect) and the cut-off test rho^2 >= 9 is
-// evaluated with numba's float64 promotion (ss_rho2), so coverage and layer
-// membership decisions are identical to the reference; the accumulation is
-// float32 (outputs are float32 in the reference as well).
+// warps own 8x4 pixel blocks and walk the tile's sorted pair list
+// independently (raster_walk.cuh: 32 packed rects per ballot, only the
+// overlapping records are gathered into the warp's shared-memory slots, no
+// CTA barrier), all 32 lanes on the same record in list order.  Coverage uses
+// a float32/FMA fast path whose decision is re-taken with the reference's
+// exact arithmetic (float32 intersection without contraction, numba's
+// float64 rho^2) whenever it is within 1% of the cut-off, so coverage and
+// layer membership are identical to the reference (verified at scale by
+// ss_debug_cover_check); accumulation is float32 (the reference's outputs are
+// float32 too).
 //
 // kTrain: the training-step variant fuses the L1 photometric loss
 // (losses.py:94-108, lambda_ssim = 0) and the per-pixel suffix recursion of
