@@ -160,6 +160,15 @@ int ss_train_forward(int width, int height, int tile, const int32_t *tile_offset
 int ss_train_backward(int width, int height, int tile, const int32_t *tile_offsets,
                       const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, int k_max,
                       const float *coef, const float *thr, const int32_t *ncl, float *rec_acc, void *stream);
+/* ss_train_backward_records: the same pass 2 with one warp per record (its
+ * whole rect), no tile lists needed; the rec_acc row of every kept record is
+ * OVERWRITTEN (committed once, no atomics, no memset needed; culled rows are
+ * left untouched -- ss_chain_backward skips them).
+ * pixel_ndc: scratch of width + height + 1 + n 32-bit words (pixel NDC
+ * tables, then the queue of records with very large rects). */
+int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
+                              int k_max, const float *coef, const float *thr, const int32_t *ncl,
+                              float *pixel_ndc, float *rec_acc, void *stream);
 
 /* ---- chain backward -------------------------------------------------------
  * Replaces the per-surfel tail of backward_image() (backward.py:398-461,

@@ -61,6 +61,7 @@ class TrainStep:
         self.coef = torch.empty((self.k_max, self.H * self.W, 4), **f32)
         self.thr = torch.empty((self.k_max, self.H * self.W), **f32)
         self.ncl = torch.empty(self.H * self.W, **i32)
+        self.pixel_ndc = torch.empty(self.W + self.H + 1 + n, **f32)  # NDC tables + big-rect queue
         self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
         he, we = env.shape
         self.T = he * we
@@ -95,7 +96,7 @@ class TrainStep:
         self._pairs, self._kept, self._nviews = [], [], 0
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
         self._stage = None
-        self.launches_per_view = 7     # preprocess, scan, scatter, tile sort, train fwd, train bwd, chain
+        self.launches_per_view = 9     # preprocess, scan, scatter, tile sort, train fwd, ndc + record bwd x2, chain
         self.launches_per_step_fixed = 3 + 7 + 1 + 3  # env adjoint, Adam x7, quat renorm, env refresh
 
     # -- buffers -----------------------------------------------------------
@@ -146,12 +147,11 @@ class TrainStep:
                                         _lib.ptr(target), _lib.ptr(self.coef), _lib.ptr(self.thr), _lib.ptr(self.ncl),
                                         _lib.ptr(self.loss), None, s), "ss_train_forward")
         self._ev_end(ev)
-        self.acc.zero_()
         ev = self._ev_begin("train_backward")
-        _lib.check(lib.ss_train_backward(self.W, self.H, self.tile, _lib.ptr(self.offsets), _lib.ptr(self.pair),
-                                         _lib.ptr(self.pair_rect), _lib.ptr(self.records), self.k_max, _lib.ptr(self.coef),
-                                         _lib.ptr(self.thr), _lib.ptr(self.ncl), _lib.ptr(self.acc), s),
-                   "ss_train_backward")
+        _lib.check(lib.ss_train_backward_records(self.n, _lib.ptr(self.cull), _lib.ptr(self.records), self.W,
+                                                 self.H, self.k_max, _lib.ptr(self.coef), _lib.ptr(self.thr),
+                                                 _lib.ptr(self.ncl), _lib.ptr(self.pixel_ndc), _lib.ptr(self.acc), s),
+                   "ss_train_backward_records")
         self._ev_end(ev)
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                          _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(self.cull),
