@@ -34,6 +34,42 @@ PARAMS = ("centers", "quats", "log_scales", "albedo_raw", "metallic_raw", "rough
 _WIDTH = {"centers": 3, "quats": 4, "log_scales": 2, "albedo_raw": 3, "metallic_raw": 1, "roughness_raw": 1}
 
 
+def shard_views(n_views, world, rank):
+    """Contiguous block of the step's views owned by `rank` (views split evenly;
+    the first n_views % world ranks take one extra)."""
+    base, extra = divmod(n_views, world)
+    start = rank * base + min(rank, extra)
+    return list(range(start, start + base + (1 if rank < extra else 0)))
+
+
+class GradPack:
+    """One flat float32 buffer holding every gradient the step all-reduces:
+    the 14 parameter channels per surfel, ss_grad, the env log-radiance
+    gradient and the loss -- a single NCCL call per step."""
+
+    def __init__(self, n, env_texels, device, dtype=torch.float32):
+        sizes = [n * _WIDTH[k] for k in PARAMS] + [n, 3 * env_texels, 1]
+        self.flat = torch.zeros(sum(sizes), device=device, dtype=dtype)
+        views, off = [], 0
+        for s in sizes:
+            views.append(self.flat[off:off + s])
+            off += s
+        self.grads = {k: views[i].view(n, _WIDTH[k]) if _WIDTH[k] > 1 else views[i] for i, k in enumerate(PARAMS)}
+        self.grads["ss_grad"] = views[len(PARAMS)]
+        self.env = views[len(PARAMS) + 1]
+        self.loss = views[len(PARAMS) + 2]
+        self.touched = torch.zeros(n, device=device, dtype=torch.int32)
+
+    def zero(self):
+        self.flat.zero_()
+        self.touched.zero_()
+
+    def all_reduce(self, group=None):
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(self.flat, group=group)
+            dist.all_reduce(self.touched, group=group)
+
+
 class TrainStep:
     def __init__(self, cloud, env, width, height, k_max=16, tile=16, background=(0.0, 0.0, 0.0),
                  lrs=None, pair_capacity=None, process_group=None, options=None):
@@ -66,17 +102,12 @@ class TrainStep:
         he, we = env.shape
         self.T = he * we
         # packed gradient buffer: params, ss_grad, env d_base_log, loss -- one all-reduce
-        sizes = [n * _WIDTH[k] for k in PARAMS] + [n, 3 * self.T, 1]
-        self.flat = torch.zeros(sum(sizes), **f32)
-        views, off = [], 0
-        for s in sizes:
-            views.append(self.flat[off:off + s])
-            off += s
-        self.grads = {k: views[i].view(n, _WIDTH[k]) if _WIDTH[k] > 1 else views[i] for i, k in enumerate(PARAMS)}
-        self.grads["ss_grad"] = views[len(PARAMS)]
-        self.g_env_log = views[len(PARAMS) + 1].view(he, we, 3)
-        self.loss_f = views[len(PARAMS) + 2]
-        self.touched = torch.zeros(n, **i32)
+        self.pack = GradPack(n, self.T, dev)
+        self.flat = self.pack.flat
+        self.grads = self.pack.grads
+        self.g_env_log = self.pack.env.view(he, we, 3)
+        self.loss_f = self.pack.loss
+        self.touched = self.pack.touched
         self.loss = torch.zeros(1, device=dev, dtype=torch.float64)
         self.d_diffuse = torch.zeros_like(env.base)
         self.d_spec = torch.zeros_like(env.specular)
@@ -208,9 +239,7 @@ class TrainStep:
                                            _lib.ptr(self.d_spec), _lib.ptr(self.d_base), _lib.ptr(self.g_env_log),
                                            _lib.stream_ptr()), "ss_env_adjoint")
         self.loss_f.copy_(self.loss)
-        if self.pg is not None or (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
-            dist.all_reduce(self.flat, group=self.pg)
-            dist.all_reduce(self.touched, group=self.pg)
+        self.pack.all_reduce(self.pg)
 
     def apply(self, lr_scale=1.0):
         """Adam on all tensors, quaternion renorm, env refresh (train.py:241-248)."""

@@ -1,0 +1,94 @@
+"""Adam and the refinement scan on the device vs the reference golden
+fixtures (tests/golden/optim_refine.npz) and the oracle (needs a B200)."""
+
+import numpy as np
+import pytest
+import torch
+
+from golden_io import cloud_of, load
+from parity import host
+
+pytestmark = pytest.mark.gpu
+
+import paper_2605_05876_b200 as ss  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def test_adam_trace_matches_reference():
+    d = load("optim_refine")
+    p = torch.tensor(d["adam_p0"], device="cuda")
+    opt = ss.Adam()
+    for k in range(3):
+        opt.step("x", p, torch.tensor(d["adam_grads"][k], device="cuda", dtype=torch.float32), 0.01)
+        np.testing.assert_allclose(host(p), d["adam_traj"][k], rtol=2e-6, atol=2e-7)
+
+
+def test_adam_remap_semantics():
+    opt = ss.Adam()
+    p = torch.zeros(4, 2, device="cuda")
+    opt.step("x", p, torch.ones(4, 2, device="cuda"), 0.1)
+    opt.remap("x", np.array([2, -1, 0]))
+    assert opt.m["x"].shape == (3, 2)
+    assert float(opt.m["x"][1].abs().sum()) == 0.0
+    assert float(opt.m["x"][0, 0]) == pytest.approx(0.1)
+
+
+def test_refine_topology_matches_reference():
+    d = load("optim_refine")
+    cloud = ss.SurfelCloud.from_host(cloud_of(d))
+    stats = ss.DensifyStats(torch.tensor(d["grad_sum"], device="cuda"),
+                            torch.tensor(d["view_count"], device="cuda", dtype=torch.int64))
+    new, index_map, reasons = ss.refine_topology(cloud, stats, d["mean_dist"], int(d["max_surfels"]), quantile=0.9)
+    np.testing.assert_array_equal(host(index_map), d["index_map"])
+    assert [reasons[k] for k in ("stale", "isolated", "floater", "split")] == list(d["reasons"])
+    for k in ("quats", "albedo_raw", "metallic_raw", "roughness_raw"):
+        np.testing.assert_array_equal(host(getattr(new, k)), d[f"new_{k}"])
+    np.testing.assert_allclose(host(new.centers), d["new_centers"], rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(host(new.log_scales), d["new_log_scales"], rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("n", [2, 3000])
+def test_isolation_matches_brute_force(n):
+    rng = np.random.default_rng(n)
+    c = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    c[1] = c[0]  # an exact duplicate is a neighbour at distance 0
+    ls = np.log(rng.uniform(0.005, 0.05, (n, 2))).astype(np.float32)
+    cloud = ss.SurfelCloud(c, np.tile([1.0, 0, 0, 0], (n, 1)), ls, np.zeros((n, 3)), np.zeros(n), np.zeros(n))
+    got = host(ss.densify.isolated_mask(cloud))
+    d2 = np.sum((c[:, None, :].astype(np.float64) - c[None, :, :]) ** 2, axis=2)
+    np.fill_diagonal(d2, np.inf)
+    want = np.sqrt(d2.min(axis=1)) > 3.0 * np.exp(ls.astype(np.float64)).max(axis=1)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_split_children_match_oracle():
+    d = load("optim_refine")
+    cl = cloud_of(d)
+    cloud = ss.SurfelCloud.from_host(cl)
+    mask = np.zeros(len(cl.centers), bool)
+    mask[[3, 10, 77, 150]] = True
+    new, index_map = ss.split_cloud(cloud, mask)
+    cp, cm, cls = O.split_children(cl.centers, cl.quats, cl.log_scales, np.flatnonzero(mask))
+    nk = len(cl.centers) - 4
+    np.testing.assert_allclose(host(new.centers)[nk:nk + 4], cp, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(host(new.centers)[nk + 4:], cm, rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(host(new.log_scales)[nk:nk + 4], cls, rtol=1e-6, atol=1e-6)
+    assert (host(index_map)[nk:] == -1).all()
+
+
+def test_train_step_stats_feed_refinement():
+    """ss_grad / touched from a training step accumulate into DensifyStats."""
+    from paper_2605_05876_b200 import scenes
+    gt = scenes.config0(3, 2000)
+    cams = ss.fibonacci_cameras(2, 3.0, 64, 64, fov_y_deg=40.0)
+    env = ss.EnvironmentLight.from_base(scenes.env_lognormal(8, 16, 1))
+    targets = [ss.render(ss.SurfelCloud(**gt), c, ss.RenderOptions(), env=env).rgb.contiguous() for c in cams]
+    cloud = ss.SurfelCloud(**scenes.perturb(gt, 4))
+    ts = ss.TrainStep(cloud, env, 64, 64)
+    ts.gradients(cams, targets)
+    stats = ss.DensifyStats.zeros(len(cloud))
+    stats.accumulate(ts.grads["ss_grad"], ts.touched)
+    assert int(stats.view_count.max()) == 1
+    assert float(stats.grad_sum.sum()) > 0
+    new, imap, reasons = ss.refine_topology(cloud, stats, np.full(len(cloud), 0.001), 2300, quantile=0.95)
+    assert len(new) <= 2300 and reasons["split"] > 0
