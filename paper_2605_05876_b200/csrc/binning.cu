@@ -69,25 +69,54 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
     }
 }
 
-// Each record drops its key into every tile bucket of its rect; the slot
-// inside a bucket comes from the tile's cursor (order inside a bucket is
-// arbitrary: the per-tile sort that follows keys on (z_start, record)).
-__global__ void __launch_bounds__(256) scatter_kernel(
-    int n, const SsRecord *__restrict__ records, const int8_t *__restrict__ cull, int ntx, int tile,
+// Each record drops its key into every tile bucket of its rect.  Atomics on
+// the tile cursors are privatised per CTA: a CTA of 4096 records counts its
+// pairs per tile in shared memory, reserves one contiguous block per touched
+// tile with a single global atomic, then hands out slots with shared-memory
+// atomics.  Global same-address traffic drops from one atomic per pair to one
+// per (CTA, tile).  Slot order inside a bucket is arbitrary: the per-tile sort
+// that follows keys on (z_start, record), so the result is deterministic.
+constexpr int kScatterThreads = 1024;
+constexpr int kScatterPerThread = 4;
+
+__global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
+    int n, const SsRecord *__restrict__ records, const int8_t *__restrict__ cull, int ntx, int ntiles, int tile,
     const int32_t *__restrict__ offsets, int32_t *__restrict__ cursors, uint64_t *__restrict__ keys,
     int64_t capacity)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || cull[i] != 0) return;
-    const int4 r = records[i].r;
-    const uint64_t key = ((uint64_t)orderable(records[i].d.z) << 32) | (uint32_t)i;
-    const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
-            const int t = ty * ntx + tx;
-            const int64_t at = (int64_t)offsets[t] + atomicAdd(&cursors[t], 1);
-            if (at < capacity) keys[at] = key;
-        }
+    extern __shared__ int32_t s_cnt[];   // ntiles counters, then ntiles block bases
+    int32_t *s_base = s_cnt + ntiles;
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_cnt[t] = 0;
+    __syncthreads();
+    const int first = blockIdx.x * kScatterThreads * kScatterPerThread;
+    for (int k = 0; k < kScatterPerThread; ++k) {
+        const int i = first + k * kScatterThreads + threadIdx.x;
+        if (i >= n || cull[i] != 0) continue;
+        const int4 r = records[i].r;
+        const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&s_cnt[ty * ntx + tx], 1);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+        const int c = s_cnt[t];
+        if (c > 0) s_base[t] = atomicAdd(&cursors[t], c);
+        s_cnt[t] = 0;
+    }
+    __syncthreads();
+    for (int k = 0; k < kScatterPerThread; ++k) {
+        const int i = first + k * kScatterThreads + threadIdx.x;
+        if (i >= n || cull[i] != 0) continue;
+        const int4 r = records[i].r;
+        const uint64_t key = ((uint64_t)orderable(records[i].d.z) << 32) | (uint32_t)i;
+        const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
+        for (int ty = ty0; ty <= ty1; ++ty)
+            for (int tx = tx0; tx <= tx1; ++tx) {
+                const int t = ty * ntx + tx;
+                const int64_t at = (int64_t)offsets[t] + s_base[t] + atomicAdd(&s_cnt[t], 1);
+                if (at < capacity) keys[at] = key;
+            }
+    }
 }
 
 // Ascending bitonic network on n elements padded (virtually) with +inf up to
@@ -182,8 +211,13 @@ extern "C" int ss_bin_sort(int n, const float *records, const int8_t *cull, int 
     tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tile_counts, ntiles, tile_offsets, cursors, pair_capacity, flags);
     SS_CUDA_CHECK_LAUNCH();
     if (n > 0) {
-        scatter_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, reinterpret_cast<const SsRecord *>(records), cull,
-                                                        ntx, tile, tile_offsets, cursors, keys, pair_capacity);
+        const size_t smem = 2 * (size_t)ntiles * sizeof(int32_t);
+        if (smem > 220 * 1024) return SS_ERR_INVALID;  // > 28k tiles: not supported by the privatised scatter
+        cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int per_cta = kScatterThreads * kScatterPerThread;
+        scatter_kernel<<<(n + per_cta - 1) / per_cta, kScatterThreads, smem, st>>>(
+            n, reinterpret_cast<const SsRecord *>(records), cull, ntx, ntiles, tile, tile_offsets, cursors, keys,
+            pair_capacity);
         SS_CUDA_CHECK_LAUNCH();
     }
     tile_sort_kernel<<<ntiles, kSortThreads, kSortCap * sizeof(uint64_t), st>>>(

@@ -97,8 +97,9 @@ constexpr int kBigArea = 512;  // rects above this go to the CTA-per-record kern
 // rect row-major, so every record is reduced and committed exactly once.
 // Records with huge rects (grazing or near-camera splats) would serialise a
 // warp: they are zeroed here and queued for big_bwd_kernel.
-__global__ void __launch_bounds__(256, 2) splat_bwd_kernel(SplatParams P, int32_t *big_list, int32_t *big_count)
+__global__ void __launch_bounds__(256, 3) splat_bwd_kernel(SplatParams P, int32_t *big_list, int32_t *big_count)
 {
+    __shared__ SsRecord s_rec[8];  // the warp's current record (broadcast reads, frees 24 registers)
     const int lane = threadIdx.x & 31;
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -106,10 +107,12 @@ __global__ void __launch_bounds__(256, 2) splat_bwd_kernel(SplatParams P, int32_
     const unsigned same = __match_any_sync(0xffffffffu, my_ch);
     const bool owner = (__ffs(same) - 1) == lane;
 
+    SsRecord &R = s_rec[threadIdx.x >> 5];
     for (int rec = gwarp; rec < P.n; rec += nwarps) {
         if (P.cull[rec] != 0) continue;  // warp-uniform
-        SsRecord R;
-        load_record(P.records, rec, R);
+        __syncwarp();
+        if (lane < 6) reinterpret_cast<float4 *>(&R)[lane] = __ldg(reinterpret_cast<const float4 *>(P.records + rec) + lane);
+        __syncwarp();
         const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
         float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
         if (area > kBigArea) {
