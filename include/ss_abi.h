@@ -178,13 +178,14 @@ int ss_train_backward_records(int n, const int8_t *cull, const float *records, i
  * g_log_scales (n,2), g_albedo_raw (n,3), g_metallic_raw, g_roughness_raw,
  * g_colors (n,3, nullable), ss_grad (n), touched (n int32 counts).  With
  * SS_COLOR_IBL it also scatters the derived-map gradients into d_diffuse
- * (He,We,3) and d_specular (L,He,We,3) (float, accumulated). */
+ * (He,We,3) and d_specular (L,He,We,3) (float64, accumulated with fp64
+ * atomics: a step sums 64 views x N surfels x 36 scatters into them). */
 typedef struct SsGrads {
     float *centers, *quats, *log_scales, *albedo_raw, *metallic_raw, *roughness_raw;
     float *colors;     /* nullable */
     float *ss_grad;
     int32_t *touched;
-    float *d_diffuse, *d_specular;   /* nullable unless SS_COLOR_IBL */
+    double *d_diffuse, *d_specular;  /* nullable unless SS_COLOR_IBL */
 } SsGrads;
 int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                       int color_source, const SsEnv *env, const int8_t *cull,
@@ -202,8 +203,8 @@ int ss_env_rowsums(int he, int we, float *rowsum, void *stream);
 int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log,
                    const float *rowsum, float *base, float *diffuse, float *specular, void *stream);
 int ss_env_adjoint(int he, int we, int levels, int samples, const float *base,
-                   const float *rowsum, const float *d_diffuse, const float *d_specular,
-                   float *d_base, float *d_base_log, void *stream);
+                   const float *rowsum, const double *d_diffuse, const double *d_specular,
+                   double *d_base, float *d_base_log, void *stream);
 
 /* ---- optimiser ------------------------------------------------------------
  * Adam.step (adam.py:21-41) fused over one parameter tensor of `count`

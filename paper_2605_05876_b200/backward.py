@@ -78,8 +78,8 @@ def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0) -> B
     ibl = result.color_source == "ibl"
     d_diff = d_spec = None
     if ibl:
-        d_diff = torch.zeros_like(env.base)
-        d_spec = torch.zeros_like(env.specular)
+        d_diff = torch.zeros(env.base.shape, device=dev, dtype=torch.float64)
+        d_spec = torch.zeros(env.specular.shape, device=dev, dtype=torch.float64)
     source = {"explicit": _lib.SS_COLOR_EXPLICIT, "ibl": _lib.SS_COLOR_IBL, "albedo": _lib.SS_COLOR_ALBEDO}[result.color_source]
     cl = _lib.make_cloud(cloud)
     camst = _lib.make_camera(cam)

@@ -194,11 +194,11 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
         const double scw[4] = {(1 - bs.tu) * (1 - bs.tv), bs.tu * (1 - bs.tv), (1 - bs.tu) * bs.tv, bs.tu * bs.tv};
         for (int h = 0; h < 2; ++h) {
             if (wts[h] == 0.0) continue;
-            float *dst = P.g.d_specular + lstride * lvs[h];
+            double *dst = P.g.d_specular + lstride * lvs[h];
             for (int k = 0; k < 4; ++k)
                 for (int c = 0; c < 3; ++c) {
-                    const float val = (float)(sg.g_ls[c] * wts[h] * scw[k]);
-                    if (val != 0.f) atomicAdd(dst + 3 * sidx[k] + c, val);
+                    const double val = sg.g_ls[c] * wts[h] * scw[k];
+                    if (val != 0.0) atomicAdd(dst + 3 * sidx[k] + c, val);
                 }
         }
         const SsBil &bd = st.bd;
@@ -206,8 +206,8 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
         const double dcw[4] = {(1 - bd.tu) * (1 - bd.tv), bd.tu * (1 - bd.tv), (1 - bd.tu) * bd.tv, bd.tu * bd.tv};
         for (int k = 0; k < 4; ++k)
             for (int c = 0; c < 3; ++c) {
-                const float val = (float)(sg.g_ld[c] * dcw[k]);
-                if (val != 0.f) atomicAdd(P.g.d_diffuse + 3 * didx[k] + c, val);
+                const double val = sg.g_ld[c] * dcw[k];
+                if (val != 0.0) atomicAdd(P.g.d_diffuse + 3 * didx[k] + c, val);
             }
     } else if (P.color_source == SS_COLOR_ALBEDO) {
         for (int c = 0; c < 3; ++c) {

@@ -71,9 +71,9 @@ __device__ __forceinline__ void texel(int b, int he, int we, float d[3], float &
 // mode 2: out_b   += om_b sum_a max(d_a.d_b,0) x_a / rowsum_a          (adjoint; roles swapped)
 constexpr int kChunk = 1024;
 
-template <int MODE>
-__global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const float *__restrict__ x,
-                                                      const float *__restrict__ rowsum, float *__restrict__ out) {
+template <int MODE, typename TIn, typename TOut>
+__global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const TIn *__restrict__ x,
+                                                      const float *__restrict__ rowsum, TOut *__restrict__ out) {
     __shared__ float4 sd[kChunk];   // column direction (xyz, w unused)
     __shared__ float4 sv[kChunk];   // column value rgb with its factor folded in (w unused)
     const int T = he * we;
@@ -95,8 +95,8 @@ __global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const floa
             } else if (MODE == 1) {
                 v = make_float4(omb * x[3 * b], omb * x[3 * b + 1], omb * x[3 * b + 2], 0.f);
             } else {
-                const float inv = 1.f / rowsum[b];
-                v = make_float4(x[3 * b] * inv, x[3 * b + 1] * inv, x[3 * b + 2] * inv, 0.f);
+                const double inv = 1.0 / (double)rowsum[b];
+                v = make_float4((float)(x[3 * b] * inv), (float)(x[3 * b + 1] * inv), (float)(x[3 * b + 2] * inv), 0.f);
             }
             sd[k] = make_float4(db[0], db[1], db[2], 0.f);
             sv[k] = v;
@@ -116,12 +116,12 @@ __global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const floa
     }
     if (a >= T) return;
     if (MODE == 0) {
-        out[a] = (float)t0;
+        out[a] = (TOut)t0;
     } else if (MODE == 1) {
         const double inv = 1.0 / (double)rowsum[a];
-        out[3 * a] = (float)(t0 * inv); out[3 * a + 1] = (float)(t1 * inv); out[3 * a + 2] = (float)(t2 * inv);
+        out[3 * a] = (TOut)(t0 * inv); out[3 * a + 1] = (TOut)(t1 * inv); out[3 * a + 2] = (TOut)(t2 * inv);
     } else {
-        out[3 * a] += (float)(t0 * oma); out[3 * a + 1] += (float)(t1 * oma); out[3 * a + 2] += (float)(t2 * oma);
+        out[3 * a] += (TOut)(t0 * oma); out[3 * a + 1] += (TOut)(t1 * oma); out[3 * a + 2] += (TOut)(t2 * oma);
     }
 }
 
@@ -197,12 +197,12 @@ __global__ void __launch_bounds__(128) spec_refresh_kernel(int he, int we, int l
 
 // d_base += S_l^T g_l (scatter form; atomics), l >= 1
 __global__ void __launch_bounds__(128) spec_adjoint_kernel(int he, int we, int levels, int samples,
-                                                           const float *__restrict__ g, float *__restrict__ d_base) {
+                                                           const double *__restrict__ g, double *__restrict__ d_base) {
     const int T = he * we;
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     const int lv = blockIdx.y + 1;
     if (a >= T) return;
-    const float *gl = g + (size_t)lv * T * 3;
+    const double *gl = g + (size_t)lv * T * 3;
     const double g0 = gl[3 * a], g1 = gl[3 * a + 1], g2 = gl[3 * a + 2];
     if (g0 == 0.0 && g1 == 0.0 && g2 == 0.0) return;
     const double rough = lv / (levels - 1.0), alpha = rough * rough;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(128) spec_adjoint_kernel(int he, int we, int l
         if (spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt)) ws += wgt;
     }
     if (ws <= 0.0) {
-        atomicAdd(d_base + 3 * a, (float)g0); atomicAdd(d_base + 3 * a + 1, (float)g1); atomicAdd(d_base + 3 * a + 2, (float)g2);
+        atomicAdd(d_base + 3 * a, g0); atomicAdd(d_base + 3 * a + 1, g1); atomicAdd(d_base + 3 * a + 2, g2);
         return;
     }
     const double inv = 1.0 / ws;
@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(128) spec_adjoint_kernel(int he, int we, int l
         if (!spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt)) continue;
         for (int k = 0; k < 4; ++k) {
             const double f = o.w[k] * inv;
-            atomicAdd(d_base + 3 * o.idx[k], (float)(f * g0));
-            atomicAdd(d_base + 3 * o.idx[k] + 1, (float)(f * g1));
-            atomicAdd(d_base + 3 * o.idx[k] + 2, (float)(f * g2));
+            atomicAdd(d_base + 3 * o.idx[k], f * g0);
+            atomicAdd(d_base + 3 * o.idx[k] + 1, f * g1);
+            atomicAdd(d_base + 3 * o.idx[k] + 2, f * g2);
         }
     }
 }
@@ -240,13 +240,13 @@ __global__ void exp_kernel(int n, const float *__restrict__ lg, float *__restric
     spec0[k] = b;
 }
 
-__global__ void adjoint_finish_kernel(int n, const float *__restrict__ g0, const float *__restrict__ base,
-                                      float *__restrict__ d_base, float *__restrict__ d_log) {
+__global__ void adjoint_finish_kernel(int n, const double *__restrict__ g0, const float *__restrict__ base,
+                                      double *__restrict__ d_base, float *__restrict__ d_log) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const float db = d_base[k] + g0[k];
+    const double db = d_base[k] + g0[k];
     d_base[k] = db;
-    d_log[k] = db * base[k];
+    d_log[k] = (float)(db * (double)base[k]);
 }
 
 
@@ -262,7 +262,7 @@ extern "C" int ss_brdf_lut(int res, int samples, float *lut, void *stream) {
 extern "C" int ss_env_rowsums(int he, int we, float *rowsum, void *stream) {
     if (he < 2 || we < 2 || !rowsum) return SS_ERR_INVALID;
     const int T = he * we;
-    diffuse_kernel<0><<<(T + 255) / 256, 256, 0, (cudaStream_t)stream>>>(he, we, nullptr, nullptr, rowsum);
+    diffuse_kernel<0, float, float><<<(T + 255) / 256, 256, 0, (cudaStream_t)stream>>>(he, we, nullptr, nullptr, rowsum);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
@@ -274,7 +274,7 @@ extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const flo
     const int T = he * we;
     exp_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular);
     SS_CUDA_CHECK_LAUNCH();
-    diffuse_kernel<1><<<(T + 255) / 256, 256, 0, st>>>(he, we, base, rowsum, diffuse);
+    diffuse_kernel<1, float, float><<<(T + 255) / 256, 256, 0, st>>>(he, we, base, rowsum, diffuse);
     SS_CUDA_CHECK_LAUNCH();
     if (levels > 1) {
         spec_refresh_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, base, specular);
@@ -284,14 +284,14 @@ extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const flo
 }
 
 extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, const float *rowsum,
-                              const float *d_diffuse, const float *d_specular, float *d_base, float *d_base_log,
+                              const double *d_diffuse, const double *d_specular, double *d_base, float *d_base_log,
                               void *stream) {
     if (he < 2 || we < 2 || levels < 1 || !base || !rowsum || !d_diffuse || !d_specular || !d_base || !d_base_log)
         return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int T = he * we;
-    cudaMemsetAsync(d_base, 0, sizeof(float) * 3 * T, st);
-    diffuse_kernel<2><<<(T + 255) / 256, 256, 0, st>>>(he, we, d_diffuse, rowsum, d_base);
+    cudaMemsetAsync(d_base, 0, sizeof(double) * 3 * T, st);
+    diffuse_kernel<2, double, double><<<(T + 255) / 256, 256, 0, st>>>(he, we, d_diffuse, rowsum, d_base);
     SS_CUDA_CHECK_LAUNCH();
     if (levels > 1) {
         spec_adjoint_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, d_specular, d_base);

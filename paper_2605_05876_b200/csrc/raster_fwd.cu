@@ -7,11 +7,11 @@
 // warps own 8x4 pixel blocks and walk the tile's sorted pair list
 // independently (raster_walk.cuh: 32 packed rects per ballot, only the
 // overlapping records are gathered into the warp's shared-memory slots, no
-// CTA barrier), all 32 lanes on the same record in list order.  Coverage uses
-// a float32/FMA fast path whose decision is re-taken with the reference's
-// exact arithmetic (float32 intersection without contraction, numba's
-// float64 rho^2) whenever it is within 1% of the cut-off, so coverage and
-// layer membership are identical to the reference (verified at scale by
+// CTA barrier), all 32 lanes on the same record in list order.  Coverage
+// (raster_walk.cuh ss_cover) reproduces the reference's float32 intersection
+// bit for bit and re-takes the decision with numba's float64 rho^2 when the
+// float32 value is within 1e-4 of the cut-off, so coverage and layer
+// membership are identical to the reference (verified at scale by
 // ss_debug_cover_check); accumulation is float32 (the reference's outputs are
 // float32 too).
 //
@@ -146,30 +146,31 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
             const float gc1 = d1 > 0.f ? sg : (d1 < 0.f ? -sg : 0.f);
             const float gc2 = d2 > 0.f ? sg : (d2 < 0.f ? -sg : 0.f);
             // suffix recursion over the layers (backward.py:201-238, no
-            // consolidation, no coverage loss): per layer A and dL/dC_raw
-            float tb[KL], av[KL];
-            float tr = 1.f;
+            // consolidation, no coverage loss) in float64 like the reference:
+            // per layer A and dL/dC_raw
+            double tb[KL], av[KL];
+            double tr = 1.0;
             for (int m = 0; m < layers; ++m) {
-                av[m] = -expm1f(-lw[m]);
+                av[m] = -expm1(-(double)lw[m]);
                 tb[m] = tr;
-                tr *= 1.f - av[m];
+                tr *= 1.0 - av[m];
             }
-            float sf0 = P.bg0, sf1 = P.bg1, sf2 = P.bg2;
+            double sf0 = P.bg0, sf1 = P.bg1, sf2 = P.bg2;
             const size_t HW = (size_t)P.W * P.H;
             for (int m = layers - 1; m >= 0; --m) {
-                const float inv = 1.f / lw[m];
-                const float ch0 = lc0[m] * inv, ch1 = lc1[m] * inv, ch2 = lc2[m] * inv;
-                const float a = av[m];
-                const float g_am = tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2));
-                const float ta = tb[m] * a;
-                const float gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
+                const double inv = 1.0 / (double)lw[m];
+                const double ch0 = lc0[m] * inv, ch1 = lc1[m] * inv, ch2 = lc2[m] * inv;
+                const double a = av[m];
+                const double g_am = tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2));
+                const double ta = tb[m] * a;
+                const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
                 float4 cf;
-                cf.x = g_am * (1.f - a) - (gh0 * ch0 + gh1 * ch1 + gh2 * ch2) * inv;
-                cf.y = gh0 * inv; cf.z = gh1 * inv; cf.w = gh2 * inv;
+                cf.x = (float)(g_am * (1.0 - a) - (gh0 * ch0 + gh1 * ch1 + gh2 * ch2) * inv);
+                cf.y = (float)(gh0 * inv); cf.z = (float)(gh1 * inv); cf.w = (float)(gh2 * inv);
                 P.coef[(size_t)m * HW + pix] = cf;
-                sf0 = a * ch0 + (1.f - a) * sf0;
-                sf1 = a * ch1 + (1.f - a) * sf1;
-                sf2 = a * ch2 + (1.f - a) * sf2;
+                sf0 = a * ch0 + (1.0 - a) * sf0;
+                sf1 = a * ch1 + (1.0 - a) * sf1;
+                sf2 = a * ch2 + (1.0 - a) * sf2;
             }
         }
     }
@@ -280,8 +281,10 @@ __global__ void __launch_bounds__(256) cover_check_kernel(int W, int H, int tile
                   SsHit h;
                   const bool exact = ss_intersect(wp.x, wp.y, t1, t2, t4, h) && ss_rho2(R.c.y, R.c.z, R.c.w, h.u, h.v) < 9.0;
                   bad += fast != exact;
-                  const float a = c.k0 * c.l1, b = c.k1 * c.l0;
-                  slow += !(fabsf(c.den) > 1e-5f * (fabsf(a) + fabsf(b)) + 1e-8f) || fabsf(c.rho2 - 9.f) < 0.09f;
+                  const float ta = R.c.y * c.u * c.u, tb = 2.f * R.c.z * c.u * c.v, tc = R.c.w * c.v * c.v;
+                  const float mag = fabsf(ta) + fabsf(tb) + fabsf(tc);
+                  const float r2 = ta + tb + tc;
+                  slow += !(r2 - 9.f >= 2e-4f * mag || (9.f - r2 >= 2e-4f * mag && mag <= 32.f));
               });
     atomicAdd(&counts[0], n);
     atomicAdd(&counts[1], bad);

@@ -71,12 +71,15 @@ __device__ __forceinline__ void walk_tile(const WarpPix &w, int p0, int p1, cons
 }
 
 // Coverage of pixel (x, y) by a record, with everything downstream.
-// Fast path: float32 with FMA and an approximate reciprocal.  Whenever the
-// decision could differ from the reference's exact float32/float64 evaluation
-// (rho^2 within 1% of the cut-off, or a denominator small relative to its
-// terms) the exact evaluation (ss_intersect + ss_rho2) decides, so coverage
-// and therefore layer membership are identical to the reference; u, v, rho^2
-// and the weight are the fast values (a few ulp from the reference's).
+// k, l, den and the two numerators are evaluated with the reference's exact
+// float32 operation sequence (no contraction), so they are bit-identical to
+// rasterizer.py:197-205 and the ray-miss test |den| < 1e-9 is exact.  The
+// quotient uses an IEEE reciprocal (u, v within 1 ulp of the reference's
+// division) and rho^2 is evaluated in float32; when the quadratic form is ill
+// conditioned (cancelling terms, |terms| > 32) or rho^2 lies within 2e-4 of
+// its term magnitude from the cut-off, the reference's exact u, v and numba's
+// float64 rho^2 decide (and are used).  Coverage and layer membership are
+// therefore identical to the reference, and weights agree to ~1e-6 relative.
 struct Cover {
     float k0, k1, k2, l0, l1, l2, den, inv_den, u, v, rho2;
 };
@@ -84,28 +87,32 @@ struct Cover {
 __device__ __forceinline__ bool ss_cover(float x, float y, const SsRecord &R, Cover &c) {
     const float t1x = R.a.x, t1y = R.a.y, t1z = R.a.z, t2x = R.a.w, t2y = R.b.x, t2z = R.b.y;
     const float t4x = R.b.z, t4y = R.b.w, t4z = R.c.x;
-    c.k0 = __fmaf_rn(x, t4x, -t1x);
-    c.k1 = __fmaf_rn(x, t4y, -t1y);
-    c.k2 = __fmaf_rn(x, t4z, -t1z);
-    c.l0 = __fmaf_rn(y, t4x, -t2x);
-    c.l1 = __fmaf_rn(y, t4y, -t2y);
-    c.l2 = __fmaf_rn(y, t4z, -t2z);
-    const float a = c.k0 * c.l1, b = c.k1 * c.l0;
-    c.den = a - b;
-    c.inv_den = __fdividef(1.0f, c.den);
-    c.u = (c.k1 * c.l2 - c.k2 * c.l1) * c.inv_den;
-    c.v = (c.k2 * c.l0 - c.k0 * c.l2) * c.inv_den;
+    c.k0 = fs(fm(x, t4x), t1x);
+    c.k1 = fs(fm(x, t4y), t1y);
+    c.k2 = fs(fm(x, t4z), t1z);
+    c.l0 = fs(fm(y, t4x), t2x);
+    c.l1 = fs(fm(y, t4y), t2y);
+    c.l2 = fs(fm(y, t4z), t2z);
+    c.den = fs(fm(c.k0, c.l1), fm(c.k1, c.l0));
+    if (fabsf(c.den) <= 9.99999972e-10f) return false;  // == (double)|den| < 1e-9 exactly
+    const float nu = fs(fm(c.k1, c.l2), fm(c.k2, c.l1));
+    const float nv = fs(fm(c.k2, c.l0), fm(c.k0, c.l2));
+    c.inv_den = __frcp_rn(c.den);
+    c.u = nu * c.inv_den;
+    c.v = nv * c.inv_den;
     const float s0 = R.c.y, s1 = R.c.z, s2 = R.c.w;
-    c.rho2 = s0 * c.u * c.u + 2.f * s1 * c.u * c.v + s2 * c.v * c.v;
-    const bool doubtful = !(fabsf(c.den) > 1e-5f * (fabsf(a) + fabsf(b)) + 1e-8f) ||
-                          fabsf(c.rho2 - 9.f) < 0.09f || !(c.rho2 == c.rho2);
-    if (!doubtful) return c.rho2 < 9.f;
-    const float t1[3] = {t1x, t1y, t1z}, t2[3] = {t2x, t2y, t2z}, t4[3] = {t4x, t4y, t4z};
-    SsHit h;
-    if (!ss_intersect(x, y, t1, t2, t4, h)) return false;
-    const double r2 = ss_rho2(s0, s1, s2, h.u, h.v);
-    if (!(r2 < 9.0)) return false;
-    c.k0 = h.k0; c.k1 = h.k1; c.k2 = h.k2; c.l0 = h.l0; c.l1 = h.l1; c.l2 = h.l2;
-    c.den = h.den; c.inv_den = 1.f / h.den; c.u = h.u; c.v = h.v; c.rho2 = (float)r2;
-    return true;
+    const float ta = s0 * c.u * c.u, tb = 2.f * s1 * c.u * c.v, tc = s2 * c.v * c.v;
+    c.rho2 = ta + tb + tc;
+    // the float32 sum is within ~4e-7 * mag of the reference's mixed-precision
+    // value when the quadratic form is well conditioned (mag <= 32); otherwise,
+    // or near the cut-off, the reference's exact arithmetic decides
+    const float mag = fabsf(ta) + fabsf(tb) + fabsf(tc);
+    if (c.rho2 - 9.f >= 2e-4f * mag) return false;                // clearly outside
+    if (9.f - c.rho2 >= 2e-4f * mag && mag <= 32.f) return true;  // clearly inside, well conditioned
+    // doubtful: the reference's exact quotient and float64 rho^2 decide
+    c.u = fd(nu, c.den);
+    c.v = fd(nv, c.den);
+    const double r2 = ss_rho2(s0, s1, s2, c.u, c.v);
+    c.rho2 = (float)r2;
+    return r2 < 9.0;
 }

@@ -88,11 +88,12 @@ class EnvironmentLight:
         """Derived-map gradients -> (d_base, d_base_log) (shading.py:381-394)."""
         lib = _lib.load()
         he, we = self.shape
-        dd = torch.as_tensor(d_diffuse, device="cuda", dtype=torch.float32).contiguous() if d_diffuse is not None \
-            else torch.zeros_like(self.base)
-        ds = torch.as_tensor(d_specular, device="cuda", dtype=torch.float32).contiguous() if d_specular is not None \
-            else torch.zeros_like(self.specular)
-        d_base = torch.empty_like(self.base)
+        f64 = dict(device="cuda", dtype=torch.float64)
+        dd = torch.as_tensor(d_diffuse, **f64).contiguous() if d_diffuse is not None \
+            else torch.zeros(self.base.shape, **f64)
+        ds = torch.as_tensor(d_specular, **f64).contiguous() if d_specular is not None \
+            else torch.zeros(self.specular.shape, **f64)
+        d_base = torch.empty(self.base.shape, **f64)
         d_log = torch.empty_like(self.base)
         _lib.check(lib.ss_env_adjoint(he, we, self.levels, self.spec_samples, _lib.ptr(self.base),
                                       _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(dd), _lib.ptr(ds),

@@ -109,9 +109,9 @@ class TrainStep:
         self.loss_f = self.pack.loss
         self.touched = self.pack.touched
         self.loss = torch.zeros(1, device=dev, dtype=torch.float64)
-        self.d_diffuse = torch.zeros_like(env.base)
-        self.d_spec = torch.zeros_like(env.specular)
-        self.d_base = torch.empty_like(env.base)
+        self.d_diffuse = torch.zeros(env.base.shape, device=dev, dtype=torch.float64)
+        self.d_spec = torch.zeros(env.specular.shape, device=dev, dtype=torch.float64)
+        self.d_base = torch.empty(env.base.shape, device=dev, dtype=torch.float64)
         self.adam = Adam()
         self._cl = _lib.make_cloud(cloud)
         self._po = make_opts(self.opts, tile)

@@ -35,8 +35,8 @@ def test_train_step_gradients_match_api_path():
     # API path: render -> L1 -> backward_image, summed over views
     acc = {k: torch.zeros_like(ts.grads[k]) for k in PARAMS}
     loss = 0.0
-    d_diff = torch.zeros_like(env.base)
-    d_spec = torch.zeros_like(env.specular)
+    d_diff = torch.zeros(env.base.shape, device="cuda", dtype=torch.float64)
+    d_spec = torch.zeros(env.specular.shape, device="cuda", dtype=torch.float64)
     for cam, tgt in zip(cams, targets):
         res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
         val, g = ss.photometric_loss(res.rgb, tgt, lambda_ssim=0.0)
