@@ -174,24 +174,29 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
     double galb[3] = {0.0, 0.0, 0.0}, gmet = 0.0, grough = 0.0;
 
     if (P.color_source == SS_COLOR_IBL) {
-        ShadeIn in;
+        // float32 shading adjoint (the forward colours are float64 in the
+        // preprocess kernel; gradients only need the 1e-3 parity bar)
+        ShadeIn<float> in;
         ss_shade_inputs(cl, i, P.cam_pos, in);
-        ShadeState st;
-        double col[3];
+        ShadeState<float> st;
+        float col[3];
         ss_shade_forward(in, P.env, st, col);
-        ShadeGrads sg;
-        ss_shade_backward(in, st, P.env, gcol, sg);
+        ShadeGrads<float> sg;
+        const float gcf[3] = {(float)gcol[0], (float)gcol[1], (float)gcol[2]};
+        ss_shade_backward(in, st, P.env, gcf, sg);
         for (int c = 0; c < 3; ++c) { gcent[c] += sg.center[c]; gN[c] = sg.normal[c]; galb[c] = sg.albedo_raw[c]; }
+        (void)col;
         gmet = sg.metallic_raw;
         grough = sg.roughness_raw;
         // derived-map scatter (bilinear_scatter, shading.py:248-260, 583-597)
         const int we = P.env.we;
         const size_t lstride = (size_t)P.env.he * we * 3;
-        const double wts[2] = {1.0 - st.frac, st.frac};
+        const double wts[2] = {1.0 - (double)st.frac, (double)st.frac};
         const int lvs[2] = {st.lvl0, st.lvl1};
-        const SsBil &bs = st.bs;
+        const SsBil<float> &bs = st.bs;
         const int sidx[4] = {bs.j0 * we + bs.i0, bs.j0 * we + bs.i1, bs.j1 * we + bs.i0, bs.j1 * we + bs.i1};
-        const double scw[4] = {(1 - bs.tu) * (1 - bs.tv), bs.tu * (1 - bs.tv), (1 - bs.tu) * bs.tv, bs.tu * bs.tv};
+        const double scw[4] = {(1.0 - bs.tu) * (1.0 - bs.tv), (double)bs.tu * (1.0 - bs.tv), (1.0 - bs.tu) * (double)bs.tv,
+                               (double)bs.tu * bs.tv};
         for (int h = 0; h < 2; ++h) {
             if (wts[h] == 0.0) continue;
             double *dst = P.g.d_specular + lstride * lvs[h];
@@ -201,9 +206,10 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
                     if (val != 0.0) atomicAdd(dst + 3 * sidx[k] + c, val);
                 }
         }
-        const SsBil &bd = st.bd;
+        const SsBil<float> &bd = st.bd;
         const int didx[4] = {bd.j0 * we + bd.i0, bd.j0 * we + bd.i1, bd.j1 * we + bd.i0, bd.j1 * we + bd.i1};
-        const double dcw[4] = {(1 - bd.tu) * (1 - bd.tv), bd.tu * (1 - bd.tv), (1 - bd.tu) * bd.tv, bd.tu * bd.tv};
+        const double dcw[4] = {(1.0 - bd.tu) * (1.0 - bd.tv), (double)bd.tu * (1.0 - bd.tv), (1.0 - bd.tu) * (double)bd.tv,
+                               (double)bd.tu * bd.tv};
         for (int k = 0; k < 4; ++k)
             for (int c = 0; c < 3; ++c) {
                 const double val = sg.g_ld[c] * dcw[k];

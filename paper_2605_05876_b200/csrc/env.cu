@@ -145,7 +145,7 @@ __device__ __forceinline__ bool spec_sample(const double d[3], const double tx[3
     if (!(wgt > 0.0)) return false;
     double fu, fv;
     ss_dir_coords(l, he, we, fu, fv);
-    const SsBil b = ss_bil_prepare(he, we, fu, fv, true);
+    const SsBil<double> b = ss_bil_prepare<double>(he, we, fu, fv, true);
     o.idx[0] = b.j0 * we + b.i0; o.idx[1] = b.j0 * we + b.i1; o.idx[2] = b.j1 * we + b.i0; o.idx[3] = b.j1 * we + b.i1;
     o.w[0] = wgt * (1 - b.tu) * (1 - b.tv); o.w[1] = wgt * b.tu * (1 - b.tv);
     o.w[2] = wgt * (1 - b.tu) * b.tv; o.w[3] = wgt * b.tu * b.tv;

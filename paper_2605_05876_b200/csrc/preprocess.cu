@@ -155,9 +155,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     } else if (color_source == SS_COLOR_ALBEDO) {
         col[0] = ss_sigmoid_f32(ar0); col[1] = ss_sigmoid_f32(ar1); col[2] = ss_sigmoid_f32(ar2);
     } else {
-        ShadeIn in;
+        ShadeIn<double> in;
         ss_shade_inputs(cloud, i, cam.cam_pos, in);
-        ShadeState st;
+        ShadeState<double> st;
         double out[3];
         ss_shade_forward(in, env, st, out);
         col[0] = (float)out[0]; col[1] = (float)out[1]; col[2] = (float)out[2];
