@@ -146,28 +146,24 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
  * (losses.py:94-108, lambda_ssim=0) against `target` (H,W,3) and with the
  * per-pixel suffix recursion of backward.py:201-238.  Writes per pixel and
  * layer the float4 (A, dL/dC_raw rgb) into `coef` (k_max*H*W*4 floats,
- * layer-major planes), the depth at which each layer closed into `thr`
- * (k_max*H*W floats) and the number of closed layers into `ncl` (H*W int32),
- * and adds sum|rgb - target| into loss_sum (1 double).  rgb is nullable.
- * ss_train_backward: pass 2 of backward.py:240-320 without the walk: layer
- * membership from `thr`/`ncl`, one thread per (record, tile) pair; accumulates
- * into rec_acc exactly like ss_raster_backward (channel 16 stays 0: no
- * consolidation term in this loss).  pair_rect is accepted for symmetry. */
+ * layer-major planes), per pixel a packed header `pix_hdr` (H*W int4:
+ * number of closed layers, then the depths at which layers 0..2 closed, as
+ * float bits) and the closing depths of layers >= 3 into `thr` (k_max*H*W
+ * floats, plane j), and adds sum|rgb - target| into loss_sum (1 double).
+ * rgb (H,W,3) is nullable.
+ * ss_train_backward_records: pass 2 of backward.py:240-320 without the walk:
+ * a covering record with interval start zs belongs to layer
+ * #{j : closing depth_j < zs}; one warp per record sweeps its
+ * rect.  The rec_acc row of every kept record is OVERWRITTEN (committed once,
+ * no atomics, no memset needed; culled rows untouched -- ss_chain_backward
+ * skips them); channel 16 (dview_z) is 0 without a consolidation term.
+ * pixel_ndc: scratch of width + height + 1 + n 32-bit words. */
 int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
                      const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
                      const float *background, int k_max, const float *target, float *coef, float *thr,
-                     int32_t *ncl, double *loss_sum, float *rgb, void *stream);
-int ss_train_backward(int width, int height, int tile, const int32_t *tile_offsets,
-                      const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, int k_max,
-                      const float *coef, const float *thr, const int32_t *ncl, float *rec_acc, void *stream);
-/* ss_train_backward_records: the same pass 2 with one warp per record (its
- * whole rect), no tile lists needed; the rec_acc row of every kept record is
- * OVERWRITTEN (committed once, no atomics, no memset needed; culled rows are
- * left untouched -- ss_chain_backward skips them).
- * pixel_ndc: scratch of width + height + 1 + n 32-bit words (pixel NDC
- * tables, then the queue of records with very large rects). */
+                     int32_t *pix_hdr, double *loss_sum, float *rgb, void *stream);
 int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
-                              int k_max, const float *coef, const float *thr, const int32_t *ncl,
+                              int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
                               float *pixel_ndc, float *rec_acc, void *stream);
 
 /* ---- chain backward -------------------------------------------------------

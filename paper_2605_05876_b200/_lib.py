@@ -82,8 +82,6 @@ _SIGNATURES = {
                      ctypes.c_int, c_p, c_p],
     "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
                          ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
-    "ss_train_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p,
-                          c_p, c_p],
     "ss_train_backward_records": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
                                   c_p, c_p, c_p],
     "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],

@@ -42,8 +42,8 @@ struct FwdParams {
     const float *target;   // (H,W,3)
     float inv_count;       // 1 / (3 H W): mean over all image entries
     float4 *coef;          // (k_max, H*W) float4
-    float *thr;            // (k_max, H*W) depth at which each layer closed
-    int32_t *ncl;          // (H*W) number of closed layers
+    float *thr;            // (k_max, H*W) depth at which layer j >= 3 closed
+    int4 *hdr;             // (H*W) packed (closed-layer count, closing depth of layers 0..2)
     double *loss;          // sum of |rgb - target| (1 double)
 };
 
@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
     constexpr int KL = kTrain ? SS_KMAX_CAP : 1;
     float lw[KL], lc0[KL], lc1[KL], lc2[KL];
     int ncl = 0;
+    float th0 = 0.f, th1 = 0.f, th2 = 0.f;  // first three closing depths (kTrain)
 
     auto close_layer = [&]() {
         const float a_k = -expm1f(-Wg);
@@ -101,7 +102,12 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
                 } else {
                     bool go = true;
                     if (Wg > 0.f && R.d.z > zmax) {
-                        if (kTrain) P.thr[(size_t)ncl * P.W * P.H + pix] = zmax;
+                        if (kTrain) {
+                            if (ncl == 0) th0 = zmax;
+                            else if (ncl == 1) th1 = zmax;
+                            else if (ncl == 2) th2 = zmax;
+                            else P.thr[(size_t)ncl * P.W * P.H + pix] = zmax;
+                        }
                         ++ncl;
                         close_layer();  // rasterizer.py:168-196
                         if (layers >= P.k_max) { stopped = true; ++discarded; go = false; }
@@ -137,7 +143,7 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
             P.depth[pix] = dden > 0.f ? dnum / dden : 0.f;
             P.nlayers[pix] = layers;
         } else {
-            P.ncl[pix] = ncl;
+            P.hdr[pix] = make_int4(ncl, __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
             // L1 loss and its image gradient (losses.py:100-104)
             const float d0 = r0 - P.target[3 * pix], d1 = r1 - P.target[3 * pix + 1], d2 = r2 - P.target[3 * pix + 2];
             lsum = (double)fabsf(d0) + (double)fabsf(d1) + (double)fabsf(d2);
@@ -238,15 +244,15 @@ extern "C" int ss_raster_forward(int width, int height, int tile, const int32_t 
 
 extern "C" int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
                                 const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
-                                int k_max, const float *target, float *coef, float *thr, int32_t *ncl,
+                                int k_max, const float *target, float *coef, float *thr, int32_t *pix_hdr,
                                 double *loss_sum, float *rgb, void *stream)
 {
     FwdParams P;
     if (!fill_common(P, width, height, tile, tile_offsets, pair_rec, pair_rect, records, background, k_max)) return SS_ERR_INVALID;
-    if (!target || !coef || !thr || !ncl || !loss_sum) return SS_ERR_INVALID;
+    if (!target || !coef || !thr || !pix_hdr || !loss_sum) return SS_ERR_INVALID;
     P.target = target;
     P.thr = thr;
-    P.ncl = ncl;
+    P.hdr = reinterpret_cast<int4 *>(pix_hdr);
     P.inv_count = (float)(1.0 / (3.0 * (double)width * (double)height));
     P.coef = reinterpret_cast<float4 *>(coef);
     P.loss = loss_sum;

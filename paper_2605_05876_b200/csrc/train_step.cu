@@ -32,8 +32,8 @@ struct SplatParams {
     const SsRecord *records;
     const float *xs, *ys;   // pixel-centre NDC per column / row
     const float4 *coef;     // (k_max, HW) per-layer (A, dL/dC_raw)
-    const float *thr;       // (k_max, HW) layer closing depths
-    const int32_t *ncl;     // (HW) number of closed layers (thresholds)
+    const float *thr;       // (k_max, HW) closing depths of layers >= 3
+    const int4 *hdr;        // (HW) (closed-layer count, closing depths of layers 0..2)
     float *acc;             // (n, 20)
 };
 
@@ -55,12 +55,16 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
     Cover c;
     if (!ss_cover(x, y, R, c)) return 0;
     const size_t pix = (size_t)iy * P.W + ix;
-    const int nc = __ldg(P.ncl + pix);
+    // packed header and the (most common) layer-0 coefficients in parallel
+    const int4 h = __ldg(P.hdr + pix);
+    const float4 cf0 = __ldg(P.coef + pix);
     const float zs = R.d.z;
-    int m = 0;
-    for (int j = 0; j < nc; ++j) m += __ldg(P.thr + j * HW + pix) < zs;
+    const int nc = h.x;
+    int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
+            (nc > 2 && __int_as_float(h.w) < zs);
+    for (int j = 3; j < nc; ++j) m += __ldg(P.thr + j * HW + pix) < zs;
     if (m >= P.k_max) return 0;  // beyond the K_MAX stop: discarded
-    const float4 cf = __ldg(P.coef + m * HW + pix);
+    const float4 cf = m == 0 ? cf0 : __ldg(P.coef + m * HW + pix);
     const float e = __expf(-0.5f * c.rho2);
     const float w = R.d.x * e;
     const float gw = cf.x + cf.y * R.e.x + cf.z * R.e.y + cf.w * R.e.z;
@@ -182,21 +186,13 @@ __global__ void __launch_bounds__(256) big_bwd_kernel(SplatParams P, const int32
 
 }  // namespace
 
-extern "C" int ss_train_backward(int width, int height, int tile, const int32_t *tile_offsets,
-                                 const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, int k_max,
-                                 const float *coef, const float *thr, const int32_t *ncl, float *rec_acc, void *stream)
-{
-    (void)pair_rect; (void)tile_offsets; (void)pair_rec; (void)tile;
-    return SS_ERR_INVALID;  // superseded by ss_train_backward_records
-}
-
 extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
-                                         int k_max, const float *coef, const float *thr, const int32_t *ncl,
+                                         int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
                                          float *pixel_ndc, float *rec_acc, void *stream)
 {
     if (n < 0 || width <= 0 || height <= 0 || k_max < 1 || k_max > SS_KMAX_CAP) return SS_ERR_INVALID;
     if (n == 0) return SS_OK;
-    if (!cull || !records || !coef || !thr || !ncl || !pixel_ndc || !rec_acc) return SS_ERR_INVALID;
+    if (!cull || !records || !coef || !thr || !pix_hdr || !pixel_ndc || !rec_acc) return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int mx = width > height ? width : height;
     int32_t *big_count = reinterpret_cast<int32_t *>(pixel_ndc + width + height);
@@ -209,7 +205,7 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     P.records = reinterpret_cast<const SsRecord *>(records);
     P.xs = pixel_ndc; P.ys = pixel_ndc + width;
     P.coef = reinterpret_cast<const float4 *>(coef);
-    P.thr = thr; P.ncl = ncl; P.acc = rec_acc;
+    P.thr = thr; P.hdr = reinterpret_cast<const int4 *>(pix_hdr); P.acc = rec_acc;
     splat_bwd_kernel<<<148 * 16, 256, 0, st>>>(P, big_list, big_count);
     SS_CUDA_CHECK_LAUNCH();
     big_bwd_kernel<<<148 * 4, 256, 0, st>>>(P, big_list, big_count);

@@ -96,7 +96,7 @@ class TrainStep:
         self.cursors = torch.empty(self.ntiles, **i32)
         self.coef = torch.empty((self.k_max, self.H * self.W, 4), **f32)
         self.thr = torch.empty((self.k_max, self.H * self.W), **f32)
-        self.ncl = torch.empty(self.H * self.W, **i32)
+        self.pix_hdr = torch.empty((self.H * self.W, 4), **i32)
         self.pixel_ndc = torch.empty(self.W + self.H + 1 + n, **f32)  # NDC tables + big-rect queue
         self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
         he, we = env.shape
@@ -175,13 +175,13 @@ class TrainStep:
         ev = self._ev_begin("train_forward")
         _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(self.offsets), _lib.ptr(self.pair),
                                         _lib.ptr(self.pair_rect), _lib.ptr(self.records), self._bg[0], self.k_max,
-                                        _lib.ptr(target), _lib.ptr(self.coef), _lib.ptr(self.thr), _lib.ptr(self.ncl),
+                                        _lib.ptr(target), _lib.ptr(self.coef), _lib.ptr(self.thr), _lib.ptr(self.pix_hdr),
                                         _lib.ptr(self.loss), None, s), "ss_train_forward")
         self._ev_end(ev)
         ev = self._ev_begin("train_backward")
         _lib.check(lib.ss_train_backward_records(self.n, _lib.ptr(self.cull), _lib.ptr(self.records), self.W,
                                                  self.H, self.k_max, _lib.ptr(self.coef), _lib.ptr(self.thr),
-                                                 _lib.ptr(self.ncl), _lib.ptr(self.pixel_ndc), _lib.ptr(self.acc), s),
+                                                 _lib.ptr(self.pix_hdr), _lib.ptr(self.pixel_ndc), _lib.ptr(self.acc), s),
                    "ss_train_backward_records")
         self._ev_end(ev)
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
