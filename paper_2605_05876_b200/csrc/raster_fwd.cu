@@ -47,14 +47,20 @@ struct FwdParams {
     double *loss;          // sum of |rgb - target| (1 double)
 };
 
+// CTAs of kFwdWarps warps (a tile is split over tile*tile/32/kFwdWarps
+// CTAs): warps never wait for each other, and a finished warp pair frees its
+// slot without waiting for the tile's slowest warp.
+constexpr int kFwdWarps = 2;
+
 template <bool kExtras, bool kTrain>
-__global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
+__global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 {
-    __shared__ SsRecord wbuf_all[8][32];
-    __shared__ double loss_red[32];
-    const int t = blockIdx.x;
-    const WarpPix wp = warp_pixels(t, P.ntx, P.tile, P.W, P.H);
-    const int lane = wp.lane, wid = wp.wid;
+    __shared__ SsRecord wbuf_all[kFwdWarps][32];
+    const int ctas_per_tile = P.tile * P.tile / (32 * kFwdWarps);
+    const int t = blockIdx.x / ctas_per_tile;
+    const int wid_in_tile = (blockIdx.x % ctas_per_tile) * kFwdWarps + (threadIdx.x >> 5);
+    const WarpPix wp = warp_pixels(t, P.ntx, P.tile, P.W, P.H, wid_in_tile);
+    const int lane = wp.lane, wid = threadIdx.x >> 5;
     const bool live = wp.live;
     const size_t pix = wp.pix;
     SsRecord *wbuf = wbuf_all[wid];
@@ -189,19 +195,14 @@ __global__ void __launch_bounds__(256) raster_fwd_kernel(FwdParams P)
     if (kTrain) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-        if (lane == 0) loss_red[wid] = lsum;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += loss_red[k];
-            atomicAdd(P.loss, s);
-        }
+        if (lane == 0) atomicAdd(P.loss, lsum);
     }
 }
 
 template <bool kExtras, bool kTrain>
 void launch(const FwdParams &P, int ntiles, int threads, cudaStream_t st) {
-    raster_fwd_kernel<kExtras, kTrain><<<ntiles, threads, 0, st>>>(P);
+    const int ctas_per_tile = threads / (32 * kFwdWarps);
+    raster_fwd_kernel<kExtras, kTrain><<<ntiles * ctas_per_tile, 32 * kFwdWarps, 0, st>>>(P);
 }
 
 bool fill_common(FwdParams &P, int width, int height, int tile, const int32_t *tile_offsets,

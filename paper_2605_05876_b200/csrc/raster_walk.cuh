@@ -11,10 +11,10 @@ struct WarpPix {
     size_t pix;
 };
 
-__device__ __forceinline__ WarpPix warp_pixels(int t, int ntx, int tile, int W, int H) {
+__device__ __forceinline__ WarpPix warp_pixels(int t, int ntx, int tile, int W, int H, int wid_in_tile) {
     WarpPix w;
     w.lane = threadIdx.x & 31;
-    w.wid = threadIdx.x >> 5;
+    w.wid = wid_in_tile;
     const int tx = t % ntx, ty = t / ntx;
     const int wpr = tile >> 3;
     w.bx = tx * tile + (w.wid % wpr) * 8;
@@ -26,6 +26,10 @@ __device__ __forceinline__ WarpPix warp_pixels(int t, int ntx, int tile, int W, 
     w.y = ss_ndc_y(w.py, H);
     w.pix = w.live ? (size_t)w.py * W + w.px : 0;
     return w;
+}
+
+__device__ __forceinline__ WarpPix warp_pixels(int t, int ntx, int tile, int W, int H) {
+    return warp_pixels(t, ntx, tile, W, H, threadIdx.x >> 5);
 }
 
 __device__ __forceinline__ bool in_rect(const WarpPix &w, int4 r) {
