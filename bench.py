@@ -110,7 +110,7 @@ def run_reference(args):
     v = 1.0 / float(np.mean(times))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
             "data": "synthetic", "config": _config({"sample": sample}),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -284,7 +284,7 @@ def run_ours(args):
     launches = ts.launches_per_step * args.steps
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": _config({"parallelism": f"dp{world} over views", "pairs_per_view": P, "kept_per_view": Nk}),
         "e2e": e2e,

@@ -193,14 +193,37 @@ int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreproc
  *   (He,We,3) -> base, diffuse (He,We,3), specular (L,He,We,3).
  * ss_env_adjoint: env_gradient (shading.py:381-394): d_diffuse, d_specular
  *   -> d_base_log (He,We,3) (and d_base when non-null).
- * Both need the diffuse row sums: ss_env_rowsums fills rowsum (He*We floats). */
+ * Both need the diffuse row sums: ss_env_rowsums fills rowsum (He*We floats).
+ * `work`: float64 scratch of 3*He*We (split-column partial sums). */
 int ss_brdf_lut(int res, int samples, float *lut, void *stream);
-int ss_env_rowsums(int he, int we, float *rowsum, void *stream);
+int ss_env_rowsums(int he, int we, float *rowsum, double *work, void *stream);
 int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log,
-                   const float *rowsum, float *base, float *diffuse, float *specular, void *stream);
+                   const float *rowsum, float *base, float *diffuse, float *specular, double *work,
+                   void *stream);
 int ss_env_adjoint(int he, int we, int levels, int samples, const float *base,
                    const float *rowsum, const double *d_diffuse, const double *d_specular,
-                   double *d_base, float *d_base_log, void *stream);
+                   double *d_base, float *d_base_log, double *work, void *stream);
+
+/* Specular prefilter operators S_l (l = 1..L-1) as a sparse matrix, built
+ * once per (He, We, L, samples) instead of regenerating 128 GGX samples per
+ * texel per call.  Rows r = (l-1)*T + i; duplicate columns are kept (the SpMV
+ * sums them); weights are divided by the row weight sum; empty rows hold one
+ * identity entry.  ss_spec_op_count -> row_nnz ((L-1)*T int32), the caller
+ * scans it into row_ptr ((L-1)*T+1 int64), ss_spec_op_fill -> col (int32),
+ * val (float).  The caller builds the per-level transpose (CSC: col_ptr over
+ * (l-1)*T + j, row, val) with a stable sort and registers both with
+ * ss_spec_op_register; ss_env_refresh / ss_env_adjoint then use them (row-
+ * gather SpMV and column-gather transpose, no atomics).  ss_spec_apply /
+ * ss_spec_apply_t expose the two products directly. */
+int ss_spec_op_count(int he, int we, int levels, int samples, int32_t *row_nnz, void *stream);
+int ss_spec_op_fill(int he, int we, int levels, int samples, const int64_t *row_ptr, int32_t *col, float *val,
+                    void *stream);
+int ss_spec_op_register(int he, int we, int levels, int samples, const int64_t *row_ptr, const int32_t *col,
+                        const float *rval, const int64_t *col_ptr, const int32_t *row, const float *cval);
+int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const float *val,
+                  const float *base, float *specular, void *stream);
+int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row, const float *val,
+                    const double *d_specular, double *d_base, void *stream);
 
 /* ---- optimiser ------------------------------------------------------------
  * Adam.step (adam.py:21-41) fused over one parameter tensor of `count`

@@ -71,9 +71,15 @@ _SIGNATURES = {
                            ctypes.POINTER(ctypes.c_float), ctypes.c_int, c_p, c_p, ctypes.c_float, c_p, c_p, c_p],
     "ss_chain_backward": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p],
     "ss_brdf_lut": [ctypes.c_int, ctypes.c_int, c_p, c_p],
-    "ss_env_rowsums": [ctypes.c_int, ctypes.c_int, c_p, c_p],
-    "ss_env_refresh": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
-    "ss_env_adjoint": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_env_rowsums": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p],
+    "ss_env_refresh": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_env_adjoint": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
+                       c_p],
+    "ss_spec_op_count": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p],
+    "ss_spec_op_fill": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
+    "ss_spec_op_register": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_spec_apply": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_spec_apply_t": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_adam_step": [ctypes.c_int64, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_float, ctypes.c_float,
                      ctypes.c_float, ctypes.c_float, c_p],
     "ss_normalize_quats": [ctypes.c_int, c_p, c_p],

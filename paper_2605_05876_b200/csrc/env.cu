@@ -69,21 +69,34 @@ __device__ __forceinline__ void texel(int b, int he, int we, float d[3], float &
 // mode 0: rowsum_a = sum_b max(d_a.d_b,0) om_b
 // mode 1: out_a    = sum_b max(d_a.d_b,0) om_b x_b / rowsum_a          (refresh)
 // mode 2: out_b   += om_b sum_a max(d_a.d_b,0) x_a / rowsum_a          (adjoint; roles swapped)
-constexpr int kChunk = 1024;
+constexpr int kChunk = 512;   // column texels staged per pass
+constexpr int kOut = 2;       // output texels per thread (register blocking over the staged columns)
+constexpr int kDiffThreads = 128;
+constexpr int kSplit = 8;     // column range split across CTAs (fills the GPU: T outputs alone do not)
 
-template <int MODE, typename TIn, typename TOut>
-__global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const TIn *__restrict__ x,
-                                                      const float *__restrict__ rowsum, TOut *__restrict__ out) {
+template <int MODE, typename TIn>
+__global__ void __launch_bounds__(kDiffThreads) diffuse_kernel(int he, int we, const TIn *__restrict__ x,
+                                                               const float *__restrict__ rowsum,
+                                                               double *__restrict__ part) {
     __shared__ float4 sd[kChunk];   // column direction (xyz, w unused)
     __shared__ float4 sv[kChunk];   // column value rgb with its factor folded in (w unused)
     const int T = he * we;
-    const int a = blockIdx.x * blockDim.x + threadIdx.x;
-    float da[3] = {0.f, 0.f, 0.f}, oma = 0.f;
-    if (a < T) texel(a, he, we, da, oma);
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    for (int base = 0; base < T; base += kChunk) {
-        const int cn = min(kChunk, T - base);
+    const int a0 = (blockIdx.x * blockDim.x + threadIdx.x) * kOut;
+    const int per = (T + kSplit - 1) / kSplit;
+    const int b0 = blockIdx.y * per, b1 = min(T, b0 + per);
+    float da[kOut][3], oma[kOut];
+#pragma unroll
+    for (int q = 0; q < kOut; ++q) {
+        da[q][0] = da[q][1] = da[q][2] = 0.f;
+        oma[q] = 0.f;
+        if (a0 + q < T) texel(a0 + q, he, we, da[q], oma[q]);
+    }
+    float s[kOut][3];
+    double t[kOut][3];
+#pragma unroll
+    for (int q = 0; q < kOut; ++q) { s[q][0] = s[q][1] = s[q][2] = 0.f; t[q][0] = t[q][1] = t[q][2] = 0.0; }
+    for (int base = b0; base < b1; base += kChunk) {
+        const int cn = min(kChunk, b1 - base);
         __syncthreads();
         for (int k = threadIdx.x; k < cn; k += blockDim.x) {
             const int b = base + k;
@@ -93,7 +106,7 @@ __global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const TIn 
             if (MODE == 0) {
                 v.x = omb;
             } else if (MODE == 1) {
-                v = make_float4(omb * x[3 * b], omb * x[3 * b + 1], omb * x[3 * b + 2], 0.f);
+                v = make_float4(omb * (float)x[3 * b], omb * (float)x[3 * b + 1], omb * (float)x[3 * b + 2], 0.f);
             } else {
                 const double inv = 1.0 / (double)rowsum[b];
                 v = make_float4((float)(x[3 * b] * inv), (float)(x[3 * b + 1] * inv), (float)(x[3 * b + 2] * inv), 0.f);
@@ -105,24 +118,58 @@ __global__ void __launch_bounds__(256) diffuse_kernel(int he, int we, const TIn 
 #pragma unroll 4
         for (int k = 0; k < cn; ++k) {
             const float4 d = sd[k];
-            const float c = fmaxf(da[0] * d.x + da[1] * d.y + da[2] * d.z, 0.f);
             const float4 v = sv[k];
-            s0 = fmaf(c, v.x, s0);
-            if (MODE != 0) { s1 = fmaf(c, v.y, s1); s2 = fmaf(c, v.z, s2); }
+#pragma unroll
+            for (int q = 0; q < kOut; ++q) {
+                const float c = fmaxf(da[q][0] * d.x + da[q][1] * d.y + da[q][2] * d.z, 0.f);
+                s[q][0] = fmaf(c, v.x, s[q][0]);
+                if (MODE != 0) { s[q][1] = fmaf(c, v.y, s[q][1]); s[q][2] = fmaf(c, v.z, s[q][2]); }
+            }
         }
-        // flush the chunk partial into float64 (keeps the 32k-term sum accurate)
-        t0 += s0; t1 += s1; t2 += s2;
-        s0 = s1 = s2 = 0.f;
+        // flush the chunk partials into float64 (keeps the 32k-term sums accurate)
+#pragma unroll
+        for (int q = 0; q < kOut; ++q) {
+            t[q][0] += s[q][0]; t[q][1] += s[q][1]; t[q][2] += s[q][2];
+            s[q][0] = s[q][1] = s[q][2] = 0.f;
+        }
     }
-    if (a >= T) return;
+#pragma unroll
+    for (int q = 0; q < kOut; ++q) {
+        const int a = a0 + q;
+        if (a >= T) break;
+        atomicAdd(part + 3 * a, t[q][0]);
+        if (MODE != 0) { atomicAdd(part + 3 * a + 1, t[q][1]); atomicAdd(part + 3 * a + 2, t[q][2]); }
+    }
+}
+
+// mode 0: rowsum_a = part; mode 1: out_a = part / rowsum_a; mode 2: out_a += om_a part
+template <int MODE, typename TOut>
+__global__ void diffuse_finish_kernel(int he, int we, const double *__restrict__ part, const float *__restrict__ rowsum,
+                                      TOut *__restrict__ out) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= he * we) return;
     if (MODE == 0) {
-        out[a] = (TOut)t0;
+        out[a] = (TOut)part[3 * a];
     } else if (MODE == 1) {
         const double inv = 1.0 / (double)rowsum[a];
-        out[3 * a] = (TOut)(t0 * inv); out[3 * a + 1] = (TOut)(t1 * inv); out[3 * a + 2] = (TOut)(t2 * inv);
+        for (int c = 0; c < 3; ++c) out[3 * a + c] = (TOut)(part[3 * a + c] * inv);
     } else {
-        out[3 * a] += (TOut)(t0 * oma); out[3 * a + 1] += (TOut)(t1 * oma); out[3 * a + 2] += (TOut)(t2 * oma);
+        float d[3], om;
+        texel(a, he, we, d, om);
+        for (int c = 0; c < 3; ++c) out[3 * a + c] += (TOut)(part[3 * a + c] * (double)om);
     }
+}
+
+template <int MODE, typename TIn, typename TOut>
+int run_diffuse(int he, int we, const TIn *x, const float *rowsum, TOut *out, double *work, cudaStream_t st) {
+    const int T = he * we;
+    cudaMemsetAsync(work, 0, sizeof(double) * 3 * T, st);
+    const dim3 grid((T + kDiffThreads * kOut - 1) / (kDiffThreads * kOut), kSplit);
+    diffuse_kernel<MODE, TIn><<<grid, kDiffThreads, 0, st>>>(he, we, x, rowsum, work);
+    SS_CUDA_CHECK_LAUNCH();
+    diffuse_finish_kernel<MODE, TOut><<<(T + 255) / 256, 256, 0, st>>>(he, we, work, rowsum, out);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
 }
 
 struct SpecSample {
@@ -232,6 +279,109 @@ __global__ void __launch_bounds__(128) spec_adjoint_kernel(int he, int we, int l
     }
 }
 
+// ---- specular operators as a sparse matrix, built once per env shape ------
+// Row r = (l-1)*T + i holds the 4 bilinear corners of every active GGX sample
+// of texel i at level l (duplicate columns are kept: the SpMV sums them), each
+// weight already divided by the row's weight sum (shading.py:306-329); empty
+// rows hold one identity entry.
+__global__ void __launch_bounds__(128) spec_count_kernel(int he, int we, int levels, int samples,
+                                                         int32_t *__restrict__ nnz) {
+    const int T = he * we;
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lv = blockIdx.y + 1;
+    if (a >= T) return;
+    const double rough = lv / (levels - 1.0), alpha = rough * rough;
+    double d[3], tx[3], ty[3];
+    texel_frame(a, he, we, d, tx, ty);
+    int act = 0;
+    for (int s = 0; s < samples; ++s) {
+        SpecSample o;
+        double wgt;
+        act += spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt);
+    }
+    nnz[(size_t)(lv - 1) * T + a] = act ? 4 * act : 1;
+}
+
+__global__ void __launch_bounds__(128) spec_fill_kernel(int he, int we, int levels, int samples,
+                                                        const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col,
+                                                        float *__restrict__ val) {
+    const int T = he * we;
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lv = blockIdx.y + 1;
+    if (a >= T) return;
+    const double rough = lv / (levels - 1.0), alpha = rough * rough;
+    double d[3], tx[3], ty[3];
+    texel_frame(a, he, we, d, tx, ty);
+    double ws = 0.0;
+    for (int s = 0; s < samples; ++s) {
+        SpecSample o;
+        double wgt;
+        if (spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt)) ws += wgt;
+    }
+    int64_t p = row_ptr[(size_t)(lv - 1) * T + a];
+    if (ws <= 0.0) { col[p] = a; val[p] = 1.f; return; }
+    const double inv = 1.0 / ws;
+    for (int s = 0; s < samples; ++s) {
+        SpecSample o;
+        double wgt;
+        if (!spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt)) continue;
+        for (int k = 0; k < 4; ++k) { col[p] = o.idx[k]; val[p] = (float)(o.w[k] * inv); ++p; }
+    }
+}
+
+// specular[l][i] = sum_e val_e base[col_e], one warp per row (l >= 1)
+__global__ void __launch_bounds__(256) spec_apply_kernel(int T, int nrows, const int64_t *__restrict__ row_ptr,
+                                                         const int32_t *__restrict__ col, const float *__restrict__ val,
+                                                         const float *__restrict__ base, float *__restrict__ spec) {
+    const int lane = threadIdx.x & 31;
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (r >= nrows) return;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    for (int64_t p = row_ptr[r] + lane; p < row_ptr[r + 1]; p += 32) {
+        const float w = val[p];
+        const int j = col[p];
+        s0 = fmaf(w, base[3 * j], s0); s1 = fmaf(w, base[3 * j + 1], s1); s2 = fmaf(w, base[3 * j + 2], s2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+        float *out = spec + (size_t)T * 3 + (size_t)r * 3;  // level l = r / T + 1
+        out[0] = s0; out[1] = s1; out[2] = s2;
+    }
+}
+
+// d_base[j] += sum_l sum_{e in column j of S_l} val_e g_l[row_e]; the
+// transpose (CSC, per level) is the caller's stable sort of the entries by
+// (level, column); one warp per output texel.
+__global__ void __launch_bounds__(256) spec_apply_t_kernel(int T, int levels, const int64_t *__restrict__ col_ptr,
+                                                           const int32_t *__restrict__ row, const float *__restrict__ val,
+                                                           const double *__restrict__ g, double *__restrict__ d_base) {
+    const int lane = threadIdx.x & 31;
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (j >= T) return;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int lv = 1; lv < levels; ++lv) {
+        const double *gl = g + (size_t)lv * T * 3;
+        const size_t c = (size_t)(lv - 1) * T + j;
+        for (int64_t p = col_ptr[c] + lane; p < col_ptr[c + 1]; p += 32) {
+            const double w = val[p];
+            const int i = row[p];
+            s0 += w * gl[3 * i]; s1 += w * gl[3 * i + 1]; s2 += w * gl[3 * i + 2];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) { d_base[3 * j] += s0; d_base[3 * j + 1] += s1; d_base[3 * j + 2] += s2; }
+}
+
 __global__ void exp_kernel(int n, const float *__restrict__ lg, float *__restrict__ base, float *__restrict__ spec0) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -259,24 +409,50 @@ extern "C" int ss_brdf_lut(int res, int samples, float *lut, void *stream) {
     return SS_OK;
 }
 
-extern "C" int ss_env_rowsums(int he, int we, float *rowsum, void *stream) {
-    if (he < 2 || we < 2 || !rowsum) return SS_ERR_INVALID;
-    const int T = he * we;
-    diffuse_kernel<0, float, float><<<(T + 255) / 256, 256, 0, (cudaStream_t)stream>>>(he, we, nullptr, nullptr, rowsum);
-    SS_CUDA_CHECK_LAUNCH();
+extern "C" int ss_env_rowsums(int he, int we, float *rowsum, double *work, void *stream) {
+    if (he < 2 || we < 2 || !rowsum || !work) return SS_ERR_INVALID;
+    return run_diffuse<0, float, float>(he, we, nullptr, nullptr, rowsum, work, (cudaStream_t)stream);
+}
+
+extern "C" int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const float *val,
+                             const float *base, float *specular, void *stream);
+extern "C" int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row,
+                               const float *val, const double *d_specular, double *d_base, void *stream);
+
+// Registered sparse specular operator (device buffers owned by the caller).
+namespace {
+struct SpecOp {
+    int he = 0, we = 0, levels = 0, samples = 0;
+    const int64_t *row_ptr = nullptr; const int32_t *col = nullptr; const float *rval = nullptr;
+    const int64_t *col_ptr = nullptr; const int32_t *row = nullptr; const float *cval = nullptr;
+};
+SpecOp g_spec_op;
+}  // namespace
+
+extern "C" int ss_spec_op_register(int he, int we, int levels, int samples, const int64_t *row_ptr, const int32_t *col,
+                                   const float *rval, const int64_t *col_ptr, const int32_t *row, const float *cval) {
+    g_spec_op = SpecOp{he, we, levels, samples, row_ptr, col, rval, col_ptr, row, cval};
     return SS_OK;
 }
 
 extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log,
-                              const float *rowsum, float *base, float *diffuse, float *specular, void *stream) {
-    if (he < 2 || we < 2 || levels < 1 || !base_log || !rowsum || !base || !diffuse || !specular) return SS_ERR_INVALID;
+                              const float *rowsum, float *base, float *diffuse, float *specular, double *work,
+                              void *stream) {
+    if (he < 2 || we < 2 || levels < 1 || !base_log || !rowsum || !base || !diffuse || !specular || !work)
+        return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int T = he * we;
     exp_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular);
     SS_CUDA_CHECK_LAUNCH();
-    diffuse_kernel<1, float, float><<<(T + 255) / 256, 256, 0, st>>>(he, we, base, rowsum, diffuse);
-    SS_CUDA_CHECK_LAUNCH();
+    {
+        const int rc = run_diffuse<1, float, float>(he, we, base, rowsum, diffuse, work, st);
+        if (rc != SS_OK) return rc;
+    }
     if (levels > 1) {
+        if (g_spec_op.row_ptr && g_spec_op.he == he && g_spec_op.we == we && g_spec_op.levels == levels &&
+            g_spec_op.samples == samples) {
+            return ss_spec_apply(he, we, levels, g_spec_op.row_ptr, g_spec_op.col, g_spec_op.rval, base, specular, stream);
+        }
         spec_refresh_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, base, specular);
         SS_CUDA_CHECK_LAUNCH();
     }
@@ -285,19 +461,66 @@ extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const flo
 
 extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, const float *rowsum,
                               const double *d_diffuse, const double *d_specular, double *d_base, float *d_base_log,
-                              void *stream) {
-    if (he < 2 || we < 2 || levels < 1 || !base || !rowsum || !d_diffuse || !d_specular || !d_base || !d_base_log)
+                              double *work, void *stream) {
+    if (he < 2 || we < 2 || levels < 1 || !base || !rowsum || !d_diffuse || !d_specular || !d_base || !d_base_log ||
+        !work)
         return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int T = he * we;
     cudaMemsetAsync(d_base, 0, sizeof(double) * 3 * T, st);
-    diffuse_kernel<2, double, double><<<(T + 255) / 256, 256, 0, st>>>(he, we, d_diffuse, rowsum, d_base);
-    SS_CUDA_CHECK_LAUNCH();
+    {
+        const int rc = run_diffuse<2, double, double>(he, we, d_diffuse, rowsum, d_base, work, st);
+        if (rc != SS_OK) return rc;
+    }
     if (levels > 1) {
-        spec_adjoint_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, d_specular, d_base);
-        SS_CUDA_CHECK_LAUNCH();
+        if (g_spec_op.col_ptr && g_spec_op.he == he && g_spec_op.we == we && g_spec_op.levels == levels &&
+            g_spec_op.samples == samples) {
+            const int rc = ss_spec_apply_t(he, we, levels, g_spec_op.col_ptr, g_spec_op.row, g_spec_op.cval, d_specular,
+                                           d_base, stream);
+            if (rc != SS_OK) return rc;
+        } else {
+            spec_adjoint_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, d_specular,
+                                                                                  d_base);
+            SS_CUDA_CHECK_LAUNCH();
+        }
     }
     adjoint_finish_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, d_specular, base, d_base, d_base_log);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_spec_op_count(int he, int we, int levels, int samples, int32_t *row_nnz, void *stream) {
+    if (he < 2 || we < 2 || levels < 2 || samples < 1 || !row_nnz) return SS_ERR_INVALID;
+    const int T = he * we;
+    spec_count_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, (cudaStream_t)stream>>>(he, we, levels, samples, row_nnz);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_spec_op_fill(int he, int we, int levels, int samples, const int64_t *row_ptr, int32_t *col,
+                               float *val, void *stream) {
+    if (he < 2 || we < 2 || levels < 2 || samples < 1 || !row_ptr || !col || !val) return SS_ERR_INVALID;
+    const int T = he * we;
+    spec_fill_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, (cudaStream_t)stream>>>(he, we, levels, samples,
+                                                                                         row_ptr, col, val);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const float *val,
+                             const float *base, float *specular, void *stream) {
+    if (he < 2 || we < 2 || levels < 2 || !row_ptr || !col || !val || !base || !specular) return SS_ERR_INVALID;
+    const int T = he * we, nrows = (levels - 1) * T;
+    spec_apply_kernel<<<(nrows + 7) / 8, 256, 0, (cudaStream_t)stream>>>(T, nrows, row_ptr, col, val, base, specular);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row,
+                               const float *val, const double *d_specular, double *d_base, void *stream) {
+    if (he < 2 || we < 2 || levels < 2 || !col_ptr || !row || !val || !d_specular || !d_base) return SS_ERR_INVALID;
+    const int T = he * we;
+    spec_apply_t_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(T, levels, col_ptr, row, val, d_specular, d_base);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

@@ -21,6 +21,7 @@ DEFAULT_SPEC_SAMPLES = 128
 
 _LUT_CACHE = {}
 _ROWSUM_CACHE = {}
+_SPEC_OP_CACHE = {}
 
 
 def brdf_lut(res=DEFAULT_LUT_RES, samples=DEFAULT_LUT_SAMPLES):
@@ -34,14 +35,62 @@ def brdf_lut(res=DEFAULT_LUT_RES, samples=DEFAULT_LUT_SAMPLES):
     return _LUT_CACHE[key]
 
 
+_WORK_CACHE = {}
+
+
+def env_workspace(he, we):
+    """float64 scratch (3*He*We) for the split-column diffuse quadrature."""
+    key = (he, we, torch.cuda.current_device())
+    if key not in _WORK_CACHE:
+        _WORK_CACHE[key] = torch.empty(3 * he * we, device="cuda", dtype=torch.float64)
+    return _WORK_CACHE[key]
+
+
 def diffuse_rowsums(he, we):
     key = (he, we, torch.cuda.current_device())
     if key not in _ROWSUM_CACHE:
         lib = _lib.load()
         rs = torch.empty(he * we, device="cuda", dtype=torch.float32)
-        _lib.check(lib.ss_env_rowsums(he, we, _lib.ptr(rs), _lib.stream_ptr()), "ss_env_rowsums")
+        _lib.check(lib.ss_env_rowsums(he, we, _lib.ptr(rs), _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()),
+                   "ss_env_rowsums")
         _ROWSUM_CACHE[key] = rs
     return _ROWSUM_CACHE[key]
+
+
+def spec_operator(he, we, levels, samples):
+    """Sparse specular prefilter operators (CSR + per-level CSC), built once per
+    shape on the device and registered with the library, which then uses them
+    in ss_env_refresh / ss_env_adjoint."""
+    key = (he, we, levels, samples, torch.cuda.current_device())
+    if levels < 2:
+        return None
+    if key not in _SPEC_OP_CACHE:
+        lib = _lib.load()
+        T = he * we
+        nrows = (levels - 1) * T
+        dev = "cuda"
+        nnz = torch.empty(nrows, device=dev, dtype=torch.int32)
+        _lib.check(lib.ss_spec_op_count(he, we, levels, samples, _lib.ptr(nnz), _lib.stream_ptr()), "ss_spec_op_count")
+        row_ptr = torch.zeros(nrows + 1, device=dev, dtype=torch.int64)
+        row_ptr[1:] = torch.cumsum(nnz.to(torch.int64), 0)
+        total = int(row_ptr[-1].item())
+        col = torch.empty(total, device=dev, dtype=torch.int32)
+        rval = torch.empty(total, device=dev, dtype=torch.float32)
+        _lib.check(lib.ss_spec_op_fill(he, we, levels, samples, _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(rval),
+                                       _lib.stream_ptr()), "ss_spec_op_fill")
+        rows = torch.repeat_interleave(torch.arange(nrows, device=dev, dtype=torch.int64), nnz.to(torch.int64))
+        level = rows // T
+        key_c = level * T + col.to(torch.int64)
+        order = torch.sort(key_c, stable=True).indices
+        row_t = (rows[order] % T).to(torch.int32).contiguous()
+        cval = rval[order].contiguous()
+        col_ptr = torch.zeros(nrows + 1, device=dev, dtype=torch.int64)
+        col_ptr[1:] = torch.cumsum(torch.bincount(key_c, minlength=nrows), 0)
+        op = (row_ptr, col, rval, col_ptr, row_t, cval)
+        _SPEC_OP_CACHE[key] = op
+    op = _SPEC_OP_CACHE[key]
+    _lib.load().ss_spec_op_register(he, we, levels, samples, *(_lib.ptr(t) for t in op))
+    return op
 
 
 class EnvironmentLight:
@@ -80,9 +129,10 @@ class EnvironmentLight:
         lib = _lib.load()
         he, we = self.shape
         rs = diffuse_rowsums(he, we)
+        spec_operator(he, we, self.levels, self.spec_samples)
         _lib.check(lib.ss_env_refresh(he, we, self.levels, self.spec_samples, _lib.ptr(self.base_log), _lib.ptr(rs),
                                       _lib.ptr(self.base), _lib.ptr(self.diffuse), _lib.ptr(self.specular),
-                                      _lib.stream_ptr()), "ss_env_refresh")
+                                      _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()), "ss_env_refresh")
 
     def env_gradient(self, d_diffuse, d_specular):
         """Derived-map gradients -> (d_base, d_base_log) (shading.py:381-394)."""
@@ -94,10 +144,12 @@ class EnvironmentLight:
         ds = torch.as_tensor(d_specular, **f64).contiguous() if d_specular is not None \
             else torch.zeros(self.specular.shape, **f64)
         d_base = torch.empty(self.base.shape, **f64)
+        spec_operator(he, we, self.levels, self.spec_samples)
         d_log = torch.empty_like(self.base)
         _lib.check(lib.ss_env_adjoint(he, we, self.levels, self.spec_samples, _lib.ptr(self.base),
                                       _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(dd), _lib.ptr(ds),
-                                      _lib.ptr(d_base), _lib.ptr(d_log), _lib.stream_ptr()), "ss_env_adjoint")
+                                      _lib.ptr(d_base), _lib.ptr(d_log), _lib.ptr(env_workspace(he, we)),
+                                      _lib.stream_ptr()), "ss_env_adjoint")
         return d_base, d_log
 
     @staticmethod

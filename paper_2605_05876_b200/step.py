@@ -128,7 +128,7 @@ class TrainStep:
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
         self._stage = None
         self.launches_per_view = 9     # preprocess, scan, scatter, tile sort, train fwd, ndc + record bwd x2, chain
-        self.launches_per_step_fixed = 3 + 7 + 1 + 3  # env adjoint, Adam x7, quat renorm, env refresh
+        self.launches_per_step_fixed = 4 + 7 + 1 + 4  # env adjoint, Adam x7, quat renorm, env refresh
 
     # -- buffers -----------------------------------------------------------
     def _alloc_pairs(self, cap):
@@ -233,11 +233,12 @@ class TrainStep:
 
     def _finish(self):
         he, we = self.env.shape
-        from .shading import diffuse_rowsums
+        from .shading import diffuse_rowsums, env_workspace, spec_operator
+        spec_operator(he, we, self.env.levels, self.env.spec_samples)
         _lib.check(self.lib.ss_env_adjoint(he, we, self.env.levels, self.env.spec_samples, _lib.ptr(self.env.base),
                                            _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(self.d_diffuse),
                                            _lib.ptr(self.d_spec), _lib.ptr(self.d_base), _lib.ptr(self.g_env_log),
-                                           _lib.stream_ptr()), "ss_env_adjoint")
+                                           _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()), "ss_env_adjoint")
         self.loss_f.copy_(self.loss)
         self.pack.all_reduce(self.pg)
 
