@@ -70,9 +70,39 @@ class GradPack:
             dist.all_reduce(self.touched, group=group)
 
 
+class ViewBuffers:
+    """Device scratch of one in-flight view (records, pair lists, per-pixel
+    training planes, record accumulator).  TrainStep keeps one set per stream
+    so consecutive views overlap on the GPU."""
+
+    def __init__(self, n, W, H, tile, k_max, ntiles, device):
+        f32 = dict(device=device, dtype=torch.float32)
+        i32 = dict(device=device, dtype=torch.int32)
+        self.records = torch.empty((n, _lib.REC_FLOATS), **f32)
+        self.cull = torch.empty(n, device=device, dtype=torch.int8)
+        self.tile_counts = torch.zeros(ntiles, **i32)
+        self.flags = torch.zeros(4, **i32)
+        self.offsets = torch.empty(ntiles + 1, **i32)
+        self.cursors = torch.empty(ntiles, **i32)
+        self.coef = torch.empty((k_max, H * W, 4), **f32)
+        self.thr = torch.empty((k_max, H * W), **f32)
+        self.pix_hdr = torch.empty((H * W, 4), **i32)
+        self.pixel_ndc = torch.empty(W + H + 1 + n, **f32)  # NDC tables + big-rect queue
+        self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
+        self.capacity = 0
+        self.keys = self.pair = self.pair_rect = None
+
+    def alloc_pairs(self, cap):
+        dev = self.records.device
+        self.keys = torch.empty(cap, device=dev, dtype=torch.int64)
+        self.pair = torch.empty(cap, device=dev, dtype=torch.int32)
+        self.pair_rect = torch.empty((cap, 2), device=dev, dtype=torch.int32)
+        self.capacity = cap
+
+
 class TrainStep:
     def __init__(self, cloud, env, width, height, k_max=16, tile=16, background=(0.0, 0.0, 0.0),
-                 lrs=None, pair_capacity=None, process_group=None, options=None):
+                 lrs=None, pair_capacity=None, process_group=None, options=None, streams=2):
         self.lib = _lib.load()
         self.cloud, self.env = cloud, env
         self.W, self.H, self.k_max, self.tile = int(width), int(height), int(k_max), int(tile)
@@ -86,19 +116,8 @@ class TrainStep:
         self.n = n
         self.ntx = (self.W + tile - 1) // tile
         self.ntiles = self.ntx * ((self.H + tile - 1) // tile)
-        f32 = dict(device=dev, dtype=torch.float32)
-        i32 = dict(device=dev, dtype=torch.int32)
-        self.records = torch.empty((n, _lib.REC_FLOATS), **f32)
-        self.cull = torch.empty(n, device=dev, dtype=torch.int8)
-        self.tile_counts = torch.zeros(self.ntiles, **i32)
-        self.flags = torch.zeros(4, **i32)
-        self.offsets = torch.empty(self.ntiles + 1, **i32)
-        self.cursors = torch.empty(self.ntiles, **i32)
-        self.coef = torch.empty((self.k_max, self.H * self.W, 4), **f32)
-        self.thr = torch.empty((self.k_max, self.H * self.W), **f32)
-        self.pix_hdr = torch.empty((self.H * self.W, 4), **i32)
-        self.pixel_ndc = torch.empty(self.W + self.H + 1 + n, **f32)  # NDC tables + big-rect queue
-        self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
+        self.bufs = [ViewBuffers(n, self.W, self.H, tile, self.k_max, self.ntiles, dev) for _ in range(max(1, streams))]
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(len(self.bufs))]
         he, we = env.shape
         self.T = he * we
         # packed gradient buffer: params, ss_grad, env d_base_log, loss -- one all-reduce
@@ -120,7 +139,6 @@ class TrainStep:
                                 _lib.ptr(self.touched), _lib.ptr(self.d_diffuse), _lib.ptr(self.d_spec))
         self._bg = _lib.fvec(self.bg)
         self.capacity = 0
-        self.keys = self.pair = None
         if pair_capacity:
             self._alloc_pairs(pair_capacity)
         self.collect_stats = False
@@ -133,66 +151,97 @@ class TrainStep:
     # -- buffers -----------------------------------------------------------
     def _alloc_pairs(self, cap):
         cap = int(cap)
-        dev = self.records.device
-        self.keys = torch.empty(cap, device=dev, dtype=torch.int64)
-        self.pair = torch.empty(cap, device=dev, dtype=torch.int32)
-        self.pair_rect = torch.empty((cap, 2), device=dev, dtype=torch.int32)
+        for b in self.bufs:
+            b.alloc_pairs(cap)
         self.capacity = cap
 
     def size_pairs(self, cameras, slack=1.5):
         """Measure the pair count of a few views (host sync) and size buffers."""
         worst = 0
+        b = self.bufs[0]
         for cam in cameras:
-            self._preprocess(cam)
-            worst = max(worst, int(self.tile_counts.sum().item()))
+            self._preprocess(cam, b)
+            worst = max(worst, int(b.tile_counts.sum().item()))
         self._alloc_pairs(max(int(worst * slack), 1024))
         return worst
 
     def check_overflow(self):
-        return bool(self.flags[2].item())
+        return any(bool(b.flags[2].item()) for b in self.bufs)
 
     # -- per-view stages ----------------------------------------------------
-    def _preprocess(self, cam):
-        self.tile_counts.zero_()
+    def _preprocess(self, cam, b):
+        b.tile_counts.zero_()
         camst = _lib.make_camera(cam)
         rc = self.lib.ss_preprocess(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
-                                    _lib.SS_COLOR_IBL, None, ctypes.byref(self._envs), _lib.ptr(self.records),
-                                    _lib.ptr(self.cull), None, _lib.ptr(self.tile_counts), None,
-                                    _lib.ptr(self.flags), _lib.stream_ptr())
+                                    _lib.SS_COLOR_IBL, None, ctypes.byref(self._envs), _lib.ptr(b.records),
+                                    _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts), None,
+                                    _lib.ptr(b.flags), _lib.stream_ptr())
         _lib.check(rc, "ss_preprocess")
         return camst
 
-    def view(self, cam, target):
-        """Forward + backward of one view; gradients accumulate into self.grads."""
+    def view(self, cam, target, b=None, chain_after=None, target_done=None):
+        """Forward + backward of one view on the CURRENT stream with buffer set
+        b; gradients accumulate into self.grads.  chain_after: event the chain
+        kernel must wait for (the previous view's chain, which updates the same
+        gradient buffers); target_done: event recorded once `target` is consumed.
+        Returns the event recorded after this view's chain kernel."""
         lib = self.lib
+        b = b if b is not None else self.bufs[0]
         s = _lib.stream_ptr()
-        camst = self._preprocess(cam)
-        _lib.check(lib.ss_bin_sort(self.n, _lib.ptr(self.records), _lib.ptr(self.cull), self.W, self.H, self.tile,
-                                   _lib.ptr(self.tile_counts), _lib.ptr(self.offsets), _lib.ptr(self.cursors),
-                                   _lib.ptr(self.keys), _lib.ptr(self.pair), _lib.ptr(self.pair_rect), self.capacity,
-                                   _lib.ptr(self.flags), s),
+        camst = self._preprocess(cam, b)
+        _lib.check(lib.ss_bin_sort(self.n, _lib.ptr(b.records), _lib.ptr(b.cull), self.W, self.H, self.tile,
+                                   _lib.ptr(b.tile_counts), _lib.ptr(b.offsets), _lib.ptr(b.cursors),
+                                   _lib.ptr(b.keys), _lib.ptr(b.pair), _lib.ptr(b.pair_rect), b.capacity,
+                                   _lib.ptr(b.flags), s),
                    "ss_bin_sort")
         ev = self._ev_begin("train_forward")
-        _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(self.offsets), _lib.ptr(self.pair),
-                                        _lib.ptr(self.pair_rect), _lib.ptr(self.records), self._bg[0], self.k_max,
-                                        _lib.ptr(target), _lib.ptr(self.coef), _lib.ptr(self.thr), _lib.ptr(self.pix_hdr),
+        _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
+                                        _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
+                                        _lib.ptr(target), _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr),
                                         _lib.ptr(self.loss), None, s), "ss_train_forward")
         self._ev_end(ev)
+        if target_done is not None:
+            target_done.record()
         ev = self._ev_begin("train_backward")
-        _lib.check(lib.ss_train_backward_records(self.n, _lib.ptr(self.cull), _lib.ptr(self.records), self.W,
-                                                 self.H, self.k_max, _lib.ptr(self.coef), _lib.ptr(self.thr),
-                                                 _lib.ptr(self.pix_hdr), _lib.ptr(self.pixel_ndc), _lib.ptr(self.acc), s),
+        _lib.check(lib.ss_train_backward_records(self.n, _lib.ptr(b.cull), _lib.ptr(b.records), self.W,
+                                                 self.H, self.k_max, _lib.ptr(b.coef), _lib.ptr(b.thr),
+                                                 _lib.ptr(b.pix_hdr), _lib.ptr(b.pixel_ndc), _lib.ptr(b.acc), s),
                    "ss_train_backward_records")
         self._ev_end(ev)
+        if chain_after is not None:
+            torch.cuda.current_stream().wait_event(chain_after)
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
-                                         _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(self.cull),
-                                         _lib.ptr(self.acc), ctypes.byref(self._gs), s), "ss_chain_backward")
+                                         _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(b.cull),
+                                         _lib.ptr(b.acc), ctypes.byref(self._gs), s), "ss_chain_backward")
+        done = torch.cuda.Event()
+        done.record()
+        return done
+
+    def _run_views(self, cameras, targets_for, target_done=None):
+        """Issue every view, alternating the worker streams (view i uses stream
+        and buffers i % S); the chain kernels are serialised by events."""
+        main = torch.cuda.current_stream()
+        for st in self.streams:
+            st.wait_stream(main)
+        prev = None
+        for i, cam in enumerate(cameras):
+            k = i % len(self.streams)
+            with torch.cuda.stream(self.streams[k]):
+                tgt = targets_for(i, self.streams[k])
+                prev = self.view(cam, tgt, self.bufs[k], chain_after=prev,
+                                 target_done=None if target_done is None else target_done[i % 2])
+                if self.collect_stats:
+                    b = self.bufs[k]
+                    self._pairs.append(int(b.offsets[-1].item()))
+                    self._kept.append(int((b.cull == 0).sum().item()))
+        for st in self.streams:
+            main.wait_stream(st)
 
     def _ev_begin(self, name):
         if self.kernel_events is None:
             return None
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        a.record()  # on the current (worker) stream
         return (name, a, b)
 
     def _ev_end(self, ev):
@@ -215,7 +264,8 @@ class TrainStep:
         self.d_diffuse.zero_()
         self.d_spec.zero_()
         self.loss.zero_()
-        self.flags.zero_()
+        for b in self.bufs:
+            b.flags.zero_()
 
     def gradients(self, cameras, targets):
         """Sum of per-view gradients over this rank's views (+ env adjoint)."""
@@ -224,11 +274,7 @@ class TrainStep:
         self.zero()
         self._nviews = len(cameras)
         self._pairs, self._kept = [], []
-        for cam, tgt in zip(cameras, targets):
-            self.view(cam, tgt)
-            if self.collect_stats:
-                self._pairs.append(int(self.offsets[-1].item()))
-                self._kept.append(int((self.cull == 0).sum().item()))
+        self._run_views(cameras, lambda i, st: targets[i])
         self._finish()
 
     def _finish(self):
@@ -263,31 +309,34 @@ class TrainStep:
         previous view's kernels."""
         if self.capacity == 0:
             self.size_pairs(cameras[:2])
-        compute = torch.cuda.current_stream()
         if self._stage is None:
-            self._stage = [torch.empty((self.H, self.W, 3), device=self.records.device, dtype=torch.float32)
+            self._stage = [torch.empty((self.H, self.W, 3), device=self.pack.flat.device, dtype=torch.float32)
                            for _ in range(2)]
             self._copy = torch.cuda.Stream()
         ready = [torch.cuda.Event(), torch.cuda.Event()]
         free = [torch.cuda.Event(), torch.cuda.Event()]
+        main = torch.cuda.current_stream()
+        self._copy.wait_stream(main)
 
         def issue(i):
-            b = i % 2
+            k = i % 2
             with torch.cuda.stream(self._copy):
                 if i >= 2:
-                    self._copy.wait_event(free[b])
-                self._stage[b].copy_(host_targets[i], non_blocking=True)
-                ready[b].record(self._copy)
+                    self._copy.wait_event(free[k])
+                self._stage[k].copy_(host_targets[i], non_blocking=True)
+                ready[k].record(self._copy)
+
+        def target_for(i, stream):
+            # view i's target is copied while the previous view computes
+            if i + 1 < len(cameras):
+                issue(i + 1)
+            stream.wait_event(ready[i % 2])
+            return self._stage[i % 2]
 
         self.zero()
         self._nviews = len(cameras)
         issue(0)
-        for i, cam in enumerate(cameras):
-            if i + 1 < len(cameras):
-                issue(i + 1)
-            compute.wait_event(ready[i % 2])
-            self.view(cam, self._stage[i % 2])
-            free[i % 2].record(compute)
+        self._run_views(cameras, target_for, target_done=free)
         self._finish()
         self.apply()
         return self.loss_f
