@@ -52,12 +52,13 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
     const int ky = (int)(((float)k + 0.5f) * inv_rw);
     const int iy = R.r.y + ky, ix = R.r.x + (k - ky * rw);
     const float x = __ldg(P.xs + ix), y = __ldg(P.ys + iy);
-    Cover c;
-    if (!ss_cover(x, y, R, c)) return 0;
+    // the packed header and the (most common) layer-0 coefficients are loaded
+    // speculatively, before the coverage test, so their latency hides behind it
     const size_t pix = (size_t)iy * P.W + ix;
-    // packed header and the (most common) layer-0 coefficients in parallel
     const int4 h = __ldg(P.hdr + pix);
     const float4 cf0 = __ldg(P.coef + pix);
+    Cover c;
+    if (!ss_cover(x, y, R, c)) return 0;
     const float zs = R.d.z;
     const int nc = h.x;
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
@@ -112,16 +113,28 @@ __global__ void __launch_bounds__(256, 3) splat_bwd_kernel(SplatParams P, int32_
     const bool owner = (__ffs(same) - 1) == lane;
 
     SsRecord &R = s_rec[threadIdx.x >> 5];
-    for (int rec = gwarp; rec < P.n; rec += nwarps) {
-        if (P.cull[rec] != 0) continue;  // warp-uniform
+    // software pipeline over the warp's records: the cull flag two records
+    // ahead and the next kept record's 96 bytes (lanes 0-5) are in flight
+    // while the current one is processed
+    auto next_kept = [&](int r) {
+        while (r < P.n && P.cull[r] != 0) r += nwarps;
+        return r;
+    };
+    int rec = next_kept(gwarp);
+    float4 nxt = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rec < P.n && lane < 6) nxt = __ldg(reinterpret_cast<const float4 *>(P.records + rec) + lane);
+    for (; rec < P.n;) {
         __syncwarp();
-        if (lane < 6) reinterpret_cast<float4 *>(&R)[lane] = __ldg(reinterpret_cast<const float4 *>(P.records + rec) + lane);
+        if (lane < 6) reinterpret_cast<float4 *>(&R)[lane] = nxt;
+        const int cur = rec;
+        rec = next_kept(rec + nwarps);
+        if (rec < P.n && lane < 6) nxt = __ldg(reinterpret_cast<const float4 *>(P.records + rec) + lane);
         __syncwarp();
         const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
-        float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
+        float *dst = P.acc + (size_t)cur * SS_ACC_FLOATS;
         if (area > kBigArea) {
             if (lane < SS_ACC_FLOATS) dst[lane] = 0.f;
-            if (lane == 0) big_list[atomicAdd(big_count, 1)] = rec;
+            if (lane == 0) big_list[atomicAdd(big_count, 1)] = cur;
             continue;
         }
         const float inv_rw = 1.f / (float)rw;
