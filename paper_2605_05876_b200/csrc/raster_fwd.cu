@@ -55,7 +55,7 @@ constexpr int kFwdWarps = 2;
 template <bool kExtras, bool kTrain>
 __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 {
-    __shared__ SsRecord wbuf_all[kFwdWarps][32];
+    __shared__ PackedScratch scratch[kFwdWarps];
     const int ctas_per_tile = P.tile * P.tile / (32 * kFwdWarps);
     const int t = blockIdx.x / ctas_per_tile;
     const int wid_in_tile = (blockIdx.x % ctas_per_tile) * kFwdWarps + (threadIdx.x >> 5);
@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     const int lane = wp.lane, wid = threadIdx.x >> 5;
     const bool live = wp.live;
     const size_t pix = wp.pix;
-    SsRecord *wbuf = wbuf_all[wid];
+    PackedScratch &sm = scratch[wid];
+    packed_init(wp, sm, P.W, P.H);
 
     float Wg = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Zg = 0.f, Z2g = 0.f, zmax = 0.f;
     float T = 1.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, dnum = 0.f, dden = 0.f;
@@ -100,40 +101,35 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     for (int cb = p0; cb < p1; cb += 32 * 8) {
         if (!kExtras && __all_sync(0xffffffffu, stopped)) break;
         const int ce = min(p1, cb + 32 * 8);
-        walk_tile(wp, cb, ce, P.pair_rec, P.pair_rect, P.records, wbuf, [&](const SsRecord &R, int pidx, int) {
-            bool cov = false;
-            if (in_rect(wp, R.r)) {
-                if (stopped) {
-                    ++discarded;
-                } else {
-                    bool go = true;
-                    if (Wg > 0.f && R.d.z > zmax) {
-                        if (kTrain) {
-                            if (ncl == 0) th0 = zmax;
-                            else if (ncl == 1) th1 = zmax;
-                            else if (ncl == 2) th2 = zmax;
-                            else P.thr[(size_t)ncl * P.W * P.H + pix] = zmax;
-                        }
-                        ++ncl;
-                        close_layer();  // rasterizer.py:168-196
-                        if (layers >= P.k_max) { stopped = true; ++discarded; go = false; }
-                    }
-                    Cover c;
-                    if (go && ss_cover(wp.x, wp.y, R, c)) {
-                        cov = true;
-                        const float w = R.d.x * __expf(-0.5f * c.rho2);
-                        const float z = R.d.y;
-                        Wg += w;
-                        C0 += w * R.e.x; C1 += w * R.e.y; C2 += w * R.e.z;
-                        if (!kTrain) { Zg += w * z; Z2g += w * z * z; }
-                        ++members;
-                        if (R.d.w > zmax) zmax = R.d.w;
-                    }
-                }
+        walk_tile_packed(wp, cb, ce, P.pair_rec, P.pair_rect, P.records, sm, kExtras ? P.pair_cover : nullptr,
+            [](const RecGeo &R, float x, float y) {
+                Cover c;
+                return ss_cover(x, y, R, c) ? R.d.x * __expf(-0.5f * c.rho2) : -1.f;
+            },
+            [&](const SlotView &v) {
+            if (stopped) {
+                ++discarded;
+                return;
             }
-            if (kExtras && P.pair_cover) {
-                const unsigned cm = __ballot_sync(0xffffffffu, cov);
-                if (cm && lane == 0) atomicAdd(&P.pair_cover[pidx], __popc(cm));
+            if (Wg > 0.f && v.zs > zmax) {
+                if (kTrain) {
+                    if (ncl == 0) th0 = zmax;
+                    else if (ncl == 1) th1 = zmax;
+                    else if (ncl == 2) th2 = zmax;
+                    else P.thr[(size_t)ncl * P.W * P.H + pix] = zmax;
+                }
+                ++ncl;
+                close_layer();  // rasterizer.py:168-196
+                if (layers >= P.k_max) { stopped = true; ++discarded; return; }
+            }
+            if (v.w >= 0.f) {
+                const float w = v.w;
+                Wg += w;
+                C0 += w * v.c0; C1 += w * v.c1; C2 += w * v.c2;
+                if (!kTrain) { Zg += w * v.vz; Z2g += w * v.vz * v.vz; }
+                ++members;
+                if (v.ze > zmax) zmax = v.ze;
+                if (kExtras && P.pair_cover) atomicAdd(&sm.ncov[v.slot], 1);
             }
         });
     }

@@ -74,6 +74,139 @@ __device__ __forceinline__ void walk_tile(const WarpPix &w, int p0, int p1, cons
     }
 }
 
+// Per-warp shared scratch of the packed walk: the chunk's overlapping records
+// (compacted, list order; the 64 bytes coverage needs), the per-slot fields
+// the compositing reads (SoA: lanes on different slots hit different banks),
+// the per (slot, pixel) weights and the per-pixel slot masks.
+struct RecGeo {
+    float4 a, b, c, d;    // the first 64 bytes of SsRecord
+};
+
+struct PackedScratch {
+    RecGeo geo[32];       // t1, t2, t4, Sigma^-1, n_f, view_z, z_start, z_end
+    float wgt[32][32];    // [slot][pixel]: n_f exp(-rho^2/2) when covered, -1 when not (in-rect only)
+    unsigned mask[32];    // per pixel: slots whose rect contains it
+    float zs[32], ze[32], vz[32], c0[32], c1[32], c2[32];
+    int meta[32];         // in-block rect: cx0 | cw << 4 | ry0 << 8 | cnt << 12
+    int pidx[32];
+    int ncov[32];         // covered lanes per slot (pair cover counts)
+    float xs[8], ys[4];
+};
+
+// What the compositing of one (slot, pixel) sees.
+struct SlotView {
+    float w;              // >= 0 covered (the weight), < 0 in rect but not covered
+    float zs, ze, vz, c0, c1, c2;
+    int slot;
+};
+
+__device__ __forceinline__ void packed_init(const WarpPix &w, PackedScratch &sm, int W, int H) {
+    if (w.lane < 8) sm.xs[w.lane] = ss_ndc_x(w.bx + w.lane, W);
+    if (w.lane < 4) sm.ys[w.lane] = ss_ndc_y(w.by + w.lane, H);
+    sm.mask[w.lane] = 0u;
+    sm.ncov[w.lane] = 0;
+    __syncwarp();
+}
+
+// Two-phase walk of the tile's sorted pair list [p0, p1) for one 8x4 warp
+// block.  Per 32-pair chunk the overlapping records are gathered (compacted,
+// list order) into the warp's shared scratch; phase 1 evaluates coverage and
+// weight for every in-rect (record, pixel) item with ONE item per lane (items
+// packed across records, so no lane idles outside a record's rect) and marks
+// the slot in the pixel's mask; phase 2 lets every lane walk only ITS pixel's
+// in-rect slots, in list order, calling f(SlotView) -- the order-dependent
+// compositing costs max-over-lanes of the in-rect count instead of the number
+// of overlapping records.
+template <typename Wt, typename F>
+__device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p1, const int32_t *__restrict__ pair_rec,
+                                                 const uint2 *__restrict__ pair_rect,
+                                                 const SsRecord *__restrict__ recs, PackedScratch &sm,
+                                                 int32_t *pair_cover, Wt &&weight, F &&f) {
+    const unsigned FULL = 0xffffffffu;
+    const unsigned lt = (1u << w.lane) - 1u;
+    for (int base = p0; base < p1; base += 32) {
+        const int p = base + w.lane;
+        bool ov = false;
+        int meta = 0;
+        if (p < p1) {
+            const uint2 pr = __ldg(pair_rect + p);
+            const int x0 = pr.x & 0xffff, y0 = pr.x >> 16, x1 = pr.y & 0xffff, y1 = pr.y >> 16;
+            ov = x0 < w.bx + 8 && x1 > w.bx && y0 < w.by + 4 && y1 > w.by;
+            const int cx0 = max(x0 - w.bx, 0), cw = min(x1 - w.bx, 8) - cx0;
+            const int ry0 = max(y0 - w.by, 0), ch = min(y1 - w.by, 4) - ry0;
+            meta = cx0 | (cw << 4) | (ry0 << 8) | ((cw * ch) << 12);
+        }
+        const unsigned ovm = __ballot_sync(FULL, ov);
+        if (ovm == 0u) continue;
+        const int n = __popc(ovm);
+        const int pos = __popc(ovm & lt);
+        if (ov) {
+            const int rec = __ldg(pair_rec + p);
+            const float4 *src = reinterpret_cast<const float4 *>(recs + rec);
+            const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3),
+                         e = __ldg(src + 4);
+            sm.geo[pos].a = a; sm.geo[pos].b = b; sm.geo[pos].c = c; sm.geo[pos].d = d;
+            sm.zs[pos] = d.z; sm.ze[pos] = d.w; sm.vz[pos] = d.y;
+            sm.c0[pos] = e.x; sm.c1[pos] = e.y; sm.c2[pos] = e.z;
+            sm.meta[pos] = meta;
+            sm.pidx[pos] = p;
+        }
+        __syncwarp();
+        // phase 1: inclusive scan of the per-slot item counts, then packed items
+        const int my_meta = w.lane < n ? sm.meta[w.lane] : 0;
+        const int cnt = my_meta >> 12;
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (w.lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(FULL, incl, 31);
+        // geometry | slot's first item << 12 | magic(cw) << 23, where
+        // (k * magic) >> 8 == k / cw for k < 32 (magic = ceil(256 / cw))
+        const unsigned cwm = (my_meta >> 4) & 15;
+        const unsigned magic = cwm ? (unsigned)((0x1F242A333F557FFFull >> ((cwm - 1) * 8)) & 0xFF) + 1u : 0u;
+        const unsigned packed = (unsigned)(my_meta & 0xfff) | ((unsigned)(incl - cnt) << 12) | (magic << 23);
+        for (int b0 = 0; b0 < total; b0 += 32) {
+            const bool bnd = w.lane < n && incl > b0 && incl < b0 + 32;
+            const unsigned B = __reduce_or_sync(FULL, bnd ? (1u << (incl - b0)) : 0u);
+            const int j0 = __popc(__ballot_sync(FULL, w.lane < n && incl <= b0));
+            const int s = min(j0 + __popc(B & ((2u << w.lane) - 1u)), 31);
+            const unsigned pk = __shfl_sync(FULL, packed, s);
+            const int i = b0 + w.lane;
+            if (i < total) {
+                const int k = i - (int)((pk >> 12) & 0x7ff);
+                const int cx0 = pk & 15, cw = (pk >> 4) & 15, ry0 = (pk >> 8) & 15;
+                const int row = (k * (int)(pk >> 23)) >> 8;
+                const int col = k - row * cw;
+                const int px = (ry0 + row) * 8 + cx0 + col;
+                sm.wgt[s][px] = weight(sm.geo[s], sm.xs[px & 7], sm.ys[px >> 3]);
+                atomicOr(&sm.mask[px], 1u << s);
+            }
+        }
+        __syncwarp();
+        // phase 2: each lane walks its own pixel's in-rect slots in list order
+        unsigned M = sm.mask[w.lane];
+        sm.mask[w.lane] = 0u;
+        while (__any_sync(FULL, M != 0u)) {
+            if (M != 0u) {
+                SlotView v;
+                v.slot = __ffs(M) - 1;
+                M &= M - 1u;
+                v.w = sm.wgt[v.slot][w.lane];
+                v.zs = sm.zs[v.slot]; v.ze = sm.ze[v.slot]; v.vz = sm.vz[v.slot];
+                v.c0 = sm.c0[v.slot]; v.c1 = sm.c1[v.slot]; v.c2 = sm.c2[v.slot];
+                f(v);
+            }
+        }
+        __syncwarp();
+        if (pair_cover && w.lane < n && sm.ncov[w.lane] > 0) {  // f counted covered lanes per slot
+            atomicAdd(&pair_cover[sm.pidx[w.lane]], sm.ncov[w.lane]);
+            sm.ncov[w.lane] = 0;
+        }
+    }
+}
+
 // Coverage of pixel (x, y) by a record, with everything downstream.
 // k, l, den and the two numerators are evaluated with the reference's exact
 // float32 operation sequence (no contraction), so they are bit-identical to
@@ -88,7 +221,8 @@ struct Cover {
     float k0, k1, k2, l0, l1, l2, den, inv_den, u, v, rho2;
 };
 
-__device__ __forceinline__ bool ss_cover(float x, float y, const SsRecord &R, Cover &c) {
+template <typename Rec>
+__device__ __forceinline__ bool ss_cover(float x, float y, const Rec &R, Cover &c) {
     const float t1x = R.a.x, t1y = R.a.y, t1z = R.a.z, t2x = R.a.w, t2y = R.b.x, t2z = R.b.y;
     const float t4x = R.b.z, t4y = R.b.w, t4z = R.c.x;
     c.k0 = fs(fm(x, t4x), t1x);

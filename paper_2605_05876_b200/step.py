@@ -188,12 +188,16 @@ class TrainStep:
         lib = self.lib
         b = b if b is not None else self.bufs[0]
         s = _lib.stream_ptr()
+        ev = self._ev_begin("preprocess")
         camst = self._preprocess(cam, b)
+        self._ev_end(ev)
+        ev = self._ev_begin("bin_sort")
         _lib.check(lib.ss_bin_sort(self.n, _lib.ptr(b.records), _lib.ptr(b.cull), self.W, self.H, self.tile,
                                    _lib.ptr(b.tile_counts), _lib.ptr(b.offsets), _lib.ptr(b.cursors),
                                    _lib.ptr(b.keys), _lib.ptr(b.pair), _lib.ptr(b.pair_rect), b.capacity,
                                    _lib.ptr(b.flags), s),
                    "ss_bin_sort")
+        self._ev_end(ev)
         ev = self._ev_begin("train_forward")
         _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
                                         _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
@@ -210,9 +214,11 @@ class TrainStep:
         self._ev_end(ev)
         if chain_after is not None:
             torch.cuda.current_stream().wait_event(chain_after)
+        ev = self._ev_begin("chain")
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                          _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(b.cull),
                                          _lib.ptr(b.acc), ctypes.byref(self._gs), s), "ss_chain_backward")
+        self._ev_end(ev)
         done = torch.cuda.Event()
         done.record()
         return done
