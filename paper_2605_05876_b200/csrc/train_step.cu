@@ -44,21 +44,22 @@ __global__ void pixel_ndc_kernel(int W, int H, float *xs, float *ys, int32_t *bi
     if (k == 0) *big_count = 0;
 }
 
-// Gradient contribution of record R at pixel k (row-major inside its rect),
-// accumulated into g[]; returns 1 when the pixel counts as touched.
-__device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &R, int k, int rw, float inv_rw,
-                                          float g[NCH]) {
+// Gradient of the covered item (pixel ix, iy of record R) with the coverage
+// quantities u, v, rho^2 of the coverage pass, accumulated into g[].
+// Returns 1 when the record reaches the pixel before the K_MAX stop.
+__device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R, int ix, int iy, float u, float v,
+                                         float rho2, float g[NCH]) {
     const size_t HW = (size_t)P.W * P.H;
-    const int ky = (int)(((float)k + 0.5f) * inv_rw);
-    const int iy = R.r.y + ky, ix = R.r.x + (k - ky * rw);
     const float x = __ldg(P.xs + ix), y = __ldg(P.ys + iy);
-    // the packed header and the (most common) layer-0 coefficients are loaded
-    // speculatively, before the coverage test, so their latency hides behind it
     const size_t pix = (size_t)iy * P.W + ix;
+    // the packed header and the (most common) layer-0 coefficients are loaded
+    // together, before the geometry below, so their latency hides behind it
     const int4 h = __ldg(P.hdr + pix);
     const float4 cf0 = __ldg(P.coef + pix);
-    Cover c;
-    if (!ss_cover(x, y, R, c)) return 0;
+    // ray / tangent-plane quantities of the backward (rasterizer.py:197-207)
+    const float k0 = fs(fm(x, R.b.z), R.a.x), k1 = fs(fm(x, R.b.w), R.a.y), k2 = fs(fm(x, R.c.x), R.a.z);
+    const float l0 = fs(fm(y, R.b.z), R.a.w), l1 = fs(fm(y, R.b.w), R.b.x), l2 = fs(fm(y, R.c.x), R.b.y);
+    const float inv_den = __frcp_rn(fs(fm(k0, l1), fm(k1, l0)));
     const float zs = R.d.z;
     const int nc = h.x;
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
@@ -66,28 +67,40 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
     for (int j = 3; j < nc; ++j) m += __ldg(P.thr + j * HW + pix) < zs;
     if (m >= P.k_max) return 0;  // beyond the K_MAX stop: discarded
     const float4 cf = m == 0 ? cf0 : __ldg(P.coef + m * HW + pix);
-    const float e = __expf(-0.5f * c.rho2);
+    const float e = __expf(-0.5f * rho2);
     const float w = R.d.x * e;
     const float gw = cf.x + cf.y * R.e.x + cf.z * R.e.y + cf.w * R.e.z;
     g[13] += w * cf.y; g[14] += w * cf.z; g[15] += w * cf.w;
     const float gr = -0.5f * w * gw;
     g[12] += e * gw;
-    const float u = c.u, v = c.v;
     g[9] += gr * u * u; g[10] += gr * 2.f * u * v; g[11] += gr * v * v;
     const float gu = 2.f * gr * (R.c.y * u + R.c.z * v);
     const float gv = 2.f * gr * (R.c.z * u + R.c.w * v);
-    const float gp0 = gu * c.inv_den, gp1 = gv * c.inv_den, gp2 = -(gu * u + gv * v) * c.inv_den;
-    const float gk0 = c.l1 * gp2 - c.l2 * gp1;
-    const float gk1 = c.l2 * gp0 - c.l0 * gp2;
-    const float gk2 = c.l0 * gp1 - c.l1 * gp0;
-    const float gl0 = gp1 * c.k2 - gp2 * c.k1;
-    const float gl1 = gp2 * c.k0 - gp0 * c.k2;
-    const float gl2 = gp0 * c.k1 - gp1 * c.k0;
+    const float gp0 = gu * inv_den, gp1 = gv * inv_den, gp2 = -(gu * u + gv * v) * inv_den;
+    const float gk0 = l1 * gp2 - l2 * gp1;
+    const float gk1 = l2 * gp0 - l0 * gp2;
+    const float gk2 = l0 * gp1 - l1 * gp0;
+    const float gl0 = gp1 * k2 - gp2 * k1;
+    const float gl1 = gp2 * k0 - gp0 * k2;
+    const float gl2 = gp0 * k1 - gp1 * k0;
     g[0] -= gk0; g[1] -= gk1; g[2] -= gk2;
     g[3] -= gl0; g[4] -= gl1; g[5] -= gl2;
     g[6] += x * gk0 + y * gl0; g[7] += x * gk1 + y * gl1; g[8] += x * gk2 + y * gl2;
     g[16] += fabsf(R.c.x) * sqrtf(gk2 * gk2 + gl2 * gl2);
     return 1;
+}
+
+// Coverage of rect pixel k (row-major) of record R; on a hit returns the
+// pixel (ix | iy << 16) and u, v, rho^2 (the forward's exact decision).
+__device__ __forceinline__ bool item_cover(const SplatParams &P, const SsRecord &R, int k, int rw, float inv_rw,
+                                           int &ixy, float4 &q) {
+    const int ky = (int)(((float)k + 0.5f) * inv_rw);
+    const int iy = R.r.y + ky, ix = R.r.x + (k - ky * rw);
+    Cover c;
+    if (!ss_cover(__ldg(P.xs + ix), __ldg(P.ys + iy), R, c)) return false;
+    ixy = ix | (iy << 16);
+    q = make_float4(c.u, c.v, c.rho2, 0.f);
+    return true;
 }
 
 __device__ __forceinline__ void load_record(const SsRecord *recs, int rec, SsRecord &R) {
@@ -96,65 +109,136 @@ __device__ __forceinline__ void load_record(const SsRecord *recs, int rec, SsRec
     R.r = __ldg(reinterpret_cast<const int4 *>(src) + 5);
 }
 
-constexpr int kBigArea = 512;  // rects above this go to the CTA-per-record kernel
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// One warp per kept record (grid-stride); lanes sweep the record's whole pixel
-// rect row-major, so every record is reduced and committed exactly once.
-// Records with huge rects (grazing or near-camera splats) would serialise a
-// warp: they are zeroed here and queued for big_bwd_kernel.
-__global__ void __launch_bounds__(256, 3) splat_bwd_kernel(SplatParams P, int32_t *big_list, int32_t *big_count)
+constexpr int kBigArea = 512;  // rects above this go to the CTA-chunked kernel (~0.1% of records)
+constexpr int kSplatWarps = 8;
+
+struct SplatWarpSmem {
+    SsRecord rec[2];          // current / prefetched record (cp.async double buffer)
+    float2 uv[kBigArea];      // covered items: u, v
+    int ixy[kBigArea];        // covered items: pixel ix | iy << 16
+};
+
+// One warp per kept record.  Warps take blocks of 32 consecutive records
+// (spatially coherent: scenes are Morton ordered) so the cull flags come with
+// one coalesced load + ballot; the next kept record is copied into the
+// other shared slot with cp.async while the current one is processed.  Per
+// record: pass 1 takes the exact coverage decision for every rect pixel and
+// compacts the covered ones (with u, v, rho^2) into the warp's list; pass 2
+// evaluates the gradient on the covered items only, 32 per iteration.
+// Records with huge rects (grazing or near-camera splats) are zeroed here
+// and queued for big_bwd_kernel.
+__global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatParams P, int32_t *big_list, int32_t *big_count)
 {
-    __shared__ SsRecord s_rec[8];  // the warp's current record (broadcast reads, frees 24 registers)
+    extern __shared__ __align__(16) unsigned char splat_smem[];
+    SplatWarpSmem &sm = reinterpret_cast<SplatWarpSmem *>(splat_smem)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int my_ch = warp_tr_index<NCH>(lane);
     const unsigned same = __match_any_sync(0xffffffffu, my_ch);
     const bool owner = (__ffs(same) - 1) == lane;
+    const int nblocks = (P.n + 31) >> 5;
 
-    SsRecord &R = s_rec[threadIdx.x >> 5];
-    // software pipeline over the warp's records: the cull flag two records
-    // ahead and the next kept record's 96 bytes (lanes 0-5) are in flight
-    // while the current one is processed
-    auto next_kept = [&](int r) {
-        while (r < P.n && P.cull[r] != 0) r += nwarps;
+    // kept-record cursor: block b, remaining kept mask
+    int blk = gwarp;
+    unsigned kept = 0u;
+    auto refill = [&]() {
+        while (kept == 0u && blk < nblocks) {
+            const int r = (blk << 5) + lane;
+            kept = __ballot_sync(0xffffffffu, r < P.n && P.cull[r] == 0);
+            if (kept == 0u) blk += nwarps;
+        }
+    };
+    auto next_rec = [&]() -> int {  // pops the next kept record (or -1)
+        refill();
+        if (kept == 0u) return -1;
+        const int r = (blk << 5) + __ffs(kept) - 1;
+        kept &= kept - 1u;
+        if (kept == 0u) blk += nwarps;
         return r;
     };
-    int rec = next_kept(gwarp);
-    float4 nxt = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (rec < P.n && lane < 6) nxt = __ldg(reinterpret_cast<const float4 *>(P.records + rec) + lane);
-    for (; rec < P.n;) {
+    int cur = next_rec();
+    int buf = 0;
+    if (cur >= 0 && lane < 6) cp_async16(reinterpret_cast<float4 *>(&sm.rec[0]) + lane,
+                                         reinterpret_cast<const float4 *>(P.records + cur) + lane);
+    cp_async_commit();
+    while (cur >= 0) {
+        const int nxt = next_rec();
+        cp_async_wait_all();
         __syncwarp();
-        if (lane < 6) reinterpret_cast<float4 *>(&R)[lane] = nxt;
-        const int cur = rec;
-        rec = next_kept(rec + nwarps);
-        if (rec < P.n && lane < 6) nxt = __ldg(reinterpret_cast<const float4 *>(P.records + rec) + lane);
-        __syncwarp();
+        if (nxt >= 0 && lane < 6) cp_async16(reinterpret_cast<float4 *>(&sm.rec[buf ^ 1]) + lane,
+                                             reinterpret_cast<const float4 *>(P.records + nxt) + lane);
+        cp_async_commit();
+        const SsRecord &R = sm.rec[buf];
         const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
         float *dst = P.acc + (size_t)cur * SS_ACC_FLOATS;
         if (area > kBigArea) {
             if (lane < SS_ACC_FLOATS) dst[lane] = 0.f;
             if (lane == 0) big_list[atomicAdd(big_count, 1)] = cur;
-            continue;
-        }
-        const float inv_rw = 1.f / (float)rw;
-        float g[NCH];
+        } else {
+            // pass 1: exact coverage, compaction of the covered pixels
+            const float inv_rw = 1.f / (float)rw;
+            int ncov = 0;
+            for (int k0 = 0; k0 < area; k0 += 32) {
+                int ixy = 0;
+                float4 q;
+                const bool hit = k0 + lane < area && item_cover(P, R, k0 + lane, rw, inv_rw, ixy, q);
+                const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                if (hit) {
+                    const int slot = ncov + __popc(hm & lt);
+                    sm.uv[slot] = make_float2(q.x, q.y);
+                    sm.ixy[slot] = ixy;
+                }
+                ncov += __popc(hm);
+            }
+            __syncwarp();
+            // pass 2: gradients of the covered items
+            float g[NCH];
 #pragma unroll
-        for (int k = 0; k < NCH; ++k) g[k] = 0.f;
-        int touch = 0;
-        for (int k = lane; k < area; k += 32) touch += pixel_grad(P, R, k, rw, inv_rw, g);
-        const int tot = __reduce_add_sync(0xffffffffu, touch);
-        if (tot == 0) {  // still commit the (zero) row: the buffer is never memset
-            if (lane < SS_ACC_FLOATS) dst[lane] = 0.f;
-            continue;
+            for (int k = 0; k < NCH; ++k) g[k] = 0.f;
+            int touch = 0;
+            for (int j = lane; j < ncov; j += 32) {
+                const float2 q = sm.uv[j];
+                const int ixy = sm.ixy[j];
+                // rho^2 with ss_cover's float32 expression (bit-identical on its fast path)
+                const float r2 = R.c.y * q.x * q.x + 2.f * R.c.z * q.x * q.y + R.c.w * q.y * q.y;
+                touch += item_grad(P, R, ixy & 0xffff, ixy >> 16, q.x, q.y, r2, g);
+            }
+            const int tot = __reduce_add_sync(0xffffffffu, touch);
+            if (tot == 0) {  // still commit the (zero) row: the buffer is never memset
+                if (lane < SS_ACC_FLOATS) dst[lane] = 0.f;
+            } else {
+                warp_tr_reduce<NCH>(g, lane);
+                // channel c -> accumulator slot (16 is dview_z, 0 here: the ss sum lives in 17)
+                if (owner) dst[my_ch == 16 ? 17 : my_ch] = g[0];
+                if (lane == 0) reinterpret_cast<int *>(dst)[18] = tot;
+                if (lane == 1) dst[16] = 0.f;
+                if (lane == 2) dst[19] = 0.f;
+            }
         }
-        warp_tr_reduce<NCH>(g, lane);
-        // channel c -> accumulator slot (16 is dview_z, 0 here: the ss sum lives in 17)
-        if (owner) dst[my_ch == 16 ? 17 : my_ch] = g[0];
-        if (lane == 0) reinterpret_cast<int *>(dst)[18] = tot;
-        if (lane == 1) dst[16] = 0.f;
-        if (lane == 2) dst[19] = 0.f;
+        __syncwarp();
+        cur = nxt;
+        buf ^= 1;
     }
+    cp_async_wait_all();
+}
+
+// Gradient contribution of record R at rect pixel k (row-major) for the big
+// records (no compaction), accumulated into g[]; returns 1 when touched.
+__device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &R, int k, int rw, float inv_rw,
+                                          float g[NCH]) {
+    int ixy;
+    float4 q;
+    if (!item_cover(P, R, k, rw, inv_rw, ixy, q)) return 0;
+    return item_grad(P, R, ixy & 0xffff, ixy >> 16, q.x, q.y, q.z, g);
 }
 
 // Big records (grazing splats whose filtered bound spans up to most of the
@@ -219,7 +303,13 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     P.xs = pixel_ndc; P.ys = pixel_ndc + width;
     P.coef = reinterpret_cast<const float4 *>(coef);
     P.thr = thr; P.hdr = reinterpret_cast<const int4 *>(pix_hdr); P.acc = rec_acc;
-    splat_bwd_kernel<<<148 * 16, 256, 0, st>>>(P, big_list, big_count);
+    const int smem = kSplatWarps * (int)sizeof(SplatWarpSmem);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(splat_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    splat_bwd_kernel<<<148 * 3, 32 * kSplatWarps, smem, st>>>(P, big_list, big_count);
     SS_CUDA_CHECK_LAUNCH();
     big_bwd_kernel<<<148 * 4, 256, 0, st>>>(P, big_list, big_count);
     SS_CUDA_CHECK_LAUNCH();
