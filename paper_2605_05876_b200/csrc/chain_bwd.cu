@@ -66,6 +66,19 @@ __device__ __forceinline__ void rows_of(const ChainParams &P, int i, float t1[3]
     }
 }
 
+// Fire-and-forget accumulation (RED, no return value, no load latency): the
+// per-view chain kernels are serialised, so each address has one writer at a
+// time and the sums stay deterministic.
+__device__ __forceinline__ void red_add(float *p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add2(float *p, float a, float b) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+__device__ __forceinline__ void red_add4(float *p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -217,7 +230,7 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
             }
     } else if (P.color_source == SS_COLOR_ALBEDO) {
         for (int c = 0; c < 3; ++c) {
-            const double al = (double)ss_sigmoid_f32(cl.albedo_raw[3 * i + c]);
+            const double al = (double)ss_sigmoid_fast(cl.albedo_raw[3 * i + c]);
             galb[c] = gcol[c] * al * (1.0 - al);
         }
     }
@@ -232,25 +245,18 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
 
     SsGrads &g = P.g;
     for (int c = 0; c < 3; ++c) {
-        g.centers[3 * i + c] += (float)gcent[c];
-        g.albedo_raw[3 * i + c] += (float)galb[c];
+        red_add(g.centers + 3 * i + c, (float)gcent[c]);
+        red_add(g.albedo_raw + 3 * i + c, (float)galb[c]);
     }
-    float4 gq = reinterpret_cast<float4 *>(g.quats)[i];
-    gq.x += (float)((gqw - radial * w) / qn);
-    gq.y += (float)((gqx - radial * x) / qn);
-    gq.z += (float)((gqy - radial * y) / qn);
-    gq.w += (float)((gqz - radial * z) / qn);
-    reinterpret_cast<float4 *>(g.quats)[i] = gq;
-    float2 gl = reinterpret_cast<float2 *>(g.log_scales)[i];
-    gl.x += (float)(gsu * su);
-    gl.y += (float)(gsv * sv);
-    reinterpret_cast<float2 *>(g.log_scales)[i] = gl;
-    g.metallic_raw[i] += (float)gmet;
-    g.roughness_raw[i] += (float)grough;
+    red_add4(g.quats + 4 * (size_t)i, (float)((gqw - radial * w) / qn), (float)((gqx - radial * x) / qn),
+             (float)((gqy - radial * y) / qn), (float)((gqz - radial * z) / qn));
+    red_add2(g.log_scales + 2 * (size_t)i, (float)(gsu * su), (float)(gsv * sv));
+    red_add(g.metallic_raw + i, (float)gmet);
+    red_add(g.roughness_raw + i, (float)grough);
     if (g.colors)
-        for (int c = 0; c < 3; ++c) g.colors[3 * i + c] += (float)gcol[c];
-    g.ss_grad[i] += ss;
-    g.touched[i] += touch;
+        for (int c = 0; c < 3; ++c) red_add(g.colors + 3 * i + c, (float)gcol[c]);
+    red_add(g.ss_grad + i, ss);
+    atomicAdd(g.touched + i, touch);
 }
 
 }  // namespace

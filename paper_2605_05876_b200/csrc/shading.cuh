@@ -13,6 +13,18 @@ __device__ __forceinline__ float ss_sigmoid_f32(float x) {
     return ex / (1.0f + ex);
 }
 
+// Fast sigmoid for the float32 shading adjoint (gradients: the 1e-3 bar).
+__device__ __forceinline__ float ss_sigmoid_fast(float x) {
+    const float e = __expf(-fabsf(x));
+    return x >= 0.0f ? __fdividef(1.0f, 1.0f + e) : __fdividef(e, 1.0f + e);
+}
+
+template <typename R>
+__device__ __forceinline__ R ss_act(float x) {
+    if constexpr (sizeof(R) == 4) return ss_sigmoid_fast(x);
+    else return (R)ss_sigmoid_f32(x);
+}
+
 template <typename R>
 __device__ __forceinline__ R ss_clip(R a, R lo, R hi) {
     if (a != a) return a;
@@ -118,11 +130,11 @@ struct ShadeState {
 // Activated materials, float64 normal and view direction of surfel i.
 template <typename R>
 __device__ __forceinline__ void ss_shade_inputs(const SsCloud &cloud, int i, const double cam_pos[3], ShadeIn<R> &in) {
-    in.albedo[0] = (R)ss_sigmoid_f32(cloud.albedo_raw[3 * i]);
-    in.albedo[1] = (R)ss_sigmoid_f32(cloud.albedo_raw[3 * i + 1]);
-    in.albedo[2] = (R)ss_sigmoid_f32(cloud.albedo_raw[3 * i + 2]);
-    in.m = (R)ss_sigmoid_f32(cloud.metallic_raw[i]);
-    in.r = (R)ss_sigmoid_f32(cloud.roughness_raw[i]);
+    in.albedo[0] = ss_act<R>(cloud.albedo_raw[3 * i]);
+    in.albedo[1] = ss_act<R>(cloud.albedo_raw[3 * i + 1]);
+    in.albedo[2] = ss_act<R>(cloud.albedo_raw[3 * i + 2]);
+    in.m = ss_act<R>(cloud.metallic_raw[i]);
+    in.r = ss_act<R>(cloud.roughness_raw[i]);
     R q0 = cloud.quats[4 * i], q1 = cloud.quats[4 * i + 1], q2 = cloud.quats[4 * i + 2], q3 = cloud.quats[4 * i + 3];
     R nrm = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
     R w = q0 / nrm, x = q1 / nrm, y = q2 / nrm, z = q3 / nrm;
