@@ -16,8 +16,14 @@
 namespace {
 
 constexpr int kScanThreads = 1024;
-constexpr int kSortThreads = 512;
-constexpr int kSortCap = 8192;  // keys per tile sorted in shared memory (64 KB)
+// Per-tile merge sort in shared memory (two ping-pong buffers).  Tiles up to
+// kSmallCap keys are sorted by a light CTA so several tiles share an SM; the
+// heavier ones by a second launch with a large buffer (each launch skips the
+// other's tiles); beyond kHeavyCap a bitonic network runs in global memory.
+constexpr int kSmallThreads = 256;
+constexpr int kSmallCap = 2048;
+constexpr int kHeavyThreads = 1024;
+constexpr int kHeavyCap = 12288;
 
 __device__ __forceinline__ uint32_t orderable(float z) {
     uint32_t u = __float_as_uint(z == 0.0f ? 0.0f : z);  // -0.0 == +0.0 like lexsort
@@ -124,19 +130,21 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
 // is past the end never exchanges and the padding never has to exist.
 template <typename Load, typename Swap>
 __device__ __forceinline__ void bitonic_sort(int n, Load ld, Swap sw) {
-    int N = 1;
-    while (N < n) N <<= 1;
-    for (int k = 2; k <= N; k <<= 1) {
-        const int hk = k >> 1;
+    int N = 1, lgN = 0;
+    while (N < n) { N <<= 1; ++lgN; }
+    for (int lk = 1; lk <= lgN; ++lk) {
+        const int lh = lk - 1;  // log2(k / 2)
+        const int hmask = (1 << lh) - 1;
         for (int p = threadIdx.x; p < (N >> 1); p += blockDim.x) {
-            int blk = p / hk, off = p % hk;
-            int lo = blk * k + off, hi = blk * k + k - 1 - off;
+            const int off = p & hmask;
+            const int lo = ((p >> lh) << lk) + off, hi = lo + (1 << lk) - 1 - 2 * off;
             if (hi < n) sw(lo, hi);
         }
         __syncthreads();
-        for (int j = hk >> 1; j >= 1; j >>= 1) {
+        for (int lj = lh - 1; lj >= 0; --lj) {
+            const int jm = (1 << lj) - 1;
             for (int p = threadIdx.x; p < (N >> 1); p += blockDim.x) {
-                int lo = (p / j) * 2 * j + (p % j), hi = lo + j;
+                const int lo = ((p >> lj) << (lj + 1)) + (p & jm), hi = lo + (1 << lj);
                 if (hi < n) sw(lo, hi);
             }
             __syncthreads();
@@ -151,7 +159,36 @@ __device__ __forceinline__ uint2 pack_rect(const SsRecord *__restrict__ recs, in
     return make_uint2((uint32_t)r.x | ((uint32_t)r.y << 16), (uint32_t)r.z | ((uint32_t)r.w << 16));
 }
 
-__global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(
+// 32 keys per warp sorted in registers (bitonic network over shuffles).
+__device__ __forceinline__ uint64_t warp_sort32(uint64_t v, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = (lane & k) == 0;           // ascending block
+            const bool lower = (lane & j) == 0;        // lower element of the pair
+            const bool keep_min = lower == up;
+            v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
+        }
+    }
+    return v;
+}
+
+// Merge path: the split (a, d - a) of diagonal d of runs x[0, la), y[0, lb)
+// (unique keys).
+__device__ __forceinline__ int merge_split(const uint64_t *x, int la, const uint64_t *y, int lb, int d) {
+    int lo = max(0, d - lb), hi = min(d, la);
+    while (lo < hi) {
+        const int a = (lo + hi) >> 1;
+        if (x[a] < y[d - a - 1]) lo = a + 1;
+        else hi = a;
+    }
+    return lo;
+}
+
+template <int kThreads, int kCap, bool kHeavy>
+__global__ void __launch_bounds__(kThreads) tile_sort_kernel(
     const int32_t *__restrict__ offsets, uint64_t *__restrict__ keys, int32_t *__restrict__ pair_rec,
     uint2 *__restrict__ pair_rect, const SsRecord *__restrict__ recs, int64_t capacity)
 {
@@ -162,21 +199,53 @@ __global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(
     if (o1 > capacity) o1 = capacity;
     if (o0 >= o1) return;
     const int n = (int)(o1 - o0);
+    if ((n > kSmallCap) != kHeavy) return;  // the other launch owns this tile
     uint64_t *g = keys + o0;
-    if (n <= kSortCap) {
-        for (int k = threadIdx.x; k < n; k += blockDim.x) skeys[k] = g[k];
+    if (n <= kCap) {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const int np = (n + 31) & ~31;  // padded with +inf to whole 32-key runs
+        uint64_t *A = skeys, *B = skeys + kCap;
+        for (int r = wid * 32; r < np; r += kThreads) {
+            const int k = r + lane;
+            const uint64_t v = k < n ? g[k] : ~0ull;
+            A[k] = warp_sort32(v, lane);
+        }
         __syncthreads();
-        bitonic_sort(n, 0, [&](int a, int b) {
-            uint64_t x = skeys[a], y = skeys[b];
-            if (x > y) { skeys[a] = y; skeys[b] = x; }
-        });
-        for (int k = threadIdx.x; k < n; k += blockDim.x) {
-            const int rec = (int32_t)(uint32_t)skeys[k];
+        for (int w = 32; w < np; w <<= 1) {
+            const int per = (np + kThreads - 1) / kThreads;
+            const int o = threadIdx.x * per;
+            if (o < np) {
+                const int pair0 = (o / (2 * w)) * (2 * w);
+                const int la = min(w, np - pair0), lb = max(0, min(w, np - pair0 - w));
+                const uint64_t *x = A + pair0, *y = A + pair0 + la;
+                const int d = o - pair0;
+                int a = merge_split(x, la, y, lb, d), b = d - a;
+                const int e = min(per, np - o);
+                // a thread's output may cross into the next pair of runs
+                int base = pair0, cla = la, clb = lb;
+                for (int q = 0; q < e; ++q) {
+                    if (a + b == cla + clb) {  // next pair of runs starts at this output
+                        base += 2 * w;
+                        cla = min(w, np - base);
+                        clb = max(0, min(w, np - base - w));
+                        x = A + base; y = A + base + cla;
+                        a = 0; b = 0;
+                    }
+                    const bool take_x = b >= clb || (a < cla && x[a] < y[b]);
+                    B[o + q] = take_x ? x[a] : y[b];
+                    a += take_x; b += !take_x;
+                }
+            }
+            __syncthreads();
+            uint64_t *tmp = A; A = B; B = tmp;
+        }
+        for (int k = threadIdx.x; k < n; k += kThreads) {
+            const int rec = (int32_t)(uint32_t)A[k];
             pair_rec[o0 + k] = rec;
             pair_rect[o0 + k] = pack_rect(recs, rec);
         }
     } else {
-        // rare oversized tile: same network directly in global memory
+        // rare oversized tile: bitonic network directly in global memory
         bitonic_sort(n, 0, [&](int a, int b) {
             uint64_t x = g[a], y = g[b];
             if (x > y) { g[a] = y; g[b] = x; }
@@ -201,8 +270,8 @@ extern "C" int ss_bin_sort(int n, const float *records, const int8_t *cull, int 
     if (width > 65535 || height > 65535) return SS_ERR_INVALID;  // rects are packed as uint16
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSortCap * (int)sizeof(uint64_t));
+        cudaFuncSetAttribute(tile_sort_kernel<kHeavyThreads, kHeavyCap, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kHeavyCap * (int)sizeof(uint64_t));
         attr_set = true;
     }
     cudaStream_t st = (cudaStream_t)stream;
@@ -220,7 +289,11 @@ extern "C" int ss_bin_sort(int n, const float *records, const int8_t *cull, int 
             pair_capacity);
         SS_CUDA_CHECK_LAUNCH();
     }
-    tile_sort_kernel<<<ntiles, kSortThreads, kSortCap * sizeof(uint64_t), st>>>(
+    tile_sort_kernel<kSmallThreads, kSmallCap, false><<<ntiles, kSmallThreads, 2 * kSmallCap * sizeof(uint64_t), st>>>(
+        tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const SsRecord *>(records),
+        pair_capacity);
+    SS_CUDA_CHECK_LAUNCH();
+    tile_sort_kernel<kHeavyThreads, kHeavyCap, true><<<ntiles, kHeavyThreads, 2 * kHeavyCap * sizeof(uint64_t), st>>>(
         tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const SsRecord *>(records),
         pair_capacity);
     SS_CUDA_CHECK_LAUNCH();

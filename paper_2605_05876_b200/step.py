@@ -145,7 +145,7 @@ class TrainStep:
         self._pairs, self._kept, self._nviews = [], [], 0
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
         self._stage = None
-        self.launches_per_view = 9     # preprocess, scan, scatter, tile sort, train fwd, ndc + record bwd x2, chain
+        self.launches_per_view = 10    # preprocess, scan, scatter, tile sort x2, train fwd, ndc + record bwd x2, chain
         self.launches_per_step_fixed = 4 + 7 + 1 + 4  # env adjoint, Adam x7, quat renorm, env refresh
 
     # -- buffers -----------------------------------------------------------
