@@ -72,7 +72,7 @@ typedef struct SsPreprocessOpts {
 } SsPreprocessOpts;
 
 /* Colour sources of render() (rasterizer.py:341-350). */
-enum { SS_COLOR_EXPLICIT = 0, SS_COLOR_IBL = 1, SS_COLOR_ALBEDO = 2 };
+enum { SS_COLOR_EXPLICIT = 0, SS_COLOR_IBL = 1, SS_COLOR_ALBEDO = 2, SS_COLOR_IBL_F32 = 3 };
 
 /* Optional per-surfel outputs of preprocess (ProjectedSurfels fields,
  * preprocess.py:195-228), all (n, ...) and nullable. */
@@ -93,7 +93,10 @@ typedef struct SsProjAux {
  * (0-4, preprocess.py:23-27), the per-record pair count and accumulates the
  * per-tile pair histogram `tile_counts` (ntiles ints, zeroed by the caller).
  * color_source: SS_COLOR_EXPLICIT reads `colors_in` (n,3); SS_COLOR_IBL shades
- * against `env`; SS_COLOR_ALBEDO uses sigmoid(albedo_raw).  `flags` (int[4],
+ * against `env` in float64 like the reference; SS_COLOR_IBL_F32 shades in
+ * float32 (the training step: colours within ~1e-6 relative, the forward
+ * state the float32 shading adjoint of ss_chain_backward recomputes);
+ * SS_COLOR_ALBEDO uses sigmoid(albedo_raw).  `flags` (int[4],
  * zeroed by caller) receives [0] zero-norm quaternion seen, [1] non-finite
  * colour seen. */
 int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,

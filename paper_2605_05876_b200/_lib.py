@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_build", "libss_b200.so")
 
 SS_OK, SS_ERR_INVALID, SS_ERR_CUDA = 0, 1, 2
-SS_COLOR_EXPLICIT, SS_COLOR_IBL, SS_COLOR_ALBEDO = 0, 1, 2
+SS_COLOR_EXPLICIT, SS_COLOR_IBL, SS_COLOR_ALBEDO, SS_COLOR_IBL_F32 = 0, 1, 2, 3
 REC_FLOATS = 24
 ACC_FLOATS = 20
 KMAX_CAP = 16

@@ -154,6 +154,12 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
         col[0] = colors_in[3 * i]; col[1] = colors_in[3 * i + 1]; col[2] = colors_in[3 * i + 2];
     } else if (color_source == SS_COLOR_ALBEDO) {
         col[0] = ss_sigmoid_f32(ar0); col[1] = ss_sigmoid_f32(ar1); col[2] = ss_sigmoid_f32(ar2);
+    } else if (color_source == SS_COLOR_IBL_F32) {
+        ShadeIn<float> in;
+        ss_shade_inputs(cloud, i, cam.cam_pos, in);
+        ShadeState<float> st;
+        ss_shade_forward(in, env, st, col);
+        if (aux.cells) ss_shade_cells(st, env, aux.cells + 15 * i);
     } else {
         ShadeIn<double> in;
         ss_shade_inputs(cloud, i, cam.cam_pos, in);
@@ -217,8 +223,10 @@ extern "C" int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const Ss
     if (cloud->n == 0) return SS_OK;
     if (!records || !cull) return SS_ERR_INVALID;
     if (color_source == SS_COLOR_EXPLICIT && !colors_in) return SS_ERR_INVALID;
-    if (color_source == SS_COLOR_IBL && (!env || !env->diffuse || !env->specular || !env->lut)) return SS_ERR_INVALID;
-    if (cloud->n == 0) return SS_OK;
+    if ((color_source == SS_COLOR_IBL || color_source == SS_COLOR_IBL_F32) &&
+        (!env || !env->diffuse || !env->specular || !env->lut))
+        return SS_ERR_INVALID;
+    if (color_source < SS_COLOR_EXPLICIT || color_source > SS_COLOR_IBL_F32) return SS_ERR_INVALID;
     CamF cf;
     for (int k = 0; k < 16; ++k) { cf.view[k] = (float)cam->view[k]; cf.proj[k] = (float)cam->proj[k]; }
     // camera.py:69-72: position = -R^T t (float64)

@@ -96,12 +96,11 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     };
 
     const int p0 = P.offsets[t], p1 = P.offsets[t + 1];
-    // per 32-pair chunk early exit once every lane of the warp stopped
-    // (only when the discard statistic is not requested)
-    for (int cb = p0; cb < p1; cb += 32 * 8) {
-        if (!kExtras && __all_sync(0xffffffffu, stopped)) break;
-        const int ce = min(p1, cb + 32 * 8);
-        walk_tile_packed(wp, cb, ce, P.pair_rec, P.pair_rect, P.records, sm, kExtras ? P.pair_cover : nullptr,
+    // early exit between chunks once every lane of the warp stopped (only
+    // when the discard statistic is not requested)
+    {
+        walk_tile_packed(wp, p0, p1, P.pair_rec, P.pair_rect, P.records, sm, kExtras ? P.pair_cover : nullptr,
+            [&]() { return !kExtras && __all_sync(0xffffffffu, stopped); },
             [](const RecGeo &R, float x, float y) {
                 Cover c;
                 return ss_cover(x, y, R, c) ? R.d.x * __expf(-0.5f * c.rho2) : -1.f;

@@ -109,48 +109,66 @@ __device__ __forceinline__ void packed_init(const WarpPix &w, PackedScratch &sm,
 }
 
 // Two-phase walk of the tile's sorted pair list [p0, p1) for one 8x4 warp
-// block.  Per 32-pair chunk the overlapping records are gathered (compacted,
-// list order) into the warp's shared scratch; phase 1 evaluates coverage and
+// block.  Per chunk the next (up to) 32 overlapping records are gathered
+// (compacted, list order) into the warp's shared scratch -- scanning as many
+// 32-pair windows as that takes, so the per-chunk work is amortised over
+// full slot sets; stop() is polled between chunks; phase 1 evaluates coverage and
 // weight for every in-rect (record, pixel) item with ONE item per lane (items
 // packed across records, so no lane idles outside a record's rect) and marks
 // the slot in the pixel's mask; phase 2 lets every lane walk only ITS pixel's
 // in-rect slots, in list order, calling f(SlotView) -- the order-dependent
 // compositing costs max-over-lanes of the in-rect count instead of the number
 // of overlapping records.
-template <typename Wt, typename F>
+template <typename Stop, typename Wt, typename F>
 __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p1, const int32_t *__restrict__ pair_rec,
                                                  const uint2 *__restrict__ pair_rect,
                                                  const SsRecord *__restrict__ recs, PackedScratch &sm,
-                                                 int32_t *pair_cover, Wt &&weight, F &&f) {
+                                                 int32_t *pair_cover, Stop &&stop, Wt &&weight, F &&f) {
     const unsigned FULL = 0xffffffffu;
     const unsigned lt = (1u << w.lane) - 1u;
-    for (int base = p0; base < p1; base += 32) {
-        const int p = base + w.lane;
-        bool ov = false;
-        int meta = 0;
-        if (p < p1) {
-            const uint2 pr = __ldg(pair_rect + p);
-            const int x0 = pr.x & 0xffff, y0 = pr.x >> 16, x1 = pr.y & 0xffff, y1 = pr.y >> 16;
-            ov = x0 < w.bx + 8 && x1 > w.bx && y0 < w.by + 4 && y1 > w.by;
-            const int cx0 = max(x0 - w.bx, 0), cw = min(x1 - w.bx, 8) - cx0;
-            const int ry0 = max(y0 - w.by, 0), ch = min(y1 - w.by, 4) - ry0;
-            meta = cx0 | (cw << 4) | (ry0 << 8) | ((cw * ch) << 12);
+    int cursor = p0;
+    while (cursor < p1) {
+        if (stop()) break;
+        // fill up to 32 slots with the next overlapping records (list order),
+        // scanning as many 32-pair windows as that takes
+        int n = 0;
+        while (n < 32 && cursor < p1) {
+            const int p = cursor + w.lane;
+            bool ov = false;
+            int meta = 0;
+            if (p < p1) {
+                const uint2 pr = __ldg(pair_rect + p);
+                const int x0 = pr.x & 0xffff, y0 = pr.x >> 16, x1 = pr.y & 0xffff, y1 = pr.y >> 16;
+                ov = x0 < w.bx + 8 && x1 > w.bx && y0 < w.by + 4 && y1 > w.by;
+                const int cx0 = max(x0 - w.bx, 0), cw = min(x1 - w.bx, 8) - cx0;
+                const int ry0 = max(y0 - w.by, 0), ch = min(y1 - w.by, 4) - ry0;
+                meta = cx0 | (cw << 4) | (ry0 << 8) | ((cw * ch) << 12);
+            }
+            unsigned ovm = __ballot_sync(FULL, ov);
+            const int room = 32 - n;
+            if (__popc(ovm) > room) {
+                // keep the first `room` overlapping pairs; resume after the last kept
+                const int last = __fns(ovm, 0, room);
+                ovm &= (2u << last) - 1u;
+                cursor += last + 1;
+            } else {
+                cursor += 32;
+            }
+            if ((ovm >> w.lane) & 1u) {
+                const int pos = n + __popc(ovm & lt);
+                const int rec = __ldg(pair_rec + p);
+                const float4 *src = reinterpret_cast<const float4 *>(recs + rec);
+                const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3),
+                             e = __ldg(src + 4);
+                sm.geo[pos].a = a; sm.geo[pos].b = b; sm.geo[pos].c = c; sm.geo[pos].d = d;
+                sm.zs[pos] = d.z; sm.ze[pos] = d.w; sm.vz[pos] = d.y;
+                sm.c0[pos] = e.x; sm.c1[pos] = e.y; sm.c2[pos] = e.z;
+                sm.meta[pos] = meta;
+                sm.pidx[pos] = p;
+            }
+            n += __popc(ovm);
         }
-        const unsigned ovm = __ballot_sync(FULL, ov);
-        if (ovm == 0u) continue;
-        const int n = __popc(ovm);
-        const int pos = __popc(ovm & lt);
-        if (ov) {
-            const int rec = __ldg(pair_rec + p);
-            const float4 *src = reinterpret_cast<const float4 *>(recs + rec);
-            const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3),
-                         e = __ldg(src + 4);
-            sm.geo[pos].a = a; sm.geo[pos].b = b; sm.geo[pos].c = c; sm.geo[pos].d = d;
-            sm.zs[pos] = d.z; sm.ze[pos] = d.w; sm.vz[pos] = d.y;
-            sm.c0[pos] = e.x; sm.c1[pos] = e.y; sm.c2[pos] = e.z;
-            sm.meta[pos] = meta;
-            sm.pidx[pos] = p;
-        }
+        if (n == 0) break;
         __syncwarp();
         // phase 1: inclusive scan of the per-slot item counts, then packed items
         const int my_meta = w.lane < n ? sm.meta[w.lane] : 0;

@@ -95,7 +95,12 @@ __device__ __forceinline__ void ss_bil_grads(const float *__restrict__ tex, int 
 // dirs_to_coords (shading.py:172-179)
 template <typename R>
 __device__ __forceinline__ void ss_dir_coords(const R d[3], int he, int we, R &fu, R &fv) {
-    R th = acos(ss_clip<R>(d[2], -R(1.0), R(1.0)));
+    // float32: theta = atan2(|d_xy|, d_z) instead of acos(d_z) -- the same
+    // angle for a unit d but well conditioned at the poles, where acos would
+    // amplify the float32 rounding of d_z
+    R th;
+    if constexpr (sizeof(R) == 4) th = atan2f(sqrtf(d[0] * d[0] + d[1] * d[1]), d[2]);
+    else th = acos(ss_clip<R>(d[2], -R(1.0), R(1.0)));
     R ph = atan2(d[1], d[0]);
     fu = (ph + R(SS_PI)) * ((R)we / (R(2) * R(SS_PI))) - R(0.5);
     fv = th * ((R)he / R(SS_PI)) - R(0.5);

@@ -173,7 +173,7 @@ class TrainStep:
         b.tile_counts.zero_()
         camst = _lib.make_camera(cam)
         rc = self.lib.ss_preprocess(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
-                                    _lib.SS_COLOR_IBL, None, ctypes.byref(self._envs), _lib.ptr(b.records),
+                                    _lib.SS_COLOR_IBL_F32, None, ctypes.byref(self._envs), _lib.ptr(b.records),
                                     _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts), None,
                                     _lib.ptr(b.flags), _lib.stream_ptr())
         _lib.check(rc, "ss_preprocess")
