@@ -47,6 +47,13 @@ __global__ void pixel_ndc_kernel(int W, int H, float *xs, float *ys, int32_t *bi
 // Gradient of the covered item (pixel ix, iy of record R) with the coverage
 // quantities u, v, rho^2 of the coverage pass, accumulated into g[].
 // Returns 1 when the record reaches the pixel before the K_MAX stop.
+// 1/x by the hardware approximation + one Newton step (no slow-path call).
+__device__ __forceinline__ float fast_rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r * (2.f - x * r);
+}
+
 __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R, int ix, int iy, float u, float v,
                                          float rho2, float g[NCH]) {
     const size_t HW = (size_t)P.W * P.H;
@@ -59,7 +66,7 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     // ray / tangent-plane quantities of the backward (rasterizer.py:197-207)
     const float k0 = fs(fm(x, R.b.z), R.a.x), k1 = fs(fm(x, R.b.w), R.a.y), k2 = fs(fm(x, R.c.x), R.a.z);
     const float l0 = fs(fm(y, R.b.z), R.a.w), l1 = fs(fm(y, R.b.w), R.b.x), l2 = fs(fm(y, R.c.x), R.b.y);
-    const float inv_den = __frcp_rn(fs(fm(k0, l1), fm(k1, l0)));
+    const float inv_den = fast_rcp(fs(fm(k0, l1), fm(k1, l0)));
     const float zs = R.d.z;
     const int nc = h.x;
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
@@ -86,7 +93,9 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     g[0] -= gk0; g[1] -= gk1; g[2] -= gk2;
     g[3] -= gl0; g[4] -= gl1; g[5] -= gl2;
     g[6] += x * gk0 + y * gl0; g[7] += x * gk1 + y * gl1; g[8] += x * gk2 + y * gl2;
-    g[16] += fabsf(R.c.x) * sqrtf(gk2 * gk2 + gl2 * gl2);
+    float nrm;  // screen-space gradient norm (Eq. 12): approximate sqrt, no slow path
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(gk2 * gk2 + gl2 * gl2));
+    g[16] += fabsf(R.c.x) * nrm;
     return 1;
 }
 
@@ -185,7 +194,8 @@ __global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatPar
             if (lane == 0) big_list[atomicAdd(big_count, 1)] = cur;
         } else {
             // pass 1: exact coverage, compaction of the covered pixels
-            const float inv_rw = 1.f / (float)rw;
+            // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
+            const float inv_rw = fast_rcp((float)rw);
             int ncov = 0;
             for (int k0 = 0; k0 < area; k0 += 32) {
                 int ixy = 0;
