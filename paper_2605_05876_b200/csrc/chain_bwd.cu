@@ -79,6 +79,29 @@ __device__ __forceinline__ void red_add4(float *p, float a, float b, float c, fl
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
+// Derived-map scatter of one bilinear tap (3 channels, float64 atomics).
+// Neighbouring surfels (Morton order) mostly hit the same env texel: when the
+// whole warp is present and agrees on the texel, the warp sums first
+// (fixed butterfly order) and one lane issues the atomics -- 32x fewer
+// same-address atomics at L2; otherwise every lane adds its own.
+__device__ __forceinline__ void scatter_rgb(double *base, int key, double v0, double v1, double v2) {
+    const unsigned am = __activemask();
+    const unsigned m = __match_any_sync(am, key);
+    if (am == 0xffffffffu && m == 0xffffffffu) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+            v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+        }
+        if ((threadIdx.x & 31) != 0) return;
+    }
+    double *d = base + 3 * (size_t)key;
+    if (v0 != 0.0) atomicAdd(d, v0);
+    if (v1 != 0.0) atomicAdd(d + 1, v1);
+    if (v2 != 0.0) atomicAdd(d + 2, v2);
+}
+
 __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -108,7 +131,8 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
         const double s01 = sg * (j00 * j10 + j01 * j11);
         const double s11 = 1.0 + sg * (j10 * j10 + j11 * j11);
         const double det = s00 * s11 - s01 * s01;
-        const double b00 = s11 / det, b01 = -s01 / det, b11 = s00 / det;
+        const double idet = 1.0 / det;
+        const double b00 = s11 * idet, b01 = -s01 * idet, b11 = s00 * idet;
         const double nf = 1.0 / sqrt(det);
         const double g00 = gs0, g01 = 0.5 * gs1, g11 = gs2;
         const double bg00 = b00 * g00 + b01 * g01, bg01 = b00 * g01 + b01 * g11;
@@ -121,7 +145,7 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
             const double gj00 = ts * (ga00 * j00 + ga01 * j10), gj01 = ts * (ga00 * j01 + ga01 * j11);
             const double gj10 = ts * (ga01 * j00 + ga11 * j10), gj11 = ts * (ga01 * j01 + ga11 * j11);
             const double T1[3] = {t1f[0], t1f[1], t1f[2]}, T2[3] = {t2f[0], t2f[1], t2f[2]}, T4[3] = {t4f[0], t4f[1], t4f[2]};
-            const double d4 = T4[2], cx = T1[2] / d4, cy = T2[2] / d4;
+            const double d4 = T4[2], id4 = 1.0 / d4, cx = T1[2] * id4, cy = T2[2] * id4;
             const double dx = 1.0 / P.W, dy = 1.0 / P.H;
             const double pr[4][4] = {{cx + dx, cy, gj00, gj10}, {cx - dx, cy, -gj00, -gj10},
                                      {cx, cy + dy, gj01, gj11}, {cx, cy - dy, -gj01, -gj11}};
@@ -135,9 +159,10 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
                 const double p1 = k[2] * l[0] - k[0] * l[2];
                 const double den = k[0] * l[1] - k[1] * l[0];
                 if (!(fabs(den) >= SS_DENOM_EPS)) continue;
-                const double u = p0 / den, v = p1 / den;
+                const double iden = 1.0 / den;
+                const double u = p0 * iden, v = p1 * iden;
                 const double gu = pr[p][2], gv = pr[p][3];
-                const double gp[3] = {gu / den, gv / den, -(gu * u + gv * v) / den};
+                const double gp[3] = {gu * iden, gv * iden, -(gu * u + gv * v) * iden};
                 const double gk[3] = {l[1] * gp[2] - l[2] * gp[1], l[2] * gp[0] - l[0] * gp[2], l[0] * gp[1] - l[1] * gp[0]};
                 const double gl[3] = {gp[1] * k[2] - gp[2] * k[1], gp[2] * k[0] - gp[0] * k[2], gp[0] * k[1] - gp[1] * k[0]};
                 for (int c = 0; c < 3; ++c) {
@@ -148,10 +173,10 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
                 gcx += (gk[0] * T4[0] + gk[1] * T4[1]) + gk[2] * T4[2];
                 gcy += (gl[0] * T4[0] + gl[1] * T4[1]) + gl[2] * T4[2];
             }
-            G1[2] += gcx / d4;
-            G4[2] -= gcx * cx / d4;
-            G2[2] += gcy / d4;
-            G4[2] -= gcy * cy / d4;
+            G1[2] += gcx * id4;
+            G4[2] -= gcx * cx * id4;
+            G2[2] += gcy * id4;
+            G4[2] -= gcy * cy * id4;
         }
     }
     // T rows -> camera (backward.py:405-410)
@@ -203,31 +228,24 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
         grough = sg.roughness_raw;
         // derived-map scatter (bilinear_scatter, shading.py:248-260, 583-597)
         const int we = P.env.we;
-        const size_t lstride = (size_t)P.env.he * we * 3;
         const double wts[2] = {1.0 - (double)st.frac, (double)st.frac};
         const int lvs[2] = {st.lvl0, st.lvl1};
         const SsBil<float> &bs = st.bs;
         const int sidx[4] = {bs.j0 * we + bs.i0, bs.j0 * we + bs.i1, bs.j1 * we + bs.i0, bs.j1 * we + bs.i1};
         const double scw[4] = {(1.0 - bs.tu) * (1.0 - bs.tv), (double)bs.tu * (1.0 - bs.tv), (1.0 - bs.tu) * (double)bs.tv,
                                (double)bs.tu * bs.tv};
-        for (int h = 0; h < 2; ++h) {
-            if (wts[h] == 0.0) continue;
-            double *dst = P.g.d_specular + lstride * lvs[h];
-            for (int k = 0; k < 4; ++k)
-                for (int c = 0; c < 3; ++c) {
-                    const double val = sg.g_ls[c] * wts[h] * scw[k];
-                    if (val != 0.0) atomicAdd(dst + 3 * sidx[k] + c, val);
-                }
-        }
+        const int T = P.env.he * we;
+        for (int h = 0; h < 2; ++h)  // level lvs[h] texel sidx[k] = element 3 * (lvs[h] * T + sidx[k])
+            for (int k = 0; k < 4; ++k) {
+                const double f = wts[h] * scw[k];
+                scatter_rgb(P.g.d_specular, lvs[h] * T + sidx[k], sg.g_ls[0] * f, sg.g_ls[1] * f, sg.g_ls[2] * f);
+            }
         const SsBil<float> &bd = st.bd;
         const int didx[4] = {bd.j0 * we + bd.i0, bd.j0 * we + bd.i1, bd.j1 * we + bd.i0, bd.j1 * we + bd.i1};
         const double dcw[4] = {(1.0 - bd.tu) * (1.0 - bd.tv), (double)bd.tu * (1.0 - bd.tv), (1.0 - bd.tu) * (double)bd.tv,
                                (double)bd.tu * bd.tv};
         for (int k = 0; k < 4; ++k)
-            for (int c = 0; c < 3; ++c) {
-                const double val = sg.g_ld[c] * dcw[k];
-                if (val != 0.0) atomicAdd(P.g.d_diffuse + 3 * didx[k] + c, val);
-            }
+            scatter_rgb(P.g.d_diffuse, didx[k], sg.g_ld[0] * dcw[k], sg.g_ld[1] * dcw[k], sg.g_ld[2] * dcw[k]);
     } else if (P.color_source == SS_COLOR_ALBEDO) {
         for (int c = 0; c < 3; ++c) {
             const double al = (double)ss_sigmoid_fast(cl.albedo_raw[3 * i + c]);
