@@ -53,6 +53,21 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files:
+        return None, None
+    try:
+        with open(files[-1]) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"]), os.path.relpath(files[-1], ROOT)
+    except Exception:
+        return None, None
+
+
 def _dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -267,6 +282,7 @@ def run_ours(args):
         return
 
     peak, peak_kind = _peaks()
+    traffic, traffic_src = _traffic()
     P, Nk = stats["pairs_mean"], stats["kept_mean"]
     HW = RES * RES
     bwd_ms = float(np.mean(per_kernel.get("train_backward", [float("nan")])))
@@ -289,7 +305,7 @@ def run_ours(args):
         "config": _config({"parallelism": f"dp{world} over views", "pairs_per_view": P, "kept_per_view": Nk}),
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "raster backward (ss_train_backward)",
+                     "traffic": traffic, "traffic_source": traffic_src, "kernel": "raster backward (ss_train_backward)",
                      "algorithmic_bytes_per_launch": bwd_bytes, "avg_launch_ms": bwd_ms,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)"},
         "view_roofline": {"bytes_per_view": view_bytes,
