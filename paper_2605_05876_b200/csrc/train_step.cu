@@ -41,7 +41,7 @@ __global__ void pixel_ndc_kernel(int W, int H, float *xs, float *ys, int32_t *bi
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < W) xs[k] = ss_ndc_x(k, W);
     if (k < H) ys[k] = ss_ndc_y(k, H);
-    if (k == 0) *big_count = 0;
+    if (k < 2) big_count[k] = 0;
 }
 
 // Gradient of the covered item (pixel ix, iy of record R) with the coverage
@@ -125,6 +125,8 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+constexpr int kBigChunk = 1024;
+constexpr int kHugeArea = 8 * kBigChunk;  // big rects above this are spread over the grid
 constexpr int kBigArea = 512;  // rects above this go to the CTA-chunked kernel (~0.1% of records)
 constexpr int kSplatWarps = 8;
 
@@ -191,7 +193,10 @@ __global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatPar
         float *dst = P.acc + (size_t)cur * SS_ACC_FLOATS;
         if (area > kBigArea) {
             if (lane < SS_ACC_FLOATS) dst[lane] = 0.f;
-            if (lane == 0) big_list[atomicAdd(big_count, 1)] = cur;
+            if (lane == 0) {
+                if (area > kHugeArea) big_list[P.n - 1 - atomicAdd(big_count + 1, 1)] = cur;
+                else big_list[atomicAdd(big_count, 1)] = cur;
+            }
         } else {
             // pass 1: exact coverage, compaction of the covered pixels
             // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
@@ -252,10 +257,35 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
 }
 
 // Big records (grazing splats whose filtered bound spans up to most of the
-// image): their rects are cut into 1024-pixel chunks spread over the whole
-// grid (chunk c of queue entry b goes to CTA (c + 37 b) mod grid), each CTA's
-// warps split a chunk in 32-pixel rows and commit with atomics.
-constexpr int kBigChunk = 1024;
+// image).  The splat kernel queues them in two lists: medium rects (up to
+// kHugeArea pixels) from the front of the queue, huge ones from its back.  A
+// medium record is processed by one CTA (grid-stride over the list), a huge
+// one is cut into 1024-pixel chunks spread over the whole grid (chunk c of
+// huge entry h goes to CTA (c + 37 h) mod grid).  Warps split the pixels in
+// 32-pixel rows, reduce, and commit with atomics (the splat kernel zeroed
+// the rows).
+__device__ __forceinline__ void big_record(const SplatParams &P, int rec, int c0, int cstep, int wid, int nw,
+                                           int lane, int my_ch, bool owner) {
+    SsRecord R;
+    load_record(P.records, rec, R);
+    const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
+    const int nchunks = (area + kBigChunk - 1) / kBigChunk;
+    const float inv_rw = fast_rcp((float)rw);
+    float g[NCH];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) g[k] = 0.f;
+    int touch = 0;
+    for (int c = c0; c < nchunks; c += cstep) {
+        const int k1 = min(area, (c + 1) * kBigChunk);
+        for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad(P, R, k, rw, inv_rw, g);
+    }
+    const int tot = __reduce_add_sync(0xffffffffu, touch);
+    if (tot == 0) return;
+    warp_tr_reduce<NCH>(g, lane);
+    float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
+    if (owner) atomicAdd(dst + (my_ch == 16 ? 17 : my_ch), g[0]);
+    if (lane == 0) atomicAdd(reinterpret_cast<int *>(dst) + 18, tot);
+}
 
 __global__ void __launch_bounds__(256) big_bwd_kernel(SplatParams P, const int32_t *big_list,
                                                       const int32_t *big_count)
@@ -264,30 +294,12 @@ __global__ void __launch_bounds__(256) big_bwd_kernel(SplatParams P, const int32
     const int my_ch = warp_tr_index<NCH>(lane);
     const unsigned same = __match_any_sync(0xffffffffu, my_ch);
     const bool owner = (__ffs(same) - 1) == lane;
-    const int nbig = *big_count;
+    const int nmed = big_count[0], nhuge = big_count[1];
     const int G = gridDim.x;
-    for (int b = 0; b < nbig; ++b) {
-        const int rec = big_list[b];
-        SsRecord R;
-        load_record(P.records, rec, R);
-        const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
-        const int nchunks = (area + kBigChunk - 1) / kBigChunk;
-        const float inv_rw = 1.f / (float)rw;
-        const int first = (int)(((long long)blockIdx.x - 37LL * b) % G + G) % G;
-        float g[NCH];
-#pragma unroll
-        for (int k = 0; k < NCH; ++k) g[k] = 0.f;
-        int touch = 0;
-        for (int c = first; c < nchunks; c += G) {
-            const int k1 = min(area, (c + 1) * kBigChunk);
-            for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad(P, R, k, rw, inv_rw, g);
-        }
-        const int tot = __reduce_add_sync(0xffffffffu, touch);
-        if (tot == 0) continue;
-        warp_tr_reduce<NCH>(g, lane);
-        float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
-        if (owner) atomicAdd(dst + (my_ch == 16 ? 17 : my_ch), g[0]);
-        if (lane == 0) atomicAdd(reinterpret_cast<int *>(dst) + 18, tot);
+    for (int b = blockIdx.x; b < nmed; b += G) big_record(P, big_list[b], 0, 1, wid, nw, lane, my_ch, owner);
+    for (int h = 0; h < nhuge; ++h) {
+        const int first = (int)(((long long)blockIdx.x - 37LL * h) % G + G) % G;
+        big_record(P, big_list[P.n - 1 - h], first, G, wid, nw, lane, my_ch, owner);
     }
 }
 
@@ -303,7 +315,7 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     cudaStream_t st = (cudaStream_t)stream;
     const int mx = width > height ? width : height;
     int32_t *big_count = reinterpret_cast<int32_t *>(pixel_ndc + width + height);
-    int32_t *big_list = big_count + 1;
+    int32_t *big_list = big_count + 2;
     pixel_ndc_kernel<<<(mx + 255) / 256, 256, 0, st>>>(width, height, pixel_ndc, pixel_ndc + width, big_count);
     SS_CUDA_CHECK_LAUNCH();
     SplatParams P{};
