@@ -11,6 +11,7 @@
 // that stay in L1/L2), writes one 96 B record + 1 B cull + 4 B pair count.
 #include "ss_common.cuh"
 #include "shading.cuh"
+#include "coverage.cuh"
 
 namespace {
 
@@ -177,7 +178,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     rec.b = make_float4(t2[1], t2[2], t4[0], t4[1]);
     rec.c = make_float4(t4[2], m00, m01, m11);
     rec.d = make_float4(nf, vz, zs, ze);
-    rec.e = make_float4(col[0], col[1], col[2], ez);
+    // e.w: certified fast-coverage margin of this record (coverage.cuh)
+    const float cm = alive ? coverage_margin(t1, t2, t4, m00, m01, m11, (int)x0, (int)y0, (int)x1, (int)y1, cam.W, cam.H)
+                           : 0.f;
+    rec.e = make_float4(col[0], col[1], col[2], cm);
     int count = 0;
     const int tile = opt.tile;
     const int ntx = (cam.W + tile - 1) / tile;

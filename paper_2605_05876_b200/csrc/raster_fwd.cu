@@ -101,6 +101,10 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     {
         walk_tile_packed(wp, p0, p1, P.pair_rec, P.pair_rect, P.records, sm, kExtras ? P.pair_cover : nullptr,
             [&]() { return !kExtras && __all_sync(0xffffffffu, stopped); },
+            // the forward keeps the reference's own float32 sequence: its weights
+            // then match the reference's to ~1e-7 (the fast linear-form path of
+            // coverage.cuh decides coverage identically but its weights carry
+            // independent rounding noise of ~1e-4 relative at the support edge)
             [](const RecGeo &R, float x, float y) {
                 Cover c;
                 return ss_cover(x, y, R, c) ? R.d.x * __expf(-0.5f * c.rho2) : -1.f;
@@ -277,16 +281,17 @@ __global__ void __launch_bounds__(256) cover_check_kernel(int W, int H, int tile
               [&](const SsRecord &R, int, int) {
                   if (!in_rect(wp, R.r)) return;
                   ++n;
-                  Cover c;
-                  const bool fast = ss_cover(wp.x, wp.y, R, c);
                   const float t1[3] = {R.a.x, R.a.y, R.a.z}, t2[3] = {R.a.w, R.b.x, R.b.y}, t4[3] = {R.b.z, R.b.w, R.c.x};
                   SsHit h;
                   const bool exact = ss_intersect(wp.x, wp.y, t1, t2, t4, h) && ss_rho2(R.c.y, R.c.z, R.c.w, h.u, h.v) < 9.0;
-                  bad += fast != exact;
-                  const float ta = R.c.y * c.u * c.u, tb = 2.f * R.c.z * c.u * c.v, tc = R.c.w * c.v * c.v;
-                  const float mag = fabsf(ta) + fabsf(tb) + fabsf(tc);
-                  const float r2 = ta + tb + tc;
-                  slow += !(r2 - 9.f >= 2e-4f * mag || (9.f - r2 >= 2e-4f * mag && mag <= 32.f));
+                  FastCov f;
+                  fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
+                  float u, v, r2;
+                  const int d = fast_cover(f, R.c.y, R.c.z, R.c.w, wp.x, wp.y, u, v, r2);
+                  Cover c;
+                  const bool cov = d >= 0 ? d == 1 : ss_cover(wp.x, wp.y, R, c);
+                  bad += cov != exact;
+                  slow += d < 0;
               });
     atomicAdd(&counts[0], n);
     atomicAdd(&counts[1], bad);

@@ -2,6 +2,7 @@
 // backward rasterisers, and the fast coverage test with exact fallback.
 #pragma once
 #include "ss_common.cuh"
+#include "coverage.cuh"
 
 // Warp layout inside a tile CTA: warps own 8x4 pixel blocks.
 struct WarpPix {
@@ -82,14 +83,20 @@ struct RecGeo {
     float4 a, b, c, d;    // the first 64 bytes of SsRecord
 };
 
+#ifndef SS_PACK_SLOTS
+#define SS_PACK_SLOTS 16
+#endif
+constexpr int kSlots = SS_PACK_SLOTS;  // overlapping records per chunk (<= 32)
+
 struct PackedScratch {
-    RecGeo geo[32];       // t1, t2, t4, Sigma^-1, n_f, view_z, z_start, z_end
-    float wgt[32][32];    // [slot][pixel]: n_f exp(-rho^2/2) when covered, -1 when not (in-rect only)
-    unsigned mask[32];    // per pixel: slots whose rect contains it
-    float zs[32], ze[32], vz[32], c0[32], c1[32], c2[32];
-    int meta[32];         // in-block rect: cx0 | cw << 4 | ry0 << 8 | cnt << 12
-    int pidx[32];
-    int ncov[32];         // covered lanes per slot (pair cover counts)
+    RecGeo geo[kSlots];       // t1, t2, t4, Sigma^-1, n_f, view_z, z_start, z_end
+    float wgt[kSlots][32];    // [slot][pixel]: n_f exp(-rho^2/2) when covered, -1 when not (in-rect only)
+    unsigned mask[32];        // per pixel: slots whose rect contains it
+    float4 zc[kSlots];        // z_start, z_end, colour r, g
+    float c2[kSlots], vz[kSlots]; // colour b, view_z
+    int meta[32];             // in-block rect: cx0 | cw << 4 | ry0 << 8 | cnt << 12 (lanes >= kSlots: 0)
+    int pidx[kSlots];
+    int ncov[32];             // covered lanes per slot (pair cover counts)
     float xs[8], ys[4];
 };
 
@@ -132,7 +139,7 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
         // fill up to 32 slots with the next overlapping records (list order),
         // scanning as many 32-pair windows as that takes
         int n = 0;
-        while (n < 32 && cursor < p1) {
+        while (n < kSlots && cursor < p1) {
             const int p = cursor + w.lane;
             bool ov = false;
             int meta = 0;
@@ -145,7 +152,7 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
                 meta = cx0 | (cw << 4) | (ry0 << 8) | ((cw * ch) << 12);
             }
             unsigned ovm = __ballot_sync(FULL, ov);
-            const int room = 32 - n;
+            const int room = kSlots - n;
             if (__popc(ovm) > room) {
                 // keep the first `room` overlapping pairs; resume after the last kept
                 const int last = __fns(ovm, 0, room);
@@ -161,8 +168,8 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
                 const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3),
                              e = __ldg(src + 4);
                 sm.geo[pos].a = a; sm.geo[pos].b = b; sm.geo[pos].c = c; sm.geo[pos].d = d;
-                sm.zs[pos] = d.z; sm.ze[pos] = d.w; sm.vz[pos] = d.y;
-                sm.c0[pos] = e.x; sm.c1[pos] = e.y; sm.c2[pos] = e.z;
+                sm.zc[pos] = make_float4(d.z, d.w, e.x, e.y);
+                sm.c2[pos] = e.z; sm.vz[pos] = d.y;
                 sm.meta[pos] = meta;
                 sm.pidx[pos] = p;
             }
@@ -212,8 +219,9 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
                 v.slot = __ffs(M) - 1;
                 M &= M - 1u;
                 v.w = sm.wgt[v.slot][w.lane];
-                v.zs = sm.zs[v.slot]; v.ze = sm.ze[v.slot]; v.vz = sm.vz[v.slot];
-                v.c0 = sm.c0[v.slot]; v.c1 = sm.c1[v.slot]; v.c2 = sm.c2[v.slot];
+                const float4 zc = sm.zc[v.slot];
+                v.zs = zc.x; v.ze = zc.y; v.c0 = zc.z; v.c1 = zc.w;
+                v.c2 = sm.c2[v.slot]; v.vz = sm.vz[v.slot];
                 f(v);
             }
         }

@@ -99,16 +99,24 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     return 1;
 }
 
-// Coverage of rect pixel k (row-major) of record R; on a hit returns the
-// pixel (ix | iy << 16) and u, v, rho^2 (the forward's exact decision).
-__device__ __forceinline__ bool item_cover(const SplatParams &P, const SsRecord &R, int k, int rw, float inv_rw,
-                                           int &ixy, float4 &q) {
+// Coverage of rect pixel k (row-major) of record R (fast path with the
+// record's certified margin, exact reference arithmetic when undecided); on
+// a hit returns the pixel (ix | iy << 16) and u, v, rho^2.
+__device__ __forceinline__ bool item_cover(const SplatParams &P, const SsRecord &R, const FastCov &f, int k, int rw,
+                                           float inv_rw, int &ixy, float4 &q) {
     const int ky = (int)(((float)k + 0.5f) * inv_rw);
     const int iy = R.r.y + ky, ix = R.r.x + (k - ky * rw);
-    Cover c;
-    if (!ss_cover(__ldg(P.xs + ix), __ldg(P.ys + iy), R, c)) return false;
+    const float x = __ldg(P.xs + ix), y = __ldg(P.ys + iy);
+    float u, v, r2;
+    const int d = fast_cover(f, R.c.y, R.c.z, R.c.w, x, y, u, v, r2);
+    if (d == 0) return false;
+    if (d < 0) {
+        Cover c;
+        if (!ss_cover(x, y, R, c)) return false;
+        u = c.u; v = c.v; r2 = c.rho2;
+    }
     ixy = ix | (iy << 16);
-    q = make_float4(c.u, c.v, c.rho2, 0.f);
+    q = make_float4(u, v, r2, 0.f);
     return true;
 }
 
@@ -201,11 +209,13 @@ __global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatPar
             // pass 1: exact coverage, compaction of the covered pixels
             // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
             const float inv_rw = fast_rcp((float)rw);
+            FastCov f;
+            fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
             int ncov = 0;
             for (int k0 = 0; k0 < area; k0 += 32) {
                 int ixy = 0;
                 float4 q;
-                const bool hit = k0 + lane < area && item_cover(P, R, k0 + lane, rw, inv_rw, ixy, q);
+                const bool hit = k0 + lane < area && item_cover(P, R, f, k0 + lane, rw, inv_rw, ixy, q);
                 const unsigned hm = __ballot_sync(0xffffffffu, hit);
                 if (hit) {
                     const int slot = ncov + __popc(hm & lt);
@@ -248,11 +258,11 @@ __global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatPar
 
 // Gradient contribution of record R at rect pixel k (row-major) for the big
 // records (no compaction), accumulated into g[]; returns 1 when touched.
-__device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &R, int k, int rw, float inv_rw,
-                                          float g[NCH]) {
+__device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &R, const FastCov &f, int k, int rw,
+                                          float inv_rw, float g[NCH]) {
     int ixy;
     float4 q;
-    if (!item_cover(P, R, k, rw, inv_rw, ixy, q)) return 0;
+    if (!item_cover(P, R, f, k, rw, inv_rw, ixy, q)) return 0;
     return item_grad(P, R, ixy & 0xffff, ixy >> 16, q.x, q.y, q.z, g);
 }
 
@@ -271,13 +281,15 @@ __device__ __forceinline__ void big_record(const SplatParams &P, int rec, int c0
     const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
     const int nchunks = (area + kBigChunk - 1) / kBigChunk;
     const float inv_rw = fast_rcp((float)rw);
+    FastCov f;
+    fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
     float g[NCH];
 #pragma unroll
     for (int k = 0; k < NCH; ++k) g[k] = 0.f;
     int touch = 0;
     for (int c = c0; c < nchunks; c += cstep) {
         const int k1 = min(area, (c + 1) * kBigChunk);
-        for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad(P, R, k, rw, inv_rw, g);
+        for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad(P, R, f, k, rw, inv_rw, g);
     }
     const int tot = __reduce_add_sync(0xffffffffu, touch);
     if (tot == 0) return;

@@ -143,7 +143,7 @@ def compact(state: ViewState) -> ProjectedSurfels:
     rect = r[:, 20:24].contiguous().view(torch.int32)
     return ProjectedSurfels(
         t1=r[:, 0:3].contiguous(), t2=r[:, 3:6].contiguous(), t4=r[:, 6:9].contiguous(),
-        view_z=r[:, 13].contiguous(), eps_z=r[:, 19].contiguous(), sinv=r[:, 9:12].contiguous(),
+        view_z=r[:, 13].contiguous(), eps_z=a["eps_z"][keep], sinv=r[:, 9:12].contiguous(),
         n_f=r[:, 12].contiguous(), center_ndc=a["center_ndc"][keep], jac=a["jac"][keep],
         jac_ok=a["jac_ok"][keep].bool(), rect=rect, source_index=keep.to(torch.int32),
         c_cam=a["c_cam"][keep], tu_cam=a["tu_cam"][keep], tv_cam=a["tv_cam"][keep],
