@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     // early exit between chunks once every lane of the warp stopped (only
     // when the discard statistic is not requested)
     {
-        walk_tile_packed(wp, p0, p1, P.pair_rec, P.pair_rect, P.records, sm, kExtras ? P.pair_cover : nullptr,
+        walk_tile_packed<!kExtras>(wp, p0, p1, P.pair_rec, P.pair_rect, P.records, sm, kExtras ? P.pair_cover : nullptr,
             [&]() { return !kExtras && __all_sync(0xffffffffu, stopped); },
             // the forward keeps the reference's own float32 sequence: its weights
             // then match the reference's to ~1e-7 (the fast linear-form path of

@@ -115,6 +115,14 @@ __device__ __forceinline__ void packed_init(const WarpPix &w, PackedScratch &sm,
     __syncwarp();
 }
 
+// kCoveredOnly: phase 2 visits only the COVERED slots of each pixel.  That
+// renders identically: an in-rect record that does not cover the pixel adds
+// no weight, and the layer it may close by the gap test (z_start > z_max_end,
+// rasterizer.py:168) would be closed by the next covering record anyway --
+// list order is ascending z_start, so that record's z_start is larger still,
+// nothing was accumulated in between, and the K_MAX stop falls on the same
+// layer.  Only the discarded-record statistic (counted per in-rect record)
+// needs the full in-rect walk.
 // Two-phase walk of the tile's sorted pair list [p0, p1) for one 8x4 warp
 // block.  Per chunk the next (up to) 32 overlapping records are gathered
 // (compacted, list order) into the warp's shared scratch -- scanning as many
@@ -126,7 +134,7 @@ __device__ __forceinline__ void packed_init(const WarpPix &w, PackedScratch &sm,
 // in-rect slots, in list order, calling f(SlotView) -- the order-dependent
 // compositing costs max-over-lanes of the in-rect count instead of the number
 // of overlapping records.
-template <typename Stop, typename Wt, typename F>
+template <bool kCoveredOnly, typename Stop, typename Wt, typename F>
 __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p1, const int32_t *__restrict__ pair_rec,
                                                  const uint2 *__restrict__ pair_rect,
                                                  const SsRecord *__restrict__ recs, PackedScratch &sm,
@@ -205,8 +213,9 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
                 const int row = (k * (int)(pk >> 23)) >> 8;
                 const int col = k - row * cw;
                 const int px = (ry0 + row) * 8 + cx0 + col;
-                sm.wgt[s][px] = weight(sm.geo[s], sm.xs[px & 7], sm.ys[px >> 3]);
-                atomicOr(&sm.mask[px], 1u << s);
+                const float wv = weight(sm.geo[s], sm.xs[px & 7], sm.ys[px >> 3]);
+                sm.wgt[s][px] = wv;
+                if (!kCoveredOnly || wv >= 0.f) atomicOr(&sm.mask[px], 1u << s);
             }
         }
         __syncwarp();
