@@ -205,7 +205,7 @@ def run_ours(args):
 
     cloud = ss.SurfelCloud(**init)
     env = ss.EnvironmentLight(np.log(env_base) + np.random.default_rng(3).normal(0, 0.1, env_base.shape))
-    ts = TrainStep(cloud, env, RES, RES, streams=int(os.environ.get("SS_STREAMS", "2")))
+    ts = TrainStep(cloud, env, RES, RES, streams=int(os.environ.get("SS_STREAMS", "3")))
     ts.size_pairs(cams[:4])
     stream = torch.cuda.current_stream()
 
