@@ -169,6 +169,24 @@ int ss_train_backward_records(int n, const int8_t *cull, const float *records, i
                               int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
                               float *pixel_ndc, float *rec_acc, void *stream);
 
+/* ---- image losses ---------------------------------------
+ * Replace the reference's numpy/scipy losses: tone_map / tone_map_backward
+ * (shading.py:54-79; tone_mode 0 = 'ldr', 1 = 'hdr-loss', -1 = identity),
+ * ssim_loss / photometric_loss (losses.py:45-108) and silhouette_loss
+ * (losses.py:111-123).  Images (H, W, C) float32, C in {1, 3}; float64
+ * internally.  ss_photometric_loss: loss = (1 - l) mean|T(x) - T(y)| +
+ * l (1 - mean SSIM(T(x), T(y))), its gradient w.r.t. x (through T) into grad,
+ * out[3] = {loss, L1, 1 - SSIM} (device doubles, no host sync); lambda = 1
+ * gives ssim_loss.  workspace: ss_photometric_workspace() bytes.
+ * ss_silhouette_loss: out[1] = 1 - soft IoU, grad d/d alpha; workspace 2 doubles. */
+size_t ss_photometric_workspace(int height, int width, int channels);
+int ss_photometric_loss(int height, int width, int channels, const float *x, const float *y, int tone_mode,
+                        double lambda_ssim, double *out, float *grad, double *workspace, void *stream);
+int ss_tone_map(int64_t n, const float *img, int tone_mode, float *out, void *stream);
+int ss_tone_map_backward(int64_t n, const float *img, int tone_mode, const float *g_out, float *g_in, void *stream);
+int ss_silhouette_loss(int64_t n, const float *alpha, const float *mask, double *out, float *grad,
+                       double *workspace, void *stream);
+
 /* ---- chain backward -------------------------------------------------------
  * Replaces the per-surfel tail of backward_image() (backward.py:398-461,
  * 473-548), shade_backward() (shading.py:525-616) and quat_frame_backward()

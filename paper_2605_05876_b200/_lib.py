@@ -90,6 +90,12 @@ _SIGNATURES = {
                          ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_train_backward_records": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
                                   c_p, c_p, c_p],
+    "ss_photometric_workspace": [ctypes.c_int, ctypes.c_int, ctypes.c_int],
+    "ss_photometric_loss": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_double, c_p, c_p,
+                            c_p, c_p],
+    "ss_tone_map": [ctypes.c_int64, c_p, ctypes.c_int, c_p, c_p],
+    "ss_tone_map_backward": [ctypes.c_int64, c_p, ctypes.c_int, c_p, c_p, c_p],
+    "ss_silhouette_loss": [ctypes.c_int64, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_split_children": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64, c_p],
 }
@@ -110,6 +116,7 @@ def load(require_cuda=True):
             if argt is not None:
                 fn.argtypes = argt
             fn.restype = ctypes.c_int
+        lib.ss_photometric_workspace.restype = ctypes.c_size_t
         lib.ss_last_error.restype = ctypes.c_char_p
         lib.ss_version.restype = ctypes.c_int
         _lib = lib

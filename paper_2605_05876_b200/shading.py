@@ -165,36 +165,42 @@ class EnvironmentLight:
 
 
 SRGB_LIN_BOUND = 0.0031308
+TONE_MODES = {"ldr": 0, "hdr-loss": 1}
 
 
-def _srgb(t):
-    return torch.where(t <= SRGB_LIN_BOUND, t * 12.92,
-                       1.055 * torch.pow(torch.clamp(t, min=SRGB_LIN_BOUND), 1.0 / 2.4) - 0.055)
+def _tone_mode(mode):
+    if mode not in TONE_MODES:
+        raise ValueError(f"unknown tone map mode {mode!r}")
+    return TONE_MODES[mode]
 
 
-def _srgb_grad(t):
-    return torch.where(t <= SRGB_LIN_BOUND, torch.full_like(t, 12.92),
-                       (1.055 / 2.4) * torch.pow(torch.clamp(t, min=SRGB_LIN_BOUND), 1.0 / 2.4 - 1.0))
+def _f32_cuda(x):
+    return torch.as_tensor(x, device="cuda", dtype=torch.float32).contiguous()
 
 
 def tone_map(img, mode="ldr"):
-    """shading.py:54-65 on device tensors."""
-    if mode == "ldr":
-        return _srgb(torch.clamp(img, 0.0, 1.0))
-    if mode == "hdr-loss":
-        return _srgb(torch.log1p(torch.clamp(img, min=0.0)))
-    raise ValueError(f"unknown tone map mode {mode!r}")
+    """shading.py:54-67 ('ldr': sRGB of the [0, 1] clamp, 'hdr-loss': sRGB of
+    log1p(max(x, 0))) -- csrc/losses.cu ss_tone_map, float64 inside."""
+    m = _tone_mode(mode)
+    x = _f32_cuda(img)
+    out = torch.empty_like(x)
+    lib = _lib.load()
+    _lib.check(lib.ss_tone_map(x.numel(), _lib.ptr(x), m, _lib.ptr(out), _lib.stream_ptr()), "ss_tone_map")
+    return out
 
 
 def tone_map_backward(img, mode, g_out):
-    """shading.py:68-79 on device tensors."""
-    if mode == "ldr":
-        inside = (img > 0.0) & (img < 1.0)
-        return torch.where(inside, g_out * _srgb_grad(torch.clamp(img, 0.0, 1.0)), torch.zeros_like(img))
-    if mode == "hdr-loss":
-        x = torch.clamp(img, min=0.0)
-        return torch.where(img > 0.0, g_out * _srgb_grad(torch.log1p(x)) / (1.0 + x), torch.zeros_like(img))
-    raise ValueError(f"unknown tone map mode {mode!r}")
+    """shading.py:70-79: d tone_map / d img applied to an upstream gradient."""
+    m = _tone_mode(mode)
+    x = _f32_cuda(img)
+    g = _f32_cuda(g_out)
+    if g.shape != x.shape:
+        raise ValueError("image shape mismatch")
+    out = torch.empty_like(x)
+    lib = _lib.load()
+    _lib.check(lib.ss_tone_map_backward(x.numel(), _lib.ptr(x), m, _lib.ptr(g), _lib.ptr(out), _lib.stream_ptr()),
+               "ss_tone_map_backward")
+    return out
 
 
 def shade_surfels(cloud, env, camera):

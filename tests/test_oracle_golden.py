@@ -164,3 +164,28 @@ def test_refine_topology():
     np.testing.assert_allclose(cp, d["new_centers"][n_new - 2 * ns:n_new - ns], rtol=1e-6, atol=1e-7)
     np.testing.assert_allclose(cm, d["new_centers"][n_new - ns:], rtol=1e-6, atol=1e-7)
     np.testing.assert_allclose(cls, d["new_log_scales"][n_new - ns:], rtol=1e-6)
+
+
+def test_loss_oracle_matches_reference_goldens():
+    """oracle tone_map / ssim_loss / photometric_loss / silhouette_loss vs the
+    reference's own outputs (tests/golden/make_golden_losses.py)."""
+    import os
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "losses.npz"))
+    x, y, g_up = d["img"], d["tgt"], d["g_up"]
+    for mode in ("ldr", "hdr-loss"):
+        k = mode.replace("-", "_")
+        np.testing.assert_allclose(O.tone_map(x, mode), d["tone_" + k], rtol=1e-15, atol=0)
+        np.testing.assert_allclose(O.tone_map_backward(x, mode, g_up), d["tone_bwd_" + k], rtol=1e-15, atol=0)
+        for lam in (0.0, 0.2):
+            v, g = O.photometric_loss(O.tone_map(x, mode), O.tone_map(y, mode), lam)
+            assert v == pytest.approx(float(d[f"photo_{k}_{int(lam * 10)}"]), rel=1e-14)
+            np.testing.assert_allclose(g, d[f"photo_grad_{k}_{int(lam * 10)}"], rtol=1e-10, atol=1e-17)
+    v, g = O.ssim_loss(x, y)
+    assert v == pytest.approx(float(d["ssim"]), rel=1e-14)
+    np.testing.assert_allclose(g, d["ssim_grad"], rtol=1e-10, atol=1e-16)
+    v, g = O.ssim_loss(d["alpha"], d["mask"])
+    assert v == pytest.approx(float(d["ssim_1c"]), rel=1e-14)
+    np.testing.assert_allclose(g, d["ssim_1c_grad"], rtol=1e-10, atol=1e-16)
+    v, g = O.silhouette_loss(d["alpha"], d["mask"])
+    assert v == pytest.approx(float(d["sil"]), rel=1e-14)
+    np.testing.assert_allclose(g, d["sil_grad"], rtol=1e-14, atol=0)
