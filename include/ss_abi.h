@@ -164,7 +164,16 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
 int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
                      const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
                      const float *background, int k_max, const float *target, float *coef, float *thr,
-                     int32_t *pix_hdr, double *loss_sum, float *rgb, void *stream);
+                     int32_t *pix_hdr, double *loss_sum, float *rgb, float *alpha, void *stream);
+/* ss_train_forward with target == NULL is the DEFERRED-loss variant (any
+ * image loss, e.g. the reference fit loss of train.py:194-206): it writes rgb
+ * (required), alpha (nullable) and, per pixel and layer, the raw layer sums
+ * (W, C rgb) into coef; after the loss has produced g_rgb (and g_alpha),
+ * ss_train_coefs turns them into the backward coefficients in place (suffix
+ * recursion of backward.py:201-238 incl. the coverage term).  pix_hdr.x =
+ * closed layers | layer count << 8. */
+int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef, const float *g_rgb,
+                   const float *g_alpha, const float *background, void *stream);
 int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
                               int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
                               float *pixel_ndc, float *rec_acc, void *stream);

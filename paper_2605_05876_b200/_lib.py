@@ -87,7 +87,8 @@ _SIGNATURES = {
     "ss_isolation": [ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float,
                      ctypes.c_int, c_p, c_p],
     "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
-                         ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+                         ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_train_coefs": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), c_p],
     "ss_train_backward_records": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
                                   c_p, c_p, c_p],
     "ss_photometric_workspace": [ctypes.c_int, ctypes.c_int, ctypes.c_int],

@@ -147,8 +147,15 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
             P.alpha[pix] = 1.f - T;
             P.depth[pix] = dden > 0.f ? dnum / dden : 0.f;
             P.nlayers[pix] = layers;
+        } else if (!P.target) {
+            // deferred loss (ss_train_coefs finishes the layer coefficients
+            // once the image-space gradient is known): raw layer sums
+            P.hdr[pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
+            const size_t HW = (size_t)P.W * P.H;
+            for (int m = 0; m < layers; ++m) P.coef[(size_t)m * HW + pix] = make_float4(lw[m], lc0[m], lc1[m], lc2[m]);
+            if (P.alpha) P.alpha[pix] = 1.f - T;
         } else {
-            P.hdr[pix] = make_int4(ncl, __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
+            P.hdr[pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
             // L1 loss and its image gradient (losses.py:100-104)
             const float d0 = r0 - P.target[3 * pix], d1 = r1 - P.target[3 * pix + 1], d2 = r2 - P.target[3 * pix + 2];
             lsum = (double)fabsf(d0) + (double)fabsf(d1) + (double)fabsf(d2);
@@ -191,10 +198,50 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
         for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
         if (lane == 0 && d) atomicAdd(P.discarded, (unsigned long long)d);
     }
-    if (kTrain) {
+    if (kTrain && P.target) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
         if (lane == 0) atomicAdd(P.loss, lsum);
+    }
+}
+
+// Deferred-loss training step: turn the forward's raw layer sums (W, C) into
+// the per-layer backward coefficients (A, dL/dC_raw) once the image-space
+// gradients g_rgb (and g_alpha) are known -- the suffix recursion of
+// backward.py:201-238 including the coverage term (g_alpha * prod(1 - a)).
+__global__ void __launch_bounds__(256) train_coef_kernel(int HW, const int4 *__restrict__ hdr, float4 *coef,
+                                                         const float *__restrict__ g_rgb,
+                                                         const float *__restrict__ g_alpha, float bg0, float bg1,
+                                                         float bg2)
+{
+    const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= HW) return;
+    const int layers = hdr[pix].x >> 8;
+    if (layers == 0) return;
+    double a[SS_KMAX_CAP], tb[SS_KMAX_CAP];
+    float4 raw[SS_KMAX_CAP];
+    double tr = 1.0;
+    for (int m = 0; m < layers; ++m) {
+        raw[m] = coef[(size_t)m * HW + pix];
+        a[m] = -expm1(-(double)raw[m].x);
+        tb[m] = tr;
+        tr *= 1.0 - a[m];
+    }
+    const double gc0 = g_rgb[3 * (size_t)pix], gc1 = g_rgb[3 * (size_t)pix + 1], gc2 = g_rgb[3 * (size_t)pix + 2];
+    const double ga = g_alpha ? (double)g_alpha[pix] : 0.0;
+    double sf0 = bg0, sf1 = bg1, sf2 = bg2, q = 1.0;
+    for (int m = layers - 1; m >= 0; --m) {
+        const double inv = 1.0 / (double)raw[m].x;
+        const double ch0 = raw[m].y * inv, ch1 = raw[m].z * inv, ch2 = raw[m].w * inv;
+        const double g_am = tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2) + ga * q);
+        const double ta = tb[m] * a[m];
+        const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
+        coef[(size_t)m * HW + pix] = make_float4((float)(g_am * (1.0 - a[m]) - (gh0 * ch0 + gh1 * ch1 + gh2 * ch2) * inv),
+                                                 (float)(gh0 * inv), (float)(gh1 * inv), (float)(gh2 * inv));
+        sf0 = a[m] * ch0 + (1.0 - a[m]) * sf0;
+        sf1 = a[m] * ch1 + (1.0 - a[m]) * sf1;
+        sf2 = a[m] * ch2 + (1.0 - a[m]) * sf2;
+        q *= 1.0 - a[m];
     }
 }
 
@@ -245,11 +292,13 @@ extern "C" int ss_raster_forward(int width, int height, int tile, const int32_t 
 extern "C" int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
                                 const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
                                 int k_max, const float *target, float *coef, float *thr, int32_t *pix_hdr,
-                                double *loss_sum, float *rgb, void *stream)
+                                double *loss_sum, float *rgb, float *alpha, void *stream)
 {
     FwdParams P;
     if (!fill_common(P, width, height, tile, tile_offsets, pair_rec, pair_rect, records, background, k_max)) return SS_ERR_INVALID;
-    if (!target || !coef || !thr || !pix_hdr || !loss_sum) return SS_ERR_INVALID;
+    if (!coef || !thr || !pix_hdr) return SS_ERR_INVALID;
+    if (target ? !loss_sum : !rgb) return SS_ERR_INVALID;  // fused L1 needs the loss sum, deferred mode the image
+    P.alpha = alpha;
     P.target = target;
     P.thr = thr;
     P.hdr = reinterpret_cast<int4 *>(pix_hdr);
@@ -259,6 +308,19 @@ extern "C" int ss_train_forward(int width, int height, int tile, const int32_t *
     P.rgb = rgb;
     const int ntiles = P.ntx * ((height + tile - 1) / tile);
     launch<false, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef,
+                              const float *g_rgb, const float *g_alpha, const float *background, void *stream)
+{
+    if (width <= 0 || height <= 0 || k_max < 1 || k_max > SS_KMAX_CAP || !pix_hdr || !coef || !g_rgb || !background)
+        return SS_ERR_INVALID;
+    const int HW = width * height;
+    train_coef_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        HW, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef), g_rgb, g_alpha, background[0],
+        background[1], background[2]);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

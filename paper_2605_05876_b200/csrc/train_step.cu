@@ -68,7 +68,7 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const float l0 = fs(fm(y, R.b.z), R.a.w), l1 = fs(fm(y, R.b.w), R.b.x), l2 = fs(fm(y, R.c.x), R.b.y);
     const float inv_den = fast_rcp(fs(fm(k0, l1), fm(k1, l0)));
     const float zs = R.d.z;
-    const int nc = h.x;
+    const int nc = h.x & 0xff;  // closed layers (the layer count sits in bits 8+)
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
             (nc > 2 && __int_as_float(h.w) < zs);
     for (int j = 3; j < nc; ++j) m += __ldg(P.thr + j * HW + pix) < zs;

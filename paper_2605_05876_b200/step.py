@@ -92,6 +92,18 @@ class ViewBuffers:
         self.capacity = 0
         self.keys = self.pair = self.pair_rect = None
 
+    def alloc_loss(self, W, H, device):
+        """Buffers of the deferred-loss step (photometric loss on the image)."""
+        from .losses import ImageLoss
+        f32 = dict(device=device, dtype=torch.float32)
+        self.rgb = torch.empty((H, W, 3), **f32)
+        self.g_rgb = torch.empty((H, W, 3), **f32)
+        self.alpha = torch.empty((H, W), **f32)
+        self.g_alpha = torch.empty((H, W), **f32)
+        self.sil = torch.zeros(1, device=device, dtype=torch.float64)
+        self.sil_ws = torch.empty(2, device=device, dtype=torch.float64)
+        self.imgloss = ImageLoss(H, W, 3, device)
+
     def alloc_pairs(self, cap):
         dev = self.records.device
         self.keys = torch.empty(cap, device=dev, dtype=torch.int64)
@@ -102,7 +114,16 @@ class ViewBuffers:
 
 class TrainStep:
     def __init__(self, cloud, env, width, height, k_max=16, tile=16, background=(0.0, 0.0, 0.0),
-                 lrs=None, pair_capacity=None, process_group=None, options=None, streams=2):
+                 lrs=None, pair_capacity=None, process_group=None, options=None, streams=2, loss="l1",
+                 tone="hdr-loss", lambda_ssim=0.2, lambda_sil=0.1):
+        """loss="l1": the BASELINE config loss (mean |rgb - target| in linear
+        space), fused into the forward kernel.  loss="photometric": the
+        reference fit loss (train.py:194-206): tone_map(tone) then
+        (1 - lambda_ssim) L1 + lambda_ssim (1 - SSIM) on the device, plus
+        lambda_sil * silhouette when masks are given to step()."""
+        if loss not in ("l1", "photometric"):
+            raise ValueError(f"unknown loss {loss!r}")
+        self.loss_mode, self.tone, self.lambda_ssim, self.lambda_sil = loss, tone, float(lambda_ssim), float(lambda_sil)
         self.lib = _lib.load()
         self.cloud, self.env = cloud, env
         self.W, self.H, self.k_max, self.tile = int(width), int(height), int(k_max), int(tile)
@@ -118,6 +139,9 @@ class TrainStep:
         self.ntiles = self.ntx * ((self.H + tile - 1) // tile)
         self.bufs = [ViewBuffers(n, self.W, self.H, tile, self.k_max, self.ntiles, dev) for _ in range(max(1, streams))]
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(len(self.bufs))]
+        if loss == "photometric":
+            for b in self.bufs:
+                b.alloc_loss(self.W, self.H, dev)
         he, we = env.shape
         self.T = he * we
         # packed gradient buffer: params, ss_grad, env d_base_log, loss -- one all-reduce
@@ -179,7 +203,7 @@ class TrainStep:
         _lib.check(rc, "ss_preprocess")
         return camst
 
-    def view(self, cam, target, b=None, chain_after=None, target_done=None):
+    def view(self, cam, target, b=None, chain_after=None, target_done=None, mask=None):
         """Forward + backward of one view on the CURRENT stream with buffer set
         b; gradients accumulate into self.grads.  chain_after: event the chain
         kernel must wait for (the previous view's chain, which updates the same
@@ -199,10 +223,28 @@ class TrainStep:
                    "ss_bin_sort")
         self._ev_end(ev)
         ev = self._ev_begin("train_forward")
-        _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
-                                        _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
-                                        _lib.ptr(target), _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr),
-                                        _lib.ptr(self.loss), None, s), "ss_train_forward")
+        if self.loss_mode == "l1":
+            _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
+                                            _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
+                                            _lib.ptr(target), _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr),
+                                            _lib.ptr(self.loss), None, None, s), "ss_train_forward")
+        else:
+            # deferred loss: image -> loss kernels -> layer coefficients
+            _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
+                                            _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
+                                            None, _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr), None,
+                                            _lib.ptr(b.rgb), _lib.ptr(b.alpha), s), "ss_train_forward")
+            out = b.imgloss(b.rgb, target, b.g_rgb, self.lambda_ssim, self.tone)
+            self.loss += out[0:1]
+            g_alpha = None
+            if mask is not None and self.lambda_sil > 0.0:
+                _lib.check(lib.ss_silhouette_loss(self.W * self.H, _lib.ptr(b.alpha), _lib.ptr(mask), _lib.ptr(b.sil),
+                                                  _lib.ptr(b.g_alpha), _lib.ptr(b.sil_ws), s), "ss_silhouette_loss")
+                b.g_alpha.mul_(self.lambda_sil)
+                self.loss += self.lambda_sil * b.sil
+                g_alpha = b.g_alpha
+            _lib.check(lib.ss_train_coefs(self.W, self.H, self.k_max, _lib.ptr(b.pix_hdr), _lib.ptr(b.coef),
+                                          _lib.ptr(b.g_rgb), _lib.ptr(g_alpha), self._bg[0], s), "ss_train_coefs")
         self._ev_end(ev)
         if target_done is not None:
             target_done.record()
@@ -223,7 +265,7 @@ class TrainStep:
         done.record()
         return done
 
-    def _run_views(self, cameras, targets_for, target_done=None):
+    def _run_views(self, cameras, targets_for, target_done=None, masks=None):
         """Issue every view, alternating the worker streams (view i uses stream
         and buffers i % S); the chain kernels are serialised by events."""
         main = torch.cuda.current_stream()
@@ -235,7 +277,8 @@ class TrainStep:
             with torch.cuda.stream(self.streams[k]):
                 tgt = targets_for(i, self.streams[k])
                 prev = self.view(cam, tgt, self.bufs[k], chain_after=prev,
-                                 target_done=None if target_done is None else target_done[i % 2])
+                                 target_done=None if target_done is None else target_done[i % 2],
+                                 mask=None if masks is None else masks[i])
                 if self.collect_stats:
                     b = self.bufs[k]
                     self._pairs.append(int(b.offsets[-1].item()))
@@ -273,14 +316,14 @@ class TrainStep:
         for b in self.bufs:
             b.flags.zero_()
 
-    def gradients(self, cameras, targets):
+    def gradients(self, cameras, targets, masks=None):
         """Sum of per-view gradients over this rank's views (+ env adjoint)."""
         if self.capacity == 0:
             self.size_pairs(cameras[:2])
         self.zero()
         self._nviews = len(cameras)
         self._pairs, self._kept = [], []
-        self._run_views(cameras, lambda i, st: targets[i])
+        self._run_views(cameras, lambda i, st: targets[i], masks=masks)
         self._finish()
 
     def _finish(self):
@@ -304,10 +347,12 @@ class TrainStep:
         self.adam.step("env_base_log", self.env.base_log, self.g_env_log, self.lrs["env_base_log"] * lr_scale)
         self.env.refresh()
 
-    def step(self, cameras, targets):
-        self.gradients(cameras, targets)
+    def step(self, cameras, targets, masks=None):
+        self.gradients(cameras, targets, masks)
         self.apply()
-        return self.loss_f  # device scalar: sum over views of sum|rgb - target|
+        # device scalar: loss="l1": sum over views of sum|rgb - target|;
+        # loss="photometric": sum over views of the per-view fit loss
+        return self.loss_f
 
     def step_host(self, cameras, host_targets):
         """step() with the targets in pinned HOST memory: each view's target is

@@ -84,3 +84,44 @@ def test_host_targets_path_equals_resident():
         outs.append((float(loss.item()), cloud.centers.clone()))
     assert outs[0][0] == outs[1][0]
     assert torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("with_masks", [False, True])
+def test_photometric_train_step_matches_api_path(with_masks):
+    """loss="photometric" (the reference fit loss, train.py:194-206: hdr-loss
+    tone map, 0.8 L1 + 0.2 (1 - SSIM), + lambda_sil silhouette) through the
+    deferred-loss kernels vs render -> image_loss / silhouette_loss ->
+    backward_image summed over views."""
+    init, env_base, cams, targets = _scene(n=2500, res=80)
+    rng = np.random.default_rng(5)
+    masks = [torch.as_tensor((rng.uniform(size=(80, 80)) > 0.5).astype(np.float32), device="cuda")
+             for _ in cams] if with_masks else None
+    cloud = ss.SurfelCloud(**init)
+    env = ss.EnvironmentLight.from_base(env_base)
+    ts = TrainStep(cloud, env, 80, 80, loss="photometric", lambda_sil=0.3)
+    ts.gradients(cams, targets, masks)
+    torch.cuda.synchronize()
+    acc = {k: torch.zeros_like(ts.grads[k]) for k in PARAMS}
+    loss = 0.0
+    d_diff = torch.zeros(env.base.shape, device="cuda", dtype=torch.float64)
+    d_spec = torch.zeros(env.specular.shape, device="cuda", dtype=torch.float64)
+    for i, (cam, tgt) in enumerate(zip(cams, targets)):
+        res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
+        val, g = ss.image_loss(res.rgb, tgt, tone="hdr-loss", lambda_ssim=0.2)
+        loss += val
+        g_alpha = None
+        if with_masks:
+            sv, ga = ss.silhouette_loss(res.alpha, masks[i])
+            loss += 0.3 * sv
+            g_alpha = 0.3 * ga
+        back = ss.backward_image(cloud, res, g_rgb=g, g_alpha=g_alpha)
+        for k in PARAMS:
+            acc[k] += getattr(back, k).reshape(acc[k].shape)
+        d_diff += back.d_diffuse
+        d_spec += back.d_specular
+    assert float(ts.loss_f.item()) == pytest.approx(loss, rel=1e-5)
+    for k in PARAMS:
+        bad, err = grad_close(ts.grads[k], acc[k])
+        assert bad == 0, (k, err)
+    _, g_env = env.env_gradient(d_diff, d_spec)
+    assert grad_close(ts.g_env_log, g_env, rel=1e-3)[0] == 0
