@@ -23,8 +23,9 @@ targets = [ss.render(gtc, c, ss.RenderOptions(), env=gt_env).rgb.contiguous() fo
 del gtc
 cloud = ss.SurfelCloud(**init)
 env = ss.EnvironmentLight(np.log(env_base))
+LOSS = os.environ.get("LOSS", "l1")
 for S in (1, 2, 3):
-    ts = TrainStep(cloud, env, 800, 800, streams=S)
+    ts = TrainStep(cloud, env, 800, 800, streams=S, loss=LOSS)
     ts.size_pairs(cams[:2])
     for _ in range(2):
         ts.step(cams, targets)
