@@ -196,6 +196,21 @@ int ss_tone_map_backward(int64_t n, const float *img, int tone_mode, const float
 int ss_silhouette_loss(int64_t n, const float *alpha, const float *mask, double *out, float *grad,
                        double *workspace, void *stream);
 
+/* ---- oriented KNN index + normal consistency ------------
+ * ss_knn_oriented replaces NeighborIndex.rebuild (knn.py:31-81): for every
+ * surfel the k (<= 16) nearest other surfels with n_i . n_j > 0, ascending
+ * (distance, index), -1 padded, into neighbors (n, k) int64; mean_dist (n)
+ * float64 = mean accepted distance, or the distance to the nearest other
+ * surfel when none qualifies.  The grid is the caller's: cells of
+ * ss_grid_cells (origin3, cell, dim <= 1024), sorted (sorted_cells, order).
+ * ss_normal_consistency replaces normal_consistency_loss (losses.py:189-220):
+ * loss (1 double), g_quats (n, 4) float32; g_normals: n*3 float64 scratch. */
+int ss_knn_oriented(int n, const float *centers, const float *quats, const int32_t *order,
+                    const int32_t *sorted_cells, const float *origin3, float cell, int dim, int k,
+                    int64_t *neighbors, double *mean_dist, void *stream);
+int ss_normal_consistency(int n, int k, const float *centers, const float *quats, const int64_t *neighbors,
+                          const double *mean_dist, double *loss, double *g_normals, float *g_quats, void *stream);
+
 /* ---- chain backward -------------------------------------------------------
  * Replaces the per-surfel tail of backward_image() (backward.py:398-461,
  * 473-548), shade_backward() (shading.py:525-616) and quat_frame_backward()

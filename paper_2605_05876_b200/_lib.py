@@ -97,6 +97,9 @@ _SIGNATURES = {
     "ss_tone_map": [ctypes.c_int64, c_p, ctypes.c_int, c_p, c_p],
     "ss_tone_map_backward": [ctypes.c_int64, c_p, ctypes.c_int, c_p, c_p, c_p],
     "ss_silhouette_loss": [ctypes.c_int64, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_knn_oriented": [ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_int,
+                        ctypes.c_int, c_p, c_p, c_p],
+    "ss_normal_consistency": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_split_children": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64, c_p],
 }

@@ -91,3 +91,23 @@ def silhouette_loss(alpha, mask):
     _lib.check(lib.ss_silhouette_loss(a.numel(), _lib.ptr(a), _lib.ptr(m), _lib.ptr(out), _lib.ptr(grad),
                                       _lib.ptr(ws), _lib.stream_ptr()), "ss_silhouette_loss")
     return float(out.item()), grad
+
+
+def normal_consistency_loss(cloud, index):
+    """losses.py:189-220: mean over surfels and neighbour slots of
+    w_ij (1 - n_i . n_j), w_ij = exp(-|c_i - c_j|^2 / (2 sigma_i^2)); returns
+    (loss, quaternion gradient (N, 4) float32)."""
+    n = len(cloud)
+    if index.neighbors.shape[0] != n:
+        raise ValueError("index built for a different cloud size")
+    dev = cloud.centers.device
+    g_q = torch.zeros((n, 4), device=dev, dtype=torch.float32)
+    if n == 0:
+        return 0.0, g_q
+    lib = _lib.load()
+    loss = torch.zeros(1, device=dev, dtype=torch.float64)
+    g_n = torch.empty((n, 3), device=dev, dtype=torch.float64)
+    _lib.check(lib.ss_normal_consistency(n, index.neighbors.shape[1], _lib.ptr(cloud.centers), _lib.ptr(cloud.quats),
+                                         _lib.ptr(index.neighbors), _lib.ptr(index.mean_dist), _lib.ptr(loss),
+                                         _lib.ptr(g_n), _lib.ptr(g_q), _lib.stream_ptr()), "ss_normal_consistency")
+    return float(loss.item()), g_q

@@ -189,3 +189,17 @@ def test_loss_oracle_matches_reference_goldens():
     v, g = O.silhouette_loss(d["alpha"], d["mask"])
     assert v == pytest.approx(float(d["sil"]), rel=1e-14)
     np.testing.assert_allclose(g, d["sil_grad"], rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("name", ["sphere", "shell"])
+def test_knn_oracle_matches_reference_goldens(name):
+    """oracle knn_oriented / normal_consistency vs the reference NeighborIndex
+    (scipy cKDTree) and normal_consistency_loss (tests/golden/make_golden_knn.py)."""
+    import os
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "knn.npz"))
+    nb, md = O.knn_oriented(d[f"{name}_centers"], d[f"{name}_quats"], k=8)
+    np.testing.assert_array_equal(nb, d[f"{name}_neighbors"])
+    np.testing.assert_allclose(md, d[f"{name}_mean_dist"], rtol=1e-14, atol=0)
+    loss, g = O.normal_consistency(d[f"{name}_centers"], d[f"{name}_quats"], nb, md)
+    assert loss == pytest.approx(float(d[f"{name}_nc_loss"]), rel=1e-13)
+    np.testing.assert_allclose(g, d[f"{name}_nc_grad"], rtol=1e-9, atol=1e-16)
