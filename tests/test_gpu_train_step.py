@@ -125,3 +125,32 @@ def test_photometric_train_step_matches_api_path(with_masks):
         assert bad == 0, (k, err)
     _, g_env = env.env_gradient(d_diff, d_spec)
     assert grad_close(ts.g_env_log, g_env, rel=1e-3)[0] == 0
+
+
+@pytest.mark.parametrize("wh", [(97, 61), (33, 120)])
+def test_train_step_ragged_image(wh):
+    """Image sizes that are not tile multiples (partial tiles and 8x4 warp
+    blocks at the right/bottom edges), training path vs API path."""
+    W, H = wh
+    gt = scenes.config0(2, 2000)
+    init = scenes.perturb(gt, 3)
+    env_base = scenes.env_lognormal(16, 32, 4)
+    cams = ss.fibonacci_cameras(3, 3.0, W, H, fov_y_deg=40.0)
+    gt_env = ss.EnvironmentLight.from_base(env_base)
+    gtc = ss.SurfelCloud(**gt)
+    targets = [ss.render(gtc, c, ss.RenderOptions(), env=gt_env).rgb.contiguous() for c in cams]
+    cloud = ss.SurfelCloud(**init)
+    env = ss.EnvironmentLight.from_base(env_base)
+    ts = TrainStep(cloud, env, W, H)
+    ts.gradients(cams, targets)
+    torch.cuda.synchronize()
+    acc = {k: torch.zeros_like(ts.grads[k]) for k in PARAMS}
+    for cam, tgt in zip(cams, targets):
+        res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
+        _, g = ss.photometric_loss(res.rgb, tgt, lambda_ssim=0.0)
+        back = ss.backward_image(cloud, res, g_rgb=g)
+        for k in PARAMS:
+            acc[k] += getattr(back, k).reshape(acc[k].shape)
+    for k in PARAMS:
+        bad, err = grad_close(ts.grads[k], acc[k])
+        assert bad == 0, (k, err)
