@@ -98,11 +98,12 @@ typedef struct SsProjAux {
  * state the float32 shading adjoint of ss_chain_backward recomputes);
  * SS_COLOR_ALBEDO uses sigmoid(albedo_raw).  `flags` (int[4],
  * zeroed by caller) receives [0] zero-norm quaternion seen, [1] non-finite
- * colour seen. */
+ * colour seen.  bininfo (n x 4 uint32, nullable): the binning input of
+ * ss_bin_sort (packed rect, order-preserving z_start bits). */
 int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                   int color_source, const float *colors_in, const SsEnv *env,
                   float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
-                  const SsProjAux *aux, int32_t *flags, void *stream);
+                  uint32_t *bininfo, const SsProjAux *aux, int32_t *flags, void *stream);
 
 /* ---- tile binning with deterministic order ---------------------------------
  * Replaces the rest of bin_and_sort() (rasterizer.py:106-116): exclusive scan
@@ -112,8 +113,10 @@ int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessO
  * pair_capacity bounds pair_rec/keys; flags[2] is set when it overflowed.
  * keys: uint64 scratch of pair_capacity entries; cursors: ntiles ints scratch.
  * pair_rect (2 uint32 per pair) receives each pair's record rect packed as
- * (x0 | y0 << 16, x1 | y1 << 16), the rasterisers' cull input. */
-int ss_bin_sort(int n, const float *records, const int8_t *cull, int width, int height, int tile,
+ * (x0 | y0 << 16, x1 | y1 << 16), the rasterisers' cull input.  bininfo: the
+ * preprocess output (n x 4 uint32: packed rect, order-preserving z_start
+ * bits, 0) -- 16 bytes per record instead of the 96-byte record. */
+int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, int width, int height, int tile,
                 const int32_t *tile_counts, int32_t *tile_offsets, int32_t *cursors,
                 uint64_t *keys, int32_t *pair_rec, uint32_t *pair_rect, int64_t pair_capacity,
                 int32_t *flags, void *stream);

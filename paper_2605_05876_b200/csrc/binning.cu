@@ -25,10 +25,6 @@ constexpr int kSmallCap = 2048;
 constexpr int kHeavyThreads = 1024;
 constexpr int kHeavyCap = 12288;
 
-__device__ __forceinline__ uint32_t orderable(float z) {
-    uint32_t u = __float_as_uint(z == 0.0f ? 0.0f : z);  // -0.0 == +0.0 like lexsort
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
     const int32_t *__restrict__ counts, int ntiles, int32_t *__restrict__ offsets,
@@ -86,7 +82,7 @@ constexpr int kScatterThreads = 1024;
 constexpr int kScatterPerThread = 4;
 
 __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
-    int n, const SsRecord *__restrict__ records, const int8_t *__restrict__ cull, int ntx, int ntiles, int tile,
+    int n, const uint4 *__restrict__ bininfo, const int8_t *__restrict__ cull, int ntx, int ntiles, int tile,
     const int32_t *__restrict__ offsets, int32_t *__restrict__ cursors, uint64_t *__restrict__ keys,
     int64_t capacity)
 {
@@ -98,8 +94,9 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     for (int k = 0; k < kScatterPerThread; ++k) {
         const int i = first + k * kScatterThreads + threadIdx.x;
         if (i >= n || cull[i] != 0) continue;
-        const int4 r = records[i].r;
-        const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
+        const uint4 b = bininfo[i];
+        const int tx0 = (int)(b.x & 0xffff) / tile, ty0 = (int)(b.x >> 16) / tile;
+        const int tx1 = ((int)(b.y & 0xffff) - 1) / tile, ty1 = ((int)(b.y >> 16) - 1) / tile;
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&s_cnt[ty * ntx + tx], 1);
     }
@@ -113,9 +110,10 @@ __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     for (int k = 0; k < kScatterPerThread; ++k) {
         const int i = first + k * kScatterThreads + threadIdx.x;
         if (i >= n || cull[i] != 0) continue;
-        const int4 r = records[i].r;
-        const uint64_t key = ((uint64_t)orderable(records[i].d.z) << 32) | (uint32_t)i;
-        const int tx0 = r.x / tile, ty0 = r.y / tile, tx1 = (r.z - 1) / tile, ty1 = (r.w - 1) / tile;
+        const uint4 b = bininfo[i];
+        const uint64_t key = ((uint64_t)b.z << 32) | (uint32_t)i;
+        const int tx0 = (int)(b.x & 0xffff) / tile, ty0 = (int)(b.x >> 16) / tile;
+        const int tx1 = ((int)(b.y & 0xffff) - 1) / tile, ty1 = ((int)(b.y >> 16) - 1) / tile;
         for (int ty = ty0; ty <= ty1; ++ty)
             for (int tx = tx0; tx <= tx1; ++tx) {
                 const int t = ty * ntx + tx;
@@ -154,9 +152,8 @@ __device__ __forceinline__ void bitonic_sort(int n, Load ld, Swap sw) {
 }
 
 // packed pixel rect of a record, in pair order, for the rasterisers' warp cull
-__device__ __forceinline__ uint2 pack_rect(const SsRecord *__restrict__ recs, int rec) {
-    const int4 r = recs[rec].r;
-    return make_uint2((uint32_t)r.x | ((uint32_t)r.y << 16), (uint32_t)r.z | ((uint32_t)r.w << 16));
+__device__ __forceinline__ uint2 pack_rect(const uint4 *__restrict__ bininfo, int rec) {
+    return *reinterpret_cast<const uint2 *>(bininfo + rec);
 }
 
 // 32 keys per warp sorted in registers (bitonic network over shuffles).
@@ -190,7 +187,7 @@ __device__ __forceinline__ int merge_split(const uint64_t *x, int la, const uint
 template <int kThreads, int kCap, bool kHeavy>
 __global__ void __launch_bounds__(kThreads) tile_sort_kernel(
     const int32_t *__restrict__ offsets, uint64_t *__restrict__ keys, int32_t *__restrict__ pair_rec,
-    uint2 *__restrict__ pair_rect, const SsRecord *__restrict__ recs, int64_t capacity)
+    uint2 *__restrict__ pair_rect, const uint4 *__restrict__ recs, int64_t capacity)
 {
     extern __shared__ uint64_t skeys[];
     const int t = blockIdx.x;
@@ -260,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) tile_sort_kernel(
 
 }  // namespace
 
-extern "C" int ss_bin_sort(int n, const float *records, const int8_t *cull, int width, int height, int tile,
+extern "C" int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, int width, int height, int tile,
                            const int32_t *tile_counts, int32_t *tile_offsets, int32_t *cursors,
                            uint64_t *keys, int32_t *pair_rec, uint32_t *pair_rect, int64_t pair_capacity,
                            int32_t *flags, void *stream)
@@ -285,16 +282,16 @@ extern "C" int ss_bin_sort(int n, const float *records, const int8_t *cull, int 
         cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int per_cta = kScatterThreads * kScatterPerThread;
         scatter_kernel<<<(n + per_cta - 1) / per_cta, kScatterThreads, smem, st>>>(
-            n, reinterpret_cast<const SsRecord *>(records), cull, ntx, ntiles, tile, tile_offsets, cursors, keys,
+            n, reinterpret_cast<const uint4 *>(bininfo), cull, ntx, ntiles, tile, tile_offsets, cursors, keys,
             pair_capacity);
         SS_CUDA_CHECK_LAUNCH();
     }
     tile_sort_kernel<kSmallThreads, kSmallCap, false><<<ntiles, kSmallThreads, 2 * kSmallCap * sizeof(uint64_t), st>>>(
-        tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const SsRecord *>(records),
+        tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const uint4 *>(bininfo),
         pair_capacity);
     SS_CUDA_CHECK_LAUNCH();
     tile_sort_kernel<kHeavyThreads, kHeavyCap, true><<<ntiles, kHeavyThreads, 2 * kHeavyCap * sizeof(uint64_t), st>>>(
-        tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const SsRecord *>(records),
+        tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const uint4 *>(bininfo),
         pair_capacity);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;

@@ -42,6 +42,7 @@ class ViewState:
     color_source: int
     aux: dict = field(default_factory=dict)
     pair_rect: torch.Tensor | None = None  # (P, 2) int32 packed rects in pair order (after binning)
+    bininfo: torch.Tensor | None = None    # (N, 4) int32 binning input (packed rect, z_start key)
 
     @property
     def ntx(self):
@@ -57,7 +58,7 @@ def make_opts(options, tile=16):
 
 
 def run_preprocess(cloud, camera, options, color_source, colors=None, env=None, tile=16, want_aux=False,
-                   records=None, cull=None, tile_counts=None, flags=None):
+                   records=None, cull=None, tile_counts=None, flags=None, bininfo=None):
     lib = _lib.load()
     n = len(cloud)
     dev = cloud.centers.device
@@ -65,6 +66,7 @@ def run_preprocess(cloud, camera, options, color_source, colors=None, env=None, 
     ntiles = ((W + tile - 1) // tile) * ((H + tile - 1) // tile)
     records = torch.empty((n, _lib.REC_FLOATS), device=dev, dtype=torch.float32) if records is None else records
     cull = torch.empty(n, device=dev, dtype=torch.int8) if cull is None else cull
+    bininfo = torch.empty((n, 4), device=dev, dtype=torch.int32) if bininfo is None else bininfo
     if tile_counts is None:
         tile_counts = torch.zeros(ntiles, device=dev, dtype=torch.int32)
     else:
@@ -90,10 +92,10 @@ def run_preprocess(cloud, camera, options, color_source, colors=None, env=None, 
         colors = torch.as_tensor(colors, device=dev, dtype=torch.float32).contiguous()
     rc = lib.ss_preprocess(ctypes_ref(cl), ctypes_ref(cam), ctypes_ref(opt), int(color_source), _lib.ptr(colors),
                            ctypes_ref(envs) if envs is not None else None, _lib.ptr(records), _lib.ptr(cull), None,
-                           _lib.ptr(tile_counts), ctypes_ref(auxs) if auxs is not None else None, _lib.ptr(flags),
-                           _lib.stream_ptr())
+                           _lib.ptr(tile_counts), _lib.ptr(bininfo), ctypes_ref(auxs) if auxs is not None else None,
+                           _lib.ptr(flags), _lib.stream_ptr())
     _lib.check(rc, "ss_preprocess")
-    return ViewState(records, cull, tile_counts, flags, W, H, tile, options, color_source, aux)
+    return ViewState(records, cull, tile_counts, flags, W, H, tile, options, color_source, aux, bininfo=bininfo)
 
 
 def ctypes_ref(s):

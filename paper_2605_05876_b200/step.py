@@ -80,6 +80,7 @@ class ViewBuffers:
         i32 = dict(device=device, dtype=torch.int32)
         self.records = torch.empty((n, _lib.REC_FLOATS), **f32)
         self.cull = torch.empty(n, device=device, dtype=torch.int8)
+        self.bininfo = torch.empty((n, 4), **i32)
         self.tile_counts = torch.zeros(ntiles, **i32)
         self.flags = torch.zeros(4, **i32)
         self.offsets = torch.empty(ntiles + 1, **i32)
@@ -198,7 +199,7 @@ class TrainStep:
         camst = _lib.make_camera(cam)
         rc = self.lib.ss_preprocess(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                     _lib.SS_COLOR_IBL_F32, None, ctypes.byref(self._envs), _lib.ptr(b.records),
-                                    _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts), None,
+                                    _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts), _lib.ptr(b.bininfo), None,
                                     _lib.ptr(b.flags), _lib.stream_ptr())
         _lib.check(rc, "ss_preprocess")
         return camst
@@ -216,7 +217,7 @@ class TrainStep:
         camst = self._preprocess(cam, b)
         self._ev_end(ev)
         ev = self._ev_begin("bin_sort")
-        _lib.check(lib.ss_bin_sort(self.n, _lib.ptr(b.records), _lib.ptr(b.cull), self.W, self.H, self.tile,
+        _lib.check(lib.ss_bin_sort(self.n, _lib.ptr(b.bininfo), _lib.ptr(b.cull), self.W, self.H, self.tile,
                                    _lib.ptr(b.tile_counts), _lib.ptr(b.offsets), _lib.ptr(b.cursors),
                                    _lib.ptr(b.keys), _lib.ptr(b.pair), _lib.ptr(b.pair_rect), b.capacity,
                                    _lib.ptr(b.flags), s),
