@@ -278,6 +278,13 @@ int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const in
  * floats; m, v float32 state; bias corrections from step t (>= 1). */
 int ss_adam_step(int64_t count, float *param, const float *grad, float *m, float *v,
                  int t, float lr, float beta1, float beta2, float eps, void *stream);
+/* ss_adam_multi: the same update for up to 8 tensors in ONE launch (params[k],
+ * grads[k], m[k], v[k] of counts[k] floats, step count steps[k], lr lrs[k]);
+ * tensors with quat_flags[k] != 0 (n x 4) are renormalised right after their
+ * update (train.py:241-246). */
+int ss_adam_multi(int ntensors, float *const *params, const float *const *grads, float *const *m,
+                  float *const *v, const int64_t *counts, const int *steps, const float *lrs,
+                  const int *quat_flags, float beta1, float beta2, float eps, void *stream);
 /* q <- q / |q| after the step (train.py:246). */
 int ss_normalize_quats(int n, float *quats, void *stream);
 

@@ -83,6 +83,8 @@ _SIGNATURES = {
     "ss_adam_step": [ctypes.c_int64, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_float, ctypes.c_float,
                      ctypes.c_float, ctypes.c_float, c_p],
     "ss_normalize_quats": [ctypes.c_int, c_p, c_p],
+    "ss_adam_multi": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_float, ctypes.c_float,
+                      ctypes.c_float, c_p],
     "ss_grid_cells": [ctypes.c_int, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_int, c_p, c_p],
     "ss_isolation": [ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float,
                      ctypes.c_int, c_p, c_p],

@@ -36,6 +36,39 @@ class Adam:
         _lib.check(rc, "ss_adam_step")
         return param
 
+    def step_multi(self, items, renorm_quats=None):
+        """Adam on several tensors in ONE fused launch (csrc/optim.cu
+        ss_adam_multi): items = [(name, param, grad, lr), ...]; the tensor
+        named `renorm_quats` (n, 4) is renormalised right after its update
+        (train.py:241-246).  Same arithmetic as step() per tensor."""
+        import ctypes
+        if not 1 <= len(items) <= 8:
+            raise ValueError("step_multi takes 1..8 tensors")
+        cols = {k: [] for k in ("p", "g", "m", "v", "n", "t", "lr", "q")}
+        keep = []
+        for name, param, grad, lr in items:
+            if tuple(grad.shape) != tuple(param.shape):
+                raise ValueError(f"gradient shape {tuple(grad.shape)} != param shape {tuple(param.shape)}")
+            if name not in self.m:
+                self.m[name] = torch.zeros_like(param, dtype=torch.float32)
+                self.v[name] = torch.zeros_like(param, dtype=torch.float32)
+                self.t[name] = 0
+            self.t[name] += 1
+            g = grad.to(torch.float32).contiguous()
+            keep.append(g)
+            for key, val in (("p", param.data_ptr()), ("g", g.data_ptr()), ("m", self.m[name].data_ptr()),
+                             ("v", self.v[name].data_ptr()), ("n", param.numel()), ("t", self.t[name]),
+                             ("lr", float(lr)), ("q", int(name == renorm_quats))):
+                cols[key].append(val)
+        k = len(items)
+        ptrs = {c: (ctypes.c_void_p * k)(*cols[c]) for c in ("p", "g", "m", "v")}
+        lib = _lib.load()
+        rc = lib.ss_adam_multi(k, ptrs["p"], ptrs["g"], ptrs["m"], ptrs["v"], (ctypes.c_int64 * k)(*cols["n"]),
+                               (ctypes.c_int * k)(*cols["t"]), (ctypes.c_float * k)(*cols["lr"]),
+                               (ctypes.c_int * k)(*cols["q"]), self.beta1, self.beta2, self.eps, _lib.stream_ptr())
+        _lib.check(rc, "ss_adam_multi")
+        return [it[1] for it in items]
+
     def remap(self, name, index):
         """adam.py:43-58: reindex rows; index -1 rows start from zero."""
         if name not in self.m:

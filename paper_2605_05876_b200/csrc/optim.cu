@@ -31,6 +31,62 @@ __global__ void normalize_quats_kernel(int n, float4 *__restrict__ q) {
     q[i] = a;
 }
 
+// Multi-tensor Adam: up to kMaxTensors (param, grad, m, v) segments in one
+// launch.  A segment flagged `quat` is processed one quaternion (4 floats)
+// per thread and renormalised right after its update (train.py:241-246).
+constexpr int kMaxTensors = 8;
+struct AdamSeg {
+    float *p;
+    const float *g;
+    float *m, *v;
+    int64_t count;      // floats
+    int64_t first;      // first work item of the segment
+    double lr, c1, c2;  // bias corrections 1 - beta^t
+    int quat;
+};
+struct AdamMulti {
+    AdamSeg seg[kMaxTensors];
+    int nseg;
+    int64_t items;
+    double b1, b2, eps;
+};
+
+__device__ __forceinline__ float adam_one(float p, float g, float *m, float *v, const AdamSeg &s, const AdamMulti &A) {
+    const double gg = g;
+    const double mm = A.b1 * (double)*m + (1.0 - A.b1) * gg;
+    const double vv = A.b2 * (double)*v + (1.0 - A.b2) * gg * gg;
+    *m = (float)mm;
+    *v = (float)vv;
+    const double mh = mm / s.c1, vh = vv / s.c2;
+    return p - (float)(s.lr * mh / (sqrt(vh) + A.eps));
+}
+
+__global__ void adam_multi_kernel(AdamMulti A) {
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < A.items;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (k + 1 < A.nseg && it >= A.seg[k + 1].first) ++k;
+        const AdamSeg &s = A.seg[k];
+        const int64_t j = it - s.first;
+        if (s.quat) {
+            float4 p = reinterpret_cast<float4 *>(s.p)[j];
+            const float4 g = reinterpret_cast<const float4 *>(s.g)[j];
+            float4 m = reinterpret_cast<float4 *>(s.m)[j], v = reinterpret_cast<float4 *>(s.v)[j];
+            p.x = adam_one(p.x, g.x, &m.x, &v.x, s, A);
+            p.y = adam_one(p.y, g.y, &m.y, &v.y, s, A);
+            p.z = adam_one(p.z, g.z, &m.z, &v.z, s, A);
+            p.w = adam_one(p.w, g.w, &m.w, &v.w, s, A);
+            const float nrm = sqrtf(((p.x * p.x + p.y * p.y) + p.z * p.z) + p.w * p.w);
+            if (nrm > 0.f) { p.x /= nrm; p.y /= nrm; p.z /= nrm; p.w /= nrm; }
+            reinterpret_cast<float4 *>(s.p)[j] = p;
+            reinterpret_cast<float4 *>(s.m)[j] = m;
+            reinterpret_cast<float4 *>(s.v)[j] = v;
+        } else {
+            s.p[j] = adam_one(s.p[j], s.g[j], s.m + j, s.v + j, s, A);
+        }
+    }
+}
+
 struct Grid { float ox, oy, oz, cell; int dim; };
 
 __device__ __forceinline__ int axis_cell(float c, float o, float cell, int dim) {
@@ -116,6 +172,36 @@ extern "C" int ss_adam_step(int64_t count, float *param, const float *grad, floa
     const double c1 = 1.0 - pow((double)beta1, t), c2 = 1.0 - pow((double)beta2, t);
     const int blocks = (int)((count + 255) / 256 < 148 * 16 ? (count + 255) / 256 : 148 * 16);
     adam_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(count, param, grad, m, v, lr, beta1, beta2, eps, c1, c2);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_adam_multi(int ntensors, float *const *params, const float *const *grads, float *const *m,
+                             float *const *v, const int64_t *counts, const int *steps, const float *lrs,
+                             const int *quat_flags, float beta1, float beta2, float eps, void *stream) {
+    if (ntensors < 1 || ntensors > kMaxTensors || !params || !grads || !m || !v || !counts || !steps || !lrs)
+        return SS_ERR_INVALID;
+    AdamMulti A{};
+    A.nseg = ntensors;
+    A.b1 = beta1; A.b2 = beta2; A.eps = eps;
+    int64_t items = 0;
+    for (int k = 0; k < ntensors; ++k) {
+        AdamSeg &sg = A.seg[k];
+        sg.p = params[k]; sg.g = grads[k]; sg.m = m[k]; sg.v = v[k];
+        sg.count = counts[k];
+        sg.quat = quat_flags ? quat_flags[k] : 0;
+        if (sg.count < 0 || steps[k] < 1 || (sg.quat && sg.count % 4)) return SS_ERR_INVALID;
+        if (sg.count > 0 && (!sg.p || !sg.g || !sg.m || !sg.v)) return SS_ERR_INVALID;
+        sg.lr = lrs[k];
+        sg.c1 = 1.0 - pow((double)beta1, steps[k]);
+        sg.c2 = 1.0 - pow((double)beta2, steps[k]);
+        sg.first = items;
+        items += sg.quat ? sg.count / 4 : sg.count;
+    }
+    A.items = items;
+    if (items == 0) return SS_OK;
+    const int blocks = (int)((items + 255) / 256 < 148 * 16 ? (items + 255) / 256 : 148 * 16);
+    adam_multi_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(A);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

@@ -171,7 +171,7 @@ class TrainStep:
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
         self._stage = None
         self.launches_per_view = 10    # preprocess, scan, scatter, tile sort x2, train fwd, ndc + record bwd x2, chain
-        self.launches_per_step_fixed = 4 + 7 + 1 + 4  # env adjoint, Adam x7, quat renorm, env refresh
+        self.launches_per_step_fixed = 4 + 1 + 4  # env adjoint, fused Adam (+ quat renorm), env refresh
 
     # -- buffers -----------------------------------------------------------
     def _alloc_pairs(self, cap):
@@ -340,12 +340,9 @@ class TrainStep:
 
     def apply(self, lr_scale=1.0):
         """Adam on all tensors, quaternion renorm, env refresh (train.py:241-248)."""
-        for k in PARAMS:
-            p = getattr(self.cloud, k)
-            self.adam.step(k, p, self.grads[k], self.lrs[k] * lr_scale)
-        _lib.check(self.lib.ss_normalize_quats(self.n, _lib.ptr(self.cloud.quats), _lib.stream_ptr()),
-                   "ss_normalize_quats")
-        self.adam.step("env_base_log", self.env.base_log, self.g_env_log, self.lrs["env_base_log"] * lr_scale)
+        items = [(k, getattr(self.cloud, k), self.grads[k], self.lrs[k] * lr_scale) for k in PARAMS]
+        items.append(("env_base_log", self.env.base_log, self.g_env_log, self.lrs["env_base_log"] * lr_scale))
+        self.adam.step_multi(items, renorm_quats="quats")  # one launch, quaternions renormalised in it
         self.env.refresh()
 
     def step(self, cameras, targets, masks=None):

@@ -92,3 +92,22 @@ def test_train_step_stats_feed_refinement():
     assert float(stats.grad_sum.sum()) > 0
     new, imap, reasons = ss.refine_topology(cloud, stats, np.full(len(cloud), 0.001), 2300, quantile=0.95)
     assert len(new) <= 2300 and reasons["split"] > 0
+
+
+def test_adam_multi_equals_per_tensor_steps():
+    """The fused multi-tensor launch (with the quaternion renormalisation)
+    equals per-tensor Adam.step + normalize_quats bit for bit."""
+    rng = np.random.default_rng(9)
+    shapes = {"centers": (500, 3), "quats": (500, 4), "log_scales": (500, 2), "metallic_raw": (500,)}
+    ps = {k: torch.tensor(rng.normal(size=s), dtype=torch.float32, device="cuda") for k, s in shapes.items()}
+    qs = {k: v.clone() for k, v in ps.items()}
+    a, b = ss.Adam(), ss.Adam()
+    for it in range(3):
+        gs = {k: torch.tensor(rng.normal(size=s), dtype=torch.float32, device="cuda") for k, s in shapes.items()}
+        for k in shapes:
+            a.step(k, ps[k], gs[k], 0.01 * (it + 1))
+        ss.normalize_quats(ps["quats"])
+        b.step_multi([(k, qs[k], gs[k], 0.01 * (it + 1)) for k in shapes], renorm_quats="quats")
+    for k in shapes:
+        assert torch.equal(ps[k], qs[k]), k
+        assert torch.equal(a.m[k], b.m[k]) and torch.equal(a.v[k], b.v[k])
