@@ -17,6 +17,7 @@ from .knn import NeighborIndex
 from .adam import Adam, normalize_quats
 from .densify import DensifyStats, mask_votes, prune_keep_mask, refine_topology, select_split, split_cloud
 from .step import TrainStep
+from . import sceneio
 
 __version__ = "0.1.0"
 
@@ -26,4 +27,4 @@ __all__ = ["Camera", "fibonacci_cameras", "look_at", "orbit_cameras", "perspecti
            "brdf_lut", "shade_surfels", "tone_map", "tone_map_backward", "photometric_loss", "silhouette_loss",
            "ssim_loss", "image_loss", "normal_consistency_loss", "NeighborIndex",
            "Adam", "normalize_quats", "DensifyStats", "mask_votes", "prune_keep_mask", "refine_topology",
-           "select_split", "split_cloud", "TrainStep"]
+           "select_split", "split_cloud", "TrainStep", "sceneio"]

@@ -8,6 +8,7 @@ evaluated in float64 per element.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -90,8 +91,24 @@ class Adam:
         for name in self.m:
             out[f"adam_m_{name}"] = self.m[name].cpu().numpy()
             out[f"adam_v_{name}"] = self.v[name].cpu().numpy()
-            out[f"adam_t_{name}"] = self.t[name]
+            out[f"adam_t_{name}"] = np.asarray(self.t[name], dtype=np.int64)
         return out
+
+
+def _load_state(self, arrays):
+    """adam.py:69-81: restore moments and step counts from checkpoint arrays."""
+    self.m.clear(); self.v.clear(); self.t.clear()
+    for key, val in arrays.items():
+        for pre, store in (("adam_m_", self.m), ("adam_v_", self.v)):
+            if key.startswith(pre):
+                store[key[len(pre):]] = torch.as_tensor(np.asarray(val), device="cuda", dtype=torch.float32).contiguous()
+        if key.startswith("adam_t_"):
+            self.t[key[len("adam_t_"):]] = int(val)
+    if set(self.m) != set(self.v) or set(self.m) != set(self.t):
+        raise ValueError("incomplete optimizer state")
+
+
+Adam.load_state_arrays = _load_state
 
 
 def normalize_quats(quats):
