@@ -77,13 +77,20 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     int ncl = 0;
     float th0 = 0.f, th1 = 0.f, th2 = 0.f;  // first three closing depths (kTrain)
 
-    auto close_layer = [&]() {
-        const float a_k = -expm1f(-Wg);
-        const float inv_w = 1.f / Wg;
+    // one layer of the over-compositing (rasterizer.py:168-181)
+    auto composite = [&](float w, float c0, float c1, float c2) {
+        const float a_k = -expm1f(-w);
+        const float inv_w = 1.f / w;
         const float ta = T * a_k;
-        o0 += ta * C0 * inv_w; o1 += ta * C1 * inv_w; o2 += ta * C2 * inv_w;
-        dnum += ta * Zg * inv_w; dden += ta;
+        o0 += ta * c0 * inv_w; o1 += ta * c1 * inv_w; o2 += ta * c2 * inv_w;
+        if (!kTrain) { dnum += ta * Zg * inv_w; dden += ta; }
         T *= 1.f - a_k;
+    };
+    // closing a layer in the training walk only parks its raw sums: the
+    // compositing is replayed (same operations, same order) once per pixel
+    // after the walk, off the hot loop
+    auto close_layer = [&]() {
+        if (!kTrain) composite(Wg, C0, C1, C2);
         if (kExtras && P.st.w) {
             const size_t o = pix * P.k_max + layers;
             P.st.w[o] = Wg; P.st.c[3 * o] = C0; P.st.c[3 * o + 1] = C1; P.st.c[3 * o + 2] = C2;
@@ -139,6 +146,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     double lsum = 0.0;
     if (live) {
         if (Wg > 0.f) close_layer();
+        if (kTrain)
+            for (int m = 0; m < layers; ++m) composite(lw[m], lc0[m], lc1[m], lc2[m]);
         const float r0 = o0 + T * P.bg0, r1 = o1 + T * P.bg1, r2 = o2 + T * P.bg2;
         if (!kTrain || P.rgb) {
             P.rgb[3 * pix] = r0; P.rgb[3 * pix + 1] = r1; P.rgb[3 * pix + 2] = r2;
