@@ -119,7 +119,9 @@ int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessO
 int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, int width, int height, int tile,
                 const int32_t *tile_counts, int32_t *tile_offsets, int32_t *cursors,
                 uint64_t *keys, int32_t *pair_rec, uint32_t *pair_rect, int64_t pair_capacity,
-                int32_t *flags, void *stream);
+                int32_t *flags, int32_t *tile_order, void *stream);
+/* tile_order (ntiles int32, nullable): a launch order for the rasterisers,
+ * tiles grouped by descending pair count (heavy first). */
 
 /* ---- raster forward -------------------------------------------------------
  * Replaces _forward_kernel (rasterizer.py:119-249), interval depth mode.
@@ -167,7 +169,8 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
 int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
                      const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
                      const float *background, int k_max, const float *target, float *coef, float *thr,
-                     int32_t *pix_hdr, double *loss_sum, float *rgb, float *alpha, void *stream);
+                     int32_t *pix_hdr, double *loss_sum, float *rgb, float *alpha, const int32_t *tile_order,
+                     void *stream);
 /* ss_train_forward with target == NULL is the DEFERRED-loss variant (any
  * image loss, e.g. the reference fit loss of train.py:194-206): it writes rgb
  * (required), alpha (nullable) and, per pixel and layer, the raw layer sums

@@ -64,7 +64,7 @@ _lib = None
 _SIGNATURES = {
     "ss_preprocess": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_bin_sort": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
-                    c_p, c_p, c_p, ctypes.c_int64, c_p, c_p],
+                    c_p, c_p, c_p, ctypes.c_int64, c_p, c_p, c_p],
     "ss_raster_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
                           ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_raster_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p,
@@ -89,7 +89,7 @@ _SIGNATURES = {
     "ss_isolation": [ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float,
                      ctypes.c_int, c_p, c_p],
     "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
-                         ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+                         ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_train_coefs": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), c_p],
     "ss_train_backward_records": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
                                   c_p, c_p, c_p],

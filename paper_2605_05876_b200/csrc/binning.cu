@@ -71,6 +71,26 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
     }
 }
 
+// Launch order for the rasterisers: tiles grouped by descending log2 of
+// their pair count (heavy tiles first, so the last wave is made of light
+// ones); the order within a group is irrelevant to the results.
+__global__ void __launch_bounds__(1024) tile_order_kernel(const int32_t *__restrict__ counts, int ntiles,
+                                                         int32_t *__restrict__ order)
+{
+    __shared__ int32_t hist[33], base[33];
+    if (threadIdx.x < 33) hist[threadIdx.x] = 0;
+    __syncthreads();
+    auto group = [](int c) { return c > 0 ? 32 - __clz(c) : 0; };  // 0 (empty) .. 32, larger = heavier
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) atomicAdd(&hist[group(counts[t])], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int g = 32; g >= 0; --g) { base[g] = acc; acc += hist[g]; }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) order[atomicAdd(&base[group(counts[t])], 1)] = t;
+}
+
 // Each record drops its key into every tile bucket of its rect.  Atomics on
 // the tile cursors are privatised per CTA: a CTA of 4096 records counts its
 // pairs per tile in shared memory, reserves one contiguous block per touched
@@ -260,7 +280,7 @@ __global__ void __launch_bounds__(kThreads) tile_sort_kernel(
 extern "C" int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, int width, int height, int tile,
                            const int32_t *tile_counts, int32_t *tile_offsets, int32_t *cursors,
                            uint64_t *keys, int32_t *pair_rec, uint32_t *pair_rect, int64_t pair_capacity,
-                           int32_t *flags, void *stream)
+                           int32_t *flags, int32_t *tile_order, void *stream)
 {
     if (width <= 0 || height <= 0 || tile <= 0 || !tile_counts || !tile_offsets || !cursors || !flags)
         return SS_ERR_INVALID;
@@ -276,6 +296,10 @@ extern "C" int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, i
     const int ntiles = ntx * nty;
     tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tile_counts, ntiles, tile_offsets, cursors, pair_capacity, flags);
     SS_CUDA_CHECK_LAUNCH();
+    if (tile_order) {
+        tile_order_kernel<<<1, 1024, 0, st>>>(tile_counts, ntiles, tile_order);
+        SS_CUDA_CHECK_LAUNCH();
+    }
     if (n > 0) {
         const size_t smem = 2 * (size_t)ntiles * sizeof(int32_t);
         if (smem > 220 * 1024) return SS_ERR_INVALID;  // > 28k tiles: not supported by the privatised scatter

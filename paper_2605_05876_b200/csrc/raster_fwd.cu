@@ -30,6 +30,7 @@ struct FwdParams {
     int W, H, tile, ntx, k_max;
     float bg0, bg1, bg2;
     const int32_t *offsets;
+    const int32_t *tile_order;  // nullable: launch order of the tiles (heavy first)
     const int32_t *pair_rec;
     const uint2 *pair_rect;
     const SsRecord *records;
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 {
     __shared__ PackedScratch scratch[kFwdWarps];
     const int ctas_per_tile = P.tile * P.tile / (32 * kFwdWarps);
-    const int t = blockIdx.x / ctas_per_tile;
+    const int t = P.tile_order ? P.tile_order[blockIdx.x / ctas_per_tile] : blockIdx.x / ctas_per_tile;
     const int wid_in_tile = (blockIdx.x % ctas_per_tile) * kFwdWarps + (threadIdx.x >> 5);
     const WarpPix wp = warp_pixels(t, P.ntx, P.tile, P.W, P.H, wid_in_tile);
     const int lane = wp.lane, wid = threadIdx.x >> 5;
@@ -301,13 +302,14 @@ extern "C" int ss_raster_forward(int width, int height, int tile, const int32_t 
 extern "C" int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
                                 const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
                                 int k_max, const float *target, float *coef, float *thr, int32_t *pix_hdr,
-                                double *loss_sum, float *rgb, float *alpha, void *stream)
+                                double *loss_sum, float *rgb, float *alpha, const int32_t *tile_order, void *stream)
 {
     FwdParams P;
     if (!fill_common(P, width, height, tile, tile_offsets, pair_rec, pair_rect, records, background, k_max)) return SS_ERR_INVALID;
     if (!coef || !thr || !pix_hdr) return SS_ERR_INVALID;
     if (target ? !loss_sum : !rgb) return SS_ERR_INVALID;  // fused L1 needs the loss sum, deferred mode the image
     P.alpha = alpha;
+    P.tile_order = tile_order;
     P.target = target;
     P.thr = thr;
     P.hdr = reinterpret_cast<int4 *>(pix_hdr);

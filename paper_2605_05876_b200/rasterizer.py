@@ -91,7 +91,7 @@ def bin_state(state: ViewState):
     rects = torch.empty((max(total, 1), 2), device=dev, dtype=torch.int32)
     rc = lib.ss_bin_sort(len(state.cull), _lib.ptr(state.bininfo), _lib.ptr(state.cull), state.width, state.height,
                          state.tile, _lib.ptr(state.tile_counts), _lib.ptr(offsets), _lib.ptr(cursors), _lib.ptr(keys),
-                         _lib.ptr(pair), _lib.ptr(rects), total, _lib.ptr(state.flags), _lib.stream_ptr())
+                         _lib.ptr(pair), _lib.ptr(rects), total, _lib.ptr(state.flags), None, _lib.stream_ptr())
     _lib.check(rc, "ss_bin_sort")
     state.pair_rect = rects
     return offsets, pair[:total]

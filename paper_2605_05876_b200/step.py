@@ -85,6 +85,7 @@ class ViewBuffers:
         self.flags = torch.zeros(4, **i32)
         self.offsets = torch.empty(ntiles + 1, **i32)
         self.cursors = torch.empty(ntiles, **i32)
+        self.tile_order = torch.empty(ntiles, **i32)
         self.coef = torch.empty((k_max, H * W, 4), **f32)
         self.thr = torch.empty((k_max, H * W), **f32)
         self.pix_hdr = torch.empty((H * W, 4), **i32)
@@ -170,7 +171,7 @@ class TrainStep:
         self._pairs, self._kept, self._nviews = [], [], 0
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
         self._stage = None
-        self.launches_per_view = 10    # preprocess, scan, scatter, tile sort x2, train fwd, ndc + record bwd x2, chain
+        self.launches_per_view = 11    # preprocess, scan, order, scatter, tile sort x2, train fwd, ndc + record bwd x2, chain
         self.launches_per_step_fixed = 4 + 1 + 4  # env adjoint, fused Adam (+ quat renorm), env refresh
 
     # -- buffers -----------------------------------------------------------
@@ -220,7 +221,7 @@ class TrainStep:
         _lib.check(lib.ss_bin_sort(self.n, _lib.ptr(b.bininfo), _lib.ptr(b.cull), self.W, self.H, self.tile,
                                    _lib.ptr(b.tile_counts), _lib.ptr(b.offsets), _lib.ptr(b.cursors),
                                    _lib.ptr(b.keys), _lib.ptr(b.pair), _lib.ptr(b.pair_rect), b.capacity,
-                                   _lib.ptr(b.flags), s),
+                                   _lib.ptr(b.flags), _lib.ptr(b.tile_order), s),
                    "ss_bin_sort")
         self._ev_end(ev)
         ev = self._ev_begin("train_forward")
@@ -228,13 +229,15 @@ class TrainStep:
             _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
                                             _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
                                             _lib.ptr(target), _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr),
-                                            _lib.ptr(self.loss), None, None, s), "ss_train_forward")
+                                            _lib.ptr(self.loss), None, None, _lib.ptr(b.tile_order), s),
+                       "ss_train_forward")
         else:
             # deferred loss: image -> loss kernels -> layer coefficients
             _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
                                             _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
                                             None, _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr), None,
-                                            _lib.ptr(b.rgb), _lib.ptr(b.alpha), s), "ss_train_forward")
+                                            _lib.ptr(b.rgb), _lib.ptr(b.alpha), _lib.ptr(b.tile_order), s),
+                       "ss_train_forward")
             out = b.imgloss(b.rgb, target, b.g_rgb, self.lambda_ssim, self.tone)
             self.loss += out[0:1]
             g_alpha = None
