@@ -41,7 +41,7 @@ __global__ void pixel_ndc_kernel(int W, int H, float *xs, float *ys, int32_t *bi
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < W) xs[k] = ss_ndc_x(k, W);
     if (k < H) ys[k] = ss_ndc_y(k, H);
-    if (k < 2) big_count[k] = 0;
+    if (k < 3) big_count[k] = 0;  // medium / huge queue sizes, record-block work counter
 }
 
 // Gradient of the covered item (pixel ix, iy of record R) with the coverage
@@ -159,21 +159,27 @@ __global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatPar
     SplatWarpSmem &sm = reinterpret_cast<SplatWarpSmem *>(splat_smem)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int my_ch = warp_tr_index<NCH>(lane);
     const unsigned same = __match_any_sync(0xffffffffu, my_ch);
     const bool owner = (__ffs(same) - 1) == lane;
     const int nblocks = (P.n + 31) >> 5;
+    int32_t *work = big_count + 2;
 
-    // kept-record cursor: block b, remaining kept mask
-    int blk = gwarp;
+    // kept-record cursor: block b, remaining kept mask.  Blocks of 32
+    // records are handed out dynamically (one counter), so warps that drew
+    // heavy records do not hold up the tail of the launch.
+    auto grab = [&]() {
+        int b = 0;
+        if (lane == 0) b = atomicAdd(work, 1);
+        return __shfl_sync(0xffffffffu, b, 0);
+    };
+    int blk = grab();
     unsigned kept = 0u;
     auto refill = [&]() {
         while (kept == 0u && blk < nblocks) {
             const int r = (blk << 5) + lane;
             kept = __ballot_sync(0xffffffffu, r < P.n && P.cull[r] == 0);
-            if (kept == 0u) blk += nwarps;
+            if (kept == 0u) blk = grab();
         }
     };
     auto next_rec = [&]() -> int {  // pops the next kept record (or -1)
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatPar
         if (kept == 0u) return -1;
         const int r = (blk << 5) + __ffs(kept) - 1;
         kept &= kept - 1u;
-        if (kept == 0u) blk += nwarps;
+        if (kept == 0u) blk = grab();
         return r;
     };
     int cur = next_rec();
@@ -327,7 +333,7 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     cudaStream_t st = (cudaStream_t)stream;
     const int mx = width > height ? width : height;
     int32_t *big_count = reinterpret_cast<int32_t *>(pixel_ndc + width + height);
-    int32_t *big_list = big_count + 2;
+    int32_t *big_list = big_count + 3;
     pixel_ndc_kernel<<<(mx + 255) / 256, 256, 0, st>>>(width, height, pixel_ndc, pixel_ndc + width, big_count);
     SS_CUDA_CHECK_LAUNCH();
     SplatParams P{};
