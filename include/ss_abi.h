@@ -165,7 +165,7 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
  * rect.  The rec_acc row of every kept record is OVERWRITTEN (committed once,
  * no atomics, no memset needed; culled rows untouched -- ss_chain_backward
  * skips them); channel 16 (dview_z) is 0 without a consolidation term.
- * pixel_ndc: scratch of width + height + 3 + n 32-bit words. */
+ * pixel_ndc: scratch of width + height + 4 + n 32-bit words. */
 int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
                      const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
                      const float *background, int k_max, const float *target, float *coef, float *thr,

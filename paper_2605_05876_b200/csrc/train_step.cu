@@ -41,7 +41,7 @@ __global__ void pixel_ndc_kernel(int W, int H, float *xs, float *ys, int32_t *bi
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < W) xs[k] = ss_ndc_x(k, W);
     if (k < H) ys[k] = ss_ndc_y(k, H);
-    if (k < 3) big_count[k] = 0;  // medium / huge queue sizes, record-block work counter
+    if (k < 4) big_count[k] = 0;  // medium / huge queue sizes, record-block and medium-record work counters
 }
 
 // Gradient of the covered item (pixel ix, iy of record R) with the coverage
@@ -314,7 +314,16 @@ __global__ void __launch_bounds__(256) big_bwd_kernel(SplatParams P, const int32
     const bool owner = (__ffs(same) - 1) == lane;
     const int nmed = big_count[0], nhuge = big_count[1];
     const int G = gridDim.x;
-    for (int b = blockIdx.x; b < nmed; b += G) big_record(P, big_list[b], 0, 1, wid, nw, lane, my_ch, owner);
+    // medium records: handed out one per CTA by a work counter
+    __shared__ int s_b;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_b = atomicAdd(const_cast<int32_t *>(big_count) + 3, 1);
+        __syncthreads();
+        const int b = s_b;
+        if (b >= nmed) break;
+        big_record(P, big_list[b], 0, 1, wid, nw, lane, my_ch, owner);
+    }
     for (int h = 0; h < nhuge; ++h) {
         const int first = (int)(((long long)blockIdx.x - 37LL * h) % G + G) % G;
         big_record(P, big_list[P.n - 1 - h], first, G, wid, nw, lane, my_ch, owner);
@@ -333,7 +342,7 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     cudaStream_t st = (cudaStream_t)stream;
     const int mx = width > height ? width : height;
     int32_t *big_count = reinterpret_cast<int32_t *>(pixel_ndc + width + height);
-    int32_t *big_list = big_count + 3;
+    int32_t *big_list = big_count + 4;
     pixel_ndc_kernel<<<(mx + 255) / 256, 256, 0, st>>>(width, height, pixel_ndc, pixel_ndc + width, big_count);
     SS_CUDA_CHECK_LAUNCH();
     SplatParams P{};
