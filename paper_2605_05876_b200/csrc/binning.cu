@@ -207,10 +207,11 @@ __device__ __forceinline__ int merge_split(const uint64_t *x, int la, const uint
 template <int kThreads, int kCap, bool kHeavy>
 __global__ void __launch_bounds__(kThreads) tile_sort_kernel(
     const int32_t *__restrict__ offsets, uint64_t *__restrict__ keys, int32_t *__restrict__ pair_rec,
-    uint2 *__restrict__ pair_rect, const uint4 *__restrict__ recs, int64_t capacity)
+    uint2 *__restrict__ pair_rect, const uint4 *__restrict__ recs, int64_t capacity,
+    const int32_t *__restrict__ order)
 {
     extern __shared__ uint64_t skeys[];
-    const int t = blockIdx.x;
+    const int t = order ? order[blockIdx.x] : blockIdx.x;  // heavy tiles first when an order is given
     const int64_t o0 = offsets[t];
     int64_t o1 = offsets[t + 1];
     if (o1 > capacity) o1 = capacity;
@@ -312,11 +313,11 @@ extern "C" int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, i
     }
     tile_sort_kernel<kSmallThreads, kSmallCap, false><<<ntiles, kSmallThreads, 2 * kSmallCap * sizeof(uint64_t), st>>>(
         tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const uint4 *>(bininfo),
-        pair_capacity);
+        pair_capacity, tile_order);
     SS_CUDA_CHECK_LAUNCH();
     tile_sort_kernel<kHeavyThreads, kHeavyCap, true><<<ntiles, kHeavyThreads, 2 * kHeavyCap * sizeof(uint64_t), st>>>(
         tile_offsets, keys, pair_rec, reinterpret_cast<uint2 *>(pair_rect), reinterpret_cast<const uint4 *>(bininfo),
-        pair_capacity);
+        pair_capacity, tile_order);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
