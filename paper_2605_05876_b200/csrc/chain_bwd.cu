@@ -102,7 +102,7 @@ __device__ __forceinline__ void scatter_rgb(double *base, int key, double v0, do
     if (v2 != 0.0) atomicAdd(d + 2, v2);
 }
 
-__global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
+__global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.cloud.n || P.cull[i] != 0) return;
@@ -179,37 +179,43 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
             G4[2] -= gcy * cy * id4;
         }
     }
-    // T rows -> camera (backward.py:405-410)
-    const double *pm = P.proj;
-    double gtu[3], gtv[3], gcc[3];
+    // T rows -> camera -> world (backward.py:405-441) and the frame
+    // adjoint in float32 (linear maps; the 1e-3 gradient bar), which keeps
+    // the kernel's register footprint down -- the MIP chain above stays float64
+    const float *pm = P.projf;
+    float gtu[3], gtv[3], gcc[3];
+    const float G1f[3] = {(float)G1[0], (float)G1[1], (float)G1[2]};
+    const float G2f[3] = {(float)G2[0], (float)G2[1], (float)G2[2]};
+    const float G4f[3] = {(float)G4[0], (float)G4[1], (float)G4[2]};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        gtu[c] = G1[0] * pm[c] + G2[0] * pm[4 + c] + G4[0] * pm[12 + c];
-        gtv[c] = G1[1] * pm[c] + G2[1] * pm[4 + c] + G4[1] * pm[12 + c];
-        gcc[c] = G1[2] * pm[c] + G2[2] * pm[4 + c] + G4[2] * pm[12 + c];
+        gtu[c] = G1f[0] * pm[c] + G2f[0] * pm[4 + c] + G4f[0] * pm[12 + c];
+        gtv[c] = G1f[1] * pm[c] + G2f[1] * pm[4 + c] + G4f[1] * pm[12 + c];
+        gcc[c] = G1f[2] * pm[c] + G2f[2] * pm[4 + c] + G4f[2] * pm[12 + c];
     }
-    gcc[2] -= gz;
-    // camera -> world (backward.py:412-441)
-    double gw[3], guw[3], gvw[3];
+    gcc[2] -= (float)gz;
+    float gw[3], guw[3], gvw[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        gw[k] = (gcc[0] * P.view[k] + gcc[1] * P.view[4 + k]) + gcc[2] * P.view[8 + k];
-        guw[k] = (gtu[0] * P.view[k] + gtu[1] * P.view[4 + k]) + gtu[2] * P.view[8 + k];
-        gvw[k] = (gtv[0] * P.view[k] + gtv[1] * P.view[4 + k]) + gtv[2] * P.view[8 + k];
+        gw[k] = (gcc[0] * P.viewf[k] + gcc[1] * P.viewf[4 + k]) + gcc[2] * P.viewf[8 + k];
+        guw[k] = (gtu[0] * P.viewf[k] + gtu[1] * P.viewf[4 + k]) + gtu[2] * P.viewf[8 + k];
+        gvw[k] = (gtv[0] * P.viewf[k] + gtv[1] * P.viewf[4 + k]) + gtv[2] * P.viewf[8 + k];
     }
     const SsCloud &cl = P.cloud;
-    const double q0 = cl.quats[4 * i], q1 = cl.quats[4 * i + 1], q2 = cl.quats[4 * i + 2], q3 = cl.quats[4 * i + 3];
-    const double qn = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
-    const double w = q0 / qn, x = q1 / qn, y = q2 / qn, z = q3 / qn;
-    const double uh[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
-    const double vh[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
-    const double su = exp((double)cl.log_scales[2 * i]), sv = exp((double)cl.log_scales[2 * i + 1]);
-    const double gsu = (guw[0] * uh[0] + guw[1] * uh[1]) + guw[2] * uh[2];
-    const double gsv = (gvw[0] * vh[0] + gvw[1] * vh[1]) + gvw[2] * vh[2];
-    double gU[3], gV[3], gN[3] = {0.0, 0.0, 0.0};
+    const float4 qv = reinterpret_cast<const float4 *>(cl.quats)[i];
+    const float qn = sqrtf(((qv.x * qv.x + qv.y * qv.y) + qv.z * qv.z) + qv.w * qv.w);
+    const float iqn = 1.f / qn;
+    const float w = qv.x * iqn, x = qv.y * iqn, y = qv.z * iqn, z = qv.w * iqn;
+    const float uh[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
+    const float vh[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
+    const float2 lsv = reinterpret_cast<const float2 *>(cl.log_scales)[i];
+    const float su = __expf(lsv.x), sv = __expf(lsv.y);
+    const float gsu = (guw[0] * uh[0] + guw[1] * uh[1]) + guw[2] * uh[2];
+    const float gsv = (gvw[0] * vh[0] + gvw[1] * vh[1]) + gvw[2] * vh[2];
+    float gU[3], gV[3], gN[3] = {0.f, 0.f, 0.f};
     for (int k = 0; k < 3; ++k) { gU[k] = su * guw[k]; gV[k] = sv * gvw[k]; }
-    double gcent[3] = {gw[0], gw[1], gw[2]};
-    double galb[3] = {0.0, 0.0, 0.0}, gmet = 0.0, grough = 0.0;
+    float gcent[3] = {gw[0], gw[1], gw[2]};
+    float galb[3] = {0.f, 0.f, 0.f}, gmet = 0.f, grough = 0.f;
 
     if (P.color_source == SS_COLOR_IBL) {
         // float32 shading adjoint (the forward colours are float64 in the
@@ -248,27 +254,27 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
             scatter_rgb(P.g.d_diffuse, didx[k], sg.g_ld[0] * dcw[k], sg.g_ld[1] * dcw[k], sg.g_ld[2] * dcw[k]);
     } else if (P.color_source == SS_COLOR_ALBEDO) {
         for (int c = 0; c < 3; ++c) {
-            const double al = (double)ss_sigmoid_fast(cl.albedo_raw[3 * i + c]);
-            galb[c] = gcol[c] * al * (1.0 - al);
+            const float al = ss_sigmoid_fast(cl.albedo_raw[3 * i + c]);
+            galb[c] = (float)gcol[c] * al * (1.f - al);
         }
     }
     // quat_frame_backward (surfels.py:54-77)
 #define D3(g, a0, a1, a2) ((g)[0] * (a0) + (g)[1] * (a1) + (g)[2] * (a2))
-    const double gqw = D3(gU, 0.0, 2 * z, -2 * y) + D3(gV, -2 * z, 0.0, 2 * x) + D3(gN, 2 * y, -2 * x, 0.0);
-    const double gqx = D3(gU, 0.0, 2 * y, 2 * z) + D3(gV, 2 * y, -4 * x, 2 * w) + D3(gN, 2 * z, -2 * w, -4 * x);
-    const double gqy = D3(gU, -4 * y, 2 * x, -2 * w) + D3(gV, 2 * x, 0.0, 2 * z) + D3(gN, 2 * w, 2 * z, -4 * y);
-    const double gqz = D3(gU, -4 * z, 2 * w, 2 * x) + D3(gV, -2 * w, -4 * z, 2 * y) + D3(gN, 2 * x, 2 * y, 0.0);
+    const float gqw = D3(gU, 0.f, 2 * z, -2 * y) + D3(gV, -2 * z, 0.f, 2 * x) + D3(gN, 2 * y, -2 * x, 0.f);
+    const float gqx = D3(gU, 0.f, 2 * y, 2 * z) + D3(gV, 2 * y, -4 * x, 2 * w) + D3(gN, 2 * z, -2 * w, -4 * x);
+    const float gqy = D3(gU, -4 * y, 2 * x, -2 * w) + D3(gV, 2 * x, 0.f, 2 * z) + D3(gN, 2 * w, 2 * z, -4 * y);
+    const float gqz = D3(gU, -4 * z, 2 * w, 2 * x) + D3(gV, -2 * w, -4 * z, 2 * y) + D3(gN, 2 * x, 2 * y, 0.f);
 #undef D3
-    const double radial = ((gqw * w + gqx * x) + gqy * y) + gqz * z;
+    const float radial = ((gqw * w + gqx * x) + gqy * y) + gqz * z;
 
     SsGrads &g = P.g;
     for (int c = 0; c < 3; ++c) {
         red_add(g.centers + 3 * i + c, (float)gcent[c]);
         red_add(g.albedo_raw + 3 * i + c, (float)galb[c]);
     }
-    red_add4(g.quats + 4 * (size_t)i, (float)((gqw - radial * w) / qn), (float)((gqx - radial * x) / qn),
-             (float)((gqy - radial * y) / qn), (float)((gqz - radial * z) / qn));
-    red_add2(g.log_scales + 2 * (size_t)i, (float)(gsu * su), (float)(gsv * sv));
+    red_add4(g.quats + 4 * (size_t)i, (gqw - radial * w) * iqn, (gqx - radial * x) * iqn, (gqy - radial * y) * iqn,
+             (gqz - radial * z) * iqn);
+    red_add2(g.log_scales + 2 * (size_t)i, gsu * su, gsv * sv);
     red_add(g.metallic_raw + i, (float)gmet);
     red_add(g.roughness_raw + i, (float)grough);
     if (g.colors)
