@@ -49,17 +49,18 @@ struct FwdParams {
 };
 
 // CTAs of kFwdWarps warps (a tile is split over tile*tile/32/kFwdWarps
-// CTAs): warps never wait for each other, and a finished warp pair frees its
-// slot without waiting for the tile's slowest warp.
-constexpr int kFwdWarps = 2;
+// CTAs; measured 4 > 2 = 8 > 1 with the heavy-first tile order): warps never
+// wait for each other.
+constexpr int kFwdWarps = 4;
 
 template <bool kExtras, bool kTrain>
 __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 {
     __shared__ PackedScratch scratch[kFwdWarps];
-    const int ctas_per_tile = P.tile * P.tile / (32 * kFwdWarps);
+    const int wpc = blockDim.x >> 5;  // kFwdWarps, or fewer for 8x8 tiles
+    const int ctas_per_tile = P.tile * P.tile / (32 * wpc);
     const int t = P.tile_order ? P.tile_order[blockIdx.x / ctas_per_tile] : blockIdx.x / ctas_per_tile;
-    const int wid_in_tile = (blockIdx.x % ctas_per_tile) * kFwdWarps + (threadIdx.x >> 5);
+    const int wid_in_tile = (blockIdx.x % ctas_per_tile) * wpc + (threadIdx.x >> 5);
     const WarpPix wp = warp_pixels(t, P.ntx, P.tile, P.W, P.H, wid_in_tile);
     const int lane = wp.lane, wid = threadIdx.x >> 5;
     const bool live = wp.live;
@@ -257,8 +258,9 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, const int4 *__r
 
 template <bool kExtras, bool kTrain>
 void launch(const FwdParams &P, int ntiles, int threads, cudaStream_t st) {
-    const int ctas_per_tile = threads / (32 * kFwdWarps);
-    raster_fwd_kernel<kExtras, kTrain><<<ntiles * ctas_per_tile, 32 * kFwdWarps, 0, st>>>(P);
+    const int wpc = threads / 32 < kFwdWarps ? threads / 32 : kFwdWarps;  // tile 8: 2 warps
+    const int ctas_per_tile = threads / (32 * wpc);
+    raster_fwd_kernel<kExtras, kTrain><<<ntiles * ctas_per_tile, 32 * wpc, 0, st>>>(P);
 }
 
 bool fill_common(FwdParams &P, int width, int height, int tile, const int32_t *tile_offsets,

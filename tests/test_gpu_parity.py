@@ -178,3 +178,14 @@ def test_fast_coverage_path_is_exact_at_scale():
         assert n > 1_000_000
         assert bad == 0, f"{bad} coverage decisions differ from the reference arithmetic"
         assert slow < 0.05 * n
+
+
+def test_tile8_forward_matches_tile16():
+    """tile = 8 (two 8x4 warp blocks per tile, a different tile list) renders
+    what tile = 16 renders (tile-size invariance, test_rasterizer.py:97-103)."""
+    d = load("config0_small")
+    _, _, _, res16 = _render(d)
+    _, _, _, res8 = _render(d, tile=8)
+    bad, err = image_close(res8.rgb, res16.rgb, rel=1e-6, abs_=1e-7)
+    assert bad == 0, err
+    assert torch.equal(res8.nlayers, res16.nlayers)
