@@ -1,10 +1,14 @@
 """backward_image() API (mirror of surfsplat.backward, backward.py:29-470).
 
-Two native launches per view: the tile-CTA raster backward (pixel replays,
-per-layer suffix recursion, consolidation, warp-reduced per-record atomics)
-and the per-surfel chain kernel (MIP chain, rows -> world, shading adjoint
-with the derived-map scatter, quaternion adjoint).  With IBL colours the env
-adjoint kernel finishes the environment gradient.
+Without the consolidation term (cons_scale = 0, the common case) the image
+gradient goes through the training step's walk-free kernels: deferred-loss
+forward (layer sums + closing depths), ss_train_coefs (suffix recursion with
+g_rgb and g_alpha) and the record-parallel backward.  With cons_scale > 0 the
+replaying tile-CTA backward (pixel replays, per-layer suffix recursion,
+consolidation, warp-reduced per-record atomics) runs instead.  Then the
+per-surfel chain kernel (MIP chain, rows -> world, shading adjoint with the
+derived-map scatter, quaternion adjoint); with IBL colours the env adjoint
+kernel finishes the environment gradient.
 """
 
 from __future__ import annotations
@@ -51,6 +55,33 @@ def grads_struct(g, d_diffuse=None, d_specular=None):
                         _lib.ptr(d_diffuse), _lib.ptr(d_specular))
 
 
+def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp):
+    """The walk-free backward of the training step for an API render
+    (cons_scale = 0): the deferred-loss forward re-derives the per-pixel layer
+    sums and closing depths, ss_train_coefs turns them into the layer
+    coefficients for (g_rgb, g_alpha), and the record-parallel kernel fills
+    the per-record accumulator."""
+    st, opt, cam = result.state, result.options, result.camera
+    dev = st.records.device
+    H, W, K = int(cam.height), int(cam.width), int(opt.k_max)
+    f32 = dict(device=dev, dtype=torch.float32)
+    coef = torch.empty((K, H * W, 4), **f32)
+    thr = torch.empty((K, H * W), **f32)
+    hdr = torch.empty((H * W, 4), device=dev, dtype=torch.int32)
+    rgb = torch.empty((H, W, 3), **f32)
+    _lib.check(lib.ss_train_forward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
+                                    _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, K, None, _lib.ptr(coef),
+                                    _lib.ptr(thr), _lib.ptr(hdr), None, _lib.ptr(rgb), None, None, _lib.stream_ptr()),
+               "ss_train_forward")
+    _lib.check(lib.ss_train_coefs(W, H, K, _lib.ptr(hdr), _lib.ptr(coef), _lib.ptr(g_rgb), _lib.ptr(g_alpha), bgp,
+                                  _lib.stream_ptr()), "ss_train_coefs")
+    n = st.records.shape[0]
+    scratch = torch.empty(W + H + 4 + n, **f32)
+    _lib.check(lib.ss_train_backward_records(n, _lib.ptr(st.cull), _lib.ptr(st.records), W, H, K, _lib.ptr(coef),
+                                             _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(scratch), _lib.ptr(acc),
+                                             _lib.stream_ptr()), "ss_train_backward_records")
+
+
 def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0) -> BackwardResult:
     opt = result.options
     if opt.depth_mode != "interval":
@@ -69,10 +100,15 @@ def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0) -> B
     acc = torch.zeros((n, _lib.ACC_FLOATS), device=dev, dtype=torch.float32)
     cons = torch.zeros(1, device=dev, dtype=torch.float64)
     bgp, _keep = _lib.fvec(opt.background)
-    rc = lib.ss_raster_backward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
-                                _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, int(opt.k_max), _lib.ptr(g_rgb), _lib.ptr(ga),
-                                float(cons_scale), _lib.ptr(acc), _lib.ptr(cons), _lib.stream_ptr())
-    _lib.check(rc, "ss_raster_backward")
+    if float(cons_scale) == 0.0:
+        _record_backward(lib, result, g_rgb, ga, acc, bgp)
+    else:
+        # the consolidation penalty needs the per-pixel layer depths of the
+        # replaying tile backward
+        rc = lib.ss_raster_backward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
+                                    _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, int(opt.k_max), _lib.ptr(g_rgb),
+                                    _lib.ptr(ga), float(cons_scale), _lib.ptr(acc), _lib.ptr(cons), _lib.stream_ptr())
+        _lib.check(rc, "ss_raster_backward")
     g = zero_grads(n, dev)
     env = result.env
     ibl = result.color_source == "ibl"
