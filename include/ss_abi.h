@@ -62,6 +62,10 @@ typedef struct SsEnv {
     const float *specular;  /* (L,He,We,3) */
     const float *lut;       /* (R,R,2) BRDF LUT, row = roughness (shading.py:118-156) */
     int he, we, levels, lut_res;
+    /* nullable: the same maps padded to 4 floats per texel (16-byte texel
+     * loads in the shading kernels) */
+    const float *diffuse4;  /* (He,We,4) */
+    const float *specular4; /* (L,He,We,4) */
 } SsEnv;
 
 typedef struct SsPreprocessOpts {

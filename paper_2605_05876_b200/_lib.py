@@ -36,7 +36,8 @@ class SsCloud(ctypes.Structure):
 
 class SsEnv(ctypes.Structure):
     _fields_ = [("diffuse", c_p), ("specular", c_p), ("lut", c_p), ("he", ctypes.c_int),
-                ("we", ctypes.c_int), ("levels", ctypes.c_int), ("lut_res", ctypes.c_int)]
+                ("we", ctypes.c_int), ("levels", ctypes.c_int), ("lut_res", ctypes.c_int),
+                ("diffuse4", c_p), ("specular4", c_p)]
 
 
 class SsPreprocessOpts(ctypes.Structure):
@@ -179,4 +180,5 @@ def make_env(env):
     if env is None:
         return None
     he, we = env.shape
-    return SsEnv(ptr(env.diffuse), ptr(env.specular), ptr(env.lut), he, we, env.levels, env.lut.shape[0])
+    return SsEnv(ptr(env.diffuse), ptr(env.specular), ptr(env.lut), he, we, env.levels, env.lut.shape[0],
+                 ptr(getattr(env, "diffuse4", None)), ptr(getattr(env, "specular4", None)))

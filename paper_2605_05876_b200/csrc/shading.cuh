@@ -80,6 +80,31 @@ __device__ __forceinline__ void ss_bil_lookup(const float *__restrict__ tex, int
     }
 }
 
+// 3-channel lookups on 16-byte texels (the padded copies of the env maps)
+template <typename R>
+__device__ __forceinline__ void ss_bil_lookup4(const float4 *__restrict__ tex, int w, const SsBil<R> &b, R *out) {
+    const float4 A = __ldg(tex + b.j0 * w + b.i0), B = __ldg(tex + b.j0 * w + b.i1);
+    const float4 Cc = __ldg(tex + b.j1 * w + b.i0), D = __ldg(tex + b.j1 * w + b.i1);
+    const R tu = b.tu, tv = b.tv;
+    const R wa = (1 - tu) * (1 - tv), wb = tu * (1 - tv), wc = (1 - tu) * tv, wd = tu * tv;
+    out[0] = wa * A.x + wb * B.x + wc * Cc.x + wd * D.x;
+    out[1] = wa * A.y + wb * B.y + wc * Cc.y + wd * D.y;
+    out[2] = wa * A.z + wb * B.z + wc * Cc.z + wd * D.z;
+}
+
+template <typename R>
+__device__ __forceinline__ void ss_bil_grads4(const float4 *__restrict__ tex, int w, const SsBil<R> &b, R *gu, R *gv) {
+    const float4 A = __ldg(tex + b.j0 * w + b.i0), B = __ldg(tex + b.j0 * w + b.i1);
+    const float4 Cc = __ldg(tex + b.j1 * w + b.i0), D = __ldg(tex + b.j1 * w + b.i1);
+    const R tu = b.tu, tv = b.tv;
+    const R a[3] = {A.x, A.y, A.z}, bb[3] = {B.x, B.y, B.z}, c[3] = {Cc.x, Cc.y, Cc.z}, d[3] = {D.x, D.y, D.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        gu[k] = b.du_ok ? (1 - tv) * (bb[k] - a[k]) + tv * (d[k] - c[k]) : R(0.0);
+        gv[k] = b.dv_ok ? (1 - tu) * (c[k] - a[k]) + tu * (d[k] - bb[k]) : R(0.0);
+    }
+}
+
 template <int C, typename R>
 __device__ __forceinline__ void ss_bil_grads(const float *__restrict__ tex, int w, const SsBil<R> &b, R *gu, R *gv) {
     const R tu = b.tu, tv = b.tv;
@@ -161,7 +186,10 @@ __device__ __forceinline__ void ss_shade_forward(const ShadeIn<R> &in, const SsE
     R fu, fv;
     ss_dir_coords(in.n, he, we, fu, fv);
     s.bd = ss_bil_prepare<R>(he, we, fu, fv, true);
-    ss_bil_lookup<3>(env.diffuse, we, s.bd, s.l_d);
+    const float4 *d4 = reinterpret_cast<const float4 *>(env.diffuse4);
+    const float4 *s4 = reinterpret_cast<const float4 *>(env.specular4);
+    if (d4) ss_bil_lookup4(d4, we, s.bd, s.l_d);
+    else ss_bil_lookup<3>(env.diffuse, we, s.bd, s.l_d);
     R lvl = ss_clip<R>(in.r, R(0.0), R(1.0)) * (L - 1);
     int cap = L - 2 > 0 ? L - 2 : 0;
     R fl = floor(lvl);
@@ -171,8 +199,13 @@ __device__ __forceinline__ void ss_shade_forward(const ShadeIn<R> &in, const SsE
     ss_dir_coords(s.refl, he, we, fu, fv);
     s.bs = ss_bil_prepare<R>(he, we, fu, fv, true);
     const size_t lstride = (size_t)he * we * 3;
-    ss_bil_lookup<3>(env.specular + lstride * s.lvl0, we, s.bs, s.spec_lo);
-    ss_bil_lookup<3>(env.specular + lstride * s.lvl1, we, s.bs, s.spec_hi);
+    if (s4) {
+        ss_bil_lookup4(s4 + (size_t)he * we * s.lvl0, we, s.bs, s.spec_lo);
+        ss_bil_lookup4(s4 + (size_t)he * we * s.lvl1, we, s.bs, s.spec_hi);
+    } else {
+        ss_bil_lookup<3>(env.specular + lstride * s.lvl0, we, s.bs, s.spec_lo);
+        ss_bil_lookup<3>(env.specular + lstride * s.lvl1, we, s.bs, s.spec_hi);
+    }
     for (int c = 0; c < 3; ++c) s.l_s[c] = (R(1.0) - s.frac) * s.spec_lo[c] + s.frac * s.spec_hi[c];
     s.bl = ss_bil_prepare<R>(LR, LR, ndv * (LR - 1), in.r * (LR - 1), false);
     R bb[2];
@@ -237,7 +270,10 @@ __device__ __forceinline__ void ss_shade_backward(const ShadeIn<R> &in, const Sh
     const int lv[2] = {s.lvl0, s.lvl1};
     for (int h = 0; h < 2; ++h) {
         R gu[3], gv[3];
-        ss_bil_grads<3>(env.specular + lstride * lv[h], we, s.bs, gu, gv);
+        if (env.specular4)
+            ss_bil_grads4(reinterpret_cast<const float4 *>(env.specular4) + (size_t)he * we * lv[h], we, s.bs, gu, gv);
+        else
+            ss_bil_grads<3>(env.specular + lstride * lv[h], we, s.bs, gu, gv);
         R gh0 = o.g_ls[0] * wts[h], gh1 = o.g_ls[1] * wts[h], gh2 = o.g_ls[2] * wts[h];
         R gfu = (gh0 * gu[0] + gh1 * gu[1]) + gh2 * gu[2];
         R gfv = (gh0 * gv[0] + gh1 * gv[1]) + gh2 * gv[2];
@@ -246,7 +282,8 @@ __device__ __forceinline__ void ss_shade_backward(const ShadeIn<R> &in, const Sh
         for (int c = 0; c < 3; ++c) g_refl[c] += gd[c];
     }
     R gu[3], gv[3];
-    ss_bil_grads<3>(env.diffuse, we, s.bd, gu, gv);
+    if (env.diffuse4) ss_bil_grads4(reinterpret_cast<const float4 *>(env.diffuse4), we, s.bd, gu, gv);
+    else ss_bil_grads<3>(env.diffuse, we, s.bd, gu, gv);
     R gfu = (o.g_ld[0] * gu[0] + o.g_ld[1] * gu[1]) + o.g_ld[2] * gu[2];
     R gfv = (o.g_ld[0] * gv[0] + o.g_ld[1] * gv[1]) + o.g_ld[2] * gv[2];
     R g_n[3];

@@ -110,6 +110,9 @@ class EnvironmentLight:
         self.base = torch.empty_like(t)
         self.diffuse = torch.empty_like(t)
         self.specular = torch.empty((self.levels, he, we, 3), device="cuda", dtype=torch.float32)
+        # 16-byte texels for the shading kernels' bilinear fetches
+        self.diffuse4 = torch.zeros((he, we, 4), device="cuda", dtype=torch.float32)
+        self.specular4 = torch.zeros((self.levels, he, we, 4), device="cuda", dtype=torch.float32)
         self.refresh()
 
     @property
@@ -133,6 +136,8 @@ class EnvironmentLight:
         _lib.check(lib.ss_env_refresh(he, we, self.levels, self.spec_samples, _lib.ptr(self.base_log), _lib.ptr(rs),
                                       _lib.ptr(self.base), _lib.ptr(self.diffuse), _lib.ptr(self.specular),
                                       _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()), "ss_env_refresh")
+        self.diffuse4[..., :3].copy_(self.diffuse)
+        self.specular4[..., :3].copy_(self.specular)
 
     def env_gradient(self, d_diffuse, d_specular):
         """Derived-map gradients -> (d_base, d_base_log) (shading.py:381-394)."""
