@@ -86,8 +86,9 @@ __device__ __forceinline__ void red_add4(float *p, float a, float b, float c, fl
 // same-address atomics at L2; otherwise every lane adds its own.
 __device__ __forceinline__ void scatter_rgb(double *base, int key, double v0, double v1, double v2) {
     const unsigned am = __activemask();
-    const unsigned m = __match_any_sync(am, key);
-    if (am == 0xffffffffu && m == 0xffffffffu) {
+    // warp-uniform texel?  (one shuffle + vote instead of a match_any)
+    const bool uniform = am == 0xffffffffu && __all_sync(0xffffffffu, key == __shfl_sync(0xffffffffu, key, 0));
+    if (uniform) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             v0 += __shfl_xor_sync(0xffffffffu, v0, o);
