@@ -237,10 +237,20 @@ typedef struct SsGrads {
     float *ss_grad;
     int32_t *touched;
     double *d_diffuse, *d_specular;  /* nullable unless SS_COLOR_IBL */
+    /* nullable: per-view float32 derived-map accumulators with 16-byte texels
+     * ((He,We,4) and (L,He,We,4), zero on entry); when given, the shading
+     * adjoint scatters into them with vector float32 reductions and
+     * ss_env_grad_merge later folds them into d_diffuse / d_specular */
+    float *d_diffuse4, *d_specular4;
 } SsGrads;
 int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                       int color_source, const SsEnv *env, const int8_t *cull,
                       const float *rec_acc, const SsGrads *grads, void *stream);
+
+/* ss_env_grad_merge: dst[3 t + c] += src4[4 t + c] (float64 += float32) for
+ * t < texels, c < 3, and zeroes src4 (the per-view derived-map accumulators
+ * of SsGrads.d_diffuse4 / d_specular4). */
+int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void *stream);
 
 /* ---- environment ----------------------------------------------------------
  * ss_brdf_lut: brdf_lut() (shading.py:118-156) -> lut (res,res,2) float.

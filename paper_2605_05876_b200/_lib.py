@@ -57,7 +57,8 @@ class SsStacks(ctypes.Structure):
 class SsGrads(ctypes.Structure):
     _fields_ = [("centers", c_p), ("quats", c_p), ("log_scales", c_p), ("albedo_raw", c_p),
                 ("metallic_raw", c_p), ("roughness_raw", c_p), ("colors", c_p), ("ss_grad", c_p),
-                ("touched", c_p), ("d_diffuse", c_p), ("d_specular", c_p)]
+                ("touched", c_p), ("d_diffuse", c_p), ("d_specular", c_p), ("d_diffuse4", c_p),
+                ("d_specular4", c_p)]
 
 
 _lib = None
@@ -84,6 +85,7 @@ _SIGNATURES = {
     "ss_adam_step": [ctypes.c_int64, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_float, ctypes.c_float,
                      ctypes.c_float, ctypes.c_float, c_p],
     "ss_normalize_quats": [ctypes.c_int, c_p, c_p],
+    "ss_env_grad_merge": [ctypes.c_int64, c_p, c_p, c_p],
     "ss_adam_multi": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_float, ctypes.c_float,
                       ctypes.c_float, c_p],
     "ss_grid_cells": [ctypes.c_int, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_int, c_p, c_p],

@@ -103,6 +103,33 @@ __device__ __forceinline__ void scatter_rgb(double *base, int key, double v0, do
     if (v2 != 0.0) atomicAdd(d + 2, v2);
 }
 
+// The same tap into a per-view float32 map with 16-byte texels: one vector
+// reduction per tap (the warp pre-sums a uniform texel first).
+__device__ __forceinline__ void scatter_rgb4(float *base, int key, float v0, float v1, float v2) {
+    const unsigned am = __activemask();
+    const bool uniform = am == 0xffffffffu && __all_sync(0xffffffffu, key == __shfl_sync(0xffffffffu, key, 0));
+    if (uniform) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+            v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+        }
+        if ((threadIdx.x & 31) != 0) return;
+    }
+    if (v0 != 0.f || v1 != 0.f || v2 != 0.f) red_add4(base + 4 * (size_t)key, v0, v1, v2, 0.f);
+}
+
+__global__ void env_merge_kernel(int64_t texels, float4 *__restrict__ src, double *__restrict__ dst) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < texels; t += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = src[t];
+        if (v.x != 0.f || v.y != 0.f || v.z != 0.f) {
+            dst[3 * t] += v.x; dst[3 * t + 1] += v.y; dst[3 * t + 2] += v.z;
+            src[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -242,17 +269,29 @@ __global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
         const double scw[4] = {(1.0 - bs.tu) * (1.0 - bs.tv), (double)bs.tu * (1.0 - bs.tv), (1.0 - bs.tu) * (double)bs.tv,
                                (double)bs.tu * bs.tv};
         const int T = P.env.he * we;
-        for (int h = 0; h < 2; ++h)  // level lvs[h] texel sidx[k] = element 3 * (lvs[h] * T + sidx[k])
-            for (int k = 0; k < 4; ++k) {
-                const double f = wts[h] * scw[k];
-                scatter_rgb(P.g.d_specular, lvs[h] * T + sidx[k], sg.g_ls[0] * f, sg.g_ls[1] * f, sg.g_ls[2] * f);
-            }
         const SsBil<float> &bd = st.bd;
         const int didx[4] = {bd.j0 * we + bd.i0, bd.j0 * we + bd.i1, bd.j1 * we + bd.i0, bd.j1 * we + bd.i1};
         const double dcw[4] = {(1.0 - bd.tu) * (1.0 - bd.tv), (double)bd.tu * (1.0 - bd.tv), (1.0 - bd.tu) * (double)bd.tv,
                                (double)bd.tu * bd.tv};
-        for (int k = 0; k < 4; ++k)
-            scatter_rgb(P.g.d_diffuse, didx[k], sg.g_ld[0] * dcw[k], sg.g_ld[1] * dcw[k], sg.g_ld[2] * dcw[k]);
+        if (P.g.d_specular4) {  // per-view float32 maps, folded into the float64 sums per view
+            for (int h = 0; h < 2; ++h)
+                for (int k = 0; k < 4; ++k) {
+                    const float f = (float)(wts[h] * scw[k]);
+                    scatter_rgb4(P.g.d_specular4, lvs[h] * T + sidx[k], sg.g_ls[0] * f, sg.g_ls[1] * f, sg.g_ls[2] * f);
+                }
+            for (int k = 0; k < 4; ++k) {
+                const float f = (float)dcw[k];
+                scatter_rgb4(P.g.d_diffuse4, didx[k], sg.g_ld[0] * f, sg.g_ld[1] * f, sg.g_ld[2] * f);
+            }
+        } else {
+            for (int h = 0; h < 2; ++h)  // level lvs[h] texel sidx[k] = element 3 * (lvs[h] * T + sidx[k])
+                for (int k = 0; k < 4; ++k) {
+                    const double f = wts[h] * scw[k];
+                    scatter_rgb(P.g.d_specular, lvs[h] * T + sidx[k], sg.g_ls[0] * f, sg.g_ls[1] * f, sg.g_ls[2] * f);
+                }
+            for (int k = 0; k < 4; ++k)
+                scatter_rgb(P.g.d_diffuse, didx[k], sg.g_ld[0] * dcw[k], sg.g_ld[1] * dcw[k], sg.g_ld[2] * dcw[k]);
+        }
     } else if (P.color_source == SS_COLOR_ALBEDO) {
         for (int c = 0; c < 3; ++c) {
             const float al = ss_sigmoid_fast(cl.albedo_raw[3 * i + c]);
@@ -285,6 +324,16 @@ __global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
 }
 
 }  // namespace
+
+extern "C" int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void *stream)
+{
+    if (texels < 0 || (texels > 0 && (!src4 || !dst))) return SS_ERR_INVALID;
+    if (texels == 0) return SS_OK;
+    const int blocks = (int)((texels + 255) / 256 < 148 * 4 ? (texels + 255) / 256 : 148 * 4);
+    env_merge_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(texels, reinterpret_cast<float4 *>(src4), dst);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
 
 extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                                  int color_source, const SsEnv *env, const int8_t *cull,

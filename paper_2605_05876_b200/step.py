@@ -140,6 +140,10 @@ class TrainStep:
         self.ntx = (self.W + tile - 1) // tile
         self.ntiles = self.ntx * ((self.H + tile - 1) // tile)
         self.bufs = [ViewBuffers(n, self.W, self.H, tile, self.k_max, self.ntiles, dev) for _ in range(max(1, streams))]
+        he, we = env.shape
+        for b in self.bufs:  # per-view float32 derived-map accumulators (16-byte texels)
+            b.d_diff4 = torch.zeros((he, we, 4), device=dev, dtype=torch.float32)
+            b.d_spec4 = torch.zeros((env.levels, he, we, 4), device=dev, dtype=torch.float32)
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(len(self.bufs))]
         if loss == "photometric":
             for b in self.bufs:
@@ -161,8 +165,10 @@ class TrainStep:
         self._cl = _lib.make_cloud(cloud)
         self._po = make_opts(self.opts, tile)
         self._envs = _lib.make_env(env)
-        self._gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
-                                _lib.ptr(self.touched), _lib.ptr(self.d_diffuse), _lib.ptr(self.d_spec))
+        for b in self.bufs:
+            b.gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
+                                _lib.ptr(self.touched), _lib.ptr(self.d_diffuse), _lib.ptr(self.d_spec),
+                                _lib.ptr(b.d_diff4), _lib.ptr(b.d_spec4))
         self._bg = _lib.fvec(self.bg)
         self.capacity = 0
         if pair_capacity:
@@ -171,7 +177,7 @@ class TrainStep:
         self._pairs, self._kept, self._nviews = [], [], 0
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
         self._stage = None
-        self.launches_per_view = 11    # preprocess, scan, order, scatter, tile sort x2, train fwd, ndc + record bwd x2, chain
+        self.launches_per_view = 13    # preprocess, scan, order, scatter, tile sort x2, train fwd, ndc + record bwd x2, chain, env merge x2
         self.launches_per_step_fixed = 4 + 1 + 4  # env adjoint, fused Adam (+ quat renorm), env refresh
 
     # -- buffers -----------------------------------------------------------
@@ -263,7 +269,12 @@ class TrainStep:
         ev = self._ev_begin("chain")
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                          _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(b.cull),
-                                         _lib.ptr(b.acc), ctypes.byref(self._gs), s), "ss_chain_backward")
+                                         _lib.ptr(b.acc), ctypes.byref(b.gs), s), "ss_chain_backward")
+        # fold this view's float32 derived-map sums into the step's float64 ones
+        _lib.check(lib.ss_env_grad_merge(b.d_diff4.numel() // 4, _lib.ptr(b.d_diff4), _lib.ptr(self.d_diffuse), s),
+                   "ss_env_grad_merge")
+        _lib.check(lib.ss_env_grad_merge(b.d_spec4.numel() // 4, _lib.ptr(b.d_spec4), _lib.ptr(self.d_spec), s),
+                   "ss_env_grad_merge")
         self._ev_end(ev)
         done = torch.cuda.Event()
         done.record()
