@@ -48,11 +48,11 @@ def zero_grads(n, dev):
             "touched": torch.zeros(n, device=dev, dtype=torch.int32)}
 
 
-def grads_struct(g, d_diffuse=None, d_specular=None):
+def grads_struct(g, d_diffuse=None, d_specular=None, d_diffuse4=None, d_specular4=None):
     return _lib.SsGrads(*(_lib.ptr(g[k]) for k in ("centers", "quats", "log_scales", "albedo_raw", "metallic_raw",
                                                    "roughness_raw")),
                         _lib.ptr(g.get("colors")), _lib.ptr(g["ss_grad"]), _lib.ptr(g["touched"]),
-                        _lib.ptr(d_diffuse), _lib.ptr(d_specular))
+                        _lib.ptr(d_diffuse), _lib.ptr(d_specular), _lib.ptr(d_diffuse4), _lib.ptr(d_specular4))
 
 
 def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp):
@@ -112,22 +112,28 @@ def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0) -> B
     g = zero_grads(n, dev)
     env = result.env
     ibl = result.color_source == "ibl"
-    d_diff = d_spec = None
+    d_diff = d_spec = d_diff4 = d_spec4 = None
     if ibl:
         d_diff = torch.zeros(env.base.shape, device=dev, dtype=torch.float64)
         d_spec = torch.zeros(env.specular.shape, device=dev, dtype=torch.float64)
+        # float32 accumulators with 16-byte texels for the scatter, folded in below
+        d_diff4 = torch.zeros((*env.base.shape[:2], 4), device=dev, dtype=torch.float32)
+        d_spec4 = torch.zeros((*env.specular.shape[:3], 4), device=dev, dtype=torch.float32)
     source = {"explicit": _lib.SS_COLOR_EXPLICIT, "ibl": _lib.SS_COLOR_IBL, "albedo": _lib.SS_COLOR_ALBEDO}[result.color_source]
     cl = _lib.make_cloud(cloud)
     camst = _lib.make_camera(cam)
     po = make_opts(opt.preprocess_options(), int(opt.tile))
     envs = _lib.make_env(env) if ibl else None
-    gs = grads_struct(g, d_diff, d_spec)
+    gs = grads_struct(g, d_diff, d_spec, d_diff4, d_spec4)
     rc = lib.ss_chain_backward(ctypes.byref(cl), ctypes.byref(camst), ctypes.byref(po), source,
                                ctypes.byref(envs) if envs is not None else None, _lib.ptr(st.cull), _lib.ptr(acc),
                                ctypes.byref(gs), _lib.stream_ptr())
     _lib.check(rc, "ss_chain_backward")
     g_env = None
     if ibl:
+        for src, dst in ((d_diff4, d_diff), (d_spec4, d_spec)):
+            _lib.check(lib.ss_env_grad_merge(src.numel() // 4, _lib.ptr(src), _lib.ptr(dst), _lib.stream_ptr()),
+                       "ss_env_grad_merge")
         _, g_env = env.env_gradient(d_diff, d_spec)
     g_bg = (g_rgb * (1.0 - result.alpha)[..., None]).sum(dim=(0, 1))
     return BackwardResult(centers=g["centers"], quats=g["quats"], log_scales=g["log_scales"],
