@@ -165,11 +165,12 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
  * rgb (H,W,3) is nullable.
  * ss_train_backward_records: pass 2 of backward.py:240-320 without the walk:
  * a covering record with interval start zs belongs to layer
- * #{j : closing depth_j < zs}; one warp per record sweeps its
- * rect.  The rec_acc row of every kept record is OVERWRITTEN (committed once,
+ * #{j : closing depth_j < zs}; records are counting-sorted
+ * by rect area and an 8-lane group per record sweeps its rect.  The rec_acc row of every kept record is OVERWRITTEN (committed once,
  * no atomics, no memset needed; culled rows untouched -- ss_chain_backward
  * skips them); channel 16 (dview_z) is 0 without a consolidation term.
- * pixel_ndc: scratch of width + height + 4 + n 32-bit words. */
+ * pixel_ndc: scratch of ss_train_backward_scratch_words(n, width, height)
+ * 32-bit words (0 on invalid sizes). */
 int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
                      const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
                      const float *background, int k_max, const float *target, float *coef, float *thr,
@@ -184,6 +185,7 @@ int ss_train_forward(int width, int height, int tile, const int32_t *tile_offset
  * closed layers | layer count << 8. */
 int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef, const float *g_rgb,
                    const float *g_alpha, const float *background, void *stream);
+size_t ss_train_backward_scratch_words(int n, int width, int height);
 int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
                               int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
                               float *pixel_ndc, float *rec_acc, void *stream);

@@ -94,6 +94,7 @@ _SIGNATURES = {
     "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
                          ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_train_coefs": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), c_p],
+    "ss_train_backward_scratch_words": [ctypes.c_int, ctypes.c_int, ctypes.c_int],
     "ss_train_backward_records": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
                                   c_p, c_p, c_p],
     "ss_photometric_workspace": [ctypes.c_int, ctypes.c_int, ctypes.c_int],
@@ -126,6 +127,7 @@ def load(require_cuda=True):
                 fn.argtypes = argt
             fn.restype = ctypes.c_int
         lib.ss_photometric_workspace.restype = ctypes.c_size_t
+        lib.ss_train_backward_scratch_words.restype = ctypes.c_size_t
         lib.ss_last_error.restype = ctypes.c_char_p
         lib.ss_version.restype = ctypes.c_int
         _lib = lib

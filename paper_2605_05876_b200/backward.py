@@ -76,7 +76,7 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp):
     _lib.check(lib.ss_train_coefs(W, H, K, _lib.ptr(hdr), _lib.ptr(coef), _lib.ptr(g_rgb), _lib.ptr(g_alpha), bgp,
                                   _lib.stream_ptr()), "ss_train_coefs")
     n = st.records.shape[0]
-    scratch = torch.empty(W + H + 4 + n, **f32)
+    scratch = torch.empty(lib.ss_train_backward_scratch_words(n, W, H), **f32)
     _lib.check(lib.ss_train_backward_records(n, _lib.ptr(st.cull), _lib.ptr(st.records), W, H, K, _lib.ptr(coef),
                                              _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(scratch), _lib.ptr(acc),
                                              _lib.stream_ptr()), "ss_train_backward_records")

@@ -26,7 +26,7 @@ BASE_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 def _compile(src, verbose=False):
     obj = os.path.join(OUT_DIR, src.replace(".cu", ".o"))
-    flags = list(BASE_FLAGS)
+    flags = list(BASE_FLAGS) + os.environ.get("SS_NVCC_FLAGS", "").split()  # experiment switches (-D...)
     if src in NO_FMAD:
         flags.append("-fmad=false")
     if verbose:

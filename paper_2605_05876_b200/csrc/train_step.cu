@@ -37,11 +37,13 @@ struct SplatParams {
     float *acc;             // (n, 20)
 };
 
+constexpr int kHeadWords = 8 + 2 * 64;  // see the scratch layout below
+
 __global__ void pixel_ndc_kernel(int W, int H, float *xs, float *ys, int32_t *big_count) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < W) xs[k] = ss_ndc_x(k, W);
     if (k < H) ys[k] = ss_ndc_y(k, H);
-    if (k < 4) big_count[k] = 0;  // medium / huge queue sizes, record-block and medium-record work counters
+    if (k < kHeadWords) big_count[k] = 0;  // counters, class histogram and cursors
 }
 
 // Gradient of the covered item (pixel ix, iy of record R) with the coverage
@@ -136,124 +138,222 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 constexpr int kBigChunk = 1024;
 constexpr int kHugeArea = 8 * kBigChunk;  // big rects above this are spread over the grid
 constexpr int kBigArea = 512;  // rects above this go to the CTA-chunked kernel (~0.1% of records)
+constexpr int kNB = 64;        // area classes of the other records
+constexpr int kGL = 8;         // lanes per record group (4 records per warp)
+constexpr int kGCap = 128;     // rect pixels compacted per group pass
 constexpr int kSplatWarps = 8;
+constexpr int kScatItems = 8;  // records per thread of the class scatter
+constexpr int kHeavyClass = 32;  // area >= 64 px: one round per work-counter ticket (else 8)
 
-struct SplatWarpSmem {
-    SsRecord rec[2];          // current / prefetched record (cp.async double buffer)
-    float2 uv[kBigArea];      // covered items: u, v
-    int ixy[kBigArea];        // covered items: pixel ix | iy << 16
+// Scratch layout (32-bit words after the two NDC tables), see
+// ss_train_backward_scratch_words: 8 counters (medium / huge queue sizes,
+// group-round and medium-record work counters, small-record count), the
+// class histogram and cursors, the big-rect queue (n), the class-sorted
+// record order (n) and the per-record class bytes.
+static_assert(kHeadWords == 8 + 2 * kNB, "scratch head layout");
+
+// Area class: exact below 16 px, then 8 classes per octave (~12% wide).
+__device__ __forceinline__ int area_class(int a) {
+    if (a < 16) return a;
+    const int e = 31 - __clz(a);
+    return 16 + (e - 4) * 8 + ((a >> (e - 3)) & 7);
+}
+
+__device__ __forceinline__ int rect_area(const int4 &r) {
+    return (r.z > r.x && r.w > r.y) ? (r.z - r.x) * (r.w - r.y) : 0;
+}
+
+// Class every kept record by rect area.  Big rects are queued for
+// big_bwd_kernel (their accumulator rows zeroed: that kernel commits with
+// atomics); the others get a class byte and count in the class histogram.
+__global__ void __launch_bounds__(256) area_class_kernel(SplatParams P, uint8_t *cls, int32_t *big_list,
+                                                         int32_t *counters, int32_t *hist)
+{
+    __shared__ int s_hist[kNB];
+    if (threadIdx.x < kNB) s_hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < P.n; r += gridDim.x * blockDim.x) {
+        uint8_t c = 0xff;
+        if (P.cull[r] == 0) {
+            const int area = rect_area(__ldg(reinterpret_cast<const int4 *>(P.records + r) + 5));
+            if (area > kBigArea) {
+                float4 *dst = reinterpret_cast<float4 *>(P.acc + (size_t)r * SS_ACC_FLOATS);
+#pragma unroll
+                for (int i = 0; i < SS_ACC_FLOATS / 4; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (area > kHugeArea) big_list[P.n - 1 - atomicAdd(counters + 1, 1)] = r;
+                else big_list[atomicAdd(counters, 1)] = r;
+            } else {
+                c = (uint8_t)area_class(area);
+                atomicAdd(&s_hist[c], 1);
+            }
+        }
+        cls[r] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x < kNB && s_hist[threadIdx.x] != 0) atomicAdd(hist + threadIdx.x, s_hist[threadIdx.x]);
+}
+
+// Counting-sort scatter: records in DESCENDING area class (heavy first);
+// the order within a class is irrelevant (every record is processed whole by
+// one group and committed with plain stores).
+__global__ void __launch_bounds__(256) area_scatter_kernel(int n, const uint8_t *cls, const int32_t *hist,
+                                                           int32_t *cursor, int32_t *order, int32_t *nsmall)
+{
+    __shared__ int s_cnt[kNB], s_base[kNB];
+    const int t = threadIdx.x;
+    if (t < kNB) s_cnt[t] = 0;
+    __syncthreads();
+    const int base = blockIdx.x * 256 * kScatItems;
+    int rank[kScatItems], c[kScatItems];
+#pragma unroll
+    for (int j = 0; j < kScatItems; ++j) {
+        const int r = base + j * 256 + t;
+        c[j] = r < n ? cls[r] : 0xff;
+        rank[j] = c[j] < kNB ? atomicAdd(&s_cnt[c[j]], 1) : 0;
+    }
+    __syncthreads();
+    if (t < 32) {
+        // positions 2t, 2t+1 of the descending order are classes 63-2t, 62-2t
+        const int ca = kNB - 1 - 2 * t, cb = ca - 1;
+        const int ha = __ldg(hist + ca), hb = __ldg(hist + cb);
+        int incl = ha + hb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (t >= o) incl += v;
+        }
+        const int excl = incl - ha - hb;
+        s_base[ca] = excl + (s_cnt[ca] ? atomicAdd(cursor + ca, s_cnt[ca]) : 0);
+        s_base[cb] = excl + ha + (s_cnt[cb] ? atomicAdd(cursor + cb, s_cnt[cb]) : 0);
+        // records of class >= kHeavyClass (positions before 2 * 16) are handed out one round at a time
+        const int nheavy = __shfl_sync(0xffffffffu, incl, kNB / 2 - kHeavyClass / 2 - 1);
+        if (blockIdx.x == 0 && t == 31) {
+            nsmall[0] = incl;
+            nsmall[1] = nheavy;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kScatItems; ++j)
+        if (c[j] < kNB) order[s_base[c[j]] + rank[j]] = base + j * 256 + t;
+}
+
+struct GroupSmem {
+    SsRecord rec[2][4];       // current / prefetched records of the 4 groups (cp.async double buffer)
+    float2 uv[4][kGCap];      // covered items: u, v
+    int ixy[4][kGCap];        // covered items: pixel ix | iy << 16
 };
 
-// One warp per kept record.  Warps take blocks of 32 consecutive records
-// (spatially coherent: scenes are Morton ordered) so the cull flags come with
-// one coalesced load + ballot; the next kept record is copied into the
-// other shared slot with cp.async while the current one is processed.  Per
-// record: pass 1 takes the exact coverage decision for every rect pixel and
-// compacts the covered ones (with u, v, rho^2) into the warp's list; pass 2
-// evaluates the gradient on the covered items only, 32 per iteration.
-// Records with huge rects (grazing or near-camera splats) are zeroed here
-// and queued for big_bwd_kernel.
-__global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatParams P, int32_t *big_list, int32_t *big_count)
+// Eight lanes per record, four records per warp, records taken in
+// descending area class so the four rects of a round (and the warps of a
+// launch) carry nearly equal work.  Rounds of 4 sorted records are handed
+// out in blocks of 8 by one counter; the next round's records are copied
+// into the other shared slot with cp.async while the current one runs.  Per
+// record: pass 1 takes the exact coverage decision for up to kGCap rect
+// pixels and compacts the covered ones (with u, v) into the group's list;
+// pass 2 evaluates the gradient on the covered items, 8 per iteration.  One
+// 3-level transposed reduction per group and plain stores of the record's
+// row (each record committed exactly once: no atomics, deterministic).
+__global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatParams P, const int32_t *order,
+                                                                        int32_t *counters)
 {
     extern __shared__ __align__(16) unsigned char splat_smem[];
-    SplatWarpSmem &sm = reinterpret_cast<SplatWarpSmem *>(splat_smem)[threadIdx.x >> 5];
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    const int my_ch = warp_tr_index<NCH>(lane);
-    const unsigned same = __match_any_sync(0xffffffffu, my_ch);
-    const bool owner = (__ffs(same) - 1) == lane;
-    const int nblocks = (P.n + 31) >> 5;
-    int32_t *work = big_count + 2;
-
-    // kept-record cursor: block b, remaining kept mask.  Blocks of 32
-    // records are handed out dynamically (one counter), so warps that drew
-    // heavy records do not hold up the tail of the launch.
-    auto grab = [&]() {
-        int b = 0;
-        if (lane == 0) b = atomicAdd(work, 1);
-        return __shfl_sync(0xffffffffu, b, 0);
+    GroupSmem &sm = reinterpret_cast<GroupSmem *>(splat_smem)[threadIdx.x >> 5];
+    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & (kGL - 1);
+    const unsigned glt = (1u << gl) - 1u;
+    int ch[3];
+    warp_tr_indices<NCH, 4>(ch, lane);
+    const int nsmall = counters[4];
+    const int nrounds = (nsmall + 3) >> 2, hrounds = (counters[5] + 3) >> 2;
+    int32_t *work = counters + 2;
+    int rend = 0;
+    auto grab = [&]() {  // ticket -> first round: heavy rounds one by one, then blocks of 8
+        int t = 0;
+        if (lane == 0) t = atomicAdd(work, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        const int b = t < hrounds ? t : hrounds + (t - hrounds) * 8;
+        rend = t < hrounds ? b + 1 : b + 8;
+        return b;
     };
-    int blk = grab();
-    unsigned kept = 0u;
-    auto refill = [&]() {
-        while (kept == 0u && blk < nblocks) {
-            const int r = (blk << 5) + lane;
-            kept = __ballot_sync(0xffffffffu, r < P.n && P.cull[r] == 0);
-            if (kept == 0u) blk = grab();
+    auto issue = [&](int r, int buf) {  // cp.async of round r's records into slot buf
+        if (r < nrounds && lane < 24) {
+            const int e = r * 4 + lane / 6;
+            if (e < nsmall)
+                cp_async16(reinterpret_cast<float4 *>(&sm.rec[buf][lane / 6]) + lane % 6,
+                           reinterpret_cast<const float4 *>(P.records + __ldg(order + e)) + lane % 6);
         }
+        cp_async_commit();
     };
-    auto next_rec = [&]() -> int {  // pops the next kept record (or -1)
-        refill();
-        if (kept == 0u) return -1;
-        const int r = (blk << 5) + __ffs(kept) - 1;
-        kept &= kept - 1u;
-        if (kept == 0u) blk = grab();
-        return r;
-    };
-    int cur = next_rec();
+    int cur = grab();
     int buf = 0;
-    if (cur >= 0 && lane < 6) cp_async16(reinterpret_cast<float4 *>(&sm.rec[0]) + lane,
-                                         reinterpret_cast<const float4 *>(P.records + cur) + lane);
-    cp_async_commit();
-    while (cur >= 0) {
-        const int nxt = next_rec();
+    issue(cur, 0);
+    while (cur < nrounds) {
+        const int nxt = cur + 1 < rend ? cur + 1 : grab();
         cp_async_wait_all();
         __syncwarp();
-        if (nxt >= 0 && lane < 6) cp_async16(reinterpret_cast<float4 *>(&sm.rec[buf ^ 1]) + lane,
-                                             reinterpret_cast<const float4 *>(P.records + nxt) + lane);
-        cp_async_commit();
-        const SsRecord &R = sm.rec[buf];
-        const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
-        float *dst = P.acc + (size_t)cur * SS_ACC_FLOATS;
-        if (area > kBigArea) {
-            if (lane < SS_ACC_FLOATS) dst[lane] = 0.f;
-            if (lane == 0) {
-                if (area > kHugeArea) big_list[P.n - 1 - atomicAdd(big_count + 1, 1)] = cur;
-                else big_list[atomicAdd(big_count, 1)] = cur;
-            }
-        } else {
-            // pass 1: exact coverage, compaction of the covered pixels
-            // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
-            const float inv_rw = fast_rcp((float)rw);
-            FastCov f;
-            fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
+        issue(nxt, buf ^ 1);
+        const int e = cur * 4 + grp;
+        const bool valid = e < nsmall;
+        const SsRecord &R = sm.rec[buf][grp];
+        int rw = 1, area = 0;
+        if (valid) {
+            rw = R.r.z - R.r.x;
+            area = rect_area(R.r);
+        }
+        // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
+        const float inv_rw = fast_rcp((float)rw);
+        FastCov f;
+        fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
+        float g[NCH];
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) g[k] = 0.f;
+        int touch = 0;
+        const int amax = __reduce_max_sync(0xffffffffu, area);
+        for (int c0 = 0; c0 < amax; c0 += kGCap) {
+            // pass 1: exact coverage of up to kGCap rect pixels, compaction
+            const int cend = min(c0 + kGCap, amax);
             int ncov = 0;
-            for (int k0 = 0; k0 < area; k0 += 32) {
+            for (int k0 = c0; k0 < cend; k0 += kGL) {
+                const int k = k0 + gl;
                 int ixy = 0;
                 float4 q;
-                const bool hit = k0 + lane < area && item_cover(P, R, f, k0 + lane, rw, inv_rw, ixy, q);
-                const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                const bool hit = k < area && item_cover(P, R, f, k, rw, inv_rw, ixy, q);
+                const unsigned gm = (__ballot_sync(0xffffffffu, hit) >> (grp * kGL)) & 0xffu;
                 if (hit) {
-                    const int slot = ncov + __popc(hm & lt);
-                    sm.uv[slot] = make_float2(q.x, q.y);
-                    sm.ixy[slot] = ixy;
+                    const int slot = ncov + __popc(gm & glt);
+                    sm.uv[grp][slot] = make_float2(q.x, q.y);
+                    sm.ixy[grp][slot] = ixy;
                 }
-                ncov += __popc(hm);
+                ncov += __popc(gm);
             }
             __syncwarp();
             // pass 2: gradients of the covered items
-            float g[NCH];
+            const int nmax = __reduce_max_sync(0xffffffffu, ncov);
+            for (int j0 = 0; j0 < nmax; j0 += kGL) {
+                const int j = j0 + gl;
+                if (j < ncov) {
+                    const float2 q = sm.uv[grp][j];
+                    const int ixy = sm.ixy[grp][j];
+                    // rho^2 with ss_cover's float32 expression (bit-identical on its fast path)
+                    const float r2 = R.c.y * q.x * q.x + 2.f * R.c.z * q.x * q.y + R.c.w * q.y * q.y;
+                    touch += item_grad(P, R, ixy & 0xffff, ixy >> 16, q.x, q.y, r2, g);
+                }
+            }
+            __syncwarp();
+        }
+        warp_tr_all<NCH, 4>(g, lane);  // 3 channel sums of the group per lane
+        touch += __shfl_xor_sync(0xffffffffu, touch, 4);
+        touch += __shfl_xor_sync(0xffffffffu, touch, 2);
+        touch += __shfl_xor_sync(0xffffffffu, touch, 1);
+        if (valid) {
+            // channel c -> accumulator slot (16 is dview_z, 0 here: the ss sum lives in 17);
+            // channels held by two lanes carry identical sums
+            float *dst = P.acc + (size_t)__ldg(order + e) * SS_ACC_FLOATS;
 #pragma unroll
-            for (int k = 0; k < NCH; ++k) g[k] = 0.f;
-            int touch = 0;
-            for (int j = lane; j < ncov; j += 32) {
-                const float2 q = sm.uv[j];
-                const int ixy = sm.ixy[j];
-                // rho^2 with ss_cover's float32 expression (bit-identical on its fast path)
-                const float r2 = R.c.y * q.x * q.x + 2.f * R.c.z * q.x * q.y + R.c.w * q.y * q.y;
-                touch += item_grad(P, R, ixy & 0xffff, ixy >> 16, q.x, q.y, r2, g);
-            }
-            const int tot = __reduce_add_sync(0xffffffffu, touch);
-            if (tot == 0) {  // still commit the (zero) row: the buffer is never memset
-                if (lane < SS_ACC_FLOATS) dst[lane] = 0.f;
-            } else {
-                warp_tr_reduce<NCH>(g, lane);
-                // channel c -> accumulator slot (16 is dview_z, 0 here: the ss sum lives in 17)
-                if (owner) dst[my_ch == 16 ? 17 : my_ch] = g[0];
-                if (lane == 0) reinterpret_cast<int *>(dst)[18] = tot;
-                if (lane == 1) dst[16] = 0.f;
-                if (lane == 2) dst[19] = 0.f;
-            }
+            for (int i = 0; i < 3; ++i) dst[ch[i] == 16 ? 17 : ch[i]] = g[i];
+            if (gl == 0) reinterpret_cast<int *>(dst)[18] = touch;
+            if (gl == 1) dst[16] = 0.f;
+            if (gl == 2) dst[19] = 0.f;
         }
         __syncwarp();
         cur = nxt;
@@ -332,6 +432,12 @@ __global__ void __launch_bounds__(256) big_bwd_kernel(SplatParams P, const int32
 
 }  // namespace
 
+extern "C" size_t ss_train_backward_scratch_words(int n, int width, int height)
+{
+    if (n < 0 || width <= 0 || height <= 0) return 0;
+    return (size_t)width + height + kHeadWords + 2 * (size_t)n + ((size_t)n + 3) / 4;
+}
+
 extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
                                          int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
                                          float *pixel_ndc, float *rec_acc, void *stream)
@@ -341,9 +447,13 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     if (!cull || !records || !coef || !thr || !pix_hdr || !pixel_ndc || !rec_acc) return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int mx = width > height ? width : height;
-    int32_t *big_count = reinterpret_cast<int32_t *>(pixel_ndc + width + height);
-    int32_t *big_list = big_count + 4;
-    pixel_ndc_kernel<<<(mx + 255) / 256, 256, 0, st>>>(width, height, pixel_ndc, pixel_ndc + width, big_count);
+    int32_t *counters = reinterpret_cast<int32_t *>(pixel_ndc + width + height);
+    int32_t *hist = counters + 8, *cursor = hist + kNB;
+    int32_t *big_list = counters + kHeadWords;
+    int32_t *order = big_list + n;
+    uint8_t *cls = reinterpret_cast<uint8_t *>(order + n);
+    pixel_ndc_kernel<<<(mx + kHeadWords + 255) / 256, 256, 0, st>>>(width, height, pixel_ndc, pixel_ndc + width,
+                                                                     counters);
     SS_CUDA_CHECK_LAUNCH();
     SplatParams P{};
     P.W = width; P.H = height; P.k_max = k_max; P.n = n;
@@ -352,15 +462,20 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     P.xs = pixel_ndc; P.ys = pixel_ndc + width;
     P.coef = reinterpret_cast<const float4 *>(coef);
     P.thr = thr; P.hdr = reinterpret_cast<const int4 *>(pix_hdr); P.acc = rec_acc;
-    const int smem = kSplatWarps * (int)sizeof(SplatWarpSmem);
+    area_class_kernel<<<148 * 4, 256, 0, st>>>(P, cls, big_list, counters, hist);
+    SS_CUDA_CHECK_LAUNCH();
+    area_scatter_kernel<<<(n + 256 * kScatItems - 1) / (256 * kScatItems), 256, 0, st>>>(n, cls, hist, cursor, order,
+                                                                                       counters + 4);
+    SS_CUDA_CHECK_LAUNCH();
+    const int smem = kSplatWarps * (int)sizeof(GroupSmem);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(splat_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    splat_bwd_kernel<<<148 * 3, 32 * kSplatWarps, smem, st>>>(P, big_list, big_count);
+    splat_bwd_kernel<<<148 * 3, 32 * kSplatWarps, smem, st>>>(P, order, counters);
     SS_CUDA_CHECK_LAUNCH();
-    big_bwd_kernel<<<148 * 4, 256, 0, st>>>(P, big_list, big_count);
+    big_bwd_kernel<<<148 * 4, 256, 0, st>>>(P, big_list, counters);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

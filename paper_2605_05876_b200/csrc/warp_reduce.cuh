@@ -50,3 +50,25 @@ __device__ __forceinline__ int warp_tr_index(int lane) {
     for (int i = 0; i < N; ++i) idx[i] = i;
     return warp_tr_index_rec<N, 16>(idx, lane);
 }
+
+template <int N, int O>
+__device__ __forceinline__ void warp_tr_indices_rec(int *idx, int lane) {
+    constexpr int H = N / 2;
+    const bool upper = (lane & O) != 0;
+#pragma unroll
+    for (int i = 0; i < H; ++i) idx[i] = upper ? idx[i + H] : idx[i];
+    if constexpr ((N & 1) != 0) idx[H] = idx[N - 1];
+    if constexpr (O > 1) warp_tr_indices_rec<N / 2 + (N & 1), O / 2>(idx, lane);
+}
+
+// Channel indices held in v[0 .. M) after warp_tr_all<N, O> (levels O .. 1,
+// i.e. a reduction within groups of 2*O lanes).
+template <int N, int O, int M>
+__device__ __forceinline__ void warp_tr_indices(int (&out)[M], int lane) {
+    int idx[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) idx[i] = i;
+    warp_tr_indices_rec<N, O>(idx, lane);
+#pragma unroll
+    for (int i = 0; i < M; ++i) out[i] = idx[i];
+}

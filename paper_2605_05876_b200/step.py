@@ -89,7 +89,8 @@ class ViewBuffers:
         self.coef = torch.empty((k_max, H * W, 4), **f32)
         self.thr = torch.empty((k_max, H * W), **f32)
         self.pix_hdr = torch.empty((H * W, 4), **i32)
-        self.pixel_ndc = torch.empty(W + H + 4 + n, **f32)  # NDC tables + 4 counters + big-rect queue
+        # NDC tables, counters, area-class sort and big-rect queue of the backward
+        self.pixel_ndc = torch.empty(_lib.load().ss_train_backward_scratch_words(n, W, H), **f32)
         self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
         self.capacity = 0
         self.keys = self.pair = self.pair_rect = None
