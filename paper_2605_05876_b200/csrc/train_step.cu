@@ -73,7 +73,11 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const int nc = h.x & 0xff;  // closed layers (the layer count sits in bits 8+)
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
             (nc > 2 && __int_as_float(h.w) < zs);
-    for (int j = 3; j < nc; ++j) m += __ldg(P.thr + j * HW + pix) < zs;
+    // the closing depths increase strictly with j: count until the first one >= zs
+    if (m == 3) {
+        const int jn = min(nc, P.k_max);
+        for (int j = 3; j < jn && __ldg(P.thr + j * HW + pix) < zs; ++j) ++m;
+    }
     if (m >= P.k_max) return 0;  // beyond the K_MAX stop: discarded
     const float4 cf = m == 0 ? cf0 : __ldg(P.coef + m * HW + pix);
     const float e = __expf(-0.5f * rho2);
