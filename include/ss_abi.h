@@ -158,10 +158,10 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
  * (losses.py:94-108, lambda_ssim=0) against `target` (H,W,3) and with the
  * per-pixel suffix recursion of backward.py:201-238.  Writes per pixel and
  * layer the float4 (A, dL/dC_raw rgb) into `coef` (k_max*H*W*4 floats,
- * layer-major planes), per pixel a packed header `pix_hdr` (H*W int4:
- * number of closed layers, then the depths at which layers 0..2 closed, as
- * float bits) and the closing depths of layers >= 3 into `thr` (k_max*H*W
- * floats, plane j), and adds sum|rgb - target| into loss_sum (1 double).
+ * layer-major planes), per pixel a packed header `pix_hdr` (H*W x 8
+ * int32: number of closed layers, then the depths at which layers 0..6
+ * closed, as float bits; words past the closed count are not written) and
+ * the closing depths of layers >= 7 into `thr` (k_max*H*W floats, plane j), and adds sum|rgb - target| into loss_sum (1 double).
  * rgb (H,W,3) is nullable.
  * ss_train_backward_records: pass 2 of backward.py:240-320 without the walk:
  * a covering record with interval start zs belongs to layer

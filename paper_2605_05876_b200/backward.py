@@ -67,7 +67,7 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp):
     f32 = dict(device=dev, dtype=torch.float32)
     coef = torch.empty((K, H * W, 4), **f32)
     thr = torch.empty((K, H * W), **f32)
-    hdr = torch.empty((H * W, 4), device=dev, dtype=torch.int32)
+    hdr = torch.empty((H * W, 8), device=dev, dtype=torch.int32)
     rgb = torch.empty((H, W, 3), **f32)
     _lib.check(lib.ss_train_forward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
                                     _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, K, None, _lib.ptr(coef),

@@ -44,7 +44,7 @@ struct FwdParams {
     float inv_count;       // 1 / (3 H W): mean over all image entries
     float4 *coef;          // (k_max, H*W) float4
     float *thr;            // (k_max, H*W) depth at which layer j >= 3 closed
-    int4 *hdr;             // (H*W) packed (closed-layer count, closing depth of layers 0..2)
+    int4 *hdr;             // (H*W, 2) packed (closed-layer count, closing depths of layers 0..2), (depths 3..6)
     double *loss;          // sum of |rgb - target| (1 double)
 };
 
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
                     if (ncl == 0) th0 = zmax;
                     else if (ncl == 1) th1 = zmax;
                     else if (ncl == 2) th2 = zmax;
+                    else if (ncl < 7) reinterpret_cast<float *>(P.hdr)[8 * pix + 1 + ncl] = zmax;
                     else P.thr[(size_t)ncl * P.W * P.H + pix] = zmax;
                 }
                 ++ncl;
@@ -161,12 +162,12 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
         } else if (!P.target) {
             // deferred loss (ss_train_coefs finishes the layer coefficients
             // once the image-space gradient is known): raw layer sums
-            P.hdr[pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
+            P.hdr[2 * pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
             const size_t HW = (size_t)P.W * P.H;
             for (int m = 0; m < layers; ++m) P.coef[(size_t)m * HW + pix] = make_float4(lw[m], lc0[m], lc1[m], lc2[m]);
             if (P.alpha) P.alpha[pix] = 1.f - T;
         } else {
-            P.hdr[pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
+            P.hdr[2 * pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
             // L1 loss and its image gradient (losses.py:100-104)
             const float d0 = r0 - P.target[3 * pix], d1 = r1 - P.target[3 * pix + 1], d2 = r2 - P.target[3 * pix + 2];
             lsum = (double)fabsf(d0) + (double)fabsf(d1) + (double)fabsf(d2);
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, const int4 *__r
 {
     const int pix = blockIdx.x * blockDim.x + threadIdx.x;
     if (pix >= HW) return;
-    const int layers = hdr[pix].x >> 8;
+    const int layers = hdr[2 * pix].x >> 8;
     if (layers == 0) return;
     double a[SS_KMAX_CAP], tb[SS_KMAX_CAP];
     float4 raw[SS_KMAX_CAP];

@@ -33,7 +33,7 @@ struct SplatParams {
     const float *xs, *ys;   // pixel-centre NDC per column / row
     const float4 *coef;     // (k_max, HW) per-layer (A, dL/dC_raw)
     const float *thr;       // (k_max, HW) closing depths of layers >= 3
-    const int4 *hdr;        // (HW) (closed-layer count, closing depths of layers 0..2)
+    const int4 *hdr;        // (HW, 2) (closed-layer count, closing depths of layers 0..2), (depths 3..6)
     float *acc;             // (n, 20)
 };
 
@@ -63,7 +63,7 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const size_t pix = (size_t)iy * P.W + ix;
     // the packed header and the (most common) layer-0 coefficients are loaded
     // together, before the geometry below, so their latency hides behind it
-    const int4 h = __ldg(P.hdr + pix);
+    const int4 h = __ldg(P.hdr + 2 * pix);
     const float4 cf0 = __ldg(P.coef + pix);
     // ray / tangent-plane quantities of the backward (rasterizer.py:197-207)
     const float k0 = fs(fm(x, R.b.z), R.a.x), k1 = fs(fm(x, R.b.w), R.a.y), k2 = fs(fm(x, R.c.x), R.a.z);
@@ -73,10 +73,16 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const int nc = h.x & 0xff;  // closed layers (the layer count sits in bits 8+)
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
             (nc > 2 && __int_as_float(h.w) < zs);
-    // the closing depths increase strictly with j: count until the first one >= zs
-    if (m == 3) {
-        const int jn = min(nc, P.k_max);
-        for (int j = 3; j < jn && __ldg(P.thr + j * HW + pix) < zs; ++j) ++m;
+    // the closing depths increase strictly with j: the second header half
+    // (same 32-byte sector) only when zs lies beyond the first three
+    if (m == 3 && nc > 3) {
+        const int4 h2 = __ldg(P.hdr + 2 * pix + 1);
+        m += (__int_as_float(h2.x) < zs) + (nc > 4 && __int_as_float(h2.y) < zs) +
+             (nc > 5 && __int_as_float(h2.z) < zs) + (nc > 6 && __int_as_float(h2.w) < zs);
+        if (m == 7) {
+            const int jn = min(nc, P.k_max);
+            for (int j = 7; j < jn && __ldg(P.thr + j * HW + pix) < zs; ++j) ++m;
+        }
     }
     if (m >= P.k_max) return 0;  // beyond the K_MAX stop: discarded
     const float4 cf = m == 0 ? cf0 : __ldg(P.coef + m * HW + pix);

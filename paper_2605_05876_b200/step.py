@@ -88,7 +88,7 @@ class ViewBuffers:
         self.tile_order = torch.empty(ntiles, **i32)
         self.coef = torch.empty((k_max, H * W, 4), **f32)
         self.thr = torch.empty((k_max, H * W), **f32)
-        self.pix_hdr = torch.empty((H * W, 4), **i32)
+        self.pix_hdr = torch.empty((H * W, 8), **i32)
         # NDC tables, counters, area-class sort and big-rect queue of the backward
         self.pixel_ndc = torch.empty(_lib.load().ss_train_backward_scratch_words(n, W, H), **f32)
         self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
