@@ -142,6 +142,19 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
     const unsigned FULL = 0xffffffffu;
     const unsigned lt = (1u << w.lane) - 1u;
     int cursor = p0;
+    // the next window's pair rects and record indices are loaded one window
+    // ahead (right after the cursor moves), so their latency hides behind
+    // the current window's record loads and the chunk's phases
+    uint2 pr_next = make_uint2(0u, 0u);
+    int rec_next = 0;
+    auto prefetch = [&](int c) {
+        const int p = c + w.lane;
+        if (p < p1) {
+            pr_next = __ldg(pair_rect + p);
+            rec_next = __ldg(pair_rec + p);
+        }
+    };
+    prefetch(cursor);
     while (cursor < p1) {
         if (stop()) break;
         // fill up to 32 slots with the next overlapping records (list order),
@@ -149,10 +162,11 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
         int n = 0;
         while (n < kSlots && cursor < p1) {
             const int p = cursor + w.lane;
+            const uint2 pr = pr_next;
+            const int rec = rec_next;
             bool ov = false;
             int meta = 0;
             if (p < p1) {
-                const uint2 pr = __ldg(pair_rect + p);
                 const int x0 = pr.x & 0xffff, y0 = pr.x >> 16, x1 = pr.y & 0xffff, y1 = pr.y >> 16;
                 ov = x0 < w.bx + 8 && x1 > w.bx && y0 < w.by + 4 && y1 > w.by;
                 const int cx0 = max(x0 - w.bx, 0), cw = min(x1 - w.bx, 8) - cx0;
@@ -169,9 +183,9 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
             } else {
                 cursor += 32;
             }
+            prefetch(cursor);
             if ((ovm >> w.lane) & 1u) {
                 const int pos = n + __popc(ovm & lt);
-                const int rec = __ldg(pair_rec + p);
                 const float4 *src = reinterpret_cast<const float4 *>(recs + rec);
                 const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3),
                              e = __ldg(src + 4);

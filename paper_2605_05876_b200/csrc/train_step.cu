@@ -152,6 +152,9 @@ constexpr int kNB = 64;        // area classes of the other records
 constexpr int kGL = 8;         // lanes per record group (4 records per warp)
 constexpr int kGCap = 128;     // rect pixels compacted per group pass
 constexpr int kSplatWarps = 8;
+#ifndef SS_SPLAT_MINB
+#define SS_SPLAT_MINB 3  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr int kScatItems = 8;  // records per thread of the class scatter
 constexpr int kHeavyClass = 32;  // area >= 64 px: one round per work-counter ticket (else 8)
 
@@ -264,7 +267,7 @@ struct GroupSmem {
 // pass 2 evaluates the gradient on the covered items, 8 per iteration.  One
 // 3-level transposed reduction per group and plain stores of the record's
 // row (each record committed exactly once: no atomics, deterministic).
-__global__ void __launch_bounds__(32 * kSplatWarps, 3) splat_bwd_kernel(SplatParams P, const int32_t *order,
+__global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_kernel(SplatParams P, const int32_t *order,
                                                                         int32_t *counters)
 {
     extern __shared__ __align__(16) unsigned char splat_smem[];
@@ -483,7 +486,7 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
         cudaFuncSetAttribute(splat_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    splat_bwd_kernel<<<148 * 3, 32 * kSplatWarps, smem, st>>>(P, order, counters);
+    splat_bwd_kernel<<<148 * SS_SPLAT_MINB, 32 * kSplatWarps, smem, st>>>(P, order, counters);
     SS_CUDA_CHECK_LAUNCH();
     big_bwd_kernel<<<148 * 4, 256, 0, st>>>(P, big_list, counters);
     SS_CUDA_CHECK_LAUNCH();
