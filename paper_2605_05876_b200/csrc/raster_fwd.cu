@@ -51,7 +51,10 @@ struct FwdParams {
 // CTAs of kFwdWarps warps (a tile is split over tile*tile/32/kFwdWarps
 // CTAs; measured 4 > 2 = 8 > 1 with the heavy-first tile order): warps never
 // wait for each other.
-constexpr int kFwdWarps = 4;
+#ifndef SS_FWD_WARPS
+#define SS_FWD_WARPS 4
+#endif
+constexpr int kFwdWarps = SS_FWD_WARPS;
 
 template <bool kExtras, bool kTrain>
 __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)

@@ -177,8 +177,11 @@ class TrainStep:
         self.collect_stats = False
         self._pairs, self._kept, self._nviews = [], [], 0
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
+        self.active_streams = None     # None: all worker streams; 1: views serialised (isolated kernel timing)
         self._stage = None
-        self.launches_per_view = 13    # preprocess, scan, order, scatter, tile sort x2, train fwd, ndc + record bwd x2, chain, env merge x2
+        # preprocess, scan, order, scatter, tile sort x2, train fwd, ndc, area class, class scatter,
+        # record bwd, big-rect bwd, chain, env merge x2
+        self.launches_per_view = 15
         self.launches_per_step_fixed = 4 + 1 + 4  # env adjoint, fused Adam (+ quat renorm), env refresh
 
     # -- buffers -----------------------------------------------------------
@@ -288,8 +291,9 @@ class TrainStep:
         for st in self.streams:
             st.wait_stream(main)
         prev = None
+        nst = min(len(self.streams), self.active_streams or len(self.streams))
         for i, cam in enumerate(cameras):
-            k = i % len(self.streams)
+            k = i % nst
             with torch.cuda.stream(self.streams[k]):
                 tgt = targets_for(i, self.streams[k])
                 prev = self.view(cam, tgt, self.bufs[k], chain_after=prev,

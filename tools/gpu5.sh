@@ -8,5 +8,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include 
     --log-file gpurun_out/launches_$TAG.csv python tools/profile_step.py > gpurun_out/ncu_launch.log 2>&1
 echo "launch rc=$?"
 NVIEWS=2 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "ss_step/" \
-    -k regex:"splat_bwd|raster_fwd|chain|scatter|tile_sort|preprocess" -c 6 -o gpurun_out/prof_$TAG python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1
+    -k regex:"splat_bwd|raster_fwd|chain|scatter|tile_sort|preprocess" -c 8 -o gpurun_out/prof_$TAG python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"

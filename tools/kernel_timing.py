@@ -25,7 +25,7 @@ cloud = ss.SurfelCloud(**init)
 env = ss.EnvironmentLight(np.log(env_base))
 LOSS = os.environ.get("LOSS", "l1")
 for S in (1, 2, 3):
-    ts = TrainStep(cloud, env, 800, 800, streams=S, loss=LOSS)
+    ts = TrainStep(cloud, env, 800, 800, streams=S, loss=LOSS, tile=int(os.environ.get("TILE", "16")))
     ts.size_pairs(cams[:2])
     for _ in range(2):
         ts.step(cams, targets)
