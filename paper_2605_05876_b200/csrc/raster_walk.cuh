@@ -88,14 +88,19 @@ struct RecGeo {
 #endif
 constexpr int kSlots = SS_PACK_SLOTS;  // overlapping records per chunk (<= 32)
 
-struct PackedScratch {
+// One chunk of overlapping records (double-buffered: the next chunk's
+// records stream in with cp.async while the current one is processed).
+struct ChunkBuf {
     RecGeo geo[kSlots];       // t1, t2, t4, Sigma^-1, n_f, view_z, z_start, z_end
+    float4 ext[kSlots];       // colour r, g, b, coverage margin (record bytes 64..79)
+    int meta[32];             // in-block rect: cx0 | cw << 4 | ry0 << 8 | cnt << 12 (lanes >= n: unread)
+    int pidx[kSlots];
+};
+
+struct PackedScratch {
+    ChunkBuf buf[2];
     float wgt[kSlots][32];    // [slot][pixel]: n_f exp(-rho^2/2) when covered, -1 when not (in-rect only)
     unsigned mask[32];        // per pixel: slots whose rect contains it
-    float4 zc[kSlots];        // z_start, z_end, colour r, g
-    float c2[kSlots], vz[kSlots]; // colour b, view_z
-    int meta[32];             // in-block rect: cx0 | cw << 4 | ry0 << 8 | cnt << 12 (lanes >= kSlots: 0)
-    int pidx[kSlots];
     int ncov[32];             // covered lanes per slot (pair cover counts)
     float xs[8], ys[4];
 };
@@ -144,7 +149,7 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
     int cursor = p0;
     // the next window's pair rects and record indices are loaded one window
     // ahead (right after the cursor moves), so their latency hides behind
-    // the current window's record loads and the chunk's phases
+    // the current window's work
     uint2 pr_next = make_uint2(0u, 0u);
     int rec_next = 0;
     auto prefetch = [&](int c) {
@@ -154,11 +159,10 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
             rec_next = __ldg(pair_rec + p);
         }
     };
-    prefetch(cursor);
-    while (cursor < p1) {
-        if (stop()) break;
-        // fill up to 32 slots with the next overlapping records (list order),
-        // scanning as many 32-pair windows as that takes
+    // fill cb with up to kSlots next overlapping records (list order),
+    // scanning as many 32-pair windows as that takes; the records are copied
+    // with cp.async (one commit group per chunk)
+    auto fill = [&](ChunkBuf &cb) -> int {
         int n = 0;
         while (n < kSlots && cursor < p1) {
             const int p = cursor + w.lane;
@@ -187,20 +191,30 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
             if ((ovm >> w.lane) & 1u) {
                 const int pos = n + __popc(ovm & lt);
                 const float4 *src = reinterpret_cast<const float4 *>(recs + rec);
-                const float4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2), d = __ldg(src + 3),
-                             e = __ldg(src + 4);
-                sm.geo[pos].a = a; sm.geo[pos].b = b; sm.geo[pos].c = c; sm.geo[pos].d = d;
-                sm.zc[pos] = make_float4(d.z, d.w, e.x, e.y);
-                sm.c2[pos] = e.z; sm.vz[pos] = d.y;
-                sm.meta[pos] = meta;
-                sm.pidx[pos] = p;
+                cp_async16(&cb.geo[pos].a, src);
+                cp_async16(&cb.geo[pos].b, src + 1);
+                cp_async16(&cb.geo[pos].c, src + 2);
+                cp_async16(&cb.geo[pos].d, src + 3);
+                cp_async16(&cb.ext[pos], src + 4);
+                cb.meta[pos] = meta;
+                cb.pidx[pos] = p;
             }
             n += __popc(ovm);
         }
-        if (n == 0) break;
+        cp_async_commit();
+        return n;
+    };
+    prefetch(cursor);
+    int cur = 0;
+    int n = stop() ? 0 : fill(sm.buf[0]);
+    while (n > 0) {
+        cp_async_wait_all();
         __syncwarp();
+        ChunkBuf &cb = sm.buf[cur];
+        // the next chunk streams into the other buffer during this one's phases
+        const int n_next = cursor < p1 ? fill(sm.buf[cur ^ 1]) : 0;
         // phase 1: inclusive scan of the per-slot item counts, then packed items
-        const int my_meta = w.lane < n ? sm.meta[w.lane] : 0;
+        const int my_meta = w.lane < n ? cb.meta[w.lane] : 0;
         const int cnt = my_meta >> 12;
         int incl = cnt;
 #pragma unroll
@@ -227,7 +241,7 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
                 const int row = (k * (int)(pk >> 23)) >> 8;
                 const int col = k - row * cw;
                 const int px = (ry0 + row) * 8 + cx0 + col;
-                const float wv = weight(sm.geo[s], sm.xs[px & 7], sm.ys[px >> 3]);
+                const float wv = weight(cb.geo[s], sm.xs[px & 7], sm.ys[px >> 3]);
                 sm.wgt[s][px] = wv;
                 if (!kCoveredOnly || wv >= 0.f) atomicOr(&sm.mask[px], 1u << s);
             }
@@ -242,18 +256,23 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
                 v.slot = __ffs(M) - 1;
                 M &= M - 1u;
                 v.w = sm.wgt[v.slot][w.lane];
-                const float4 zc = sm.zc[v.slot];
-                v.zs = zc.x; v.ze = zc.y; v.c0 = zc.z; v.c1 = zc.w;
-                v.c2 = sm.c2[v.slot]; v.vz = sm.vz[v.slot];
+                const float4 d = cb.geo[v.slot].d;
+                const float4 e = cb.ext[v.slot];
+                v.zs = d.z; v.ze = d.w; v.vz = d.y;
+                v.c0 = e.x; v.c1 = e.y; v.c2 = e.z;
                 f(v);
             }
         }
         __syncwarp();
         if (pair_cover && w.lane < n && sm.ncov[w.lane] > 0) {  // f counted covered lanes per slot
-            atomicAdd(&pair_cover[sm.pidx[w.lane]], sm.ncov[w.lane]);
+            atomicAdd(&pair_cover[cb.pidx[w.lane]], sm.ncov[w.lane]);
             sm.ncov[w.lane] = 0;
         }
+        if (stop()) break;  // polled between chunks
+        n = n_next;
+        cur ^= 1;
     }
+    cp_async_wait_all();
 }
 
 // Coverage of pixel (x, y) by a record, with everything downstream.

@@ -138,13 +138,6 @@ __device__ __forceinline__ void load_record(const SsRecord *recs, int rec, SsRec
     R.r = __ldg(reinterpret_cast<const int4 *>(src) + 5);
 }
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-
 constexpr int kBigChunk = 1024;
 constexpr int kHugeArea = 8 * kBigChunk;  // big rects above this are spread over the grid
 constexpr int kBigArea = 512;  // rects above this go to the CTA-chunked kernel (~0.1% of records)
