@@ -37,7 +37,11 @@ extern "C" {
 enum { SS_OK = 0, SS_ERR_INVALID = 1, SS_ERR_CUDA = 2 };
 
 #define SS_REC_FLOATS 24  /* 96-byte record, see SsRecord in csrc/ss_common.cuh */
-#define SS_ACC_FLOATS 20  /* per-record backward accumulator: 17 grads + ss + touch + pad */
+#define SS_ACC_FLOATS 20  /* per-record backward accumulator: 17 grads + ss + touch + layout flag */
+/* slot 19 of an accumulator row: 0 = slots 0..8 hold dL/dt1, dt2, dt4;
+ * SS_ACC_MOMENTS = they hold sum gp, sum x gp, sum y gp of the ray-plane
+ * gradient (record-parallel backward; ss_chain_backward converts) */
+#define SS_ACC_MOMENTS 1.0f
 #define SS_KMAX_CAP 16    /* largest k_max the kernels accept (= reference default K_MAX) */
 
 typedef struct SsCamera {

@@ -149,6 +149,21 @@ __global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
 
     float t1f[3], t2f[3], t4f[3];
     rows_of(P, i, t1f, t2f, t4f);
+    if (a4.w == SS_ACC_MOMENTS) {
+        // moments of the ray-plane gradient (train_step.cu item_grad): with
+        // k = x t4 - t1, l = y t4 - t2,  sum l x gp = t4 x Sy - t2 x S,
+        // sum gp x k = Sx x t4 - S x t1, sum x (l x gp) + y (gp x k) = t1 x Sy - t2 x Sx
+        const double S[3] = {G1[0], G1[1], G1[2]}, Sx[3] = {G2[0], G2[1], G2[2]}, Sy[3] = {G4[0], G4[1], G4[2]};
+        const double T1[3] = {t1f[0], t1f[1], t1f[2]}, T2[3] = {t2f[0], t2f[1], t2f[2]};
+        const double T4[3] = {t4f[0], t4f[1], t4f[2]};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int c1 = (c + 1) % 3, c2 = (c + 2) % 3;
+            G1[c] = (T2[c1] * S[c2] - T2[c2] * S[c1]) - (T4[c1] * Sy[c2] - T4[c2] * Sy[c1]);
+            G2[c] = (S[c1] * T1[c2] - S[c2] * T1[c1]) - (Sx[c1] * T4[c2] - Sx[c2] * T4[c1]);
+            G4[c] = (T1[c1] * Sy[c2] - T1[c2] * Sy[c1]) - (T2[c1] * Sx[c2] - T2[c2] * Sx[c1]);
+        }
+    }
     if (P.mip) {
         // _mip_chain_backward (backward.py:473-548)
         float jf[4];

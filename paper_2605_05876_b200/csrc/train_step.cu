@@ -66,8 +66,8 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const int4 h = __ldg(P.hdr + 2 * pix);
     const float4 cf0 = __ldg(P.coef + pix);
     // ray / tangent-plane quantities of the backward (rasterizer.py:197-207)
-    const float k0 = fs(fm(x, R.b.z), R.a.x), k1 = fs(fm(x, R.b.w), R.a.y), k2 = fs(fm(x, R.c.x), R.a.z);
-    const float l0 = fs(fm(y, R.b.z), R.a.w), l1 = fs(fm(y, R.b.w), R.b.x), l2 = fs(fm(y, R.c.x), R.b.y);
+    const float k0 = fs(fm(x, R.b.z), R.a.x), k1 = fs(fm(x, R.b.w), R.a.y);
+    const float l0 = fs(fm(y, R.b.z), R.a.w), l1 = fs(fm(y, R.b.w), R.b.x);
     const float inv_den = fast_rcp(fs(fm(k0, l1), fm(k1, l0)));
     const float zs = R.d.z;
     const int nc = h.x & 0xff;  // closed layers (the layer count sits in bits 8+)
@@ -96,15 +96,16 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const float gu = 2.f * gr * (R.c.y * u + R.c.z * v);
     const float gv = 2.f * gr * (R.c.z * u + R.c.w * v);
     const float gp0 = gu * inv_den, gp1 = gv * inv_den, gp2 = -(gu * u + gv * v) * inv_den;
-    const float gk0 = l1 * gp2 - l2 * gp1;
-    const float gk1 = l2 * gp0 - l0 * gp2;
+    // k = x t4 - t1 and l = y t4 - t2 are linear in the pixel centre, so the
+    // per-item dL/dk = l x gp, dL/dl = gp x k and their T-row images sum to
+    // cross products of the record's rows with three moments of gp
+    // (sum gp, sum x gp, sum y gp): those 9 channels are accumulated here
+    // and turned into dL/dt1, dt2, dt4 by the chain kernel (SS_ACC_MOMENTS)
+    g[0] += gp0; g[1] += gp1; g[2] += gp2;
+    g[3] += x * gp0; g[4] += x * gp1; g[5] += x * gp2;
+    g[6] += y * gp0; g[7] += y * gp1; g[8] += y * gp2;
     const float gk2 = l0 * gp1 - l1 * gp0;
-    const float gl0 = gp1 * k2 - gp2 * k1;
-    const float gl1 = gp2 * k0 - gp0 * k2;
     const float gl2 = gp0 * k1 - gp1 * k0;
-    g[0] -= gk0; g[1] -= gk1; g[2] -= gk2;
-    g[3] -= gl0; g[4] -= gl1; g[5] -= gl2;
-    g[6] += x * gk0 + y * gl0; g[7] += x * gk1 + y * gl1; g[8] += x * gk2 + y * gl2;
     float nrm;  // screen-space gradient norm (Eq. 12): approximate sqrt, no slow path
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(gk2 * gk2 + gl2 * gl2));
     g[16] += fabsf(R.c.x) * nrm;
@@ -185,7 +186,8 @@ __global__ void __launch_bounds__(256) area_class_kernel(SplatParams P, uint8_t 
             if (area > kBigArea) {
                 float4 *dst = reinterpret_cast<float4 *>(P.acc + (size_t)r * SS_ACC_FLOATS);
 #pragma unroll
-                for (int i = 0; i < SS_ACC_FLOATS / 4; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int i = 0; i < SS_ACC_FLOATS / 4 - 1; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                dst[SS_ACC_FLOATS / 4 - 1] = make_float4(0.f, 0.f, 0.f, SS_ACC_MOMENTS);
                 if (area > kHugeArea) big_list[P.n - 1 - atomicAdd(counters + 1, 1)] = r;
                 else big_list[atomicAdd(counters, 1)] = r;
             } else {
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
             for (int i = 0; i < 3; ++i) dst[ch[i] == 16 ? 17 : ch[i]] = g[i];
             if (gl == 0) reinterpret_cast<int *>(dst)[18] = touch;
             if (gl == 1) dst[16] = 0.f;
-            if (gl == 2) dst[19] = 0.f;
+            if (gl == 2) dst[19] = SS_ACC_MOMENTS;
         }
         __syncwarp();
         cur = nxt;
