@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
             }
             Cover c;
             if (!ss_cover(x, y, R, c)) return;
-            const float w = R.d.x * __expf(-0.5f * c.rho2);
+            const float w = R.d.x * ss_exp_fast(-0.5f * c.rho2);
             const float z = R.d.y;
             if (Wg == 0.f) z0 = z;
             const float dz = z - z0;
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
                         cov = true;
                         ++group_n;
                         if (R.d.w > zmax) zmax = R.d.w;
-                        const float e = __expf(-0.5f * c.rho2);
+                        const float e = ss_exp_fast(-0.5f * c.rho2);
                         const float w = R.d.x * e;
                         const float dz = R.d.y - Zb;
                         const float gw = A + G0 * R.e.x + G1 * R.e.y + G2 * R.e.z + Bz * dz + Qv * (dz * dz - Vr);

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
             // independent rounding noise of ~1e-4 relative at the support edge)
             [](const RecGeo &R, float x, float y) {
                 Cover c;
-                return ss_cover(x, y, R, c) ? R.d.x * __expf(-0.5f * c.rho2) : -1.f;
+                return ss_cover(x, y, R, c) ? R.d.x * ss_exp_fast(-0.5f * c.rho2) : -1.f;
             },
             [&](const SlotView &v) {
             if (stopped) {
