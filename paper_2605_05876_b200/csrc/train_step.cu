@@ -30,7 +30,8 @@ struct SplatParams {
     int W, H, k_max, n;
     const int8_t *cull;
     const SsRecord *records;
-    const float *xs, *ys;   // pixel-centre NDC per column / row
+    const float *xs, *ys;   // pixel-centre NDC per column / row (exact: coverage decisions)
+    float sx, ox, sy, oy;   // x ~ ix * sx + ox, y ~ iy * sy + oy (within an ulp: gradient arithmetic)
     const float4 *coef;     // (k_max, HW) per-layer (A, dL/dC_raw)
     const float *thr;       // (k_max, HW) closing depths of layers >= 3
     const int4 *hdr;        // (HW, 2) (closed-layer count, closing depths of layers 0..2), (depths 3..6)
@@ -59,7 +60,9 @@ __device__ __forceinline__ float fast_rcp(float x) {
 __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R, int ix, int iy, float u, float v,
                                          float rho2, float g[NCH]) {
     const size_t HW = (size_t)P.W * P.H;
-    const float x = __ldg(P.xs + ix), y = __ldg(P.ys + iy);
+    // the gradient only needs the pixel centre to float accuracy: one FMA
+    // each instead of the exact tables the coverage decision reads
+    const float x = fmaf((float)ix, P.sx, P.ox), y = fmaf((float)iy, P.sy, P.oy);
     const size_t pix = (size_t)iy * P.W + ix;
     // the packed header and the (most common) layer-0 coefficients are loaded
     // together, before the geometry below, so their latency hides behind it
@@ -469,6 +472,8 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     P.cull = cull;
     P.records = reinterpret_cast<const SsRecord *>(records);
     P.xs = pixel_ndc; P.ys = pixel_ndc + width;
+    P.sx = (float)(2.0 / width); P.ox = (float)(1.0 / width - 1.0);
+    P.sy = (float)(-2.0 / height); P.oy = (float)(1.0 - 1.0 / height);
     P.coef = reinterpret_cast<const float4 *>(coef);
     P.thr = thr; P.hdr = reinterpret_cast<const int4 *>(pix_hdr); P.acc = rec_acc;
     area_class_kernel<<<148 * 4, 256, 0, st>>>(P, cls, big_list, counters, hist);
