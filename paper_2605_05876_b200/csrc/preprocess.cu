@@ -33,7 +33,10 @@ struct CamF {
     int W, H;
 };
 
-__global__ void __launch_bounds__(256) preprocess_kernel(
+#ifndef SS_PRE_MINB
+#define SS_PRE_MINB 3  // 85 registers, 3 CTAs per SM (small spill, better latency hiding)
+#endif
+__global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
     SsCloud cloud, CamF cam, SsPreprocessOpts opt, int color_source, const float *__restrict__ colors_in,
     SsEnv env, SsRecord *__restrict__ records, int8_t *__restrict__ cull_out,
     int32_t *__restrict__ pair_count, int32_t *__restrict__ tile_counts, uint4 *__restrict__ bininfo, SsProjAux aux,
@@ -198,7 +201,10 @@ __global__ void __launch_bounds__(256) preprocess_kernel(
     }
     // per-tile histogram (one global atomic per (record, tile); records in
     // source order spread over the image, so the counters see little contention)
-    for (int s = 0; s < count; ++s) atomicAdd(&tile_counts[(ty0 + s / sx) * ntx + tx0 + s % sx], 1);
+    for (int s = 0, tx = tx0, ty = ty0; s < count; ++s) {
+        atomicAdd(&tile_counts[ty * ntx + tx], 1);
+        if (++tx == tx0 + sx) { tx = tx0; ++ty; }
+    }
     if (!in_range) return;
     records[i] = rec;
     cull_out[i] = (int8_t)code;
