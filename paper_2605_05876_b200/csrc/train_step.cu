@@ -119,11 +119,11 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
 // Coverage of rect pixel k (row-major) of record R (fast path with the
 // record's certified margin, exact reference arithmetic when undecided); on
 // a hit returns the pixel (ix | iy << 16) and u, v, rho^2.
-__device__ __forceinline__ bool item_cover(const SplatParams &P, const SsRecord &R, const FastCov &f, int k, int rw,
-                                           float inv_rw, int &ixy, float4 &q) {
+__device__ __forceinline__ bool item_cover(const float *xs, const float *ys, const SsRecord &R, const FastCov &f, int k,
+                                           int rw, float inv_rw, int &ixy, float4 &q) {
     const int ky = (int)(((float)k + 0.5f) * inv_rw);
     const int iy = R.r.y + ky, ix = R.r.x + (k - ky * rw);
-    const float x = __ldg(P.xs + ix), y = __ldg(P.ys + iy);
+    const float x = xs[ix], y = ys[iy];
     float u, v, r2;
     const int d = fast_cover(f, R.c.y, R.c.z, R.c.w, x, y, u, v, r2);
     if (d == 0) return false;
@@ -150,6 +150,7 @@ constexpr int kNB = 64;        // area classes of the other records
 constexpr int kGL = 8;         // lanes per record group (4 records per warp)
 constexpr int kGCap = 128;     // rect pixels compacted per group pass
 constexpr int kSplatWarps = 8;
+constexpr int kNdcSmem = 4096;  // W + H up to this: pixel-centre tables staged in shared memory
 #ifndef SS_SPLAT_MINB
 #define SS_SPLAT_MINB 3  // resident CTAs per SM the register budget is sized for
 #endif
@@ -266,11 +267,22 @@ struct GroupSmem {
 // pass 2 evaluates the gradient on the covered items, 8 per iteration.  One
 // 3-level transposed reduction per group and plain stores of the record's
 // row (each record committed exactly once: no atomics, deterministic).
+template <bool kSmemNdc>
 __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_kernel(SplatParams P, const int32_t *order,
                                                                         int32_t *counters)
 {
     extern __shared__ __align__(16) unsigned char splat_smem[];
     GroupSmem &sm = reinterpret_cast<GroupSmem *>(splat_smem)[threadIdx.x >> 5];
+    // the exact pixel-centre tables of the coverage decisions, staged in
+    // shared memory when they fit (one CTA barrier, at the start)
+    const float *xs = P.xs, *ys = P.ys;
+    if constexpr (kSmemNdc) {
+        float *s_ndc = reinterpret_cast<float *>(splat_smem + kSplatWarps * sizeof(GroupSmem));
+        for (int t = threadIdx.x; t < P.W + P.H; t += blockDim.x) s_ndc[t] = P.xs[t];
+        __syncthreads();
+        xs = s_ndc;
+        ys = s_ndc + P.W;
+    }
     const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & (kGL - 1);
     const unsigned glt = (1u << gl) - 1u;
     int ch[3];
@@ -329,7 +341,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
                 const int k = k0 + gl;
                 int ixy = 0;
                 float4 q;
-                const bool hit = k < area && item_cover(P, R, f, k, rw, inv_rw, ixy, q);
+                const bool hit = k < area && item_cover(xs, ys, R, f, k, rw, inv_rw, ixy, q);
                 const unsigned gm = (__ballot_sync(0xffffffffu, hit) >> (grp * kGL)) & 0xffu;
                 if (hit) {
                     const int slot = ncov + __popc(gm & glt);
@@ -380,7 +392,7 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
                                           float inv_rw, float g[NCH]) {
     int ixy;
     float4 q;
-    if (!item_cover(P, R, f, k, rw, inv_rw, ixy, q)) return 0;
+    if (!item_cover(P.xs, P.ys, R, f, k, rw, inv_rw, ixy, q)) return 0;
     return item_grad(P, R, ixy & 0xffff, ixy >> 16, q.x, q.y, q.z, g);
 }
 
@@ -482,12 +494,20 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
                                                                                        counters + 4);
     SS_CUDA_CHECK_LAUNCH();
     const int smem = kSplatWarps * (int)sizeof(GroupSmem);
+    const bool ndc_smem = width + height <= kNdcSmem;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(splat_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(splat_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem + kNdcSmem * (int)sizeof(float));
+        cudaFuncSetAttribute(splat_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    splat_bwd_kernel<<<148 * SS_SPLAT_MINB, 32 * kSplatWarps, smem, st>>>(P, order, counters);
+    // (the tables sit right after the NDC scratch: xs then ys, contiguous)
+    if (ndc_smem)
+        splat_bwd_kernel<true><<<148 * SS_SPLAT_MINB, 32 * kSplatWarps, smem + (width + height) * (int)sizeof(float),
+                                 st>>>(P, order, counters);
+    else
+        splat_bwd_kernel<false><<<148 * SS_SPLAT_MINB, 32 * kSplatWarps, smem, st>>>(P, order, counters);
     SS_CUDA_CHECK_LAUNCH();
     big_bwd_kernel<<<148 * 4, 256, 0, st>>>(P, big_list, counters);
     SS_CUDA_CHECK_LAUNCH();

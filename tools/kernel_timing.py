@@ -24,7 +24,7 @@ del gtc
 cloud = ss.SurfelCloud(**init)
 env = ss.EnvironmentLight(np.log(env_base))
 LOSS = os.environ.get("LOSS", "l1")
-for S in (1, 2, 3):
+for S in tuple(int(v) for v in os.environ.get("STREAMS", "1,2,3").split(",")):
     ts = TrainStep(cloud, env, 800, 800, streams=S, loss=LOSS, tile=int(os.environ.get("TILE", "16")))
     ts.size_pairs(cams[:2])
     for _ in range(2):
