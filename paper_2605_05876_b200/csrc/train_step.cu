@@ -154,7 +154,10 @@ constexpr int kNdcSmem = 4096;  // W + H up to this: pixel-centre tables staged 
 #ifndef SS_SPLAT_MINB
 #define SS_SPLAT_MINB 3  // resident CTAs per SM the register budget is sized for
 #endif
-constexpr int kScatItems = 8;  // records per thread of the class scatter
+#ifndef SS_SCAT_ITEMS
+#define SS_SCAT_ITEMS 8
+#endif
+constexpr int kScatItems = SS_SCAT_ITEMS;  // records per thread of the class scatter
 constexpr int kHeavyClass = 32;  // area >= 64 px: one round per work-counter ticket (else 8)
 
 // Scratch layout (32-bit words after the two NDC tables), see
