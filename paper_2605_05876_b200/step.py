@@ -297,7 +297,7 @@ class TrainStep:
             with torch.cuda.stream(self.streams[k]):
                 tgt = targets_for(i, self.streams[k])
                 prev = self.view(cam, tgt, self.bufs[k], chain_after=prev,
-                                 target_done=None if target_done is None else target_done[i % 2],
+                                 target_done=None if target_done is None else target_done[i % len(target_done)],
                                  mask=None if masks is None else masks[i])
                 if self.collect_stats:
                     b = self.bufs[k]
@@ -373,33 +373,35 @@ class TrainStep:
 
     def step_host(self, cameras, host_targets):
         """step() with the targets in pinned HOST memory: each view's target is
-        copied on a side stream into a double buffer, overlapped with the
-        previous view's kernels."""
+        copied on a side stream into a ring of staging buffers (one more than
+        the worker streams, so a copy never waits on a view still in flight on
+        another stream), overlapped with the previous views' kernels."""
         if self.capacity == 0:
             self.size_pairs(cameras[:2])
-        if self._stage is None:
+        nst = len(self.streams) + 1
+        if self._stage is None or len(self._stage) != nst:
             self._stage = [torch.empty((self.H, self.W, 3), device=self.pack.flat.device, dtype=torch.float32)
-                           for _ in range(2)]
+                           for _ in range(nst)]
             self._copy = torch.cuda.Stream()
-        ready = [torch.cuda.Event(), torch.cuda.Event()]
-        free = [torch.cuda.Event(), torch.cuda.Event()]
+        ready = [torch.cuda.Event() for _ in range(nst)]
+        free = [torch.cuda.Event() for _ in range(nst)]
         main = torch.cuda.current_stream()
         self._copy.wait_stream(main)
 
         def issue(i):
-            k = i % 2
+            k = i % nst
             with torch.cuda.stream(self._copy):
-                if i >= 2:
+                if i >= nst:
                     self._copy.wait_event(free[k])
                 self._stage[k].copy_(host_targets[i], non_blocking=True)
                 ready[k].record(self._copy)
 
         def target_for(i, stream):
-            # view i's target is copied while the previous view computes
+            # view i's target is copied while the previous views compute
             if i + 1 < len(cameras):
                 issue(i + 1)
-            stream.wait_event(ready[i % 2])
-            return self._stage[i % 2]
+            stream.wait_event(ready[i % nst])
+            return self._stage[i % nst]
 
         self.zero()
         self._nviews = len(cameras)
