@@ -92,6 +92,9 @@ class ViewBuffers:
         # NDC tables, counters, area-class sort and big-rect queue of the backward
         self.pixel_ndc = torch.empty(_lib.load().ss_train_backward_scratch_words(n, W, H), **f32)
         self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
+        # this buffer set's share of the step loss (photometric mode): views on
+        # different worker streams never read-modify-write the same scalar
+        self.loss_part = torch.zeros(1, device=device, dtype=torch.float64)
         self.capacity = 0
         self.keys = self.pair = self.pair_rect = None
 
@@ -217,10 +220,11 @@ class TrainStep:
 
     def view(self, cam, target, b=None, chain_after=None, target_done=None, mask=None):
         """Forward + backward of one view on the CURRENT stream with buffer set
-        b; gradients accumulate into self.grads.  chain_after: event the chain
-        kernel must wait for (the previous view's chain, which updates the same
-        gradient buffers); target_done: event recorded once `target` is consumed.
-        Returns the event recorded after this view's chain kernel."""
+        b; gradients accumulate into self.grads.  chain_after: event the
+        derived-map merge must wait for (the previous view's merge, which
+        updates the same float64 maps); target_done: event recorded once
+        `target` is consumed.  Returns the event recorded after this view's
+        merge."""
         lib = self.lib
         b = b if b is not None else self.bufs[0]
         s = _lib.stream_ptr()
@@ -249,13 +253,13 @@ class TrainStep:
                                             _lib.ptr(b.rgb), _lib.ptr(b.alpha), _lib.ptr(b.tile_order), s),
                        "ss_train_forward")
             out = b.imgloss(b.rgb, target, b.g_rgb, self.lambda_ssim, self.tone)
-            self.loss += out[0:1]
+            b.loss_part += out[0:1]
             g_alpha = None
             if mask is not None and self.lambda_sil > 0.0:
                 _lib.check(lib.ss_silhouette_loss(self.W * self.H, _lib.ptr(b.alpha), _lib.ptr(mask), _lib.ptr(b.sil),
                                                   _lib.ptr(b.g_alpha), _lib.ptr(b.sil_ws), s), "ss_silhouette_loss")
                 b.g_alpha.mul_(self.lambda_sil)
-                self.loss += self.lambda_sil * b.sil
+                b.loss_part += self.lambda_sil * b.sil
                 g_alpha = b.g_alpha
             _lib.check(lib.ss_train_coefs(self.W, self.H, self.k_max, _lib.ptr(b.pix_hdr), _lib.ptr(b.coef),
                                           _lib.ptr(b.g_rgb), _lib.ptr(g_alpha), self._bg[0], s), "ss_train_coefs")
@@ -268,13 +272,17 @@ class TrainStep:
                                                  _lib.ptr(b.pix_hdr), _lib.ptr(b.pixel_ndc), _lib.ptr(b.acc), s),
                    "ss_train_backward_records")
         self._ev_end(ev)
-        if chain_after is not None:
-            torch.cuda.current_stream().wait_event(chain_after)
         ev = self._ev_begin("chain")
+        # the chain kernels of concurrent views may overlap: their parameter
+        # gradients are vector reductions (atomic), the derived-map sums go to
+        # this buffer set's own float32 maps
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                          _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(b.cull),
                                          _lib.ptr(b.acc), ctypes.byref(b.gs), s), "ss_chain_backward")
-        # fold this view's float32 derived-map sums into the step's float64 ones
+        # fold this view's float32 derived-map sums into the step's float64
+        # ones: plain read-modify-write, so the merges are serialised
+        if chain_after is not None:
+            torch.cuda.current_stream().wait_event(chain_after)
         _lib.check(lib.ss_env_grad_merge(b.d_diff4.numel() // 4, _lib.ptr(b.d_diff4), _lib.ptr(self.d_diffuse), s),
                    "ss_env_grad_merge")
         _lib.check(lib.ss_env_grad_merge(b.d_spec4.numel() // 4, _lib.ptr(b.d_spec4), _lib.ptr(self.d_spec), s),
@@ -334,6 +342,8 @@ class TrainStep:
         self.d_spec.zero_()
         self.loss.zero_()
         for b in self.bufs:
+            b.loss_part.zero_()
+        for b in self.bufs:
             b.flags.zero_()
 
     def gradients(self, cameras, targets, masks=None):
@@ -354,6 +364,8 @@ class TrainStep:
                                            _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(self.d_diffuse),
                                            _lib.ptr(self.d_spec), _lib.ptr(self.d_base), _lib.ptr(self.g_env_log),
                                            _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()), "ss_env_adjoint")
+        for b in self.bufs:
+            self.loss += b.loss_part
         self.loss_f.copy_(self.loss)
         self.pack.all_reduce(self.pg)
 
