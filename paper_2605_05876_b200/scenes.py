@@ -103,6 +103,32 @@ def config0(seed=0, n=10_000):
     return _raw_cloud(p, p, ls, rng.uniform(0, 1, (n, 3)), rng.uniform(0.1, 0.9, n), rng.uniform(0, 1, n))
 
 
+def config1(seed=0, n=200_000, amp=0.05, octaves=3):
+    """200k surfels area-uniform on torus(R=1, r=0.35) U sphere(0.6), displaced
+    along the analytic normal by 3-octave value noise (BASELINE cfg 1)."""
+    rng = np.random.default_rng(seed)
+    R, r, rs = 1.0, 0.35, 0.6
+    a_t, a_s = 4.0 * np.pi ** 2 * R * r, 4.0 * np.pi * rs ** 2
+    nt = int(round(n * a_t / (a_t + a_s)))
+    # torus: area element (R + r cos v) du dv, rejection on v
+    vs = np.empty(0)
+    while len(vs) < nt:
+        v = rng.uniform(0, 2 * np.pi, 2 * nt)
+        keep = rng.uniform(0, R + r, 2 * nt) < R + r * np.cos(v)
+        vs = np.concatenate([vs, v[keep]])
+    v = vs[:nt]
+    u = rng.uniform(0, 2 * np.pi, nt)
+    nrm_t = np.stack([np.cos(v) * np.cos(u), np.cos(v) * np.sin(u), np.sin(v)], 1)
+    pts_t = np.stack([(R + r * np.cos(v)) * np.cos(u), (R + r * np.cos(v)) * np.sin(u), r * np.sin(v)], 1)
+    d = rng.normal(size=(n - nt, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    pts = np.concatenate([pts_t, rs * d])
+    nrm = np.concatenate([nrm_t, d])
+    pts = pts + (amp * _value_noise(pts, seed + 1, octaves))[:, None] * nrm
+    ls = rng.uniform(np.log(0.005), np.log(0.02), size=(n, 2))
+    return _raw_cloud(pts, nrm, ls, rng.uniform(0, 1, (n, 3)), rng.uniform(0.1, 0.9, n), rng.uniform(0, 1, n))
+
+
 def config2(seed=0, n=1_000_000, amp=0.08, octaves=3):
     """1M surfels on a noise-displaced unit icosphere (BASELINE cfg 2)."""
     rng = np.random.default_rng(seed)

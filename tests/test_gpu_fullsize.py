@@ -138,3 +138,35 @@ def test_config0_step_full_size():
         assert bad == 0, (k, err)
     bad, err = grad_close(ts.g_env_log, og["env_base_log"])
     assert bad == 0, err
+
+
+def test_config1_training_gradients_full_size():
+    """Config 1 (200k surfels on a displaced torus + sphere, 512x512, env
+    64x128): tile lists bit-exact, image within 1e-4, training gradients vs the
+    oracle."""
+    gt = scenes.config1(0, 200_000)
+    opt = scenes.perturb(gt, 1)
+    base_log = np.log(scenes.env_lognormal(64, 128, 3))
+    cam = ss.fibonacci_cameras(8, 3.5, 512, 512)[2]
+    env = ss.EnvironmentLight(base_log)
+    target = ss.render(ss.SurfelCloud(**gt), cam, ss.RenderOptions(), env=env).rgb.contiguous()
+    cloud = ss.SurfelCloud(**opt)
+    res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
+    oenv = _oracle_env(base_log)
+    co = SimpleNamespace(**opt)
+    ores = O.render(co, cam, env=oenv)
+    np.testing.assert_array_equal(host(res.pair_rec), ores.pair_rec)
+    np.testing.assert_array_equal(host(res.nlayers), ores.nlayers)
+    bad, err = image_close(res.rgb, ores.rgb)
+    assert bad == 0, err
+    ts = TrainStep(cloud, env, 512, 512)
+    ts.gradients([cam], [target])
+    rgb = host(res.rgb).astype(np.float64)
+    g = np.sign(rgb - host(target)) / rgb.size  # same L1 sign pattern on both sides
+    og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
+    for k in PARAMS:
+        bad, err = grad_close(ts.grads[k], og[k])
+        assert bad <= 1e-4 * og[k].size, (k, bad, err)
+    np.testing.assert_array_equal(host(ts.touched) > 0, og["touched"])
+    bad, err = grad_close(ts.g_env_log, og["env_base_log"])
+    assert bad == 0, err
