@@ -356,7 +356,7 @@ class TrainStep:
         self._run_views(cameras, lambda i, st: targets[i], masks=masks)
         self._finish()
 
-    def _finish(self):
+    def _env_adjoint(self):
         he, we = self.env.shape
         from .shading import diffuse_rowsums, env_workspace, spec_operator
         spec_operator(he, we, self.env.levels, self.env.spec_samples)
@@ -364,10 +364,32 @@ class TrainStep:
                                            _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(self.d_diffuse),
                                            _lib.ptr(self.d_spec), _lib.ptr(self.d_base), _lib.ptr(self.g_env_log),
                                            _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()), "ss_env_adjoint")
+
+    def _finish(self):
+        self._env_adjoint()
         for b in self.bufs:
             self.loss += b.loss_part
         self.loss_f.copy_(self.loss)
         self.pack.all_reduce(self.pg)
+
+    def fixed_costs(self):
+        """CUDA-event times (ms, current stream) of the per-step fixed stages,
+        each run once more on the current state (SURVEY §8d reports them beside
+        the per-view numbers): env adjoint, all-reduce, Adam (+ quaternion
+        renorm), env refresh.  Leaves the parameters one Adam step further."""
+        def timed(fn):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            return a.elapsed_time(b)
+        items = [(k, getattr(self.cloud, k), self.grads[k], self.lrs[k]) for k in PARAMS]
+        items.append(("env_base_log", self.env.base_log, self.g_env_log, self.lrs["env_base_log"]))
+        return {"env_adjoint": timed(self._env_adjoint),
+                "allreduce": timed(lambda: self.pack.all_reduce(self.pg)),
+                "adam": timed(lambda: self.adam.step_multi(items, renorm_quats="quats")),
+                "env_refresh": timed(self.env.refresh)}
 
     def apply(self, lr_scale=1.0):
         """Adam on all tensors, quaternion renorm, env refresh (train.py:241-248)."""
