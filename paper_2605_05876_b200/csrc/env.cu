@@ -160,9 +160,179 @@ __global__ void diffuse_finish_kernel(int he, int we, const double *__restrict__
     }
 }
 
+// ---- spectral form of the same quadrature ----------------------------------
+// Between lat-long texels, d_a . d_b = s_i s_j cos(phi_a - phi_b) + c_i c_j
+// (rows i, j; s = sin theta, c = cos theta) and phi_a - phi_b = 2 pi (c_a -
+// c_b) / we: the clamped-cosine kernel depends on the columns only through
+// (c_a - c_b) mod we.  Row pair by row pair the T x T product is therefore a
+// circular convolution along phi, K_ij(m) = max(s_i s_j cos(2 pi m / we) +
+// c_i c_j, 0), and along the DFT of each row
+//     y_i^(k) = sum_j K_ij^(k) v_j^(k).
+// K_ij is even in m, so K_ij^ is real; it depends on the grid only and is
+// built once per shape (float64, he^2 (we/2 + 1) values).  One application
+// costs O(he^2 we + he we^2) float64 operations instead of the O(he^2 we^2)
+// of the N-body form above (which remains for odd widths).
+
+struct DiffSpectrum {
+    int dev = -1, he = 0, we = 0;
+    double *khat = nullptr;
+};
+DiffSpectrum g_dspec;
+
+__device__ __forceinline__ void twiddles(int we, double *tc, double *ts) {
+    for (int m = threadIdx.x; m < we; m += blockDim.x) {
+        double sv, cv;
+        sincospi(2.0 * m / we, &sv, &cv);
+        tc[m] = cv;
+        ts[m] = sv;
+    }
+}
+
+// K^_ij(k) = sum_m K_ij(m) cos(2 pi k m / we); one CTA per (i, j), threads over k
+__global__ void __launch_bounds__(128) dspec_kernel(int he, int we, double *__restrict__ khat) {
+    extern __shared__ double dsm[];
+    double *tc = dsm, *ts = dsm + we, *kv = dsm + 2 * we;
+    const int i = blockIdx.x / he, j = blockIdx.x % he;
+    twiddles(we, tc, ts);
+    double si, ci, sj, cj;
+    sincospi((i + 0.5) / he, &si, &ci);
+    sincospi((j + 0.5) / he, &sj, &cj);
+    __syncthreads();
+    for (int m = threadIdx.x; m < we; m += blockDim.x) kv[m] = fmax(si * sj * tc[m] + ci * cj, 0.0);
+    __syncthreads();
+    const int nk = we / 2 + 1;
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+        double acc = 0.0;
+        int idx = 0;
+        for (int m = 0; m < we; ++m) {
+            acc += kv[m] * tc[idx];
+            idx += k;
+            if (idx >= we) idx -= we;
+        }
+        khat[((size_t)i * he + j) * nk + k] = acc;
+    }
+}
+
+// Row DFTs of the weighted input v (mode 0: v = om; 1: om x; 2: x / rowsum),
+// packed per (channel, row) as we doubles: re0, re_{we/2}, re1, im1, ...
+template <int MODE, typename TIn>
+__global__ void __launch_bounds__(256) drow_dft_kernel(int he, int we, const TIn *__restrict__ x,
+                                                       const float *__restrict__ rowsum, double *__restrict__ vhat) {
+    extern __shared__ double dsm[];
+    constexpr int NC = MODE == 0 ? 1 : 3;
+    double *tc = dsm, *ts = dsm + we, *sv = dsm + 2 * we;
+    const int r = blockIdx.x;
+    twiddles(we, tc, ts);
+    const double om = sinpi((r + 0.5) / he) * (SS_PI / he) * (2.0 * SS_PI / we);
+    for (int t = threadIdx.x; t < NC * we; t += blockDim.x) {
+        const int c = t / we, m = t % we, b = r * we + m;
+        double v;
+        if (MODE == 0) v = om;
+        else if (MODE == 1) v = om * (double)x[3 * b + c];
+        else v = (double)x[3 * b + c] / (double)rowsum[b];
+        sv[c * we + m] = v;
+    }
+    __syncthreads();
+    const int nk = we / 2 + 1;
+    for (int t = threadIdx.x; t < NC * nk; t += blockDim.x) {
+        const int c = t / nk, k = t % nk;
+        const double *v = sv + c * we;
+        double re = 0.0, im = 0.0;
+        int idx = 0;
+        for (int m = 0; m < we; ++m) {
+            re += v[m] * tc[idx];
+            im -= v[m] * ts[idx];
+            idx += k;
+            if (idx >= we) idx -= we;
+        }
+        double *o = vhat + ((size_t)c * he + r) * we;
+        if (k == 0) o[0] = re;
+        else if (k == we / 2) o[1] = re;
+        else { o[2 * k] = re; o[2 * k + 1] = im; }
+    }
+}
+
+// One CTA per output row i: spectrum y_i^ = sum_j K^_ij v_j^, inverse DFT,
+// then the mode's finish (0: rowsum; 1: out = y / rowsum; 2: out += om y).
+template <int MODE, typename TOut>
+__global__ void __launch_bounds__(256) dapply_kernel(int he, int we, const double *__restrict__ khat,
+                                                     const double *__restrict__ vhat, const float *__restrict__ rowsum,
+                                                     TOut *__restrict__ out) {
+    extern __shared__ double dsm[];
+    constexpr int NC = MODE == 0 ? 1 : 3;
+    const int nk = we / 2 + 1;
+    double *tc = dsm, *ts = dsm + we, *yre = dsm + 2 * we, *yim = yre + NC * nk;
+    const int i = blockIdx.x;
+    twiddles(we, tc, ts);
+    for (int t = threadIdx.x; t < NC * nk; t += blockDim.x) {
+        const int c = t / nk, k = t % nk;
+        const double *kh = khat + (size_t)i * he * nk + k;
+        const double *vb = vhat + (size_t)c * he * we;
+        double re = 0.0, im = 0.0;
+        for (int j = 0; j < he; ++j) {
+            const double kk = kh[(size_t)j * nk];
+            const double *v = vb + (size_t)j * we;
+            if (k == 0) re += kk * v[0];
+            else if (k == we / 2) re += kk * v[1];
+            else { re += kk * v[2 * k]; im += kk * v[2 * k + 1]; }
+        }
+        yre[c * nk + k] = re;
+        yim[c * nk + k] = im;
+    }
+    __syncthreads();
+    const double om = sinpi((i + 0.5) / he) * (SS_PI / he) * (2.0 * SS_PI / we);
+    for (int t = threadIdx.x; t < NC * we; t += blockDim.x) {
+        const int c = t / we, col = t % we;
+        const double *ar = yre + c * nk, *ai = yim + c * nk;
+        double y = ar[0] + ((col & 1) ? -ar[nk - 1] : ar[nk - 1]);
+        double h = 0.0;
+        int idx = col;
+        for (int k = 1; k < nk - 1; ++k) {
+            h += ar[k] * tc[idx] - ai[k] * ts[idx];
+            idx += col;
+            if (idx >= we) idx -= we;
+        }
+        y = (y + 2.0 * h) / we;
+        const int a = i * we + col;
+        if (MODE == 0) out[a] = (TOut)y;
+        else if (MODE == 1) out[3 * a + c] = (TOut)(y / (double)rowsum[a]);
+        else out[3 * a + c] += (TOut)(om * y);
+    }
+}
+
+const double *diffuse_spectrum(int he, int we, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_dspec.khat && g_dspec.dev == dev && g_dspec.he == he && g_dspec.we == we) return g_dspec.khat;
+    if (g_dspec.khat && g_dspec.dev == dev) cudaFree(g_dspec.khat);
+    double *k = nullptr;
+    const size_t n = (size_t)he * he * (we / 2 + 1);
+    if (cudaMalloc(&k, n * sizeof(double)) != cudaSuccess) return nullptr;
+    dspec_kernel<<<he * he, 128, 3 * we * sizeof(double), st>>>(he, we, k);
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaFree(k);
+        return nullptr;
+    }
+    g_dspec = DiffSpectrum{dev, he, we, k};
+    return k;
+}
+
 template <int MODE, typename TIn, typename TOut>
 int run_diffuse(int he, int we, const TIn *x, const float *rowsum, TOut *out, double *work, cudaStream_t st) {
     const int T = he * we;
+    // spectral form (even widths up to 1024: the row tables fit 48 KB of shared memory)
+    if ((we & 1) == 0 && we <= 1024) {
+        const double *khat = diffuse_spectrum(he, we, st);
+        if (!khat) return SS_ERR_CUDA;
+        const int nk = we / 2 + 1;
+        drow_dft_kernel<MODE, TIn><<<he, 256, (2 + (MODE == 0 ? 1 : 3)) * we * sizeof(double), st>>>(he, we, x, rowsum,
+                                                                                                      work);
+        SS_CUDA_CHECK_LAUNCH();
+        dapply_kernel<MODE, TOut><<<he, 256, (2 * we + 2 * (MODE == 0 ? 1 : 3) * nk) * sizeof(double), st>>>(
+            he, we, khat, work, rowsum, out);
+        SS_CUDA_CHECK_LAUNCH();
+        return SS_OK;
+    }
     cudaMemsetAsync(work, 0, sizeof(double) * 3 * T, st);
     const dim3 grid((T + kDiffThreads * kOut - 1) / (kDiffThreads * kOut), kSplit);
     diffuse_kernel<MODE, TIn><<<grid, kDiffThreads, 0, st>>>(he, we, x, rowsum, work);
