@@ -188,7 +188,8 @@ __device__ __forceinline__ void twiddles(int we, double *tc, double *ts) {
     }
 }
 
-// K^_ij(k) = sum_m K_ij(m) cos(2 pi k m / we); one CTA per (i, j), threads over k
+// K^_ij(k) = sum_m K_ij(m) cos(2 pi k m / we), stored [k][i][j]; one CTA per
+// (i, j), threads over k
 __global__ void __launch_bounds__(128) dspec_kernel(int he, int we, double *__restrict__ khat) {
     extern __shared__ double dsm[];
     double *tc = dsm, *ts = dsm + we, *kv = dsm + 2 * we;
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(128) dspec_kernel(int he, int we, double *__re
             idx += k;
             if (idx >= we) idx -= we;
         }
-        khat[((size_t)i * he + j) * nk + k] = acc;
+        khat[((size_t)k * he + i) * he + j] = acc;
     }
 }
 
@@ -252,51 +253,75 @@ __global__ void __launch_bounds__(256) drow_dft_kernel(int he, int we, const TIn
     }
 }
 
-// One CTA per output row i: spectrum y_i^ = sum_j K^_ij v_j^, inverse DFT,
-// then the mode's finish (0: rowsum; 1: out = y / rowsum; 2: out += om y).
+// One CTA per frequency k: y^_i(k) = sum_j K^_ij(k) v^_j(k) for every row i
+// and channel, written over v^(k) in place (no other CTA touches column k).
+template <int NC>
+__global__ void __launch_bounds__(128) dmul_kernel(int he, int we, const double *__restrict__ khat,
+                                                   double *__restrict__ vhat) {
+    extern __shared__ double dsm[];
+    double *vr = dsm, *vi = dsm + NC * he;  // [c][j]
+    const int k = blockIdx.x, nk = we / 2 + 1;
+    const bool real = k == 0 || k == nk - 1;
+    const int ore = k == 0 ? 0 : (k == nk - 1 ? 1 : 2 * k);
+    for (int t = threadIdx.x; t < NC * he; t += blockDim.x) {
+        const double *v = vhat + (size_t)t * we;  // t = c * he + j
+        vr[t] = v[ore];
+        vi[t] = real ? 0.0 : v[ore + 1];
+    }
+    __syncthreads();
+    const double *K = khat + (size_t)k * he * he;
+    for (int i = threadIdx.x; i < he; i += blockDim.x) {
+        double re[NC], im[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) re[c] = im[c] = 0.0;
+        const double *row = K + (size_t)i * he;
+        for (int j = 0; j < he; ++j) {
+            const double kk = __ldg(row + j);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                re[c] = fma(kk, vr[c * he + j], re[c]);
+                im[c] = fma(kk, vi[c * he + j], im[c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            double *o = vhat + ((size_t)c * he + i) * we;
+            o[ore] = re[c];
+            if (!real) o[ore + 1] = im[c];
+        }
+    }
+}
+
+// One CTA per output row i: inverse DFT of y^_i, then the mode's finish
+// (0: rowsum; 1: out = y / rowsum; 2: out += om y).
 template <int MODE, typename TOut>
-__global__ void __launch_bounds__(256) dapply_kernel(int he, int we, const double *__restrict__ khat,
-                                                     const double *__restrict__ vhat, const float *__restrict__ rowsum,
-                                                     TOut *__restrict__ out) {
+__global__ void __launch_bounds__(256) dinv_kernel(int he, int we, const double *__restrict__ yhat,
+                                                   const float *__restrict__ rowsum, TOut *__restrict__ out) {
     extern __shared__ double dsm[];
     constexpr int NC = MODE == 0 ? 1 : 3;
-    const int nk = we / 2 + 1;
-    double *tc = dsm, *ts = dsm + we, *yre = dsm + 2 * we, *yim = yre + NC * nk;
-    const int i = blockIdx.x;
+    double *tc = dsm, *ts = dsm + we, *sy = dsm + 2 * we;  // sy[c][we] packed spectrum
+    const int i = blockIdx.x, nk = we / 2 + 1;
     twiddles(we, tc, ts);
-    for (int t = threadIdx.x; t < NC * nk; t += blockDim.x) {
-        const int c = t / nk, k = t % nk;
-        const double *kh = khat + (size_t)i * he * nk + k;
-        const double *vb = vhat + (size_t)c * he * we;
-        double re = 0.0, im = 0.0;
-        for (int j = 0; j < he; ++j) {
-            const double kk = kh[(size_t)j * nk];
-            const double *v = vb + (size_t)j * we;
-            if (k == 0) re += kk * v[0];
-            else if (k == we / 2) re += kk * v[1];
-            else { re += kk * v[2 * k]; im += kk * v[2 * k + 1]; }
-        }
-        yre[c * nk + k] = re;
-        yim[c * nk + k] = im;
-    }
+    for (int t = threadIdx.x; t < NC * we; t += blockDim.x)
+        sy[t] = yhat[((size_t)(t / we) * he + i) * we + t % we];
     __syncthreads();
     const double om = sinpi((i + 0.5) / he) * (SS_PI / he) * (2.0 * SS_PI / we);
     for (int t = threadIdx.x; t < NC * we; t += blockDim.x) {
         const int c = t / we, col = t % we;
-        const double *ar = yre + c * nk, *ai = yim + c * nk;
-        double y = ar[0] + ((col & 1) ? -ar[nk - 1] : ar[nk - 1]);
+        const double *a = sy + c * we;
+        double y = a[0] + ((col & 1) ? -a[1] : a[1]);
         double h = 0.0;
         int idx = col;
         for (int k = 1; k < nk - 1; ++k) {
-            h += ar[k] * tc[idx] - ai[k] * ts[idx];
+            h += a[2 * k] * tc[idx] - a[2 * k + 1] * ts[idx];
             idx += col;
             if (idx >= we) idx -= we;
         }
         y = (y + 2.0 * h) / we;
-        const int a = i * we + col;
-        if (MODE == 0) out[a] = (TOut)y;
-        else if (MODE == 1) out[3 * a + c] = (TOut)(y / (double)rowsum[a]);
-        else out[3 * a + c] += (TOut)(om * y);
+        const int b = i * we + col;
+        if (MODE == 0) out[b] = (TOut)y;
+        else if (MODE == 1) out[3 * b + c] = (TOut)(y / (double)rowsum[b]);
+        else out[3 * b + c] += (TOut)(om * y);
     }
 }
 
@@ -321,15 +346,17 @@ template <int MODE, typename TIn, typename TOut>
 int run_diffuse(int he, int we, const TIn *x, const float *rowsum, TOut *out, double *work, cudaStream_t st) {
     const int T = he * we;
     // spectral form (even widths up to 1024: the row tables fit 48 KB of shared memory)
-    if ((we & 1) == 0 && we <= 1024) {
+    if ((we & 1) == 0 && we <= 1024 && he <= 1024) {
         const double *khat = diffuse_spectrum(he, we, st);
         if (!khat) return SS_ERR_CUDA;
         const int nk = we / 2 + 1;
         drow_dft_kernel<MODE, TIn><<<he, 256, (2 + (MODE == 0 ? 1 : 3)) * we * sizeof(double), st>>>(he, we, x, rowsum,
                                                                                                       work);
         SS_CUDA_CHECK_LAUNCH();
-        dapply_kernel<MODE, TOut><<<he, 256, (2 * we + 2 * (MODE == 0 ? 1 : 3) * nk) * sizeof(double), st>>>(
-            he, we, khat, work, rowsum, out);
+        constexpr int NC = MODE == 0 ? 1 : 3;
+        dmul_kernel<NC><<<nk, 128, 2 * NC * he * sizeof(double), st>>>(he, we, khat, work);
+        SS_CUDA_CHECK_LAUNCH();
+        dinv_kernel<MODE, TOut><<<he, 256, (2 + NC) * we * sizeof(double), st>>>(he, we, work, rowsum, out);
         SS_CUDA_CHECK_LAUNCH();
         return SS_OK;
     }
