@@ -9,14 +9,14 @@
 // covering record with interval start zs belongs to layer
 //     m = #{ j : thr_j < zs },   discarded when m >= k_max
 // (proof in DESIGN.md §kernels).  So the backward needs neither the walk nor
-// the tile lists: one WARP owns one record and its lanes sweep the record's
-// pixel rect (dense: ~85% lane utilisation for the typical 5x5-10x10 px
-// rects, vs ~28% for a pixel-parallel replay where most lanes of a warp block
-// lie outside the record).  Each lane re-evaluates coverage with the
-// forward's exact-decision fast path, reads its pixel's layer thresholds and
-// coefficients (L2-resident planes) and accumulates 17 gradient channels in
-// registers; one transposed warp reduction per record and plain stores (each
-// record is committed exactly once: no atomics, deterministic).
+// the tile lists: records are counting-sorted by rect area and an 8-lane
+// group owns one record (4 per warp, ~95% lane packing at the measured area
+// distribution, vs ~28% for a pixel-parallel replay where most lanes of a
+// warp block lie outside the record).  The lanes re-evaluate coverage with
+// the certified fast path (coverage.cuh), read their pixel's layer header
+// and coefficients (L2-resident planes) and accumulate 17 gradient channels
+// in registers; one 3-level transposed reduction per group and plain stores
+// (each record is committed exactly once: no atomics, deterministic).
 #include "ss_common.cuh"
 #include "raster_walk.cuh"
 #include "warp_reduce.cuh"
