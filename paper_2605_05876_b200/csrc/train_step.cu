@@ -69,9 +69,10 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const int4 h = __ldg(P.hdr + 2 * pix);
     const float4 cf0 = __ldg(P.coef + pix);
     // ray / tangent-plane quantities of the backward (rasterizer.py:197-207)
-    const float k0 = fs(fm(x, R.b.z), R.a.x), k1 = fs(fm(x, R.b.w), R.a.y);
-    const float l0 = fs(fm(y, R.b.z), R.a.w), l1 = fs(fm(y, R.b.w), R.b.x);
-    const float inv_den = fast_rcp(fs(fm(k0, l1), fm(k1, l0)));
+    // (gradient arithmetic: contracted FMAs, no reference rounding sequence)
+    const float k0 = fmaf(x, R.b.z, -R.a.x), k1 = fmaf(x, R.b.w, -R.a.y);
+    const float l0 = fmaf(y, R.b.z, -R.a.w), l1 = fmaf(y, R.b.w, -R.b.x);
+    const float inv_den = fast_rcp(fmaf(k0, l1, -k1 * l0));
     const float zs = R.d.z;
     const int nc = h.x & 0xff;  // closed layers (the layer count sits in bits 8+)
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
