@@ -279,8 +279,8 @@ __device__ __forceinline__ void walk_tile_packed(const WarpPix &w, int p0, int p
 // k, l, den and the two numerators are evaluated with the reference's exact
 // float32 operation sequence (no contraction), so they are bit-identical to
 // rasterizer.py:197-205 and the ray-miss test |den| < 1e-9 is exact.  The
-// quotient uses an IEEE reciprocal (u, v within 1 ulp of the reference's
-// division) and rho^2 is evaluated in float32; when the quadratic form is ill
+// quotient uses a Newton-refined hardware reciprocal (u, v within ~2 ulp of
+// the reference's division) and rho^2 is evaluated in float32; when the quadratic form is ill
 // conditioned (cancelling terms, |terms| > 32) or rho^2 lies within 2e-4 of
 // its term magnitude from the cut-off, the reference's exact u, v and numba's
 // float64 rho^2 decide (and are used).  Coverage and layer membership are
@@ -303,7 +303,7 @@ __device__ __forceinline__ bool ss_cover(float x, float y, const Rec &R, Cover &
     if (fabsf(c.den) <= 9.99999972e-10f) return false;  // == (double)|den| < 1e-9 exactly
     const float nu = fs(fm(c.k1, c.l2), fm(c.k2, c.l1));
     const float nv = fs(fm(c.k2, c.l0), fm(c.k0, c.l2));
-    c.inv_den = __frcp_rn(c.den);
+    c.inv_den = fc_rcp(c.den);  // hardware rcp + one Newton step (~1 ulp; no slow-path branch)
     c.u = nu * c.inv_den;
     c.v = nv * c.inv_den;
     const float s0 = R.c.y, s1 = R.c.z, s2 = R.c.w;
