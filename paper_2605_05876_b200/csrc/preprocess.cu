@@ -34,7 +34,7 @@ struct CamF {
 };
 
 #ifndef SS_PRE_MINB
-#define SS_PRE_MINB 3  // 85 registers, 3 CTAs per SM (small spill, better latency hiding)
+#define SS_PRE_MINB 3  // 80 registers, 3 CTAs per SM (small spill, better latency hiding)
 #endif
 __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
     SsCloud cloud, CamF cam, SsPreprocessOpts opt, int color_source, const float *__restrict__ colors_in,
