@@ -14,6 +14,9 @@ from paper_2605_05876_b200.step import TrainStep  # noqa: E402
 
 NV = int(os.environ.get("NVIEWS", "16"))
 gt = scenes.config2(0, 1_000_000)
+if os.environ.get("MORTON"):  # spatially coherent surfel order (study)
+    perm = scenes.morton_order(gt["centers"])
+    gt = {k: v[perm] for k, v in gt.items()}
 init = scenes.perturb(gt, 1)
 env_base = scenes.env_lognormal(128, 256, 2)
 cams = ss.fibonacci_cameras(64, 3.5, 800, 800)[:NV]
