@@ -31,7 +31,6 @@ struct SplatParams {
     const int8_t *cull;
     const SsRecord *records;
     const float *xs, *ys;   // pixel-centre NDC per column / row (exact: coverage decisions)
-    float sx, ox, sy, oy;   // x ~ ix * sx + ox, y ~ iy * sy + oy (within an ulp: gradient arithmetic)
     const float4 *coef;     // (k_max, HW) per-layer (A, dL/dC_raw)
     const float *thr;       // (k_max, HW) closing depths of layers >= 3
     const int4 *hdr;        // (HW, 2) (closed-layer count, closing depths of layers 0..2), (depths 3..6)
@@ -57,12 +56,9 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return r * (2.f - x * r);
 }
 
-__device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R, int ix, int iy, float u, float v,
-                                         float rho2, float g[NCH]) {
+__device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R, int ix, int iy, float x, float y,
+                                         float u, float v, float rho2, float g[NCH]) {
     const size_t HW = (size_t)P.W * P.H;
-    // the gradient only needs the pixel centre to float accuracy: one FMA
-    // each instead of the exact tables the coverage decision reads
-    const float x = fmaf((float)ix, P.sx, P.ox), y = fmaf((float)iy, P.sy, P.oy);
     const size_t pix = (size_t)iy * P.W + ix;
     // the packed header and the (most common) layer-0 coefficients are loaded
     // together, before the geometry below, so their latency hides behind it
@@ -364,7 +360,9 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
                     const int ixy = sm.ixy[grp][j];
                     // rho^2 with ss_cover's float32 expression (bit-identical on its fast path)
                     const float r2 = R.c.y * q.x * q.x + 2.f * R.c.z * q.x * q.y + R.c.w * q.y * q.y;
-                    touch += item_grad(P, R, ixy & 0xffff, ixy >> 16, q.x, q.y, r2, g);
+                    // pixel centres from the (shared-memory) tables: no int->float conversions
+                    const int ix = ixy & 0xffff, iy = ixy >> 16;
+                    touch += item_grad(P, R, ix, iy, xs[ix], ys[iy], q.x, q.y, r2, g);
                 }
             }
             __syncwarp();
@@ -397,7 +395,8 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
     int ixy;
     float4 q;
     if (!item_cover(P.xs, P.ys, R, f, k, rw, inv_rw, ixy, q)) return 0;
-    return item_grad(P, R, ixy & 0xffff, ixy >> 16, q.x, q.y, q.z, g);
+    const int ix = ixy & 0xffff, iy = ixy >> 16;
+    return item_grad(P, R, ix, iy, __ldg(P.xs + ix), __ldg(P.ys + iy), q.x, q.y, q.z, g);
 }
 
 // Big records (grazing splats whose filtered bound spans up to most of the
@@ -488,8 +487,6 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     P.cull = cull;
     P.records = reinterpret_cast<const SsRecord *>(records);
     P.xs = pixel_ndc; P.ys = pixel_ndc + width;
-    P.sx = (float)(2.0 / width); P.ox = (float)(1.0 / width - 1.0);
-    P.sy = (float)(-2.0 / height); P.oy = (float)(1.0 - 1.0 / height);
     P.coef = reinterpret_cast<const float4 *>(coef);
     P.thr = thr; P.hdr = reinterpret_cast<const int4 *>(pix_hdr); P.acc = rec_acc;
     area_class_kernel<<<148 * 4, 256, 0, st>>>(P, cls, big_list, counters, hist);
