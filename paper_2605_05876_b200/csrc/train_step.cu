@@ -113,13 +113,11 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     return 1;
 }
 
-// Coverage of rect pixel k (row-major) of record R (fast path with the
-// record's certified margin, exact reference arithmetic when undecided); on
-// a hit returns the pixel (ix | iy << 16) and u, v, rho^2.
-__device__ __forceinline__ bool item_cover(const float *xs, const float *ys, const SsRecord &R, const FastCov &f, int k,
-                                           int rw, float inv_rw, int &ixy, float4 &q) {
-    const int ky = (int)(((float)k + 0.5f) * inv_rw);
-    const int iy = R.r.y + ky, ix = R.r.x + (k - ky * rw);
+// Coverage of pixel (ix, iy) of record R (fast path with the record's
+// certified margin, exact reference arithmetic when undecided); on a hit
+// returns the pixel (ix | iy << 16) and u, v, rho^2.
+__device__ __forceinline__ bool item_cover(const float *xs, const float *ys, const SsRecord &R, const FastCov &f, int ix,
+                                           int iy, int &ixy, float4 &q) {
     const float x = xs[ix], y = ys[iy];
     float u, v, r2;
     const int d = fast_cover(f, R.c.y, R.c.z, R.c.w, x, y, u, v, r2);
@@ -324,8 +322,9 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
             rw = R.r.z - R.r.x;
             area = rect_area(R.r);
         }
-        // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
-        const float inv_rw = fast_rcp((float)rw);
+        // k / rw as (k * mrw) >> 20 with mrw = ceil(2^20 / rw): exact while
+        // k * rw < 2^20 (k < area <= kBigArea, rw <= kBigArea)
+        const unsigned mrw = ((1u << 20) + (unsigned)rw - 1u) / (unsigned)rw;
         FastCov f;
         fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
         float g[NCH];
@@ -341,7 +340,8 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
                 const int k = k0 + gl;
                 int ixy = 0;
                 float4 q;
-                const bool hit = k < area && item_cover(xs, ys, R, f, k, rw, inv_rw, ixy, q);
+                const int ky = (int)(((unsigned)k * mrw) >> 20);
+                const bool hit = k < area && item_cover(xs, ys, R, f, R.r.x + (k - ky * rw), R.r.y + ky, ixy, q);
                 const unsigned gm = (__ballot_sync(0xffffffffu, hit) >> (grp * kGL)) & 0xffu;
                 if (hit) {
                     const int slot = ncov + __popc(gm & glt);
@@ -394,7 +394,9 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
                                           float inv_rw, float g[NCH]) {
     int ixy;
     float4 q;
-    if (!item_cover(P.xs, P.ys, R, f, k, rw, inv_rw, ixy, q)) return 0;
+    // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
+    const int ky = (int)(((float)k + 0.5f) * inv_rw);
+    if (!item_cover(P.xs, P.ys, R, f, R.r.x + (k - ky * rw), R.r.y + ky, ixy, q)) return 0;
     const int ix = ixy & 0xffff, iy = ixy >> 16;
     return item_grad(P, R, ix, iy, __ldg(P.xs + ix), __ldg(P.ys + iy), q.x, q.y, q.z, g);
 }
