@@ -26,10 +26,18 @@ constexpr int kHeavyThreads = 1024;
 constexpr int kHeavyCap = 12288;
 
 
+__device__ void tile_order(const int32_t *__restrict__ counts, int ntiles, int32_t *__restrict__ order);
+
+// CTA 0: exclusive scan of the tile counts into the offsets; CTA 1 (when an
+// order is requested): the heavy-first launch order of the tiles.
 __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
     const int32_t *__restrict__ counts, int ntiles, int32_t *__restrict__ offsets,
-    int32_t *__restrict__ cursors, int64_t capacity, int32_t *__restrict__ flags)
+    int32_t *__restrict__ cursors, int64_t capacity, int32_t *__restrict__ flags, int32_t *__restrict__ order)
 {
+    if (blockIdx.x == 1) {
+        tile_order(counts, ntiles, order);
+        return;
+    }
     __shared__ int32_t warp_sums[kScanThreads / 32];
     __shared__ int32_t carry;
     if (threadIdx.x == 0) carry = 0;
@@ -74,8 +82,7 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
 // Launch order for the rasterisers: tiles grouped by descending log2 of
 // their pair count (heavy tiles first, so the last wave is made of light
 // ones); the order within a group is irrelevant to the results.
-__global__ void __launch_bounds__(1024) tile_order_kernel(const int32_t *__restrict__ counts, int ntiles,
-                                                         int32_t *__restrict__ order)
+__device__ void tile_order(const int32_t *__restrict__ counts, int ntiles, int32_t *__restrict__ order)
 {
     __shared__ int32_t hist[33], base[33];
     if (threadIdx.x < 33) hist[threadIdx.x] = 0;
@@ -295,12 +302,9 @@ extern "C" int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, i
     cudaStream_t st = (cudaStream_t)stream;
     const int ntx = (width + tile - 1) / tile, nty = (height + tile - 1) / tile;
     const int ntiles = ntx * nty;
-    tile_scan_kernel<<<1, kScanThreads, 0, st>>>(tile_counts, ntiles, tile_offsets, cursors, pair_capacity, flags);
+    tile_scan_kernel<<<tile_order ? 2 : 1, kScanThreads, 0, st>>>(tile_counts, ntiles, tile_offsets, cursors,
+                                                                  pair_capacity, flags, tile_order);
     SS_CUDA_CHECK_LAUNCH();
-    if (tile_order) {
-        tile_order_kernel<<<1, 1024, 0, st>>>(tile_counts, ntiles, tile_order);
-        SS_CUDA_CHECK_LAUNCH();
-    }
     if (n > 0) {
         const size_t smem = 2 * (size_t)ntiles * sizeof(int32_t);
         if (smem > 220 * 1024) return SS_ERR_INVALID;  // > 28k tiles: not supported by the privatised scatter

@@ -182,9 +182,9 @@ class TrainStep:
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
         self.active_streams = None     # None: all worker streams; 1: views serialised (isolated kernel timing)
         self._stage = None
-        # preprocess, scan, order, scatter, tile sort x2, train fwd, ndc, area class, class scatter,
+        # preprocess, scan + order, scatter, tile sort x2, train fwd, ndc, area class, class scatter,
         # record bwd, big-rect bwd, chain, env merge x2
-        self.launches_per_view = 15
+        self.launches_per_view = 14
         self.launches_per_step_fixed = 4 + 1 + 4  # env adjoint, fused Adam (+ quat renorm), env refresh
 
     # -- buffers -----------------------------------------------------------
