@@ -53,10 +53,18 @@ __device__ __forceinline__ SsBil<R> ss_bil_prepare(int h, int w, R fu, R fv, boo
     if (wrap) {
         R i0f = floor(fu);
         b.tu = fu - i0f;
-        long long ii = (long long)i0f % w;
+        // fu = (phi + pi) w / (2 pi) - 1/2 lies in [-1/2, w - 1/2]: one
+        // conditional wrap instead of a 64-bit modulo (the modulo stays for
+        // anything outside (-w, 2w))
+        long long ii = (long long)i0f;
         if (ii < 0) ii += w;
+        else if (ii >= w) ii -= w;
+        if (ii < 0 || ii >= w) {
+            ii = (long long)i0f % w;
+            if (ii < 0) ii += w;
+        }
         b.i0 = (int)ii;
-        b.i1 = (b.i0 + 1) % w;
+        b.i1 = b.i0 + 1 == w ? 0 : b.i0 + 1;
         b.du_ok = true;
     } else {
         R fuc = ss_clip<R>(fu, R(0.0), w - R(1.0));
