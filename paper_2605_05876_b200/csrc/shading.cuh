@@ -125,6 +125,26 @@ __device__ __forceinline__ void ss_bil_grads(const float *__restrict__ tex, int 
     }
 }
 
+// float atan2 with ~3e-7 rad error (range reduction to |t| <= tan(pi/8) and
+// the classic 4-term minimax polynomial for atan(t)/t), IEEE signed-zero
+// quadrants; finite inputs only (shading directions).  About a sixth of
+// atan2f's instruction count.
+__device__ __forceinline__ float ss_atan2f(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float a = mx > 0.f ? __fdividef(mn, mx) : 0.f;  // [0, 1]
+    const bool big = a > 0.41421356237f;
+    const float t = big ? __fdividef(a - 1.f, a + 1.f) : a;  // |t| <= tan(pi/8)
+    const float z = t * t;
+    const float p = fmaf(fmaf(fmaf(8.05374449538e-2f, z, -1.38776856032e-1f), z, 1.99777106478e-1f), z,
+                         -3.33329491539e-1f);
+    float r = fmaf(p * z, t, t);
+    if (big) r += 0.785398163397448310f;
+    if (ay > ax) r = 1.57079632679489662f - r;
+    if (signbit(x)) r = 3.14159265358979324f - r;
+    return copysignf(r, y);
+}
+
 // dirs_to_coords (shading.py:172-179)
 template <typename R>
 __device__ __forceinline__ void ss_dir_coords(const R d[3], int he, int we, R &fu, R &fv) {
@@ -132,9 +152,11 @@ __device__ __forceinline__ void ss_dir_coords(const R d[3], int he, int we, R &f
     // angle for a unit d but well conditioned at the poles, where acos would
     // amplify the float32 rounding of d_z
     R th;
-    if constexpr (sizeof(R) == 4) th = atan2f(sqrtf(d[0] * d[0] + d[1] * d[1]), d[2]);
+    if constexpr (sizeof(R) == 4) th = ss_atan2f(sqrtf(d[0] * d[0] + d[1] * d[1]), d[2]);
     else th = acos(ss_clip<R>(d[2], -R(1.0), R(1.0)));
-    R ph = atan2(d[1], d[0]);
+    R ph;
+    if constexpr (sizeof(R) == 4) ph = ss_atan2f(d[1], d[0]);
+    else ph = atan2(d[1], d[0]);
     fu = (ph + R(SS_PI)) * ((R)we / (R(2) * R(SS_PI))) - R(0.5);
     fv = th * ((R)he / R(SS_PI)) - R(0.5);
 }
