@@ -346,7 +346,8 @@ template <int MODE, typename TIn, typename TOut>
 int run_diffuse(int he, int we, const TIn *x, const float *rowsum, TOut *out, double *work, cudaStream_t st) {
     const int T = he * we;
     // spectral form (even widths up to 1024: the row tables fit 48 KB of shared memory)
-    if ((we & 1) == 0 && we <= 1024 && he <= 1024) {
+    // (and K^ of at most 512 MB: 256 x 512 needs 135 MB, larger maps take the N-body form)
+    if ((we & 1) == 0 && we <= 1024 && he <= 1024 && (double)he * he * (we / 2 + 1) * 8.0 <= 512.0 * (1 << 20)) {
         const double *khat = diffuse_spectrum(he, we, st);
         if (!khat) return SS_ERR_CUDA;
         const int nk = we / 2 + 1;

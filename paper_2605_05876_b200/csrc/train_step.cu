@@ -144,7 +144,10 @@ constexpr int kBigArea = 512;  // rects above this go to the CTA-chunked kernel 
 constexpr int kNB = 64;        // area classes of the other records
 constexpr int kGL = 8;         // lanes per record group (4 records per warp)
 constexpr int kGCap = 128;     // rect pixels compacted per group pass
-constexpr int kSplatWarps = 8;
+#ifndef SS_SPLAT_WARPS
+#define SS_SPLAT_WARPS 8
+#endif
+constexpr int kSplatWarps = SS_SPLAT_WARPS;
 constexpr int kNdcSmem = 4096;  // W + H up to this: pixel-centre tables staged in shared memory
 #ifndef SS_SPLAT_MINB
 #define SS_SPLAT_MINB 3  // resident CTAs per SM the register budget is sized for
