@@ -189,3 +189,28 @@ def test_tile8_forward_matches_tile16():
     bad, err = image_close(res8.rgb, res16.rgb, rel=1e-6, abs_=1e-7)
     assert bad == 0, err
     assert torch.equal(res8.nlayers, res16.nlayers)
+
+
+@pytest.mark.parametrize("shape", [(8, 16), (12, 24), (9, 15), (64, 128)])
+def test_diffuse_quadrature_spectral_and_nbody(shape):
+    """The diffuse quadrature (spectral form for even widths, N-body form for
+    odd ones) against the dense row-normalised clamped-cosine operator of
+    shading.py:275-283 built in float64 here: refresh and its adjoint."""
+    he, we = shape
+    rng = np.random.default_rng(he * we)
+    base_log = rng.normal(0.0, 1.0, (he, we, 3))
+    env = ss.EnvironmentLight(base_log, levels=1)
+    th = (np.arange(he) + 0.5) * (np.pi / he)
+    ph = (np.arange(we) + 0.5) * (2.0 * np.pi / we) - np.pi
+    tt, pp = np.meshgrid(th, ph, indexing="ij")
+    dirs = np.stack([np.sin(tt) * np.cos(pp), np.sin(tt) * np.sin(pp), np.cos(tt)], -1).reshape(-1, 3)
+    solid = (np.sin(tt) * (np.pi / he) * (2.0 * np.pi / we)).reshape(-1)
+    D = np.maximum(dirs @ dirs.T, 0.0) * solid[None, :]
+    D /= D.sum(axis=1, keepdims=True)
+    base = host(env.base).astype(np.float64).reshape(-1, 3)
+    bad, err = image_close(env.diffuse, (D @ base).reshape(he, we, 3), rel=1e-5, abs_=1e-7)
+    assert bad == 0, err
+    g = rng.normal(0.0, 1.0, (he, we, 3))
+    db, _ = env.env_gradient(g, np.zeros((1, he, we, 3)))
+    ref = (D.T @ g.reshape(-1, 3)).reshape(he, we, 3)
+    assert grad_close(db, ref, rel=1e-5, floor=1e-6)[0] == 0  # outputs of mixed-sign sums: array-scaled floor
