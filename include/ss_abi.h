@@ -189,6 +189,25 @@ int ss_train_forward(int width, int height, int tile, const int32_t *tile_offset
  * closed layers | layer count << 8. */
 int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef, const float *g_rgb,
                    const float *g_alpha, const float *background, void *stream);
+/* The same three steps with the consolidation penalty (backward.py:160-320
+ * with cons_scale > 0): ss_train_forward_zstats is the deferred forward that
+ * also writes, per pixel and layer, the depth moments (z0, sum w dz,
+ * sum w dz^2, 0), dz = view_z - z0 of the layer's first covering member,
+ * into `zstats` (k_max*H*W float4); ss_train_coefs_cons turns coef and zstats
+ * in place into the layer coefficients and the penalty's per-layer
+ * (B, Q, z_bar, var) and adds the penalty value into cons_loss (1 double);
+ * ss_train_backward_records_cons adds the penalty's weight and depth terms
+ * (accumulator slot 16 = dL/dview_z). */
+int ss_train_forward_zstats(int width, int height, int tile, const int32_t *tile_offsets,
+                            const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
+                            const float *background, int k_max, float *coef, float *thr, int32_t *pix_hdr,
+                            float *rgb, float *alpha, const int32_t *tile_order, float *zstats, void *stream);
+int ss_train_coefs_cons(int width, int height, int k_max, const int32_t *pix_hdr, float *coef, float *zstats,
+                        const float *g_rgb, const float *g_alpha, const float *background, double cons_scale,
+                        double *cons_loss, void *stream);
+int ss_train_backward_records_cons(int n, const int8_t *cull, const float *records, int width, int height,
+                                   int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
+                                   const float *zcoef, float *pixel_ndc, float *rec_acc, void *stream);
 size_t ss_train_backward_scratch_words(int n, int width, int height);
 int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
                               int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,

@@ -94,6 +94,12 @@ _SIGNATURES = {
     "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
                          ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_train_coefs": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), c_p],
+    "ss_train_forward_zstats": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, ctypes.c_int,
+                                c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_train_coefs_cons": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_double,
+                            c_p, c_p],
+    "ss_train_backward_records_cons": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
+                                       c_p, c_p, c_p, c_p],
     "ss_train_backward_scratch_words": [ctypes.c_int, ctypes.c_int, ctypes.c_int],
     "ss_train_backward_records": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
                                   c_p, c_p, c_p],

@@ -55,12 +55,14 @@ def grads_struct(g, d_diffuse=None, d_specular=None, d_diffuse4=None, d_specular
                         _lib.ptr(d_diffuse), _lib.ptr(d_specular), _lib.ptr(d_diffuse4), _lib.ptr(d_specular4))
 
 
-def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp):
-    """The walk-free backward of the training step for an API render
-    (cons_scale = 0): the deferred-loss forward re-derives the per-pixel layer
-    sums and closing depths, ss_train_coefs turns them into the layer
-    coefficients for (g_rgb, g_alpha), and the record-parallel kernel fills
-    the per-record accumulator."""
+def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp, cons_scale=0.0, cons=None):
+    """The walk-free backward of the training step for an API render: the
+    deferred-loss forward re-derives the per-pixel layer sums and closing
+    depths, ss_train_coefs turns them into the layer coefficients for (g_rgb,
+    g_alpha), and the record-parallel kernel fills the per-record accumulator
+    (DESIGN.md §4).  With cons_scale > 0 the forward also parks the layer
+    depth moments, ss_train_coefs_cons adds the consolidation penalty
+    (value into `cons`) and the record kernels its depth / weight terms."""
     st, opt, cam = result.state, result.options, result.camera
     dev = st.records.device
     H, W, K = int(cam.height), int(cam.width), int(opt.k_max)
@@ -69,20 +71,39 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp):
     thr = torch.empty((K, H * W), **f32)
     hdr = torch.empty((H * W, 8), device=dev, dtype=torch.int32)
     rgb = torch.empty((H, W, 3), **f32)
+    n = st.records.shape[0]
+    scratch = torch.empty(lib.ss_train_backward_scratch_words(n, W, H), **f32)
+    if float(cons_scale) > 0.0:
+        zst = torch.empty((K, H * W, 4), **f32)
+        _lib.check(lib.ss_train_forward_zstats(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32),
+                                               _lib.ptr(result.pair_src), _lib.ptr(st.pair_rect), _lib.ptr(st.records),
+                                               bgp, K, _lib.ptr(coef), _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(rgb), None,
+                                               None, _lib.ptr(zst), _lib.stream_ptr()), "ss_train_forward_zstats")
+        _lib.check(lib.ss_train_coefs_cons(W, H, K, _lib.ptr(hdr), _lib.ptr(coef), _lib.ptr(zst), _lib.ptr(g_rgb),
+                                           _lib.ptr(g_alpha), bgp, float(cons_scale), _lib.ptr(cons),
+                                           _lib.stream_ptr()), "ss_train_coefs_cons")
+        _lib.check(lib.ss_train_backward_records_cons(n, _lib.ptr(st.cull), _lib.ptr(st.records), W, H, K,
+                                                      _lib.ptr(coef), _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(zst),
+                                                      _lib.ptr(scratch), _lib.ptr(acc), _lib.stream_ptr()),
+                   "ss_train_backward_records_cons")
+        return
     _lib.check(lib.ss_train_forward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
                                     _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, K, None, _lib.ptr(coef),
                                     _lib.ptr(thr), _lib.ptr(hdr), None, _lib.ptr(rgb), None, None, _lib.stream_ptr()),
                "ss_train_forward")
     _lib.check(lib.ss_train_coefs(W, H, K, _lib.ptr(hdr), _lib.ptr(coef), _lib.ptr(g_rgb), _lib.ptr(g_alpha), bgp,
                                   _lib.stream_ptr()), "ss_train_coefs")
-    n = st.records.shape[0]
-    scratch = torch.empty(lib.ss_train_backward_scratch_words(n, W, H), **f32)
     _lib.check(lib.ss_train_backward_records(n, _lib.ptr(st.cull), _lib.ptr(st.records), W, H, K, _lib.ptr(coef),
                                              _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(scratch), _lib.ptr(acc),
                                              _lib.stream_ptr()), "ss_train_backward_records")
 
 
-def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0) -> BackwardResult:
+def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0, path="records") -> BackwardResult:
+    """backward.py:324-470.  path: "records" (default) -- the walk-free
+    record-parallel kernels of the training step; "walk" -- the replaying
+    tile backward (ss_raster_backward, the reference's own two-pass order)."""
+    if path not in ("records", "walk"):
+        raise ValueError("path must be 'records' or 'walk'")
     opt = result.options
     if opt.depth_mode != "interval":
         raise ValueError("backward requires depth_mode='interval'")
@@ -100,11 +121,11 @@ def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0) -> B
     acc = torch.zeros((n, _lib.ACC_FLOATS), device=dev, dtype=torch.float32)
     cons = torch.zeros(1, device=dev, dtype=torch.float64)
     bgp, _keep = _lib.fvec(opt.background)
-    if float(cons_scale) == 0.0:
-        _record_backward(lib, result, g_rgb, ga, acc, bgp)
+    if not float(cons_scale) >= 0.0:
+        raise ValueError("cons_scale must be >= 0")
+    if path == "records":
+        _record_backward(lib, result, g_rgb, ga, acc, bgp, cons_scale, cons)
     else:
-        # the consolidation penalty needs the per-pixel layer depths of the
-        # replaying tile backward
         rc = lib.ss_raster_backward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
                                     _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, int(opt.k_max), _lib.ptr(g_rgb),
                                     _lib.ptr(ga), float(cons_scale), _lib.ptr(acc), _lib.ptr(cons), _lib.stream_ptr())

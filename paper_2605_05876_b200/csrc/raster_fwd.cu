@@ -46,6 +46,7 @@ struct FwdParams {
     float *thr;            // (k_max, H*W) depth at which layer j >= 3 closed
     int4 *hdr;             // (H*W, 2) packed (closed-layer count, closing depths of layers 0..2), (depths 3..6)
     double *loss;          // sum of |rgb - target| (1 double)
+    float4 *zst;           // kCons: (k_max, H*W) per layer (z0, sum w dz, sum w dz^2, 0), dz = view_z - z0
 };
 
 // CTAs of kFwdWarps warps (a tile is split over tile*tile/32/kFwdWarps
@@ -56,7 +57,10 @@ struct FwdParams {
 #endif
 constexpr int kFwdWarps = SS_FWD_WARPS;
 
-template <bool kExtras, bool kTrain>
+// kCons (deferred training mode only): also the per-layer depth moments the
+// consolidation penalty needs, relative to the layer's first covering member
+// like the reference's pass 1 (raster_bwd.cu), parked in P.zst per layer.
+template <bool kExtras, bool kTrain, bool kCons = false>
 __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 {
     __shared__ PackedScratch scratch[kFwdWarps];
@@ -81,6 +85,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     float lw[KL], lc0[KL], lc1[KL], lc2[KL];
     int ncl = 0;
     float th0 = 0.f, th1 = 0.f, th2 = 0.f;  // first three closing depths (kTrain)
+    float z0 = 0.f, Zs = 0.f, Z2s = 0.f;     // kCons: layer depth moments about the first member
 
     // one layer of the over-compositing (rasterizer.py:168-181)
     auto composite = [&](float w, float c0, float c1, float c2) {
@@ -102,6 +107,10 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
             P.st.z[o] = Zg; P.st.z2[o] = Z2g; P.st.n[o] = members;
         }
         if (kTrain) { lw[layers] = Wg; lc0[layers] = C0; lc1[layers] = C1; lc2[layers] = C2; }
+        if (kCons) {
+            P.zst[(size_t)layers * P.W * P.H + pix] = make_float4(z0, Zs, Z2s, 0.f);
+            Zs = Z2s = 0.f;
+        }
         ++layers;
         Wg = C0 = C1 = C2 = Zg = Z2g = zmax = 0.f;
         members = 0;
@@ -140,6 +149,12 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
             }
             if (v.w >= 0.f) {
                 const float w = v.w;
+                if (kCons) {
+                    if (Wg == 0.f) z0 = v.vz;
+                    const float dz = v.vz - z0;
+                    Zs += w * dz;
+                    Z2s += w * dz * dz;
+                }
                 Wg += w;
                 C0 += w * v.c0; C1 += w * v.c1; C2 += w * v.c2;
                 if (!kTrain) { Zg += w * v.vz; Z2g += w * v.vz * v.vz; }
@@ -260,11 +275,94 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, const int4 *__r
     }
 }
 
-template <bool kExtras, bool kTrain>
+// train_coef_kernel plus the consolidation penalty (backward.py:160-238 with
+// cons_scale > 0, the float64 pixel pass of raster_bwd.cu): from the layer
+// depth moments in zst it adds the penalty's weight term to A and rewrites
+// zst in place as the per-layer (B, Q, z_bar, var) of the record gradient
+//     g_w += B dz + Q (dz^2 - var),  g_vz = w (B + 2 Q dz),  dz = view_z - z_bar;
+// the penalty value is block-reduced into cons_loss.
+__global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, const int4 *__restrict__ hdr, float4 *coef,
+                                                              float4 *zst, const float *__restrict__ g_rgb,
+                                                              const float *__restrict__ g_alpha, float bg0,
+                                                              float bg1, float bg2, double s, double *cons_loss)
+{
+    __shared__ double red[8];
+    const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+    double cons_pix = 0.0;
+    const int layers = pix < HW ? hdr[2 * pix].x >> 8 : 0;
+    if (layers > 0) {
+        double a[SS_KMAX_CAP], tb[SS_KMAX_CAP], zb[SS_KMAX_CAP], vr[SS_KMAX_CAP];
+        double gw_c[SS_KMAX_CAP], gz_c[SS_KMAX_CAP], gv_c[SS_KMAX_CAP], wm[SS_KMAX_CAP];
+        float4 raw[SS_KMAX_CAP];
+        double tr = 1.0;
+        for (int m = 0; m < layers; ++m) {
+            raw[m] = coef[(size_t)m * HW + pix];
+            const float4 z = zst[(size_t)m * HW + pix];
+            a[m] = -expm1(-(double)raw[m].x);
+            tb[m] = tr;
+            tr *= 1.0 - a[m];
+            const double inv = 1.0 / (double)raw[m].x;
+            const double mz = (double)z.y * inv;
+            zb[m] = (double)z.x + mz;
+            vr[m] = (double)z.z * inv - mz * mz;
+            wm[m] = tb[m] * a[m];
+            gv_c[m] = vr[m] > 0.0 ? s * wm[m] * wm[m] : 0.0;
+            gw_c[m] = gz_c[m] = 0.0;
+        }
+        double l_pix = 0.0;
+        for (int i = 0; i < layers; ++i) {
+            const double var = vr[i] > 0.0 ? vr[i] : 0.0;
+            l_pix += wm[i] * wm[i] * var;
+            gw_c[i] += s * 2.0 * wm[i] * var;
+            for (int j = i + 1; j < layers; ++j) {
+                const double dz = zb[i] - zb[j];
+                const double adz = fabs(dz);
+                l_pix += wm[i] * wm[j] * adz;
+                gw_c[i] += s * wm[j] * adz;
+                gw_c[j] += s * wm[i] * adz;
+                const double sgn = dz > 0.0 ? 1.0 : (dz < 0.0 ? -1.0 : 0.0);
+                gz_c[i] += s * wm[i] * wm[j] * sgn;
+                gz_c[j] -= s * wm[i] * wm[j] * sgn;
+            }
+        }
+        cons_pix = s * l_pix;
+        const double gc0 = g_rgb[3 * (size_t)pix], gc1 = g_rgb[3 * (size_t)pix + 1], gc2 = g_rgb[3 * (size_t)pix + 2];
+        const double ga = g_alpha ? (double)g_alpha[pix] : 0.0;
+        double sf0 = bg0, sf1 = bg1, sf2 = bg2, q = 1.0, rw = 0.0;
+        for (int m = layers - 1; m >= 0; --m) {
+            const double inv = 1.0 / (double)raw[m].x;
+            const double ch0 = raw[m].y * inv, ch1 = raw[m].z * inv, ch2 = raw[m].w * inv;
+            const double g_am =
+                tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2) + ga * q + gw_c[m] - rw);
+            const double ta = tb[m] * a[m];
+            const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
+            coef[(size_t)m * HW + pix] = make_float4((float)(g_am * (1.0 - a[m]) - (gh0 * ch0 + gh1 * ch1 + gh2 * ch2) * inv),
+                                                     (float)(gh0 * inv), (float)(gh1 * inv), (float)(gh2 * inv));
+            zst[(size_t)m * HW + pix] = make_float4((float)(gz_c[m] * inv), (float)(gv_c[m] * inv), (float)zb[m],
+                                                    (float)vr[m]);
+            sf0 = a[m] * ch0 + (1.0 - a[m]) * sf0;
+            sf1 = a[m] * ch1 + (1.0 - a[m]) * sf1;
+            sf2 = a[m] * ch2 + (1.0 - a[m]) * sf2;
+            q *= 1.0 - a[m];
+            rw = gw_c[m] * a[m] + (1.0 - a[m]) * rw;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cons_pix += __shfl_xor_sync(0xffffffffu, cons_pix, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cons_pix;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+        if (t != 0.0) atomicAdd(cons_loss, t);
+    }
+}
+
+template <bool kExtras, bool kTrain, bool kCons = false>
 void launch(const FwdParams &P, int ntiles, int threads, cudaStream_t st) {
     const int wpc = threads / 32 < kFwdWarps ? threads / 32 : kFwdWarps;  // tile 8: 2 warps
     const int ctas_per_tile = threads / (32 * wpc);
-    raster_fwd_kernel<kExtras, kTrain><<<ntiles * ctas_per_tile, 32 * wpc, 0, st>>>(P);
+    raster_fwd_kernel<kExtras, kTrain, kCons><<<ntiles * ctas_per_tile, 32 * wpc, 0, st>>>(P);
 }
 
 bool fill_common(FwdParams &P, int width, int height, int tile, const int32_t *tile_offsets,
@@ -305,10 +403,10 @@ extern "C" int ss_raster_forward(int width, int height, int tile, const int32_t 
     return SS_OK;
 }
 
-extern "C" int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
-                                const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
-                                int k_max, const float *target, float *coef, float *thr, int32_t *pix_hdr,
-                                double *loss_sum, float *rgb, float *alpha, const int32_t *tile_order, void *stream)
+static int train_forward(int width, int height, int tile, const int32_t *tile_offsets, const int32_t *pair_rec,
+                         const uint32_t *pair_rect, const float *records, const float *background, int k_max,
+                         const float *target, float *coef, float *thr, int32_t *pix_hdr, double *loss_sum, float *rgb,
+                         float *alpha, const int32_t *tile_order, float *zstats, void *stream)
 {
     FwdParams P;
     if (!fill_common(P, width, height, tile, tile_offsets, pair_rec, pair_rect, records, background, k_max)) return SS_ERR_INVALID;
@@ -323,10 +421,31 @@ extern "C" int ss_train_forward(int width, int height, int tile, const int32_t *
     P.coef = reinterpret_cast<float4 *>(coef);
     P.loss = loss_sum;
     P.rgb = rgb;
+    P.zst = reinterpret_cast<float4 *>(zstats);
     const int ntiles = P.ntx * ((height + tile - 1) / tile);
-    launch<false, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
+    if (zstats) launch<false, true, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
+    else launch<false, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
+}
+
+extern "C" int ss_train_forward(int width, int height, int tile, const int32_t *tile_offsets,
+                                const int32_t *pair_rec, const uint32_t *pair_rect, const float *records, const float *background,
+                                int k_max, const float *target, float *coef, float *thr, int32_t *pix_hdr,
+                                double *loss_sum, float *rgb, float *alpha, const int32_t *tile_order, void *stream)
+{
+    return train_forward(width, height, tile, tile_offsets, pair_rec, pair_rect, records, background, k_max, target,
+                         coef, thr, pix_hdr, loss_sum, rgb, alpha, tile_order, nullptr, stream);
+}
+
+extern "C" int ss_train_forward_zstats(int width, int height, int tile, const int32_t *tile_offsets,
+                                       const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
+                                       const float *background, int k_max, float *coef, float *thr, int32_t *pix_hdr,
+                                       float *rgb, float *alpha, const int32_t *tile_order, float *zstats, void *stream)
+{
+    if (!zstats) return SS_ERR_INVALID;
+    return train_forward(width, height, tile, tile_offsets, pair_rec, pair_rect, records, background, k_max, nullptr,
+                         coef, thr, pix_hdr, nullptr, rgb, alpha, tile_order, zstats, stream);
 }
 
 extern "C" int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef,
@@ -338,6 +457,22 @@ extern "C" int ss_train_coefs(int width, int height, int k_max, const int32_t *p
     train_coef_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
         HW, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef), g_rgb, g_alpha, background[0],
         background[1], background[2]);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_train_coefs_cons(int width, int height, int k_max, const int32_t *pix_hdr, float *coef,
+                                   float *zstats, const float *g_rgb, const float *g_alpha, const float *background,
+                                   double cons_scale, double *cons_loss, void *stream)
+{
+    if (width <= 0 || height <= 0 || k_max < 1 || k_max > SS_KMAX_CAP || !pix_hdr || !coef || !zstats || !g_rgb ||
+        !background || !cons_loss || !(cons_scale >= 0.0))
+        return SS_ERR_INVALID;
+    const int HW = width * height;
+    train_coef_cons_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        HW, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef),
+        reinterpret_cast<float4 *>(zstats), g_rgb, g_alpha, background[0], background[1], background[2], cons_scale,
+        cons_loss);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

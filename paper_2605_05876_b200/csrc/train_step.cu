@@ -25,6 +25,10 @@ namespace {
 
 constexpr int KS = 4;   // layers per pixel staged in shared memory (rest read from global)
 constexpr int NCH = 17; // t1(3) t2(3) t4(3) Sigma^-1(3) n_f colour(3) screen-space |g|
+constexpr int NCHC = 18; // + d/d view_z (consolidation)
+template <bool kCons> __host__ __device__ constexpr int nch() { return kCons ? NCHC : NCH; }
+// reduced channel -> accumulator slot (slot 16 = dview_z, 17 = ss sum)
+__device__ __forceinline__ int acc_slot(int c) { return c < 16 ? c : (c == 16 ? 17 : 16); }
 
 struct SplatParams {
     int W, H, k_max, n;
@@ -34,6 +38,7 @@ struct SplatParams {
     const float4 *coef;     // (k_max, HW) per-layer (A, dL/dC_raw)
     const float *thr;       // (k_max, HW) closing depths of layers >= 3
     const int4 *hdr;        // (HW, 2) (closed-layer count, closing depths of layers 0..2), (depths 3..6)
+    const float4 *zc;       // kCons: (k_max, HW) per layer (B, Q, z_bar, var) of the consolidation penalty
     float *acc;             // (n, 20)
 };
 
@@ -56,8 +61,9 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return r * (2.f - x * r);
 }
 
+template <bool kCons>
 __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R, int ix, int iy, float x, float y,
-                                         float u, float v, float rho2, float g[NCH]) {
+                                         float u, float v, float rho2, float *g) {
     const size_t HW = (size_t)P.W * P.H;
     const size_t pix = (size_t)iy * P.W + ix;
     // the packed header and the (most common) layer-0 coefficients are loaded
@@ -89,7 +95,13 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     float e;  // exp(-rho^2 / 2) by the hardware ex2 (ftz: no range fix-up)
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(rho2 * -0.72134752044448170368f));
     const float w = R.d.x * e;
-    const float gw = cf.x + cf.y * R.e.x + cf.z * R.e.y + cf.w * R.e.z;
+    float gw = cf.x + cf.y * R.e.x + cf.z * R.e.y + cf.w * R.e.z;
+    if constexpr (kCons) {  // consolidation penalty (backward.py:272-286, centred depth form)
+        const float4 zq = __ldg(P.zc + m * HW + pix);
+        const float dz = R.d.y - zq.z;
+        gw += zq.x * dz + zq.y * (dz * dz - zq.w);
+        g[17] += w * (zq.x + 2.f * zq.y * dz);
+    }
     g[13] += w * cf.y; g[14] += w * cf.z; g[15] += w * cf.w;
     const float gr = -0.5f * w * gw;
     g[12] += e * gw;
@@ -268,7 +280,7 @@ struct GroupSmem {
 // pass 2 evaluates the gradient on the covered items, 8 per iteration.  One
 // 3-level transposed reduction per group and plain stores of the record's
 // row (each record committed exactly once: no atomics, deterministic).
-template <bool kSmemNdc>
+template <bool kSmemNdc, bool kCons>
 __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_kernel(SplatParams P, const int32_t *order,
                                                                         int32_t *counters)
 {
@@ -287,7 +299,8 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
     const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & (kGL - 1);
     const unsigned glt = (1u << gl) - 1u;
     int ch[3];
-    warp_tr_indices<NCH, 4>(ch, lane);
+    constexpr int NC = nch<kCons>();
+    warp_tr_indices<NC, 4>(ch, lane);
     const int nsmall = counters[4];
     const int nrounds = (nsmall + 3) >> 2, hrounds = (counters[5] + 3) >> 2;
     int32_t *work = counters + 2;
@@ -330,9 +343,9 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
         const unsigned mrw = ((1u << 20) + (unsigned)rw - 1u) / (unsigned)rw;
         FastCov f;
         fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
-        float g[NCH];
+        float g[NC];
 #pragma unroll
-        for (int k = 0; k < NCH; ++k) g[k] = 0.f;
+        for (int k = 0; k < NC; ++k) g[k] = 0.f;
         int touch = 0;
         const int amax = __reduce_max_sync(0xffffffffu, area);
         for (int c0 = 0; c0 < amax; c0 += kGCap) {
@@ -365,12 +378,12 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
                     const float r2 = R.c.y * q.x * q.x + 2.f * R.c.z * q.x * q.y + R.c.w * q.y * q.y;
                     // pixel centres from the (shared-memory) tables: no int->float conversions
                     const int ix = ixy & 0xffff, iy = ixy >> 16;
-                    touch += item_grad(P, R, ix, iy, xs[ix], ys[iy], q.x, q.y, r2, g);
+                    touch += item_grad<kCons>(P, R, ix, iy, xs[ix], ys[iy], q.x, q.y, r2, g);
                 }
             }
             __syncwarp();
         }
-        warp_tr_all<NCH, 4>(g, lane);  // 3 channel sums of the group per lane
+        warp_tr_all<NC, 4>(g, lane);  // 3 channel sums of the group per lane
         touch += __shfl_xor_sync(0xffffffffu, touch, 4);
         touch += __shfl_xor_sync(0xffffffffu, touch, 2);
         touch += __shfl_xor_sync(0xffffffffu, touch, 1);
@@ -379,9 +392,9 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
             // channels held by two lanes carry identical sums
             float *dst = P.acc + (size_t)__ldg(order + e) * SS_ACC_FLOATS;
 #pragma unroll
-            for (int i = 0; i < 3; ++i) dst[ch[i] == 16 ? 17 : ch[i]] = g[i];
+            for (int i = 0; i < 3; ++i) dst[acc_slot(ch[i])] = g[i];
             if (gl == 0) reinterpret_cast<int *>(dst)[18] = touch;
-            if (gl == 1) dst[16] = 0.f;
+            if (!kCons && gl == 1) dst[16] = 0.f;
             if (gl == 2) dst[19] = SS_ACC_MOMENTS;
         }
         __syncwarp();
@@ -393,15 +406,16 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
 
 // Gradient contribution of record R at rect pixel k (row-major) for the big
 // records (no compaction), accumulated into g[]; returns 1 when touched.
+template <bool kCons>
 __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &R, const FastCov &f, int k, int rw,
-                                          float inv_rw, float g[NCH]) {
+                                          float inv_rw, float *g) {
     int ixy;
     float4 q;
     // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
     const int ky = (int)(((float)k + 0.5f) * inv_rw);
     if (!item_cover(P.xs, P.ys, R, f, R.r.x + (k - ky * rw), R.r.y + ky, ixy, q)) return 0;
     const int ix = ixy & 0xffff, iy = ixy >> 16;
-    return item_grad(P, R, ix, iy, __ldg(P.xs + ix), __ldg(P.ys + iy), q.x, q.y, q.z, g);
+    return item_grad<kCons>(P, R, ix, iy, __ldg(P.xs + ix), __ldg(P.ys + iy), q.x, q.y, q.z, g);
 }
 
 // Big records (grazing splats whose filtered bound spans up to most of the
@@ -412,8 +426,10 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
 // huge entry h goes to CTA (c + 37 h) mod grid).  Warps split the pixels in
 // 32-pixel rows, reduce, and commit with atomics (the splat kernel zeroed
 // the rows).
+template <bool kCons>
 __device__ __forceinline__ void big_record(const SplatParams &P, int rec, int c0, int cstep, int wid, int nw,
                                            int lane, int my_ch, bool owner) {
+    constexpr int NC = nch<kCons>();
     SsRecord R;
     load_record(P.records, rec, R);
     const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
@@ -421,27 +437,28 @@ __device__ __forceinline__ void big_record(const SplatParams &P, int rec, int c0
     const float inv_rw = fast_rcp((float)rw);
     FastCov f;
     fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
-    float g[NCH];
+    float g[NC];
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) g[k] = 0.f;
+    for (int k = 0; k < NC; ++k) g[k] = 0.f;
     int touch = 0;
     for (int c = c0; c < nchunks; c += cstep) {
         const int k1 = min(area, (c + 1) * kBigChunk);
-        for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad(P, R, f, k, rw, inv_rw, g);
+        for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad<kCons>(P, R, f, k, rw, inv_rw, g);
     }
     const int tot = __reduce_add_sync(0xffffffffu, touch);
     if (tot == 0) return;
-    warp_tr_reduce<NCH>(g, lane);
+    warp_tr_reduce<NC>(g, lane);
     float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
-    if (owner) atomicAdd(dst + (my_ch == 16 ? 17 : my_ch), g[0]);
+    if (owner) atomicAdd(dst + acc_slot(my_ch), g[0]);
     if (lane == 0) atomicAdd(reinterpret_cast<int *>(dst) + 18, tot);
 }
 
+template <bool kCons>
 __global__ void __launch_bounds__(256) big_bwd_kernel(SplatParams P, const int32_t *big_list,
                                                       const int32_t *big_count)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int my_ch = warp_tr_index<NCH>(lane);
+    const int my_ch = warp_tr_index<nch<kCons>()>(lane);
     const unsigned same = __match_any_sync(0xffffffffu, my_ch);
     const bool owner = (__ffs(same) - 1) == lane;
     const int nmed = big_count[0], nhuge = big_count[1];
@@ -454,11 +471,11 @@ __global__ void __launch_bounds__(256) big_bwd_kernel(SplatParams P, const int32
         __syncthreads();
         const int b = s_b;
         if (b >= nmed) break;
-        big_record(P, big_list[b], 0, 1, wid, nw, lane, my_ch, owner);
+        big_record<kCons>(P, big_list[b], 0, 1, wid, nw, lane, my_ch, owner);
     }
     for (int h = 0; h < nhuge; ++h) {
         const int first = (int)(((long long)blockIdx.x - 37LL * h) % G + G) % G;
-        big_record(P, big_list[P.n - 1 - h], first, G, wid, nw, lane, my_ch, owner);
+        big_record<kCons>(P, big_list[P.n - 1 - h], first, G, wid, nw, lane, my_ch, owner);
     }
 }
 
@@ -470,9 +487,20 @@ extern "C" size_t ss_train_backward_scratch_words(int n, int width, int height)
     return (size_t)width + height + kHeadWords + 2 * (size_t)n + ((size_t)n + 3) / 4;
 }
 
-extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
-                                         int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
-                                         float *pixel_ndc, float *rec_acc, void *stream)
+template <bool kSmemNdc, bool kCons>
+void launch_splat(const SplatParams &P, const int32_t *order, int32_t *counters, int smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(splat_bwd_kernel<kSmemNdc, kCons>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSplatWarps * (int)sizeof(GroupSmem) + (kSmemNdc ? kNdcSmem * (int)sizeof(float) : 0));
+        attr = true;
+    }
+    splat_bwd_kernel<kSmemNdc, kCons><<<148 * SS_SPLAT_MINB, 32 * kSplatWarps, smem, st>>>(P, order, counters);
+}
+
+static int backward_records(int n, const int8_t *cull, const float *records, int width, int height, int k_max,
+                            const float *coef, const float *thr, const int32_t *pix_hdr, const float *zcoef,
+                            float *pixel_ndc, float *rec_acc, void *stream)
 {
     if (n < 0 || width <= 0 || height <= 0 || k_max < 1 || k_max > SS_KMAX_CAP) return SS_ERR_INVALID;
     if (n == 0) return SS_OK;
@@ -494,28 +522,43 @@ extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float 
     P.xs = pixel_ndc; P.ys = pixel_ndc + width;
     P.coef = reinterpret_cast<const float4 *>(coef);
     P.thr = thr; P.hdr = reinterpret_cast<const int4 *>(pix_hdr); P.acc = rec_acc;
+    P.zc = reinterpret_cast<const float4 *>(zcoef);
+    const bool cons = zcoef != nullptr;
     area_class_kernel<<<148 * 4, 256, 0, st>>>(P, cls, big_list, counters, hist);
     SS_CUDA_CHECK_LAUNCH();
     area_scatter_kernel<<<(n + 256 * kScatItems - 1) / (256 * kScatItems), 256, 0, st>>>(n, cls, hist, cursor, order,
                                                                                        counters + 4);
     SS_CUDA_CHECK_LAUNCH();
     const int smem = kSplatWarps * (int)sizeof(GroupSmem);
-    const bool ndc_smem = width + height <= kNdcSmem;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(splat_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             smem + kNdcSmem * (int)sizeof(float));
-        cudaFuncSetAttribute(splat_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
+    // (the pixel-centre tables sit right after the NDC scratch: xs then ys, contiguous)
+    const int smem_ndc = smem + (width + height) * (int)sizeof(float);
+    if (width + height <= kNdcSmem) {
+        if (cons) launch_splat<true, true>(P, order, counters, smem_ndc, st);
+        else launch_splat<true, false>(P, order, counters, smem_ndc, st);
+    } else {
+        if (cons) launch_splat<false, true>(P, order, counters, smem, st);
+        else launch_splat<false, false>(P, order, counters, smem, st);
     }
-    // (the tables sit right after the NDC scratch: xs then ys, contiguous)
-    if (ndc_smem)
-        splat_bwd_kernel<true><<<148 * SS_SPLAT_MINB, 32 * kSplatWarps, smem + (width + height) * (int)sizeof(float),
-                                 st>>>(P, order, counters);
-    else
-        splat_bwd_kernel<false><<<148 * SS_SPLAT_MINB, 32 * kSplatWarps, smem, st>>>(P, order, counters);
     SS_CUDA_CHECK_LAUNCH();
-    big_bwd_kernel<<<148 * 4, 256, 0, st>>>(P, big_list, counters);
+    if (cons) big_bwd_kernel<true><<<148 * 4, 256, 0, st>>>(P, big_list, counters);
+    else big_bwd_kernel<false><<<148 * 4, 256, 0, st>>>(P, big_list, counters);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
+}
+
+extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
+                                         int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
+                                         float *pixel_ndc, float *rec_acc, void *stream)
+{
+    return backward_records(n, cull, records, width, height, k_max, coef, thr, pix_hdr, nullptr, pixel_ndc, rec_acc,
+                            stream);
+}
+
+extern "C" int ss_train_backward_records_cons(int n, const int8_t *cull, const float *records, int width, int height,
+                                              int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
+                                              const float *zcoef, float *pixel_ndc, float *rec_acc, void *stream)
+{
+    if (!zcoef) return SS_ERR_INVALID;
+    return backward_records(n, cull, records, width, height, k_max, coef, thr, pix_hdr, zcoef, pixel_ndc, rec_acc,
+                            stream);
 }

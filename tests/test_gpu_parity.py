@@ -84,12 +84,13 @@ def test_stacks_and_cover_counts():
         assert bad == 0, (k, err)
 
 
+@pytest.mark.parametrize("path", ["records", "walk"])
 @pytest.mark.parametrize("name", SCENES)
-def test_backward_matches_reference(name):
+def test_backward_matches_reference(name, path):
     d = load(name)
     cloud, cam, env, res = _render(d)
     back = ss.backward_image(cloud, res, g_rgb=d["g_rgb_in"], g_alpha=d.get("g_alpha_in"),
-                             cons_scale=float(d["cons_scale"]))
+                             cons_scale=float(d["cons_scale"]), path=path)
     for k in ("centers", "quats", "log_scales", "albedo_raw", "metallic_raw", "roughness_raw", "colors",
               "ss_grad", "env_base_log"):
         if f"g_{k}" not in d:

@@ -1,10 +1,9 @@
 """The record-parallel backward of the training step (csrc/train_step.cu:
 area-class sort, 8-lane groups, medium and huge big-rect paths) against the
 walk-based backward that mirrors the reference (_backward_kernel,
-backward.py:48-321; checked against the reference goldens in
-test_gpu_parity.py).  A vanishing consolidation weight routes
-backward_image() through the walk; cons_scale = 0 through the record kernels.
-Needs a B200."""
+backward.py:48-321; both are checked against the reference goldens in
+test_gpu_parity.py), with and without the consolidation penalty.  Needs a
+B200."""
 
 import numpy as np
 import pytest
@@ -32,12 +31,12 @@ def _mixed_cloud(n=600, seed=0, big=20, huge=5):
     return scenes._raw_cloud(p, p, ls, rng.uniform(0, 1, (n, 3)), rng.uniform(0.1, 0.9, n), rng.uniform(0, 1, n))
 
 
-def _both_paths(cloud, cam, env, g_seed=1):
+def _both_paths(cloud, cam, env, g_seed=1, cons_scale=0.0):
     res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
     g = torch.from_numpy(np.random.default_rng(g_seed).normal(0, 1e-3, (cam.height, cam.width, 3)).astype(np.float32))
     g = g.cuda()
-    rec = ss.backward_image(cloud, res, g_rgb=g, cons_scale=0.0)
-    walk = ss.backward_image(cloud, res, g_rgb=g, cons_scale=1e-30)
+    rec = ss.backward_image(cloud, res, g_rgb=g, cons_scale=cons_scale, path="records")
+    walk = ss.backward_image(cloud, res, g_rgb=g, cons_scale=cons_scale, path="walk")
     return res, rec, walk
 
 
@@ -48,13 +47,16 @@ def _rect_areas(res):
     return host((r[:, 2] - r[:, 0]) * (r[:, 3] - r[:, 1]))
 
 
-@pytest.mark.parametrize("wh", [(200, 200), (231, 157)])
-def test_record_backward_matches_walk_with_big_rects(wh):
+@pytest.mark.parametrize("wh,cons", [((200, 200), 0.0), ((231, 157), 0.0), ((200, 200), 1e-3), ((231, 157), 1e-2)])
+def test_record_backward_matches_walk_with_big_rects(wh, cons):
     W, H = wh
     cloud = ss.SurfelCloud(**_mixed_cloud())
     env = ss.EnvironmentLight.from_base(scenes.env_lognormal(16, 32, 2))
     cam = ss.fibonacci_cameras(3, 3.0, W, H, fov_y_deg=40.0)[1]
-    res, rec, walk = _both_paths(cloud, cam, env)
+    res, rec, walk = _both_paths(cloud, cam, env, cons_scale=cons)
+    assert rec.cons_loss == pytest.approx(walk.cons_loss, rel=1e-5, abs=1e-12)
+    if cons > 0.0:
+        assert rec.cons_loss > 0.0
     a = _rect_areas(res)
     assert (a > 512).sum() >= 2 and (a > 8192).sum() >= 1, "scene must exercise the medium and huge paths"
     np.testing.assert_array_equal(host(rec.touch_count), host(walk.touch_count))
