@@ -98,6 +98,12 @@ class ViewBuffers:
         self.capacity = 0
         self.keys = self.pair = self.pair_rect = None
 
+    def alloc_zstats(self, k_max, W, H):
+        """Per-layer depth moments / penalty coefficients of the consolidation
+        term (allocated on first use)."""
+        if getattr(self, "zst", None) is None:
+            self.zst = torch.empty((k_max, H * W, 4), device=self.coef.device, dtype=torch.float32)
+
     def alloc_loss(self, W, H, device):
         """Buffers of the deferred-loss step (photometric loss on the image)."""
         from .losses import ImageLoss
@@ -121,15 +127,21 @@ class ViewBuffers:
 class TrainStep:
     def __init__(self, cloud, env, width, height, k_max=16, tile=16, background=(0.0, 0.0, 0.0),
                  lrs=None, pair_capacity=None, process_group=None, options=None, streams=2, loss="l1",
-                 tone="hdr-loss", lambda_ssim=0.2, lambda_sil=0.1):
+                 tone="hdr-loss", lambda_ssim=0.2, lambda_sil=0.1, cons_scale=0.0):
         """loss="l1": the BASELINE config loss (mean |rgb - target| in linear
         space), fused into the forward kernel.  loss="photometric": the
         reference fit loss (train.py:194-206): tone_map(tone) then
         (1 - lambda_ssim) L1 + lambda_ssim (1 - SSIM) on the device, plus
-        lambda_sil * silhouette when masks are given to step()."""
+        lambda_sil * silhouette when masks are given to step(), plus the
+        depth-consolidation penalty with weight cons_scale (the reference's
+        lambda_cons / (extent * npix) of its main phase, train.py:208-213;
+        settable between steps as `ts.cons_scale`)."""
         if loss not in ("l1", "photometric"):
             raise ValueError(f"unknown loss {loss!r}")
         self.loss_mode, self.tone, self.lambda_ssim, self.lambda_sil = loss, tone, float(lambda_ssim), float(lambda_sil)
+        if float(cons_scale) > 0.0 and loss != "photometric":
+            raise ValueError("the consolidation penalty needs loss='photometric' (deferred coefficients)")
+        self.cons_scale = float(cons_scale)
         self.lib = _lib.load()
         self.cloud, self.env = cloud, env
         self.W, self.H, self.k_max, self.tile = int(width), int(height), int(k_max), int(tile)
@@ -247,11 +259,21 @@ class TrainStep:
                        "ss_train_forward")
         else:
             # deferred loss: image -> loss kernels -> layer coefficients
-            _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
-                                            _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
-                                            None, _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr), None,
-                                            _lib.ptr(b.rgb), _lib.ptr(b.alpha), _lib.ptr(b.tile_order), s),
-                       "ss_train_forward")
+            cons = self.cons_scale > 0.0
+            if cons:
+                b.alloc_zstats(self.k_max, self.W, self.H)
+                _lib.check(lib.ss_train_forward_zstats(self.W, self.H, self.tile, _lib.ptr(b.offsets),
+                                                       _lib.ptr(b.pair), _lib.ptr(b.pair_rect), _lib.ptr(b.records),
+                                                       self._bg[0], self.k_max, _lib.ptr(b.coef), _lib.ptr(b.thr),
+                                                       _lib.ptr(b.pix_hdr), _lib.ptr(b.rgb), _lib.ptr(b.alpha),
+                                                       _lib.ptr(b.tile_order), _lib.ptr(b.zst), s),
+                           "ss_train_forward_zstats")
+            else:
+                _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
+                                                _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
+                                                None, _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr), None,
+                                                _lib.ptr(b.rgb), _lib.ptr(b.alpha), _lib.ptr(b.tile_order), s),
+                           "ss_train_forward")
             out = b.imgloss(b.rgb, target, b.g_rgb, self.lambda_ssim, self.tone)
             b.loss_part += out[0:1]
             g_alpha = None
@@ -261,16 +283,27 @@ class TrainStep:
                 b.g_alpha.mul_(self.lambda_sil)
                 b.loss_part += self.lambda_sil * b.sil
                 g_alpha = b.g_alpha
-            _lib.check(lib.ss_train_coefs(self.W, self.H, self.k_max, _lib.ptr(b.pix_hdr), _lib.ptr(b.coef),
-                                          _lib.ptr(b.g_rgb), _lib.ptr(g_alpha), self._bg[0], s), "ss_train_coefs")
+            if cons:
+                _lib.check(lib.ss_train_coefs_cons(self.W, self.H, self.k_max, _lib.ptr(b.pix_hdr), _lib.ptr(b.coef),
+                                                   _lib.ptr(b.zst), _lib.ptr(b.g_rgb), _lib.ptr(g_alpha), self._bg[0],
+                                                   self.cons_scale, _lib.ptr(b.loss_part), s), "ss_train_coefs_cons")
+            else:
+                _lib.check(lib.ss_train_coefs(self.W, self.H, self.k_max, _lib.ptr(b.pix_hdr), _lib.ptr(b.coef),
+                                              _lib.ptr(b.g_rgb), _lib.ptr(g_alpha), self._bg[0], s), "ss_train_coefs")
         self._ev_end(ev)
         if target_done is not None:
             target_done.record()
         ev = self._ev_begin("train_backward")
-        _lib.check(lib.ss_train_backward_records(self.n, _lib.ptr(b.cull), _lib.ptr(b.records), self.W,
-                                                 self.H, self.k_max, _lib.ptr(b.coef), _lib.ptr(b.thr),
-                                                 _lib.ptr(b.pix_hdr), _lib.ptr(b.pixel_ndc), _lib.ptr(b.acc), s),
-                   "ss_train_backward_records")
+        if self.loss_mode == "photometric" and self.cons_scale > 0.0:
+            _lib.check(lib.ss_train_backward_records_cons(self.n, _lib.ptr(b.cull), _lib.ptr(b.records), self.W,
+                                                          self.H, self.k_max, _lib.ptr(b.coef), _lib.ptr(b.thr),
+                                                          _lib.ptr(b.pix_hdr), _lib.ptr(b.zst), _lib.ptr(b.pixel_ndc),
+                                                          _lib.ptr(b.acc), s), "ss_train_backward_records_cons")
+        else:
+            _lib.check(lib.ss_train_backward_records(self.n, _lib.ptr(b.cull), _lib.ptr(b.records), self.W,
+                                                     self.H, self.k_max, _lib.ptr(b.coef), _lib.ptr(b.thr),
+                                                     _lib.ptr(b.pix_hdr), _lib.ptr(b.pixel_ndc), _lib.ptr(b.acc), s),
+                       "ss_train_backward_records")
         self._ev_end(ev)
         ev = self._ev_begin("chain")
         # the chain kernels of concurrent views may overlap: their parameter

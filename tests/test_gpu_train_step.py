@@ -86,23 +86,24 @@ def test_host_targets_path_equals_resident():
     assert torch.equal(outs[0][1], outs[1][1])
 
 
-@pytest.mark.parametrize("with_masks", [False, True])
-def test_photometric_train_step_matches_api_path(with_masks):
-    """loss="photometric" (the reference fit loss, train.py:194-206: hdr-loss
-    tone map, 0.8 L1 + 0.2 (1 - SSIM), + lambda_sil silhouette) through the
-    deferred-loss kernels vs render -> image_loss / silhouette_loss ->
-    backward_image summed over views."""
+@pytest.mark.parametrize("with_masks,cons", [(False, 0.0), (True, 0.0), (True, 2e-4)])
+def test_photometric_train_step_matches_api_path(with_masks, cons):
+    """loss="photometric" (the reference fit loss, train.py:194-213: hdr-loss
+    tone map, 0.8 L1 + 0.2 (1 - SSIM), + lambda_sil silhouette, + the
+    consolidation penalty of the main phase) through the deferred-loss
+    kernels vs render -> image_loss / silhouette_loss -> backward_image
+    (walk path) summed over views."""
     init, env_base, cams, targets = _scene(n=2500, res=80)
     rng = np.random.default_rng(5)
     masks = [torch.as_tensor((rng.uniform(size=(80, 80)) > 0.5).astype(np.float32), device="cuda")
              for _ in cams] if with_masks else None
     cloud = ss.SurfelCloud(**init)
     env = ss.EnvironmentLight.from_base(env_base)
-    ts = TrainStep(cloud, env, 80, 80, loss="photometric", lambda_sil=0.3)
+    ts = TrainStep(cloud, env, 80, 80, loss="photometric", lambda_sil=0.3, cons_scale=cons)
     ts.gradients(cams, targets, masks)
     torch.cuda.synchronize()
     acc = {k: torch.zeros_like(ts.grads[k]) for k in PARAMS}
-    loss = 0.0
+    loss = cons_total = 0.0
     d_diff = torch.zeros(env.base.shape, device="cuda", dtype=torch.float64)
     d_spec = torch.zeros(env.specular.shape, device="cuda", dtype=torch.float64)
     for i, (cam, tgt) in enumerate(zip(cams, targets)):
@@ -114,12 +115,15 @@ def test_photometric_train_step_matches_api_path(with_masks):
             sv, ga = ss.silhouette_loss(res.alpha, masks[i])
             loss += 0.3 * sv
             g_alpha = 0.3 * ga
-        back = ss.backward_image(cloud, res, g_rgb=g, g_alpha=g_alpha)
+        back = ss.backward_image(cloud, res, g_rgb=g, g_alpha=g_alpha, cons_scale=cons, path="walk")
+        loss += back.cons_loss
+        cons_total += back.cons_loss
         for k in PARAMS:
             acc[k] += getattr(back, k).reshape(acc[k].shape)
         d_diff += back.d_diffuse
         d_spec += back.d_specular
     assert float(ts.loss_f.item()) == pytest.approx(loss, rel=1e-5)
+    assert (cons_total > 0.01 * loss) == (cons > 0.0)  # the penalty is exercised when on
     for k in PARAMS:
         bad, err = grad_close(ts.grads[k], acc[k])
         assert bad == 0, (k, err)
