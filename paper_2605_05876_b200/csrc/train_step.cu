@@ -23,10 +23,31 @@
 
 namespace {
 
+
 constexpr int KS = 4;   // layers per pixel staged in shared memory (rest read from global)
 constexpr int NCH = 17; // t1(3) t2(3) t4(3) Sigma^-1(3) n_f colour(3) screen-space |g|
 constexpr int NCHC = 18; // + d/d view_z (consolidation)
 template <bool kCons> __host__ __device__ constexpr int nch() { return kCons ? NCHC : NCH; }
+// Warp max / sum by xor shuffles.  The faster loop bounds (redux.sync max,
+// or vote.any loop conditions) were measured to hang the record kernel
+// intermittently on B200 (5 of 28 and 2 of 12 runs of a 3-step
+// single-stream loop: tools/hang_variants.sh, tools/hang_hunt.py), the
+// shuffle form 0 of 52 -- root cause not identified; see DESIGN.md.
+__device__ __forceinline__ int warp_max(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+// max over the 4 groups of a value uniform within each 8-lane group
+__device__ __forceinline__ int group_max(int v) {
+    v = max(v, __shfl_xor_sync(0xffffffffu, v, 8));
+    return max(v, __shfl_xor_sync(0xffffffffu, v, 16));
+}
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 // reduced channel -> accumulator slot (slot 16 = dview_z, 17 = ss sum)
 __device__ __forceinline__ int acc_slot(int c) { return c < 16 ? c : (c == 16 ? 17 : 16); }
 
@@ -347,7 +368,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
 #pragma unroll
         for (int k = 0; k < NC; ++k) g[k] = 0.f;
         int touch = 0;
-        const int amax = __reduce_max_sync(0xffffffffu, area);
+        const int amax = group_max(area);  // area is uniform within a group
         for (int c0 = 0; c0 < amax; c0 += kGCap) {
             // pass 1: exact coverage of up to kGCap rect pixels, compaction
             const int cend = min(c0 + kGCap, amax);
@@ -368,7 +389,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
             }
             __syncwarp();
             // pass 2: gradients of the covered items
-            const int nmax = __reduce_max_sync(0xffffffffu, ncov);
+            const int nmax = group_max(ncov);  // ncov is uniform within a group
             for (int j0 = 0; j0 < nmax; j0 += kGL) {
                 const int j = j0 + gl;
                 if (j < ncov) {
@@ -445,7 +466,7 @@ __device__ __forceinline__ void big_record(const SplatParams &P, int rec, int c0
         const int k1 = min(area, (c + 1) * kBigChunk);
         for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad<kCons>(P, R, f, k, rw, inv_rw, g);
     }
-    const int tot = __reduce_add_sync(0xffffffffu, touch);
+    const int tot = warp_sum(touch);
     if (tot == 0) return;
     warp_tr_reduce<NC>(g, lane);
     float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
