@@ -379,6 +379,34 @@ class TrainStep:
         for b in self.bufs:
             b.flags.zero_()
 
+    def set_normal_consistency(self, index, lambda_nc):
+        """Add lambda_nc * normal_consistency_loss(cloud, index) to every step
+        (its quaternion gradient and value; train.py:216-221).  The index is
+        the caller's NeighborIndex (rebuilt on its own schedule, like the
+        reference's); pass index=None to turn the term off."""
+        self._nc = None if index is None or float(lambda_nc) == 0.0 else (index, float(lambda_nc))
+
+    def _normal_consistency(self):
+        nc = getattr(self, "_nc", None)
+        if nc is None:
+            return
+        if dist.is_available() and dist.is_initialized() and dist.get_rank(self.pg) != 0:
+            return  # a per-step (not per-view) term: added once, on rank 0, before the all-reduce
+        index, lam = nc
+        n = self.n
+        if index.neighbors.shape[0] != n:
+            raise ValueError("normal-consistency index built for a different cloud size")
+        dev = self.cloud.centers.device
+        val = torch.zeros(1, device=dev, dtype=torch.float64)
+        g_n = torch.empty((n, 3), device=dev, dtype=torch.float64)
+        g_q = torch.zeros((n, 4), device=dev, dtype=torch.float32)
+        _lib.check(self.lib.ss_normal_consistency(n, index.neighbors.shape[1], _lib.ptr(self.cloud.centers),
+                                                  _lib.ptr(self.cloud.quats), _lib.ptr(index.neighbors),
+                                                  _lib.ptr(index.mean_dist), _lib.ptr(val), _lib.ptr(g_n),
+                                                  _lib.ptr(g_q), _lib.stream_ptr()), "ss_normal_consistency")
+        self.grads["quats"].view(-1).add_(g_q.view(-1), alpha=lam)
+        self.loss.add_(val, alpha=lam)
+
     def gradients(self, cameras, targets, masks=None):
         """Sum of per-view gradients over this rank's views (+ env adjoint)."""
         if self.capacity == 0:
@@ -387,6 +415,7 @@ class TrainStep:
         self._nviews = len(cameras)
         self._pairs, self._kept = [], []
         self._run_views(cameras, lambda i, st: targets[i], masks=masks)
+        self._normal_consistency()
         self._finish()
 
     def _env_adjoint(self):

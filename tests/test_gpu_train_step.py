@@ -158,3 +158,25 @@ def test_train_step_ragged_image(wh):
     for k in PARAMS:
         bad, err = grad_close(ts.grads[k], acc[k])
         assert bad == 0, (k, err)
+
+
+def test_train_step_with_normal_consistency():
+    """set_normal_consistency adds lambda_nc * normal_consistency_loss (value and
+    quaternion gradient) to the step, as train.py:216-221."""
+    init, env_base, cams, targets = _scene(n=2000, res=64)
+    cloud = ss.SurfelCloud(**init)
+    env = ss.EnvironmentLight.from_base(env_base)
+    ts = TrainStep(cloud, env, 64, 64)
+    ts.gradients(cams, targets)
+    base_loss = float(ts.loss_f.item())
+    base_q = ts.grads["quats"].clone()
+    idx = ss.NeighborIndex(cloud, k=8)
+    ts.set_normal_consistency(idx, 0.05)
+    ts.gradients(cams, targets)
+    nc, g = ss.normal_consistency_loss(cloud, idx)
+    assert float(ts.loss_f.item()) == pytest.approx(base_loss + 0.05 * nc, rel=1e-6)
+    bad, err = grad_close(ts.grads["quats"], base_q + 0.05 * g.reshape(base_q.shape))
+    assert bad == 0, err
+    ts.set_normal_consistency(None, 0.0)
+    ts.gradients(cams, targets)
+    assert float(ts.loss_f.item()) == pytest.approx(base_loss, rel=1e-6)
