@@ -28,11 +28,12 @@ constexpr int KS = 4;   // layers per pixel staged in shared memory (rest read f
 constexpr int NCH = 17; // t1(3) t2(3) t4(3) Sigma^-1(3) n_f colour(3) screen-space |g|
 constexpr int NCHC = 18; // + d/d view_z (consolidation)
 template <bool kCons> __host__ __device__ constexpr int nch() { return kCons ? NCHC : NCH; }
-// Warp max / sum by xor shuffles.  The faster loop bounds (redux.sync max,
-// or vote.any loop conditions) were measured to hang the record kernel
-// intermittently on B200 (5 of 28 and 2 of 12 runs of a 3-step
-// single-stream loop: tools/hang_variants.sh, tools/hang_hunt.py), the
-// shuffle form 0 of 52 -- root cause not identified; see DESIGN.md.
+// Warp max / sum by xor shuffles.  Loop bounds the compiler can prove
+// warp-uniform (redux.sync max, vote.any loop conditions, or a broadcast
+// from lane 0) make the record kernel ~9% faster but hang it intermittently
+// on B200 (2-5 of 12-28 runs of a 3-step single-stream loop:
+// tools/hang_variants.sh, tools/hang_hunt.py); these forms: 0 of 96 -- root
+// cause not identified; see DESIGN.md.  Keep the bounds non-uniform.
 __device__ __forceinline__ int warp_max(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
