@@ -34,11 +34,6 @@ template <bool kCons> __host__ __device__ constexpr int nch() { return kCons ? N
 // on B200 (2-5 of 12-28 runs of a 3-step single-stream loop:
 // tools/hang_variants.sh, tools/hang_hunt.py); these forms: 0 of 96 -- root
 // cause not identified; see DESIGN.md.  Keep the bounds non-uniform.
-__device__ __forceinline__ int warp_max(int v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
 // max over the 4 groups of a value uniform within each 8-lane group
 __device__ __forceinline__ int group_max(int v) {
     v = max(v, __shfl_xor_sync(0xffffffffu, v, 8));
