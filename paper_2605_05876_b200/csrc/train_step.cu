@@ -36,8 +36,12 @@ template <bool kCons> __host__ __device__ constexpr int nch() { return kCons ? N
 // cause not identified; see DESIGN.md.  Keep the bounds non-uniform.
 // max over the 4 groups of a value uniform within each 8-lane group
 __device__ __forceinline__ int group_max(int v) {
+#ifdef SS_UNIFORM_BOUNDS  // the faster, intermittently hanging form (investigation switch)
+    return __reduce_max_sync(0xffffffffu, v);
+#else
     v = max(v, __shfl_xor_sync(0xffffffffu, v, 8));
     return max(v, __shfl_xor_sync(0xffffffffu, v, 16));
+#endif
 }
 __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
