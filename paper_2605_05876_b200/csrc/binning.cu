@@ -105,8 +105,14 @@ __device__ void tile_order(const int32_t *__restrict__ counts, int ntiles, int32
 // atomics.  Global same-address traffic drops from one atomic per pair to one
 // per (CTA, tile).  Slot order inside a bucket is arbitrary: the per-tile sort
 // that follows keys on (z_start, record), so the result is deterministic.
-constexpr int kScatterThreads = 1024;
-constexpr int kScatterPerThread = 4;
+#ifndef SS_SCATTER_THREADS
+#define SS_SCATTER_THREADS 1024
+#endif
+#ifndef SS_SCATTER_PER_THREAD
+#define SS_SCATTER_PER_THREAD 4
+#endif
+constexpr int kScatterThreads = SS_SCATTER_THREADS;
+constexpr int kScatterPerThread = SS_SCATTER_PER_THREAD;
 
 __global__ void __launch_bounds__(kScatterThreads) scatter_kernel(
     int n, const uint4 *__restrict__ bininfo, const int8_t *__restrict__ cull, int ntx, int ntiles, int tile,
