@@ -86,3 +86,19 @@ def test_record_backward_single_area_class():
     for k in KEYS:
         bad, err = grad_close(getattr(rec, k), getattr(walk, k))
         assert bad == 0, (k, err)
+
+
+def test_record_backward_with_consolidation_at_config2_size():
+    """BASELINE config-2 view (1M surfels, 800x800) with the reference's
+    main-phase consolidation weight: record path vs walk path."""
+    gt = scenes.config2(0, 1_000_000)
+    cloud = ss.SurfelCloud(**scenes.perturb(gt, 1))
+    env = ss.EnvironmentLight(np.log(scenes.env_lognormal(128, 256, 2)))
+    cam = ss.fibonacci_cameras(64, 3.5, 800, 800)[21]
+    res, rec, walk = _both_paths(cloud, cam, env, g_seed=4, cons_scale=100.0 / (800 * 800))
+    assert rec.cons_loss > 0.0
+    assert rec.cons_loss == pytest.approx(walk.cons_loss, rel=1e-5)
+    np.testing.assert_array_equal(host(rec.touch_count), host(walk.touch_count))
+    for k in KEYS:
+        bad, err = grad_close(getattr(rec, k), getattr(walk, k))
+        assert bad <= 1e-4 * getattr(rec, k).numel(), (k, bad, err)
