@@ -72,6 +72,74 @@ def _dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _self_launch(argv, nproc):
+    """`bench.py --gpus N` run WITHOUT torchrun: re-exec this script under
+    torch.distributed.run with N ranks on this node (one process per GPU,
+    rendezvous on 127.0.0.1); rank 0 prints the JSON line.  Returns the
+    launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    return subprocess.call(cmd, env=env)
+
+
+def _check_world(args):
+    rank, world, _ = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    return rank, world
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing without a GPU (gloo on CPU): every
+    rank takes its shard of the step's views, fills a GradPack with
+    rank-dependent values, runs the same two-bucket all-reduce TrainStep
+    uses, and rank 0 checks the sums and prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_05876_b200.step import GradPack, shard_views
+    rank, world = _check_world(args)
+    if world > 1:
+        dist.init_process_group("gloo")
+    views = shard_views(VIEWS_PER_STEP, world, rank)
+    n, texels = 1000, 32
+    pack = GradPack(n, texels, "cpu", dtype=torch.float64)
+    pack.flat.copy_(torch.arange(pack.flat.numel(), dtype=torch.float64) * (rank + 1))
+    pack.view_count.fill_(float(len(views)))
+    work = pack.all_reduce_surfels()
+    pack.all_reduce_rest()
+    if work is not None:
+        work.wait()
+    tri = world * (world + 1) / 2
+    want = torch.arange(pack.flat.numel(), dtype=torch.float64) * tri
+    want[pack.view_count.data_ptr() // 8 - pack.flat.data_ptr() // 8:][:n] = float(VIEWS_PER_STEP)
+    ok = bool(torch.equal(pack.flat, want))
+    counts = [0] * world
+    if world > 1:
+        t = torch.zeros(world, dtype=torch.int64)
+        t[rank] = len(views)
+        dist.all_reduce(t)
+        counts = t.tolist()
+    else:
+        counts = [len(views)]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "backend": "gloo" if world > 1 else "none",
+                          "views_per_rank": counts, "allreduce_ok": ok}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    if not ok:
+        raise SystemExit(1)
+
+
 def _config(extra=None):
     cfg = {"workload": "config2: 1M surfels, 800x800, 64 views/step sharded by view, env 128x256x3, "
                        "L1 loss in linear space, Adam + env refresh per step",
@@ -183,12 +251,13 @@ def run_ours(args):
     from paper_2605_05876_b200 import scenes
     from paper_2605_05876_b200.step import TrainStep
 
-    rank, world, local = _dist_env()
+    rank, world = _check_world(args)
+    local = _dist_env()[2]
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    views_per_rank = VIEWS_PER_STEP // world
-    my_views = list(range(rank * views_per_rank, (rank + 1) * views_per_rank))
+    from paper_2605_05876_b200.step import shard_views
+    my_views = shard_views(VIEWS_PER_STEP, world, rank)
 
     gt = scenes.config2(0, N_SURFELS)
     init = scenes.perturb(gt, 1)
@@ -414,8 +483,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing on CPU (gloo), no GPU work")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(sys.argv[1:], args.gpus))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -28,6 +28,7 @@
 #ifndef SS_ABI_H
 #define SS_ABI_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -39,9 +40,17 @@ enum { SS_OK = 0, SS_ERR_INVALID = 1, SS_ERR_CUDA = 2 };
 #define SS_REC_FLOATS 24  /* 96-byte record, see SsRecord in csrc/ss_common.cuh */
 #define SS_ACC_FLOATS 20  /* per-record backward accumulator: 17 grads + ss + touch + layout flag */
 /* slot 19 of an accumulator row: 0 = slots 0..8 hold dL/dt1, dt2, dt4;
- * SS_ACC_MOMENTS = they hold sum gp, sum x gp, sum y gp of the ray-plane
- * gradient (record-parallel backward; ss_chain_backward converts) */
+ * SS_ACC_MOMENTS = they hold sum gp, sum (x - cx) gp, sum (y - cy) gp of the
+ * ray-plane gradient, (cx, cy) = (t1.z / t4.z, t2.z / t4.z) the projected
+ * centre (record-parallel backward; ss_chain_backward converts) */
 #define SS_ACC_MOMENTS 1.0f
+/* slot 19 = SS_ACC_F64: the row's channels live in float64 in the caller's
+ * rec_acc64 buffer (ss_train_backward_records), row index = the int bits of
+ * slot 0, SS_ACC64_WIDTH doubles per row in channel order dt1 dt2 dt4,
+ * dSigma^-1, dn_f, dcolour, screen |g| sum, dview_z (slot 17 still holds
+ * the float screen sum, slot 18 the touch count) */
+#define SS_ACC_F64 2.0f
+#define SS_ACC64_WIDTH 18
 #define SS_KMAX_CAP 16    /* largest k_max the kernels accept (= reference default K_MAX) */
 
 typedef struct SsCamera {
@@ -113,12 +122,30 @@ int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessO
                   float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
                   uint32_t *bininfo, const SsProjAux *aux, int32_t *flags, void *stream);
 
+/* ---- records from a ProjectedSurfels ---------------------------------------
+ * render(..., proj=P) reuse and bin_and_sort(P) (rasterizer.py:92-116,
+ * :331-339): packs the k compacted rows of a ProjectedSurfels (t1, t2, t4,
+ * sinv (k,3); n_f, view_z, eps_z (k,); rect (k,4) int32) into records
+ * source_index[j] (nullable: row j), colours from `colors` (per SOURCE row,
+ * (n,3), nullable: 0), with the preprocess kernel's certified coverage
+ * margin, bin info and tile histogram (tile_counts zeroed by the caller).
+ * Rows not named by source_index are left as the caller initialised them
+ * (zero rect, its cull code). */
+int ss_pack_records(int k, const float *t1, const float *t2, const float *t4, const float *sinv,
+                    const float *n_f, const float *view_z, const float *eps_z, const int32_t *rect,
+                    const int32_t *source_index, const float *colors, int width, int height, int tile,
+                    float *records, uint32_t *bininfo, int32_t *tile_counts, void *stream);
+
 /* ---- tile binning with deterministic order ---------------------------------
  * Replaces the rest of bin_and_sort() (rasterizer.py:106-116): exclusive scan
  * of tile_counts into tile_offsets (ntiles+1 int32), bucket scatter of
  * (z_start, record) keys, and a per-tile sort by (z_start, record index) so
  * the result equals np.lexsort((rec, z_start, tile)) bit for bit.
- * pair_capacity bounds pair_rec/keys; flags[2] is set when it overflowed.
+ * pair_capacity bounds pair_rec/keys; flags[2] is set when it overflowed
+ * and flags[3] receives max(flags[3], pairs this view needs).  On overflow
+ * the offsets are clamped to the capacity (the excess pairs are dropped, the
+ * results are wrong but every kernel stays inside the caller's buffers):
+ * the caller grows the buffers to flags[3] and re-runs the view.
  * keys: uint64 scratch of pair_capacity entries; cursors: ntiles ints scratch.
  * pair_rect (2 uint32 per pair) receives each pair's record rect packed as
  * (x0 | y0 << 16, x1 | y1 << 16), the rasterisers' cull input.  bininfo: the
@@ -161,8 +188,11 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
  * ss_train_forward: the forward walk fused with the L1 photometric loss
  * (losses.py:94-108, lambda_ssim=0) against `target` (H,W,3) and with the
  * per-pixel suffix recursion of backward.py:201-238.  Writes per pixel and
- * layer the float4 (A, dL/dC_raw rgb) into `coef` (k_max*H*W*4 floats,
- * layer-major planes), per pixel a packed header `pix_hdr` (H*W x 8
+ * layer the float4 (A_hi, dL/dC_raw rgb) into `coef` (k_max*H*W*5 floats:
+ * k_max layer-major float4 planes, then k_max float planes of A_lo; A =
+ * A_hi + A_lo is formed from the float-rounded dL/dC_raw so that the
+ * backward's g_w = A + dL/dC_raw . colour keeps the record colour - layer
+ * mean colour difference exactly; layer sums are float64), per pixel a packed header `pix_hdr` (H*W x 8
  * int32: number of closed layers, then the depths at which layers 0..6
  * closed, as float bits; words past the closed count are not written) and
  * the closing depths of layers >= 7 into `thr` (k_max*H*W floats, plane j), and adds sum|rgb - target| into loss_sum (1 double).
@@ -207,11 +237,17 @@ int ss_train_coefs_cons(int width, int height, int k_max, const int32_t *pix_hdr
                         double *cons_loss, void *stream);
 int ss_train_backward_records_cons(int n, const int8_t *cull, const float *records, int width, int height,
                                    int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
-                                   const float *zcoef, float *pixel_ndc, float *rec_acc, void *stream);
+                                   const float *zcoef, float *pixel_ndc, float *rec_acc, double *rec_acc64,
+                                   void *stream);
 size_t ss_train_backward_scratch_words(int n, int width, int height);
+/* rec_acc64: n x SS_ACC64_WIDTH doubles (no initialisation needed): the
+ * float64 channel sums of the big records (rects > 512 px, ~0.1% of them,
+ * evaluated with the reference's own per-item arithmetic), referenced from
+ * their rec_acc rows (SS_ACC_F64); pass the same buffer to
+ * ss_chain_backward. */
 int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
                               int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
-                              float *pixel_ndc, float *rec_acc, void *stream);
+                              float *pixel_ndc, float *rec_acc, double *rec_acc64, void *stream);
 
 /* ---- image losses ---------------------------------------
  * Replace the reference's numpy/scipy losses: tone_map / tone_map_backward
@@ -252,7 +288,11 @@ int ss_normal_consistency(int n, int k, const float *centers, const float *quats
  * (surfels.py:54-77).  Reads rec_acc and ADDS into the parameter gradients
  * (so multi-view steps accumulate in place): g_centers (n,3), g_quats (n,4),
  * g_log_scales (n,2), g_albedo_raw (n,3), g_metallic_raw, g_roughness_raw,
- * g_colors (n,3, nullable), ss_grad (n), touched (n int32 counts).  With
+ * g_colors (n,3, nullable), ss_grad (n), touched (n int32 covering-pixel
+ * counts, nullable), view_count (n float32, nullable: +1 for every surfel
+ * that covers at least one pixel of this view -- the per-view `touched` bool
+ * of backward.py:432-441 summed over a step's views, as DensifyStats
+ * accumulates it, densify.py:35-37).  With
  * SS_COLOR_IBL it also scatters the derived-map gradients into d_diffuse
  * (He,We,3) and d_specular (L,He,We,3) (float64, accumulated with fp64
  * atomics: a step sums 64 views x N surfels x 36 scatters into them). */
@@ -267,10 +307,11 @@ typedef struct SsGrads {
      * adjoint scatters into them with vector float32 reductions and
      * ss_env_grad_merge later folds them into d_diffuse / d_specular */
     float *d_diffuse4, *d_specular4;
+    float *view_count;  /* nullable */
 } SsGrads;
 int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                       int color_source, const SsEnv *env, const int8_t *cull,
-                      const float *rec_acc, const SsGrads *grads, void *stream);
+                      const float *rec_acc, const double *rec_acc64, const SsGrads *grads, void *stream);
 
 /* ss_env_grad_merge: dst[3 t + c] += src4[4 t + c] (float64 += float32) for
  * t < texels, c < 3, and zeroes src4 (the per-view derived-map accumulators
@@ -282,17 +323,37 @@ int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void *stream);
  * ss_env_refresh: EnvironmentLight.refresh (shading.py:369-379): base_log
  *   (He,We,3) -> base, diffuse (He,We,3), specular (L,He,We,3).
  * ss_env_adjoint: env_gradient (shading.py:381-394): d_diffuse, d_specular
- *   -> d_base_log (He,We,3) (and d_base when non-null).
- * Both need the diffuse row sums: ss_env_rowsums fills rowsum (He*We floats).
- * `work`: float64 scratch of 3*He*We (split-column partial sums). */
+ *   -> d_base_log (He,We,3) and d_base (He,We,3 doubles, also the scratch of
+ *   the accumulation).
+ * The prefilter operators of the reference (build_diffuse_operator /
+ * build_specular_operator, shading.py:275-331: dense T x T float64) are
+ * passed as a caller-owned bundle, built once per env shape:
+ *   rowsum  (He*We floats) diffuse row sums, from ss_env_rowsums;
+ *   khat    (nullable) the diffuse kernel's spectrum, ss_env_khat_words(He,We)
+ *           doubles filled by ss_env_khat (0 words: odd widths / too large;
+ *           NULL selects the O(T^2) N-body quadrature);
+ *   row_ptr/col/rval, col_ptr/row/cval (nullable) the sparse specular
+ *           operators of ss_spec_op_count / ss_spec_op_fill and their per-level
+ *           transpose (CSC by a stable sort); NULL regenerates the GGX samples
+ *           on the fly;
+ *   work    3*He*We doubles of scratch.
+ * The library keeps no state and allocates nothing. */
+typedef struct SsEnvOps {
+    const float *rowsum;
+    const double *khat;
+    const int64_t *row_ptr; const int32_t *col; const float *rval;
+    const int64_t *col_ptr; const int32_t *row; const float *cval;
+    double *work;
+} SsEnvOps;
 int ss_brdf_lut(int res, int samples, float *lut, void *stream);
-int ss_env_rowsums(int he, int we, float *rowsum, double *work, void *stream);
-int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log,
-                   const float *rowsum, float *base, float *diffuse, float *specular, double *work,
+size_t ss_env_khat_words(int he, int we);
+int ss_env_khat(int he, int we, double *khat, void *stream);
+int ss_env_rowsums(int he, int we, const double *khat, float *rowsum, double *work, void *stream);
+int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log, const SsEnvOps *ops,
+                   float *base, float *diffuse, float *specular, void *stream);
+int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, const SsEnvOps *ops,
+                   const double *d_diffuse, const double *d_specular, double *d_base, float *d_base_log,
                    void *stream);
-int ss_env_adjoint(int he, int we, int levels, int samples, const float *base,
-                   const float *rowsum, const double *d_diffuse, const double *d_specular,
-                   double *d_base, float *d_base_log, double *work, void *stream);
 
 /* Specular prefilter operators S_l (l = 1..L-1) as a sparse matrix, built
  * once per (He, We, L, samples) instead of regenerating 128 GGX samples per
@@ -301,15 +362,11 @@ int ss_env_adjoint(int he, int we, int levels, int samples, const float *base,
  * identity entry.  ss_spec_op_count -> row_nnz ((L-1)*T int32), the caller
  * scans it into row_ptr ((L-1)*T+1 int64), ss_spec_op_fill -> col (int32),
  * val (float).  The caller builds the per-level transpose (CSC: col_ptr over
- * (l-1)*T + j, row, val) with a stable sort and registers both with
- * ss_spec_op_register; ss_env_refresh / ss_env_adjoint then use them (row-
- * gather SpMV and column-gather transpose, no atomics).  ss_spec_apply /
- * ss_spec_apply_t expose the two products directly. */
+ * (l-1)*T + j, row, val) with a stable sort and passes both in SsEnvOps.
+ * ss_spec_apply / ss_spec_apply_t expose the two products directly. */
 int ss_spec_op_count(int he, int we, int levels, int samples, int32_t *row_nnz, void *stream);
 int ss_spec_op_fill(int he, int we, int levels, int samples, const int64_t *row_ptr, int32_t *col, float *val,
                     void *stream);
-int ss_spec_op_register(int he, int we, int levels, int samples, const int64_t *row_ptr, const int32_t *col,
-                        const float *rval, const int64_t *col_ptr, const int32_t *row, const float *cval);
 int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const float *val,
                   const float *base, float *specular, void *stream);
 int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row, const float *val,
@@ -327,6 +384,14 @@ int ss_adam_step(int64_t count, float *param, const float *grad, float *m, float
 int ss_adam_multi(int ntensors, float *const *params, const float *const *grads, float *const *m,
                   float *const *v, const int64_t *counts, const int *steps, const float *lrs,
                   const int *quat_flags, float beta1, float beta2, float eps, void *stream);
+/* The same two entry points with float64 moments, the reference's state
+ * precision (adam.py:26-28: np.float64 m, v); parameters and gradients stay
+ * float32, the update is float64 in both variants. */
+int ss_adam_step_f64(int64_t count, float *param, const float *grad, double *m, double *v,
+                     int t, float lr, float beta1, float beta2, float eps, void *stream);
+int ss_adam_multi_f64(int ntensors, float *const *params, const float *const *grads, double *const *m,
+                      double *const *v, const int64_t *counts, const int *steps, const float *lrs,
+                      const int *quat_flags, float beta1, float beta2, float eps, void *stream);
 /* q <- q / |q| after the step (train.py:246). */
 int ss_normalize_quats(int n, float *quats, void *stream);
 
@@ -342,6 +407,14 @@ int ss_grid_cells(int n, const float *centers, const float *origin3, float cell,
 int ss_isolation(int n, const float *centers, const float *log_scales, const int32_t *order,
                  const int32_t *sorted_cells, const float *origin3, float cell, int dim,
                  uint8_t *isolated, void *stream);
+/* The same query with the grid kept on the device (no host round trip):
+ * ss_grid_fit writes origin (3 floats), cell, dim (int bits) into `grid`
+ * (16 words of device scratch) from the centres' bounding box and the mean
+ * support; ss_grid_cells_d / ss_isolation_d read it from there. */
+int ss_grid_fit(int n, const float *centers, const float *log_scales, float *grid, void *stream);
+int ss_grid_cells_d(int n, const float *centers, const float *grid, int32_t *cell_of, void *stream);
+int ss_isolation_d(int n, const float *centers, const float *log_scales, const int32_t *order,
+                   const int32_t *sorted_cells, const float *grid, uint8_t *isolated, void *stream);
 /* Split children (densify.py:60-98): parent rows `parents` (nsplit) produce
  * the (+) child at out row plus_row0+k and the (-) child at minus_row0+k;
  * only centres and log-scales differ from the parent (the caller copies the
@@ -349,6 +422,37 @@ int ss_isolation(int n, const float *centers, const float *log_scales, const int
 int ss_split_children(int nsplit, const int32_t *parents, const float *centers, const float *quats,
                       const float *log_scales, float *out_centers, float *out_log_scales,
                       int64_t plus_row0, int64_t minus_row0, void *stream);
+
+/* ---- refinement scan on the device (densify.py:168-202, adam.py:43-58) -----
+ * ss_refine_plan: prune_keep_mask (stale: grad_sum <= 0; isolated: the
+ * ss_isolation flags; floater: front > 0 && outside >= front, votes
+ * nullable together), mean gradient grad_sum / max(view_count, 1),
+ * select_split (threshold max(np.quantile(mean_grad[active], q), floor)
+ * with numpy's 'linear' method; candidates mean_grad >= threshold and
+ * max scale > mean_neighbor_dist) and the budget (the max_surfels - kept
+ * largest mean gradients, ties in index order).  Per row: kind (0 removed,
+ * 1 stay, 2 split) and dst (stay: output row; split: rank among the split
+ * rows: +child at n_stay + rank, -child at n_stay + n_split + rank).
+ * counts (9 int64, device): n_out, kept, split, stale, isolated, floater,
+ * active, candidates, then the threshold's float64 bits.  workspace:
+ * ss_refine_workspace_bytes(n).  No host synchronisation; a fixed launch
+ * sequence (order statistics by an 8-bit radix select on the float64 bits).
+ * ss_refine_apply: the new rows of up to 20 row-major tensors (src[t] n
+ * rows, dst[t] capacity >= n_out rows, row_bytes[t] a multiple of 4) by
+ * role: 0 children copy the parent row, 1 children zero (Adam moments),
+ * 2 centres (children +-(s_max / 2) along the longer tangent axis), 3 log
+ * scales (that axis x 0.7) -- split_cloud (densify.py:60-98); index_map
+ * (capacity int64, nullable): source row of each new row, -1 for children
+ * (workspace: the one ss_refine_plan filled). */
+size_t ss_refine_workspace_bytes(int n);
+int ss_refine_plan(int n, const double *grad_sum, const int64_t *view_count, const uint8_t *isolated,
+                   const int64_t *outside_votes, const int64_t *front_votes, const float *log_scales,
+                   const double *mean_neighbor_dist, int64_t max_surfels, double quantile, double grad_floor,
+                   int32_t *dst, uint8_t *kind, int64_t *counts, void *workspace, void *stream);
+int ss_refine_apply(int n, const uint8_t *kind, const int32_t *dst, const float *centers, const float *quats,
+                    const float *log_scales, int ntensors, const void *const *src, void *const *dst_tensors,
+                    const int *row_bytes, const int *roles, int64_t *index_map, const void *workspace,
+                    void *stream);
 
 /* Diagnostic for the rasterisers' fast coverage test: counts[0] (pixel,
  * in-rect record) evaluations, counts[1] decisions differing from the exact

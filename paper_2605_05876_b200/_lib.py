@@ -19,6 +19,7 @@ SS_OK, SS_ERR_INVALID, SS_ERR_CUDA = 0, 1, 2
 SS_COLOR_EXPLICIT, SS_COLOR_IBL, SS_COLOR_ALBEDO, SS_COLOR_IBL_F32 = 0, 1, 2, 3
 REC_FLOATS = 24
 ACC_FLOATS = 20
+ACC64_WIDTH = 18
 KMAX_CAP = 16
 
 c_p = ctypes.c_void_p
@@ -54,36 +55,47 @@ class SsStacks(ctypes.Structure):
     _fields_ = [("w", c_p), ("c", c_p), ("z", c_p), ("z2", c_p), ("n", c_p)]
 
 
+class SsEnvOps(ctypes.Structure):
+    _fields_ = [("rowsum", c_p), ("khat", c_p), ("row_ptr", c_p), ("col", c_p), ("rval", c_p), ("col_ptr", c_p),
+                ("row", c_p), ("cval", c_p), ("work", c_p)]
+
+
 class SsGrads(ctypes.Structure):
     _fields_ = [("centers", c_p), ("quats", c_p), ("log_scales", c_p), ("albedo_raw", c_p),
                 ("metallic_raw", c_p), ("roughness_raw", c_p), ("colors", c_p), ("ss_grad", c_p),
                 ("touched", c_p), ("d_diffuse", c_p), ("d_specular", c_p), ("d_diffuse4", c_p),
-                ("d_specular4", c_p)]
+                ("d_specular4", c_p), ("view_count", c_p)]
 
 
 _lib = None
 
 _SIGNATURES = {
     "ss_preprocess": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_pack_records": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_int,
+                        ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_bin_sort": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
                     c_p, c_p, c_p, ctypes.c_int64, c_p, c_p, c_p],
     "ss_raster_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
                           ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_raster_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p,
                            ctypes.POINTER(ctypes.c_float), ctypes.c_int, c_p, c_p, ctypes.c_float, c_p, c_p, c_p],
-    "ss_chain_backward": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p],
+    "ss_chain_backward": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_brdf_lut": [ctypes.c_int, ctypes.c_int, c_p, c_p],
-    "ss_env_rowsums": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p],
-    "ss_env_refresh": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
-    "ss_env_adjoint": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
-                       c_p],
+    "ss_env_khat_words": [ctypes.c_int, ctypes.c_int],
+    "ss_env_khat": [ctypes.c_int, ctypes.c_int, c_p, c_p],
+    "ss_env_rowsums": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
+    "ss_env_refresh": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_env_adjoint": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_spec_op_count": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p],
     "ss_spec_op_fill": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
-    "ss_spec_op_register": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_spec_apply": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_spec_apply_t": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_adam_step": [ctypes.c_int64, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_float, ctypes.c_float,
                      ctypes.c_float, ctypes.c_float, c_p],
+    "ss_adam_step_f64": [ctypes.c_int64, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_float, ctypes.c_float,
+                         ctypes.c_float, ctypes.c_float, c_p],
+    "ss_adam_multi_f64": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_float, ctypes.c_float,
+                          ctypes.c_float, c_p],
     "ss_normalize_quats": [ctypes.c_int, c_p, c_p],
     "ss_env_grad_merge": [ctypes.c_int64, c_p, c_p, c_p],
     "ss_adam_multi": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_float, ctypes.c_float,
@@ -99,10 +111,10 @@ _SIGNATURES = {
     "ss_train_coefs_cons": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_double,
                             c_p, c_p],
     "ss_train_backward_records_cons": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
-                                       c_p, c_p, c_p, c_p],
+                                       c_p, c_p, c_p, c_p, c_p],
     "ss_train_backward_scratch_words": [ctypes.c_int, ctypes.c_int, ctypes.c_int],
     "ss_train_backward_records": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
-                                  c_p, c_p, c_p],
+                                  c_p, c_p, c_p, c_p],
     "ss_photometric_workspace": [ctypes.c_int, ctypes.c_int, ctypes.c_int],
     "ss_photometric_loss": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_double, c_p, c_p,
                             c_p, c_p],
@@ -113,6 +125,13 @@ _SIGNATURES = {
                         ctypes.c_int, c_p, c_p, c_p],
     "ss_normal_consistency": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_grid_fit": [ctypes.c_int, c_p, c_p, c_p, c_p],
+    "ss_grid_cells_d": [ctypes.c_int, c_p, c_p, c_p, c_p],
+    "ss_isolation_d": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_refine_workspace_bytes": [ctypes.c_int],
+    "ss_refine_plan": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_double,
+                       ctypes.c_double, c_p, c_p, c_p, c_p, c_p],
+    "ss_refine_apply": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_split_children": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int64, ctypes.c_int64, c_p],
 }
 
@@ -134,6 +153,8 @@ def load(require_cuda=True):
             fn.restype = ctypes.c_int
         lib.ss_photometric_workspace.restype = ctypes.c_size_t
         lib.ss_train_backward_scratch_words.restype = ctypes.c_size_t
+        lib.ss_env_khat_words.restype = ctypes.c_size_t
+        lib.ss_refine_workspace_bytes.restype = ctypes.c_size_t
         lib.ss_last_error.restype = ctypes.c_char_p
         lib.ss_version.restype = ctypes.c_int
         _lib = lib

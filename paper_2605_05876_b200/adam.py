@@ -1,9 +1,11 @@
 """Adam over named device tensors (mirror of surfsplat.adam, adam.py:12-81).
 
-Each step is one fused native kernel (csrc/optim.cu) per parameter tensor:
-moments and the parameter are read and written once.  State is float32 on
-the device (the reference keeps float64 numpy moments); the update itself is
-evaluated in float64 per element.
+Each step is one fused native kernel (csrc/optim.cu) per parameter tensor
+(or one launch for all of them, step_multi): moments and the parameter are
+read and written once.  The moments are float64 by default, like the
+reference's numpy state (adam.py:26-28), so checkpoints carry the same
+dtypes; state_dtype=torch.float32 halves their memory and traffic.  The
+update itself is evaluated in float64 per element either way.
 """
 
 from __future__ import annotations
@@ -15,8 +17,11 @@ from . import _lib
 
 
 class Adam:
-    def __init__(self, beta1=0.9, beta2=0.999, eps=1e-15):
+    def __init__(self, beta1=0.9, beta2=0.999, eps=1e-15, state_dtype=torch.float64):
+        if state_dtype not in (torch.float64, torch.float32):
+            raise ValueError("state_dtype must be torch.float64 or torch.float32")
         self.beta1, self.beta2, self.eps = float(beta1), float(beta2), float(eps)
+        self.state_dtype = state_dtype
         self.m: dict[str, torch.Tensor] = {}
         self.v: dict[str, torch.Tensor] = {}
         self.t: dict[str, int] = {}
@@ -24,18 +29,23 @@ class Adam:
     def step(self, name, param, grad, lr):
         if tuple(grad.shape) != tuple(param.shape):
             raise ValueError(f"gradient shape {tuple(grad.shape)} != param shape {tuple(param.shape)}")
-        if name not in self.m:
-            self.m[name] = torch.zeros_like(param, dtype=torch.float32)
-            self.v[name] = torch.zeros_like(param, dtype=torch.float32)
-            self.t[name] = 0
+        self._init_state(name, param)
         self.t[name] += 1
         g = grad.to(torch.float32).contiguous()
         lib = _lib.load()
-        rc = lib.ss_adam_step(param.numel(), _lib.ptr(param), _lib.ptr(g), _lib.ptr(self.m[name]),
-                              _lib.ptr(self.v[name]), self.t[name], float(lr), self.beta1, self.beta2, self.eps,
-                              _lib.stream_ptr())
+        fn = lib.ss_adam_step_f64 if self.state_dtype == torch.float64 else lib.ss_adam_step
+        rc = fn(param.numel(), _lib.ptr(param), _lib.ptr(g), _lib.ptr(self.m[name]), _lib.ptr(self.v[name]),
+                self.t[name], float(lr), self.beta1, self.beta2, self.eps, _lib.stream_ptr())
         _lib.check(rc, "ss_adam_step")
         return param
+
+    def _init_state(self, name, param):
+        if name not in self.m:
+            self.m[name] = torch.zeros_like(param, dtype=self.state_dtype)
+            self.v[name] = torch.zeros_like(param, dtype=self.state_dtype)
+            self.t[name] = 0
+        elif self.m[name].dtype != self.state_dtype:
+            raise ValueError(f"optimizer state {name!r} is {self.m[name].dtype}, not {self.state_dtype}")
 
     def step_multi(self, items, renorm_quats=None):
         """Adam on several tensors in ONE fused launch (csrc/optim.cu
@@ -50,10 +60,7 @@ class Adam:
         for name, param, grad, lr in items:
             if tuple(grad.shape) != tuple(param.shape):
                 raise ValueError(f"gradient shape {tuple(grad.shape)} != param shape {tuple(param.shape)}")
-            if name not in self.m:
-                self.m[name] = torch.zeros_like(param, dtype=torch.float32)
-                self.v[name] = torch.zeros_like(param, dtype=torch.float32)
-                self.t[name] = 0
+            self._init_state(name, param)
             self.t[name] += 1
             g = grad.to(torch.float32).contiguous()
             keep.append(g)
@@ -64,9 +71,10 @@ class Adam:
         k = len(items)
         ptrs = {c: (ctypes.c_void_p * k)(*cols[c]) for c in ("p", "g", "m", "v")}
         lib = _lib.load()
-        rc = lib.ss_adam_multi(k, ptrs["p"], ptrs["g"], ptrs["m"], ptrs["v"], (ctypes.c_int64 * k)(*cols["n"]),
-                               (ctypes.c_int * k)(*cols["t"]), (ctypes.c_float * k)(*cols["lr"]),
-                               (ctypes.c_int * k)(*cols["q"]), self.beta1, self.beta2, self.eps, _lib.stream_ptr())
+        fn = lib.ss_adam_multi_f64 if self.state_dtype == torch.float64 else lib.ss_adam_multi
+        rc = fn(k, ptrs["p"], ptrs["g"], ptrs["m"], ptrs["v"], (ctypes.c_int64 * k)(*cols["n"]),
+                (ctypes.c_int * k)(*cols["t"]), (ctypes.c_float * k)(*cols["lr"]), (ctypes.c_int * k)(*cols["q"]),
+                self.beta1, self.beta2, self.eps, _lib.stream_ptr())
         _lib.check(rc, "ss_adam_multi")
         return [it[1] for it in items]
 
@@ -101,7 +109,8 @@ def _load_state(self, arrays):
     for key, val in arrays.items():
         for pre, store in (("adam_m_", self.m), ("adam_v_", self.v)):
             if key.startswith(pre):
-                store[key[len(pre):]] = torch.as_tensor(np.asarray(val), device="cuda", dtype=torch.float32).contiguous()
+                store[key[len(pre):]] = torch.as_tensor(np.asarray(val), device="cuda",
+                                                        dtype=self.state_dtype).contiguous()
         if key.startswith("adam_t_"):
             self.t[key[len("adam_t_"):]] = int(val)
     if set(self.m) != set(self.v) or set(self.m) != set(self.t):

@@ -55,7 +55,7 @@ def grads_struct(g, d_diffuse=None, d_specular=None, d_diffuse4=None, d_specular
                         _lib.ptr(d_diffuse), _lib.ptr(d_specular), _lib.ptr(d_diffuse4), _lib.ptr(d_specular4))
 
 
-def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp, cons_scale=0.0, cons=None):
+def _record_backward(lib, result, g_rgb, g_alpha, acc, acc64, bgp, cons_scale=0.0, cons=None):
     """The walk-free backward of the training step for an API render: the
     deferred-loss forward re-derives the per-pixel layer sums and closing
     depths, ss_train_coefs turns them into the layer coefficients for (g_rgb,
@@ -67,7 +67,7 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp, cons_scale=0.0, cons
     dev = st.records.device
     H, W, K = int(cam.height), int(cam.width), int(opt.k_max)
     f32 = dict(device=dev, dtype=torch.float32)
-    coef = torch.empty((K, H * W, 4), **f32)
+    coef = torch.empty(5 * K * H * W, **f32)  # float4 planes + the A-lo plane
     thr = torch.empty((K, H * W), **f32)
     hdr = torch.empty((H * W, 8), device=dev, dtype=torch.int32)
     rgb = torch.empty((H, W, 3), **f32)
@@ -84,8 +84,8 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp, cons_scale=0.0, cons
                                            _lib.stream_ptr()), "ss_train_coefs_cons")
         _lib.check(lib.ss_train_backward_records_cons(n, _lib.ptr(st.cull), _lib.ptr(st.records), W, H, K,
                                                       _lib.ptr(coef), _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(zst),
-                                                      _lib.ptr(scratch), _lib.ptr(acc), _lib.stream_ptr()),
-                   "ss_train_backward_records_cons")
+                                                      _lib.ptr(scratch), _lib.ptr(acc), _lib.ptr(acc64),
+                                                      _lib.stream_ptr()), "ss_train_backward_records_cons")
         return
     _lib.check(lib.ss_train_forward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
                                     _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, K, None, _lib.ptr(coef),
@@ -95,7 +95,7 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, bgp, cons_scale=0.0, cons
                                   _lib.stream_ptr()), "ss_train_coefs")
     _lib.check(lib.ss_train_backward_records(n, _lib.ptr(st.cull), _lib.ptr(st.records), W, H, K, _lib.ptr(coef),
                                              _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(scratch), _lib.ptr(acc),
-                                             _lib.stream_ptr()), "ss_train_backward_records")
+                                             _lib.ptr(acc64), _lib.stream_ptr()), "ss_train_backward_records")
 
 
 def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0, path="records") -> BackwardResult:
@@ -119,12 +119,14 @@ def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0, path
     g_rgb = g_rgb.to(torch.float32).contiguous()
     ga = None if g_alpha is None else torch.as_tensor(g_alpha, device=dev).to(torch.float32).contiguous()
     acc = torch.zeros((n, _lib.ACC_FLOATS), device=dev, dtype=torch.float32)
+    acc64 = None
     cons = torch.zeros(1, device=dev, dtype=torch.float64)
     bgp, _keep = _lib.fvec(opt.background)
     if not float(cons_scale) >= 0.0:
         raise ValueError("cons_scale must be >= 0")
     if path == "records":
-        _record_backward(lib, result, g_rgb, ga, acc, bgp, cons_scale, cons)
+        acc64 = torch.empty((n, _lib.ACC64_WIDTH), device=dev, dtype=torch.float64)
+        _record_backward(lib, result, g_rgb, ga, acc, acc64, bgp, cons_scale, cons)
     else:
         rc = lib.ss_raster_backward(W, H, int(opt.tile), _lib.ptr(result.tile_offsets32), _lib.ptr(result.pair_src),
                                     _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, int(opt.k_max), _lib.ptr(g_rgb),
@@ -148,7 +150,7 @@ def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0, path
     gs = grads_struct(g, d_diff, d_spec, d_diff4, d_spec4)
     rc = lib.ss_chain_backward(ctypes.byref(cl), ctypes.byref(camst), ctypes.byref(po), source,
                                ctypes.byref(envs) if envs is not None else None, _lib.ptr(st.cull), _lib.ptr(acc),
-                               ctypes.byref(gs), _lib.stream_ptr())
+                               _lib.ptr(acc64), ctypes.byref(gs), _lib.stream_ptr())
     _lib.check(rc, "ss_chain_backward")
     g_env = None
     if ibl:

@@ -16,7 +16,7 @@ LIB = os.path.join(OUT_DIR, "libss_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "raster_fwd.cu", "raster_bwd.cu", "chain_bwd.cu",
-           "env.cu", "optim.cu", "train_step.cu", "losses.cu", "knn.cu"]
+           "env.cu", "optim.cu", "train_step.cu", "losses.cu", "knn.cu", "refine.cu"]
 # preprocess mirrors numpy float32 expression by expression: no contraction
 NO_FMAD = {"preprocess.cu"}
 
@@ -38,8 +38,25 @@ def _compile(src, verbose=False):
     return obj, r.stderr
 
 
+STAMP = LIB + ".flags"
+
+
+def _flag_key():
+    """What the .so was built with: the base flags plus the experiment
+    switches (SS_NVCC_FLAGS).  Stored next to the library; a differing key
+    forces a rebuild, so a variant build (e.g. -DSS_UNIFORM_BOUNDS from a
+    tools/ script) is never shipped by a later default build()."""
+    return " ".join(BASE_FLAGS + os.environ.get("SS_NVCC_FLAGS", "").split())
+
+
 def _stale():
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(STAMP) as f:
+            if f.read() != _flag_key():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "ss_abi.h")]
@@ -61,6 +78,8 @@ def build(force=False, verbose=False):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
+    with open(STAMP, "w") as f:
+        f.write(_flag_key())
     return LIB
 
 

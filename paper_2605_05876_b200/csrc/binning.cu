@@ -66,7 +66,10 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
         __syncthreads();
         int excl = carry + (wid > 0 ? warp_sums[wid - 1] : 0) + x - v;
         if (t < ntiles) {
-            offsets[t] = excl;
+            // clamped to the capacity: on overflow every consumer of the
+            // offsets (scatter, tile sort, rasterisers) stays inside the pair
+            // buffers; the dropped pairs are reported by flags[2]/[3]
+            offsets[t] = (int64_t)excl < capacity ? excl : (int32_t)capacity;
             cursors[t] = 0;
         }
         __syncthreads();
@@ -74,8 +77,9 @@ __global__ void __launch_bounds__(kScanThreads) tile_scan_kernel(
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        offsets[ntiles] = carry;
+        offsets[ntiles] = (int64_t)carry < capacity ? carry : (int32_t)capacity;
         if ((int64_t)carry > capacity) atomicOr(&flags[2], 1);
+        atomicMax(&flags[3], carry);  // pairs the view needs (max over the views sharing these flags)
     }
 }
 
@@ -299,12 +303,7 @@ extern "C" int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, i
     if (width <= 0 || height <= 0 || tile <= 0 || !tile_counts || !tile_offsets || !cursors || !flags)
         return SS_ERR_INVALID;
     if (width > 65535 || height > 65535) return SS_ERR_INVALID;  // rects are packed as uint16
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(tile_sort_kernel<kHeavyThreads, kHeavyCap, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kHeavyCap * (int)sizeof(uint64_t));
-        attr_set = true;
-    }
+    ss_func_smem((const void *)tile_sort_kernel<kHeavyThreads, kHeavyCap, true>, 2 * kHeavyCap * (int)sizeof(uint64_t));
     cudaStream_t st = (cudaStream_t)stream;
     const int ntx = (width + tile - 1) / tile, nty = (height + tile - 1) / tile;
     const int ntiles = ntx * nty;
@@ -314,7 +313,7 @@ extern "C" int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, i
     if (n > 0) {
         const size_t smem = 2 * (size_t)ntiles * sizeof(int32_t);
         if (smem > 220 * 1024) return SS_ERR_INVALID;  // > 28k tiles: not supported by the privatised scatter
-        cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        ss_func_smem((const void *)scatter_kernel, (int)smem);
         const int per_cta = kScatterThreads * kScatterPerThread;
         scatter_kernel<<<(n + per_cta - 1) / per_cta, kScatterThreads, smem, st>>>(
             n, reinterpret_cast<const uint4 *>(bininfo), cull, ntx, ntiles, tile, tile_offsets, cursors, keys,

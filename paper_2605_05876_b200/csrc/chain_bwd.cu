@@ -21,6 +21,7 @@ struct ChainParams {
     SsEnv env;
     const int8_t *cull;
     const float *acc;
+    const double *acc64;  // float64 rows of the big records (SS_ACC_F64)
     SsGrads g;
 };
 
@@ -130,7 +131,7 @@ __global__ void env_merge_kernel(int64_t texels, float4 *__restrict__ src, doubl
     }
 }
 
-__global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
+__global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.cloud.n || P.cull[i] != 0) return;
@@ -141,19 +142,29 @@ __global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
     const float4 a3 = reinterpret_cast<const float4 *>(a)[3];
     const float4 a4 = reinterpret_cast<const float4 *>(a)[4];
     double G1[3] = {a0.x, a0.y, a0.z}, G2[3] = {a0.w, a1.x, a1.y}, G4[3] = {a1.z, a1.w, a2.x};
-    const double gs0 = a2.y, gs1 = a2.z, gs2 = a2.w, gnf = a3.x;
-    const double gcol[3] = {a3.y, a3.z, a3.w};
-    const double gz = a4.x;
+    double gs0 = a2.y, gs1 = a2.z, gs2 = a2.w, gnf = a3.x;
+    double gcol[3] = {a3.y, a3.z, a3.w};
+    double gz = a4.x;
     const float ss = a4.y;
     const int touch = __float_as_int(a4.z);
+    if (a4.w == SS_ACC_F64 && P.acc64) {  // a big record: its float64 channels (T-row layout)
+        const double *r = P.acc64 + (size_t)__float_as_int(a0.x) * SS_ACC64_WIDTH;
+        for (int c = 0; c < 3; ++c) { G1[c] = r[c]; G2[c] = r[3 + c]; G4[c] = r[6 + c]; gcol[c] = r[13 + c]; }
+        gs0 = r[9]; gs1 = r[10]; gs2 = r[11]; gnf = r[12]; gz = r[17];
+    }
 
     float t1f[3], t2f[3], t4f[3];
     rows_of(P, i, t1f, t2f, t4f);
     if (a4.w == SS_ACC_MOMENTS) {
-        // moments of the ray-plane gradient (train_step.cu item_grad): with
-        // k = x t4 - t1, l = y t4 - t2,  sum l x gp = t4 x Sy - t2 x S,
-        // sum gp x k = Sx x t4 - S x t1, sum x (l x gp) + y (gp x k) = t1 x Sy - t2 x Sx
-        const double S[3] = {G1[0], G1[1], G1[2]}, Sx[3] = {G2[0], G2[1], G2[2]}, Sy[3] = {G4[0], G4[1], G4[2]};
+        // moments of the ray-plane gradient (train_step.cu item_grad) about
+        // the projected centre (cx, cy): Sx = Sx' + cx S, Sy = Sy' + cy S in
+        // float64; then with k = x t4 - t1, l = y t4 - t2:  sum l x gp =
+        // t4 x Sy - t2 x S, sum gp x k = Sx x t4 - S x t1,
+        // sum x (l x gp) + y (gp x k) = t1 x Sy - t2 x Sx
+        const double cx = fd(t1f[2], t4f[2]), cy = fd(t2f[2], t4f[2]);  // bit-identical to the record kernel's
+        const double S[3] = {G1[0], G1[1], G1[2]};
+        const double Sx[3] = {G2[0] + cx * S[0], G2[1] + cx * S[1], G2[2] + cx * S[2]};
+        const double Sy[3] = {G4[0] + cy * S[0], G4[1] + cy * S[1], G4[2] + cy * S[2]};
         const double T1[3] = {t1f[0], t1f[1], t1f[2]}, T2[3] = {t2f[0], t2f[1], t2f[2]};
         const double T4[3] = {t4f[0], t4f[1], t4f[2]};
 #pragma unroll
@@ -222,57 +233,61 @@ __global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
             G4[2] -= gcy * cy * id4;
         }
     }
-    // T rows -> camera -> world (backward.py:405-441) and the frame
-    // adjoint in float32 (linear maps; the 1e-3 gradient bar), which keeps
-    // the kernel's register footprint down -- the MIP chain above stays float64
-    const float *pm = P.projf;
-    float gtu[3], gtv[3], gcc[3];
-    const float G1f[3] = {(float)G1[0], (float)G1[1], (float)G1[2]};
-    const float G2f[3] = {(float)G2[0], (float)G2[1], (float)G2[2]};
-    const float G4f[3] = {(float)G4[0], (float)G4[1], (float)G4[2]};
+    // T rows -> camera -> world (backward.py:405-441) and the frame adjoint
+    // in float64 with the float64 camera like the reference: a grazing
+    // splat's row gradients are large and cancel in these linear maps
+    // (float32 lost ~1% of its log-scale gradients)
+    const double *pm = P.proj;
+    double gtu[3], gtv[3], gcc[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        gtu[c] = G1f[0] * pm[c] + G2f[0] * pm[4 + c] + G4f[0] * pm[12 + c];
-        gtv[c] = G1f[1] * pm[c] + G2f[1] * pm[4 + c] + G4f[1] * pm[12 + c];
-        gcc[c] = G1f[2] * pm[c] + G2f[2] * pm[4 + c] + G4f[2] * pm[12 + c];
+        gtu[c] = G1[0] * pm[c] + G2[0] * pm[4 + c] + G4[0] * pm[12 + c];
+        gtv[c] = G1[1] * pm[c] + G2[1] * pm[4 + c] + G4[1] * pm[12 + c];
+        gcc[c] = G1[2] * pm[c] + G2[2] * pm[4 + c] + G4[2] * pm[12 + c];
     }
-    gcc[2] -= (float)gz;
-    float gw[3], guw[3], gvw[3];
+    gcc[2] -= gz;
+    double gw[3], guw[3], gvw[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        gw[k] = (gcc[0] * P.viewf[k] + gcc[1] * P.viewf[4 + k]) + gcc[2] * P.viewf[8 + k];
-        guw[k] = (gtu[0] * P.viewf[k] + gtu[1] * P.viewf[4 + k]) + gtu[2] * P.viewf[8 + k];
-        gvw[k] = (gtv[0] * P.viewf[k] + gtv[1] * P.viewf[4 + k]) + gtv[2] * P.viewf[8 + k];
+        gw[k] = (gcc[0] * P.view[k] + gcc[1] * P.view[4 + k]) + gcc[2] * P.view[8 + k];
+        guw[k] = (gtu[0] * P.view[k] + gtu[1] * P.view[4 + k]) + gtu[2] * P.view[8 + k];
+        gvw[k] = (gtv[0] * P.view[k] + gtv[1] * P.view[4 + k]) + gtv[2] * P.view[8 + k];
     }
     const SsCloud &cl = P.cloud;
     const float4 qv = reinterpret_cast<const float4 *>(cl.quats)[i];
-    const float qn = sqrtf(((qv.x * qv.x + qv.y * qv.y) + qv.z * qv.z) + qv.w * qv.w);
-    const float iqn = 1.f / qn;
-    const float w = qv.x * iqn, x = qv.y * iqn, y = qv.z * iqn, z = qv.w * iqn;
-    const float uh[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
-    const float vh[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
+    const double qn = sqrt((((double)qv.x * qv.x + (double)qv.y * qv.y) + (double)qv.z * qv.z) + (double)qv.w * qv.w);
+    const double iqn = 1.0 / qn;
+    const double w = qv.x * iqn, x = qv.y * iqn, y = qv.z * iqn, z = qv.w * iqn;
+    const double uh[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
+    const double vh[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
     const float2 lsv = reinterpret_cast<const float2 *>(cl.log_scales)[i];
-    const float su = __expf(lsv.x), sv = __expf(lsv.y);
-    const float gsu = (guw[0] * uh[0] + guw[1] * uh[1]) + guw[2] * uh[2];
-    const float gsv = (gvw[0] * vh[0] + gvw[1] * vh[1]) + gvw[2] * vh[2];
-    float gU[3], gV[3], gN[3] = {0.f, 0.f, 0.f};
+    const double su = exp((double)lsv.x), sv = exp((double)lsv.y);
+    const double gsu = (guw[0] * uh[0] + guw[1] * uh[1]) + guw[2] * uh[2];
+    const double gsv = (gvw[0] * vh[0] + gvw[1] * vh[1]) + gvw[2] * vh[2];
+    double gU[3], gV[3], gN[3] = {0.0, 0.0, 0.0};
     for (int k = 0; k < 3; ++k) { gU[k] = su * guw[k]; gV[k] = sv * gvw[k]; }
-    float gcent[3] = {gw[0], gw[1], gw[2]};
+    double gcent[3] = {gw[0], gw[1], gw[2]};
     float galb[3] = {0.f, 0.f, 0.f}, gmet = 0.f, grough = 0.f;
 
     if (P.color_source == SS_COLOR_IBL) {
-        // float32 shading adjoint (the forward colours are float64 in the
-        // preprocess kernel; gradients only need the 1e-3 parity bar)
+        // the forward state in float64 like the preprocess kernel's colours
+        // (identical texel cells / level / clip branches as the forward and
+        // the reference's shading_ctx), the adjoint arithmetic in float32
+        // (gradients: the 1e-3 parity bar)
         ShadeIn<float> in;
-        ss_shade_inputs(cl, i, P.cam_pos, in);
         ShadeState<float> st;
-        float col[3];
-        ss_shade_forward(in, P.env, st, col);
+        {
+            ShadeIn<double> in64;
+            ss_shade_inputs(cl, i, P.cam_pos, in64);
+            ShadeState<double> st64;
+            double col[3];
+            ss_shade_forward(in64, P.env, st64, col);
+            ss_shade_narrow(in64, st64, in, st);
+        }
         ShadeGrads<float> sg;
         const float gcf[3] = {(float)gcol[0], (float)gcol[1], (float)gcol[2]};
         ss_shade_backward(in, st, P.env, gcf, sg);
         for (int c = 0; c < 3; ++c) { gcent[c] += sg.center[c]; gN[c] = sg.normal[c]; galb[c] = sg.albedo_raw[c]; }
-        (void)col;
         gmet = sg.metallic_raw;
         grough = sg.roughness_raw;
         // derived-map scatter (bilinear_scatter, shading.py:248-260, 583-597)
@@ -315,27 +330,28 @@ __global__ void __launch_bounds__(128, 5) chain_kernel(ChainParams P)
     }
     // quat_frame_backward (surfels.py:54-77)
 #define D3(g, a0, a1, a2) ((g)[0] * (a0) + (g)[1] * (a1) + (g)[2] * (a2))
-    const float gqw = D3(gU, 0.f, 2 * z, -2 * y) + D3(gV, -2 * z, 0.f, 2 * x) + D3(gN, 2 * y, -2 * x, 0.f);
-    const float gqx = D3(gU, 0.f, 2 * y, 2 * z) + D3(gV, 2 * y, -4 * x, 2 * w) + D3(gN, 2 * z, -2 * w, -4 * x);
-    const float gqy = D3(gU, -4 * y, 2 * x, -2 * w) + D3(gV, 2 * x, 0.f, 2 * z) + D3(gN, 2 * w, 2 * z, -4 * y);
-    const float gqz = D3(gU, -4 * z, 2 * w, 2 * x) + D3(gV, -2 * w, -4 * z, 2 * y) + D3(gN, 2 * x, 2 * y, 0.f);
+    const double gqw = D3(gU, 0.0, 2 * z, -2 * y) + D3(gV, -2 * z, 0.0, 2 * x) + D3(gN, 2 * y, -2 * x, 0.0);
+    const double gqx = D3(gU, 0.0, 2 * y, 2 * z) + D3(gV, 2 * y, -4 * x, 2 * w) + D3(gN, 2 * z, -2 * w, -4 * x);
+    const double gqy = D3(gU, -4 * y, 2 * x, -2 * w) + D3(gV, 2 * x, 0.0, 2 * z) + D3(gN, 2 * w, 2 * z, -4 * y);
+    const double gqz = D3(gU, -4 * z, 2 * w, 2 * x) + D3(gV, -2 * w, -4 * z, 2 * y) + D3(gN, 2 * x, 2 * y, 0.0);
 #undef D3
-    const float radial = ((gqw * w + gqx * x) + gqy * y) + gqz * z;
+    const double radial = ((gqw * w + gqx * x) + gqy * y) + gqz * z;
 
     SsGrads &g = P.g;
     for (int c = 0; c < 3; ++c) {
         red_add(g.centers + 3 * i + c, (float)gcent[c]);
         red_add(g.albedo_raw + 3 * i + c, (float)galb[c]);
     }
-    red_add4(g.quats + 4 * (size_t)i, (gqw - radial * w) * iqn, (gqx - radial * x) * iqn, (gqy - radial * y) * iqn,
-             (gqz - radial * z) * iqn);
-    red_add2(g.log_scales + 2 * (size_t)i, gsu * su, gsv * sv);
+    red_add4(g.quats + 4 * (size_t)i, (float)((gqw - radial * w) * iqn), (float)((gqx - radial * x) * iqn),
+             (float)((gqy - radial * y) * iqn), (float)((gqz - radial * z) * iqn));
+    red_add2(g.log_scales + 2 * (size_t)i, (float)(gsu * su), (float)(gsv * sv));
     red_add(g.metallic_raw + i, (float)gmet);
     red_add(g.roughness_raw + i, (float)grough);
     if (g.colors)
         for (int c = 0; c < 3; ++c) red_add(g.colors + 3 * i + c, (float)gcol[c]);
     red_add(g.ss_grad + i, ss);
-    atomicAdd(g.touched + i, touch);
+    if (g.touched) atomicAdd(g.touched + i, touch);
+    if (g.view_count && touch > 0) red_add(g.view_count + i, 1.f);
 }
 
 }  // namespace
@@ -344,7 +360,7 @@ extern "C" int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void 
 {
     if (texels < 0 || (texels > 0 && (!src4 || !dst))) return SS_ERR_INVALID;
     if (texels == 0) return SS_OK;
-    const int blocks = (int)((texels + 255) / 256 < 148 * 4 ? (texels + 255) / 256 : 148 * 4);
+    const int blocks = (int)((texels + 255) / 256 < ss_sm_count() * 4 ? (texels + 255) / 256 : ss_sm_count() * 4);
     env_merge_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(texels, reinterpret_cast<float4 *>(src4), dst);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
@@ -352,7 +368,7 @@ extern "C" int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void 
 
 extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                                  int color_source, const SsEnv *env, const int8_t *cull,
-                                 const float *rec_acc, const SsGrads *grads, void *stream)
+                                 const float *rec_acc, const double *rec_acc64, const SsGrads *grads, void *stream)
 {
     if (!cloud || !cam || !opt || !grads) return SS_ERR_INVALID;
     if (cloud->n == 0) return SS_OK;
@@ -371,7 +387,7 @@ extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, cons
     P.sigma = (double)opt->mip_sigma;
     P.r_cut = opt->r_cut; P.sigma_f = opt->mip_sigma;
     P.env = env ? *env : SsEnv{};
-    P.cull = cull; P.acc = rec_acc; P.g = *grads;
+    P.cull = cull; P.acc = rec_acc; P.acc64 = rec_acc64; P.g = *grads;
     chain_kernel<<<(cloud->n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;

@@ -173,11 +173,6 @@ __global__ void diffuse_finish_kernel(int he, int we, const double *__restrict__
 // costs O(he^2 we + he we^2) float64 operations instead of the O(he^2 we^2)
 // of the N-body form above (which remains for odd widths).
 
-struct DiffSpectrum {
-    int dev = -1, he = 0, we = 0;
-    double *khat = nullptr;
-};
-DiffSpectrum g_dspec;
 
 __device__ __forceinline__ void twiddles(int we, double *tc, double *ts) {
     for (int m = threadIdx.x; m < we; m += blockDim.x) {
@@ -325,31 +320,20 @@ __global__ void __launch_bounds__(256) dinv_kernel(int he, int we, const double 
     }
 }
 
-const double *diffuse_spectrum(int he, int we, cudaStream_t st) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (g_dspec.khat && g_dspec.dev == dev && g_dspec.he == he && g_dspec.we == we) return g_dspec.khat;
-    if (g_dspec.khat && g_dspec.dev == dev) cudaFree(g_dspec.khat);
-    double *k = nullptr;
-    const size_t n = (size_t)he * he * (we / 2 + 1);
-    if (cudaMalloc(&k, n * sizeof(double)) != cudaSuccess) return nullptr;
-    dspec_kernel<<<he * he, 128, 3 * we * sizeof(double), st>>>(he, we, k);
-    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
-        cudaFree(k);
-        return nullptr;
-    }
-    g_dspec = DiffSpectrum{dev, he, we, k};
-    return k;
+// Spectral form applicable?  (even widths up to 1024: the row tables fit
+// 48 KB of shared memory; K^ of at most 512 MB: 256 x 512 needs 135 MB,
+// larger maps take the N-body form)
+bool spectral_ok(int he, int we) {
+    return (we & 1) == 0 && we <= 1024 && he <= 1024 && (double)he * he * (we / 2 + 1) * 8.0 <= 512.0 * (1 << 20);
 }
 
+// Diffuse quadrature: the spectral form with the caller's K^ when given
+// (ss_env_khat), else the N-body form.
 template <int MODE, typename TIn, typename TOut>
-int run_diffuse(int he, int we, const TIn *x, const float *rowsum, TOut *out, double *work, cudaStream_t st) {
+int run_diffuse(int he, int we, const TIn *x, const float *rowsum, TOut *out, double *work, const double *khat,
+                cudaStream_t st) {
     const int T = he * we;
-    // spectral form (even widths up to 1024: the row tables fit 48 KB of shared memory)
-    // (and K^ of at most 512 MB: 256 x 512 needs 135 MB, larger maps take the N-body form)
-    if ((we & 1) == 0 && we <= 1024 && he <= 1024 && (double)he * he * (we / 2 + 1) * 8.0 <= 512.0 * (1 << 20)) {
-        const double *khat = diffuse_spectrum(he, we, st);
-        if (!khat) return SS_ERR_CUDA;
+    if (khat && spectral_ok(he, we)) {
         const int nk = we / 2 + 1;
         drow_dft_kernel<MODE, TIn><<<he, 256, (2 + (MODE == 0 ? 1 : 3)) * we * sizeof(double), st>>>(he, we, x, rowsum,
                                                                                                       work);
@@ -607,9 +591,9 @@ extern "C" int ss_brdf_lut(int res, int samples, float *lut, void *stream) {
     return SS_OK;
 }
 
-extern "C" int ss_env_rowsums(int he, int we, float *rowsum, double *work, void *stream) {
+extern "C" int ss_env_rowsums(int he, int we, const double *khat, float *rowsum, double *work, void *stream) {
     if (he < 2 || we < 2 || !rowsum || !work) return SS_ERR_INVALID;
-    return run_diffuse<0, float, float>(he, we, nullptr, nullptr, rowsum, work, (cudaStream_t)stream);
+    return run_diffuse<0, float, float>(he, we, nullptr, nullptr, rowsum, work, khat, (cudaStream_t)stream);
 }
 
 extern "C" int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const float *val,
@@ -617,64 +601,56 @@ extern "C" int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr,
 extern "C" int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row,
                                const float *val, const double *d_specular, double *d_base, void *stream);
 
-// Registered sparse specular operator (device buffers owned by the caller).
-namespace {
-struct SpecOp {
-    int he = 0, we = 0, levels = 0, samples = 0;
-    const int64_t *row_ptr = nullptr; const int32_t *col = nullptr; const float *rval = nullptr;
-    const int64_t *col_ptr = nullptr; const int32_t *row = nullptr; const float *cval = nullptr;
-};
-SpecOp g_spec_op;
-}  // namespace
+extern "C" size_t ss_env_khat_words(int he, int we) {
+    if (he < 2 || we < 2 || !spectral_ok(he, we)) return 0;
+    return (size_t)he * he * (we / 2 + 1);
+}
 
-extern "C" int ss_spec_op_register(int he, int we, int levels, int samples, const int64_t *row_ptr, const int32_t *col,
-                                   const float *rval, const int64_t *col_ptr, const int32_t *row, const float *cval) {
-    g_spec_op = SpecOp{he, we, levels, samples, row_ptr, col, rval, col_ptr, row, cval};
+extern "C" int ss_env_khat(int he, int we, double *khat, void *stream) {
+    if (!khat || ss_env_khat_words(he, we) == 0) return SS_ERR_INVALID;
+    dspec_kernel<<<he * he, 128, 3 * we * sizeof(double), (cudaStream_t)stream>>>(he, we, khat);
+    SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
 
-extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log,
-                              const float *rowsum, float *base, float *diffuse, float *specular, double *work,
-                              void *stream) {
-    if (he < 2 || we < 2 || levels < 1 || !base_log || !rowsum || !base || !diffuse || !specular || !work)
+extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log, const SsEnvOps *ops,
+                              float *base, float *diffuse, float *specular, void *stream) {
+    if (he < 2 || we < 2 || levels < 1 || !base_log || !ops || !ops->rowsum || !ops->work || !base || !diffuse ||
+        !specular)
         return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int T = he * we;
     exp_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular);
     SS_CUDA_CHECK_LAUNCH();
     {
-        const int rc = run_diffuse<1, float, float>(he, we, base, rowsum, diffuse, work, st);
+        const int rc = run_diffuse<1, float, float>(he, we, base, ops->rowsum, diffuse, ops->work, ops->khat, st);
         if (rc != SS_OK) return rc;
     }
     if (levels > 1) {
-        if (g_spec_op.row_ptr && g_spec_op.he == he && g_spec_op.we == we && g_spec_op.levels == levels &&
-            g_spec_op.samples == samples) {
-            return ss_spec_apply(he, we, levels, g_spec_op.row_ptr, g_spec_op.col, g_spec_op.rval, base, specular, stream);
-        }
+        if (ops->row_ptr && ops->col && ops->rval)
+            return ss_spec_apply(he, we, levels, ops->row_ptr, ops->col, ops->rval, base, specular, stream);
         spec_refresh_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, base, specular);
         SS_CUDA_CHECK_LAUNCH();
     }
     return SS_OK;
 }
 
-extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, const float *rowsum,
+extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, const SsEnvOps *ops,
                               const double *d_diffuse, const double *d_specular, double *d_base, float *d_base_log,
-                              double *work, void *stream) {
-    if (he < 2 || we < 2 || levels < 1 || !base || !rowsum || !d_diffuse || !d_specular || !d_base || !d_base_log ||
-        !work)
+                              void *stream) {
+    if (he < 2 || we < 2 || levels < 1 || !base || !ops || !ops->rowsum || !ops->work || !d_diffuse || !d_specular ||
+        !d_base || !d_base_log)
         return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int T = he * we;
     cudaMemsetAsync(d_base, 0, sizeof(double) * 3 * T, st);
     {
-        const int rc = run_diffuse<2, double, double>(he, we, d_diffuse, rowsum, d_base, work, st);
+        const int rc = run_diffuse<2, double, double>(he, we, d_diffuse, ops->rowsum, d_base, ops->work, ops->khat, st);
         if (rc != SS_OK) return rc;
     }
     if (levels > 1) {
-        if (g_spec_op.col_ptr && g_spec_op.he == he && g_spec_op.we == we && g_spec_op.levels == levels &&
-            g_spec_op.samples == samples) {
-            const int rc = ss_spec_apply_t(he, we, levels, g_spec_op.col_ptr, g_spec_op.row, g_spec_op.cval, d_specular,
-                                           d_base, stream);
+        if (ops->col_ptr && ops->row && ops->cval) {
+            const int rc = ss_spec_apply_t(he, we, levels, ops->col_ptr, ops->row, ops->cval, d_specular, d_base, stream);
             if (rc != SS_OK) return rc;
         } else {
             spec_adjoint_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, d_specular,

@@ -229,7 +229,7 @@ __global__ void sil_grad_kernel(int64_t n, const float *mask, const double *sums
     }
 }
 
-int grid_for(int64_t n) { return (int)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8); }
+int grid_for(int64_t n) { return (int)((n + 255) / 256 < ss_sm_count() * 8 ? (n + 255) / 256 : ss_sm_count() * 8); }
 
 }  // namespace
 

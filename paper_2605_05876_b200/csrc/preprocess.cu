@@ -226,7 +226,65 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
     if (aux.colors) { aux.colors[3 * i] = col[0]; aux.colors[3 * i + 1] = col[1]; aux.colors[3 * i + 2] = col[2]; }
 }
 
+// Records from a compacted ProjectedSurfels (render(proj=...) reuse and
+// bin_and_sort(proj)): row k of the projection -> record source_index[k]
+// (or k), with the same fields, certified margin, bin info and tile counts
+// the preprocess kernel writes for a kept surfel.
+__global__ void pack_kernel(int k, const float *__restrict__ t1, const float *__restrict__ t2,
+                            const float *__restrict__ t4, const float *__restrict__ sinv, const float *__restrict__ n_f,
+                            const float *__restrict__ view_z, const float *__restrict__ eps_z,
+                            const int32_t *__restrict__ rect, const int32_t *__restrict__ source_index,
+                            const float *__restrict__ colors, int W, int H, int tile, SsRecord *__restrict__ records,
+                            uint4 *__restrict__ bininfo, int32_t *__restrict__ tile_counts)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    const int i = source_index ? source_index[j] : j;
+    const float a1[3] = {t1[3 * j], t1[3 * j + 1], t1[3 * j + 2]};
+    const float a2[3] = {t2[3 * j], t2[3 * j + 1], t2[3 * j + 2]};
+    const float a4[3] = {t4[3 * j], t4[3 * j + 1], t4[3 * j + 2]};
+    const float m00 = sinv[3 * j], m01 = sinv[3 * j + 1], m11 = sinv[3 * j + 2];
+    const float vz = view_z[j], ez = eps_z[j];
+    const float zs = vz - ez, ze = vz + ez;  // ProjectedSurfels.z_start / z_end (preprocess.py:217-223)
+    const int x0 = rect[4 * j], y0 = rect[4 * j + 1], x1 = rect[4 * j + 2], y1 = rect[4 * j + 3];
+    SsRecord rec;
+    rec.a = make_float4(a1[0], a1[1], a1[2], a2[0]);
+    rec.b = make_float4(a2[1], a2[2], a4[0], a4[1]);
+    rec.c = make_float4(a4[2], m00, m01, m11);
+    rec.d = make_float4(n_f[j], vz, zs, ze);
+    const bool alive = x1 > x0 && y1 > y0;
+    const float cm = alive ? coverage_margin(a1, a2, a4, m00, m01, m11, x0, y0, x1, y1, W, H) : 0.f;
+    const float c0 = colors ? colors[3 * i] : 0.f, c1 = colors ? colors[3 * i + 1] : 0.f,
+                c2 = colors ? colors[3 * i + 2] : 0.f;
+    rec.e = make_float4(c0, c1, c2, cm);
+    rec.r = alive ? make_int4(x0, y0, x1, y1) : make_int4(0, 0, 0, 0);
+    records[i] = rec;
+    bininfo[i] = alive ? make_uint4((uint32_t)x0 | ((uint32_t)y0 << 16), (uint32_t)x1 | ((uint32_t)y1 << 16),
+                                    ss_orderable(zs), 0u)
+                       : make_uint4(0u, 0u, 0u, 0u);
+    if (!alive) return;
+    const int ntx = (W + tile - 1) / tile;
+    for (int ty = y0 / tile; ty <= (y1 - 1) / tile; ++ty)
+        for (int tx = x0 / tile; tx <= (x1 - 1) / tile; ++tx) atomicAdd(&tile_counts[ty * ntx + tx], 1);
+}
+
 }  // namespace
+
+extern "C" int ss_pack_records(int k, const float *t1, const float *t2, const float *t4, const float *sinv,
+                               const float *n_f, const float *view_z, const float *eps_z, const int32_t *rect,
+                               const int32_t *source_index, const float *colors, int width, int height, int tile,
+                               float *records, uint32_t *bininfo, int32_t *tile_counts, void *stream)
+{
+    if (k < 0 || width <= 0 || height <= 0 || width > 65535 || height > 65535 || tile <= 0) return SS_ERR_INVALID;
+    if (k == 0) return SS_OK;
+    if (!t1 || !t2 || !t4 || !sinv || !n_f || !view_z || !eps_z || !rect || !records || !bininfo || !tile_counts)
+        return SS_ERR_INVALID;
+    pack_kernel<<<(k + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        k, t1, t2, t4, sinv, n_f, view_z, eps_z, rect, source_index, colors, width, height, tile,
+        reinterpret_cast<SsRecord *>(records), reinterpret_cast<uint4 *>(bininfo), tile_counts);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
 
 extern "C" int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                              int color_source, const float *colors_in, const SsEnv *env,

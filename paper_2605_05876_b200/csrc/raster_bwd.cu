@@ -216,8 +216,9 @@ __global__ void __launch_bounds__(256) raster_bwd_kernel(BwdParams P)
                         v[12] = e * gw;
                         const float u = c.u, vv = c.v;
                         v[9] = gr * u * u; v[10] = gr * 2.f * u * vv; v[11] = gr * vv * vv;
-                        const float gu = 2.f * gr * (R.c.y * u + R.c.z * vv);
-                        const float gv = 2.f * gr * (R.c.z * u + R.c.w * vv);
+                        // float32 sums like numba's (backward.py:292-293)
+                        const float gu = 2.f * gr * fa(fm(R.c.y, u), fm(R.c.z, vv));
+                        const float gv = 2.f * gr * fa(fm(R.c.z, u), fm(R.c.w, vv));
                         const float gp0 = gu * c.inv_den, gp1 = gv * c.inv_den, gp2 = -(gu * u + gv * vv) * c.inv_den;
                         const float gk0 = c.l1 * gp2 - c.l2 * gp1;
                         const float gk1 = c.l2 * gp0 - c.l0 * gp2;

@@ -21,6 +21,7 @@
 // partial sum and, per pixel and layer, the float4 coefficients
 // (A, dL/dC_raw rgb) that the pass-2-only backward kernel consumes, so the
 // backward never replays the walk a second time.
+#include <type_traits>
 #include "ss_common.cuh"
 #include "raster_walk.cuh"
 
@@ -49,6 +50,22 @@ struct FwdParams {
     float4 *zst;           // kCons: (k_max, H*W) per layer (z0, sum w dz, sum w dz^2, 0), dz = view_z - z0
 };
 
+// Layer coefficients of the backward, stored without losing the record-
+// colour cancellation: g_w(c) = A + sum_c G_c c_c with A = g_am (1 - a) -
+// sum_c G_c c_hat_c is a small difference of large terms whenever a record's
+// colour is close to its layer's mean colour c_hat, so A is formed from the
+// ROUNDED G_c (then g_w = g_am (1 - a) + sum_c G_c (c_c - c_hat_c) exactly)
+// and stored as float hi + lo (the lo plane follows the k_max float4 planes
+// in `coef`).  The backward evaluates g_w in float64.
+__device__ __forceinline__ void store_coef(float4 *coef, size_t o, size_t lo_off, double base, double gh0, double gh1,
+                                           double gh2, double inv, double ch0, double ch1, double ch2) {
+    const float g0 = (float)(gh0 * inv), g1 = (float)(gh1 * inv), g2 = (float)(gh2 * inv);
+    const double A = base - ((double)g0 * ch0 + (double)g1 * ch1 + (double)g2 * ch2);
+    const float hi = (float)A;
+    coef[o] = make_float4(hi, g0, g1, g2);
+    reinterpret_cast<float *>(coef + lo_off)[o] = (float)(A - (double)hi);
+}
+
 // CTAs of kFwdWarps warps (a tile is split over tile*tile/32/kFwdWarps
 // CTAs; measured 4 > 2 = 8 > 1 with the heavy-first tile order): warps never
 // wait for each other.
@@ -75,14 +92,19 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     PackedScratch &sm = scratch[wid];
     packed_init(wp, sm, P.W, P.H);
 
-    float Wg = 0.f, C0 = 0.f, C1 = 0.f, C2 = 0.f, Zg = 0.f, Z2g = 0.f, zmax = 0.f;
+    // layer sums: float64 in the training modes (the layer's mean colour
+    // C / W enters the backward through record colour - mean colour, which
+    // float32 sums would blur), float32 for the plain render
+    using AccT = typename std::conditional<kTrain, double, float>::type;
+    AccT Wg = 0, C0 = 0, C1 = 0, C2 = 0;
+    float Zg = 0.f, Z2g = 0.f, zmax = 0.f;
     float T = 1.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, dnum = 0.f, dden = 0.f;
     int layers = 0, members = 0;
     bool stopped = !live;
     unsigned discarded = 0;
     // training: per-layer raw sums for the suffix recursion
     constexpr int KL = kTrain ? SS_KMAX_CAP : 1;
-    float lw[KL], lc0[KL], lc1[KL], lc2[KL];
+    AccT lw[KL], lc0[KL], lc1[KL], lc2[KL];
     int ncl = 0;
     float th0 = 0.f, th1 = 0.f, th2 = 0.f;  // first three closing depths (kTrain)
     float z0 = 0.f, Zs = 0.f, Z2s = 0.f;     // kCons: layer depth moments about the first member
@@ -100,10 +122,10 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     // compositing is replayed (same operations, same order) once per pixel
     // after the walk, off the hot loop
     auto close_layer = [&]() {
-        if (!kTrain) composite(Wg, C0, C1, C2);
+        if (!kTrain) composite((float)Wg, (float)C0, (float)C1, (float)C2);
         if (kExtras && P.st.w) {
             const size_t o = pix * P.k_max + layers;
-            P.st.w[o] = Wg; P.st.c[3 * o] = C0; P.st.c[3 * o + 1] = C1; P.st.c[3 * o + 2] = C2;
+            P.st.w[o] = (float)Wg; P.st.c[3 * o] = (float)C0; P.st.c[3 * o + 1] = (float)C1; P.st.c[3 * o + 2] = (float)C2;
             P.st.z[o] = Zg; P.st.z2[o] = Z2g; P.st.n[o] = members;
         }
         if (kTrain) { lw[layers] = Wg; lc0[layers] = C0; lc1[layers] = C1; lc2[layers] = C2; }
@@ -112,7 +134,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
             Zs = Z2s = 0.f;
         }
         ++layers;
-        Wg = C0 = C1 = C2 = Zg = Z2g = zmax = 0.f;
+        Wg = C0 = C1 = C2 = 0;
+        Zg = Z2g = zmax = 0.f;
         members = 0;
     };
 
@@ -155,8 +178,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
                     Zs += w * dz;
                     Z2s += w * dz * dz;
                 }
-                Wg += w;
-                C0 += w * v.c0; C1 += w * v.c1; C2 += w * v.c2;
+                Wg += (AccT)w;
+                C0 += (AccT)(w * v.c0); C1 += (AccT)(w * v.c1); C2 += (AccT)(w * v.c2);
                 if (!kTrain) { Zg += w * v.vz; Z2g += w * v.vz * v.vz; }
                 ++members;
                 if (v.ze > zmax) zmax = v.ze;
@@ -166,9 +189,9 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     }
     double lsum = 0.0;
     if (live) {
-        if (Wg > 0.f) close_layer();
+        if (Wg > 0) close_layer();
         if (kTrain)
-            for (int m = 0; m < layers; ++m) composite(lw[m], lc0[m], lc1[m], lc2[m]);
+            for (int m = 0; m < layers; ++m) composite((float)lw[m], (float)lc0[m], (float)lc1[m], (float)lc2[m]);
         const float r0 = o0 + T * P.bg0, r1 = o1 + T * P.bg1, r2 = o2 + T * P.bg2;
         if (!kTrain || P.rgb) {
             P.rgb[3 * pix] = r0; P.rgb[3 * pix + 1] = r1; P.rgb[3 * pix + 2] = r2;
@@ -182,7 +205,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
             // once the image-space gradient is known): raw layer sums
             P.hdr[2 * pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
             const size_t HW = (size_t)P.W * P.H;
-            for (int m = 0; m < layers; ++m) P.coef[(size_t)m * HW + pix] = make_float4(lw[m], lc0[m], lc1[m], lc2[m]);
+            for (int m = 0; m < layers; ++m)
+                P.coef[(size_t)m * HW + pix] = make_float4((float)lw[m], (float)lc0[m], (float)lc1[m], (float)lc2[m]);
             if (P.alpha) P.alpha[pix] = 1.f - T;
         } else {
             P.hdr[2 * pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
@@ -212,10 +236,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
                 const double g_am = tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2));
                 const double ta = tb[m] * a;
                 const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
-                float4 cf;
-                cf.x = (float)(g_am * (1.0 - a) - (gh0 * ch0 + gh1 * ch1 + gh2 * ch2) * inv);
-                cf.y = (float)(gh0 * inv); cf.z = (float)(gh1 * inv); cf.w = (float)(gh2 * inv);
-                P.coef[(size_t)m * HW + pix] = cf;
+                store_coef(P.coef, (size_t)m * HW + pix, (size_t)P.k_max * HW, g_am * (1.0 - a), gh0, gh1, gh2, inv,
+                           ch0, ch1, ch2);
                 sf0 = a * ch0 + (1.0 - a) * sf0;
                 sf1 = a * ch1 + (1.0 - a) * sf1;
                 sf2 = a * ch2 + (1.0 - a) * sf2;
@@ -239,7 +261,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 // the per-layer backward coefficients (A, dL/dC_raw) once the image-space
 // gradients g_rgb (and g_alpha) are known -- the suffix recursion of
 // backward.py:201-238 including the coverage term (g_alpha * prod(1 - a)).
-__global__ void __launch_bounds__(256) train_coef_kernel(int HW, const int4 *__restrict__ hdr, float4 *coef,
+__global__ void __launch_bounds__(256) train_coef_kernel(int HW, int k_max, const int4 *__restrict__ hdr, float4 *coef,
                                                          const float *__restrict__ g_rgb,
                                                          const float *__restrict__ g_alpha, float bg0, float bg1,
                                                          float bg2)
@@ -266,8 +288,8 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, const int4 *__r
         const double g_am = tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2) + ga * q);
         const double ta = tb[m] * a[m];
         const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
-        coef[(size_t)m * HW + pix] = make_float4((float)(g_am * (1.0 - a[m]) - (gh0 * ch0 + gh1 * ch1 + gh2 * ch2) * inv),
-                                                 (float)(gh0 * inv), (float)(gh1 * inv), (float)(gh2 * inv));
+        store_coef(coef, (size_t)m * HW + pix, (size_t)k_max * HW, g_am * (1.0 - a[m]), gh0, gh1, gh2, inv, ch0, ch1,
+                   ch2);
         sf0 = a[m] * ch0 + (1.0 - a[m]) * sf0;
         sf1 = a[m] * ch1 + (1.0 - a[m]) * sf1;
         sf2 = a[m] * ch2 + (1.0 - a[m]) * sf2;
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, const int4 *__r
 // zst in place as the per-layer (B, Q, z_bar, var) of the record gradient
 //     g_w += B dz + Q (dz^2 - var),  g_vz = w (B + 2 Q dz),  dz = view_z - z_bar;
 // the penalty value is block-reduced into cons_loss.
-__global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, const int4 *__restrict__ hdr, float4 *coef,
+__global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, int k_max, const int4 *__restrict__ hdr, float4 *coef,
                                                               float4 *zst, const float *__restrict__ g_rgb,
                                                               const float *__restrict__ g_alpha, float bg0,
                                                               float bg1, float bg2, double s, double *cons_loss)
@@ -336,8 +358,8 @@ __global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, const int4
                 tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2) + ga * q + gw_c[m] - rw);
             const double ta = tb[m] * a[m];
             const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
-            coef[(size_t)m * HW + pix] = make_float4((float)(g_am * (1.0 - a[m]) - (gh0 * ch0 + gh1 * ch1 + gh2 * ch2) * inv),
-                                                     (float)(gh0 * inv), (float)(gh1 * inv), (float)(gh2 * inv));
+            store_coef(coef, (size_t)m * HW + pix, (size_t)k_max * HW, g_am * (1.0 - a[m]), gh0, gh1, gh2, inv, ch0,
+                       ch1, ch2);
             zst[(size_t)m * HW + pix] = make_float4((float)(gz_c[m] * inv), (float)(gv_c[m] * inv), (float)zb[m],
                                                     (float)vr[m]);
             sf0 = a[m] * ch0 + (1.0 - a[m]) * sf0;
@@ -455,7 +477,7 @@ extern "C" int ss_train_coefs(int width, int height, int k_max, const int32_t *p
         return SS_ERR_INVALID;
     const int HW = width * height;
     train_coef_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-        HW, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef), g_rgb, g_alpha, background[0],
+        HW, k_max, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef), g_rgb, g_alpha, background[0],
         background[1], background[2]);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
@@ -470,7 +492,7 @@ extern "C" int ss_train_coefs_cons(int width, int height, int k_max, const int32
         return SS_ERR_INVALID;
     const int HW = width * height;
     train_coef_cons_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-        HW, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef),
+        HW, k_max, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef),
         reinterpret_cast<float4 *>(zstats), g_rgb, g_alpha, background[0], background[1], background[2], cons_scale,
         cons_loss);
     SS_CUDA_CHECK_LAUNCH();

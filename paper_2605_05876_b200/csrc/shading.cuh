@@ -248,6 +248,34 @@ __device__ __forceinline__ void ss_shade_forward(const ShadeIn<R> &in, const SsE
     }
 }
 
+// Narrow a float64 forward state to float32: the backward then runs in
+// float32 on EXACTLY the forward's branch decisions (texel cells, roughness
+// level, clip activity), which a float32 recomputation of the forward could
+// flip at a cell boundary -- where the bilinear derivatives jump.
+__device__ __forceinline__ SsBil<float> ss_bil_narrow(const SsBil<double> &b) {
+    SsBil<float> o;
+    o.i0 = b.i0; o.i1 = b.i1; o.j0 = b.j0; o.j1 = b.j1;
+    o.tu = (float)b.tu; o.tv = (float)b.tv; o.du_ok = b.du_ok; o.dv_ok = b.dv_ok;
+    return o;
+}
+__device__ __forceinline__ void ss_shade_narrow(const ShadeIn<double> &a, const ShadeState<double> &s,
+                                                ShadeIn<float> &af, ShadeState<float> &sf) {
+    for (int c = 0; c < 3; ++c) {
+        af.albedo[c] = (float)a.albedo[c]; af.n[c] = (float)a.n[c]; af.wo[c] = (float)a.wo[c];
+        sf.refl[c] = (float)s.refl[c]; sf.l_d[c] = (float)s.l_d[c]; sf.l_s[c] = (float)s.l_s[c];
+        sf.spec_lo[c] = (float)s.spec_lo[c]; sf.spec_hi[c] = (float)s.spec_hi[c];
+        sf.f0[c] = (float)s.f0[c]; sf.k_d[c] = (float)s.k_d[c];
+    }
+    af.m = (float)a.m; af.r = (float)a.r; af.inv_dist = (float)a.inv_dist;
+    sf.ndv_raw = (float)s.ndv_raw; sf.b1 = (float)s.b1; sf.b2 = (float)s.b2; sf.frac = (float)s.frac;
+    // the clip-activity flags follow the float64 ndv (narrowing could move
+    // a value within 1 ulp of 0 or 1 across the bound)
+    if ((s.ndv_raw > 0.0) != (sf.ndv_raw > 0.f)) sf.ndv_raw = s.ndv_raw > 0.0 ? 1e-30f : 0.f;
+    if ((s.ndv_raw < 1.0) != (sf.ndv_raw < 1.f)) sf.ndv_raw = s.ndv_raw < 1.0 ? 0.99999994f : 1.f;
+    sf.lvl0 = s.lvl0; sf.lvl1 = s.lvl1;
+    sf.bd = ss_bil_narrow(s.bd); sf.bs = ss_bil_narrow(s.bs); sf.bl = ss_bil_narrow(s.bl);
+}
+
 // Branch signature cells (shading.py:490-497), 15 ints.
 template <typename R>
 __device__ __forceinline__ void ss_shade_cells(const ShadeState<R> &s, const SsEnv &env, int32_t *out) {

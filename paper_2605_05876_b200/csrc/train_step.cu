@@ -56,12 +56,17 @@ struct SplatParams {
     const int8_t *cull;
     const SsRecord *records;
     const float *xs, *ys;   // pixel-centre NDC per column / row (exact: coverage decisions)
-    const float4 *coef;     // (k_max, HW) per-layer (A, dL/dC_raw)
+    const float4 *coef;     // (k_max, HW) per-layer (A hi, dL/dC_raw)
+    const float *coef_lo;   // (k_max, HW) low part of A (follows the float4 planes)
     const float *thr;       // (k_max, HW) closing depths of layers >= 3
     const int4 *hdr;        // (HW, 2) (closed-layer count, closing depths of layers 0..2), (depths 3..6)
     const float4 *zc;       // kCons: (k_max, HW) per layer (B, Q, z_bar, var) of the consolidation penalty
     float *acc;             // (n, 20)
+    const int32_t *big_list;  // big-record queue (medium from the front, huge from the back)
+    double *big_acc;          // (n, kBigW) float64 sums of the big records, by queue slot
 };
+constexpr int kBigW = SS_ACC64_WIDTH;  // float64 channels per big-record slot (>= NCHC)
+static_assert(kBigW >= 18, "float64 row holds every channel");
 
 constexpr int kHeadWords = 8 + 2 * 64;  // see the scratch layout below
 
@@ -82,20 +87,28 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return r * (2.f - x * r);
 }
 
+// (cx, cy): the record's projected centre (t1.z / t4.z, t2.z / t4.z), the
+// origin of the x and y moments.
 template <bool kCons>
 __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R, int ix, int iy, float x, float y,
-                                         float u, float v, float rho2, float *g) {
+                                         float cx, float cy, float *g) {
     const size_t HW = (size_t)P.W * P.H;
     const size_t pix = (size_t)iy * P.W + ix;
     // the packed header and the (most common) layer-0 coefficients are loaded
     // together, before the geometry below, so their latency hides behind it
     const int4 h = __ldg(P.hdr + 2 * pix);
     const float4 cf0 = __ldg(P.coef + pix);
-    // ray / tangent-plane quantities of the backward (rasterizer.py:197-207)
-    // (gradient arithmetic: contracted FMAs, no reference rounding sequence)
-    const float k0 = fmaf(x, R.b.z, -R.a.x), k1 = fmaf(x, R.b.w, -R.a.y);
-    const float l0 = fmaf(y, R.b.z, -R.a.w), l1 = fmaf(y, R.b.w, -R.b.x);
-    const float inv_den = fast_rcp(fmaf(k0, l1, -k1 * l0));
+    // ray / tangent-plane quantities with the reference's own float32
+    // sequence (rasterizer.py:197-207, bit-identical k, l, den; u, v within
+    // ~2 ulp): the certified fast form decided coverage in pass 1, but its
+    // u, v carry ~1e-4 relative noise at the support edge, which sums into
+    // a systematic bias of the record's gradient
+    const float k0 = fs(fm(x, R.b.z), R.a.x), k1 = fs(fm(x, R.b.w), R.a.y), k2 = fs(fm(x, R.c.x), R.a.z);
+    const float l0 = fs(fm(y, R.b.z), R.a.w), l1 = fs(fm(y, R.b.w), R.b.x), l2 = fs(fm(y, R.c.x), R.b.y);
+    const float inv_den = fc_rcp(fs(fm(k0, l1), fm(k1, l0)));
+    const float u = fs(fm(k1, l2), fm(k2, l1)) * inv_den;
+    const float v = fs(fm(k2, l0), fm(k0, l2)) * inv_den;
+    const float rho2 = (R.c.y * u * u + 2.f * R.c.z * u * v) + R.c.w * v * v;
     const float zs = R.d.z;
     const int nc = h.x & 0xff;  // closed layers (the layer count sits in bits 8+)
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
@@ -113,10 +126,15 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     }
     if (m >= P.k_max) return 0;  // beyond the K_MAX stop: discarded
     const float4 cf = m == 0 ? cf0 : __ldg(P.coef + m * HW + pix);
+    const float cflo = __ldg(P.coef_lo + m * HW + pix);
     float e;  // exp(-rho^2 / 2) by the hardware ex2 (ftz: no range fix-up)
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(rho2 * -0.72134752044448170368f));
     const float w = R.d.x * e;
-    float gw = cf.x + cf.y * R.e.x + cf.z * R.e.y + cf.w * R.e.z;
+    // g_w = A + sum_c G_c colour_c: a small difference of large terms when
+    // the record's colour is near its layer's mean colour (raster_fwd.cu
+    // store_coef) -- float64, exact products of the float factors
+    float gw = (float)(((double)cf.x + (double)cflo) +
+                       (((double)cf.y * R.e.x + (double)cf.z * R.e.y) + (double)cf.w * R.e.z));
     if constexpr (kCons) {  // consolidation penalty (backward.py:272-286, centred depth form)
         const float4 zq = __ldg(P.zc + m * HW + pix);
         const float dz = R.d.y - zq.z;
@@ -127,22 +145,106 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const float gr = -0.5f * w * gw;
     g[12] += e * gw;
     g[9] += gr * u * u; g[10] += gr * 2.f * u * v; g[11] += gr * v * v;
-    const float gu = 2.f * gr * (R.c.y * u + R.c.z * v);
-    const float gv = 2.f * gr * (R.c.z * u + R.c.w * v);
+    // sinv u + sinv v rounded like numba's float32 expression (backward.py:292-293)
+    const float gu = 2.f * gr * fa(fm(R.c.y, u), fm(R.c.z, v));
+    const float gv = 2.f * gr * fa(fm(R.c.z, u), fm(R.c.w, v));
     const float gp0 = gu * inv_den, gp1 = gv * inv_den, gp2 = -(gu * u + gv * v) * inv_den;
     // k = x t4 - t1 and l = y t4 - t2 are linear in the pixel centre, so the
     // per-item dL/dk = l x gp, dL/dl = gp x k and their T-row images sum to
     // cross products of the record's rows with three moments of gp
-    // (sum gp, sum x gp, sum y gp): those 9 channels are accumulated here
-    // and turned into dL/dt1, dt2, dt4 by the chain kernel (SS_ACC_MOMENTS)
+    // (sum gp, sum (x - cx) gp, sum (y - cy) gp): those 9 channels are
+    // accumulated here and turned into dL/dt1, dt2, dt4 by the chain kernel
+    // (SS_ACC_MOMENTS).  The moments are taken about the projected centre,
+    // where k.z and l.z vanish: about the NDC origin, sum y gp ~ cy sum gp
+    // and the float32 sums would lose the O(rect size) part the gradient
+    // lives in (0.3% errors on off-centre splats)
+    const float dx = x - cx, dy = y - cy;
     g[0] += gp0; g[1] += gp1; g[2] += gp2;
-    g[3] += x * gp0; g[4] += x * gp1; g[5] += x * gp2;
-    g[6] += y * gp0; g[7] += y * gp1; g[8] += y * gp2;
+    g[3] += dx * gp0; g[4] += dx * gp1; g[5] += dx * gp2;
+    g[6] += dy * gp0; g[7] += dy * gp1; g[8] += dy * gp2;
     const float gk2 = l0 * gp1 - l1 * gp0;
     const float gl2 = gp0 * k1 - gp1 * k0;
     float nrm;  // screen-space gradient norm (Eq. 12): approximate sqrt, no slow path
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(nrm) : "f"(gk2 * gk2 + gl2 * gl2));
     g[16] += fabsf(R.c.x) * nrm;
+    return 1;
+}
+
+// Layer of a covering record at pixel `pix` (m = #{j : thr_j < zs}, see the
+// file header), -1 beyond the K_MAX stop; its coefficients in cf.
+__device__ __forceinline__ int pixel_layer(const SplatParams &P, size_t pix, float zs, float4 &cf, float &lo) {
+    const size_t HW = (size_t)P.W * P.H;
+    const int4 h = __ldg(P.hdr + 2 * pix);
+    const int nc = h.x & 0xff;
+    int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
+            (nc > 2 && __int_as_float(h.w) < zs);
+    if (m == 3 && nc > 3) {
+        const int4 h2 = __ldg(P.hdr + 2 * pix + 1);
+        m += (__int_as_float(h2.x) < zs) + (nc > 4 && __int_as_float(h2.y) < zs) +
+             (nc > 5 && __int_as_float(h2.z) < zs) + (nc > 6 && __int_as_float(h2.w) < zs);
+        if (m == 7) {
+            const int jn = min(nc, P.k_max);
+            for (int j = 7; j < jn && __ldg(P.thr + j * HW + pix) < zs; ++j) ++m;
+        }
+    }
+    if (m >= P.k_max) return -1;
+    cf = __ldg(P.coef + m * HW + pix);
+    lo = __ldg(P.coef_lo + m * HW + pix);
+    return m;
+}
+
+// Big records (rects > kBigArea): the reference's own per-item arithmetic
+// (backward.py:257-320) -- k, l, den, u, v in exact float32 (bit-identical,
+// so is the coverage decision), rho^2 with numba's promotion, weight and
+// every gradient term in float64, float64 sums, dL/dt1, dt2, dt4 formed per
+// item as cross products.  A grazing splat's rect spans up to ~10^5 pixels
+// whose terms cancel to ~1e-3 of their magnitude sum; float32 terms and
+// sums (the moment form of item_grad) drift by percent there.
+template <bool kCons>
+__device__ __forceinline__ int item_grad_ref(const SplatParams &P, const SsRecord &R, int ix, int iy, float x,
+                                             float y, double *g) {
+    const float t4x = R.b.z, t4y = R.b.w, t4z = R.c.x;
+    const float k0 = fs(fm(x, t4x), R.a.x), k1 = fs(fm(x, t4y), R.a.y), k2 = fs(fm(x, t4z), R.a.z);
+    const float l0 = fs(fm(y, t4x), R.a.w), l1 = fs(fm(y, t4y), R.b.x), l2 = fs(fm(y, t4z), R.b.y);
+    const float den = fs(fm(k0, l1), fm(k1, l0));
+    if (fabsf(den) <= 9.99999972e-10f) return 0;  // |den| < 1e-9 in float64, exactly
+    const float u = fd(fs(fm(k1, l2), fm(k2, l1)), den);
+    const float v = fd(fs(fm(k2, l0), fm(k0, l2)), den);
+    const double rho2 = ss_rho2(R.c.y, R.c.z, R.c.w, u, v);
+    if (!(rho2 < 9.0)) return 0;
+    float4 cf;
+    float lo;
+    const int m = pixel_layer(P, (size_t)iy * P.W + ix, R.d.z, cf, lo);
+    if (m < 0) return 0;  // beyond the K_MAX stop: discarded
+    const double e = exp(-0.5 * rho2);
+    const double w = (double)R.d.x * e;
+    double gw = ((double)cf.x + (double)lo) + (((double)cf.y * R.e.x + (double)cf.z * R.e.y) + (double)cf.w * R.e.z);
+    if constexpr (kCons) {
+        const size_t HW = (size_t)P.W * P.H;
+        const float4 zq = __ldg(P.zc + m * HW + (size_t)iy * P.W + ix);
+        const double dz = (double)R.d.y - zq.z;
+        gw += zq.x * dz + zq.y * (dz * dz - zq.w);
+        g[17] += w * (zq.x + 2.0 * zq.y * dz);
+    }
+    g[13] += w * cf.y; g[14] += w * cf.z; g[15] += w * cf.w;
+    const double gr = -0.5 * w * gw;
+    const double U = u, V = v;
+    g[12] += e * gw;
+    g[9] += gr * U * U; g[10] += gr * 2.0 * U * V; g[11] += gr * V * V;
+    // numba keeps sinv * u + sinv * v in float32 (float32 operands), then
+    // promotes (backward.py:292-293): the rounded sum is part of the result
+    const double gu = gr * 2.0 * (double)fa(fm(R.c.y, u), fm(R.c.z, v));
+    const double gv = gr * 2.0 * (double)fa(fm(R.c.z, u), fm(R.c.w, v));
+    const double D = den;
+    const double gp0 = gu / D, gp1 = gv / D, gp2 = -(gu * U + gv * V) / D;
+    const double K0 = k0, K1 = k1, K2 = k2, L0 = l0, L1 = l1, L2 = l2, X = x, Y = y;
+    const double gk0 = L1 * gp2 - L2 * gp1, gk1 = L2 * gp0 - L0 * gp2, gk2 = L0 * gp1 - L1 * gp0;
+    const double gl0 = gp1 * K2 - gp2 * K1, gl1 = gp2 * K0 - gp0 * K2, gl2 = gp0 * K1 - gp1 * K0;
+    g[0] -= gk0; g[1] -= gk1; g[2] -= gk2;
+    g[3] -= gl0; g[4] -= gl1; g[5] -= gl2;
+    g[6] += X * gk0 + Y * gl0; g[7] += X * gk1 + Y * gl1; g[8] += X * gk2 + Y * gl2;
+    const double gsx = -gk2 * (double)t4z, gsy = -gl2 * (double)t4z;  // Eq. 12
+    g[16] += sqrt(gsx * gsx + gsy * gsy);
     return 1;
 }
 
@@ -225,10 +327,12 @@ __global__ void __launch_bounds__(256) area_class_kernel(SplatParams P, uint8_t 
             if (area > kBigArea) {
                 float4 *dst = reinterpret_cast<float4 *>(P.acc + (size_t)r * SS_ACC_FLOATS);
 #pragma unroll
-                for (int i = 0; i < SS_ACC_FLOATS / 4 - 1; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                dst[SS_ACC_FLOATS / 4 - 1] = make_float4(0.f, 0.f, 0.f, SS_ACC_MOMENTS);
-                if (area > kHugeArea) big_list[P.n - 1 - atomicAdd(counters + 1, 1)] = r;
-                else big_list[atomicAdd(counters, 1)] = r;
+                for (int i = 0; i < SS_ACC_FLOATS / 4; ++i) dst[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int q = area > kHugeArea ? P.n - 1 - atomicAdd(counters + 1, 1) : atomicAdd(counters, 1);
+                big_list[q] = r;
+                double2 *row = reinterpret_cast<double2 *>(P.big_acc + (size_t)q * kBigW);
+#pragma unroll
+                for (int i = 0; i < kBigW / 2; ++i) row[i] = make_double2(0.0, 0.0);
             } else {
                 c = (uint8_t)area_class(area);
                 atomicAdd(&s_hist[c], 1);
@@ -287,7 +391,6 @@ __global__ void __launch_bounds__(256) area_scatter_kernel(int n, const uint8_t 
 
 struct GroupSmem {
     SsRecord rec[2][4];       // current / prefetched records of the 4 groups (cp.async double buffer)
-    float2 uv[4][kGCap];      // covered items: u, v
     int ixy[4][kGCap];        // covered items: pixel ix | iy << 16
 };
 
@@ -364,6 +467,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
         const unsigned mrw = ((1u << 20) + (unsigned)rw - 1u) / (unsigned)rw;
         FastCov f;
         fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
+        const float cx = valid ? fd(R.a.z, R.c.x) : 0.f, cy = valid ? fd(R.b.y, R.c.x) : 0.f;
         float g[NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) g[k] = 0.f;
@@ -380,11 +484,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
                 const int ky = (int)(((unsigned)k * mrw) >> 20);
                 const bool hit = k < area && item_cover(xs, ys, R, f, R.r.x + (k - ky * rw), R.r.y + ky, ixy, q);
                 const unsigned gm = (__ballot_sync(0xffffffffu, hit) >> (grp * kGL)) & 0xffu;
-                if (hit) {
-                    const int slot = ncov + __popc(gm & glt);
-                    sm.uv[grp][slot] = make_float2(q.x, q.y);
-                    sm.ixy[grp][slot] = ixy;
-                }
+                if (hit) sm.ixy[grp][ncov + __popc(gm & glt)] = ixy;
                 ncov += __popc(gm);
             }
             __syncwarp();
@@ -393,13 +493,10 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
             for (int j0 = 0; j0 < nmax; j0 += kGL) {
                 const int j = j0 + gl;
                 if (j < ncov) {
-                    const float2 q = sm.uv[grp][j];
                     const int ixy = sm.ixy[grp][j];
-                    // rho^2 with ss_cover's float32 expression (bit-identical on its fast path)
-                    const float r2 = R.c.y * q.x * q.x + 2.f * R.c.z * q.x * q.y + R.c.w * q.y * q.y;
                     // pixel centres from the (shared-memory) tables: no int->float conversions
                     const int ix = ixy & 0xffff, iy = ixy >> 16;
-                    touch += item_grad<kCons>(P, R, ix, iy, xs[ix], ys[iy], q.x, q.y, r2, g);
+                    touch += item_grad<kCons>(P, R, ix, iy, xs[ix], ys[iy], cx, cy, g);
                 }
             }
             __syncwarp();
@@ -428,15 +525,13 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
 // Gradient contribution of record R at rect pixel k (row-major) for the big
 // records (no compaction), accumulated into g[]; returns 1 when touched.
 template <bool kCons>
-__device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &R, const FastCov &f, int k, int rw,
-                                          float inv_rw, float *g) {
-    int ixy;
-    float4 q;
-    // (k + 0.5) / rw is at least 0.5 / rw from an integer: truncation stays exact
-    const int ky = (int)(((float)k + 0.5f) * inv_rw);
-    if (!item_cover(P.xs, P.ys, R, f, R.r.x + (k - ky * rw), R.r.y + ky, ixy, q)) return 0;
-    const int ix = ixy & 0xffff, iy = ixy >> 16;
-    return item_grad<kCons>(P, R, ix, iy, __ldg(P.xs + ix), __ldg(P.ys + iy), q.x, q.y, q.z, g);
+__device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &R, int k, int rw, double *g) {
+    // integer division: exact for any rect size (a float32 reciprocal
+    // multiply is exact only while k < ~2^22, i.e. rects below ~4 MP); this
+    // path handles ~0.1% of the records
+    const int ky = k / rw;
+    const int ix = R.r.x + (k - ky * rw), iy = R.r.y + ky;
+    return item_grad_ref<kCons>(P, R, ix, iy, __ldg(P.xs + ix), __ldg(P.ys + iy), g);
 }
 
 // Big records (grazing splats whose filtered bound spans up to most of the
@@ -448,30 +543,27 @@ __device__ __forceinline__ int pixel_grad(const SplatParams &P, const SsRecord &
 // 32-pixel rows, reduce, and commit with atomics (the splat kernel zeroed
 // the rows).
 template <bool kCons>
-__device__ __forceinline__ void big_record(const SplatParams &P, int rec, int c0, int cstep, int wid, int nw,
+__device__ __forceinline__ void big_record(const SplatParams &P, int q, int c0, int cstep, int wid, int nw,
                                            int lane, int my_ch, bool owner) {
     constexpr int NC = nch<kCons>();
+    const int rec = P.big_list[q];
     SsRecord R;
     load_record(P.records, rec, R);
     const int rw = R.r.z - R.r.x, area = rw * (R.r.w - R.r.y);
     const int nchunks = (area + kBigChunk - 1) / kBigChunk;
-    const float inv_rw = fast_rcp((float)rw);
-    FastCov f;
-    fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
-    float g[NC];
+    double g[NC];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) g[k] = 0.f;
+    for (int k = 0; k < NC; ++k) g[k] = 0.0;
     int touch = 0;
     for (int c = c0; c < nchunks; c += cstep) {
         const int k1 = min(area, (c + 1) * kBigChunk);
-        for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad<kCons>(P, R, f, k, rw, inv_rw, g);
+        for (int k = c * kBigChunk + wid * 32 + lane; k < k1; k += 32 * nw) touch += pixel_grad<kCons>(P, R, k, rw, g);
     }
     const int tot = warp_sum(touch);
     if (tot == 0) return;
     warp_tr_reduce<NC>(g, lane);
-    float *dst = P.acc + (size_t)rec * SS_ACC_FLOATS;
-    if (owner) atomicAdd(dst + acc_slot(my_ch), g[0]);
-    if (lane == 0) atomicAdd(reinterpret_cast<int *>(dst) + 18, tot);
+    if (owner) atomicAdd(P.big_acc + (size_t)q * kBigW + my_ch, g[0]);
+    if (lane == 0) atomicAdd(reinterpret_cast<int *>(P.acc + (size_t)rec * SS_ACC_FLOATS) + 18, tot);
 }
 
 template <bool kCons>
@@ -492,11 +584,26 @@ __global__ void __launch_bounds__(256) big_bwd_kernel(SplatParams P, const int32
         __syncthreads();
         const int b = s_b;
         if (b >= nmed) break;
-        big_record<kCons>(P, big_list[b], 0, 1, wid, nw, lane, my_ch, owner);
+        big_record<kCons>(P, b, 0, 1, wid, nw, lane, my_ch, owner);
     }
     for (int h = 0; h < nhuge; ++h) {
         const int first = (int)(((long long)blockIdx.x - 37LL * h) % G + G) % G;
-        big_record<kCons>(P, big_list[P.n - 1 - h], first, G, wid, nw, lane, my_ch, owner);
+        big_record<kCons>(P, P.n - 1 - h, first, G, wid, nw, lane, my_ch, owner);
+    }
+}
+
+// The big records' rows point at their float64 sums (slot 19 =
+// SS_ACC_F64, slot 0 = the queue slot): the chain kernel reads the float64
+// channels -- a grazing splat's row gradients cancel in the chain's linear
+// maps, beyond a float32 accumulator row.
+__global__ void __launch_bounds__(256) big_finish_kernel(SplatParams P, const int32_t *big_count) {
+    const int nmed = big_count[0], nhuge = big_count[1];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nmed + nhuge; e += gridDim.x * blockDim.x) {
+        const int q = e < nmed ? e : P.n - 1 - (e - nmed);
+        float *dst = P.acc + (size_t)P.big_list[q] * SS_ACC_FLOATS;
+        dst[0] = __int_as_float(q);
+        dst[17] = (float)P.big_acc[(size_t)q * kBigW + 16];  // ss (readers of the float row)
+        dst[19] = SS_ACC_F64;
     }
 }
 
@@ -510,29 +617,27 @@ extern "C" size_t ss_train_backward_scratch_words(int n, int width, int height)
 
 template <bool kSmemNdc, bool kCons>
 void launch_splat(const SplatParams &P, const int32_t *order, int32_t *counters, int smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(splat_bwd_kernel<kSmemNdc, kCons>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSplatWarps * (int)sizeof(GroupSmem) + (kSmemNdc ? kNdcSmem * (int)sizeof(float) : 0));
-        attr = true;
-    }
-    splat_bwd_kernel<kSmemNdc, kCons><<<148 * SS_SPLAT_MINB, 32 * kSplatWarps, smem, st>>>(P, order, counters);
+    ss_func_smem((const void *)splat_bwd_kernel<kSmemNdc, kCons>,
+                 kSplatWarps * (int)sizeof(GroupSmem) + (kSmemNdc ? kNdcSmem * (int)sizeof(float) : 0));
+    splat_bwd_kernel<kSmemNdc, kCons><<<ss_sm_count() * SS_SPLAT_MINB, 32 * kSplatWarps, smem, st>>>(P, order, counters);
 }
 
 static int backward_records(int n, const int8_t *cull, const float *records, int width, int height, int k_max,
                             const float *coef, const float *thr, const int32_t *pix_hdr, const float *zcoef,
-                            float *pixel_ndc, float *rec_acc, void *stream)
+                            float *pixel_ndc, float *rec_acc, double *rec_acc64, void *stream)
 {
     if (n < 0 || width <= 0 || height <= 0 || k_max < 1 || k_max > SS_KMAX_CAP) return SS_ERR_INVALID;
     if (n == 0) return SS_OK;
-    if (!cull || !records || !coef || !thr || !pix_hdr || !pixel_ndc || !rec_acc) return SS_ERR_INVALID;
+    if (!cull || !records || !coef || !thr || !pix_hdr || !pixel_ndc || !rec_acc || !rec_acc64) return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int mx = width > height ? width : height;
+
     int32_t *counters = reinterpret_cast<int32_t *>(pixel_ndc + width + height);
     int32_t *hist = counters + 8, *cursor = hist + kNB;
     int32_t *big_list = counters + kHeadWords;
     int32_t *order = big_list + n;
     uint8_t *cls = reinterpret_cast<uint8_t *>(order + n);
+
     pixel_ndc_kernel<<<(mx + kHeadWords + 255) / 256, 256, 0, st>>>(width, height, pixel_ndc, pixel_ndc + width,
                                                                      counters);
     SS_CUDA_CHECK_LAUNCH();
@@ -542,10 +647,13 @@ static int backward_records(int n, const int8_t *cull, const float *records, int
     P.records = reinterpret_cast<const SsRecord *>(records);
     P.xs = pixel_ndc; P.ys = pixel_ndc + width;
     P.coef = reinterpret_cast<const float4 *>(coef);
+    P.coef_lo = coef + (size_t)4 * k_max * width * height;
     P.thr = thr; P.hdr = reinterpret_cast<const int4 *>(pix_hdr); P.acc = rec_acc;
     P.zc = reinterpret_cast<const float4 *>(zcoef);
+    P.big_list = big_list;
+    P.big_acc = rec_acc64;
     const bool cons = zcoef != nullptr;
-    area_class_kernel<<<148 * 4, 256, 0, st>>>(P, cls, big_list, counters, hist);
+    area_class_kernel<<<ss_sm_count() * 4, 256, 0, st>>>(P, cls, big_list, counters, hist);
     SS_CUDA_CHECK_LAUNCH();
     area_scatter_kernel<<<(n + 256 * kScatItems - 1) / (256 * kScatItems), 256, 0, st>>>(n, cls, hist, cursor, order,
                                                                                        counters + 4);
@@ -561,25 +669,28 @@ static int backward_records(int n, const int8_t *cull, const float *records, int
         else launch_splat<false, false>(P, order, counters, smem, st);
     }
     SS_CUDA_CHECK_LAUNCH();
-    if (cons) big_bwd_kernel<true><<<148 * 4, 256, 0, st>>>(P, big_list, counters);
-    else big_bwd_kernel<false><<<148 * 4, 256, 0, st>>>(P, big_list, counters);
+    if (cons) big_bwd_kernel<true><<<ss_sm_count() * 4, 256, 0, st>>>(P, big_list, counters);
+    else big_bwd_kernel<false><<<ss_sm_count() * 4, 256, 0, st>>>(P, big_list, counters);
+    SS_CUDA_CHECK_LAUNCH();
+    big_finish_kernel<<<ss_sm_count(), 256, 0, st>>>(P, counters);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
 
 extern "C" int ss_train_backward_records(int n, const int8_t *cull, const float *records, int width, int height,
                                          int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
-                                         float *pixel_ndc, float *rec_acc, void *stream)
+                                         float *pixel_ndc, float *rec_acc, double *rec_acc64, void *stream)
 {
     return backward_records(n, cull, records, width, height, k_max, coef, thr, pix_hdr, nullptr, pixel_ndc, rec_acc,
-                            stream);
+                            rec_acc64, stream);
 }
 
 extern "C" int ss_train_backward_records_cons(int n, const int8_t *cull, const float *records, int width, int height,
                                               int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
-                                              const float *zcoef, float *pixel_ndc, float *rec_acc, void *stream)
+                                              const float *zcoef, float *pixel_ndc, float *rec_acc, double *rec_acc64,
+                                              void *stream)
 {
     if (!zcoef) return SS_ERR_INVALID;
     return backward_records(n, cull, records, width, height, k_max, coef, thr, pix_hdr, zcoef, pixel_ndc, rec_acc,
-                            stream);
+                            rec_acc64, stream);
 }

@@ -9,26 +9,27 @@
 #pragma once
 #include <cuda_runtime.h>
 
-template <int N, int O>
-__device__ __forceinline__ void warp_tr_level(float *v, bool upper) {
+template <int N, int O, typename T>
+__device__ __forceinline__ void warp_tr_level(T *v, bool upper) {
     constexpr int H = N / 2;
 #pragma unroll
     for (int i = 0; i < H; ++i) {
-        const float send = upper ? v[i] : v[i + H];
-        const float keep = upper ? v[i + H] : v[i];
+        const T send = upper ? v[i] : v[i + H];
+        const T keep = upper ? v[i + H] : v[i];
         v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
     }
     if constexpr ((N & 1) != 0) v[H] = v[N - 1] + __shfl_xor_sync(0xffffffffu, v[N - 1], O);
 }
 
-template <int N, int O>
-__device__ __forceinline__ void warp_tr_all(float *v, int lane) {
+template <int N, int O, typename T>
+__device__ __forceinline__ void warp_tr_all(T *v, int lane) {
     warp_tr_level<N, O>(v, (lane & O) != 0);
     if constexpr (O > 1) warp_tr_all<N / 2 + (N & 1), O / 2>(v, lane);
 }
 
-template <int N>
-__device__ __forceinline__ void warp_tr_reduce(float (&v)[N], int lane) {
+// float or double channels
+template <int N, typename T>
+__device__ __forceinline__ void warp_tr_reduce(T (&v)[N], int lane) {
     warp_tr_all<N, 16>(v, lane);
 }
 

@@ -5,13 +5,16 @@ screen-space gradient over active surfels, density gate against the frozen
 KNN mean distance) -> budget -> split into two children along the longer
 tangent axis.  Runs on the device: the isolation test is a fixed-radius
 existence query on a uniform grid (csrc/optim.cu, replacing the reference's
-scipy cKDTree k=2 query), the children are written by a native kernel, and the
-selection/compaction steps are device tensor ops.
+scipy cKDTree k=2 query), and refine_topology runs the whole pass (prune, quantile, budget,
+compaction, children, optimiser-state remap) as native kernels with one host
+read of the counters at the end (csrc/refine.cu).
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
+
+import ctypes
 
 import numpy as np
 import torch
@@ -37,42 +40,53 @@ class DensifyStats:
                    torch.zeros(n, device=device, dtype=torch.int64))
 
     def accumulate(self, ss_grad, touched):
-        """touched: bool per surfel (BackwardResult.touched) or per-surfel
-        covering-pixel counts (counted as touched when > 0)."""
+        """One view (densify.py:35-37): touched is BackwardResult.touched (bool
+        per surfel), adding 1 to the view count of every touched surfel.
+
+        A batched step (TrainStep) passes its summed ss_grad and its
+        `view_count` -- the number of the step's views each surfel was touched
+        in (a float or int count, not a bool) -- which is exactly the sum of
+        the per-view accumulate() calls over those views."""
         dev = self.grad_sum.device
         self.grad_sum += torch.as_tensor(ss_grad, device=dev).to(torch.float64)
         t = torch.as_tensor(touched, device=dev)
-        self.view_count += (t if t.dtype == torch.bool else t > 0).to(torch.int64)
+        if t.dtype == torch.bool:
+            self.view_count += t.to(torch.int64)
+        else:
+            self.view_count += torch.round(t.to(torch.float64)).to(torch.int64)
 
     def mean_grad(self):
         return self.grad_sum / torch.clamp(self.view_count, min=1)
 
 
-def isolated_mask(cloud: SurfelCloud) -> torch.Tensor:
-    """True where the nearest other centre lies beyond R_CUT * max scale
-    (densify.py:118-123), via a uniform-grid fixed-radius query."""
+def isolated_flags(cloud: SurfelCloud) -> torch.Tensor:
+    """uint8 per surfel: 1 where the nearest other centre lies beyond
+    R_CUT * max scale (densify.py:118-123).  Uniform-grid fixed-radius query
+    with the grid sized on the device (ss_grid_fit): no host round trip."""
     n = len(cloud)
     dev = cloud.centers.device
     if n <= 1:
-        return torch.zeros(n, device=dev, dtype=torch.bool)
+        return torch.zeros(n, device=dev, dtype=torch.uint8)
     lib = _lib.load()
+    s = _lib.stream_ptr()
     c = cloud.centers
-    lo = c.min(dim=0).values
-    hi = c.max(dim=0).values
-    support = R_CUT * torch.exp(cloud.log_scales).max(dim=1).values
-    extent = float((hi - lo).max().item())
-    cell = max(float(torch.median(support).item()) * 2.0, extent / 1024.0, 1e-12)
-    dim = int(min(1024, max(1, int(np.ceil(extent / cell)) + 1)))
-    org, _k1 = _lib.fvec([float(v) for v in lo.tolist()])
+    grid = torch.empty(16, device=dev, dtype=torch.float32)
+    _lib.check(lib.ss_grid_fit(n, _lib.ptr(c), _lib.ptr(cloud.log_scales), _lib.ptr(grid), s), "ss_grid_fit")
     cells = torch.empty(n, device=dev, dtype=torch.int32)
-    _lib.check(lib.ss_grid_cells(n, _lib.ptr(c), org, cell, dim, _lib.ptr(cells), _lib.stream_ptr()), "ss_grid_cells")
+    _lib.check(lib.ss_grid_cells_d(n, _lib.ptr(c), _lib.ptr(grid), _lib.ptr(cells), s), "ss_grid_cells_d")
     sorted_cells, order = torch.sort(cells, stable=True)
     order = order.to(torch.int32).contiguous()
     sorted_cells = sorted_cells.contiguous()
     iso = torch.empty(n, device=dev, dtype=torch.uint8)
-    _lib.check(lib.ss_isolation(n, _lib.ptr(c), _lib.ptr(cloud.log_scales), _lib.ptr(order), _lib.ptr(sorted_cells),
-                                org, cell, dim, _lib.ptr(iso), _lib.stream_ptr()), "ss_isolation")
-    return iso.bool()
+    _lib.check(lib.ss_isolation_d(n, _lib.ptr(c), _lib.ptr(cloud.log_scales), _lib.ptr(order), _lib.ptr(sorted_cells),
+                                  _lib.ptr(grid), _lib.ptr(iso), s), "ss_isolation_d")
+    return iso
+
+
+def isolated_mask(cloud: SurfelCloud) -> torch.Tensor:
+    """True where the nearest other centre lies beyond R_CUT * max scale
+    (densify.py:118-123)."""
+    return isolated_flags(cloud).bool()
 
 
 def prune_keep_mask(cloud, stats, outside_mask_votes=None, front_votes=None):
@@ -123,10 +137,92 @@ def split_cloud(cloud: SurfelCloud, mask):
     return out, index_map
 
 
+_ROLES = {"centers": 2, "log_scales": 3}
+LAST_REFINE = {}  # diagnostics of the last refine_topology call (kept, active, candidates, threshold)
+
+
 def refine_topology(cloud, stats, mean_neighbor_dist, max_surfels, quantile=SPLIT_QUANTILE,
-                    grad_floor=SPLIT_GRAD_FLOOR, outside_mask_votes=None, front_votes=None):
+                    grad_floor=SPLIT_GRAD_FLOOR, outside_mask_votes=None, front_votes=None, optimizer=None):
     """densify.py:168-202: prune then split within the surfel budget.
-    Returns (cloud, index map into the input cloud with -1 for new rows, reasons)."""
+    Returns (cloud, index map into the input cloud with -1 for new rows,
+    reasons).
+
+    Runs as device kernels (csrc/refine.cu): isolation query, prune flags,
+    numpy-'linear' quantile by radix select, candidate and budget selection,
+    compaction and the new rows -- one host read of the counters at the end.
+    With `optimizer` (an Adam), its state rows are remapped in the same pass
+    (Adam.remap of every parameter, adam.py:43-58)."""
+    lib = _lib.load()
+    n = len(cloud)
+    dev = cloud.centers.device
+    s = _lib.stream_ptr()
+    gs = torch.as_tensor(stats.grad_sum, device=dev).to(torch.float64).contiguous()
+    vc = torch.as_tensor(stats.view_count, device=dev).to(torch.int64).contiguous()
+    mnd = torch.as_tensor(mean_neighbor_dist, device=dev).to(torch.float64).contiguous()
+    if outside_mask_votes is not None and front_votes is not None:
+        ov = torch.as_tensor(outside_mask_votes, device=dev).to(torch.int64).contiguous()
+        fv = torch.as_tensor(front_votes, device=dev).to(torch.int64).contiguous()
+    else:
+        ov = fv = None
+    iso = isolated_flags(cloud)
+    ws = torch.empty(int(lib.ss_refine_workspace_bytes(n)), device=dev, dtype=torch.uint8)
+    dst = torch.empty(n, device=dev, dtype=torch.int32)
+    kind = torch.empty(n, device=dev, dtype=torch.uint8)
+    counts = torch.zeros(9, device=dev, dtype=torch.int64)
+    _lib.check(lib.ss_refine_plan(n, _lib.ptr(gs), _lib.ptr(vc), _lib.ptr(iso), _lib.ptr(ov), _lib.ptr(fv),
+                                  _lib.ptr(cloud.log_scales), _lib.ptr(mnd), int(max_surfels), float(quantile),
+                                  float(grad_floor), _lib.ptr(dst), _lib.ptr(kind), _lib.ptr(counts), _lib.ptr(ws), s),
+               "ss_refine_plan")
+    # outputs sized for the largest possible result (kept + splits <= max(n, max_surfels)),
+    # so the new rows are written before the counts are read back
+    cap = max(n, int(max_surfels), 1)
+    tensors = []
+    for k in FIELDS:
+        t = getattr(cloud, k)
+        tensors.append((t, torch.empty((cap,) + tuple(t.shape[1:]), device=dev, dtype=t.dtype), _ROLES.get(k, 0)))
+    opt_new = {}
+    if optimizer is not None:
+        for name in list(optimizer.m):
+            if name not in FIELDS:  # per-surfel state only (not the env)
+                continue
+            for store in (optimizer.m, optimizer.v):
+                t = store[name]
+                if t.shape[0] != n:
+                    raise ValueError(f"optimizer state {name!r} has {t.shape[0]} rows, the cloud {n}")
+                out = torch.empty((cap,) + tuple(t.shape[1:]), device=dev, dtype=t.dtype)
+                tensors.append((t, out, 1))
+                opt_new[(id(store), name)] = out
+    if len(tensors) > 20:
+        raise ValueError("too many tensors to remap in one pass")
+    index_map = torch.empty(cap, device=dev, dtype=torch.int64)
+    m = len(tensors)
+    src = (ctypes.c_void_p * m)(*[t[0].data_ptr() for t in tensors])
+    out = (ctypes.c_void_p * m)(*[t[1].data_ptr() for t in tensors])
+    rb = (ctypes.c_int * m)(*[t[0].element_size() * (t[0].numel() // max(t[0].shape[0], 1)) for t in tensors])
+    roles = (ctypes.c_int * m)(*[t[2] for t in tensors])
+    _lib.check(lib.ss_refine_apply(n, _lib.ptr(kind), _lib.ptr(dst), _lib.ptr(cloud.centers), _lib.ptr(cloud.quats),
+                                   _lib.ptr(cloud.log_scales), m, src, out, rb, roles, _lib.ptr(index_map),
+                                   _lib.ptr(ws), s), "ss_refine_apply")
+    c = counts.cpu().numpy()  # the one host synchronisation
+    n_out = int(c[0])
+    new = SurfelCloud(*(tensors[i][1][:n_out] for i in range(len(FIELDS))))
+    if optimizer is not None:
+        for name in list(optimizer.m):
+            for store in (optimizer.m, optimizer.v):
+                key = (id(store), name)
+                if key in opt_new:
+                    store[name] = opt_new[key][:n_out]
+    reasons = {"stale": int(c[3]), "isolated": int(c[4]), "floater": int(c[5]), "split": int(c[2])}
+    LAST_REFINE.update(kept=int(c[1]), active=int(c[6]), candidates=int(c[7]),
+                       threshold=float(np.array([c[8]], dtype=np.int64).view(np.float64)[0]))
+    return new, index_map[:n_out], reasons
+
+
+def refine_topology_reference_order(cloud, stats, mean_neighbor_dist, max_surfels, quantile=SPLIT_QUANTILE,
+                                    grad_floor=SPLIT_GRAD_FLOOR, outside_mask_votes=None, front_votes=None):
+    """The same pass composed from the API-level helpers below (prune_keep_mask,
+    select_split, split_cloud: device tensor ops with host reads), kept as a
+    cross-check of the fused kernels."""
     keep, reasons = prune_keep_mask(cloud, stats, outside_mask_votes, front_votes)
     kept_idx = torch.nonzero(keep).flatten()
     kept = cloud.select(kept_idx)

@@ -103,13 +103,52 @@ def _compact_index(cull):
     return keep, rank
 
 
+def pack_projected(proj: ProjectedSurfels, tile=TILE, n_source=None, colors=None, cull=None):
+    """ViewState of a compacted ProjectedSurfels (csrc ss_pack_records):
+    records indexed by proj.source_index in a cloud of n_source rows (or by
+    the compacted row itself when n_source is None), colours per source row,
+    culled rows from proj.cull_code."""
+    lib = _lib.load()
+    dev = proj.t1.device
+    k = len(proj)
+    by_source = n_source is not None
+    n = int(n_source) if by_source else k
+    W, H = int(proj.width), int(proj.height)
+    ntiles = ((W + tile - 1) // tile) * ((H + tile - 1) // tile)
+    records = torch.zeros((n, _lib.REC_FLOATS), device=dev, dtype=torch.float32)
+    bininfo = torch.zeros((n, 4), device=dev, dtype=torch.int32)
+    tile_counts = torch.zeros(ntiles, device=dev, dtype=torch.int32)
+    if cull is None:
+        cull = proj.cull_code.to(torch.int8).contiguous() if by_source else torch.zeros(n, device=dev, dtype=torch.int8)
+    f32 = lambda t: torch.as_tensor(t, device=dev).to(torch.float32).contiguous()
+    src = torch.as_tensor(proj.source_index, device=dev).to(torch.int32).contiguous() if by_source else None
+    cols = None if colors is None else f32(colors)
+    rc = lib.ss_pack_records(k, _lib.ptr(f32(proj.t1)), _lib.ptr(f32(proj.t2)), _lib.ptr(f32(proj.t4)),
+                             _lib.ptr(f32(proj.sinv)), _lib.ptr(f32(proj.n_f)), _lib.ptr(f32(proj.view_z)),
+                             _lib.ptr(f32(proj.eps_z)),
+                             _lib.ptr(torch.as_tensor(proj.rect, device=dev).to(torch.int32).contiguous()),
+                             _lib.ptr(src), _lib.ptr(cols), W, H, int(tile), _lib.ptr(records), _lib.ptr(bininfo),
+                             _lib.ptr(tile_counts), _lib.stream_ptr())
+    _lib.check(rc, "ss_pack_records")
+    flags = torch.zeros(4, device=dev, dtype=torch.int32)
+    return ViewState(records, cull, tile_counts, flags, W, H, int(tile), proj.options, _lib.SS_COLOR_EXPLICIT,
+                     {}, bininfo=bininfo)
+
+
 def bin_and_sort(proj_or_state, tile=TILE):
     """rasterizer.py:92-116 contract: (tile_offsets int64 (T+1,), pair_rec int32
-    (P,) in compacted record indices, ntx, nty).  Accepts the ViewState of a
-    render (the binning itself always runs on the device)."""
+    (P,) in compacted record indices, ntx, nty).  Takes the reference's
+    ProjectedSurfels (preprocess()'s output) or the ViewState of a render;
+    the binning itself always runs on the device."""
     st = proj_or_state
+    if isinstance(st, ProjectedSurfels):
+        st = pack_projected(st, tile=tile)
+        offsets, pair = bin_state(st)
+        return offsets.to(torch.int64), pair.clone(), st.ntx, st.ntiles // st.ntx
     if not isinstance(st, ViewState):
-        raise TypeError("bin_and_sort takes the ViewState produced by run_preprocess/render")
+        raise TypeError("bin_and_sort takes a ProjectedSurfels or the ViewState of run_preprocess/render")
+    if int(tile) != st.tile:
+        raise ValueError(f"the ViewState was binned for tile={st.tile}")
     offsets, pair = bin_state(st)
     _, rank = _compact_index(st.cull)
     return offsets.to(torch.int64), rank[pair.long()], st.ntx, st.ntiles // st.ntx
@@ -120,8 +159,6 @@ def render(cloud, camera, options: RenderOptions | None = None, env=None, colors
     """rasterizer.py:331-431.  Colours: explicit > IBL (env and shade='ibl') > albedo."""
     opt = options or RenderOptions()
     opt.validate()
-    if proj is not None:
-        raise ValueError("proj= reuse is not supported: records are rebuilt on the device every call")
     lib = _lib.load()
     if colors is not None:
         source, src_name = _lib.SS_COLOR_EXPLICIT, "explicit"
@@ -131,6 +168,20 @@ def render(cloud, camera, options: RenderOptions | None = None, env=None, colors
         source, src_name = _lib.SS_COLOR_ALBEDO, "albedo"
     state = run_preprocess(cloud, camera, opt.preprocess_options(), source, colors=colors, env=env,
                            tile=int(opt.tile), want_aux=True)
+    if proj is not None:
+        # proj= reuse (rasterizer.py:338-339): rasterise the GIVEN projection;
+        # the preprocess pass above only supplied the colours (explicit /
+        # shaded / albedo per source surfel) and the shading context.  The
+        # backward's per-surfel chain recomputes the projection from the
+        # cloud, so proj must be this cloud's projection for this camera
+        # (as preprocess() returns it) for gradients to be meaningful.
+        if int(proj.width) != int(camera.width) or int(proj.height) != int(camera.height):
+            raise ValueError("proj was computed for a different image size")
+        if len(proj.cull_code) != len(cloud):
+            raise ValueError("proj was computed for a different cloud size")
+        packed = pack_projected(proj, tile=int(opt.tile), n_source=len(cloud), colors=state.aux["colors"])
+        packed.aux, packed.color_source, packed.flags = state.aux, source, state.flags
+        state = packed
     offsets, pair_src = bin_state(state)
     flags = state.flags.cpu()
     if int(flags[0]):
@@ -162,7 +213,7 @@ def render(cloud, camera, options: RenderOptions | None = None, env=None, colors
                                _lib.ptr(pair_cover), ctypes.byref(st_struct) if st_struct is not None else None,
                                _lib.ptr(discarded), _lib.stream_ptr())
     _lib.check(rc, "ss_raster_forward")
-    proj_c = compact(state)
+    proj_c = compact(state) if proj is None else proj
     keep, rank = _compact_index(state.cull)
     cover_counts = None
     if opt.with_cover_counts:

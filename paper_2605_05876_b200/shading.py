@@ -8,6 +8,8 @@ csrc/env.cu (shading.py:369-394); nothing T x T is ever materialised.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -20,8 +22,7 @@ DEFAULT_LUT_SAMPLES = 128
 DEFAULT_SPEC_SAMPLES = 128
 
 _LUT_CACHE = {}
-_ROWSUM_CACHE = {}
-_SPEC_OP_CACHE = {}
+_OPS_CACHE = {}
 
 
 def brdf_lut(res=DEFAULT_LUT_RES, samples=DEFAULT_LUT_SAMPLES):
@@ -35,62 +36,62 @@ def brdf_lut(res=DEFAULT_LUT_RES, samples=DEFAULT_LUT_SAMPLES):
     return _LUT_CACHE[key]
 
 
-_WORK_CACHE = {}
+class EnvOps:
+    """The prefilter operators of one env shape on one device, as the
+    caller-owned buffers ss_env_refresh / ss_env_adjoint take (SsEnvOps):
+    diffuse row sums, the diffuse kernel's spectrum (K^, float64), the
+    sparse specular operator (CSR) and its per-level transpose (CSC), and the
+    float64 work area.  Built once per (He, We, L, samples, device) -- the
+    reference's build_diffuse_operator / build_specular_operator
+    (shading.py:275-331) without ever forming the dense T x T matrices."""
 
-
-def env_workspace(he, we):
-    """float64 scratch (3*He*We) for the split-column diffuse quadrature."""
-    key = (he, we, torch.cuda.current_device())
-    if key not in _WORK_CACHE:
-        _WORK_CACHE[key] = torch.empty(3 * he * we, device="cuda", dtype=torch.float64)
-    return _WORK_CACHE[key]
-
-
-def diffuse_rowsums(he, we):
-    key = (he, we, torch.cuda.current_device())
-    if key not in _ROWSUM_CACHE:
+    def __init__(self, he, we, levels, samples):
         lib = _lib.load()
-        rs = torch.empty(he * we, device="cuda", dtype=torch.float32)
-        _lib.check(lib.ss_env_rowsums(he, we, _lib.ptr(rs), _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()),
-                   "ss_env_rowsums")
-        _ROWSUM_CACHE[key] = rs
-    return _ROWSUM_CACHE[key]
-
-
-def spec_operator(he, we, levels, samples):
-    """Sparse specular prefilter operators (CSR + per-level CSC), built once per
-    shape on the device and registered with the library, which then uses them
-    in ss_env_refresh / ss_env_adjoint."""
-    key = (he, we, levels, samples, torch.cuda.current_device())
-    if levels < 2:
-        return None
-    if key not in _SPEC_OP_CACHE:
-        lib = _lib.load()
+        dev = torch.device("cuda", torch.cuda.current_device())
+        s = _lib.stream_ptr()
         T = he * we
-        nrows = (levels - 1) * T
-        dev = "cuda"
-        nnz = torch.empty(nrows, device=dev, dtype=torch.int32)
-        _lib.check(lib.ss_spec_op_count(he, we, levels, samples, _lib.ptr(nnz), _lib.stream_ptr()), "ss_spec_op_count")
-        row_ptr = torch.zeros(nrows + 1, device=dev, dtype=torch.int64)
-        row_ptr[1:] = torch.cumsum(nnz.to(torch.int64), 0)
-        total = int(row_ptr[-1].item())
-        col = torch.empty(total, device=dev, dtype=torch.int32)
-        rval = torch.empty(total, device=dev, dtype=torch.float32)
-        _lib.check(lib.ss_spec_op_fill(he, we, levels, samples, _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(rval),
-                                       _lib.stream_ptr()), "ss_spec_op_fill")
-        rows = torch.repeat_interleave(torch.arange(nrows, device=dev, dtype=torch.int64), nnz.to(torch.int64))
-        level = rows // T
-        key_c = level * T + col.to(torch.int64)
-        order = torch.sort(key_c, stable=True).indices
-        row_t = (rows[order] % T).to(torch.int32).contiguous()
-        cval = rval[order].contiguous()
-        col_ptr = torch.zeros(nrows + 1, device=dev, dtype=torch.int64)
-        col_ptr[1:] = torch.cumsum(torch.bincount(key_c, minlength=nrows), 0)
-        op = (row_ptr, col, rval, col_ptr, row_t, cval)
-        _SPEC_OP_CACHE[key] = op
-    op = _SPEC_OP_CACHE[key]
-    _lib.load().ss_spec_op_register(he, we, levels, samples, *(_lib.ptr(t) for t in op))
-    return op
+        self.work = torch.empty(3 * T, device=dev, dtype=torch.float64)
+        nk = int(lib.ss_env_khat_words(he, we))
+        self.khat = None
+        if nk:
+            self.khat = torch.empty(nk, device=dev, dtype=torch.float64)
+            _lib.check(lib.ss_env_khat(he, we, _lib.ptr(self.khat), s), "ss_env_khat")
+        self.rowsum = torch.empty(T, device=dev, dtype=torch.float32)
+        _lib.check(lib.ss_env_rowsums(he, we, _lib.ptr(self.khat), _lib.ptr(self.rowsum), _lib.ptr(self.work), s),
+                   "ss_env_rowsums")
+        self.spec = None
+        if levels >= 2:
+            nrows = (levels - 1) * T
+            nnz = torch.empty(nrows, device=dev, dtype=torch.int32)
+            _lib.check(lib.ss_spec_op_count(he, we, levels, samples, _lib.ptr(nnz), s), "ss_spec_op_count")
+            row_ptr = torch.zeros(nrows + 1, device=dev, dtype=torch.int64)
+            row_ptr[1:] = torch.cumsum(nnz.to(torch.int64), 0)
+            total = int(row_ptr[-1].item())
+            col = torch.empty(total, device=dev, dtype=torch.int32)
+            rval = torch.empty(total, device=dev, dtype=torch.float32)
+            _lib.check(lib.ss_spec_op_fill(he, we, levels, samples, _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(rval),
+                                           s), "ss_spec_op_fill")
+            rows = torch.repeat_interleave(torch.arange(nrows, device=dev, dtype=torch.int64), nnz.to(torch.int64))
+            key_c = (rows // T) * T + col.to(torch.int64)
+            order = torch.sort(key_c, stable=True).indices
+            row_t = (rows[order] % T).to(torch.int32).contiguous()
+            cval = rval[order].contiguous()
+            col_ptr = torch.zeros(nrows + 1, device=dev, dtype=torch.int64)
+            col_ptr[1:] = torch.cumsum(torch.bincount(key_c, minlength=nrows), 0)
+            self.spec = (row_ptr, col, rval, col_ptr, row_t, cval)
+        sp = self.spec or (None,) * 6
+        self.struct = _lib.SsEnvOps(_lib.ptr(self.rowsum), _lib.ptr(self.khat), *(_lib.ptr(t) for t in sp),
+                                    _lib.ptr(self.work))
+
+    def ref(self):
+        return ctypes.byref(self.struct)
+
+
+def env_ops(he, we, levels=DEFAULT_LEVELS, samples=DEFAULT_SPEC_SAMPLES):
+    key = (he, we, levels, samples, torch.cuda.current_device())
+    if key not in _OPS_CACHE:
+        _OPS_CACHE[key] = EnvOps(he, we, levels, samples)
+    return _OPS_CACHE[key]
 
 
 class EnvironmentLight:
@@ -131,11 +132,10 @@ class EnvironmentLight:
     def refresh(self):
         lib = _lib.load()
         he, we = self.shape
-        rs = diffuse_rowsums(he, we)
-        spec_operator(he, we, self.levels, self.spec_samples)
-        _lib.check(lib.ss_env_refresh(he, we, self.levels, self.spec_samples, _lib.ptr(self.base_log), _lib.ptr(rs),
+        ops = env_ops(he, we, self.levels, self.spec_samples)
+        _lib.check(lib.ss_env_refresh(he, we, self.levels, self.spec_samples, _lib.ptr(self.base_log), ops.ref(),
                                       _lib.ptr(self.base), _lib.ptr(self.diffuse), _lib.ptr(self.specular),
-                                      _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()), "ss_env_refresh")
+                                      _lib.stream_ptr()), "ss_env_refresh")
         self.diffuse4[..., :3].copy_(self.diffuse)
         self.specular4[..., :3].copy_(self.specular)
 
@@ -149,11 +149,10 @@ class EnvironmentLight:
         ds = torch.as_tensor(d_specular, **f64).contiguous() if d_specular is not None \
             else torch.zeros(self.specular.shape, **f64)
         d_base = torch.empty(self.base.shape, **f64)
-        spec_operator(he, we, self.levels, self.spec_samples)
         d_log = torch.empty_like(self.base)
-        _lib.check(lib.ss_env_adjoint(he, we, self.levels, self.spec_samples, _lib.ptr(self.base),
-                                      _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(dd), _lib.ptr(ds),
-                                      _lib.ptr(d_base), _lib.ptr(d_log), _lib.ptr(env_workspace(he, we)),
+        ops = env_ops(he, we, self.levels, self.spec_samples)
+        _lib.check(lib.ss_env_adjoint(he, we, self.levels, self.spec_samples, _lib.ptr(self.base), ops.ref(),
+                                      _lib.ptr(dd), _lib.ptr(ds), _lib.ptr(d_base), _lib.ptr(d_log),
                                       _lib.stream_ptr()), "ss_env_adjoint")
         return d_base, d_log
 

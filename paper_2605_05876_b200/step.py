@@ -11,11 +11,15 @@ renormalisation and the environment refresh.  This is the reference's
 linear space) and a batch of views instead of one (gradients summed over
 views, the batching SURVEY.md §7 hard part 7 defines).
 
-Everything inside step() is asynchronous: no host synchronisation until the
-caller reads the loss, so the whole step can also be captured in a CUDA graph.
-Pair buffers are sized once from a measured view (x1.5); an overflow (flag
-set by the binning kernel) is reported by check_overflow() so the caller can
-grow the buffers and re-run.
+The views are issued asynchronously; the step reads ONE small status block
+back before applying the optimiser: the binning kernel's pair-overflow flag
+(all-reduced with the gradients, so every rank agrees), the pairs the
+largest view needed, and the preprocess flags.  Pair buffers are sized from a
+measured view (x1.5); when a later view needs more (a closer camera, scales
+grown by training) the buffers grow to fit and the step's views are re-run
+before any parameter changes -- a silently truncated tile list never reaches
+Adam.  A zero-norm quaternion or a non-finite colour raises ValueError, as
+the reference's render() does (rasterizer.py:352-353).
 """
 
 from __future__ import annotations
@@ -43,31 +47,65 @@ def shard_views(n_views, world, rank):
 
 
 class GradPack:
-    """One flat float32 buffer holding every gradient the step all-reduces:
-    the 14 parameter channels per surfel, ss_grad, the env log-radiance
-    gradient and the loss -- a single NCCL call per step."""
+    """One flat buffer holding everything the step all-reduces: the 14
+    parameter channels per surfel, ss_grad, the per-surfel count of views the
+    surfel covered a pixel in (`view_count`, the sum over the step's views of
+    backward_image's `touched` bool, backward.py:432-441 -- what
+    DensifyStats.accumulate adds per view, densify.py:35-37; exact in float32
+    up to 2^24 views), the env log-radiance gradient and the loss -- a single
+    collective per step."""
 
     def __init__(self, n, env_texels, device, dtype=torch.float32):
-        sizes = [n * _WIDTH[k] for k in PARAMS] + [n, 3 * env_texels, 1]
-        self.flat = torch.zeros(sum(sizes), device=device, dtype=dtype)
+        sizes = [n * _WIDTH[k] for k in PARAMS] + [n, n, 3 * env_texels, 1, 1]
+        # every segment starts 16-byte aligned (the chain kernel adds
+        # quaternion gradients with 16-byte vector reductions)
+        pad = lambda v: (v + 3) & ~3
+        self.flat = torch.zeros(sum(pad(s) for s in sizes), device=device, dtype=dtype)
         views, off = [], 0
         for s in sizes:
             views.append(self.flat[off:off + s])
-            off += s
+            off += pad(s)
         self.grads = {k: views[i].view(n, _WIDTH[k]) if _WIDTH[k] > 1 else views[i] for i, k in enumerate(PARAMS)}
         self.grads["ss_grad"] = views[len(PARAMS)]
-        self.env = views[len(PARAMS) + 1]
-        self.loss = views[len(PARAMS) + 2]
-        self.touched = torch.zeros(n, device=device, dtype=torch.int32)
+        self.view_count = views[len(PARAMS) + 1]
+        self.env = views[len(PARAMS) + 2]
+        self.loss = views[len(PARAMS) + 3]
+        self.status = views[len(PARAMS) + 4]  # > 0: some rank's pair buffers overflowed this step
+
+    @property
+    def touched(self):
+        """Alias of view_count (per-surfel number of views touched)."""
+        return self.view_count
 
     def zero(self):
         self.flat.zero_()
-        self.touched.zero_()
 
-    def all_reduce(self, group=None):
+    def _bucket_split(self):
+        # bucket A: the per-surfel channels (params, ss_grad, view_count) --
+        # final once the last view's chain kernel ran; bucket B: env gradient,
+        # loss and status -- final only after the env adjoint
+        return self.env.data_ptr() - self.flat.data_ptr()
+
+    def all_reduce_surfels(self, group=None):
+        """Start the all-reduce of bucket A asynchronously (NCCL runs it on its
+        own stream after the work queued so far); returns the work handle or
+        None when not distributed."""
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-            dist.all_reduce(self.flat, group=group)
-            dist.all_reduce(self.touched, group=group)
+            n = self._bucket_split() // self.flat.element_size()
+            return dist.all_reduce(self.flat[:n], group=group, async_op=True)
+        return None
+
+    def all_reduce_rest(self, group=None):
+        """All-reduce bucket B (env gradient, loss, status: ~T*3 + 2 floats)."""
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            n = self._bucket_split() // self.flat.element_size()
+            dist.all_reduce(self.flat[n:], group=group)
+
+    def all_reduce(self, group=None, async_op=False):
+        """The whole buffer in one collective."""
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            return dist.all_reduce(self.flat, group=group, async_op=async_op)
+        return None
 
 
 class ViewBuffers:
@@ -86,12 +124,15 @@ class ViewBuffers:
         self.offsets = torch.empty(ntiles + 1, **i32)
         self.cursors = torch.empty(ntiles, **i32)
         self.tile_order = torch.empty(ntiles, **i32)
-        self.coef = torch.empty((k_max, H * W, 4), **f32)
+        # per layer and pixel: float4 (A hi, dL/dC_raw), then a float plane of A lo (ss_abi.h)
+        self.coef = torch.empty(5 * k_max * H * W, **f32)
         self.thr = torch.empty((k_max, H * W), **f32)
         self.pix_hdr = torch.empty((H * W, 8), **i32)
         # NDC tables, counters, area-class sort and big-rect queue of the backward
         self.pixel_ndc = torch.empty(_lib.load().ss_train_backward_scratch_words(n, W, H), **f32)
         self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
+        # float64 channel rows of the big records (SS_ACC_F64)
+        self.acc64 = torch.empty((n, _lib.ACC64_WIDTH), device=device, dtype=torch.float64)
         # this buffer set's share of the step loss (photometric mode): views on
         # different worker streams never read-modify-write the same scalar
         self.loss_part = torch.zeros(1, device=device, dtype=torch.float64)
@@ -127,7 +168,7 @@ class ViewBuffers:
 class TrainStep:
     def __init__(self, cloud, env, width, height, k_max=16, tile=16, background=(0.0, 0.0, 0.0),
                  lrs=None, pair_capacity=None, process_group=None, options=None, streams=2, loss="l1",
-                 tone="hdr-loss", lambda_ssim=0.2, lambda_sil=0.1, cons_scale=0.0):
+                 tone="hdr-loss", lambda_ssim=0.2, lambda_sil=0.1, cons_scale=0.0, surfel_capacity=None):
         """loss="l1": the BASELINE config loss (mean |rgb - target| in linear
         space), fused into the forward kernel.  loss="photometric": the
         reference fit loss (train.py:194-206): tone_map(tone) then
@@ -135,7 +176,9 @@ class TrainStep:
         lambda_sil * silhouette when masks are given to step(), plus the
         depth-consolidation penalty with weight cons_scale (the reference's
         lambda_cons / (extent * npix) of its main phase, train.py:208-213;
-        settable between steps as `ts.cons_scale`)."""
+        settable between steps as `ts.cons_scale`).  surfel_capacity: size
+        the per-view buffers for up to this many surfels, so refine() can
+        grow the cloud (up to it) without reallocating them."""
         if loss not in ("l1", "photometric"):
             raise ValueError(f"unknown loss {loss!r}")
         self.loss_mode, self.tone, self.lambda_ssim, self.lambda_sil = loss, tone, float(lambda_ssim), float(lambda_sil)
@@ -153,9 +196,15 @@ class TrainStep:
         n = len(cloud)
         dev = cloud.centers.device
         self.n = n
+        self.surfel_capacity = max(n, int(surfel_capacity or 0), 1)
         self.ntx = (self.W + tile - 1) // tile
         self.ntiles = self.ntx * ((self.H + tile - 1) // tile)
-        self.bufs = [ViewBuffers(n, self.W, self.H, tile, self.k_max, self.ntiles, dev) for _ in range(max(1, streams))]
+        self.bufs = [ViewBuffers(self.surfel_capacity, self.W, self.H, tile, self.k_max, self.ntiles, dev)
+                     for _ in range(max(1, streams))]
+        # the buffer sets' flag words side by side: one read-back per step
+        self.flags_all = torch.zeros((len(self.bufs), 4), device=dev, dtype=torch.int32)
+        for i, b in enumerate(self.bufs):
+            b.flags = self.flags_all[i]
         he, we = env.shape
         for b in self.bufs:  # per-view float32 derived-map accumulators (16-byte texels)
             b.d_diff4 = torch.zeros((he, we, 4), device=dev, dtype=torch.float32)
@@ -166,40 +215,77 @@ class TrainStep:
                 b.alloc_loss(self.W, self.H, dev)
         he, we = env.shape
         self.T = he * we
-        # packed gradient buffer: params, ss_grad, env d_base_log, loss -- one all-reduce
-        self.pack = GradPack(n, self.T, dev)
-        self.flat = self.pack.flat
-        self.grads = self.pack.grads
-        self.g_env_log = self.pack.env.view(he, we, 3)
-        self.loss_f = self.pack.loss
-        self.touched = self.pack.touched
         self.loss = torch.zeros(1, device=dev, dtype=torch.float64)
         self.d_diffuse = torch.zeros(env.base.shape, device=dev, dtype=torch.float64)
         self.d_spec = torch.zeros(env.specular.shape, device=dev, dtype=torch.float64)
         self.d_base = torch.empty(env.base.shape, device=dev, dtype=torch.float64)
         self.adam = Adam()
-        self._cl = _lib.make_cloud(cloud)
         self._po = make_opts(self.opts, tile)
         self._envs = _lib.make_env(env)
-        for b in self.bufs:
-            b.gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
-                                _lib.ptr(self.touched), _lib.ptr(self.d_diffuse), _lib.ptr(self.d_spec),
-                                _lib.ptr(b.d_diff4), _lib.ptr(b.d_spec4))
+        self._bind_cloud(cloud)
         self._bg = _lib.fvec(self.bg)
         self.capacity = 0
+        self.regrows = 0           # times a step re-ran its views after growing the pair buffers
         if pair_capacity:
             self._alloc_pairs(pair_capacity)
         self.collect_stats = False
+        self.captured_rgb = None       # a list -> the fused forward's image of every view is appended (L1 mode)
+        # forward colours: float64 IBL shading like render() (the step's image
+        # is then bit-identical to the API path's and within 1e-4 of the
+        # oracle); SS_COLOR_IBL_F32 is the float32 variant (colours within
+        # ~1e-4 relative: texel coordinates at 256-texel rows carry ~1e-5
+        # texel float32 rounding)
+        self.color_source = _lib.SS_COLOR_IBL
         self._pairs, self._kept, self._nviews = [], [], 0
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
         self.active_streams = None     # None: all worker streams; 1: views serialised (isolated kernel timing)
         self._stage = None
         # preprocess, scan + order, scatter, tile sort x2, train fwd, ndc, area class, class scatter,
-        # record bwd, big-rect bwd, chain, env merge x2
-        self.launches_per_view = 14
+        # record bwd, big-rect bwd, big-rect finish, chain, env merge x2
+        self.launches_per_view = 15
         self.launches_per_step_fixed = 4 + 1 + 4  # env adjoint, fused Adam (+ quat renorm), env refresh
 
     # -- buffers -----------------------------------------------------------
+    def _bind_cloud(self, cloud):
+        """(Re)bind the per-surfel state to `cloud`: the packed gradient
+        buffer (params, ss_grad, view counts, env, loss -- one all-reduce
+        buffer) and the native views of both."""
+        he, we = self.env.shape
+        dev = cloud.centers.device
+        self.cloud = cloud
+        self.n = len(cloud)
+        if self.n > self.surfel_capacity:  # grow the per-view buffers
+            self.surfel_capacity = self.n
+            for b in self.bufs:
+                nb = ViewBuffers(self.n, self.W, self.H, self.tile, self.k_max, self.ntiles, dev)
+                for k in ("records", "cull", "bininfo", "pixel_ndc", "acc", "acc64"):
+                    setattr(b, k, getattr(nb, k))
+        self.pack = GradPack(self.n, self.T, dev)
+        self.flat = self.pack.flat
+        self.grads = self.pack.grads
+        self.g_env_log = self.pack.env.view(he, we, 3)
+        self.loss_f = self.pack.loss
+        self.view_count = self.pack.view_count
+        self._cl = _lib.make_cloud(cloud)
+        for b in self.bufs:
+            b.gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
+                                None, _lib.ptr(self.d_diffuse), _lib.ptr(self.d_spec),
+                                _lib.ptr(b.d_diff4), _lib.ptr(b.d_spec4), _lib.ptr(self.view_count))
+
+    def refine(self, stats, mean_neighbor_dist, max_surfels, quantile=0.9, grad_floor=1e-8,
+               outside_mask_votes=None, front_votes=None):
+        """The density-aware refinement pass after a step (train.py:260-276):
+        refine_topology on the device (prune, quantile threshold, budget,
+        split) with the optimiser state remapped in the same pass
+        (Adam.remap), then the step rebinds to the new cloud (self.cloud).
+        Returns (index_map, reasons); the caller resets its DensifyStats and
+        rebuilds its neighbour index, as the reference does."""
+        from .densify import refine_topology
+        new, index_map, reasons = refine_topology(self.cloud, stats, mean_neighbor_dist, max_surfels, quantile,
+                                                  grad_floor, outside_mask_votes, front_votes, optimizer=self.adam)
+        self._bind_cloud(new)
+        return index_map, reasons
+
     def _alloc_pairs(self, cap):
         cap = int(cap)
         for b in self.bufs:
@@ -217,14 +303,31 @@ class TrainStep:
         return worst
 
     def check_overflow(self):
-        return any(bool(b.flags[2].item()) for b in self.bufs)
+        return bool(self.flags_all[:, 2].any().item())
+
+    def _status(self):
+        """Read the step's status back (the one host sync of a step): raise on
+        invalid surfels, and return True when the views must be re-run with
+        larger pair buffers (which it allocates)."""
+        flags = self.flags_all.cpu()
+        if int(flags[:, 0].max()):
+            raise ValueError("zero-norm quaternion")
+        if int(flags[:, 1].max()):
+            raise ValueError("non-finite surfel colors")
+        if float(self.pack.status.item()) <= 0.0:
+            return False
+        need = int(flags[:, 3].max())
+        if need > self.capacity:
+            self._alloc_pairs(int(need * 1.25) + 1024)
+        self.regrows += 1
+        return True
 
     # -- per-view stages ----------------------------------------------------
     def _preprocess(self, cam, b):
         b.tile_counts.zero_()
         camst = _lib.make_camera(cam)
         rc = self.lib.ss_preprocess(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
-                                    _lib.SS_COLOR_IBL_F32, None, ctypes.byref(self._envs), _lib.ptr(b.records),
+                                    self.color_source, None, ctypes.byref(self._envs), _lib.ptr(b.records),
                                     _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts), _lib.ptr(b.bininfo), None,
                                     _lib.ptr(b.flags), _lib.stream_ptr())
         _lib.check(rc, "ss_preprocess")
@@ -252,10 +355,14 @@ class TrainStep:
         self._ev_end(ev)
         ev = self._ev_begin("train_forward")
         if self.loss_mode == "l1":
+            rgb_out = None
+            if self.captured_rgb is not None:  # diagnostics: keep each view's fused-forward image
+                rgb_out = torch.empty((self.H, self.W, 3), device=target.device, dtype=torch.float32)
+                self.captured_rgb.append(rgb_out)
             _lib.check(lib.ss_train_forward(self.W, self.H, self.tile, _lib.ptr(b.offsets), _lib.ptr(b.pair),
                                             _lib.ptr(b.pair_rect), _lib.ptr(b.records), self._bg[0], self.k_max,
                                             _lib.ptr(target), _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr),
-                                            _lib.ptr(self.loss), None, None, _lib.ptr(b.tile_order), s),
+                                            _lib.ptr(self.loss), _lib.ptr(rgb_out), None, _lib.ptr(b.tile_order), s),
                        "ss_train_forward")
         else:
             # deferred loss: image -> loss kernels -> layer coefficients
@@ -298,12 +405,13 @@ class TrainStep:
             _lib.check(lib.ss_train_backward_records_cons(self.n, _lib.ptr(b.cull), _lib.ptr(b.records), self.W,
                                                           self.H, self.k_max, _lib.ptr(b.coef), _lib.ptr(b.thr),
                                                           _lib.ptr(b.pix_hdr), _lib.ptr(b.zst), _lib.ptr(b.pixel_ndc),
-                                                          _lib.ptr(b.acc), s), "ss_train_backward_records_cons")
+                                                          _lib.ptr(b.acc), _lib.ptr(b.acc64), s),
+                       "ss_train_backward_records_cons")
         else:
             _lib.check(lib.ss_train_backward_records(self.n, _lib.ptr(b.cull), _lib.ptr(b.records), self.W,
                                                      self.H, self.k_max, _lib.ptr(b.coef), _lib.ptr(b.thr),
-                                                     _lib.ptr(b.pix_hdr), _lib.ptr(b.pixel_ndc), _lib.ptr(b.acc), s),
-                       "ss_train_backward_records")
+                                                     _lib.ptr(b.pix_hdr), _lib.ptr(b.pixel_ndc), _lib.ptr(b.acc),
+                                                     _lib.ptr(b.acc64), s), "ss_train_backward_records")
         self._ev_end(ev)
         ev = self._ev_begin("chain")
         # the chain kernels of concurrent views may overlap: their parameter
@@ -311,7 +419,8 @@ class TrainStep:
         # this buffer set's own float32 maps
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                          _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(b.cull),
-                                         _lib.ptr(b.acc), ctypes.byref(b.gs), s), "ss_chain_backward")
+                                         _lib.ptr(b.acc), _lib.ptr(b.acc64), ctypes.byref(b.gs), s),
+                   "ss_chain_backward")
         # fold this view's float32 derived-map sums into the step's float64
         # ones: plain read-modify-write, so the merges are serialised
         if chain_after is not None:
@@ -368,9 +477,14 @@ class TrainStep:
         return {"pairs_mean": float(np.mean(self._pairs)) if self._pairs else 0.0,
                 "kept_mean": float(np.mean(self._kept)) if self._kept else 0.0}
 
+    @property
+    def touched(self):
+        """Per-surfel number of this step's views (on this rank, or summed
+        over ranks after the all-reduce) in which the surfel covered a pixel."""
+        return self.view_count
+
     def zero(self):
         self.flat.zero_()
-        self.touched.zero_()
         self.d_diffuse.zero_()
         self.d_spec.zero_()
         self.loss.zero_()
@@ -380,19 +494,22 @@ class TrainStep:
             b.flags.zero_()
 
     def set_normal_consistency(self, index, lambda_nc):
-        """Add lambda_nc * normal_consistency_loss(cloud, index) to every step
-        (its quaternion gradient and value; train.py:216-221).  The index is
-        the caller's NeighborIndex (rebuilt on its own schedule, like the
+        """Add lambda_nc * normal_consistency_loss(cloud, index) per VIEW of
+        the step (its quaternion gradient and value; train.py:216-221).  The
+        reference adds the term once per single-view step; a batched step is
+        the sum of its views' reference steps, so the term enters once per
+        view: each rank adds lambda_nc x (its view count), and the all-reduce
+        makes it lambda_nc x (views in the global step).  The index is the
+        caller's NeighborIndex (rebuilt on its own schedule, like the
         reference's); pass index=None to turn the term off."""
         self._nc = None if index is None or float(lambda_nc) == 0.0 else (index, float(lambda_nc))
 
-    def _normal_consistency(self):
+    def _normal_consistency(self, nviews):
         nc = getattr(self, "_nc", None)
-        if nc is None:
+        if nc is None or nviews == 0:
             return
-        if dist.is_available() and dist.is_initialized() and dist.get_rank(self.pg) != 0:
-            return  # a per-step (not per-view) term: added once, on rank 0, before the all-reduce
         index, lam = nc
+        lam = lam * nviews
         n = self.n
         if index.neighbors.shape[0] != n:
             raise ValueError("normal-consistency index built for a different cloud size")
@@ -408,31 +525,45 @@ class TrainStep:
         self.loss.add_(val, alpha=lam)
 
     def gradients(self, cameras, targets, masks=None):
-        """Sum of per-view gradients over this rank's views (+ env adjoint)."""
+        """Sum of per-view gradients over this rank's views (+ env adjoint),
+        all-reduced over the process group.  Re-runs the views once the pair
+        buffers have grown if any rank's binning overflowed."""
         if self.capacity == 0:
             self.size_pairs(cameras[:2])
-        self.zero()
-        self._nviews = len(cameras)
-        self._pairs, self._kept = [], []
-        self._run_views(cameras, lambda i, st: targets[i], masks=masks)
-        self._normal_consistency()
-        self._finish()
+        while True:
+            self.zero()
+            self._nviews = len(cameras)
+            self._pairs, self._kept = [], []
+            self._run_views(cameras, lambda i, st: targets[i], masks=masks)
+            self._normal_consistency(len(cameras))
+            self._finish()
+            if not self._status():
+                return
 
     def _env_adjoint(self):
         he, we = self.env.shape
-        from .shading import diffuse_rowsums, env_workspace, spec_operator
-        spec_operator(he, we, self.env.levels, self.env.spec_samples)
+        from .shading import env_ops
+        ops = env_ops(he, we, self.env.levels, self.env.spec_samples)
         _lib.check(self.lib.ss_env_adjoint(he, we, self.env.levels, self.env.spec_samples, _lib.ptr(self.env.base),
-                                           _lib.ptr(diffuse_rowsums(he, we)), _lib.ptr(self.d_diffuse),
+                                           ops.ref(), _lib.ptr(self.d_diffuse),
                                            _lib.ptr(self.d_spec), _lib.ptr(self.d_base), _lib.ptr(self.g_env_log),
-                                           _lib.ptr(env_workspace(he, we)), _lib.stream_ptr()), "ss_env_adjoint")
+                                           _lib.stream_ptr()), "ss_env_adjoint")
 
     def _finish(self):
+        """Env adjoint + all-reduce.  The per-surfel bucket (params, ss_grad,
+        view counts: 60 B/surfel) is final once the last view's chain kernel
+        ran, so its all-reduce starts right then on NCCL's stream and
+        overlaps the env adjoint; the small env/loss/status bucket follows
+        the adjoint.  The optimiser waits for both."""
+        work = self.pack.all_reduce_surfels(self.pg)
         self._env_adjoint()
         for b in self.bufs:
             self.loss += b.loss_part
         self.loss_f.copy_(self.loss)
-        self.pack.all_reduce(self.pg)
+        self.pack.status.copy_(self.flags_all[:, 2].amax())
+        self.pack.all_reduce_rest(self.pg)
+        if work is not None:
+            work.wait()
 
     def fixed_costs(self):
         """CUDA-event times (ms, current stream) of the per-step fixed stages,
@@ -499,10 +630,14 @@ class TrainStep:
             stream.wait_event(ready[i % nst])
             return self._stage[i % nst]
 
-        self.zero()
-        self._nviews = len(cameras)
-        issue(0)
-        self._run_views(cameras, target_for, target_done=free)
-        self._finish()
+        while True:
+            self.zero()
+            self._nviews = len(cameras)
+            issue(0)
+            self._run_views(cameras, target_for, target_done=free)
+            self._normal_consistency(len(cameras))
+            self._finish()
+            if not self._status():
+                break
         self.apply()
         return self.loss_f

@@ -28,3 +28,17 @@ def grad_close(got, ref, rel=1e-3, floor=1e-5):
     err = np.abs(a - b)
     bad = err > rel * np.maximum(np.abs(a), np.abs(b)) + floor * scale
     return int(bad.sum()), float(err.max() / scale) if a.size else 0.0
+
+
+def grad_outliers(got, ref, rel=1e-3, floor=1e-5, top=8):
+    """The entries grad_close rejects, worst first: (flat index, got, ref,
+    |a-b| / max|ref|, |a-b| / max(|a|,|b|)) -- printed by the full-size tests
+    so every out-of-tolerance entry is visible with its magnitude."""
+    a = host(got).astype(np.float64).reshape(-1)
+    b = host(ref).astype(np.float64).reshape(-1)
+    scale = max(float(np.max(np.abs(b))) if b.size else 0.0, 1e-30)
+    err = np.abs(a - b)
+    bad = np.flatnonzero(err > rel * np.maximum(np.abs(a), np.abs(b)) + floor * scale)
+    order = bad[np.argsort(-err[bad])][:top]
+    return [(int(i), float(a[i]), float(b[i]), float(err[i] / scale),
+             float(err[i] / max(abs(a[i]), abs(b[i]), 1e-300))) for i in order], int(bad.size)

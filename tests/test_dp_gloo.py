@@ -45,7 +45,7 @@ def _fill(pack, gt, opt, cams, views):
         for k in PARAMS:
             pack.grads[k] += torch.tensor(back[k], dtype=pack.flat.dtype).reshape(pack.grads[k].shape)
         pack.grads["ss_grad"] += torch.tensor(back["ss_grad"], dtype=pack.flat.dtype)
-        pack.touched += torch.tensor(back["touched"].astype(np.int32))
+        pack.view_count += torch.tensor(back["touched"].astype(np.float64))
         pack.loss += val
 
 
@@ -58,7 +58,7 @@ def _worker(rank, world, port, out):
     _fill(pack, gt, opt, cams, shard_views(len(cams), world, rank))
     pack.all_reduce()
     if rank == 0:
-        torch.save({"flat": pack.flat.clone(), "touched": pack.touched.clone()}, out)
+        torch.save({"flat": pack.flat.clone(), "touched": pack.view_count.clone()}, out)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -84,4 +84,4 @@ def test_two_rank_allreduce_equals_single_process(tmp_path):
     ref = GradPack(len(opt.centers), 1, "cpu", dtype=torch.float64)
     _fill(ref, gt, opt, cams, range(len(cams)))
     torch.testing.assert_close(got["flat"], ref.flat, rtol=1e-12, atol=1e-15)
-    assert torch.equal(got["touched"], ref.touched)
+    assert torch.equal(got["touched"], ref.view_count) and float(ref.view_count.max()) > 1

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 import torch
 
-from parity import grad_close, host, image_close
+from parity import grad_close, grad_outliers, host, image_close
 
 pytestmark = pytest.mark.gpu
 
@@ -25,6 +25,26 @@ from paper_2605_05876_b200.step import PARAMS, TrainStep  # noqa: E402
 
 def _oracle_env(base_log, levels=6):
     return O.EnvOracle(np.asarray(base_log, np.float64), levels=levels)
+
+
+def _check_step_grads(ts, og, label, ores=None):
+    """Every parameter channel, ss_grad and the env gradient of a training
+    step vs the oracle's backward_image: 0 entries outside the gradient
+    tolerance (north_star: 1e-3 relative, with the 1e-5 x array-scale floor
+    of tests/parity.py); outliers are listed with their magnitudes.  The
+    per-view touched flags equal the step's view counts (1 view)."""
+    report = {}
+    if ores is not None:  # the step's float32-shaded image vs the oracle's float64 one
+        bad, err = image_close(ts.captured_rgb[-1], ores.rgb)
+        assert bad == 0, (label, "fused-forward image", bad, err)
+    pairs = [(k, ts.grads[k], og[k]) for k in PARAMS]
+    pairs += [("ss_grad", ts.grads["ss_grad"], og["ss_grad"]), ("env_base_log", ts.g_env_log, og["env_base_log"])]
+    for k, got, ref in pairs:
+        outl, nbad = grad_outliers(got, ref)
+        if nbad:
+            report[k] = (nbad, outl)
+    assert not report, f"{label}: gradient entries outside tolerance: {report}"
+    np.testing.assert_array_equal(host(ts.view_count), og["touched"].astype(np.float32))
 
 
 @pytest.fixture(scope="module")
@@ -59,6 +79,7 @@ def test_config2_training_gradients_full_size(config2):
     target = ss.render(ss.SurfelCloud(**gt), cam, ss.RenderOptions(), env=env).rgb.contiguous()
     cloud = ss.SurfelCloud(**opt)
     ts = TrainStep(cloud, env, 800, 800)
+    ts.captured_rgb = []
     ts.gradients([cam], [target])
     oenv = _oracle_env(base_log)
     co = SimpleNamespace(**opt)
@@ -66,19 +87,15 @@ def test_config2_training_gradients_full_size(config2):
     val, _ = O.photometric_l1(ores.rgb, host(target))
     assert float(ts.loss_f.item()) / (800 * 800 * 3) == pytest.approx(val, rel=1e-4)
     # L1's sign(rgb - target) is discontinuous: pixels whose residual is below
-    # the float32/float64 rounding of the image can flip sign between the two
-    # implementations.  Feed the oracle the B200 image's sign pattern (the
-    # fused kernel's rgb is bit-identical to render()'s) so the comparison
-    # isolates the backward pass.
-    rgb = host(ss.render(cloud, cam, ss.RenderOptions(), env=env).rgb).astype(np.float64)
+    # the rounding of the image (the step shades in float32, the oracle in
+    # float64: colours differ by ~1e-7 relative) can flip sign between the
+    # two implementations, and one flipped pixel moves every gradient of the
+    # few surfels covering it.  Feed the oracle the sign pattern of the
+    # step's own fused-forward image so the comparison isolates the backward.
+    rgb = host(ts.captured_rgb[-1]).astype(np.float64)  # the step's own image (float32 shading)
     g = np.sign(rgb - host(target)) / rgb.size
     og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
-    for k in PARAMS:
-        bad, err = grad_close(ts.grads[k], og[k])
-        assert bad <= 1e-4 * og[k].size, (k, bad, err)
-    np.testing.assert_array_equal(host(ts.touched) > 0, og["touched"])
-    bad, err = grad_close(ts.g_env_log, og["env_base_log"])
-    assert bad == 0, err
+    _check_step_grads(ts, og, "config2", ores)
 
 
 def test_config3_kmax_stress():
@@ -96,25 +113,61 @@ def test_config3_kmax_stress():
 
 
 def test_config3_training_backward_kmax():
-    """The walk-free training backward reproduces the k_max stop."""
+    """The walk-free training backward reproduces the k_max stop: gradients
+    vs the ORACLE's backward_image (not the CUDA API path)."""
     cl = scenes.config3(2, 60_000)
     cam = ss.fibonacci_cameras(16, 3.5, 256, 256)[1]
-    env_base = scenes.env_lognormal(16, 32, 3)
-    env = ss.EnvironmentLight.from_base(env_base)
+    base_log = np.log(scenes.env_lognormal(16, 32, 3))
+    env = ss.EnvironmentLight(base_log)
     rng = np.random.default_rng(4)
     target = torch.tensor(rng.uniform(0, 1, (256, 256, 3)), device="cuda", dtype=torch.float32)
     cloud = ss.SurfelCloud(**cl)
     ts = TrainStep(cloud, env, 256, 256)
+    ts.captured_rgb = []
     ts.gradients([cam], [target])
+    oenv = _oracle_env(base_log)
+    co = SimpleNamespace(**cl)
+    ores = O.render(co, cam, env=oenv)
+    assert ores.discarded > 0 and int(ores.nlayers.max()) == 16
+    rgb = host(ts.captured_rgb[-1]).astype(np.float64)  # the step's own image (float32 shading)
+    g = np.sign(rgb - host(target)) / rgb.size
+    og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
+    _check_step_grads(ts, og, "config3-small")
+
+
+def test_config3_full_size_vs_oracle():
+    """BASELINE config 3 at full size: 500k surfels on 16 concentric shells,
+    1024x1024, env 64x128 -- tile lists and sort order bit-exact, layer
+    counts (k_max = 16 stop) and the discarded-record statistic exact,
+    images within 1e-4, training gradients vs the oracle
+    (rasterizer.py:168-196, backward.py:86-320)."""
+    cl = scenes.config3(0, 500_000)
+    base_log = np.log(scenes.env_lognormal(64, 128, 3))
+    cam = ss.fibonacci_cameras(16, 3.5, 1024, 1024)[3]
+    env = ss.EnvironmentLight(base_log)
+    gt_cloud = ss.SurfelCloud(**cl)
+    opt = scenes.perturb(cl, 1)
+    target = ss.render(gt_cloud, cam, ss.RenderOptions(), env=env).rgb.contiguous()
+    cloud = ss.SurfelCloud(**opt)
     res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
-    val, g = ss.photometric_loss(res.rgb, target, lambda_ssim=0.0)
-    back = ss.backward_image(cloud, res, g_rgb=g)
-    for k in PARAMS:
-        # two float32 pipelines with different summation orders (record-
-        # parallel vs pixel-parallel): the floor is 1e-4 of the array scale
-        bad, err = grad_close(ts.grads[k], getattr(back, k).reshape(ts.grads[k].shape), floor=1e-4)
-        assert bad == 0, (k, err)
-    assert torch.equal(ts.touched > 0, back.touched)
+    oenv = _oracle_env(base_log)
+    co = SimpleNamespace(**opt)
+    ores = O.render(co, cam, env=oenv)
+    np.testing.assert_array_equal(host(res.tile_offsets), ores.tile_offsets)
+    np.testing.assert_array_equal(host(res.pair_rec), ores.pair_rec)
+    np.testing.assert_array_equal(host(res.nlayers), ores.nlayers)
+    assert int(ores.nlayers.max()) == 16 and ores.discarded > 1_000_000
+    assert res.stats["discarded_overflow"] == ores.discarded
+    for k in ("rgb", "alpha", "depth"):
+        bad, err = image_close(getattr(res, k), getattr(ores, k))
+        assert bad == 0, (k, bad, err)
+    ts = TrainStep(cloud, env, 1024, 1024)
+    ts.captured_rgb = []
+    ts.gradients([cam], [target])
+    rgb = host(ts.captured_rgb[-1]).astype(np.float64)  # the step's own image (float32 shading)
+    g = np.sign(rgb - host(target)) / rgb.size
+    og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
+    _check_step_grads(ts, og, "config3", ores)
 
 
 def test_config0_step_full_size():
@@ -126,18 +179,15 @@ def test_config0_step_full_size():
     target = ss.render(ss.SurfelCloud(**gt), cam, ss.RenderOptions(), env=env).rgb.contiguous()
     cloud = ss.SurfelCloud(**opt)
     ts = TrainStep(cloud, env, 128, 128)
+    ts.captured_rgb = []
     ts.gradients([cam], [target])
     oenv = _oracle_env(base_log)
     co = SimpleNamespace(**opt)
     ores = O.render(co, cam, env=oenv)
-    rgb = host(ss.render(cloud, cam, ss.RenderOptions(), env=env).rgb).astype(np.float64)
+    rgb = host(ts.captured_rgb[-1]).astype(np.float64)  # the step's own image (float32 shading)
     g = np.sign(rgb - host(target)) / rgb.size  # same L1 sign pattern on both sides
     og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
-    for k in PARAMS:
-        bad, err = grad_close(ts.grads[k], og[k])
-        assert bad == 0, (k, err)
-    bad, err = grad_close(ts.g_env_log, og["env_base_log"])
-    assert bad == 0, err
+    _check_step_grads(ts, og, "config0", ores)
 
 
 def test_config1_training_gradients_full_size():
@@ -160,13 +210,9 @@ def test_config1_training_gradients_full_size():
     bad, err = image_close(res.rgb, ores.rgb)
     assert bad == 0, err
     ts = TrainStep(cloud, env, 512, 512)
+    ts.captured_rgb = []
     ts.gradients([cam], [target])
-    rgb = host(res.rgb).astype(np.float64)
+    rgb = host(ts.captured_rgb[-1]).astype(np.float64)  # the step's own image (float32 shading)
     g = np.sign(rgb - host(target)) / rgb.size  # same L1 sign pattern on both sides
     og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
-    for k in PARAMS:
-        bad, err = grad_close(ts.grads[k], og[k])
-        assert bad <= 1e-4 * og[k].size, (k, bad, err)
-    np.testing.assert_array_equal(host(ts.touched) > 0, og["touched"])
-    bad, err = grad_close(ts.g_env_log, og["env_base_log"])
-    assert bad == 0, err
+    _check_step_grads(ts, og, "config1", ores)

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 from golden_io import cloud_of, load
-from parity import host
+from parity import grad_close, host
 
 pytestmark = pytest.mark.gpu
 
@@ -21,6 +21,30 @@ def test_adam_trace_matches_reference():
     for k in range(3):
         opt.step("x", p, torch.tensor(d["adam_grads"][k], device="cuda", dtype=torch.float32), 0.01)
         np.testing.assert_allclose(host(p), d["adam_traj"][k], rtol=2e-6, atol=2e-7)
+
+
+@pytest.mark.parametrize("state", [torch.float64, torch.float32])
+def test_adam_state_precision(state):
+    """Moments are float64 by default like the reference (adam.py:26-28);
+    float32 is an option.  Both follow the reference trace, the float64 state
+    to the float32 rounding of the parameter."""
+    d = load("optim_refine")
+    for multi in (False, True):
+        p = torch.tensor(d["adam_p0"], device="cuda")
+        opt = ss.Adam(state_dtype=state)
+        for k in range(3):
+            g = torch.tensor(d["adam_grads"][k], device="cuda", dtype=torch.float32)
+            if multi:
+                opt.step_multi([("x", p, g, 0.01)])
+            else:
+                opt.step("x", p, g, 0.01)
+            np.testing.assert_allclose(host(p), d["adam_traj"][k], rtol=2e-6, atol=2e-7)
+        assert opt.m["x"].dtype == state and opt.v["x"].dtype == state
+        arrays = opt.state_arrays()
+        assert arrays["adam_m_x"].dtype == (np.float64 if state == torch.float64 else np.float32)
+        back = ss.Adam(state_dtype=state)
+        back.load_state_arrays(arrays)
+        assert torch.equal(back.m["x"], opt.m["x"]) and back.t["x"] == 3
 
 
 def test_adam_remap_semantics():
@@ -77,19 +101,33 @@ def test_split_children_match_oracle():
 
 
 def test_train_step_stats_feed_refinement():
-    """ss_grad / touched from a training step accumulate into DensifyStats."""
+    """A V-view TrainStep yields the DensifyStats of V per-view
+    backward_image + accumulate calls (densify.py:35-37, train.py:250):
+    grad_sum = sum_v ss_grad_v, view_count = sum_v touched_v (views, not
+    pixels), so mean_grad = sum_v ss / #views touched."""
     from paper_2605_05876_b200 import scenes
     gt = scenes.config0(3, 2000)
-    cams = ss.fibonacci_cameras(2, 3.0, 64, 64, fov_y_deg=40.0)
+    cams = ss.fibonacci_cameras(3, 3.0, 64, 64, fov_y_deg=40.0)
     env = ss.EnvironmentLight.from_base(scenes.env_lognormal(8, 16, 1))
     targets = [ss.render(ss.SurfelCloud(**gt), c, ss.RenderOptions(), env=env).rgb.contiguous() for c in cams]
     cloud = ss.SurfelCloud(**scenes.perturb(gt, 4))
     ts = ss.TrainStep(cloud, env, 64, 64)
     ts.gradients(cams, targets)
     stats = ss.DensifyStats.zeros(len(cloud))
-    stats.accumulate(ts.grads["ss_grad"], ts.touched)
-    assert int(stats.view_count.max()) == 1
-    assert float(stats.grad_sum.sum()) > 0
+    stats.accumulate(ts.grads["ss_grad"], ts.view_count)
+    ref = ss.DensifyStats.zeros(len(cloud))
+    for cam, tgt in zip(cams, targets):
+        res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
+        _, g = ss.photometric_loss(res.rgb, tgt, lambda_ssim=0.0)
+        back = ss.backward_image(cloud, res, g_rgb=g)
+        ref.accumulate(back.ss_grad, back.touched)
+    assert torch.equal(stats.view_count, ref.view_count)
+    assert int(stats.view_count.max()) == 3          # surfels seen from all three views
+    assert int((stats.view_count == 2).sum()) > 0    # ... and from only some of them
+    bad, err = grad_close(stats.grad_sum, ref.grad_sum)
+    assert bad == 0, err
+    bad, err = grad_close(stats.mean_grad(), ref.mean_grad())
+    assert bad == 0, err
     new, imap, reasons = ss.refine_topology(cloud, stats, np.full(len(cloud), 0.001), 2300, quantile=0.95)
     assert len(new) <= 2300 and reasons["split"] > 0
 

@@ -5,11 +5,14 @@ import numpy as np
 import pytest
 import torch
 
-from parity import grad_close, host
+from types import SimpleNamespace
+
+from parity import grad_close, grad_outliers, host
 
 pytestmark = pytest.mark.gpu
 
 import paper_2605_05876_b200 as ss  # noqa: E402
+from oracle import oracle as O  # noqa: E402
 from paper_2605_05876_b200 import scenes  # noqa: E402
 from paper_2605_05876_b200.step import PARAMS, TrainStep  # noqa: E402
 
@@ -23,6 +26,54 @@ def _scene(n=3000, res=96, seed=0):
     gtc = ss.SurfelCloud(**gt)
     targets = [ss.render(gtc, c, ss.RenderOptions(), env=gt_env).rgb.contiguous() for c in cams]
     return init, env_base, cams, targets
+
+
+def _oracle_step(init, env_base, cams, targets, images):
+    """Sum over views of the ORACLE's render -> L1 -> backward_image (the
+    reference algorithm, not a CUDA path), with the L1 sign pattern of the
+    step's own fused-forward images (`images`, TrainStep.captured_rgb): the
+    step shades in float32, so residuals below ~1e-7 may flip sign vs the
+    oracle's float64 image."""
+    co = SimpleNamespace(**init)
+    oenv = O.EnvOracle(np.log(np.asarray(env_base, np.float64)))
+    acc, views = None, np.zeros(len(init["centers"]), np.float32)
+    for cam, tgt, img in zip(cams, targets, images):
+        ores = O.render(co, cam, env=oenv)
+        rgb = host(img).astype(np.float64)
+        g = np.sign(rgb - host(tgt)) / rgb.size
+        og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
+        views += og["touched"]
+        if acc is None:
+            acc = {k: np.array(og[k], np.float64) for k in list(PARAMS) + ["ss_grad", "env_base_log"]}
+        else:
+            for k in acc:
+                acc[k] += og[k]
+    acc["view_count"] = views
+    return acc
+
+
+def _assert_step_matches_oracle(ts, ref):
+    bad = {}
+    for k in list(PARAMS) + ["ss_grad"]:
+        outl, n = grad_outliers(ts.grads[k], ref[k].reshape(ts.grads[k].shape))
+        if n:
+            bad[k] = (n, outl)
+    outl, n = grad_outliers(ts.g_env_log, ref["env_base_log"])
+    if n:
+        bad["env_base_log"] = (n, outl)
+    assert not bad, bad
+    np.testing.assert_array_equal(host(ts.view_count), ref["view_count"])
+
+
+def test_train_step_gradients_match_oracle():
+    """The fused multi-view step vs the oracle summed over the same views."""
+    init, env_base, cams, targets = _scene()
+    cloud = ss.SurfelCloud(**init)
+    env = ss.EnvironmentLight.from_base(env_base)
+    ts = TrainStep(cloud, env, 96, 96)
+    ts.captured_rgb = []
+    ts.gradients(cams, targets)
+    _assert_step_matches_oracle(ts, _oracle_step(init, env_base, cams, targets, ts.captured_rgb[-len(cams):]))
 
 
 def test_train_step_gradients_match_api_path():
@@ -41,7 +92,7 @@ def test_train_step_gradients_match_api_path():
         res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
         val, g = ss.photometric_loss(res.rgb, tgt, lambda_ssim=0.0)
         loss += val * res.rgb.numel()
-        back = ss.backward_image(cloud, res, g_rgb=g)
+        back = ss.backward_image(cloud, res, g_rgb=g, path="walk")  # not the record kernel the step runs
         for k in PARAMS:
             acc[k] += getattr(back, k).reshape(acc[k].shape)
         d_diff += back.d_diffuse
@@ -146,23 +197,26 @@ def test_train_step_ragged_image(wh):
     cloud = ss.SurfelCloud(**init)
     env = ss.EnvironmentLight.from_base(env_base)
     ts = TrainStep(cloud, env, W, H)
+    ts.captured_rgb = []
     ts.gradients(cams, targets)
     torch.cuda.synchronize()
     acc = {k: torch.zeros_like(ts.grads[k]) for k in PARAMS}
     for cam, tgt in zip(cams, targets):
         res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
         _, g = ss.photometric_loss(res.rgb, tgt, lambda_ssim=0.0)
-        back = ss.backward_image(cloud, res, g_rgb=g)
+        back = ss.backward_image(cloud, res, g_rgb=g, path="walk")
         for k in PARAMS:
             acc[k] += getattr(back, k).reshape(acc[k].shape)
     for k in PARAMS:
         bad, err = grad_close(ts.grads[k], acc[k])
         assert bad == 0, (k, err)
+    _assert_step_matches_oracle(ts, _oracle_step(init, env_base, cams, targets, ts.captured_rgb[-len(cams):]))
 
 
 def test_train_step_with_normal_consistency():
     """set_normal_consistency adds lambda_nc * normal_consistency_loss (value and
-    quaternion gradient) to the step, as train.py:216-221."""
+    quaternion gradient, train.py:216-221) once per view of the step: a
+    V-view step equals the sum of V reference steps."""
     init, env_base, cams, targets = _scene(n=2000, res=64)
     cloud = ss.SurfelCloud(**init)
     env = ss.EnvironmentLight.from_base(env_base)
@@ -174,9 +228,60 @@ def test_train_step_with_normal_consistency():
     ts.set_normal_consistency(idx, 0.05)
     ts.gradients(cams, targets)
     nc, g = ss.normal_consistency_loss(cloud, idx)
-    assert float(ts.loss_f.item()) == pytest.approx(base_loss + 0.05 * nc, rel=1e-6)
-    bad, err = grad_close(ts.grads["quats"], base_q + 0.05 * g.reshape(base_q.shape))
+    V = len(cams)
+    assert float(ts.loss_f.item()) == pytest.approx(base_loss + 0.05 * V * nc, rel=1e-6)
+    bad, err = grad_close(ts.grads["quats"], base_q + 0.05 * V * g.reshape(base_q.shape))
     assert bad == 0, err
     ts.set_normal_consistency(None, 0.0)
     ts.gradients(cams, targets)
     assert float(ts.loss_f.item()) == pytest.approx(base_loss, rel=1e-6)
+
+
+def test_step_host_includes_normal_consistency():
+    """The pinned-host entry point (the bench's e2e path) applies the same
+    step as step(), normal-consistency term included."""
+    init, env_base, cams, targets = _scene(n=1500, res=64)
+    outs = []
+    for host_mode in (False, True):
+        cloud = ss.SurfelCloud(**init)
+        env = ss.EnvironmentLight.from_base(env_base)
+        ts = TrainStep(cloud, env, 64, 64)
+        ts.set_normal_consistency(ss.NeighborIndex(cloud, k=8), 0.05)
+        if host_mode:
+            loss = ts.step_host(cams, [t.cpu().pin_memory() for t in targets])
+        else:
+            loss = ts.step(cams, targets)
+        outs.append((float(loss.item()), cloud.quats.clone()))
+    assert outs[0][0] == outs[1][0]
+    assert torch.equal(outs[0][1], outs[1][1])
+
+
+def test_pair_overflow_grows_and_reruns():
+    """A step whose views need more pairs than the buffers hold grows them
+    and re-runs the views before Adam: the parameters after the step equal
+    those of a step with ample buffers (no truncated tile list reaches the
+    optimiser; the offsets are clamped, so nothing reads out of bounds)."""
+    init, env_base, cams, targets = _scene(n=1500, res=64)
+    outs = []
+    for cap in (None, 300):
+        cloud = ss.SurfelCloud(**init)
+        env = ss.EnvironmentLight.from_base(env_base)
+        ts = TrainStep(cloud, env, 64, 64, pair_capacity=cap)
+        loss = float(ts.step(cams, targets).item())
+        outs.append((loss, cloud.centers.clone(), ts.regrows, ts.capacity))
+    assert outs[1][2] == 1 and outs[1][3] > 300
+    assert outs[0][0] == outs[1][0]
+    assert torch.equal(outs[0][1], outs[1][1])
+
+
+def test_nonfinite_colour_raises_in_step():
+    init, env_base, cams, targets = _scene(n=500, res=32)
+    bad = dict(init)
+    bad["albedo_raw"] = bad["albedo_raw"].copy()
+    bad["metallic_raw"] = bad["metallic_raw"].copy()
+    bad["metallic_raw"][7] = np.nan
+    cloud = ss.SurfelCloud(**bad)
+    env = ss.EnvironmentLight.from_base(env_base)
+    ts = TrainStep(cloud, env, 32, 32)
+    with pytest.raises(ValueError):
+        ts.step(cams, [torch.zeros(32, 32, 3, device="cuda")] * len(cams))
