@@ -101,6 +101,11 @@ typedef struct SsProjAux {
     uint8_t *jac_ok;                  /* (n,)  */
     float *colors;                    /* (n,3) the per-surfel colours used */
     int32_t *cells;                   /* (n,15) shading branch signature (shading.py:490-497) */
+    /* (n,4) uint32, the same branch state packed for ss_chain_backward:
+     * diffuse cell i0 | j0 << 16, specular cell, LUT cell, roughness level
+     * | flags << 8 (bit 0 diffuse dv_ok, 1 specular dv_ok, 2 LUT du_ok,
+     * 3 LUT dv_ok, 4 n.w_o > 0, 5 n.w_o < 1) -- from the float64 forward */
+    uint32_t *cells_packed;
 } SsProjAux;
 
 /* ---- preprocess + shade + tile count --------------------------------------
@@ -309,9 +314,14 @@ typedef struct SsGrads {
     float *d_diffuse4, *d_specular4;
     float *view_count;  /* nullable */
 } SsGrads;
+/* shade_cells (nullable, SS_COLOR_IBL): the SsProjAux.cells_packed of this
+ * view's preprocess; the shading adjoint then runs in float32 on the
+ * forward's own float64 branch decisions (texel cells, level, clip flags)
+ * instead of re-deriving them in float64. */
 int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                       int color_source, const SsEnv *env, const int8_t *cull,
-                      const float *rec_acc, const double *rec_acc64, const SsGrads *grads, void *stream);
+                      const float *rec_acc, const double *rec_acc64, const uint32_t *shade_cells,
+                      const SsGrads *grads, void *stream);
 
 /* ss_env_grad_merge: dst[3 t + c] += src4[4 t + c] (float64 += float32) for
  * t < texels, c < 3, and zeroes src4 (the per-view derived-map accumulators

@@ -48,7 +48,8 @@ class SsPreprocessOpts(ctypes.Structure):
 
 class SsProjAux(ctypes.Structure):
     _fields_ = [("c_cam", c_p), ("tu_cam", c_p), ("tv_cam", c_p), ("eps_z", c_p),
-                ("center_ndc", c_p), ("jac", c_p), ("jac_ok", c_p), ("colors", c_p), ("cells", c_p)]
+                ("center_ndc", c_p), ("jac", c_p), ("jac_ok", c_p), ("colors", c_p), ("cells", c_p),
+                ("cells_packed", c_p)]
 
 
 class SsStacks(ctypes.Structure):
@@ -79,7 +80,7 @@ _SIGNATURES = {
                           ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_raster_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p,
                            ctypes.POINTER(ctypes.c_float), ctypes.c_int, c_p, c_p, ctypes.c_float, c_p, c_p, c_p],
-    "ss_chain_backward": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_chain_backward": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_brdf_lut": [ctypes.c_int, ctypes.c_int, c_p, c_p],
     "ss_env_khat_words": [ctypes.c_int, ctypes.c_int],
     "ss_env_khat": [ctypes.c_int, ctypes.c_int, c_p, c_p],

@@ -150,7 +150,8 @@ def backward_image(cloud, result, g_rgb=None, g_alpha=None, cons_scale=0.0, path
     gs = grads_struct(g, d_diff, d_spec, d_diff4, d_spec4)
     rc = lib.ss_chain_backward(ctypes.byref(cl), ctypes.byref(camst), ctypes.byref(po), source,
                                ctypes.byref(envs) if envs is not None else None, _lib.ptr(st.cull), _lib.ptr(acc),
-                               _lib.ptr(acc64), ctypes.byref(gs), _lib.stream_ptr())
+                               _lib.ptr(acc64), _lib.ptr(st.aux.get("cells_packed") if ibl else None),
+                               ctypes.byref(gs), _lib.stream_ptr())
     _lib.check(rc, "ss_chain_backward")
     g_env = None
     if ibl:

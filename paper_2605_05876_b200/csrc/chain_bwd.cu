@@ -22,6 +22,7 @@ struct ChainParams {
     const int8_t *cull;
     const float *acc;
     const double *acc64;  // float64 rows of the big records (SS_ACC_F64)
+    const uint4 *cells;   // nullable: the forward's packed shading branch state
     SsGrads g;
 };
 
@@ -276,7 +277,11 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
         // (gradients: the 1e-3 parity bar)
         ShadeIn<float> in;
         ShadeState<float> st;
-        {
+        if (P.cells && P.env.diffuse4 && P.env.specular4) {
+            // the preprocess kernel's float64 branch decisions, float32 state
+            ss_shade_inputs(cl, i, P.cam_pos, in);
+            ss_shade_forward_cells(in, P.env, __ldg(P.cells + i), st);
+        } else {
             ShadeIn<double> in64;
             ss_shade_inputs(cl, i, P.cam_pos, in64);
             ShadeState<double> st64;
@@ -368,7 +373,8 @@ extern "C" int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void 
 
 extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
                                  int color_source, const SsEnv *env, const int8_t *cull,
-                                 const float *rec_acc, const double *rec_acc64, const SsGrads *grads, void *stream)
+                                 const float *rec_acc, const double *rec_acc64, const uint32_t *shade_cells,
+                                 const SsGrads *grads, void *stream)
 {
     if (!cloud || !cam || !opt || !grads) return SS_ERR_INVALID;
     if (cloud->n == 0) return SS_OK;
@@ -388,6 +394,7 @@ extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, cons
     P.r_cut = opt->r_cut; P.sigma_f = opt->mip_sigma;
     P.env = env ? *env : SsEnv{};
     P.cull = cull; P.acc = rec_acc; P.acc64 = rec_acc64; P.g = *grads;
+    P.cells = reinterpret_cast<const uint4 *>(shade_cells);
     chain_kernel<<<(cloud->n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;

@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
         ss_shade_forward(in, env, st, out);
         col[0] = (float)out[0]; col[1] = (float)out[1]; col[2] = (float)out[2];
         if (aux.cells) ss_shade_cells(st, env, aux.cells + 15 * i);
+        if (aux.cells_packed && in_range) reinterpret_cast<uint4 *>(aux.cells_packed)[i] = ss_shade_pack(st);
     }
     if (in_range && !(isfinite(col[0]) && isfinite(col[1]) && isfinite(col[2]))) atomicOr(&flags[1], 1);
 

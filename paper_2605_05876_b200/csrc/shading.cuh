@@ -276,6 +276,78 @@ __device__ __forceinline__ void ss_shade_narrow(const ShadeIn<double> &a, const 
     sf.bd = ss_bil_narrow(s.bd); sf.bs = ss_bil_narrow(s.bs); sf.bl = ss_bil_narrow(s.bl);
 }
 
+// The float64 forward's branch state, packed (SsProjAux.cells_packed).
+template <typename R>
+__device__ __forceinline__ uint4 ss_shade_pack(const ShadeState<R> &s) {
+    const unsigned flags = (s.bd.dv_ok ? 1u : 0u) | (s.bs.dv_ok ? 2u : 0u) | (s.bl.du_ok ? 4u : 0u) |
+                           (s.bl.dv_ok ? 8u : 0u) | (s.ndv_raw > R(0.0) ? 16u : 0u) | (s.ndv_raw < R(1.0) ? 32u : 0u);
+    return make_uint4((unsigned)s.bd.i0 | ((unsigned)s.bd.j0 << 16), (unsigned)s.bs.i0 | ((unsigned)s.bs.j0 << 16),
+                      (unsigned)s.bl.i0 | ((unsigned)s.bl.j0 << 16), (unsigned)s.lvl0 | (flags << 8));
+}
+
+// A bilinear cell forced to (i0, j0): the weights from this evaluation's own
+// coordinates relative to the forced cell (wrapping columns: the nearest
+// image of fu).
+__device__ __forceinline__ SsBil<float> ss_bil_forced(int h, int w, float fu, float fv, bool wrap, unsigned cell,
+                                                      bool du_ok, bool dv_ok) {
+    SsBil<float> b;
+    b.i0 = (int)(cell & 0xffffu);
+    b.j0 = (int)(cell >> 16);
+    b.j1 = b.j0 + 1;
+    b.tv = ss_clip<float>(fv, 0.f, h - 1.f) - (float)b.j0;
+    if (wrap) {
+        float t = fu - (float)b.i0;
+        if (t < -0.5f * w) t += (float)w;
+        else if (t > 0.5f * w) t -= (float)w;
+        b.tu = t;
+        b.i1 = b.i0 + 1 == w ? 0 : b.i0 + 1;
+    } else {
+        b.tu = ss_clip<float>(fu, 0.f, w - 1.f) - (float)b.i0;
+        b.i1 = b.i0 + 1;
+    }
+    b.du_ok = du_ok;
+    b.dv_ok = dv_ok;
+    return b;
+}
+
+// shade_surfels body in float32 on the branch state of the float64 forward
+// (ss_shade_pack): the state the adjoint needs, without re-deriving the
+// cells in float64.
+__device__ __forceinline__ void ss_shade_forward_cells(const ShadeIn<float> &in, const SsEnv &env, uint4 cells,
+                                                       ShadeState<float> &s) {
+    const int he = env.he, we = env.we, L = env.levels, LR = env.lut_res;
+    const unsigned fl = cells.w >> 8;
+    s.ndv_raw = (in.n[0] * in.wo[0] + in.n[1] * in.wo[1]) + in.n[2] * in.wo[2];
+    // the clip-activity flags are the float64 forward's
+    if ((s.ndv_raw > 0.f) != ((fl & 16u) != 0)) s.ndv_raw = (fl & 16u) ? 1e-30f : 0.f;
+    if ((s.ndv_raw < 1.f) != ((fl & 32u) != 0)) s.ndv_raw = (fl & 32u) ? 0.99999994f : 1.f;
+    const float ndv = ss_clip<float>(s.ndv_raw, 0.f, 1.f);
+    for (int c = 0; c < 3; ++c) s.refl[c] = 2.f * s.ndv_raw * in.n[c] - in.wo[c];
+    float fu, fv;
+    ss_dir_coords(in.n, he, we, fu, fv);
+    s.bd = ss_bil_forced(he, we, fu, fv, true, cells.x, true, (fl & 1u) != 0);
+    const float4 *d4 = reinterpret_cast<const float4 *>(env.diffuse4);
+    const float4 *s4 = reinterpret_cast<const float4 *>(env.specular4);
+    ss_bil_lookup4(d4, we, s.bd, s.l_d);
+    const float lvl = ss_clip<float>(in.r, 0.f, 1.f) * (L - 1);
+    s.lvl0 = (int)(cells.w & 0xffu);
+    s.frac = L > 1 ? lvl - (float)s.lvl0 : 0.f;
+    s.lvl1 = s.lvl0 + 1 < L - 1 ? s.lvl0 + 1 : L - 1;
+    ss_dir_coords(s.refl, he, we, fu, fv);
+    s.bs = ss_bil_forced(he, we, fu, fv, true, cells.y, true, (fl & 2u) != 0);
+    ss_bil_lookup4(s4 + (size_t)he * we * s.lvl0, we, s.bs, s.spec_lo);
+    ss_bil_lookup4(s4 + (size_t)he * we * s.lvl1, we, s.bs, s.spec_hi);
+    for (int c = 0; c < 3; ++c) s.l_s[c] = (1.f - s.frac) * s.spec_lo[c] + s.frac * s.spec_hi[c];
+    s.bl = ss_bil_forced(LR, LR, ndv * (LR - 1), in.r * (LR - 1), false, cells.z, (fl & 4u) != 0, (fl & 8u) != 0);
+    float bb[2];
+    ss_bil_lookup<2>(env.lut, LR, s.bl, bb);
+    s.b1 = bb[0]; s.b2 = bb[1];
+    for (int c = 0; c < 3; ++c) {
+        s.f0[c] = 0.04f * (1.f - in.m) + in.albedo[c] * in.m;
+        s.k_d[c] = (1.f - s.f0[c]) * (1.f - in.m);
+    }
+}
+
 // Branch signature cells (shading.py:490-497), 15 ints.
 template <typename R>
 __device__ __forceinline__ void ss_shade_cells(const ShadeState<R> &s, const SsEnv &env, int32_t *out) {

@@ -81,9 +81,10 @@ def run_preprocess(cloud, camera, options, color_source, colors=None, env=None, 
         f = lambda *s: torch.zeros(s, device=dev, dtype=torch.float32)
         aux = {"c_cam": f(n, 3), "tu_cam": f(n, 3), "tv_cam": f(n, 3), "eps_z": f(n), "center_ndc": f(n, 2),
                "jac": f(n, 2, 2), "jac_ok": torch.zeros(n, device=dev, dtype=torch.uint8), "colors": f(n, 3),
-               "cells": torch.zeros((n, 15), device=dev, dtype=torch.int32)}
+               "cells": torch.zeros((n, 15), device=dev, dtype=torch.int32),
+               "cells_packed": torch.zeros((n, 4), device=dev, dtype=torch.int32)}
         auxs = _lib.SsProjAux(*(_lib.ptr(aux[k]) for k in ("c_cam", "tu_cam", "tv_cam", "eps_z", "center_ndc",
-                                                            "jac", "jac_ok", "colors", "cells")))
+                                                            "jac", "jac_ok", "colors", "cells", "cells_packed")))
     cam = _lib.make_camera(camera)
     cl = _lib.make_cloud(cloud)
     opt = make_opts(options, tile)

@@ -131,6 +131,9 @@ class ViewBuffers:
         # NDC tables, counters, area-class sort and big-rect queue of the backward
         self.pixel_ndc = torch.empty(_lib.load().ss_train_backward_scratch_words(n, W, H), **f32)
         self.acc = torch.zeros((n, _lib.ACC_FLOATS), **f32)
+        # the float64 shading forward's packed branch state (SsProjAux.cells_packed)
+        self.cells = torch.empty((n, 4), device=device, dtype=torch.int32)
+        self.aux = _lib.SsProjAux(*([None] * 9), _lib.ptr(self.cells))
         # float64 channel rows of the big records (SS_ACC_F64)
         self.acc64 = torch.empty((n, _lib.ACC64_WIDTH), device=device, dtype=torch.float64)
         # this buffer set's share of the step loss (photometric mode): views on
@@ -258,7 +261,7 @@ class TrainStep:
             self.surfel_capacity = self.n
             for b in self.bufs:
                 nb = ViewBuffers(self.n, self.W, self.H, self.tile, self.k_max, self.ntiles, dev)
-                for k in ("records", "cull", "bininfo", "pixel_ndc", "acc", "acc64"):
+                for k in ("records", "cull", "bininfo", "pixel_ndc", "acc", "acc64", "cells", "aux"):
                     setattr(b, k, getattr(nb, k))
         self.pack = GradPack(self.n, self.T, dev)
         self.flat = self.pack.flat
@@ -328,7 +331,8 @@ class TrainStep:
         camst = _lib.make_camera(cam)
         rc = self.lib.ss_preprocess(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                     self.color_source, None, ctypes.byref(self._envs), _lib.ptr(b.records),
-                                    _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts), _lib.ptr(b.bininfo), None,
+                                    _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts), _lib.ptr(b.bininfo),
+                                    ctypes.byref(b.aux) if self.color_source == _lib.SS_COLOR_IBL else None,
                                     _lib.ptr(b.flags), _lib.stream_ptr())
         _lib.check(rc, "ss_preprocess")
         return camst
@@ -419,7 +423,9 @@ class TrainStep:
         # this buffer set's own float32 maps
         _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
                                          _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(b.cull),
-                                         _lib.ptr(b.acc), _lib.ptr(b.acc64), ctypes.byref(b.gs), s),
+                                         _lib.ptr(b.acc), _lib.ptr(b.acc64),
+                                         _lib.ptr(b.cells) if self.color_source == _lib.SS_COLOR_IBL else None,
+                                         ctypes.byref(b.gs), s),
                    "ss_chain_backward")
         # fold this view's float32 derived-map sums into the step's float64
         # ones: plain read-modify-write, so the merges are serialised
