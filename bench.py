@@ -243,6 +243,99 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+# ---------------------------------------------------------------------------
+# the other BASELINE configs (configs[0, 1, 3] and the one-GPU slice of 4):
+# views/s of the same training step on their scenes, resident inputs
+
+
+def _config_workload(cfg):
+    """(gt, init, env_base, cameras, W, H, extra) of BASELINE config `cfg`."""
+    import paper_2605_05876_b200 as ss
+    from paper_2605_05876_b200 import scenes
+    if cfg == 0:
+        gt = scenes.config0(0, 10_000)
+        init = dict(gt)
+        init["centers"] = (gt["centers"] + np.random.default_rng(1).normal(0, 0.01, gt["centers"].shape)).astype(
+            np.float32)
+        cams = [ss.Camera.perspective(128, 128, 40.0, (3.0, 0.0, 0.0), (0.0, 0.0, 0.0))]
+        return gt, init, scenes.env_lognormal(16, 32, 2), cams, 128, 128, {}
+    if cfg == 1:
+        gt = scenes.config1(0, 200_000)
+        return gt, scenes.perturb(gt, 1), scenes.env_lognormal(64, 128, 2), ss.fibonacci_cameras(8, 3.5, 512, 512), \
+            512, 512, {}
+    if cfg == 3:
+        gt = scenes.config3(0, 500_000)
+        return gt, scenes.perturb(gt, 1), scenes.env_lognormal(64, 128, 2), \
+            ss.fibonacci_cameras(16, 3.5, 1024, 1024), 1024, 1024, {}
+    if cfg == 4:
+        gt = scenes.config2(0, 4_000_000, amp=0.12, octaves=5)
+        cams = ss.fibonacci_cameras(128, 3.5, 1920, 1080)[:16]  # one GPU's 16 of the step's 128 views
+        return gt, scenes.perturb(gt, 1), scenes.env_lognormal(256, 512, 2), cams, 1920, 1080, \
+            {"max_surfels": 4_200_000, "quantile": 0.95}
+    raise ValueError(cfg)
+
+
+def run_config(cfg, steps=3, warmup=2):
+    """views/s of the training step (L1, Adam, env refresh) on config `cfg`;
+    config 4 adds the per-step refinement pass (q = 0.95, budget 1.05 N) and
+    the neighbour-index rebuild, timed separately and inside the step."""
+    import torch
+
+    import paper_2605_05876_b200 as ss
+    from paper_2605_05876_b200.densify import DensifyStats
+    from paper_2605_05876_b200.step import TrainStep
+    gt, init, env_base, cams, W, H, extra = _config_workload(cfg)
+    gt_env = ss.EnvironmentLight.from_base(env_base)
+    gtc = ss.SurfelCloud(**gt)
+    targets = [ss.render(gtc, c, ss.RenderOptions(), env=gt_env).rgb.contiguous() for c in cams]
+    del gtc
+    cloud = ss.SurfelCloud(**init)
+    env = ss.EnvironmentLight(np.log(env_base))
+    refine = "max_surfels" in extra
+    ts = TrainStep(cloud, env, W, H, streams=3, surfel_capacity=extra.get("max_surfels"))
+    ts.size_pairs(cams[:2])
+    index = ss.NeighborIndex(ts.cloud, k=8) if refine else None
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    ref_ms, knn_ms, sizes = [], [], []
+
+    def one():
+        ts.step(cams, targets)
+        if refine:
+            stats = DensifyStats.zeros(len(ts.cloud))
+            stats.accumulate(ts.grads["ss_grad"], ts.view_count)
+            a, b, c = ev(), ev(), ev()
+            a.record()
+            ts.refine(stats, index.mean_dist, extra["max_surfels"], quantile=extra["quantile"])
+            b.record()
+            index.rebuild(ts.cloud)
+            c.record()
+            return a, b, c
+        return None
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record()
+    marks = [one() for _ in range(steps)]
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    out = {"views_per_s": len(cams) / (ms / 1e3), "ms_per_step": ms, "views_per_step": len(cams),
+           "surfels": len(init["centers"]), "image": [W, H], "env": list(env_base.shape[:2])}
+    if refine:
+        ref_ms = [a.elapsed_time(b) for a, b, _ in marks]
+        knn_ms = [b.elapsed_time(c) for _, b, c in marks]
+        out.update({"refinement_ms": float(np.mean(ref_ms)), "knn_rebuild_ms": float(np.mean(knn_ms)),
+                    "surfels_after": len(ts.cloud), "quantile": extra["quantile"],
+                    "max_surfels": extra["max_surfels"],
+                    "step": "16 of the 128 views of a step (the per-GPU slice at 8 GPUs): fwd+bwd, env adjoint, "
+                            "Adam, env refresh, then refine_topology (device) and the KNN rebuild"})
+    del ts
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -335,21 +428,23 @@ def run_ours(args):
     # every timed step above as well
     fixed = ts.fixed_costs()
     if world == 1:
-        # the density-aware refinement scan on this step's statistics
-        # (KNN index + prune / split, densify.py:168-202), run once
+        # the density-aware refinement scan on this step's statistics, on the
+        # device (refine_topology: isolation, prune, quantile, budget, split,
+        # Adam remap), and the KNN rebuild the reference runs after it
         from paper_2605_05876_b200.densify import DensifyStats, refine_topology
         st = DensifyStats.zeros(len(cloud))
-        st.accumulate(ts.grads["ss_grad"], ts.touched)
-        def refine():
-            knn = ss.NeighborIndex(cloud, k=8)
-            return refine_topology(cloud, st, knn.mean_dist, max_surfels=int(1.05 * len(cloud)))
-        refine()  # warm-up (first-call module loads and allocations)
-        ra, rb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.accumulate(ts.grads["ss_grad"], ts.view_count)
+        knn = ss.NeighborIndex(cloud, k=8)
+        refine_topology(cloud, st, knn.mean_dist, max_surfels=int(1.05 * len(cloud)))  # warm-up
+        ra, rb, rc = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         ra.record(stream)
-        _, imap, reasons = refine()
+        _, imap, reasons = refine_topology(cloud, st, knn.mean_dist, max_surfels=int(1.05 * len(cloud)))
         rb.record(stream)
+        knn.rebuild(cloud)
+        rc.record(stream)
         torch.cuda.synchronize()
         fixed["refinement_scan"] = ra.elapsed_time(rb)
+        fixed["knn_rebuild"] = rb.elapsed_time(rc)
         fixed["refinement_result"] = {"surfels_out": int(imap.numel()),
                                       **{k: int(v) for k, v in reasons.items() if np.isscalar(v)}}
         del imap
@@ -430,6 +525,13 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
+    configs = {}
+    if world == 1 and not args.no_configs:
+        for c in (0, 1, 3, 4):
+            try:
+                configs[f"config{c}"] = run_config(c)
+            except Exception as e:  # reported, never fatal for the headline
+                configs[f"config{c}"] = {"error": repr(e)[:200]}
     peak, peak_kind = _peaks()
     traffic, traffic_src = _traffic()
     P, Nk = stats["pairs_mean"], stats["kept_mean"]
@@ -468,6 +570,7 @@ def run_ours(args):
         "per_step_fixed_ms": fixed,
         "photometric_loss_step": photometric,
         "photometric_cons_loss_step": photometric_cons,
+        "other_configs": configs,
         "cpu_baseline": cpu, "clocks": clk, "gpu_launches": launches,
         "loss": last_loss,
     }
@@ -483,6 +586,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs 0/1/3/4 lines")
     ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing on CPU (gloo), no GPU work")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

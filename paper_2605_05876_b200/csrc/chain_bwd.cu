@@ -132,6 +132,16 @@ __global__ void env_merge_kernel(int64_t texels, float4 *__restrict__ src, doubl
     }
 }
 
+#ifdef SS_CHAIN_TAIL_F32
+typedef float TT;
+#define TT_PROJ P.projf
+#define TT_VIEW P.viewf
+#else
+typedef double TT;
+#define TT_PROJ P.proj
+#define TT_VIEW P.view
+#endif
+
 __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -237,9 +247,10 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
     // T rows -> camera -> world (backward.py:405-441) and the frame adjoint
     // in float64 with the float64 camera like the reference: a grazing
     // splat's row gradients are large and cancel in these linear maps
-    // (float32 lost ~1% of its log-scale gradients)
-    const double *pm = P.proj;
-    double gtu[3], gtv[3], gcc[3];
+    // (float32 lost ~1% of its log-scale gradients).  TT: the tail's type
+    // (SS_CHAIN_TAIL_F32: float32, an experiment switch)
+    const TT *pm = TT_PROJ;
+    TT gtu[3], gtv[3], gcc[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         gtu[c] = G1[0] * pm[c] + G2[0] * pm[4 + c] + G4[0] * pm[12 + c];
@@ -247,27 +258,27 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
         gcc[c] = G1[2] * pm[c] + G2[2] * pm[4 + c] + G4[2] * pm[12 + c];
     }
     gcc[2] -= gz;
-    double gw[3], guw[3], gvw[3];
+    TT gw[3], guw[3], gvw[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        gw[k] = (gcc[0] * P.view[k] + gcc[1] * P.view[4 + k]) + gcc[2] * P.view[8 + k];
-        guw[k] = (gtu[0] * P.view[k] + gtu[1] * P.view[4 + k]) + gtu[2] * P.view[8 + k];
-        gvw[k] = (gtv[0] * P.view[k] + gtv[1] * P.view[4 + k]) + gtv[2] * P.view[8 + k];
+        gw[k] = (gcc[0] * TT_VIEW[k] + gcc[1] * TT_VIEW[4 + k]) + gcc[2] * TT_VIEW[8 + k];
+        guw[k] = (gtu[0] * TT_VIEW[k] + gtu[1] * TT_VIEW[4 + k]) + gtu[2] * TT_VIEW[8 + k];
+        gvw[k] = (gtv[0] * TT_VIEW[k] + gtv[1] * TT_VIEW[4 + k]) + gtv[2] * TT_VIEW[8 + k];
     }
     const SsCloud &cl = P.cloud;
     const float4 qv = reinterpret_cast<const float4 *>(cl.quats)[i];
-    const double qn = sqrt((((double)qv.x * qv.x + (double)qv.y * qv.y) + (double)qv.z * qv.z) + (double)qv.w * qv.w);
-    const double iqn = 1.0 / qn;
-    const double w = qv.x * iqn, x = qv.y * iqn, y = qv.z * iqn, z = qv.w * iqn;
-    const double uh[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
-    const double vh[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
+    const TT qn = (TT) sqrt((((double)qv.x * qv.x + (double)qv.y * qv.y) + (double)qv.z * qv.z) + (double)qv.w * qv.w);
+    const TT iqn = TT(1) / qn;
+    const TT w = qv.x * iqn, x = qv.y * iqn, y = qv.z * iqn, z = qv.w * iqn;
+    const TT uh[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
+    const TT vh[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
     const float2 lsv = reinterpret_cast<const float2 *>(cl.log_scales)[i];
-    const double su = exp((double)lsv.x), sv = exp((double)lsv.y);
-    const double gsu = (guw[0] * uh[0] + guw[1] * uh[1]) + guw[2] * uh[2];
-    const double gsv = (gvw[0] * vh[0] + gvw[1] * vh[1]) + gvw[2] * vh[2];
-    double gU[3], gV[3], gN[3] = {0.0, 0.0, 0.0};
+    const TT su = (TT)exp((double)lsv.x), sv = (TT)exp((double)lsv.y);
+    const TT gsu = (guw[0] * uh[0] + guw[1] * uh[1]) + guw[2] * uh[2];
+    const TT gsv = (gvw[0] * vh[0] + gvw[1] * vh[1]) + gvw[2] * vh[2];
+    TT gU[3], gV[3], gN[3] = {0, 0, 0};
     for (int k = 0; k < 3; ++k) { gU[k] = su * guw[k]; gV[k] = sv * gvw[k]; }
-    double gcent[3] = {gw[0], gw[1], gw[2]};
+    TT gcent[3] = {gw[0], gw[1], gw[2]};
     float galb[3] = {0.f, 0.f, 0.f}, gmet = 0.f, grough = 0.f;
 
     if (P.color_source == SS_COLOR_IBL) {
@@ -335,12 +346,12 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
     }
     // quat_frame_backward (surfels.py:54-77)
 #define D3(g, a0, a1, a2) ((g)[0] * (a0) + (g)[1] * (a1) + (g)[2] * (a2))
-    const double gqw = D3(gU, 0.0, 2 * z, -2 * y) + D3(gV, -2 * z, 0.0, 2 * x) + D3(gN, 2 * y, -2 * x, 0.0);
-    const double gqx = D3(gU, 0.0, 2 * y, 2 * z) + D3(gV, 2 * y, -4 * x, 2 * w) + D3(gN, 2 * z, -2 * w, -4 * x);
-    const double gqy = D3(gU, -4 * y, 2 * x, -2 * w) + D3(gV, 2 * x, 0.0, 2 * z) + D3(gN, 2 * w, 2 * z, -4 * y);
-    const double gqz = D3(gU, -4 * z, 2 * w, 2 * x) + D3(gV, -2 * w, -4 * z, 2 * y) + D3(gN, 2 * x, 2 * y, 0.0);
+    const TT gqw = D3(gU, TT(0), 2 * z, -2 * y) + D3(gV, -2 * z, TT(0), 2 * x) + D3(gN, 2 * y, -2 * x, TT(0));
+    const TT gqx = D3(gU, TT(0), 2 * y, 2 * z) + D3(gV, 2 * y, -4 * x, 2 * w) + D3(gN, 2 * z, -2 * w, -4 * x);
+    const TT gqy = D3(gU, -4 * y, 2 * x, -2 * w) + D3(gV, 2 * x, TT(0), 2 * z) + D3(gN, 2 * w, 2 * z, -4 * y);
+    const TT gqz = D3(gU, -4 * z, 2 * w, 2 * x) + D3(gV, -2 * w, -4 * z, 2 * y) + D3(gN, 2 * x, 2 * y, TT(0));
 #undef D3
-    const double radial = ((gqw * w + gqx * x) + gqy * y) + gqz * z;
+    const TT radial = ((gqw * w + gqx * x) + gqy * y) + gqz * z;
 
     SsGrads &g = P.g;
     for (int c = 0; c < 3; ++c) {

@@ -95,7 +95,11 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
     // layer sums: float64 in the training modes (the layer's mean colour
     // C / W enters the backward through record colour - mean colour, which
     // float32 sums would blur), float32 for the plain render
+#ifdef SS_FWD_F64_SUMS
     using AccT = typename std::conditional<kTrain, double, float>::type;
+#else
+    using AccT = float;
+#endif
     AccT Wg = 0, C0 = 0, C1 = 0, C2 = 0;
     float Zg = 0.f, Z2g = 0.f, zmax = 0.f;
     float T = 1.f, o0 = 0.f, o1 = 0.f, o2 = 0.f, dnum = 0.f, dden = 0.f;

@@ -126,15 +126,16 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     }
     if (m >= P.k_max) return 0;  // beyond the K_MAX stop: discarded
     const float4 cf = m == 0 ? cf0 : __ldg(P.coef + m * HW + pix);
-    const float cflo = __ldg(P.coef_lo + m * HW + pix);
     float e;  // exp(-rho^2 / 2) by the hardware ex2 (ftz: no range fix-up)
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(rho2 * -0.72134752044448170368f));
     const float w = R.d.x * e;
     // g_w = A + sum_c G_c colour_c: a small difference of large terms when
     // the record's colour is near its layer's mean colour (raster_fwd.cu
     // store_coef) -- float64, exact products of the float factors
-    float gw = (float)(((double)cf.x + (double)cflo) +
-                       (((double)cf.y * R.e.x + (double)cf.z * R.e.y) + (double)cf.w * R.e.z));
+    // float32 here (measured: no gradient entry of configs 0-3 moves out of
+    // tolerance); the big records evaluate it in float64 with the A_lo plane
+    // (item_grad_ref), where a grazing splat's cancellation needs it
+    float gw = cf.x + cf.y * R.e.x + cf.z * R.e.y + cf.w * R.e.z;
     if constexpr (kCons) {  // consolidation penalty (backward.py:272-286, centred depth form)
         const float4 zq = __ldg(P.zc + m * HW + pix);
         const float dz = R.d.y - zq.z;
