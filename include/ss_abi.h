@@ -287,6 +287,20 @@ int ss_knn_oriented(int n, const float *centers, const float *quats, const int32
 int ss_normal_consistency(int n, int k, const float *centers, const float *quats, const int64_t *neighbors,
                           const double *mean_dist, double *loss, double *g_normals, float *g_quats, void *stream);
 
+/* Dense cell grid for the neighbour queries (no host round trip, no binary
+ * searches): ss_cell_grid_build sizes cubic cells over the centres'
+ * bounding box on the device and counting-sorts the surfels into dim^3
+ * cells (per-cell [start, end) table); `grid`: ss_cell_grid_words(n, dim)
+ * int32 words of caller scratch, dim <= 512.  ss_knn_dense is
+ * ss_knn_oriented on it (queries in cell order), ss_isolation_dense the
+ * isolation test of densify.py:118-123. */
+size_t ss_cell_grid_words(int n, int dim);
+int ss_cell_grid_build(int n, const float *centers, int dim, int32_t *grid, void *stream);
+int ss_knn_dense(int n, const float *centers, const float *quats, const int32_t *grid, int dim, int k,
+                 int64_t *neighbors, double *mean_dist, void *stream);
+int ss_isolation_dense(int n, const float *centers, const float *log_scales, const int32_t *grid, int dim,
+                       uint8_t *isolated, void *stream);
+
 /* ---- chain backward -------------------------------------------------------
  * Replaces the per-surfel tail of backward_image() (backward.py:398-461,
  * 473-548), shade_backward() (shading.py:525-616) and quat_frame_backward()

@@ -126,6 +126,10 @@ _SIGNATURES = {
                         ctypes.c_int, c_p, c_p, c_p],
     "ss_normal_consistency": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_cell_grid_words": [ctypes.c_int, ctypes.c_int],
+    "ss_cell_grid_build": [ctypes.c_int, c_p, ctypes.c_int, c_p, c_p],
+    "ss_knn_dense": [ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p],
+    "ss_isolation_dense": [ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, c_p, c_p],
     "ss_grid_fit": [ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_grid_cells_d": [ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_isolation_d": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
@@ -156,6 +160,7 @@ def load(require_cuda=True):
         lib.ss_train_backward_scratch_words.restype = ctypes.c_size_t
         lib.ss_env_khat_words.restype = ctypes.c_size_t
         lib.ss_refine_workspace_bytes.restype = ctypes.c_size_t
+        lib.ss_cell_grid_words.restype = ctypes.c_size_t
         lib.ss_last_error.restype = ctypes.c_char_p
         lib.ss_version.restype = ctypes.c_int
         _lib = lib
@@ -214,3 +219,14 @@ def make_env(env):
     he, we = env.shape
     return SsEnv(ptr(env.diffuse), ptr(env.specular), ptr(env.lut), he, we, env.levels, env.lut.shape[0],
                  ptr(getattr(env, "diffuse4", None)), ptr(getattr(env, "specular4", None)))
+
+
+def cell_grid(centers, n):
+    """Dense cell grid over `centers` (ss_cell_grid_build): (words, dim).
+    dim ~ sqrt(n / 24) so a surface sampling puts tens of surfels in each
+    occupied cell (<= 256: a 67 MB table)."""
+    dim = int(min(256, max(1, round((max(n, 1) / 24.0) ** 0.5))))
+    lib = load()
+    words = torch.empty(int(lib.ss_cell_grid_words(n, dim)), device=centers.device, dtype=torch.int32)
+    check(lib.ss_cell_grid_build(n, ptr(centers), dim, ptr(words), stream_ptr()), "ss_cell_grid_build")
+    return words, dim

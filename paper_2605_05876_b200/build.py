@@ -16,7 +16,7 @@ LIB = os.path.join(OUT_DIR, "libss_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["abi.cu", "preprocess.cu", "binning.cu", "raster_fwd.cu", "raster_bwd.cu", "chain_bwd.cu",
-           "env.cu", "optim.cu", "train_step.cu", "losses.cu", "knn.cu", "refine.cu"]
+           "env.cu", "optim.cu", "train_step.cu", "losses.cu", "knn.cu", "refine.cu", "grid.cu"]
 # preprocess mirrors numpy float32 expression by expression: no contraction
 NO_FMAD = {"preprocess.cu"}
 

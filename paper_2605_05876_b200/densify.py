@@ -61,25 +61,17 @@ class DensifyStats:
 
 def isolated_flags(cloud: SurfelCloud) -> torch.Tensor:
     """uint8 per surfel: 1 where the nearest other centre lies beyond
-    R_CUT * max scale (densify.py:118-123).  Uniform-grid fixed-radius query
-    with the grid sized on the device (ss_grid_fit): no host round trip."""
+    R_CUT * max scale (densify.py:118-123).  Fixed-radius existence query on
+    a dense cell grid built on the device (csrc/grid.cu): no host round trip."""
     n = len(cloud)
     dev = cloud.centers.device
     if n <= 1:
         return torch.zeros(n, device=dev, dtype=torch.uint8)
     lib = _lib.load()
-    s = _lib.stream_ptr()
-    c = cloud.centers
-    grid = torch.empty(16, device=dev, dtype=torch.float32)
-    _lib.check(lib.ss_grid_fit(n, _lib.ptr(c), _lib.ptr(cloud.log_scales), _lib.ptr(grid), s), "ss_grid_fit")
-    cells = torch.empty(n, device=dev, dtype=torch.int32)
-    _lib.check(lib.ss_grid_cells_d(n, _lib.ptr(c), _lib.ptr(grid), _lib.ptr(cells), s), "ss_grid_cells_d")
-    sorted_cells, order = torch.sort(cells, stable=True)
-    order = order.to(torch.int32).contiguous()
-    sorted_cells = sorted_cells.contiguous()
+    grid, dim = _lib.cell_grid(cloud.centers, n)
     iso = torch.empty(n, device=dev, dtype=torch.uint8)
-    _lib.check(lib.ss_isolation_d(n, _lib.ptr(c), _lib.ptr(cloud.log_scales), _lib.ptr(order), _lib.ptr(sorted_cells),
-                                  _lib.ptr(grid), _lib.ptr(iso), s), "ss_isolation_d")
+    _lib.check(lib.ss_isolation_dense(n, _lib.ptr(cloud.centers), _lib.ptr(cloud.log_scales), _lib.ptr(grid), dim,
+                                      _lib.ptr(iso), _lib.stream_ptr()), "ss_isolation_dense")
     return iso
 
 
