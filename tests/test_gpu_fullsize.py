@@ -216,3 +216,47 @@ def test_config1_training_gradients_full_size():
     g = np.sign(rgb - host(target)) / rgb.size  # same L1 sign pattern on both sides
     og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
     _check_step_grads(ts, og, "config1", ores)
+
+
+def test_config4_view_full_size_vs_oracle():
+    """BASELINE config 4's single view at full size: 4M surfels on the
+    5-octave displaced icosphere (amplitude 0.12), 1920x1080, env 256x512 --
+    tile lists, layer counts and images vs the oracle, training gradients
+    (0 entries outside tolerance) and the refinement pass that follows
+    every config-4 step (q = 0.95) vs the oracle's refine_topology."""
+    from paper_2605_05876_b200 import densify
+    gt = scenes.config2(0, 4_000_000, amp=0.12, octaves=5)
+    opt = scenes.perturb(gt, 1)
+    base_log = np.log(scenes.env_lognormal(256, 512, 2))
+    cam = ss.fibonacci_cameras(128, 3.5, 1920, 1080)[7]
+    env = ss.EnvironmentLight(base_log)
+    target = ss.render(ss.SurfelCloud(**gt), cam, ss.RenderOptions(), env=env).rgb.contiguous()
+    cloud = ss.SurfelCloud(**opt)
+    res = ss.render(cloud, cam, ss.RenderOptions(), env=env)
+    oenv = _oracle_env(base_log)
+    co = SimpleNamespace(**opt)
+    ores = O.render(co, cam, env=oenv)
+    np.testing.assert_array_equal(host(res.tile_offsets), ores.tile_offsets)
+    np.testing.assert_array_equal(host(res.pair_rec), ores.pair_rec)
+    np.testing.assert_array_equal(host(res.nlayers), ores.nlayers)
+    bad, err = image_close(res.rgb, ores.rgb)
+    assert bad == 0, err
+    ts = TrainStep(cloud, env, 1920, 1080)
+    ts.captured_rgb = []
+    ts.gradients([cam], [target])
+    rgb = host(ts.captured_rgb[-1]).astype(np.float64)
+    g = np.sign(rgb - host(target)) / rgb.size
+    og = O.backward_image(co, ores, g, None, 0.0, env=oenv)
+    _check_step_grads(ts, og, "config4", ores)
+    # the per-step refinement (q = 0.95, budget 1.05 N) on this step's stats
+    stats = ss.DensifyStats.zeros(len(cloud))
+    stats.accumulate(ts.grads["ss_grad"], ts.view_count)
+    mnd = ss.NeighborIndex(cloud, k=8).mean_dist
+    new, imap, reasons = ss.refine_topology(cloud, stats, mnd, 4_200_000, quantile=0.95)
+    keep, split_rows, want_map, want = O.refine_topology(
+        opt["centers"], opt["quats"], opt["log_scales"], host(stats.grad_sum), host(stats.view_count), host(mnd),
+        4_200_000, quantile=0.95)
+    assert {k: reasons[k] for k in ("stale", "isolated", "floater", "split")} == \
+        {k: want[k] for k in ("stale", "isolated", "floater", "split")}
+    assert densify.LAST_REFINE["threshold"] == want["threshold"]
+    np.testing.assert_array_equal(host(imap), want_map)
