@@ -142,7 +142,10 @@ typedef double TT;
 #define TT_VIEW P.view
 #endif
 
-__global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
+#ifndef SS_CHAIN_MINB
+#define SS_CHAIN_MINB 4
+#endif
+__global__ void __launch_bounds__(128, SS_CHAIN_MINB) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.cloud.n || P.cull[i] != 0) return;
@@ -186,7 +189,11 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
             G4[c] = (T1[c1] * Sy[c2] - T1[c2] * Sy[c1]) - (T2[c1] * Sx[c2] - T2[c2] * Sx[c1]);
         }
     }
+#ifdef SS_EXP_NO_MIP
+    if (false) {
+#else
     if (P.mip) {
+#endif
         // _mip_chain_backward (backward.py:473-548)
         float jf[4];
         const bool ok = ss_center_jacobian(t1f, t2f, t4f, P.W, P.H, jf);
@@ -281,17 +288,25 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
     TT gcent[3] = {gw[0], gw[1], gw[2]};
     float galb[3] = {0.f, 0.f, 0.f}, gmet = 0.f, grough = 0.f;
 
+#ifdef SS_EXP_NO_SHADE
+    if (false) {
+#else
     if (P.color_source == SS_COLOR_IBL) {
+#endif
         // the forward state in float64 like the preprocess kernel's colours
         // (identical texel cells / level / clip branches as the forward and
         // the reference's shading_ctx), the adjoint arithmetic in float32
         // (gradients: the 1e-3 parity bar)
         ShadeIn<float> in;
         ShadeState<float> st;
+        ShadeGrads<float> sg;
+        const float gcf[3] = {(float)gcol[0], (float)gcol[1], (float)gcol[2]};
         if (P.cells && P.env.diffuse4 && P.env.specular4) {
             // the preprocess kernel's float64 branch decisions, float32 state
+            // with the texel derivatives read together with the values
             ss_shade_inputs(cl, i, P.cam_pos, in);
             ss_shade_forward_cells(in, P.env, __ldg(P.cells + i), st);
+            ss_shade_backward<float, true>(in, st, P.env, gcf, sg);
         } else {
             ShadeIn<double> in64;
             ss_shade_inputs(cl, i, P.cam_pos, in64);
@@ -299,10 +314,8 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
             double col[3];
             ss_shade_forward(in64, P.env, st64, col);
             ss_shade_narrow(in64, st64, in, st);
+            ss_shade_backward(in, st, P.env, gcf, sg);
         }
-        ShadeGrads<float> sg;
-        const float gcf[3] = {(float)gcol[0], (float)gcol[1], (float)gcol[2]};
-        ss_shade_backward(in, st, P.env, gcf, sg);
         for (int c = 0; c < 3; ++c) { gcent[c] += sg.center[c]; gN[c] = sg.normal[c]; galb[c] = sg.albedo_raw[c]; }
         gmet = sg.metallic_raw;
         grough = sg.roughness_raw;
@@ -319,7 +332,11 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
         const int didx[4] = {bd.j0 * we + bd.i0, bd.j0 * we + bd.i1, bd.j1 * we + bd.i0, bd.j1 * we + bd.i1};
         const double dcw[4] = {(1.0 - bd.tu) * (1.0 - bd.tv), (double)bd.tu * (1.0 - bd.tv), (1.0 - bd.tu) * (double)bd.tv,
                                (double)bd.tu * bd.tv};
+#ifdef SS_EXP_NO_SCATTER
+        if (P.g.d_specular4 && sg.g_ls[0] == 12345.f) {  // (experiment: never true)
+#else
         if (P.g.d_specular4) {  // per-view float32 maps, folded into the float64 sums per view
+#endif
             for (int h = 0; h < 2; ++h)
                 for (int k = 0; k < 4; ++k) {
                     const float f = (float)(wts[h] * scw[k]);
@@ -329,7 +346,7 @@ __global__ void __launch_bounds__(128, 4) chain_kernel(ChainParams P)
                 const float f = (float)dcw[k];
                 scatter_rgb4(P.g.d_diffuse4, didx[k], sg.g_ld[0] * f, sg.g_ld[1] * f, sg.g_ld[2] * f);
             }
-        } else {
+        } else if (!P.g.d_specular4) {
             for (int h = 0; h < 2; ++h)  // level lvs[h] texel sidx[k] = element 3 * (lvs[h] * T + sidx[k])
                 for (int k = 0; k < 4; ++k) {
                     const double f = wts[h] * scw[k];

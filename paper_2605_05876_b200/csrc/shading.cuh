@@ -113,6 +113,38 @@ __device__ __forceinline__ void ss_bil_grads4(const float4 *__restrict__ tex, in
     }
 }
 
+// value and coordinate derivatives of one bilinear lookup from ONE read of
+// its four texels (the forward and the adjoint of the chain kernel share it)
+template <typename R>
+__device__ __forceinline__ void ss_bil_lookup_grads4(const float4 *__restrict__ tex, int w, const SsBil<R> &b, R *out,
+                                                     R *gu, R *gv) {
+    const float4 A = __ldg(tex + b.j0 * w + b.i0), B = __ldg(tex + b.j0 * w + b.i1);
+    const float4 Cc = __ldg(tex + b.j1 * w + b.i0), D = __ldg(tex + b.j1 * w + b.i1);
+    const R tu = b.tu, tv = b.tv;
+    const R wa = (1 - tu) * (1 - tv), wb = tu * (1 - tv), wc = (1 - tu) * tv, wd = tu * tv;
+    const R a[3] = {A.x, A.y, A.z}, bb[3] = {B.x, B.y, B.z}, c[3] = {Cc.x, Cc.y, Cc.z}, d[3] = {D.x, D.y, D.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        out[k] = wa * a[k] + wb * bb[k] + wc * c[k] + wd * d[k];
+        gu[k] = b.du_ok ? (1 - tv) * (bb[k] - a[k]) + tv * (d[k] - c[k]) : R(0.0);
+        gv[k] = b.dv_ok ? (1 - tu) * (c[k] - a[k]) + tu * (d[k] - bb[k]) : R(0.0);
+    }
+}
+
+template <int C, typename R>
+__device__ __forceinline__ void ss_bil_lookup_grads(const float *__restrict__ tex, int w, const SsBil<R> &b, R *out,
+                                                    R *gu, R *gv) {
+    const R tu = b.tu, tv = b.tv;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        R A = tex[(b.j0 * w + b.i0) * C + c], B = tex[(b.j0 * w + b.i1) * C + c];
+        R Cc = tex[(b.j1 * w + b.i0) * C + c], D = tex[(b.j1 * w + b.i1) * C + c];
+        out[c] = (1 - tu) * (1 - tv) * A + tu * (1 - tv) * B + (1 - tu) * tv * Cc + tu * tv * D;
+        gu[c] = b.du_ok ? (1 - tv) * (B - A) + tv * (D - Cc) : R(0.0);
+        gv[c] = b.dv_ok ? (1 - tu) * (Cc - A) + tu * (D - B) : R(0.0);
+    }
+}
+
 template <int C, typename R>
 __device__ __forceinline__ void ss_bil_grads(const float *__restrict__ tex, int w, const SsBil<R> &b, R *gu, R *gv) {
     const R tu = b.tu, tv = b.tv;
@@ -185,6 +217,9 @@ struct ShadeState {
     R ndv_raw, refl[3], l_d[3], l_s[3], spec_lo[3], spec_hi[3], b1, b2, f0[3], k_d[3], frac;
     int lvl0, lvl1;
     SsBil<R> bd, bs, bl;
+    // texel derivatives of the lookups, when the forward kept them
+    // (ss_shade_forward_cells): diffuse, specular lo / hi, LUT
+    R dgu[3], dgv[3], sgu[2][3], sgv[2][3], lgu[2], lgv[2];
 };
 
 // Activated materials, float64 normal and view direction of surfel i.
@@ -328,19 +363,19 @@ __device__ __forceinline__ void ss_shade_forward_cells(const ShadeIn<float> &in,
     s.bd = ss_bil_forced(he, we, fu, fv, true, cells.x, true, (fl & 1u) != 0);
     const float4 *d4 = reinterpret_cast<const float4 *>(env.diffuse4);
     const float4 *s4 = reinterpret_cast<const float4 *>(env.specular4);
-    ss_bil_lookup4(d4, we, s.bd, s.l_d);
+    ss_bil_lookup_grads4(d4, we, s.bd, s.l_d, s.dgu, s.dgv);
     const float lvl = ss_clip<float>(in.r, 0.f, 1.f) * (L - 1);
     s.lvl0 = (int)(cells.w & 0xffu);
     s.frac = L > 1 ? lvl - (float)s.lvl0 : 0.f;
     s.lvl1 = s.lvl0 + 1 < L - 1 ? s.lvl0 + 1 : L - 1;
     ss_dir_coords(s.refl, he, we, fu, fv);
     s.bs = ss_bil_forced(he, we, fu, fv, true, cells.y, true, (fl & 2u) != 0);
-    ss_bil_lookup4(s4 + (size_t)he * we * s.lvl0, we, s.bs, s.spec_lo);
-    ss_bil_lookup4(s4 + (size_t)he * we * s.lvl1, we, s.bs, s.spec_hi);
+    ss_bil_lookup_grads4(s4 + (size_t)he * we * s.lvl0, we, s.bs, s.spec_lo, s.sgu[0], s.sgv[0]);
+    ss_bil_lookup_grads4(s4 + (size_t)he * we * s.lvl1, we, s.bs, s.spec_hi, s.sgu[1], s.sgv[1]);
     for (int c = 0; c < 3; ++c) s.l_s[c] = (1.f - s.frac) * s.spec_lo[c] + s.frac * s.spec_hi[c];
     s.bl = ss_bil_forced(LR, LR, ndv * (LR - 1), in.r * (LR - 1), false, cells.z, (fl & 4u) != 0, (fl & 8u) != 0);
     float bb[2];
-    ss_bil_lookup<2>(env.lut, LR, s.bl, bb);
+    ss_bil_lookup_grads<2>(env.lut, LR, s.bl, bb, s.lgu, s.lgv);
     s.b1 = bb[0]; s.b2 = bb[1];
     for (int c = 0; c < 3; ++c) {
         s.f0[c] = 0.04f * (1.f - in.m) + in.albedo[c] * in.m;
@@ -365,7 +400,9 @@ struct ShadeGrads {
 };
 
 // shade_backward for one surfel (shading.py:525-615), env adjoint excluded.
-template <typename R>
+// kStored: the texel derivatives come from the forward state (one texel
+// read per lookup); else they are re-read here
+template <typename R, bool kStored = false>
 __device__ __forceinline__ void ss_shade_backward(const ShadeIn<R> &in, const ShadeState<R> &s, const SsEnv &env,
                                                   const R g[3], ShadeGrads<R> &o) {
     const int he = env.he, we = env.we, L = env.levels, LR = env.lut_res;
@@ -384,7 +421,11 @@ __device__ __forceinline__ void ss_shade_backward(const ShadeIn<R> &in, const Sh
     g_met += (g_f0[0] * (in.albedo[0] - R(0.04)) + g_f0[1] * (in.albedo[1] - R(0.04))) + g_f0[2] * (in.albedo[2] - R(0.04));
     for (int c = 0; c < 3; ++c) g_alb[c] += g_f0[c] * in.m;
     R dfx[2], dfy[2];
-    ss_bil_grads<2>(env.lut, LR, s.bl, dfx, dfy);
+    if constexpr (kStored) {
+        dfx[0] = s.lgu[0]; dfx[1] = s.lgu[1]; dfy[0] = s.lgv[0]; dfy[1] = s.lgv[1];
+    } else {
+        ss_bil_grads<2>(env.lut, LR, s.bl, dfx, dfy);
+    }
     R g_ndv = (g_b1 * dfx[0] + g_b2 * dfx[1]) * (LR - 1);
     R g_rough = (g_b1 * dfy[0] + g_b2 * dfy[1]) * (LR - 1);
     bool active = (s.ndv_raw > R(0.0)) && (s.ndv_raw < R(1.0));
@@ -400,10 +441,13 @@ __device__ __forceinline__ void ss_shade_backward(const ShadeIn<R> &in, const Sh
     const int lv[2] = {s.lvl0, s.lvl1};
     for (int h = 0; h < 2; ++h) {
         R gu[3], gv[3];
-        if (env.specular4)
+        if constexpr (kStored) {
+            for (int c = 0; c < 3; ++c) { gu[c] = s.sgu[h][c]; gv[c] = s.sgv[h][c]; }
+        } else if (env.specular4) {
             ss_bil_grads4(reinterpret_cast<const float4 *>(env.specular4) + (size_t)he * we * lv[h], we, s.bs, gu, gv);
-        else
+        } else {
             ss_bil_grads<3>(env.specular + lstride * lv[h], we, s.bs, gu, gv);
+        }
         R gh0 = o.g_ls[0] * wts[h], gh1 = o.g_ls[1] * wts[h], gh2 = o.g_ls[2] * wts[h];
         R gfu = (gh0 * gu[0] + gh1 * gu[1]) + gh2 * gu[2];
         R gfv = (gh0 * gv[0] + gh1 * gv[1]) + gh2 * gv[2];
@@ -412,8 +456,13 @@ __device__ __forceinline__ void ss_shade_backward(const ShadeIn<R> &in, const Sh
         for (int c = 0; c < 3; ++c) g_refl[c] += gd[c];
     }
     R gu[3], gv[3];
-    if (env.diffuse4) ss_bil_grads4(reinterpret_cast<const float4 *>(env.diffuse4), we, s.bd, gu, gv);
-    else ss_bil_grads<3>(env.diffuse, we, s.bd, gu, gv);
+    if constexpr (kStored) {
+        for (int c = 0; c < 3; ++c) { gu[c] = s.dgu[c]; gv[c] = s.dgv[c]; }
+    } else if (env.diffuse4) {
+        ss_bil_grads4(reinterpret_cast<const float4 *>(env.diffuse4), we, s.bd, gu, gv);
+    } else {
+        ss_bil_grads<3>(env.diffuse, we, s.bd, gu, gv);
+    }
     R gfu = (o.g_ld[0] * gu[0] + o.g_ld[1] * gu[1]) + o.g_ld[2] * gu[2];
     R gfv = (o.g_ld[0] * gv[0] + o.g_ld[1] * gv[1]) + o.g_ld[2] * gv[2];
     R g_n[3];

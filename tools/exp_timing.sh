@@ -1,0 +1,8 @@
+# per-stage timing for each build variant in VARIANTS (';'-separated SS_NVCC_FLAGS), baseline first
+IFS=';' read -ra VS <<< "${VARIANTS:-}"
+for F in "" "${VS[@]}"; do
+  echo "=== variant: ${F:-baseline}"
+  SS_NVCC_FLAGS="$F" python -c "from paper_2605_05876_b200 import build as b; b.build(force=True)" || exit 1
+  NVIEWS=16 STREAMS=${STREAMS:-1,3} python tools/kernel_timing.py 2>&1 | tail -9
+done
+SS_NVCC_FLAGS="" python -c "from paper_2605_05876_b200 import build as b; b.build(force=True)"
