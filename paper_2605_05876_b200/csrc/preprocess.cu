@@ -156,6 +156,10 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
     float col[3] = {0.f, 0.f, 0.f};
     if (color_source == SS_COLOR_EXPLICIT) {
         col[0] = colors_in[3 * i]; col[1] = colors_in[3 * i + 1]; col[2] = colors_in[3 * i + 2];
+#ifdef SS_EXP_NO_SHADE
+    } else if (true) {
+        col[0] = ss_sigmoid_f32(ar0); col[1] = ss_sigmoid_f32(ar1); col[2] = ss_sigmoid_f32(ar2);
+#endif
     } else if (color_source == SS_COLOR_ALBEDO) {
         col[0] = ss_sigmoid_f32(ar0); col[1] = ss_sigmoid_f32(ar1); col[2] = ss_sigmoid_f32(ar2);
     } else if (color_source == SS_COLOR_IBL_F32) {
@@ -183,7 +187,11 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
     rec.c = make_float4(t4[2], m00, m01, m11);
     rec.d = make_float4(nf, vz, zs, ze);
     // e.w: certified fast-coverage margin of this record (coverage.cuh)
+#ifdef SS_EXP_NO_MARGIN
+    const float cm = alive ? 1.f
+#else
     const float cm = alive ? coverage_margin(t1, t2, t4, m00, m01, m11, (int)x0, (int)y0, (int)x1, (int)y1, cam.W, cam.H)
+#endif
                            : 0.f;
     rec.e = make_float4(col[0], col[1], col[2], cm);
     int count = 0;
