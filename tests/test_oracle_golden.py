@@ -203,3 +203,25 @@ def test_knn_oracle_matches_reference_goldens(name):
     loss, g = O.normal_consistency(d[f"{name}_centers"], d[f"{name}_quats"], nb, md)
     assert loss == pytest.approx(float(d[f"{name}_nc_loss"]), rel=1e-13)
     np.testing.assert_allclose(g, d[f"{name}_nc_grad"], rtol=1e-9, atol=1e-16)
+
+
+def test_refine_oracle_tree_path_matches_brute_force():
+    """The oracle's refine_topology switches to the reference's own cKDTree
+    isolation query above 4000 surfels (densify.py:119-121); both paths give
+    the same plan on the same input."""
+    rng = np.random.default_rng(3)
+    n = 3000
+    c = rng.normal(size=(n, 3)).astype(np.float32)
+    c /= np.linalg.norm(c, axis=1, keepdims=True)
+    c[:20] *= 3.0
+    q = rng.normal(size=(n, 4)).astype(np.float32)
+    ls = np.log(rng.uniform(0.01, 0.05, (n, 2))).astype(np.float32)
+    gs = rng.exponential(1e-4, n)
+    gs[rng.uniform(size=n) < 0.1] = 0.0
+    vc = rng.integers(0, 5, n)
+    mnd = rng.uniform(0.01, 0.04, n)
+    a = O.refine_topology(c, q, ls, gs, vc, mnd, int(1.02 * n), quantile=0.95)
+    big = np.concatenate([c, c + 100.0])  # a far copy: > 4000 rows takes the tree path
+    b = O.refine_topology(big, np.concatenate([q, q]), np.concatenate([ls, ls]), np.concatenate([gs, gs]),
+                          np.concatenate([vc, vc]), np.concatenate([mnd, mnd]), int(2.04 * n), quantile=0.95)
+    assert np.array_equal(b[0][:n], a[0]) and b[3]["isolated"] == 2 * a[3]["isolated"]
