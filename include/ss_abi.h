@@ -79,6 +79,9 @@ typedef struct SsEnv {
      * loads in the shading kernels) */
     const float *diffuse4;  /* (He,We,4) */
     const float *specular4; /* (L,He,We,4) */
+    /* nullable: the float64 maps (ss_env_refresh), read by the float64 shading */
+    const double *diffuse64;  /* (He,We,3) */
+    const double *specular64; /* (L,He,We,3) */
 } SsEnv;
 
 typedef struct SsPreprocessOpts {
@@ -193,11 +196,12 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
  * ss_train_forward: the forward walk fused with the L1 photometric loss
  * (losses.py:94-108, lambda_ssim=0) against `target` (H,W,3) and with the
  * per-pixel suffix recursion of backward.py:201-238.  Writes per pixel and
- * layer the float4 (A_hi, dL/dC_raw rgb) into `coef` (k_max*H*W*5 floats:
- * k_max layer-major float4 planes, then k_max float planes of A_lo; A =
- * A_hi + A_lo is formed from the float-rounded dL/dC_raw so that the
- * backward's g_w = A + dL/dC_raw . colour keeps the record colour - layer
- * mean colour difference exactly; layer sums are float64), per pixel a packed header `pix_hdr` (H*W x 8
+ * layer the float4 (A_hi, dL/dC_raw rgb) into `coef` (k_max*H*W*9 floats:
+ * k_max layer-major float4 planes, then k_max float planes of A_lo, then
+ * k_max float4 planes the deferred variant uses for the low parts of its
+ * float64 layer sums; A = A_hi + A_lo is formed from the float-rounded
+ * dL/dC_raw so that the backward's g_w = A + dL/dC_raw . colour keeps the
+ * record colour - layer mean colour difference exactly), per pixel a packed header `pix_hdr` (H*W x 8
  * int32: number of closed layers, then the depths at which layers 0..6
  * closed, as float bits; words past the closed count are not written) and
  * the closing depths of layers >= 7 into `thr` (k_max*H*W floats, plane j), and adds sum|rgb - target| into loss_sum (1 double).
@@ -222,8 +226,11 @@ int ss_train_forward(int width, int height, int tile, const int32_t *tile_offset
  * ss_train_coefs turns them into the backward coefficients in place (suffix
  * recursion of backward.py:201-238 incl. the coverage term).  pix_hdr.x =
  * closed layers | layer count << 8. */
+/* g_rgb64 (nullable): the same image gradient in float64 (ss_photometric_loss
+ * grad64), used instead of g_rgb -- the layer coefficients' colour terms
+ * cancel, so a float32-rounded gradient biases them by ~1e-5 */
 int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef, const float *g_rgb,
-                   const float *g_alpha, const float *background, void *stream);
+                   const double *g_rgb64, const float *g_alpha, const float *background, void *stream);
 /* The same three steps with the consolidation penalty (backward.py:160-320
  * with cons_scale > 0): ss_train_forward_zstats is the deferred forward that
  * also writes, per pixel and layer, the depth moments (z0, sum w dz,
@@ -238,8 +245,8 @@ int ss_train_forward_zstats(int width, int height, int tile, const int32_t *tile
                             const float *background, int k_max, float *coef, float *thr, int32_t *pix_hdr,
                             float *rgb, float *alpha, const int32_t *tile_order, float *zstats, void *stream);
 int ss_train_coefs_cons(int width, int height, int k_max, const int32_t *pix_hdr, float *coef, float *zstats,
-                        const float *g_rgb, const float *g_alpha, const float *background, double cons_scale,
-                        double *cons_loss, void *stream);
+                        const float *g_rgb, const double *g_rgb64, const float *g_alpha, const float *background,
+                        double cons_scale, double *cons_loss, void *stream);
 int ss_train_backward_records_cons(int n, const int8_t *cull, const float *records, int width, int height,
                                    int k_max, const float *coef, const float *thr, const int32_t *pix_hdr,
                                    const float *zcoef, float *pixel_ndc, float *rec_acc, double *rec_acc64,
@@ -260,13 +267,15 @@ int ss_train_backward_records(int n, const int8_t *cull, const float *records, i
  * ssim_loss / photometric_loss (losses.py:45-108) and silhouette_loss
  * (losses.py:111-123).  Images (H, W, C) float32, C in {1, 3}; float64
  * internally.  ss_photometric_loss: loss = (1 - l) mean|T(x) - T(y)| +
- * l (1 - mean SSIM(T(x), T(y))), its gradient w.r.t. x (through T) into grad,
+ * l (1 - mean SSIM(T(x), T(y))), its gradient w.r.t. x (through T) into grad
+ * (and, nullable, in float64 into grad64),
  * out[3] = {loss, L1, 1 - SSIM} (device doubles, no host sync); lambda = 1
  * gives ssim_loss.  workspace: ss_photometric_workspace() bytes.
  * ss_silhouette_loss: out[1] = 1 - soft IoU, grad d/d alpha; workspace 2 doubles. */
 size_t ss_photometric_workspace(int height, int width, int channels);
 int ss_photometric_loss(int height, int width, int channels, const float *x, const float *y, int tone_mode,
-                        double lambda_ssim, double *out, float *grad, double *workspace, void *stream);
+                        double lambda_ssim, double *out, float *grad, double *grad64, double *workspace,
+                        void *stream);
 int ss_tone_map(int64_t n, const float *img, int tone_mode, float *out, void *stream);
 int ss_tone_map_backward(int64_t n, const float *img, int tone_mode, const float *g_out, float *g_in, void *stream);
 int ss_silhouette_loss(int64_t n, const float *alpha, const float *mask, double *out, float *grad,
@@ -352,7 +361,7 @@ int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void *stream);
  * The prefilter operators of the reference (build_diffuse_operator /
  * build_specular_operator, shading.py:275-331: dense T x T float64) are
  * passed as a caller-owned bundle, built once per env shape:
- *   rowsum  (He*We floats) diffuse row sums, from ss_env_rowsums;
+ *   rowsum  (He*We doubles) diffuse row sums, from ss_env_rowsums;
  *   khat    (nullable) the diffuse kernel's spectrum, ss_env_khat_words(He,We)
  *           doubles filled by ss_env_khat (0 words: odd widths / too large;
  *           NULL selects the O(T^2) N-body quadrature);
@@ -363,19 +372,24 @@ int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void *stream);
  *   work    3*He*We doubles of scratch.
  * The library keeps no state and allocates nothing. */
 typedef struct SsEnvOps {
-    const float *rowsum;
+    const double *rowsum;
     const double *khat;
-    const int64_t *row_ptr; const int32_t *col; const float *rval;
-    const int64_t *col_ptr; const int32_t *row; const float *cval;
+    const int64_t *row_ptr; const int32_t *col; const double *rval;
+    const int64_t *col_ptr; const int32_t *row; const double *cval;
     double *work;
 } SsEnvOps;
 int ss_brdf_lut(int res, int samples, float *lut, void *stream);
 size_t ss_env_khat_words(int he, int we);
 int ss_env_khat(int he, int we, double *khat, void *stream);
-int ss_env_rowsums(int he, int we, const double *khat, float *rowsum, double *work, void *stream);
+int ss_env_rowsums(int he, int we, const double *khat, double *rowsum, double *work, void *stream);
+/* The maps are computed in float64 like the reference's (base = exp(base_log),
+ * dense float64 operator products, shading.py:369-379) into base64 (He,We,3),
+ * diffuse64 (He,We,3), specular64 (L,He,We,3) -- read by the float64 shading
+ * (SsEnv.diffuse64/specular64) -- and rounded into the float maps. */
 int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log, const SsEnvOps *ops,
-                   float *base, float *diffuse, float *specular, void *stream);
-int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, const SsEnvOps *ops,
+                   float *base, float *diffuse, float *specular, double *base64, double *diffuse64,
+                   double *specular64, void *stream);
+int ss_env_adjoint(int he, int we, int levels, int samples, const double *base64, const SsEnvOps *ops,
                    const double *d_diffuse, const double *d_specular, double *d_base, float *d_base_log,
                    void *stream);
 
@@ -385,15 +399,15 @@ int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, c
  * sums them); weights are divided by the row weight sum; empty rows hold one
  * identity entry.  ss_spec_op_count -> row_nnz ((L-1)*T int32), the caller
  * scans it into row_ptr ((L-1)*T+1 int64), ss_spec_op_fill -> col (int32),
- * val (float).  The caller builds the per-level transpose (CSC: col_ptr over
+ * val (double).  The caller builds the per-level transpose (CSC: col_ptr over
  * (l-1)*T + j, row, val) with a stable sort and passes both in SsEnvOps.
  * ss_spec_apply / ss_spec_apply_t expose the two products directly. */
 int ss_spec_op_count(int he, int we, int levels, int samples, int32_t *row_nnz, void *stream);
-int ss_spec_op_fill(int he, int we, int levels, int samples, const int64_t *row_ptr, int32_t *col, float *val,
+int ss_spec_op_fill(int he, int we, int levels, int samples, const int64_t *row_ptr, int32_t *col, double *val,
                     void *stream);
-int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const float *val,
-                  const float *base, float *specular, void *stream);
-int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row, const float *val,
+int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const double *val,
+                  const double *base, double *specular, float *specular_f, void *stream);
+int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row, const double *val,
                     const double *d_specular, double *d_base, void *stream);
 
 /* ---- optimiser ------------------------------------------------------------

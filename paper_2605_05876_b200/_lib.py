@@ -38,7 +38,7 @@ class SsCloud(ctypes.Structure):
 class SsEnv(ctypes.Structure):
     _fields_ = [("diffuse", c_p), ("specular", c_p), ("lut", c_p), ("he", ctypes.c_int),
                 ("we", ctypes.c_int), ("levels", ctypes.c_int), ("lut_res", ctypes.c_int),
-                ("diffuse4", c_p), ("specular4", c_p)]
+                ("diffuse4", c_p), ("specular4", c_p), ("diffuse64", c_p), ("specular64", c_p)]
 
 
 class SsPreprocessOpts(ctypes.Structure):
@@ -85,11 +85,12 @@ _SIGNATURES = {
     "ss_env_khat_words": [ctypes.c_int, ctypes.c_int],
     "ss_env_khat": [ctypes.c_int, ctypes.c_int, c_p, c_p],
     "ss_env_rowsums": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
-    "ss_env_refresh": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_env_refresh": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
+                       c_p],
     "ss_env_adjoint": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_spec_op_count": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p],
     "ss_spec_op_fill": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
-    "ss_spec_apply": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_spec_apply": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_spec_apply_t": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_adam_step": [ctypes.c_int64, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_float, ctypes.c_float,
                      ctypes.c_float, ctypes.c_float, c_p],
@@ -106,11 +107,12 @@ _SIGNATURES = {
                      ctypes.c_int, c_p, c_p],
     "ss_train_forward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
                          ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
-    "ss_train_coefs": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), c_p],
+    "ss_train_coefs": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float),
+                       c_p],
     "ss_train_forward_zstats": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, ctypes.c_int,
                                 c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
-    "ss_train_coefs_cons": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_double,
-                            c_p, c_p],
+    "ss_train_coefs_cons": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
+                            ctypes.c_double, c_p, c_p],
     "ss_train_backward_records_cons": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
                                        c_p, c_p, c_p, c_p, c_p],
     "ss_train_backward_scratch_words": [ctypes.c_int, ctypes.c_int, ctypes.c_int],
@@ -118,7 +120,7 @@ _SIGNATURES = {
                                   c_p, c_p, c_p, c_p],
     "ss_photometric_workspace": [ctypes.c_int, ctypes.c_int, ctypes.c_int],
     "ss_photometric_loss": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_double, c_p, c_p,
-                            c_p, c_p],
+                            c_p, c_p, c_p],
     "ss_tone_map": [ctypes.c_int64, c_p, ctypes.c_int, c_p, c_p],
     "ss_tone_map_backward": [ctypes.c_int64, c_p, ctypes.c_int, c_p, c_p, c_p],
     "ss_silhouette_loss": [ctypes.c_int64, c_p, c_p, c_p, c_p, c_p, c_p],
@@ -218,7 +220,8 @@ def make_env(env):
         return None
     he, we = env.shape
     return SsEnv(ptr(env.diffuse), ptr(env.specular), ptr(env.lut), he, we, env.levels, env.lut.shape[0],
-                 ptr(getattr(env, "diffuse4", None)), ptr(getattr(env, "specular4", None)))
+                 ptr(getattr(env, "diffuse4", None)), ptr(getattr(env, "specular4", None)),
+                 ptr(getattr(env, "diffuse64", None)), ptr(getattr(env, "specular64", None)))
 
 
 def cell_grid(centers, n):

@@ -67,7 +67,7 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, acc64, bgp, cons_scale=0.
     dev = st.records.device
     H, W, K = int(cam.height), int(cam.width), int(opt.k_max)
     f32 = dict(device=dev, dtype=torch.float32)
-    coef = torch.empty(5 * K * H * W, **f32)  # float4 planes + the A-lo plane
+    coef = torch.empty(9 * K * H * W, **f32)  # float4 planes, A_lo planes, raw-sum lo planes
     thr = torch.empty((K, H * W), **f32)
     hdr = torch.empty((H * W, 8), device=dev, dtype=torch.int32)
     rgb = torch.empty((H, W, 3), **f32)
@@ -80,7 +80,7 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, acc64, bgp, cons_scale=0.
                                                bgp, K, _lib.ptr(coef), _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(rgb), None,
                                                None, _lib.ptr(zst), _lib.stream_ptr()), "ss_train_forward_zstats")
         _lib.check(lib.ss_train_coefs_cons(W, H, K, _lib.ptr(hdr), _lib.ptr(coef), _lib.ptr(zst), _lib.ptr(g_rgb),
-                                           _lib.ptr(g_alpha), bgp, float(cons_scale), _lib.ptr(cons),
+                                           None, _lib.ptr(g_alpha), bgp, float(cons_scale), _lib.ptr(cons),
                                            _lib.stream_ptr()), "ss_train_coefs_cons")
         _lib.check(lib.ss_train_backward_records_cons(n, _lib.ptr(st.cull), _lib.ptr(st.records), W, H, K,
                                                       _lib.ptr(coef), _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(zst),
@@ -91,8 +91,8 @@ def _record_backward(lib, result, g_rgb, g_alpha, acc, acc64, bgp, cons_scale=0.
                                     _lib.ptr(st.pair_rect), _lib.ptr(st.records), bgp, K, None, _lib.ptr(coef),
                                     _lib.ptr(thr), _lib.ptr(hdr), None, _lib.ptr(rgb), None, None, _lib.stream_ptr()),
                "ss_train_forward")
-    _lib.check(lib.ss_train_coefs(W, H, K, _lib.ptr(hdr), _lib.ptr(coef), _lib.ptr(g_rgb), _lib.ptr(g_alpha), bgp,
-                                  _lib.stream_ptr()), "ss_train_coefs")
+    _lib.check(lib.ss_train_coefs(W, H, K, _lib.ptr(hdr), _lib.ptr(coef), _lib.ptr(g_rgb), None, _lib.ptr(g_alpha),
+                                  bgp, _lib.stream_ptr()), "ss_train_coefs")
     _lib.check(lib.ss_train_backward_records(n, _lib.ptr(st.cull), _lib.ptr(st.records), W, H, K, _lib.ptr(coef),
                                              _lib.ptr(thr), _lib.ptr(hdr), _lib.ptr(scratch), _lib.ptr(acc),
                                              _lib.ptr(acc64), _lib.stream_ptr()), "ss_train_backward_records")

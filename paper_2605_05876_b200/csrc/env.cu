@@ -76,7 +76,7 @@ constexpr int kSplit = 8;     // column range split across CTAs (fills the GPU: 
 
 template <int MODE, typename TIn>
 __global__ void __launch_bounds__(kDiffThreads) diffuse_kernel(int he, int we, const TIn *__restrict__ x,
-                                                               const float *__restrict__ rowsum,
+                                                               const double *__restrict__ rowsum,
                                                                double *__restrict__ part) {
     __shared__ float4 sd[kChunk];   // column direction (xyz, w unused)
     __shared__ float4 sv[kChunk];   // column value rgb with its factor folded in (w unused)
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kDiffThreads) diffuse_kernel(int he, int we, c
 
 // mode 0: rowsum_a = part; mode 1: out_a = part / rowsum_a; mode 2: out_a += om_a part
 template <int MODE, typename TOut>
-__global__ void diffuse_finish_kernel(int he, int we, const double *__restrict__ part, const float *__restrict__ rowsum,
+__global__ void diffuse_finish_kernel(int he, int we, const double *__restrict__ part, const double *__restrict__ rowsum,
                                       TOut *__restrict__ out) {
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= he * we) return;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(128) dspec_kernel(int he, int we, double *__re
 // packed per (channel, row) as we doubles: re0, re_{we/2}, re1, im1, ...
 template <int MODE, typename TIn>
 __global__ void __launch_bounds__(256) drow_dft_kernel(int he, int we, const TIn *__restrict__ x,
-                                                       const float *__restrict__ rowsum, double *__restrict__ vhat) {
+                                                       const double *__restrict__ rowsum, double *__restrict__ vhat) {
     extern __shared__ double dsm[];
     constexpr int NC = MODE == 0 ? 1 : 3;
     double *tc = dsm, *ts = dsm + we, *sv = dsm + 2 * we;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(128) dmul_kernel(int he, int we, const double 
 // (0: rowsum; 1: out = y / rowsum; 2: out += om y).
 template <int MODE, typename TOut>
 __global__ void __launch_bounds__(256) dinv_kernel(int he, int we, const double *__restrict__ yhat,
-                                                   const float *__restrict__ rowsum, TOut *__restrict__ out) {
+                                                   const double *__restrict__ rowsum, TOut *__restrict__ out) {
     extern __shared__ double dsm[];
     constexpr int NC = MODE == 0 ? 1 : 3;
     double *tc = dsm, *ts = dsm + we, *sy = dsm + 2 * we;  // sy[c][we] packed spectrum
@@ -330,7 +330,7 @@ bool spectral_ok(int he, int we) {
 // Diffuse quadrature: the spectral form with the caller's K^ when given
 // (ss_env_khat), else the N-body form.
 template <int MODE, typename TIn, typename TOut>
-int run_diffuse(int he, int we, const TIn *x, const float *rowsum, TOut *out, double *work, const double *khat,
+int run_diffuse(int he, int we, const TIn *x, const double *rowsum, TOut *out, double *work, const double *khat,
                 cudaStream_t st) {
     const int T = he * we;
     if (khat && spectral_ok(he, we)) {
@@ -396,7 +396,7 @@ __device__ __forceinline__ void texel_frame(int a, int he, int we, double d[3], 
 
 // specular[l] = S_l base (l >= 1); level 0 is the identity (shading.py:287-289)
 __global__ void __launch_bounds__(128) spec_refresh_kernel(int he, int we, int levels, int samples,
-                                                           const float *__restrict__ base, float *__restrict__ spec) {
+                                                           const double *__restrict__ base, double *__restrict__ spec) {
     const int T = he * we;
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     const int lv = blockIdx.y + 1;
@@ -416,11 +416,11 @@ __global__ void __launch_bounds__(128) spec_refresh_kernel(int he, int we, int l
             acc2 += o.w[k] * base[3 * o.idx[k] + 2];
         }
     }
-    float *out = spec + (size_t)lv * T * 3 + 3 * a;
+    double *out = spec + (size_t)lv * T * 3 + 3 * a;
     if (ws <= 0.0) {
         out[0] = base[3 * a]; out[1] = base[3 * a + 1]; out[2] = base[3 * a + 2];
     } else {
-        out[0] = (float)(acc0 / ws); out[1] = (float)(acc1 / ws); out[2] = (float)(acc2 / ws);
+        out[0] = acc0 / ws; out[1] = acc1 / ws; out[2] = acc2 / ws;
     }
 }
 
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(128) spec_count_kernel(int he, int we, int lev
 
 __global__ void __launch_bounds__(128) spec_fill_kernel(int he, int we, int levels, int samples,
                                                         const int64_t *__restrict__ row_ptr, int32_t *__restrict__ col,
-                                                        float *__restrict__ val) {
+                                                        double *__restrict__ val) {
     const int T = he * we;
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     const int lv = blockIdx.y + 1;
@@ -507,22 +507,25 @@ __global__ void __launch_bounds__(128) spec_fill_kernel(int he, int we, int leve
         SpecSample o;
         double wgt;
         if (!spec_sample(d, tx, ty, s, samples, alpha, he, we, o, wgt)) continue;
-        for (int k = 0; k < 4; ++k) { col[p] = o.idx[k]; val[p] = (float)(o.w[k] * inv); ++p; }
+        for (int k = 0; k < 4; ++k) { col[p] = o.idx[k]; val[p] = o.w[k] * inv; ++p; }
     }
 }
 
-// specular[l][i] = sum_e val_e base[col_e], one warp per row (l >= 1)
+// specular[l][i] = sum_e val_e base[col_e], one warp per row (l >= 1),
+// float64 like the reference's dense operator products; the float copy for
+// the float32 consumers (nullable)
 __global__ void __launch_bounds__(256) spec_apply_kernel(int T, int nrows, const int64_t *__restrict__ row_ptr,
-                                                         const int32_t *__restrict__ col, const float *__restrict__ val,
-                                                         const float *__restrict__ base, float *__restrict__ spec) {
+                                                         const int32_t *__restrict__ col, const double *__restrict__ val,
+                                                         const double *__restrict__ base, double *__restrict__ spec,
+                                                         float *__restrict__ spec_f) {
     const int lane = threadIdx.x & 31;
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (r >= nrows) return;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     for (int64_t p = row_ptr[r] + lane; p < row_ptr[r + 1]; p += 32) {
-        const float w = val[p];
+        const double w = val[p];
         const int j = col[p];
-        s0 = fmaf(w, base[3 * j], s0); s1 = fmaf(w, base[3 * j + 1], s1); s2 = fmaf(w, base[3 * j + 2], s2);
+        s0 = fma(w, base[3 * j], s0); s1 = fma(w, base[3 * j + 1], s1); s2 = fma(w, base[3 * j + 2], s2);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -531,8 +534,9 @@ __global__ void __launch_bounds__(256) spec_apply_kernel(int T, int nrows, const
         s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     }
     if (lane == 0) {
-        float *out = spec + (size_t)T * 3 + (size_t)r * 3;  // level l = r / T + 1
-        out[0] = s0; out[1] = s1; out[2] = s2;
+        const size_t o = (size_t)T * 3 + (size_t)r * 3;  // level l = r / T + 1
+        spec[o] = s0; spec[o + 1] = s1; spec[o + 2] = s2;
+        if (spec_f) { spec_f[o] = (float)s0; spec_f[o + 1] = (float)s1; spec_f[o + 2] = (float)s2; }
     }
 }
 
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(256) spec_apply_kernel(int T, int nrows, const
 // transpose (CSC, per level) is the caller's stable sort of the entries by
 // (level, column); one warp per output texel.
 __global__ void __launch_bounds__(256) spec_apply_t_kernel(int T, int levels, const int64_t *__restrict__ col_ptr,
-                                                           const int32_t *__restrict__ row, const float *__restrict__ val,
+                                                           const int32_t *__restrict__ row, const double *__restrict__ val,
                                                            const double *__restrict__ g, double *__restrict__ d_base) {
     const int lane = threadIdx.x & 31;
     const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -564,21 +568,31 @@ __global__ void __launch_bounds__(256) spec_apply_t_kernel(int T, int levels, co
     if (lane == 0) { d_base[3 * j] += s0; d_base[3 * j + 1] += s1; d_base[3 * j + 2] += s2; }
 }
 
-__global__ void exp_kernel(int n, const float *__restrict__ lg, float *__restrict__ base, float *__restrict__ spec0) {
+// base = exp(base_log) in float64 (the reference's base, shading.py:373)
+// and its float copies; level 0 of the specular chain is the base itself
+__global__ void exp_kernel(int n, const float *__restrict__ lg, float *__restrict__ base, float *__restrict__ spec0,
+                           double *__restrict__ base64, double *__restrict__ spec0_64) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const float b = (float)exp((double)lg[k]);
-    base[k] = b;
-    spec0[k] = b;
+    const double b = exp((double)lg[k]);
+    base[k] = (float)b;
+    spec0[k] = (float)b;
+    base64[k] = b;
+    spec0_64[k] = b;
 }
 
-__global__ void adjoint_finish_kernel(int n, const double *__restrict__ g0, const float *__restrict__ base,
+__global__ void narrow_kernel(int n, const double *__restrict__ a, float *__restrict__ b) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) b[k] = (float)a[k];
+}
+
+__global__ void adjoint_finish_kernel(int n, const double *__restrict__ g0, const double *__restrict__ base,
                                       double *__restrict__ d_base, float *__restrict__ d_log) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double db = d_base[k] + g0[k];
     d_base[k] = db;
-    d_log[k] = (float)(db * (double)base[k]);
+    d_log[k] = (float)(db * base[k]);
 }
 
 
@@ -591,15 +605,16 @@ extern "C" int ss_brdf_lut(int res, int samples, float *lut, void *stream) {
     return SS_OK;
 }
 
-extern "C" int ss_env_rowsums(int he, int we, const double *khat, float *rowsum, double *work, void *stream) {
+extern "C" int ss_env_rowsums(int he, int we, const double *khat, double *rowsum, double *work, void *stream) {
     if (he < 2 || we < 2 || !rowsum || !work) return SS_ERR_INVALID;
-    return run_diffuse<0, float, float>(he, we, nullptr, nullptr, rowsum, work, khat, (cudaStream_t)stream);
+    return run_diffuse<0, float, double>(he, we, nullptr, nullptr, rowsum, work, khat, (cudaStream_t)stream);
 }
 
-extern "C" int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const float *val,
-                             const float *base, float *specular, void *stream);
+extern "C" int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col,
+                             const double *val, const double *base, double *specular, float *specular_f,
+                             void *stream);
 extern "C" int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row,
-                               const float *val, const double *d_specular, double *d_base, void *stream);
+                               const double *val, const double *d_specular, double *d_base, void *stream);
 
 extern "C" size_t ss_env_khat_words(int he, int we) {
     if (he < 2 || we < 2 || !spectral_ok(he, we)) return 0;
@@ -614,28 +629,36 @@ extern "C" int ss_env_khat(int he, int we, double *khat, void *stream) {
 }
 
 extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log, const SsEnvOps *ops,
-                              float *base, float *diffuse, float *specular, void *stream) {
+                              float *base, float *diffuse, float *specular, double *base64, double *diffuse64,
+                              double *specular64, void *stream) {
     if (he < 2 || we < 2 || levels < 1 || !base_log || !ops || !ops->rowsum || !ops->work || !base || !diffuse ||
-        !specular)
+        !specular || !base64 || !diffuse64 || !specular64)
         return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int T = he * we;
-    exp_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular);
+    exp_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular, base64, specular64);
     SS_CUDA_CHECK_LAUNCH();
     {
-        const int rc = run_diffuse<1, float, float>(he, we, base, ops->rowsum, diffuse, ops->work, ops->khat, st);
+        const int rc = run_diffuse<1, double, double>(he, we, base64, ops->rowsum, diffuse64, ops->work, ops->khat, st);
         if (rc != SS_OK) return rc;
+        narrow_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, diffuse64, diffuse);
+        SS_CUDA_CHECK_LAUNCH();
     }
     if (levels > 1) {
         if (ops->row_ptr && ops->col && ops->rval)
-            return ss_spec_apply(he, we, levels, ops->row_ptr, ops->col, ops->rval, base, specular, stream);
-        spec_refresh_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, base, specular);
+            return ss_spec_apply(he, we, levels, ops->row_ptr, ops->col, ops->rval, base64, specular64, specular,
+                                 stream);
+        spec_refresh_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, st>>>(he, we, levels, samples, base64,
+                                                                              specular64);
+        SS_CUDA_CHECK_LAUNCH();
+        narrow_kernel<<<(int)(((size_t)3 * T * (levels - 1) + 255) / 256), 256, 0, st>>>(
+            3 * T * (levels - 1), specular64 + (size_t)3 * T, specular + (size_t)3 * T);
         SS_CUDA_CHECK_LAUNCH();
     }
     return SS_OK;
 }
 
-extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const float *base, const SsEnvOps *ops,
+extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const double *base, const SsEnvOps *ops,
                               const double *d_diffuse, const double *d_specular, double *d_base, float *d_base_log,
                               void *stream) {
     if (he < 2 || we < 2 || levels < 1 || !base || !ops || !ops->rowsum || !ops->work || !d_diffuse || !d_specular ||
@@ -672,7 +695,7 @@ extern "C" int ss_spec_op_count(int he, int we, int levels, int samples, int32_t
 }
 
 extern "C" int ss_spec_op_fill(int he, int we, int levels, int samples, const int64_t *row_ptr, int32_t *col,
-                               float *val, void *stream) {
+                               double *val, void *stream) {
     if (he < 2 || we < 2 || levels < 2 || samples < 1 || !row_ptr || !col || !val) return SS_ERR_INVALID;
     const int T = he * we;
     spec_fill_kernel<<<dim3((T + 127) / 128, levels - 1), 128, 0, (cudaStream_t)stream>>>(he, we, levels, samples,
@@ -681,17 +704,19 @@ extern "C" int ss_spec_op_fill(int he, int we, int levels, int samples, const in
     return SS_OK;
 }
 
-extern "C" int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col, const float *val,
-                             const float *base, float *specular, void *stream) {
+extern "C" int ss_spec_apply(int he, int we, int levels, const int64_t *row_ptr, const int32_t *col,
+                             const double *val, const double *base, double *specular, float *specular_f,
+                             void *stream) {
     if (he < 2 || we < 2 || levels < 2 || !row_ptr || !col || !val || !base || !specular) return SS_ERR_INVALID;
     const int T = he * we, nrows = (levels - 1) * T;
-    spec_apply_kernel<<<(nrows + 7) / 8, 256, 0, (cudaStream_t)stream>>>(T, nrows, row_ptr, col, val, base, specular);
+    spec_apply_kernel<<<(nrows + 7) / 8, 256, 0, (cudaStream_t)stream>>>(T, nrows, row_ptr, col, val, base, specular,
+                                                                         specular_f);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
 
 extern "C" int ss_spec_apply_t(int he, int we, int levels, const int64_t *col_ptr, const int32_t *row,
-                               const float *val, const double *d_specular, double *d_base, void *stream) {
+                               const double *val, const double *d_specular, double *d_base, void *stream) {
     if (he < 2 || we < 2 || levels < 2 || !col_ptr || !row || !val || !d_specular || !d_base) return SS_ERR_INVALID;
     const int T = he * we;
     spec_apply_t_kernel<<<(T + 7) / 8, 256, 0, (cudaStream_t)stream>>>(T, levels, col_ptr, row, val, d_specular, d_base);

@@ -31,6 +31,7 @@ struct LossParams {
     double *gmu, *gx2, *gxy;     // SSIM adjoint maps
     double *sums;                // [0] sum |mx - my|, [1] sum of the SSIM map over the interior
     float *grad;                 // d loss / d x (pre-tone-map input)
+    double *grad64;              // nullable: the same in float64
 };
 
 __device__ __forceinline__ double srgb(double t) {
@@ -173,7 +174,9 @@ __global__ void __launch_bounds__(256) ssim_bwd_kernel(LossParams P) {
             const double d = a - b;
             const double g_l1 = (d > 0.0 ? inv_n : (d < 0.0 ? -inv_n : 0.0));
             const double g = (1.0 - P.lambda_ssim) * g_l1 + P.lambda_ssim * g_ssim;
-            P.grad[idx] = (float)tone_bwd((double)P.x[idx], P.mode, g);
+            const double gx = tone_bwd((double)P.x[idx], P.mode, g);
+            P.grad[idx] = (float)gx;
+            if (P.grad64) P.grad64[idx] = gx;
         }
         __syncthreads();
     }
@@ -184,7 +187,9 @@ __global__ void l1_grad_kernel(LossParams P, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double d = P.mx[i] - P.my[i];
         const double g = d > 0.0 ? inv_n : (d < 0.0 ? -inv_n : 0.0);
-        P.grad[i] = (float)tone_bwd((double)P.x[i], P.mode, (1.0 - P.lambda_ssim) * g);
+        const double gx = tone_bwd((double)P.x[i], P.mode, (1.0 - P.lambda_ssim) * g);
+        P.grad[i] = (float)gx;
+        if (P.grad64) P.grad64[i] = gx;
     }
 }
 
@@ -238,7 +243,8 @@ extern "C" size_t ss_photometric_workspace(int height, int width, int channels) 
 }
 
 extern "C" int ss_photometric_loss(int height, int width, int channels, const float *x, const float *y, int tone_mode,
-                                   double lambda_ssim, double *out, float *grad, double *workspace, void *stream)
+                                   double lambda_ssim, double *out, float *grad, double *grad64, double *workspace,
+                                   void *stream)
 {
     if (height <= 0 || width <= 0 || (channels != 1 && channels != 3) || tone_mode < -1 || tone_mode > 1)
         return SS_ERR_INVALID;
@@ -258,6 +264,7 @@ extern "C" int ss_photometric_loss(int height, int width, int channels, const fl
     P.mx = workspace; P.my = P.mx + n; P.gmu = P.my + n; P.gx2 = P.gmu + n; P.gxy = P.gx2 + n;
     P.sums = P.gxy + n;
     P.grad = grad;
+    P.grad64 = grad64;
     cudaMemsetAsync(P.sums, 0, 8 * sizeof(double), st);
     tone_l1_kernel<<<grid_for(n), 256, 0, st>>>(P, n);
     SS_CUDA_CHECK_LAUNCH();

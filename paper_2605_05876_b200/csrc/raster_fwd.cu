@@ -77,7 +77,10 @@ constexpr int kFwdWarps = SS_FWD_WARPS;
 // kCons (deferred training mode only): also the per-layer depth moments the
 // consolidation penalty needs, relative to the layer's first covering member
 // like the reference's pass 1 (raster_bwd.cu), parked in P.zst per layer.
-template <bool kExtras, bool kTrain, bool kCons = false>
+// kDeferred (deferred-loss training forward): float64 layer sums, stored
+// as float hi + lo parts (the coefficient kernel forms the layer mean colour
+// from them)
+template <bool kExtras, bool kTrain, bool kCons = false, bool kDeferred = false>
 __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 {
     __shared__ PackedScratch scratch[kFwdWarps];
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 #ifdef SS_FWD_F64_SUMS
     using AccT = typename std::conditional<kTrain, double, float>::type;
 #else
-    using AccT = float;
+    using AccT = typename std::conditional<kDeferred, double, float>::type;
 #endif
     AccT Wg = 0, C0 = 0, C1 = 0, C2 = 0;
     float Zg = 0.f, Z2g = 0.f, zmax = 0.f;
@@ -209,8 +212,15 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
             // once the image-space gradient is known): raw layer sums
             P.hdr[2 * pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
             const size_t HW = (size_t)P.W * P.H;
-            for (int m = 0; m < layers; ++m)
-                P.coef[(size_t)m * HW + pix] = make_float4((float)lw[m], (float)lc0[m], (float)lc1[m], (float)lc2[m]);
+            // the lo parts go to the third region of `coef` (after the float4
+            // planes and the A_lo planes)
+            float4 *raw_lo = reinterpret_cast<float4 *>(reinterpret_cast<float *>(P.coef) + (size_t)5 * P.k_max * HW);
+            for (int m = 0; m < layers; ++m) {
+                const float4 hi = make_float4((float)lw[m], (float)lc0[m], (float)lc1[m], (float)lc2[m]);
+                P.coef[(size_t)m * HW + pix] = hi;
+                raw_lo[(size_t)m * HW + pix] = make_float4((float)((double)lw[m] - hi.x), (float)((double)lc0[m] - hi.y),
+                                                           (float)((double)lc1[m] - hi.z), (float)((double)lc2[m] - hi.w));
+            }
             if (P.alpha) P.alpha[pix] = 1.f - T;
         } else {
             P.hdr[2 * pix] = make_int4(ncl | (layers << 8), __float_as_int(th0), __float_as_int(th1), __float_as_int(th2));
@@ -266,7 +276,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 // gradients g_rgb (and g_alpha) are known -- the suffix recursion of
 // backward.py:201-238 including the coverage term (g_alpha * prod(1 - a)).
 __global__ void __launch_bounds__(256) train_coef_kernel(int HW, int k_max, const int4 *__restrict__ hdr, float4 *coef,
-                                                         const float *__restrict__ g_rgb,
+                                                         const float *__restrict__ g_rgb, const double *__restrict__ g64,
                                                          const float *__restrict__ g_alpha, float bg0, float bg1,
                                                          float bg2)
 {
@@ -277,18 +287,27 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, int k_max, cons
     double a[SS_KMAX_CAP], tb[SS_KMAX_CAP];
     float4 raw[SS_KMAX_CAP];
     double tr = 1.0;
+    const float4 *raw_lo = reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(coef) + (size_t)5 * k_max * HW);
+    double rw_[SS_KMAX_CAP];
     for (int m = 0; m < layers; ++m) {
         raw[m] = coef[(size_t)m * HW + pix];
-        a[m] = -expm1(-(double)raw[m].x);
+        const float4 lo = raw_lo[(size_t)m * HW + pix];
+        rw_[m] = (double)raw[m].x + lo.x;
+        a[m] = -expm1(-rw_[m]);
         tb[m] = tr;
         tr *= 1.0 - a[m];
     }
-    const double gc0 = g_rgb[3 * (size_t)pix], gc1 = g_rgb[3 * (size_t)pix + 1], gc2 = g_rgb[3 * (size_t)pix + 2];
+    // the float64 image gradient when the loss kept it (ss_photometric_loss grad64)
+    const double gc0 = g64 ? g64[3 * (size_t)pix] : (double)g_rgb[3 * (size_t)pix];
+    const double gc1 = g64 ? g64[3 * (size_t)pix + 1] : (double)g_rgb[3 * (size_t)pix + 1];
+    const double gc2 = g64 ? g64[3 * (size_t)pix + 2] : (double)g_rgb[3 * (size_t)pix + 2];
     const double ga = g_alpha ? (double)g_alpha[pix] : 0.0;
     double sf0 = bg0, sf1 = bg1, sf2 = bg2, q = 1.0;
     for (int m = layers - 1; m >= 0; --m) {
-        const double inv = 1.0 / (double)raw[m].x;
-        const double ch0 = raw[m].y * inv, ch1 = raw[m].z * inv, ch2 = raw[m].w * inv;
+        const double inv = 1.0 / rw_[m];
+        const float4 hi = coef[(size_t)m * HW + pix], lo = raw_lo[(size_t)m * HW + pix];
+        const double ch0 = ((double)hi.y + lo.y) * inv, ch1 = ((double)hi.z + lo.z) * inv,
+                     ch2 = ((double)hi.w + lo.w) * inv;
         const double g_am = tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2) + ga * q);
         const double ta = tb[m] * a[m];
         const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
@@ -309,6 +328,7 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, int k_max, cons
 // the penalty value is block-reduced into cons_loss.
 __global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, int k_max, const int4 *__restrict__ hdr, float4 *coef,
                                                               float4 *zst, const float *__restrict__ g_rgb,
+                                                              const double *__restrict__ g64,
                                                               const float *__restrict__ g_alpha, float bg0,
                                                               float bg1, float bg2, double s, double *cons_loss)
 {
@@ -319,15 +339,18 @@ __global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, int k_max,
     if (layers > 0) {
         double a[SS_KMAX_CAP], tb[SS_KMAX_CAP], zb[SS_KMAX_CAP], vr[SS_KMAX_CAP];
         double gw_c[SS_KMAX_CAP], gz_c[SS_KMAX_CAP], gv_c[SS_KMAX_CAP], wm[SS_KMAX_CAP];
-        float4 raw[SS_KMAX_CAP];
+        const float4 *raw_lo = reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(coef) + (size_t)5 * k_max * HW);
+        double raw[SS_KMAX_CAP][4];  // float64 layer sums W, C (hi + lo)
         double tr = 1.0;
         for (int m = 0; m < layers; ++m) {
-            raw[m] = coef[(size_t)m * HW + pix];
+            const float4 hi = coef[(size_t)m * HW + pix], lo = raw_lo[(size_t)m * HW + pix];
+            raw[m][0] = (double)hi.x + lo.x; raw[m][1] = (double)hi.y + lo.y;
+            raw[m][2] = (double)hi.z + lo.z; raw[m][3] = (double)hi.w + lo.w;
             const float4 z = zst[(size_t)m * HW + pix];
-            a[m] = -expm1(-(double)raw[m].x);
+            a[m] = -expm1(-raw[m][0]);
             tb[m] = tr;
             tr *= 1.0 - a[m];
-            const double inv = 1.0 / (double)raw[m].x;
+            const double inv = 1.0 / raw[m][0];
             const double mz = (double)z.y * inv;
             zb[m] = (double)z.x + mz;
             vr[m] = (double)z.z * inv - mz * mz;
@@ -352,12 +375,15 @@ __global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, int k_max,
             }
         }
         cons_pix = s * l_pix;
-        const double gc0 = g_rgb[3 * (size_t)pix], gc1 = g_rgb[3 * (size_t)pix + 1], gc2 = g_rgb[3 * (size_t)pix + 2];
+        // the float64 image gradient when the loss kept it (ss_photometric_loss grad64)
+        const double gc0 = g64 ? g64[3 * (size_t)pix] : (double)g_rgb[3 * (size_t)pix];
+        const double gc1 = g64 ? g64[3 * (size_t)pix + 1] : (double)g_rgb[3 * (size_t)pix + 1];
+        const double gc2 = g64 ? g64[3 * (size_t)pix + 2] : (double)g_rgb[3 * (size_t)pix + 2];
         const double ga = g_alpha ? (double)g_alpha[pix] : 0.0;
         double sf0 = bg0, sf1 = bg1, sf2 = bg2, q = 1.0, rw = 0.0;
         for (int m = layers - 1; m >= 0; --m) {
-            const double inv = 1.0 / (double)raw[m].x;
-            const double ch0 = raw[m].y * inv, ch1 = raw[m].z * inv, ch2 = raw[m].w * inv;
+            const double inv = 1.0 / raw[m][0];
+            const double ch0 = raw[m][1] * inv, ch1 = raw[m][2] * inv, ch2 = raw[m][3] * inv;
             const double g_am =
                 tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2) + ga * q + gw_c[m] - rw);
             const double ta = tb[m] * a[m];
@@ -384,11 +410,11 @@ __global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, int k_max,
     }
 }
 
-template <bool kExtras, bool kTrain, bool kCons = false>
+template <bool kExtras, bool kTrain, bool kCons = false, bool kDeferred = false>
 void launch(const FwdParams &P, int ntiles, int threads, cudaStream_t st) {
     const int wpc = threads / 32 < kFwdWarps ? threads / 32 : kFwdWarps;  // tile 8: 2 warps
     const int ctas_per_tile = threads / (32 * wpc);
-    raster_fwd_kernel<kExtras, kTrain, kCons><<<ntiles * ctas_per_tile, 32 * wpc, 0, st>>>(P);
+    raster_fwd_kernel<kExtras, kTrain, kCons, kDeferred><<<ntiles * ctas_per_tile, 32 * wpc, 0, st>>>(P);
 }
 
 bool fill_common(FwdParams &P, int width, int height, int tile, const int32_t *tile_offsets,
@@ -449,7 +475,8 @@ static int train_forward(int width, int height, int tile, const int32_t *tile_of
     P.rgb = rgb;
     P.zst = reinterpret_cast<float4 *>(zstats);
     const int ntiles = P.ntx * ((height + tile - 1) / tile);
-    if (zstats) launch<false, true, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
+    if (zstats) launch<false, true, true, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
+    else if (!target) launch<false, true, false, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
     else launch<false, true>(P, ntiles, tile * tile, (cudaStream_t)stream);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
@@ -475,21 +502,22 @@ extern "C" int ss_train_forward_zstats(int width, int height, int tile, const in
 }
 
 extern "C" int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef,
-                              const float *g_rgb, const float *g_alpha, const float *background, void *stream)
+                              const float *g_rgb, const double *g_rgb64, const float *g_alpha,
+                              const float *background, void *stream)
 {
     if (width <= 0 || height <= 0 || k_max < 1 || k_max > SS_KMAX_CAP || !pix_hdr || !coef || !g_rgb || !background)
         return SS_ERR_INVALID;
     const int HW = width * height;
     train_coef_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-        HW, k_max, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef), g_rgb, g_alpha, background[0],
-        background[1], background[2]);
+        HW, k_max, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef), g_rgb, g_rgb64, g_alpha,
+        background[0], background[1], background[2]);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
 
 extern "C" int ss_train_coefs_cons(int width, int height, int k_max, const int32_t *pix_hdr, float *coef,
-                                   float *zstats, const float *g_rgb, const float *g_alpha, const float *background,
-                                   double cons_scale, double *cons_loss, void *stream)
+                                   float *zstats, const float *g_rgb, const double *g_rgb64, const float *g_alpha,
+                                   const float *background, double cons_scale, double *cons_loss, void *stream)
 {
     if (width <= 0 || height <= 0 || k_max < 1 || k_max > SS_KMAX_CAP || !pix_hdr || !coef || !zstats || !g_rgb ||
         !background || !cons_loss || !(cons_scale >= 0.0))
@@ -497,8 +525,8 @@ extern "C" int ss_train_coefs_cons(int width, int height, int k_max, const int32
     const int HW = width * height;
     train_coef_cons_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
         HW, k_max, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef),
-        reinterpret_cast<float4 *>(zstats), g_rgb, g_alpha, background[0], background[1], background[2], cons_scale,
-        cons_loss);
+        reinterpret_cast<float4 *>(zstats), g_rgb, g_rgb64, g_alpha, background[0], background[1], background[2],
+        cons_scale, cons_loss);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

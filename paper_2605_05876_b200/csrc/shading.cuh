@@ -77,8 +77,8 @@ __device__ __forceinline__ SsBil<R> ss_bil_prepare(int h, int w, R fu, R fv, boo
     return b;
 }
 
-template <int C, typename R>
-__device__ __forceinline__ void ss_bil_lookup(const float *__restrict__ tex, int w, const SsBil<R> &b, R *out) {
+template <int C, typename R, typename T = float>
+__device__ __forceinline__ void ss_bil_lookup(const T *__restrict__ tex, int w, const SsBil<R> &b, R *out) {
     const R tu = b.tu, tv = b.tv;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -253,7 +253,10 @@ __device__ __forceinline__ void ss_shade_forward(const ShadeIn<R> &in, const SsE
     s.bd = ss_bil_prepare<R>(he, we, fu, fv, true);
     const float4 *d4 = reinterpret_cast<const float4 *>(env.diffuse4);
     const float4 *s4 = reinterpret_cast<const float4 *>(env.specular4);
-    if (d4) ss_bil_lookup4(d4, we, s.bd, s.l_d);
+    // float64 shading reads the float64 maps (the reference's, shading.py:369-379)
+    const bool m64 = sizeof(R) == 8 && env.diffuse64 && env.specular64;
+    if (m64) ss_bil_lookup<3>(env.diffuse64, we, s.bd, s.l_d);
+    else if (d4) ss_bil_lookup4(d4, we, s.bd, s.l_d);
     else ss_bil_lookup<3>(env.diffuse, we, s.bd, s.l_d);
     R lvl = ss_clip<R>(in.r, R(0.0), R(1.0)) * (L - 1);
     int cap = L - 2 > 0 ? L - 2 : 0;
@@ -264,7 +267,10 @@ __device__ __forceinline__ void ss_shade_forward(const ShadeIn<R> &in, const SsE
     ss_dir_coords(s.refl, he, we, fu, fv);
     s.bs = ss_bil_prepare<R>(he, we, fu, fv, true);
     const size_t lstride = (size_t)he * we * 3;
-    if (s4) {
+    if (m64) {
+        ss_bil_lookup<3>(env.specular64 + lstride * s.lvl0, we, s.bs, s.spec_lo);
+        ss_bil_lookup<3>(env.specular64 + lstride * s.lvl1, we, s.bs, s.spec_hi);
+    } else if (s4) {
         ss_bil_lookup4(s4 + (size_t)he * we * s.lvl0, we, s.bs, s.spec_lo);
         ss_bil_lookup4(s4 + (size_t)he * we * s.lvl1, we, s.bs, s.spec_hi);
     } else {

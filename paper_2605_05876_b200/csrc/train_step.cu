@@ -89,9 +89,15 @@ __device__ __forceinline__ float fast_rcp(float x) {
 
 // (cx, cy): the record's projected centre (t1.z / t4.z, t2.z / t4.z), the
 // origin of the x and y moments.
+#ifdef SS_SPLAT_ACC_F64
+typedef double SplatAcc;  // experiment: float64 per-lane channel sums
+#else
+typedef float SplatAcc;
+#endif
+
 template <bool kCons>
 __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R, int ix, int iy, float x, float y,
-                                         float cx, float cy, float *g) {
+                                         float cx, float cy, SplatAcc *g) {
     const size_t HW = (size_t)P.W * P.H;
     const size_t pix = (size_t)iy * P.W + ix;
     // the packed header and the (most common) layer-0 coefficients are loaded
@@ -105,10 +111,21 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     // a systematic bias of the record's gradient
     const float k0 = fs(fm(x, R.b.z), R.a.x), k1 = fs(fm(x, R.b.w), R.a.y), k2 = fs(fm(x, R.c.x), R.a.z);
     const float l0 = fs(fm(y, R.b.z), R.a.w), l1 = fs(fm(y, R.b.w), R.b.x), l2 = fs(fm(y, R.c.x), R.b.y);
+#ifdef SS_ITEM_DIV
+    const float den_ = fs(fm(k0, l1), fm(k1, l0));
+    const float inv_den = fc_rcp(den_);
+    const float u = fd(fs(fm(k1, l2), fm(k2, l1)), den_);
+    const float v = fd(fs(fm(k2, l0), fm(k0, l2)), den_);
+#else
     const float inv_den = fc_rcp(fs(fm(k0, l1), fm(k1, l0)));
     const float u = fs(fm(k1, l2), fm(k2, l1)) * inv_den;
     const float v = fs(fm(k2, l0), fm(k0, l2)) * inv_den;
+#endif
+#ifdef SS_ITEM_RHO64
+    const double rho2 = ss_rho2(R.c.y, R.c.z, R.c.w, u, v);
+#else
     const float rho2 = (R.c.y * u * u + 2.f * R.c.z * u * v) + R.c.w * v * v;
+#endif
     const float zs = R.d.z;
     const int nc = h.x & 0xff;  // closed layers (the layer count sits in bits 8+)
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
@@ -126,23 +143,30 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     }
     if (m >= P.k_max) return 0;  // beyond the K_MAX stop: discarded
     const float4 cf = m == 0 ? cf0 : __ldg(P.coef + m * HW + pix);
+#if defined(SS_ITEM_RHO64)
+    const double e = exp(-0.5 * rho2);
+    const double w = (double)R.d.x * e;
+#elif defined(SS_EXP_EXPF)
+    const float e = expf(-0.5f * rho2);
+    const float w = R.d.x * e;
+#else
     float e;  // exp(-rho^2 / 2) by the hardware ex2 (ftz: no range fix-up)
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(rho2 * -0.72134752044448170368f));
     const float w = R.d.x * e;
+#endif
     // g_w = A + sum_c G_c colour_c: a small difference of large terms when
     // the record's colour is near its layer's mean colour (raster_fwd.cu
-    // store_coef) -- float64, exact products of the float factors
-    // float32 here (measured: no gradient entry of configs 0-3 moves out of
-    // tolerance); the big records evaluate it in float64 with the A_lo plane
-    // (item_grad_ref), where a grazing splat's cancellation needs it
-    float gw = cf.x + cf.y * R.e.x + cf.z * R.e.y + cf.w * R.e.z;
+    // store_coef) -- float64, exact products of the float factors, A_lo
+    const float G0 = cf.y, G1 = cf.z, G2 = cf.w;
+    float gw = (float)(((double)cf.x + (double)__ldg(P.coef_lo + m * HW + pix)) +
+                       (((double)cf.y * R.e.x + (double)cf.z * R.e.y) + (double)cf.w * R.e.z));
     if constexpr (kCons) {  // consolidation penalty (backward.py:272-286, centred depth form)
         const float4 zq = __ldg(P.zc + m * HW + pix);
         const float dz = R.d.y - zq.z;
         gw += zq.x * dz + zq.y * (dz * dz - zq.w);
         g[17] += w * (zq.x + 2.f * zq.y * dz);
     }
-    g[13] += w * cf.y; g[14] += w * cf.z; g[15] += w * cf.w;
+    g[13] += w * G0; g[14] += w * G1; g[15] += w * G2;
     const float gr = -0.5f * w * gw;
     g[12] += e * gw;
     g[9] += gr * u * u; g[10] += gr * 2.f * u * v; g[11] += gr * v * v;
@@ -469,7 +493,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
         FastCov f;
         fast_cov_setup(R.a, R.b, R.c, R.e.w, f);
         const float cx = valid ? fd(R.a.z, R.c.x) : 0.f, cy = valid ? fd(R.b.y, R.c.x) : 0.f;
-        float g[NC];
+        SplatAcc g[NC];
 #pragma unroll
         for (int k = 0; k < NC; ++k) g[k] = 0.f;
         int touch = 0;
@@ -511,7 +535,7 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
             // channels held by two lanes carry identical sums
             float *dst = P.acc + (size_t)__ldg(order + e) * SS_ACC_FLOATS;
 #pragma unroll
-            for (int i = 0; i < 3; ++i) dst[acc_slot(ch[i])] = g[i];
+            for (int i = 0; i < 3; ++i) dst[acc_slot(ch[i])] = (float)g[i];
             if (gl == 0) reinterpret_cast<int *>(dst)[18] = touch;
             if (!kCons && gl == 1) dst[16] = 0.f;
             if (gl == 2) dst[19] = SS_ACC_MOMENTS;

@@ -39,15 +39,16 @@ class ImageLoss:
         self.ws = torch.empty((nbytes + 7) // 8, device=device, dtype=torch.float64)
         self.out = torch.zeros(3, device=device, dtype=torch.float64)  # loss, L1, 1 - SSIM
 
-    def __call__(self, x, y, grad, lambda_ssim=0.2, tone=None):
-        """Launch on the current stream; returns the device `out` tensor."""
+    def __call__(self, x, y, grad, lambda_ssim=0.2, tone=None, grad64=None):
+        """Launch on the current stream; returns the device `out` tensor.
+        grad64 (optional): the gradient in float64 as well."""
         mode = -1 if tone is None else TONE_MODES[tone]
         if not 0.0 <= lambda_ssim <= 1.0:
             raise ValueError("lambda_ssim must lie in [0, 1]")
         h, w, c = self.shape
         _lib.check(self.lib.ss_photometric_loss(h, w, c, _lib.ptr(x), _lib.ptr(y), mode, float(lambda_ssim),
-                                                _lib.ptr(self.out), _lib.ptr(grad), _lib.ptr(self.ws),
-                                                _lib.stream_ptr()), "ss_photometric_loss")
+                                                _lib.ptr(self.out), _lib.ptr(grad), _lib.ptr(grad64),
+                                                _lib.ptr(self.ws), _lib.stream_ptr()), "ss_photometric_loss")
         return self.out
 
 

@@ -56,7 +56,7 @@ class EnvOps:
         if nk:
             self.khat = torch.empty(nk, device=dev, dtype=torch.float64)
             _lib.check(lib.ss_env_khat(he, we, _lib.ptr(self.khat), s), "ss_env_khat")
-        self.rowsum = torch.empty(T, device=dev, dtype=torch.float32)
+        self.rowsum = torch.empty(T, device=dev, dtype=torch.float64)
         _lib.check(lib.ss_env_rowsums(he, we, _lib.ptr(self.khat), _lib.ptr(self.rowsum), _lib.ptr(self.work), s),
                    "ss_env_rowsums")
         self.spec = None
@@ -68,7 +68,7 @@ class EnvOps:
             row_ptr[1:] = torch.cumsum(nnz.to(torch.int64), 0)
             total = int(row_ptr[-1].item())
             col = torch.empty(total, device=dev, dtype=torch.int32)
-            rval = torch.empty(total, device=dev, dtype=torch.float32)
+            rval = torch.empty(total, device=dev, dtype=torch.float64)
             _lib.check(lib.ss_spec_op_fill(he, we, levels, samples, _lib.ptr(row_ptr), _lib.ptr(col), _lib.ptr(rval),
                                            s), "ss_spec_op_fill")
             rows = torch.repeat_interleave(torch.arange(nrows, device=dev, dtype=torch.int64), nnz.to(torch.int64))
@@ -114,6 +114,10 @@ class EnvironmentLight:
         # 16-byte texels for the shading kernels' bilinear fetches
         self.diffuse4 = torch.zeros((he, we, 4), device="cuda", dtype=torch.float32)
         self.specular4 = torch.zeros((self.levels, he, we, 4), device="cuda", dtype=torch.float32)
+        # the float64 maps (the reference's precision), read by the float64 shading
+        self.base64 = torch.empty((he, we, 3), device="cuda", dtype=torch.float64)
+        self.diffuse64 = torch.empty((he, we, 3), device="cuda", dtype=torch.float64)
+        self.specular64 = torch.empty((self.levels, he, we, 3), device="cuda", dtype=torch.float64)
         self.refresh()
 
     @property
@@ -135,6 +139,7 @@ class EnvironmentLight:
         ops = env_ops(he, we, self.levels, self.spec_samples)
         _lib.check(lib.ss_env_refresh(he, we, self.levels, self.spec_samples, _lib.ptr(self.base_log), ops.ref(),
                                       _lib.ptr(self.base), _lib.ptr(self.diffuse), _lib.ptr(self.specular),
+                                      _lib.ptr(self.base64), _lib.ptr(self.diffuse64), _lib.ptr(self.specular64),
                                       _lib.stream_ptr()), "ss_env_refresh")
         self.diffuse4[..., :3].copy_(self.diffuse)
         self.specular4[..., :3].copy_(self.specular)
@@ -151,7 +156,7 @@ class EnvironmentLight:
         d_base = torch.empty(self.base.shape, **f64)
         d_log = torch.empty_like(self.base)
         ops = env_ops(he, we, self.levels, self.spec_samples)
-        _lib.check(lib.ss_env_adjoint(he, we, self.levels, self.spec_samples, _lib.ptr(self.base), ops.ref(),
+        _lib.check(lib.ss_env_adjoint(he, we, self.levels, self.spec_samples, _lib.ptr(self.base64), ops.ref(),
                                       _lib.ptr(dd), _lib.ptr(ds), _lib.ptr(d_base), _lib.ptr(d_log),
                                       _lib.stream_ptr()), "ss_env_adjoint")
         return d_base, d_log

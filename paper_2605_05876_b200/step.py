@@ -124,8 +124,8 @@ class ViewBuffers:
         self.offsets = torch.empty(ntiles + 1, **i32)
         self.cursors = torch.empty(ntiles, **i32)
         self.tile_order = torch.empty(ntiles, **i32)
-        # per layer and pixel: float4 (A hi, dL/dC_raw), then a float plane of A lo (ss_abi.h)
-        self.coef = torch.empty(5 * k_max * H * W, **f32)
+        # per layer and pixel: float4 (A hi, dL/dC_raw), a float plane of A lo, a float4 plane of raw-sum lo (ss_abi.h)
+        self.coef = torch.empty(9 * k_max * H * W, **f32)
         self.thr = torch.empty((k_max, H * W), **f32)
         self.pix_hdr = torch.empty((H * W, 8), **i32)
         # NDC tables, counters, area-class sort and big-rect queue of the backward
@@ -154,6 +154,9 @@ class ViewBuffers:
         f32 = dict(device=device, dtype=torch.float32)
         self.rgb = torch.empty((H, W, 3), **f32)
         self.g_rgb = torch.empty((H, W, 3), **f32)
+        # the image gradient in float64 as well: the layer coefficients'
+        # colour terms cancel, and a float32-rounded gradient biases them
+        self.g_rgb64 = torch.empty((H, W, 3), device=device, dtype=torch.float64)
         self.alpha = torch.empty((H, W), **f32)
         self.g_alpha = torch.empty((H, W), **f32)
         self.sil = torch.zeros(1, device=device, dtype=torch.float64)
@@ -232,7 +235,7 @@ class TrainStep:
         if pair_capacity:
             self._alloc_pairs(pair_capacity)
         self.collect_stats = False
-        self.captured_rgb = None       # a list -> the fused forward's image of every view is appended (L1 mode)
+        self.captured_rgb = None       # a list -> the forward's image of every view is appended
         # forward colours: float64 IBL shading like render() (the step's image
         # is then bit-identical to the API path's and within 1e-4 of the
         # oracle); SS_COLOR_IBL_F32 is the float32 variant (colours within
@@ -385,7 +388,9 @@ class TrainStep:
                                                 None, _lib.ptr(b.coef), _lib.ptr(b.thr), _lib.ptr(b.pix_hdr), None,
                                                 _lib.ptr(b.rgb), _lib.ptr(b.alpha), _lib.ptr(b.tile_order), s),
                            "ss_train_forward")
-            out = b.imgloss(b.rgb, target, b.g_rgb, self.lambda_ssim, self.tone)
+            if self.captured_rgb is not None:
+                self.captured_rgb.append(b.rgb.clone())
+            out = b.imgloss(b.rgb, target, b.g_rgb, self.lambda_ssim, self.tone, grad64=b.g_rgb64)
             b.loss_part += out[0:1]
             g_alpha = None
             if mask is not None and self.lambda_sil > 0.0:
@@ -396,11 +401,13 @@ class TrainStep:
                 g_alpha = b.g_alpha
             if cons:
                 _lib.check(lib.ss_train_coefs_cons(self.W, self.H, self.k_max, _lib.ptr(b.pix_hdr), _lib.ptr(b.coef),
-                                                   _lib.ptr(b.zst), _lib.ptr(b.g_rgb), _lib.ptr(g_alpha), self._bg[0],
+                                                   _lib.ptr(b.zst), _lib.ptr(b.g_rgb), _lib.ptr(b.g_rgb64),
+                                                   _lib.ptr(g_alpha), self._bg[0],
                                                    self.cons_scale, _lib.ptr(b.loss_part), s), "ss_train_coefs_cons")
             else:
                 _lib.check(lib.ss_train_coefs(self.W, self.H, self.k_max, _lib.ptr(b.pix_hdr), _lib.ptr(b.coef),
-                                              _lib.ptr(b.g_rgb), _lib.ptr(g_alpha), self._bg[0], s), "ss_train_coefs")
+                                              _lib.ptr(b.g_rgb), _lib.ptr(b.g_rgb64), _lib.ptr(g_alpha), self._bg[0],
+                                              s), "ss_train_coefs")
         self._ev_end(ev)
         if target_done is not None:
             target_done.record()
@@ -550,7 +557,7 @@ class TrainStep:
         he, we = self.env.shape
         from .shading import env_ops
         ops = env_ops(he, we, self.env.levels, self.env.spec_samples)
-        _lib.check(self.lib.ss_env_adjoint(he, we, self.env.levels, self.env.spec_samples, _lib.ptr(self.env.base),
+        _lib.check(self.lib.ss_env_adjoint(he, we, self.env.levels, self.env.spec_samples, _lib.ptr(self.env.base64),
                                            ops.ref(), _lib.ptr(self.d_diffuse),
                                            _lib.ptr(self.d_spec), _lib.ptr(self.d_base), _lib.ptr(self.g_env_log),
                                            _lib.stream_ptr()), "ss_env_adjoint")

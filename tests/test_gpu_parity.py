@@ -208,9 +208,17 @@ def test_diffuse_quadrature_spectral_and_nbody(shape):
     solid = (np.sin(tt) * (np.pi / he) * (2.0 * np.pi / we)).reshape(-1)
     D = np.maximum(dirs @ dirs.T, 0.0) * solid[None, :]
     D /= D.sum(axis=1, keepdims=True)
-    base = host(env.base).astype(np.float64).reshape(-1, 3)
+    base = host(env.base64).reshape(-1, 3)
+    # device exp vs libm exp: within an ulp or two
+    np.testing.assert_allclose(host(env.base64), np.exp(np.asarray(base_log, np.float32).astype(np.float64)),
+                               rtol=1e-15, atol=0)
     bad, err = image_close(env.diffuse, (D @ base).reshape(he, we, 3), rel=1e-5, abs_=1e-7)
     assert bad == 0, err
+    # the float64 maps the float64 shading reads: the dense product's precision
+    # for the spectral form (even widths); the N-body form (odd widths) sums
+    # float32 products in float64 chunks
+    rtol = 1e-12 if we % 2 == 0 else 1e-6
+    np.testing.assert_allclose(host(env.diffuse64), (D @ base).reshape(he, we, 3), rtol=rtol, atol=rtol * 1e-2)
     g = rng.normal(0.0, 1.0, (he, we, 3))
     db, _ = env.env_gradient(g, np.zeros((1, he, we, 3)))
     ref = (D.T @ g.reshape(-1, 3)).reshape(he, we, 3)

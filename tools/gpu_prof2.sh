@@ -8,6 +8,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --nvtx-include "ss_step/" --csv --log-file gpurun_out/launches_$TAG.csv python tools/profile_step.py > /dev/null 2>&1
 echo "launch rc=$?"
 NVIEWS=2 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "ss_step/" \
-    -k regex:"splat_bwd|raster_fwd|chain_kernel|preprocess_kernel|tile_sort|scatter_kernel|big_bwd" -c 7 \
+    -k regex:"splat_bwd|raster_fwd|chain_kernel|preprocess_kernel|tile_sort|^scatter_kernel|big_bwd" -c 8 \
     -o gpurun_out/prof_$TAG -f python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"

@@ -142,7 +142,8 @@ def record_probe():
     env = ss.EnvironmentLight(base_log)
     target = ss.render(ss.SurfelCloud(**gt), cam, ss.RenderOptions(), env=env).rgb.contiguous()
     cloud = ss.SurfelCloud(**opt)
-    ts = TrainStep(cloud, env, R, R, streams=1)
+    photo = "--photometric" in sys.argv
+    ts = TrainStep(cloud, env, R, R, streams=1, loss="photometric" if photo else "l1")
     ts.captured_rgb = []
     ts.gradients([cam], [target])
     acc = ts.bufs[0].acc.cpu().numpy()
@@ -151,20 +152,46 @@ def record_probe():
     co = SimpleNamespace(**opt)
     ores = O.render(co, cam, env=oenv)
     rgb = ts.captured_rgb[-1].cpu().numpy().astype(np.float64)
-    g = np.sign(rgb - target.cpu().numpy()) / rgb.size
+    if photo:
+        tg = target.cpu().numpy().astype(np.float64)
+        _, gm = O.photometric_loss(O.tone_map(rgb, "hdr-loss"), O.tone_map(tg, "hdr-loss"), 0.2)
+        g = O.tone_map_backward(rgb, "hdr-loss", gm)
+        probe = tuple(int(a) for a in sys.argv[sys.argv.index("--photometric") + 1].split(","))
+        g64 = ts.bufs[0].g_rgb64.cpu().numpy()
+        d = np.abs(g64 - g)
+        print("image gradient: max |g64 - oracle|", d.max(), "max |oracle|", np.abs(g).max(),
+              "max rel", (d / np.maximum(np.abs(g), 1e-300)).max())
+    else:
+        g = np.sign(rgb - target.cpu().numpy()) / rgb.size
     og = O.backward_image(co, ores, g, None, 0.0, env=oenv, return_records=True)
     src = ores.proj["source_index"]
     pos = {int(s): k for k, s in enumerate(src)}
     np.set_printoptions(precision=9, linewidth=200)
     for i in probe:
         k = pos[i]
-        a = acc[i].copy()
-        if a[19] == 1.0:
+        a = acc[i].astype(np.float64)
+        if a[19] == 2.0:  # big record: float64 rows in acc64 (T-row layout)
+            r = ts.bufs[0].acc64[int(acc[i][0].view(np.int32))].cpu().numpy()
+            a[0:17] = r[0:17]
+            print("   (big record, float64 rows; gz", r[17], ")")
+        elif a[19] == 1.0:
             a[0:9] = _moments_to_rows(a, recs[i])
-        print(i, "layout", a[19], "touch", a[18].view(np.int32) if a.dtype == np.float32 else a[18],
+        print(i, "layout", a[19], "touch", acc[i][18].view(np.int32),
               "oracle touch", og["touch_rec"][k])
         print("   ours  ", a[:17], "ss", a[17])
         print("   oracle", og["records"][k], "ss", og["ss_rec"][k])
+        o = np.asarray(og["records"][k], np.float64)
+        print("   rel   ", np.abs(a[:17] - o) / np.maximum(np.abs(o), 1e-30))
+        rr = recs[i]
+        pj = ores.proj
+        ours = {"t1": rr[0:3], "t2": rr[3:6], "t4": rr[6:9], "sinv": rr[9:12], "n_f": rr[12:13], "view_z": rr[13:14],
+                "z_start": rr[14:15], "z_end": rr[15:16], "color": rr[16:19], "rect": rr[20:24].view(np.int32)}
+        for key, val in ours.items():
+            if key == "color":
+                ref = np.asarray(ores.colors)[i] if hasattr(ores, "colors") else None
+            else:
+                ref = np.asarray(pj[key])[k] if key in pj else None
+            print("   ", key, val, "oracle", ref)
 
 
 if __name__ == "__main__" and "--records" in sys.argv:
