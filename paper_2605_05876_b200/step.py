@@ -224,6 +224,12 @@ class TrainStep:
         self.loss = torch.zeros(1, device=dev, dtype=torch.float64)
         self.d_diffuse = torch.zeros(env.base.shape, device=dev, dtype=torch.float64)
         self.d_spec = torch.zeros(env.specular.shape, device=dev, dtype=torch.float64)
+        # each buffer set folds its views' derived-map sums into its own
+        # float64 maps (no ordering between the worker streams); the sets are
+        # summed once per step (the first set's maps are the step's own)
+        for k, b in enumerate(self.bufs):
+            b.d_diffuse64 = self.d_diffuse if k == 0 else torch.zeros_like(self.d_diffuse)
+            b.d_spec64 = self.d_spec if k == 0 else torch.zeros_like(self.d_spec)
         self.d_base = torch.empty(env.base.shape, device=dev, dtype=torch.float64)
         self.adam = Adam()
         self._po = make_opts(self.opts, tile)
@@ -275,7 +281,7 @@ class TrainStep:
         self._cl = _lib.make_cloud(cloud)
         for b in self.bufs:
             b.gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
-                                None, _lib.ptr(self.d_diffuse), _lib.ptr(self.d_spec),
+                                None, _lib.ptr(b.d_diffuse64), _lib.ptr(b.d_spec64),
                                 _lib.ptr(b.d_diff4), _lib.ptr(b.d_spec4), _lib.ptr(self.view_count))
 
     def refine(self, stats, mean_neighbor_dist, max_surfels, quantile=0.9, grad_floor=1e-8,
@@ -340,13 +346,10 @@ class TrainStep:
         _lib.check(rc, "ss_preprocess")
         return camst
 
-    def view(self, cam, target, b=None, chain_after=None, target_done=None, mask=None):
+    def view(self, cam, target, b=None, target_done=None, mask=None):
         """Forward + backward of one view on the CURRENT stream with buffer set
-        b; gradients accumulate into self.grads.  chain_after: event the
-        derived-map merge must wait for (the previous view's merge, which
-        updates the same float64 maps); target_done: event recorded once
-        `target` is consumed.  Returns the event recorded after this view's
-        merge."""
+        b; gradients accumulate into self.grads and b's derived-map sums.
+        target_done: event recorded once `target` is consumed."""
         lib = self.lib
         b = b if b is not None else self.bufs[0]
         s = _lib.stream_ptr()
@@ -434,32 +437,26 @@ class TrainStep:
                                          _lib.ptr(b.cells) if self.color_source == _lib.SS_COLOR_IBL else None,
                                          ctypes.byref(b.gs), s),
                    "ss_chain_backward")
-        # fold this view's float32 derived-map sums into the step's float64
-        # ones: plain read-modify-write, so the merges are serialised
-        if chain_after is not None:
-            torch.cuda.current_stream().wait_event(chain_after)
-        _lib.check(lib.ss_env_grad_merge(b.d_diff4.numel() // 4, _lib.ptr(b.d_diff4), _lib.ptr(self.d_diffuse), s),
+        # fold this view's float32 derived-map sums into the buffer set's
+        # float64 ones (same stream: no ordering with the other sets)
+        _lib.check(lib.ss_env_grad_merge(b.d_diff4.numel() // 4, _lib.ptr(b.d_diff4), _lib.ptr(b.d_diffuse64), s),
                    "ss_env_grad_merge")
-        _lib.check(lib.ss_env_grad_merge(b.d_spec4.numel() // 4, _lib.ptr(b.d_spec4), _lib.ptr(self.d_spec), s),
+        _lib.check(lib.ss_env_grad_merge(b.d_spec4.numel() // 4, _lib.ptr(b.d_spec4), _lib.ptr(b.d_spec64), s),
                    "ss_env_grad_merge")
         self._ev_end(ev)
-        done = torch.cuda.Event()
-        done.record()
-        return done
 
     def _run_views(self, cameras, targets_for, target_done=None, masks=None):
         """Issue every view, alternating the worker streams (view i uses stream
-        and buffers i % S); the chain kernels are serialised by events."""
+        and buffers i % S); the streams are independent until the join."""
         main = torch.cuda.current_stream()
         for st in self.streams:
             st.wait_stream(main)
-        prev = None
         nst = min(len(self.streams), self.active_streams or len(self.streams))
         for i, cam in enumerate(cameras):
             k = i % nst
             with torch.cuda.stream(self.streams[k]):
                 tgt = targets_for(i, self.streams[k])
-                prev = self.view(cam, tgt, self.bufs[k], chain_after=prev,
+                self.view(cam, tgt, self.bufs[k],
                                  target_done=None if target_done is None else target_done[i % len(target_done)],
                                  mask=None if masks is None else masks[i])
                 if self.collect_stats:
@@ -468,6 +465,11 @@ class TrainStep:
                     self._kept.append(int((b.cull == 0).sum().item()))
         for st in self.streams:
             main.wait_stream(st)
+        for b in self.bufs[1:nst]:  # the other sets' derived-map sums into the step's
+            self.d_diffuse.add_(b.d_diffuse64)
+            self.d_spec.add_(b.d_spec64)
+            b.d_diffuse64.zero_()
+            b.d_spec64.zero_()
 
     def _ev_begin(self, name):
         if self.kernel_events is None:
@@ -498,8 +500,9 @@ class TrainStep:
 
     def zero(self):
         self.flat.zero_()
-        self.d_diffuse.zero_()
-        self.d_spec.zero_()
+        for b in self.bufs:
+            b.d_diffuse64.zero_()
+            b.d_spec64.zero_()
         self.loss.zero_()
         for b in self.bufs:
             b.loss_part.zero_()
