@@ -179,6 +179,57 @@ def cpu_oracle_view(n=N_SURFELS, env_shape=(64, 128), seed=0):
                                  f"env reduced to {env_shape[0]}x{env_shape[1]} (BASELINE.md)")
 
 
+def env_cpu_timings(shapes=((16, 32), (64, 128)), seed=0):
+    """the environment refresh (prefilter) and env_gradient
+    (its adjoint) on the CPU oracle at 16x32 and 64x128 (best of 3 / 1)."""
+    from oracle import oracle as O
+    from paper_2605_05876_b200 import scenes
+    out = {}
+    for he, we in shapes:
+        env = O.EnvOracle(np.log(scenes.env_lognormal(he, we, seed)))
+        rng = np.random.default_rng(seed)
+        dd, ds = rng.normal(size=(he, we, 3)), rng.normal(size=(env.levels, he, we, 3))
+        reps = 3 if he * we <= 4096 else 1
+        tr, tg = [], []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            env.refresh()
+            tr.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            env.env_gradient(dd, ds)
+            tg.append(time.perf_counter() - t0)
+        out[f"{he}x{we}"] = {"refresh_ms": 1e3 * min(tr), "env_gradient_ms": 1e3 * min(tg)}
+    return out
+
+
+def env_gpu_timings(shapes=((16, 32), (64, 128), (128, 256), (256, 512)), seed=0):
+    """The same two operations on the device (ss_env_refresh / ss_env_adjoint),
+    CUDA events, mean of 10 after a warm-up."""
+    import torch
+
+    import paper_2605_05876_b200 as ss
+    from paper_2605_05876_b200 import scenes
+    out = {}
+    for he, we in shapes:
+        env = ss.EnvironmentLight(np.log(scenes.env_lognormal(he, we, seed)))
+        rng = np.random.default_rng(seed)
+        dd = torch.tensor(rng.normal(size=(he, we, 3)), device="cuda", dtype=torch.float64)
+        ds = torch.tensor(rng.normal(size=(env.levels, he, we, 3)), device="cuda", dtype=torch.float64)
+        env.refresh()
+        env.env_gradient(dd, ds)
+        res = {}
+        for name, fn in (("refresh_ms", env.refresh), ("env_gradient_ms", lambda: env.env_gradient(dd, ds))):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(10):
+                fn()
+            b.record()
+            b.synchronize()
+            res[name] = a.elapsed_time(b) / 10
+        out[f"{he}x{we}"] = res
+    return out
+
+
 def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
@@ -275,7 +326,7 @@ def _config_workload(cfg):
     raise ValueError(cfg)
 
 
-def run_config(cfg, steps=3, warmup=2):
+def run_config(cfg, steps=None, warmup=3):
     """views/s of the training step (L1, Adam, env refresh) on config `cfg`;
     config 4 adds the per-step refinement pass (q = 0.95, budget 1.05 N) and
     the neighbour-index rebuild, timed separately and inside the step."""
@@ -285,6 +336,7 @@ def run_config(cfg, steps=3, warmup=2):
     from paper_2605_05876_b200.densify import DensifyStats
     from paper_2605_05876_b200.step import TrainStep
     gt, init, env_base, cams, W, H, extra = _config_workload(cfg)
+    steps = steps or {0: 50, 1: 20}.get(cfg, 3)
     gt_env = ss.EnvironmentLight.from_base(env_base)
     gtc = ss.SurfelCloud(**gt)
     targets = [ss.render(gtc, c, ss.RenderOptions(), env=gt_env).rgb.contiguous() for c in cams]
@@ -298,8 +350,10 @@ def run_config(cfg, steps=3, warmup=2):
     ev = lambda: torch.cuda.Event(enable_timing=True)
     ref_ms, knn_ms, sizes = [], [], []
 
+    graph = [not refine]  # CUDA-graph replay of the gradient pass (the refining step rebinds the cloud)
+
     def one():
-        ts.step(cams, targets)
+        ts.step(cams, targets, graph=graph[0])
         if refine:
             stats = DensifyStats.zeros(len(ts.cloud))
             stats.accumulate(ts.grads["ss_grad"], ts.view_count)
@@ -312,17 +366,25 @@ def run_config(cfg, steps=3, warmup=2):
             return a, b, c
         return None
 
-    for _ in range(warmup):
-        one()
-    torch.cuda.synchronize()
-    e0, e1 = ev(), ev()
-    e0.record()
-    marks = [one() for _ in range(steps)]
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
+    def timed():
+        for _ in range(warmup):
+            one()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record()
+        marks = [one() for _ in range(steps)]
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps, marks
+
+    ms, marks = timed()
     out = {"views_per_s": len(cams) / (ms / 1e3), "ms_per_step": ms, "views_per_step": len(cams),
-           "surfels": len(init["centers"]), "image": [W, H], "env": list(env_base.shape[:2])}
+           "surfels": len(init["centers"]), "image": [W, H], "env": list(env_base.shape[:2]),
+           "cuda_graph": graph[0]}
+    if graph[0]:  # the same step issued eagerly (Python + ctypes launches per view)
+        graph[0] = False
+        ms_e, _ = timed()
+        out["views_per_s_eager"] = len(cams) / (ms_e / 1e3)
     if refine:
         ref_ms = [a.elapsed_time(b) for a, b, _ in marks]
         knn_ms = [b.elapsed_time(c) for _, b, c in marks]
@@ -387,8 +449,8 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # dominant-kernel timing: events around every train_backward launch
-    ts.kernel_events = []
+    # the timed steps carry no instrumentation (per-kernel events between the
+    # launches cost ~3% of the step by perturbing the worker streams' overlap)
     ev0.record(stream)
     for _ in range(args.steps):
         one_step()
@@ -397,9 +459,14 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     step_ms = ev0.elapsed_time(ev1) / args.steps
+    clk = clocks.stop() if clocks else None
+    # one more step with events around every stage launch (the in-step
+    # per-kernel times: concurrent streams, so each span includes overlap)
+    ts.kernel_events = []
+    one_step()
+    torch.cuda.synchronize()
     kev = ts.kernel_events
     ts.kernel_events = None
-    clk = clocks.stop() if clocks else None
     t = torch.tensor([step_ms], device="cuda", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -427,6 +494,7 @@ def run_ours(args):
     # per-step fixed stages, timed on their own: they are inside
     # every timed step above as well
     fixed = ts.fixed_costs()
+    fixed["env_by_size"] = env_gpu_timings()  # BASELINE.md §2 sizes (+ configs 2 and 4)
     if world == 1:
         # the density-aware refinement scan on this step's statistics, on the
         # device (refine_topology: isolation, prune, quantile, budget, split,
@@ -538,25 +606,33 @@ def run_ours(args):
     HW = RES * RES
     bwd_ms = float(np.mean(iso.get("train_backward", [float("nan")])))
     bwd_ms_step = float(np.mean(per_kernel.get("train_backward", [float("nan")])))
-    # algorithmic bytes per launch: raster bwd gathers 96 B/pair
-    # + 4 B list entry, reads its per-pixel upstream (16 B/px) and writes the
-    # 80 B record accumulator of every kept record
-    bwd_bytes = 100.0 * P + 16.0 * HW + 80.0 * Nk
+    # algorithmic (compulsory) bytes per launch of the record-parallel
+    # backward: every kept record read once (96 B) and its 80 B accumulator
+    # row written, the per-pixel layer header read once (32 B/px) and the
+    # 16 B coefficient texel of every (pixel, layer) once (LP = sum over
+    # pixels of the layer count, measured on the step's views)
+    LP = stats.get("layer_pixels_mean", 0.0)
+    bwd_bytes = 96.0 * Nk + 80.0 * Nk + 32.0 * HW + 16.0 * LP
     achieved = bwd_bytes / (bwd_ms / 1e3) / 1e9
     view_bytes = 176.0 * N_SURFELS + 352.0 * Nk + 236.0 * P + 40.0 * HW
     cpu = None
     if world == 1 and not args.no_cpu:
         dt, cores, sample = cpu_oracle_view()
-        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+               "env": env_cpu_timings()}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": _config({"parallelism": f"dp{world} over views", "pairs_per_view": P, "kept_per_view": Nk}),
+        "config": _config({"parallelism": f"dp{world} over views", "pairs_per_view": P, "kept_per_view": Nk,
+                                 "layer_pixels_per_view": LP}),
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src, "kernel": "record backward (ss_train_backward_records: area classes, splat_bwd, big rects)",
-                     "algorithmic_bytes_per_launch": bwd_bytes, "avg_launch_ms": bwd_ms,
+                     "algorithmic_bytes_per_launch": bwd_bytes,
+                     "algorithmic_bytes_formula": "96 Nk + 80 Nk + 32 HW + 16 LP (records, accumulator rows, "
+                                                  "pixel headers, (pixel, layer) coefficients)",
+                     "avg_launch_ms": bwd_ms,
                      "avg_launch_ms_in_step": bwd_ms_step,
                      "timing": "CUDA events around each ss_train_backward_records call on its worker stream, one "
                                "step with the views serialised (avg_launch_ms); in the timed 3-stream step the "

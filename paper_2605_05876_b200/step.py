@@ -248,8 +248,9 @@ class TrainStep:
         # ~1e-4 relative: texel coordinates at 256-texel rows carry ~1e-5
         # texel float32 rounding)
         self.color_source = _lib.SS_COLOR_IBL
-        self._pairs, self._kept, self._nviews = [], [], 0
+        self._pairs, self._kept, self._layer_px, self._nviews = [], [], [], 0
         self.kernel_events = None      # list -> (name, start, end) CUDA events per raster launch
+        self._graphs = {}              # step(graph=True): captured gradient passes by (cameras, inputs)
         self.active_streams = None     # None: all worker streams; 1: views serialised (isolated kernel timing)
         self._stage = None
         # preprocess, scan + order, scatter, tile sort x2, train fwd, ndc, area class, class scatter,
@@ -264,6 +265,7 @@ class TrainStep:
         buffer) and the native views of both."""
         he, we = self.env.shape
         dev = cloud.centers.device
+        self._graphs = {}  # captured launches hold the old cloud's pointers
         self.cloud = cloud
         self.n = len(cloud)
         if self.n > self.surfel_capacity:  # grow the per-view buffers
@@ -463,6 +465,7 @@ class TrainStep:
                     b = self.bufs[k]
                     self._pairs.append(int(b.offsets[-1].item()))
                     self._kept.append(int((b.cull == 0).sum().item()))
+                    self._layer_px.append(self._view_layer_pixels(b))
         for st in self.streams:
             main.wait_stream(st)
         for b in self.bufs[1:nst]:  # the other sets' derived-map sums into the step's
@@ -487,10 +490,22 @@ class TrainStep:
     def launches_per_step(self):
         return self.launches_per_view * self._nviews + self.launches_per_step_fixed
 
+    def _view_layer_pixels(self, b):
+        """Sum over pixels of the layer count of the view just run on buffer
+        set b (pixels of tiles with pairs; the others hold no header)."""
+        t = self.tile
+        ntx, nty = self.ntx, self.ntiles // self.ntx
+        live = (b.offsets[1:self.ntiles + 1] > b.offsets[:self.ntiles]).view(nty, ntx)
+        live = live.repeat_interleave(t, 0).repeat_interleave(t, 1)[:self.H, :self.W].reshape(-1)
+        layers = (b.pix_hdr[:, 0] >> 8) & 0xff
+        return int((layers * live).sum().item())
+
     def last_stats(self):
-        """Pair and kept-record counts of the last step's views (host sync)."""
+        """Pair and kept-record counts and layer-pixels of the last step's
+        views (collect_stats; host syncs)."""
         return {"pairs_mean": float(np.mean(self._pairs)) if self._pairs else 0.0,
-                "kept_mean": float(np.mean(self._kept)) if self._kept else 0.0}
+                "kept_mean": float(np.mean(self._kept)) if self._kept else 0.0,
+                "layer_pixels_mean": float(np.mean(self._layer_px)) if getattr(self, "_layer_px", None) else 0.0}
 
     @property
     def touched(self):
@@ -549,7 +564,7 @@ class TrainStep:
         while True:
             self.zero()
             self._nviews = len(cameras)
-            self._pairs, self._kept = [], []
+            self._pairs, self._kept, self._layer_px = [], [], []
             self._run_views(cameras, lambda i, st: targets[i], masks=masks)
             self._normal_consistency(len(cameras))
             self._finish()
@@ -607,8 +622,60 @@ class TrainStep:
         self.adam.step_multi(items, renorm_quats="quats")  # one launch, quaternions renormalised in it
         self.env.refresh()
 
-    def step(self, cameras, targets, masks=None):
-        self.gradients(cameras, targets, masks)
+    # -- CUDA-graph replay ----------------------------------------------------
+    MAX_GRAPHS = 8
+
+    def _graph_key(self, cameras, targets, masks):
+        cams = b"".join(bytes(_lib.make_camera(c)) for c in cameras)
+        ptrs = tuple(int(t.data_ptr()) for t in targets)
+        mptrs = None if masks is None else tuple(int(m.data_ptr()) for m in masks)
+        return (cams, ptrs, mptrs, self.cons_scale, self.capacity, self.n, len(self.streams), self.active_streams)
+
+    def gradients_graphed(self, cameras, targets, masks=None):
+        """gradients() replayed from a CUDA graph: the first call with a given
+        camera list and input tensors runs eagerly and then captures the whole
+        gradient pass (every view's launches on the worker streams, the env
+        adjoint, the status copy); later calls replay it with ONE host launch.
+        Kernel arguments (cameras, the consolidation weight) are baked into the
+        graph, so the cache is keyed by them and by the input tensors' device
+        addresses; it is dropped when the pair buffers grow or the cloud is
+        rebound.  The status read and the overflow re-run stay as in
+        gradients().  Single process only (the NCCL all-reduce is not captured)."""
+        if self.pg is not None or (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+            return self.gradients(cameras, targets, masks)
+        if self.kernel_events is not None or self.collect_stats or self.captured_rgb is not None:
+            return self.gradients(cameras, targets, masks)
+        if self.capacity == 0:
+            self.size_pairs(cameras[:2])
+        key = self._graph_key(cameras, targets, masks)
+        g = self._graphs.get(key)
+        if g is None:
+            self.gradients(cameras, targets, masks)  # eager: sizes buffers, sets kernel attributes
+            key = self._graph_key(cameras, targets, masks)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.zero()
+                self._nviews = len(cameras)
+                self._run_views(cameras, lambda i, st: targets[i], masks=masks)
+                self._normal_consistency(len(cameras))
+                self._finish()
+            if len(self._graphs) >= self.MAX_GRAPHS:
+                self._graphs.pop(next(iter(self._graphs)))
+            self._graphs[key] = g
+            return  # the eager pass's gradients stand (capture runs nothing)
+        g.replay()
+        if self._status():  # pair buffers grew: the captured launches are stale
+            self._graphs.clear()
+            self.gradients(cameras, targets, masks)
+
+    def step(self, cameras, targets, masks=None, graph=False):
+        """One optimisation step over `cameras` (gradients, Adam, env refresh);
+        graph=True replays the gradient pass from a CUDA graph (see
+        gradients_graphed)."""
+        if graph:
+            self.gradients_graphed(cameras, targets, masks)
+        else:
+            self.gradients(cameras, targets, masks)
         self.apply()
         # device scalar: loss="l1": sum over views of sum|rgb - target|;
         # loss="photometric": sum over views of the per-view fit loss

@@ -285,3 +285,42 @@ def test_nonfinite_colour_raises_in_step():
     ts = TrainStep(cloud, env, 32, 32)
     with pytest.raises(ValueError):
         ts.step(cams, [torch.zeros(32, 32, 3, device="cuda")] * len(cams))
+
+
+def test_graph_replay_matches_eager():
+    """TrainStep.step(graph=True): the captured gradient pass replays the
+    eager one (same gradients up to the float atomics' order), the cache is
+    keyed by the cameras, and a pair-buffer overflow drops it and re-runs."""
+    gt = scenes.config0(0, 10_000)
+    cams = ss.fibonacci_cameras(4, 3.0, 128, 128)
+    env = ss.EnvironmentLight(np.log(scenes.env_lognormal(16, 32, 2)))
+    targets = [ss.render(ss.SurfelCloud(**gt), c, ss.RenderOptions(), env=env).rgb.contiguous() for c in cams]
+    cloud = ss.SurfelCloud(**scenes.perturb(gt, 1))
+    ts = TrainStep(cloud, env, 128, 128, streams=2)
+    ts.gradients(cams, targets)
+    ref = {k: ts.grads[k].clone() for k in PARAMS}
+    ref_env = ts.g_env_log.clone()
+    for _ in range(3):  # eager + capture, then two replays
+        ts.gradients_graphed(cams, targets)
+        for k in PARAMS:
+            torch.testing.assert_close(ts.grads[k], ref[k], rtol=1e-5, atol=1e-6 * float(ref[k].abs().max()))
+        torch.testing.assert_close(ts.g_env_log, ref_env, rtol=1e-5, atol=1e-6 * float(ref_env.abs().max()))
+    assert len(ts._graphs) == 1
+    ts.gradients_graphed(cams[:2], targets[:2])  # another camera list: its own graph
+    assert len(ts._graphs) == 2
+    # replay overflow: the surfels grow in place (as Adam would grow them),
+    # the captured pass overflows its pair buffers, which grow, and the step
+    # re-runs eagerly (and drops the stale graphs)
+    ts._alloc_pairs(int(ts.bufs[0].offsets[-1].item()) + 64)
+    ts._graphs.clear()
+    ts.gradients_graphed(cams[:1], targets[:1])
+    ts.gradients_graphed(cams[:1], targets[:1])
+    grows = ts.regrows
+    with torch.no_grad():
+        cloud.log_scales.add_(0.4)
+    ts.gradients_graphed(cams[:1], targets[:1])
+    assert ts.regrows > grows and len(ts._graphs) == 0
+    want = {k: ts.grads[k].clone() for k in PARAMS}
+    ts.gradients(cams[:1], targets[:1])
+    for k in PARAMS:
+        torch.testing.assert_close(want[k], ts.grads[k], rtol=1e-5, atol=1e-6 * float(ts.grads[k].abs().max()))
