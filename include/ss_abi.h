@@ -300,13 +300,15 @@ int ss_normal_consistency(int n, int k, const float *centers, const float *quats
  * searches): ss_cell_grid_build sizes cubic cells over the centres'
  * bounding box on the device and counting-sorts the surfels into dim^3
  * cells (per-cell [start, end) table); `grid`: ss_cell_grid_words(n, dim)
- * int32 words of caller scratch, dim <= 512.  ss_knn_dense is
- * ss_knn_oriented on it (queries in cell order), ss_isolation_dense the
+ * int32 words of caller scratch, dim <= 512; it also keeps a cell-ordered
+ * float4 copy of the centres (x, y, z, source index).  ss_knn_dense is
+ * ss_knn_oriented on it (queries in cell order; normals_ws: 4 n float64 of
+ * caller scratch for the cell-ordered normals), ss_isolation_dense the
  * isolation test of densify.py:118-123. */
 size_t ss_cell_grid_words(int n, int dim);
 int ss_cell_grid_build(int n, const float *centers, int dim, int32_t *grid, void *stream);
 int ss_knn_dense(int n, const float *centers, const float *quats, const int32_t *grid, int dim, int k,
-                 int64_t *neighbors, double *mean_dist, void *stream);
+                 double *normals_ws, int64_t *neighbors, double *mean_dist, void *stream);
 int ss_isolation_dense(int n, const float *centers, const float *log_scales, const int32_t *grid, int dim,
                        uint8_t *isolated, void *stream);
 

@@ -130,7 +130,7 @@ _SIGNATURES = {
     "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_cell_grid_words": [ctypes.c_int, ctypes.c_int],
     "ss_cell_grid_build": [ctypes.c_int, c_p, ctypes.c_int, c_p, c_p],
-    "ss_knn_dense": [ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p],
+    "ss_knn_dense": [ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_isolation_dense": [ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, c_p, c_p],
     "ss_grid_fit": [ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_grid_cells_d": [ctypes.c_int, c_p, c_p, c_p, c_p],
@@ -226,9 +226,9 @@ def make_env(env):
 
 def cell_grid(centers, n):
     """Dense cell grid over `centers` (ss_cell_grid_build): (words, dim).
-    dim ~ sqrt(n / 24) so a surface sampling puts tens of surfels in each
-    occupied cell (<= 256: a 67 MB table)."""
-    dim = int(min(256, max(1, round((max(n, 1) / 24.0) ** 0.5))))
+    dim ~ sqrt(n / 24) so a surface sampling puts about ten surfels in each
+    occupied cell (<= 512: at most a 1 GB table; 4M surfels take dim 408)."""
+    dim = int(min(512, max(1, round((max(n, 1) / 24.0) ** 0.5))))
     lib = load()
     words = torch.empty(int(lib.ss_cell_grid_words(n, dim)), device=centers.device, dtype=torch.int32)
     check(lib.ss_cell_grid_build(n, ptr(centers), dim, ptr(words), stream_ptr()), "ss_cell_grid_build")

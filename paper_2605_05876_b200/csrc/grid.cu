@@ -161,66 +161,97 @@ __global__ void __launch_bounds__(256) scan_apply_kernel(int m, int32_t *__restr
     if (blockIdx.x == 0 && threadIdx.x == 0) v[m] = n;
 }
 
-__global__ void cell_scatter_kernel(int n, const int32_t *__restrict__ cell_of, const int32_t *__restrict__ starts,
-                                    int32_t *__restrict__ cursor, int32_t *__restrict__ order) {
+__global__ void cell_scatter_kernel(int n, const float *__restrict__ c, const int32_t *__restrict__ cell_of,
+                                    const int32_t *__restrict__ starts, int32_t *__restrict__ cursor,
+                                    int32_t *__restrict__ order, float4 *__restrict__ pk) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int cid = cell_of[i];
-    order[starts[cid] + atomicAdd(cursor + cid, 1)] = i;
+    const int at = starts[cid] + atomicAdd(cursor + cid, 1);
+    order[at] = i;
+    pk[at] = make_float4(c[3 * i], c[3 * i + 1], c[3 * i + 2], __int_as_float(i));
 }
 
 // ---- oriented KNN (knn.py:31-81) on the dense grid ------------------------
+// The candidates of a query stream from the grid's cell-ordered copy of the
+// centres (float4: x, y, z, source index) and a cell-ordered float64 normal
+// table built once per call, so the inner loop is a broadcast load, a
+// float64 squared distance and a compare against the current k-th best; the
+// k best (squared distance, index) pairs live in registers (K is a template
+// parameter: the insertion is unrolled, no local-memory arrays).  Ordering
+// by the squared distance is cKDTree's own (it compares squared distances
+// and takes the root of the results).
 constexpr int kMaxK = 16;
 
+// quat_to_frame's normal column (surfels.py:40-51), float64 without contraction
 __device__ __forceinline__ void quat_normal(const float *q4, double n[3]) {
     const double q0 = q4[0], q1 = q4[1], q2 = q4[2], q3 = q4[3];
-    const double qn = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
-    const double w = q0 / qn, x = q1 / qn, y = q2 / qn, z = q3 / qn;
-    n[0] = 2 * (x * z + w * y);
-    n[1] = 2 * (y * z - w * x);
-    n[2] = 1 - 2 * (x * x + y * y);
+    const double qn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q0, q0), __dmul_rn(q1, q1)), __dmul_rn(q2, q2)),
+                                           __dmul_rn(q3, q3)));
+    const double w = __ddiv_rn(q0, qn), x = __ddiv_rn(q1, qn), y = __ddiv_rn(q2, qn), z = __ddiv_rn(q3, qn);
+    n[0] = __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, z), __dmul_rn(w, y)));
+    n[1] = __dmul_rn(2.0, __dsub_rn(__dmul_rn(y, z), __dmul_rn(w, x)));
+    n[2] = __dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y))));
 }
 
+// cell-ordered float64 normals of the query pass
+__global__ void knn_normals_kernel(int n, const float *__restrict__ q, const int32_t *__restrict__ order,
+                                   double4 *__restrict__ nrm) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double v[3];
+    quat_normal(q + 4 * (size_t)__ldg(order + t), v);
+    nrm[t] = make_double4(v[0], v[1], v[2], 0.0);
+}
+
+__device__ __forceinline__ double sqdist(double px, double py, double pz, float4 c) {
+    const double dx = __dsub_rn(px, (double)c.x), dy = __dsub_rn(py, (double)c.y), dz = __dsub_rn(pz, (double)c.z);
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// (d, j) before (e, k): by distance, then index
+__device__ __forceinline__ bool before(double d, int j, double e, int k) { return d < e || (d == e && j < k); }
+
 template <int K>
-__global__ void __launch_bounds__(128) knn_dense_kernel(int n, const float *__restrict__ c, const float *__restrict__ q,
-                                                        const int32_t *__restrict__ gw,
-                                                        const int32_t *__restrict__ order, int k,
+__global__ void __launch_bounds__(128) knn_dense_kernel(int n, const int32_t *__restrict__ gw,
+                                                        const float4 *__restrict__ pk, const double4 *__restrict__ nrm,
                                                         int64_t *__restrict__ neighbors,
                                                         double *__restrict__ mean_dist) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
-    const int i = __ldg(order + t);  // cell order: a warp's queries are neighbours
     const Grid g = read_grid(gw);
     const int32_t *starts = gw + 16;
-    const double px = c[3 * i], py = c[3 * i + 1], pz = c[3 * i + 2];
-    double ni[3];
-    quat_normal(q + 4 * i, ni);
+    const float4 me = __ldg(pk + t);  // cell order: a warp's queries are neighbours
+    const int i = __float_as_int(me.w);
+    const double px = me.x, py = me.y, pz = me.z;
+    const double4 ni = nrm[t];
     double bd[K];
     int bj[K];
-    int cnt = 0;
-    double any_d = 1e300;  // nearest other surfel of any orientation (the fallback scale)
+#pragma unroll
+    for (int s = 0; s < K; ++s) { bd[s] = INFINITY; bj[s] = 0x7fffffff; }
+    double any_d = INFINITY;  // nearest other surfel of any orientation (the fallback scale)
     int any_j = 0x7fffffff;
     const int cx = gaxis(px, g.ox, g.cell, g.dim), cy = gaxis(py, g.oy, g.cell, g.dim), cz = gaxis(pz, g.oz, g.cell, g.dim);
     auto visit_cell = [&](int cid) {
         const int s1 = __ldg(starts + cid + 1);
         for (int s = __ldg(starts + cid); s < s1; ++s) {
-            const int j = __ldg(order + s);
+            const float4 c = __ldg(pk + s);
+            const int j = __float_as_int(c.w);
             if (j == i) continue;
-            const double dx = px - c[3 * j], dy = py - c[3 * j + 1], dz = pz - c[3 * j + 2];
-            const double d = sqrt(dx * dx + dy * dy + dz * dz);
-            if (d < any_d || (d == any_d && j < any_j)) { any_d = d; any_j = j; }
-            if (cnt == k && !(d < bd[k - 1] || (d == bd[k - 1] && j < bj[k - 1]))) continue;
-            double nj[3];
-            quat_normal(q + 4 * j, nj);
-            if (!((ni[0] * nj[0] + ni[1] * nj[1]) + ni[2] * nj[2] > 0.0)) continue;
-            int sl = cnt < k ? cnt++ : k - 1;  // insertion by (distance, index)
-            while (sl > 0 && (bd[sl - 1] > d || (bd[sl - 1] == d && bj[sl - 1] > j))) {
-                bd[sl] = bd[sl - 1];
-                bj[sl] = bj[sl - 1];
-                --sl;
+            const double d = sqdist(px, py, pz, c);
+            if (before(d, j, any_d, any_j)) { any_d = d; any_j = j; }
+            if (!before(d, j, bd[K - 1], bj[K - 1])) continue;
+            const double4 nj = nrm[s];
+            if (!(__dadd_rn(__dadd_rn(__dmul_rn(ni.x, nj.x), __dmul_rn(ni.y, nj.y)), __dmul_rn(ni.z, nj.z)) > 0.0))
+                continue;
+            // unrolled insertion (from the back: bd[s - 1] is still the old value)
+#pragma unroll
+            for (int m = K - 1; m >= 0; --m) {
+                if (before(d, j, bd[m], bj[m])) {
+                    if (m > 0 && before(d, j, bd[m - 1], bj[m - 1])) { bd[m] = bd[m - 1]; bj[m] = bj[m - 1]; }
+                    else { bd[m] = d; bj[m] = j; }
+                }
             }
-            bd[sl] = d;
-            bj[sl] = j;
         }
     };
     for (int r = 0;; ++r) {
@@ -236,28 +267,32 @@ __global__ void __launch_bounds__(128) knn_dense_kernel(int n, const float *__re
                 }
             }
         // every unvisited surfel lies more than r cells (r * cell) away
-        const double reach = (double)r * (double)g.cell;
         const bool covered = x0 <= 0 && y0 <= 0 && z0 <= 0 && x1 >= g.dim - 1 && y1 >= g.dim - 1 && z1 >= g.dim - 1;
         if (covered) break;
-        if (cnt == k && bd[k - 1] <= reach) break;  // (a short row keeps searching, like knn.py:60-63)
+        // a full row whose k-th distance is within reach is final (a short
+        // row keeps searching, like knn.py:60-63)
+        if (bj[K - 1] != 0x7fffffff && __dsqrt_rn(bd[K - 1]) <= (double)r * (double)g.cell) break;
     }
     double sum = 0.0;
-    for (int s = 0; s < k; ++s) {
-        neighbors[(size_t)i * k + s] = s < cnt ? (int64_t)bj[s] : (int64_t)-1;
-        if (s < cnt) sum += bd[s];
+    int cnt = 0;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+        const bool ok = bj[s] != 0x7fffffff;
+        neighbors[(size_t)i * K + s] = ok ? (int64_t)bj[s] : (int64_t)-1;
+        if (ok) { sum += __dsqrt_rn(bd[s]); ++cnt; }
     }
-    mean_dist[i] = cnt > 0 ? sum / cnt : any_d;
+    mean_dist[i] = cnt > 0 ? sum / cnt : __dsqrt_rn(any_d);
 }
 
 // ---- isolation (densify.py:118-123) on the dense grid ----------------------
 __global__ void __launch_bounds__(128) isolation_dense_kernel(int n, const float *__restrict__ c,
                                                               const float *__restrict__ ls,
                                                               const int32_t *__restrict__ gw,
-                                                              const int32_t *__restrict__ order,
+                                                              const float4 *__restrict__ pk,
                                                               uint8_t *__restrict__ isolated) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
-    const int i = __ldg(order + t);
+    const int i = __float_as_int(__ldg(pk + t).w);
     if (n <= 1) { isolated[i] = 0; return; }
     const Grid g = read_grid(gw);
     const int32_t *starts = gw + 16;
@@ -273,10 +308,9 @@ __global__ void __launch_bounds__(128) isolation_dense_kernel(int n, const float
     auto near_in = [&](int cid) {
         const int s1e = __ldg(starts + cid + 1);
         for (int s = __ldg(starts + cid); s < s1e; ++s) {
-            const int j = __ldg(order + s);
-            if (j == i) continue;
-            const double dx = px - c[3 * j], dy = py - c[3 * j + 1], dz = pz - c[3 * j + 2];
-            if (sqrt(dx * dx + dy * dy + dz * dz) <= sup) return true;
+            const float4 cj = __ldg(pk + s);
+            if (__float_as_int(cj.w) == i) continue;
+            if (__dsqrt_rn(sqdist(px, py, pz, cj)) <= sup) return true;
         }
         return false;
     };
@@ -294,12 +328,17 @@ __global__ void __launch_bounds__(128) isolation_dense_kernel(int n, const float
 
 }  // namespace
 
+static size_t pk_offset(size_t cells, size_t nb, int n) {
+    return (16 + (cells + 1) + nb + cells + 2 * (size_t)n + 3) & ~(size_t)3;
+}
+
 extern "C" size_t ss_cell_grid_words(int n, int dim) {
     if (n < 0 || dim < 1 || dim > 512) return 0;
     const size_t cells = (size_t)dim * dim * dim;
     const size_t nb = (cells + kScan - 1) / kScan;
-    // params + starts (cells + 1) + block sums + cursors (cells) + cell of (n) + order (n)
-    return 16 + (cells + 1) + nb + cells + 2 * (size_t)n;
+    // params + starts (cells + 1) + block sums + cursors (cells) + cell of (n) + order (n),
+    // then the cell-ordered centres (float4, 16-byte aligned)
+    return pk_offset(cells, nb, n) + 4 * (size_t)n;
 }
 
 extern "C" int ss_cell_grid_build(int n, const float *centers, int dim, int32_t *grid, void *stream) {
@@ -319,7 +358,8 @@ extern "C" int ss_cell_grid_build(int n, const float *centers, int dim, int32_t 
     scan_sum_kernel<<<nb, 256, 0, s>>>((int)cells, starts, bsum);
     scan_blocks_kernel<<<1, 1024, 0, s>>>(nb, bsum);
     scan_apply_kernel<<<nb, 256, 0, s>>>((int)cells, starts, bsum, n);
-    if (n > 0) cell_scatter_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, cell_of, starts, cursor, order);
+    float4 *pk = reinterpret_cast<float4 *>(grid + pk_offset(cells, nb, n));
+    if (n > 0) cell_scatter_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, centers, cell_of, starts, cursor, order, pk);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
@@ -330,13 +370,34 @@ static const int32_t *grid_order(const int32_t *grid, int n, int dim) {
     return grid + 16 + (cells + 1) + nb + cells + n;
 }
 
+static const float4 *grid_packed(const int32_t *grid, int n, int dim) {
+    const size_t cells = (size_t)dim * dim * dim;
+    const size_t nb = (cells + kScan - 1) / kScan;
+    return reinterpret_cast<const float4 *>(grid + pk_offset(cells, nb, n));
+}
+
+template <int K>
+static void launch_knn(int n, const int32_t *grid, const float4 *pk, const double4 *nrm, int64_t *neighbors,
+                       double *mean_dist, cudaStream_t s) {
+    knn_dense_kernel<K><<<(n + 127) / 128, 128, 0, s>>>(n, grid, pk, nrm, neighbors, mean_dist);
+}
+
 extern "C" int ss_knn_dense(int n, const float *centers, const float *quats, const int32_t *grid, int dim, int k,
-                            int64_t *neighbors, double *mean_dist, void *stream) {
+                            double *normals_ws, int64_t *neighbors, double *mean_dist, void *stream) {
     if (n < 0 || k < 1 || k > kMaxK || dim < 1 || dim > 512 || !grid) return SS_ERR_INVALID;
     if (n == 0) return SS_OK;
-    if (!centers || !quats || !neighbors || !mean_dist) return SS_ERR_INVALID;
-    knn_dense_kernel<kMaxK><<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(
-        n, centers, quats, grid, grid_order(grid, n, dim), k, neighbors, mean_dist);
+    if (!centers || !quats || !normals_ws || !neighbors || !mean_dist) return SS_ERR_INVALID;
+    cudaStream_t s = (cudaStream_t)stream;
+    double4 *nrm = reinterpret_cast<double4 *>(normals_ws);
+    knn_normals_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, quats, grid_order(grid, n, dim), nrm);
+    const float4 *pk = grid_packed(grid, n, dim);
+    switch (k) {
+#define SS_KNN_CASE(K) case K: launch_knn<K>(n, grid, pk, nrm, neighbors, mean_dist, s); break;
+        SS_KNN_CASE(1) SS_KNN_CASE(2) SS_KNN_CASE(3) SS_KNN_CASE(4) SS_KNN_CASE(5) SS_KNN_CASE(6)
+        SS_KNN_CASE(7) SS_KNN_CASE(8) SS_KNN_CASE(9) SS_KNN_CASE(10) SS_KNN_CASE(11) SS_KNN_CASE(12)
+        SS_KNN_CASE(13) SS_KNN_CASE(14) SS_KNN_CASE(15) SS_KNN_CASE(16)
+#undef SS_KNN_CASE
+    }
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
@@ -347,7 +408,7 @@ extern "C" int ss_isolation_dense(int n, const float *centers, const float *log_
     if (n == 0) return SS_OK;
     if (!centers || !log_scales || !isolated) return SS_ERR_INVALID;
     isolation_dense_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(n, centers, log_scales, grid,
-                                                                              grid_order(grid, n, dim), isolated);
+                                                                              grid_packed(grid, n, dim), isolated);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

@@ -35,6 +35,8 @@ class NeighborIndex:
             return
         lib = _lib.load()
         grid, dim = _lib.cell_grid(cloud.centers, n)
+        normals = torch.empty((n, 4), device=dev, dtype=torch.float64)  # cell-ordered normals (scratch)
         _lib.check(lib.ss_knn_dense(n, _lib.ptr(cloud.centers), _lib.ptr(cloud.quats), _lib.ptr(grid), dim, k,
-                                    _lib.ptr(self.neighbors), _lib.ptr(self.mean_dist), _lib.stream_ptr()),
+                                    _lib.ptr(normals), _lib.ptr(self.neighbors), _lib.ptr(self.mean_dist),
+                                    _lib.stream_ptr()),
                    "ss_knn_dense")
