@@ -498,6 +498,12 @@ int ss_refine_apply(int n, const uint8_t *kind, const int32_t *dst, const float 
  * in-rect record) evaluations, counts[1] decisions differing from the exact
  * reference arithmetic (0 by construction), counts[2] exact fallbacks taken.
  * counts: 3 uint64, zeroed by the caller. */
+/* Per-CTA (forward) / per-warp (record backward) timestamps for the tail
+ * analysis: only in a library built with -DSS_CTA_TIMING (else
+ * SS_ERR_INVALID); buf = 3 uint64 (start ns, end ns, SM id) per CTA / warp
+ * of the next launches, nullptr to stop. */
+int ss_debug_set_fwd_timing(void *buf);
+int ss_debug_set_bwd_timing(void *buf);
 int ss_debug_cover_check(int width, int height, int tile, const int32_t *tile_offsets,
                          const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
                          unsigned long long *counts, void *stream);

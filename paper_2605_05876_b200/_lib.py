@@ -127,6 +127,8 @@ _SIGNATURES = {
     "ss_knn_oriented": [ctypes.c_int, c_p, c_p, c_p, c_p, ctypes.POINTER(ctypes.c_float), ctypes.c_float, ctypes.c_int,
                         ctypes.c_int, c_p, c_p, c_p],
     "ss_normal_consistency": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_debug_set_fwd_timing": [c_p],
+    "ss_debug_set_bwd_timing": [c_p],
     "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_cell_grid_words": [ctypes.c_int, ctypes.c_int],
     "ss_cell_grid_build": [ctypes.c_int, c_p, ctypes.c_int, c_p, c_p],

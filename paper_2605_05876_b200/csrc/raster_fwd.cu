@@ -25,6 +25,15 @@
 #include "ss_common.cuh"
 #include "raster_walk.cuh"
 
+#ifdef SS_CTA_TIMING
+__device__ unsigned long long *g_fwd_times;  // (3 per CTA): start, end, smid
+extern "C" int ss_debug_set_fwd_timing(void *buf) {
+    return cudaMemcpyToSymbol(g_fwd_times, &buf, sizeof(buf)) == cudaSuccess ? SS_OK : SS_ERR_CUDA;
+}
+#else
+extern "C" int ss_debug_set_fwd_timing(void *) { return SS_ERR_INVALID; }
+#endif
+
 namespace {
 
 struct FwdParams {
@@ -84,6 +93,9 @@ template <bool kExtras, bool kTrain, bool kCons = false, bool kDeferred = false>
 __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 {
     __shared__ PackedScratch scratch[kFwdWarps];
+#ifdef SS_CTA_TIMING
+    const unsigned long long t_start = ss_globaltimer();
+#endif
     const int wpc = blockDim.x >> 5;  // kFwdWarps, or fewer for 8x8 tiles
     const int ctas_per_tile = P.tile * P.tile / (32 * wpc);
     const int t = P.tile_order ? P.tile_order[blockIdx.x / ctas_per_tile] : blockIdx.x / ctas_per_tile;
@@ -269,6 +281,13 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
         if (lane == 0) atomicAdd(P.loss, lsum);
     }
+#ifdef SS_CTA_TIMING
+    __syncthreads();
+    if (threadIdx.x == 0 && g_fwd_times) {
+        unsigned long long *o = g_fwd_times + 3 * (size_t)blockIdx.x;
+        o[0] = t_start; o[1] = ss_globaltimer(); o[2] = ss_smid();
+    }
+#endif
 }
 
 // Deferred-loss training step: turn the forward's raw layer sums (W, C) into

@@ -21,6 +21,15 @@
 #include "raster_walk.cuh"
 #include "warp_reduce.cuh"
 
+#ifdef SS_CTA_TIMING
+__device__ unsigned long long *g_bwd_times;  // (3 per warp of splat_bwd_kernel): start, end, smid
+extern "C" int ss_debug_set_bwd_timing(void *buf) {
+    return cudaMemcpyToSymbol(g_bwd_times, &buf, sizeof(buf)) == cudaSuccess ? SS_OK : SS_ERR_CUDA;
+}
+#else
+extern "C" int ss_debug_set_bwd_timing(void *) { return SS_ERR_INVALID; }
+#endif
+
 namespace {
 
 
@@ -316,6 +325,9 @@ constexpr int kNdcSmem = 4096;  // W + H up to this: pixel-centre tables staged 
 #ifndef SS_SPLAT_MINB
 #define SS_SPLAT_MINB 3  // resident CTAs per SM the register budget is sized for
 #endif
+#ifndef SS_SPLAT_GRID
+#define SS_SPLAT_GRID SS_SPLAT_MINB  // persistent CTAs launched per SM
+#endif
 #ifndef SS_SCAT_ITEMS
 #define SS_SCAT_ITEMS 8
 #endif
@@ -438,6 +450,9 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
                                                                         int32_t *counters)
 {
     extern __shared__ __align__(16) unsigned char splat_smem[];
+#ifdef SS_CTA_TIMING
+    const unsigned long long t_start = ss_globaltimer();
+#endif
     GroupSmem &sm = reinterpret_cast<GroupSmem *>(splat_smem)[threadIdx.x >> 5];
     // the exact pixel-centre tables of the coverage decisions, staged in
     // shared memory when they fit (one CTA barrier, at the start)
@@ -549,6 +564,12 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
         buf ^= 1;
     }
     cp_async_wait_all();
+#ifdef SS_CTA_TIMING
+    if (lane == 0 && g_bwd_times) {
+        unsigned long long *o = g_bwd_times + 3 * ((size_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+        o[0] = t_start; o[1] = ss_globaltimer(); o[2] = ss_smid();
+    }
+#endif
 }
 
 // Gradient contribution of record R at rect pixel k (row-major) for the big
@@ -648,7 +669,7 @@ template <bool kSmemNdc, bool kCons>
 void launch_splat(const SplatParams &P, const int32_t *order, int32_t *counters, int smem, cudaStream_t st) {
     ss_func_smem((const void *)splat_bwd_kernel<kSmemNdc, kCons>,
                  kSplatWarps * (int)sizeof(GroupSmem) + (kSmemNdc ? kNdcSmem * (int)sizeof(float) : 0));
-    splat_bwd_kernel<kSmemNdc, kCons><<<ss_sm_count() * SS_SPLAT_MINB, 32 * kSplatWarps, smem, st>>>(P, order, counters);
+    splat_bwd_kernel<kSmemNdc, kCons><<<ss_sm_count() * SS_SPLAT_GRID, 32 * kSplatWarps, smem, st>>>(P, order, counters);
 }
 
 static int backward_records(int n, const int8_t *cull, const float *records, int width, int height, int k_max,

@@ -352,8 +352,15 @@ class TrainStep:
         """Forward + backward of one view on the CURRENT stream with buffer set
         b; gradients accumulate into self.grads and b's derived-map sums.
         target_done: event recorded once `target` is consumed."""
-        lib = self.lib
         b = b if b is not None else self.bufs[0]
+        camst = self._front(cam, b)
+        self._raster(target, b, target_done=target_done, mask=mask)
+        self._chain(camst, b)
+
+    def _front(self, cam, b):
+        """Stage 1 of a view (current stream): preprocess + shading, binning
+        and the per-tile sort into buffer set b; returns the native camera."""
+        lib = self.lib
         s = _lib.stream_ptr()
         ev = self._ev_begin("preprocess")
         camst = self._preprocess(cam, b)
@@ -365,6 +372,13 @@ class TrainStep:
                                    _lib.ptr(b.flags), _lib.ptr(b.tile_order), s),
                    "ss_bin_sort")
         self._ev_end(ev)
+        return camst
+
+    def _raster(self, target, b, target_done=None, mask=None):
+        """Stage 2 (current stream): fused forward + loss + layer coefficients,
+        then the record-parallel backward into b's accumulator rows."""
+        lib = self.lib
+        s = _lib.stream_ptr()
         ev = self._ev_begin("train_forward")
         if self.loss_mode == "l1":
             rgb_out = None
@@ -429,6 +443,12 @@ class TrainStep:
                                                      _lib.ptr(b.pix_hdr), _lib.ptr(b.pixel_ndc), _lib.ptr(b.acc),
                                                      _lib.ptr(b.acc64), s), "ss_train_backward_records")
         self._ev_end(ev)
+
+    def _chain(self, camst, b):
+        """Stage 3 (current stream): the per-surfel chain into the step's
+        gradient buffer and b's derived-map sums."""
+        lib = self.lib
+        s = _lib.stream_ptr()
         ev = self._ev_begin("chain")
         # the chain kernels of concurrent views may overlap: their parameter
         # gradients are vector reductions (atomic), the derived-map sums go to
