@@ -302,13 +302,17 @@ int ss_normal_consistency(int n, int k, const float *centers, const float *quats
  * cells (per-cell [start, end) table); `grid`: ss_cell_grid_words(n, dim)
  * int32 words of caller scratch, dim <= 512; it also keeps a cell-ordered
  * float4 copy of the centres (x, y, z, source index).  ss_knn_dense is
- * ss_knn_oriented on it (queries in cell order; normals_ws: 4 n float64 of
- * caller scratch for the cell-ordered normals), ss_isolation_dense the
- * isolation test of densify.py:118-123. */
+ * ss_knn_oriented on it (queries in cell order; grid_coarse: a second grid
+ * of the same centres with wider cells, dim_coarse ~ dim / 4, on which the
+ * queries whose k-th oriented neighbour lies beyond a few fine shells are
+ * finished; workspace: ss_knn_workspace_bytes(n) of caller scratch, 8-byte
+ * aligned), ss_isolation_dense the isolation test of densify.py:118-123. */
 size_t ss_cell_grid_words(int n, int dim);
 int ss_cell_grid_build(int n, const float *centers, int dim, int32_t *grid, void *stream);
-int ss_knn_dense(int n, const float *centers, const float *quats, const int32_t *grid, int dim, int k,
-                 double *normals_ws, int64_t *neighbors, double *mean_dist, void *stream);
+size_t ss_knn_workspace_bytes(int n);
+int ss_knn_dense(int n, const float *centers, const float *quats, const int32_t *grid, int dim,
+                 const int32_t *grid_coarse, int dim_coarse, int k, void *workspace, int64_t *neighbors,
+                 double *mean_dist, void *stream);
 int ss_isolation_dense(int n, const float *centers, const float *log_scales, const int32_t *grid, int dim,
                        uint8_t *isolated, void *stream);
 

@@ -131,8 +131,9 @@ _SIGNATURES = {
     "ss_debug_set_bwd_timing": [c_p],
     "ss_debug_cover_check": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_cell_grid_words": [ctypes.c_int, ctypes.c_int],
+    "ss_knn_workspace_bytes": [ctypes.c_int],
     "ss_cell_grid_build": [ctypes.c_int, c_p, ctypes.c_int, c_p, c_p],
-    "ss_knn_dense": [ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
+    "ss_knn_dense": [ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, c_p, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_isolation_dense": [ctypes.c_int, c_p, c_p, c_p, ctypes.c_int, c_p, c_p],
     "ss_grid_fit": [ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_grid_cells_d": [ctypes.c_int, c_p, c_p, c_p, c_p],
@@ -165,6 +166,7 @@ def load(require_cuda=True):
         lib.ss_env_khat_words.restype = ctypes.c_size_t
         lib.ss_refine_workspace_bytes.restype = ctypes.c_size_t
         lib.ss_cell_grid_words.restype = ctypes.c_size_t
+        lib.ss_knn_workspace_bytes.restype = ctypes.c_size_t
         lib.ss_last_error.restype = ctypes.c_char_p
         lib.ss_version.restype = ctypes.c_int
         _lib = lib
@@ -226,11 +228,12 @@ def make_env(env):
                  ptr(getattr(env, "diffuse64", None)), ptr(getattr(env, "specular64", None)))
 
 
-def cell_grid(centers, n):
+def cell_grid(centers, n, dim=None):
     """Dense cell grid over `centers` (ss_cell_grid_build): (words, dim).
     dim ~ sqrt(n / 24) so a surface sampling puts about ten surfels in each
     occupied cell (<= 512: at most a 1 GB table; 4M surfels take dim 408)."""
-    dim = int(min(512, max(1, round((max(n, 1) / 24.0) ** 0.5))))
+    if dim is None:
+        dim = int(min(512, max(1, round((max(n, 1) / 24.0) ** 0.5))))
     lib = load()
     words = torch.empty(int(lib.ss_cell_grid_words(n, dim)), device=centers.device, dtype=torch.int32)
     check(lib.ss_cell_grid_build(n, ptr(centers), dim, ptr(words), stream_ptr()), "ss_cell_grid_build")

@@ -212,11 +212,72 @@ __device__ __forceinline__ double sqdist(double px, double py, double pz, float4
 // (d, j) before (e, k): by distance, then index
 __device__ __forceinline__ bool before(double d, int j, double e, int k) { return d < e || (d == e && j < k); }
 
+// The k best (squared distance, index) pairs of one query in registers,
+// plus the nearest surfel of any orientation (the fallback scale).
+template <int K>
+struct TopK {
+    double bd[K];
+    int bj[K];
+    double any_d;
+    int any_j;
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int s = 0; s < K; ++s) { bd[s] = INFINITY; bj[s] = 0x7fffffff; }
+        any_d = INFINITY;
+        any_j = 0x7fffffff;
+    }
+    __device__ __forceinline__ bool full() const { return bj[K - 1] != 0x7fffffff; }
+    // unrolled insertion (from the back: bd[m - 1] is still the old value)
+    __device__ __forceinline__ void insert(double d, int j) {
+#pragma unroll
+        for (int m = K - 1; m >= 0; --m) {
+            if (before(d, j, bd[m], bj[m])) {
+                if (m > 0 && before(d, j, bd[m - 1], bj[m - 1])) { bd[m] = bd[m - 1]; bj[m] = bj[m - 1]; }
+                else { bd[m] = d; bj[m] = j; }
+            }
+        }
+    }
+    // candidate s of the cell-ordered tables for the query (i, p, ni)
+    __device__ __forceinline__ void visit(int i, double px, double py, double pz, const double4 &ni, float4 c,
+                                          const double4 *__restrict__ nrm, int s) {
+        const int j = __float_as_int(c.w);
+        if (j == i) return;
+        const double d = sqdist(px, py, pz, c);
+        if (before(d, j, any_d, any_j)) { any_d = d; any_j = j; }
+        if (!before(d, j, bd[K - 1], bj[K - 1])) return;
+        const double4 nj = nrm[s];
+        if (!(__dadd_rn(__dadd_rn(__dmul_rn(ni.x, nj.x), __dmul_rn(ni.y, nj.y)), __dmul_rn(ni.z, nj.z)) > 0.0)) return;
+        insert(d, j);
+    }
+    __device__ __forceinline__ void write(int i, int64_t *__restrict__ neighbors, double *__restrict__ mean_dist) const {
+        double sum = 0.0;
+        int cnt = 0;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const bool ok = bj[s] != 0x7fffffff;
+            neighbors[(size_t)i * K + s] = ok ? (int64_t)bj[s] : (int64_t)-1;
+            if (ok) { sum += __dsqrt_rn(bd[s]); ++cnt; }
+        }
+        mean_dist[i] = cnt > 0 ? sum / cnt : __dsqrt_rn(any_d);
+    }
+};
+
+// Shells of cells around the query's cell.  A query whose row is not final
+// after kMaxShell shells (its k-th oriented neighbour lies far away: a
+// surfel facing against its surroundings, an outlier) is deferred to
+// knn_far_kernel (a CTA per query, on the coarse grid) instead of expanding
+// shells of mostly empty cells one thread at a time (a single such query at
+// r ~ 60 visits ~2M cells).
+#ifndef SS_KNN_MAX_SHELL
+#define SS_KNN_MAX_SHELL 3
+#endif
+constexpr int kMaxShell = SS_KNN_MAX_SHELL;
+
 template <int K>
 __global__ void __launch_bounds__(128) knn_dense_kernel(int n, const int32_t *__restrict__ gw,
                                                         const float4 *__restrict__ pk, const double4 *__restrict__ nrm,
                                                         int64_t *__restrict__ neighbors,
-                                                        double *__restrict__ mean_dist) {
+                                                        double *__restrict__ mean_dist, int32_t *__restrict__ defer) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const Grid g = read_grid(gw);
@@ -225,35 +286,19 @@ __global__ void __launch_bounds__(128) knn_dense_kernel(int n, const int32_t *__
     const int i = __float_as_int(me.w);
     const double px = me.x, py = me.y, pz = me.z;
     const double4 ni = nrm[t];
-    double bd[K];
-    int bj[K];
-#pragma unroll
-    for (int s = 0; s < K; ++s) { bd[s] = INFINITY; bj[s] = 0x7fffffff; }
-    double any_d = INFINITY;  // nearest other surfel of any orientation (the fallback scale)
-    int any_j = 0x7fffffff;
+    TopK<K> tk;
+    tk.init();
     const int cx = gaxis(px, g.ox, g.cell, g.dim), cy = gaxis(py, g.oy, g.cell, g.dim), cz = gaxis(pz, g.oz, g.cell, g.dim);
     auto visit_cell = [&](int cid) {
         const int s1 = __ldg(starts + cid + 1);
-        for (int s = __ldg(starts + cid); s < s1; ++s) {
-            const float4 c = __ldg(pk + s);
-            const int j = __float_as_int(c.w);
-            if (j == i) continue;
-            const double d = sqdist(px, py, pz, c);
-            if (before(d, j, any_d, any_j)) { any_d = d; any_j = j; }
-            if (!before(d, j, bd[K - 1], bj[K - 1])) continue;
-            const double4 nj = nrm[s];
-            if (!(__dadd_rn(__dadd_rn(__dmul_rn(ni.x, nj.x), __dmul_rn(ni.y, nj.y)), __dmul_rn(ni.z, nj.z)) > 0.0))
-                continue;
-            // unrolled insertion (from the back: bd[s - 1] is still the old value)
-#pragma unroll
-            for (int m = K - 1; m >= 0; --m) {
-                if (before(d, j, bd[m], bj[m])) {
-                    if (m > 0 && before(d, j, bd[m - 1], bj[m - 1])) { bd[m] = bd[m - 1]; bj[m] = bj[m - 1]; }
-                    else { bd[m] = d; bj[m] = j; }
-                }
-            }
-        }
+        for (int s = __ldg(starts + cid); s < s1; ++s) tk.visit(i, px, py, pz, ni, __ldg(pk + s), nrm, s);
     };
+    // distances from the query to its own cell's faces (the block of shell r
+    // extends r cells beyond them); faces on the grid boundary bound nothing
+    const double cl = g.cell;
+    const double fxl = px - ((double)g.ox + cx * cl), fxh = ((double)g.ox + (cx + 1) * cl) - px;
+    const double fyl = py - ((double)g.oy + cy * cl), fyh = ((double)g.oy + (cy + 1) * cl) - py;
+    const double fzl = pz - ((double)g.oz + cz * cl), fzh = ((double)g.oz + (cz + 1) * cl) - pz;
     for (int r = 0;; ++r) {
         const int x0 = cx - r, x1 = cx + r, y0 = cy - r, y1 = cy + r, z0 = cz - r, z1 = cz + r;
         for (int x = max(x0, 0); x <= min(x1, g.dim - 1); ++x)
@@ -266,22 +311,168 @@ __global__ void __launch_bounds__(128) knn_dense_kernel(int n, const int32_t *__
                     if (z1 < g.dim && z1 != z0) visit_cell(base + z1);
                 }
             }
-        // every unvisited surfel lies more than r cells (r * cell) away
         const bool covered = x0 <= 0 && y0 <= 0 && z0 <= 0 && x1 >= g.dim - 1 && y1 >= g.dim - 1 && z1 >= g.dim - 1;
         if (covered) break;
-        // a full row whose k-th distance is within reach is final (a short
-        // row keeps searching, like knn.py:60-63)
-        if (bj[K - 1] != 0x7fffffff && __dsqrt_rn(bd[K - 1]) <= (double)r * (double)g.cell) break;
+        // every unvisited surfel lies beyond an interior face of the visited
+        // (2r+1)^3 block: at least `reach` away (shrunk by a relative 1e-9 for
+        // the rounding of the cell assignment).  A full row whose k-th
+        // distance is strictly below it is final (ties could still prefer an
+        // unvisited lower index); a short row keeps searching, like knn.py:60-63
+        double reach = INFINITY;
+        if (x0 > 0) reach = fmin(reach, fxl);
+        if (x1 < g.dim - 1) reach = fmin(reach, fxh);
+        if (y0 > 0) reach = fmin(reach, fyl);
+        if (y1 < g.dim - 1) reach = fmin(reach, fyh);
+        if (z0 > 0) reach = fmin(reach, fzl);
+        if (z1 < g.dim - 1) reach = fmin(reach, fzh);
+        reach = (reach + r * cl) * (1.0 - 1e-9);
+        if (tk.full() && tk.bd[K - 1] < reach * reach) break;
+        if (r == kMaxShell) {  // far k-th neighbour: the whole-cloud pass
+            defer[2 + atomicAdd(defer, 1)] = t;
+            return;
+        }
     }
-    double sum = 0.0;
-    int cnt = 0;
+    tk.write(i, neighbors, mean_dist);
+}
+
+// Deferred queries, one CTA each (taken by a work counter), on a COARSE
+// grid of the same centres (cells 4x wider: a far k-th neighbour is a few
+// coarse shells away instead of tens of fine ones).  The CTA's threads split
+// each shell's cells (the six faces of the (2r+1)^3 block, flattened), keep
+// thread-local rows, stop once the smallest thread-local k-th distance lies
+// strictly inside the shell's reach (the row's k-th distance can only be
+// smaller), and merge the rows pairwise in shared memory in the same
+// (distance, index) order -- the row equals the fine search's.
+template <int K> __host__ __device__ constexpr int far_threads() { return K > 8 ? 128 : 256; }
+
+// cell of shell r >= 1 number e (0 <= e < 24 r^2 + 2) around (cx, cy, cz)
+__device__ __forceinline__ void shell_cell(int r, int e, int cx, int cy, int cz, int &x, int &y, int &z) {
+    const int side = 2 * r + 1, inner = 2 * r - 1;
+    if (e < 2 * side * side) {  // the two z faces
+        const int f = e / (side * side), rem = e - f * side * side;
+        x = cx - r + rem / side; y = cy - r + rem % side; z = f ? cz + r : cz - r;
+        return;
+    }
+    e -= 2 * side * side;
+    if (e < 2 * side * inner) {  // the two y faces (z inside)
+        const int f = e / (side * inner), rem = e - f * side * inner;
+        x = cx - r + rem / inner; z = cz - r + 1 + rem % inner; y = f ? cy + r : cy - r;
+        return;
+    }
+    e -= 2 * side * inner;  // the two x faces (y, z inside)
+    const int f = e / (inner * inner), rem = e - f * inner * inner;
+    y = cy - r + 1 + rem / inner; z = cz - r + 1 + rem % inner; x = f ? cx + r : cx - r;
+}
+
+template <int K>
+__global__ void __launch_bounds__(far_threads<K>()) knn_far_kernel(const float4 *__restrict__ pk,
+                                                                   const double4 *__restrict__ nrm,
+                                                                   const int32_t *__restrict__ gwc,
+                                                                   const float4 *__restrict__ pkc,
+                                                                   const double4 *__restrict__ nrmc,
+                                                                   int64_t *__restrict__ neighbors,
+                                                                   double *__restrict__ mean_dist,
+                                                                   int32_t *__restrict__ defer) {
+    constexpr int NT = far_threads<K>();
+    __shared__ double sd[NT][K + 1];
+    __shared__ int sj[NT][K + 1];
+    __shared__ double s_min[NT / 32];
+    __shared__ int s_q;
+    const Grid g = read_grid(gwc);
+    const int32_t *starts = gwc + 16;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_q = atomicAdd(defer + 1, 1);
+        __syncthreads();
+        const int q = s_q;
+        if (q >= defer[0]) return;
+        const int t = defer[2 + q];
+        const float4 me = __ldg(pk + t);
+        const int i = __float_as_int(me.w);
+        const double px = me.x, py = me.y, pz = me.z;
+        const double4 ni = nrm[t];
+        TopK<K> tk;
+        tk.init();
+        auto visit_cell = [&](int cid) {
+            const int s1 = __ldg(starts + cid + 1);
+            for (int s = __ldg(starts + cid); s < s1; ++s) tk.visit(i, px, py, pz, ni, __ldg(pkc + s), nrmc, s);
+        };
+        const int cx = gaxis(px, g.ox, g.cell, g.dim), cy = gaxis(py, g.oy, g.cell, g.dim),
+                  cz = gaxis(pz, g.oz, g.cell, g.dim);
+        const double cl = g.cell;
+        const double fxl = px - ((double)g.ox + cx * cl), fxh = ((double)g.ox + (cx + 1) * cl) - px;
+        const double fyl = py - ((double)g.oy + cy * cl), fyh = ((double)g.oy + (cy + 1) * cl) - py;
+        const double fzl = pz - ((double)g.oz + cz * cl), fzh = ((double)g.oz + (cz + 1) * cl) - pz;
+        for (int r = 0;; ++r) {
+            if (r == 0) {
+                if (threadIdx.x == 0) visit_cell((cx * g.dim + cy) * g.dim + cz);
+            } else {
+                const int ncell = 24 * r * r + 2;
+                for (int e = threadIdx.x; e < ncell; e += NT) {
+                    int x, y, z;
+                    shell_cell(r, e, cx, cy, cz, x, y, z);
+                    if (x >= 0 && y >= 0 && z >= 0 && x < g.dim && y < g.dim && z < g.dim)
+                        visit_cell((x * g.dim + y) * g.dim + z);
+                }
+            }
+            const int x0 = cx - r, x1 = cx + r, y0 = cy - r, y1 = cy + r, z0 = cz - r, z1 = cz + r;
+            if (x0 <= 0 && y0 <= 0 && z0 <= 0 && x1 >= g.dim - 1 && y1 >= g.dim - 1 && z1 >= g.dim - 1) break;
+            double reach = INFINITY;
+            if (x0 > 0) reach = fmin(reach, fxl);
+            if (x1 < g.dim - 1) reach = fmin(reach, fxh);
+            if (y0 > 0) reach = fmin(reach, fyl);
+            if (y1 < g.dim - 1) reach = fmin(reach, fyh);
+            if (z0 > 0) reach = fmin(reach, fzl);
+            if (z1 < g.dim - 1) reach = fmin(reach, fzh);
+            reach = (reach + r * cl) * (1.0 - 1e-9);
+            double m = tk.full() ? tk.bd[K - 1] : INFINITY;
 #pragma unroll
-    for (int s = 0; s < K; ++s) {
-        const bool ok = bj[s] != 0x7fffffff;
-        neighbors[(size_t)i * K + s] = ok ? (int64_t)bj[s] : (int64_t)-1;
-        if (ok) { sum += __dsqrt_rn(bd[s]); ++cnt; }
+            for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) s_min[wid] = m;
+            __syncthreads();
+            double mm = s_min[0];
+#pragma unroll
+            for (int w = 1; w < NT / 32; ++w) mm = fmin(mm, s_min[w]);
+            __syncthreads();
+            if (mm < reach * reach) break;
+        }
+#pragma unroll
+        for (int m = 0; m < K; ++m) { sd[threadIdx.x][m] = tk.bd[m]; sj[threadIdx.x][m] = tk.bj[m]; }
+        sd[threadIdx.x][K] = tk.any_d;
+        sj[threadIdx.x][K] = tk.any_j;
+        for (int half = NT / 2; half > 0; half >>= 1) {
+            __syncthreads();
+            if (threadIdx.x < half) {  // merge row threadIdx.x + half into row threadIdx.x
+                const int o = threadIdx.x + half;
+                double md[K];
+                int mj[K];
+                int a = 0, b = 0;
+#pragma unroll
+                for (int m = 0; m < K; ++m) {
+                    const bool ta = before(sd[threadIdx.x][a], sj[threadIdx.x][a], sd[o][b], sj[o][b]);
+                    md[m] = ta ? sd[threadIdx.x][a] : sd[o][b];
+                    mj[m] = ta ? sj[threadIdx.x][a] : sj[o][b];
+                    a += ta;
+                    b += !ta;
+                }
+#pragma unroll
+                for (int m = 0; m < K; ++m) { sd[threadIdx.x][m] = md[m]; sj[threadIdx.x][m] = mj[m]; }
+                if (before(sd[o][K], sj[o][K], sd[threadIdx.x][K], sj[threadIdx.x][K])) {
+                    sd[threadIdx.x][K] = sd[o][K];
+                    sj[threadIdx.x][K] = sj[o][K];
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int m = 0; m < K; ++m) { tk.bd[m] = sd[0][m]; tk.bj[m] = sj[0][m]; }
+            tk.any_d = sd[0][K];
+            tk.any_j = sj[0][K];
+            tk.write(i, neighbors, mean_dist);
+        }
     }
-    mean_dist[i] = cnt > 0 ? sum / cnt : __dsqrt_rn(any_d);
 }
 
 // ---- isolation (densify.py:118-123) on the dense grid ----------------------
@@ -377,22 +568,38 @@ static const float4 *grid_packed(const int32_t *grid, int n, int dim) {
 }
 
 template <int K>
-static void launch_knn(int n, const int32_t *grid, const float4 *pk, const double4 *nrm, int64_t *neighbors,
-                       double *mean_dist, cudaStream_t s) {
-    knn_dense_kernel<K><<<(n + 127) / 128, 128, 0, s>>>(n, grid, pk, nrm, neighbors, mean_dist);
+static void launch_knn(int n, const int32_t *grid, const float4 *pk, const double4 *nrm, const int32_t *gridc,
+                       const float4 *pkc, const double4 *nrmc, int64_t *neighbors, double *mean_dist, int32_t *defer,
+                       cudaStream_t s) {
+    knn_dense_kernel<K><<<(n + 127) / 128, 128, 0, s>>>(n, grid, pk, nrm, neighbors, mean_dist, defer);
+    knn_far_kernel<K><<<ss_sm_count() * 4, far_threads<K>(), 0, s>>>(pk, nrm, gridc, pkc, nrmc, neighbors, mean_dist,
+                                                                    defer);
 }
 
-extern "C" int ss_knn_dense(int n, const float *centers, const float *quats, const int32_t *grid, int dim, int k,
-                            double *normals_ws, int64_t *neighbors, double *mean_dist, void *stream) {
+extern "C" size_t ss_knn_workspace_bytes(int n) {
+    if (n < 0) return 0;
+    // the fine and the coarse grid's cell-ordered float64 normals (32 B each),
+    // then the deferred-query list (2 counters + n)
+    return 64 * (size_t)n + 4 * ((size_t)n + 2);
+}
+
+extern "C" int ss_knn_dense(int n, const float *centers, const float *quats, const int32_t *grid, int dim,
+                            const int32_t *grid_coarse, int dim_coarse, int k, void *workspace, int64_t *neighbors,
+                            double *mean_dist, void *stream) {
     if (n < 0 || k < 1 || k > kMaxK || dim < 1 || dim > 512 || !grid) return SS_ERR_INVALID;
+    if (dim_coarse < 1 || dim_coarse > 512 || !grid_coarse) return SS_ERR_INVALID;
     if (n == 0) return SS_OK;
-    if (!centers || !quats || !normals_ws || !neighbors || !mean_dist) return SS_ERR_INVALID;
+    if (!centers || !quats || !workspace || !neighbors || !mean_dist) return SS_ERR_INVALID;
     cudaStream_t s = (cudaStream_t)stream;
-    double4 *nrm = reinterpret_cast<double4 *>(normals_ws);
+    double4 *nrm = reinterpret_cast<double4 *>(workspace), *nrmc = nrm + n;
+    int32_t *defer = reinterpret_cast<int32_t *>(nrmc + n);
+    cudaMemsetAsync(defer, 0, 2 * sizeof(int32_t), s);
     knn_normals_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, quats, grid_order(grid, n, dim), nrm);
-    const float4 *pk = grid_packed(grid, n, dim);
+    knn_normals_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, quats, grid_order(grid_coarse, n, dim_coarse), nrmc);
+    const float4 *pk = grid_packed(grid, n, dim), *pkc = grid_packed(grid_coarse, n, dim_coarse);
     switch (k) {
-#define SS_KNN_CASE(K) case K: launch_knn<K>(n, grid, pk, nrm, neighbors, mean_dist, s); break;
+#define SS_KNN_CASE(K) \
+    case K: launch_knn<K>(n, grid, pk, nrm, grid_coarse, pkc, nrmc, neighbors, mean_dist, defer, s); break;
         SS_KNN_CASE(1) SS_KNN_CASE(2) SS_KNN_CASE(3) SS_KNN_CASE(4) SS_KNN_CASE(5) SS_KNN_CASE(6)
         SS_KNN_CASE(7) SS_KNN_CASE(8) SS_KNN_CASE(9) SS_KNN_CASE(10) SS_KNN_CASE(11) SS_KNN_CASE(12)
         SS_KNN_CASE(13) SS_KNN_CASE(14) SS_KNN_CASE(15) SS_KNN_CASE(16)

@@ -35,8 +35,13 @@ class NeighborIndex:
             return
         lib = _lib.load()
         grid, dim = _lib.cell_grid(cloud.centers, n)
-        normals = torch.empty((n, 4), device=dev, dtype=torch.float64)  # cell-ordered normals (scratch)
-        _lib.check(lib.ss_knn_dense(n, _lib.ptr(cloud.centers), _lib.ptr(cloud.quats), _lib.ptr(grid), dim, k,
-                                    _lib.ptr(normals), _lib.ptr(self.neighbors), _lib.ptr(self.mean_dist),
+        # coarse grid (4x wider cells) for the queries whose k-th oriented
+        # neighbour lies far away
+        gridc, dimc = _lib.cell_grid(cloud.centers, n, dim=max(1, dim // 4))
+        # cell-ordered normals + the deferred-query list (scratch)
+        ws = torch.empty((int(lib.ss_knn_workspace_bytes(n)) + 7) // 8, device=dev, dtype=torch.float64)
+        _lib.check(lib.ss_knn_dense(n, _lib.ptr(cloud.centers), _lib.ptr(cloud.quats), _lib.ptr(grid), dim,
+                                    _lib.ptr(gridc), dimc, k,
+                                    _lib.ptr(ws), _lib.ptr(self.neighbors), _lib.ptr(self.mean_dist),
                                     _lib.stream_ptr()),
                    "ss_knn_dense")

@@ -53,10 +53,29 @@ def test_knn_matches_oracle(k):
     assert grad_close(gq, rg, rel=1e-6, floor=1e-7)[0] == 0
 
 
-def test_knn_full_size_rows():
-    """1M surfels (BASELINE config 2 geometry): sampled rows equal a GPU brute
-    force over all surfels."""
-    g = scenes.config2(0, 1_000_000)
+@pytest.mark.parametrize("k", [8, 16])
+def test_knn_deferred_queries_match_oracle(k):
+    """Surfels facing against their surroundings have their oriented
+    neighbours far away: those queries leave the shell search for the
+    whole-cloud pass (knn_brute_kernel); rows still equal the oracle's."""
+    g = scenes.config2(4, 4000)
+    q = g["quats"].copy()
+    flip = np.random.default_rng(3).choice(len(q), 25, replace=False)
+    w, x, y, z = q[flip].T
+    q[flip] = np.stack([-x, w, z, -y], 1)  # q * (0, 1, 0, 0): the normal reversed
+    g["quats"] = q.astype(np.float32)
+    idx = ss.NeighborIndex(ss.SurfelCloud(**g), k=k)
+    nb, md = O.knn_oriented(g["centers"], g["quats"], k=k)
+    np.testing.assert_array_equal(host(idx.neighbors), nb)
+    np.testing.assert_allclose(host(idx.mean_dist), md, rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("n,amp,octaves", [(1_000_000, 0.08, 3), (4_000_000, 0.12, 5)])
+def test_knn_full_size_rows(n, amp, octaves):
+    """1M surfels (BASELINE config 2 geometry) and 4M (config 4: the grid's
+    dim cap, 408 cells per axis): sampled rows equal a GPU brute force over
+    all surfels."""
+    g = scenes.config2(0, n, amp=amp, octaves=octaves)
     cl = ss.SurfelCloud(**g)
     idx = ss.NeighborIndex(cl, k=8)
     c = cl.centers.double()
