@@ -130,6 +130,24 @@ int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessO
                   float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
                   uint32_t *bininfo, const SsProjAux *aux, int32_t *flags, void *stream);
 
+/* ---- per-step surfel prepass ----------------------------------------------
+ * The view-independent part of ss_preprocess for one optimisation step
+ * (every view of a step sees the same parameters): the float32 scaled
+ * tangent frame (quat_to_frame and exp(log_scales), surfels.py:40-51,
+ * preprocess.py:38-60), the finiteness test, and -- with the float64 env maps
+ * -- the float64 activations, normal and diffuse lookup of shade_surfels
+ * (shading.py:463-471).  `prepass`: ss_surfel_prepass_bytes(n) of caller
+ * scratch, 16-byte aligned.  ss_preprocess_prepared is ss_preprocess reading
+ * it instead of recomputing: records, colours and branch state are
+ * bit-identical. */
+size_t ss_surfel_prepass_bytes(int n);
+int ss_surfel_prepass(const SsCloud *cloud, const SsEnv *env, void *prepass, void *stream);
+int ss_preprocess_prepared(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                           int color_source, const float *colors_in, const SsEnv *env,
+                           float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
+                           uint32_t *bininfo, const SsProjAux *aux, int32_t *flags, const void *prepass,
+                           void *stream);
+
 /* ---- records from a ProjectedSurfels ---------------------------------------
  * render(..., proj=P) reuse and bin_and_sort(P) (rasterizer.py:92-116,
  * :331-339): packs the k compacted rows of a ProjectedSurfels (t1, t2, t4,

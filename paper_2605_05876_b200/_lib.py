@@ -72,6 +72,9 @@ _lib = None
 
 _SIGNATURES = {
     "ss_preprocess": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_preprocess_prepared": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_surfel_prepass_bytes": [ctypes.c_int],
+    "ss_surfel_prepass": [c_p, c_p, c_p, c_p],
     "ss_pack_records": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_int,
                         ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_bin_sort": [ctypes.c_int, c_p, c_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p,
@@ -166,6 +169,7 @@ def load(require_cuda=True):
         lib.ss_env_khat_words.restype = ctypes.c_size_t
         lib.ss_refine_workspace_bytes.restype = ctypes.c_size_t
         lib.ss_cell_grid_words.restype = ctypes.c_size_t
+        lib.ss_surfel_prepass_bytes.restype = ctypes.c_size_t
         lib.ss_knn_workspace_bytes.restype = ctypes.c_size_t
         lib.ss_last_error.restype = ctypes.c_char_p
         lib.ss_version.restype = ctypes.c_int

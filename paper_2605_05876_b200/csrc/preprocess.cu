@@ -33,6 +33,72 @@ struct CamF {
     int W, H;
 };
 
+// View-independent per-surfel state of one optimisation step
+// (ss_surfel_prepass): the float32 scaled tangent frame and the float64
+// shading inputs plus the diffuse lookup, computed once per step instead of
+// once per view, with exactly the preprocess kernel's operations (this file
+// is compiled with -fmad=false), so the records are bit-identical.
+struct PreGeom {
+    float su0, su1, su2, sv0;
+    float sv1, sv2;
+    int finite, zero_norm;
+};
+struct PreShade {
+    double n[3], l_d[3];
+    float alb[3], m, r;
+    uint32_t cell;   // diffuse cell i0 | j0 << 16
+    uint32_t dv_ok;  // diffuse dv_ok
+    uint32_t pad;
+};
+static_assert(sizeof(PreGeom) == 32 && sizeof(PreShade) == 80, "prepass layout");
+
+// quat_to_frame + exp(log_scales) in float32 (surfels.py:40-51), the
+// preprocess kernel's expressions
+__device__ __forceinline__ void scaled_frame(float4 q, float2 ls, float &nrm, float s[6]) {
+    nrm = sqrtf(((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w);
+    float w = q.x / nrm, x = q.y / nrm, y = q.z / nrm, z = q.w / nrm;
+    float uh0 = 1.0f - 2.0f * (y * y + z * z), uh1 = 2.0f * (x * y + w * z), uh2 = 2.0f * (x * z - w * y);
+    float vh0 = 2.0f * (x * y - w * z), vh1 = 1.0f - 2.0f * (x * x + z * z), vh2 = 2.0f * (y * z + w * x);
+    // numpy's float32 exp is a SIMD kernel; the correctly rounded value is the
+    // documented stand-in (oracle/ss_oracle.c does the same).
+    float su = (float)exp((double)ls.x), sv = (float)exp((double)ls.y);
+    s[0] = su * uh0; s[1] = su * uh1; s[2] = su * uh2;
+    s[3] = sv * vh0; s[4] = sv * vh1; s[5] = sv * vh2;
+}
+
+__global__ void __launch_bounds__(256) surfel_prepass_kernel(SsCloud cloud, SsEnv env, int shade,
+                                                             PreGeom *__restrict__ geom,
+                                                             PreShade *__restrict__ sh) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cloud.n) return;
+    const float4 q = reinterpret_cast<const float4 *>(cloud.quats)[i];
+    const float2 ls = reinterpret_cast<const float2 *>(cloud.log_scales)[i];
+    const bool finite = isfinite(cloud.centers[3 * i]) && isfinite(cloud.centers[3 * i + 1]) &&
+                        isfinite(cloud.centers[3 * i + 2]) && isfinite(q.x) && isfinite(q.y) && isfinite(q.z) &&
+                        isfinite(q.w) && isfinite(ls.x) && isfinite(ls.y) && isfinite(cloud.albedo_raw[3 * i]) &&
+                        isfinite(cloud.albedo_raw[3 * i + 1]) && isfinite(cloud.albedo_raw[3 * i + 2]) &&
+                        isfinite(cloud.metallic_raw[i]) && isfinite(cloud.roughness_raw[i]);
+    float nrm, f[6];
+    scaled_frame(q, ls, nrm, f);
+    PreGeom g;
+    g.su0 = f[0]; g.su1 = f[1]; g.su2 = f[2]; g.sv0 = f[3]; g.sv1 = f[4]; g.sv2 = f[5];
+    g.finite = finite;
+    g.zero_norm = nrm == 0.0f;
+    geom[i] = g;
+    if (!shade) return;
+    ShadeIn<double> in;
+    ss_shade_material(cloud, i, in);
+    SsBil<double> bd;
+    PreShade o;
+    ss_shade_diffuse(in.n, env, bd, o.l_d);
+    for (int c = 0; c < 3; ++c) { o.n[c] = in.n[c]; o.alb[c] = (float)in.albedo[c]; }
+    o.m = (float)in.m; o.r = (float)in.r;
+    o.cell = (unsigned)bd.i0 | ((unsigned)bd.j0 << 16);
+    o.dv_ok = bd.dv_ok;
+    o.pad = 0;
+    sh[i] = o;
+}
+
 #ifndef SS_PRE_MINB
 #define SS_PRE_MINB 3  // 80 registers, 3 CTAs per SM (small spill, better latency hiding)
 #endif
@@ -40,33 +106,34 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
     SsCloud cloud, CamF cam, SsPreprocessOpts opt, int color_source, const float *__restrict__ colors_in,
     SsEnv env, SsRecord *__restrict__ records, int8_t *__restrict__ cull_out,
     int32_t *__restrict__ pair_count, int32_t *__restrict__ tile_counts, uint4 *__restrict__ bininfo, SsProjAux aux,
-    int32_t *__restrict__ flags)
+    int32_t *__restrict__ flags, const PreGeom *__restrict__ pre_geom, const PreShade *__restrict__ pre_shade)
 {
     const int i_raw = blockIdx.x * blockDim.x + threadIdx.x;
     const bool in_range = i_raw < cloud.n;
     const int i = in_range ? i_raw : cloud.n - 1;  // tail lanes recompute the last row, write nothing
     const float c0 = cloud.centers[3 * i], c1 = cloud.centers[3 * i + 1], c2 = cloud.centers[3 * i + 2];
-    const float4 q = reinterpret_cast<const float4 *>(cloud.quats)[i];
-    const float2 ls = reinterpret_cast<const float2 *>(cloud.log_scales)[i];
-    const float ar0 = cloud.albedo_raw[3 * i], ar1 = cloud.albedo_raw[3 * i + 1], ar2 = cloud.albedo_raw[3 * i + 2];
-    const float mr = cloud.metallic_raw[i], rr = cloud.roughness_raw[i];
-
-    bool finite = in_range && isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(q.x) && isfinite(q.y) &&
-                  isfinite(q.z) && isfinite(q.w) && isfinite(ls.x) && isfinite(ls.y) && isfinite(ar0) &&
-                  isfinite(ar1) && isfinite(ar2) && isfinite(mr) && isfinite(rr);
+    float su0, su1, su2, sv0, sv1, sv2;
+    bool finite;
+    if (pre_geom) {  // this step's prepass (ss_surfel_prepass)
+        const PreGeom g = pre_geom[i];
+        su0 = g.su0; su1 = g.su1; su2 = g.su2; sv0 = g.sv0; sv1 = g.sv1; sv2 = g.sv2;
+        finite = in_range && g.finite;
+        if (in_range && g.zero_norm) atomicOr(&flags[0], 1);
+    } else {
+        const float4 q = reinterpret_cast<const float4 *>(cloud.quats)[i];
+        const float2 ls = reinterpret_cast<const float2 *>(cloud.log_scales)[i];
+        finite = in_range && isfinite(c0) && isfinite(c1) && isfinite(c2) && isfinite(q.x) && isfinite(q.y) &&
+                 isfinite(q.z) && isfinite(q.w) && isfinite(ls.x) && isfinite(ls.y) &&
+                 isfinite(cloud.albedo_raw[3 * i]) && isfinite(cloud.albedo_raw[3 * i + 1]) &&
+                 isfinite(cloud.albedo_raw[3 * i + 2]) && isfinite(cloud.metallic_raw[i]) &&
+                 isfinite(cloud.roughness_raw[i]);
+        // quat_to_frame in float32 (surfels.py:40-51)
+        float nrm, f[6];
+        scaled_frame(q, ls, nrm, f);
+        if (in_range && nrm == 0.0f) atomicOr(&flags[0], 1);
+        su0 = f[0]; su1 = f[1]; su2 = f[2]; sv0 = f[3]; sv1 = f[4]; sv2 = f[5];
+    }
     int code = finite ? 0 : 1;
-
-    // quat_to_frame in float32 (surfels.py:40-51)
-    float nrm = sqrtf(((q.x * q.x + q.y * q.y) + q.z * q.z) + q.w * q.w);
-    if (in_range && nrm == 0.0f) atomicOr(&flags[0], 1);
-    float w = q.x / nrm, x = q.y / nrm, y = q.z / nrm, z = q.w / nrm;
-    float uh0 = 1.0f - 2.0f * (y * y + z * z), uh1 = 2.0f * (x * y + w * z), uh2 = 2.0f * (x * z - w * y);
-    float vh0 = 2.0f * (x * y - w * z), vh1 = 1.0f - 2.0f * (x * x + z * z), vh2 = 2.0f * (y * z + w * x);
-    // numpy's float32 exp is a SIMD kernel; the correctly rounded value is the
-    // documented stand-in (oracle/ss_oracle.c does the same).
-    float su = (float)exp((double)ls.x), sv = (float)exp((double)ls.y);
-    float su0 = su * uh0, su1 = su * uh1, su2 = su * uh2;
-    float sv0 = sv * vh0, sv1 = sv * vh1, sv2 = sv * vh2;
     float cc[3], tu[3], tv[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
@@ -158,10 +225,28 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
         col[0] = colors_in[3 * i]; col[1] = colors_in[3 * i + 1]; col[2] = colors_in[3 * i + 2];
 #ifdef SS_EXP_NO_SHADE
     } else if (true) {
-        col[0] = ss_sigmoid_f32(ar0); col[1] = ss_sigmoid_f32(ar1); col[2] = ss_sigmoid_f32(ar2);
+        col[0] = ss_sigmoid_f32(cloud.albedo_raw[3 * i]); col[1] = ss_sigmoid_f32(cloud.albedo_raw[3 * i + 1]);
+    col[2] = ss_sigmoid_f32(cloud.albedo_raw[3 * i + 2]);
 #endif
     } else if (color_source == SS_COLOR_ALBEDO) {
-        col[0] = ss_sigmoid_f32(ar0); col[1] = ss_sigmoid_f32(ar1); col[2] = ss_sigmoid_f32(ar2);
+        col[0] = ss_sigmoid_f32(cloud.albedo_raw[3 * i]); col[1] = ss_sigmoid_f32(cloud.albedo_raw[3 * i + 1]);
+        col[2] = ss_sigmoid_f32(cloud.albedo_raw[3 * i + 2]);
+    } else if (color_source == SS_COLOR_IBL && pre_shade) {
+        // materials, normal and the diffuse lookup from this step's prepass
+        const PreShade &ps = pre_shade[i];
+        ShadeIn<double> in;
+        for (int c = 0; c < 3; ++c) { in.n[c] = ps.n[c]; in.albedo[c] = (double)ps.alb[c]; }
+        in.m = (double)ps.m; in.r = (double)ps.r;
+        ss_shade_view(cloud, i, cam.cam_pos, in);
+        ShadeState<double> st;
+        for (int c = 0; c < 3; ++c) st.l_d[c] = ps.l_d[c];
+        st.bd.i0 = (int)(ps.cell & 0xffffu); st.bd.j0 = (int)(ps.cell >> 16);
+        st.bd.du_ok = true; st.bd.dv_ok = ps.dv_ok != 0;
+        double out[3];
+        ss_shade_forward_view(in, env, st, out);
+        col[0] = (float)out[0]; col[1] = (float)out[1]; col[2] = (float)out[2];
+        if (aux.cells) ss_shade_cells(st, env, aux.cells + 15 * i);
+        if (aux.cells_packed && in_range) reinterpret_cast<uint4 *>(aux.cells_packed)[i] = ss_shade_pack(st);
     } else if (color_source == SS_COLOR_IBL_F32) {
         ShadeIn<float> in;
         ss_shade_inputs(cloud, i, cam.cam_pos, in);
@@ -295,10 +380,28 @@ extern "C" int ss_pack_records(int k, const float *t1, const float *t2, const fl
     return SS_OK;
 }
 
-extern "C" int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
-                             int color_source, const float *colors_in, const SsEnv *env,
-                             float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
-                             uint32_t *bininfo, const SsProjAux *aux, int32_t *flags, void *stream)
+extern "C" size_t ss_surfel_prepass_bytes(int n) {
+    return n < 0 ? 0 : (sizeof(PreGeom) + sizeof(PreShade)) * (size_t)n;
+}
+
+extern "C" int ss_surfel_prepass(const SsCloud *cloud, const SsEnv *env, void *prepass, void *stream)
+{
+    if (!cloud || !prepass) return SS_ERR_INVALID;
+    if (cloud->n == 0) return SS_OK;
+    const bool shade = env && env->diffuse && env->diffuse64 && env->specular64;
+    PreGeom *g = reinterpret_cast<PreGeom *>(prepass);
+    PreShade *sh = reinterpret_cast<PreShade *>(g + cloud->n);
+    surfel_prepass_kernel<<<(cloud->n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*cloud, env ? *env : SsEnv{},
+                                                                                     shade ? 1 : 0, g, sh);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+static int preprocess_impl(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                           int color_source, const float *colors_in, const SsEnv *env,
+                           float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
+                           uint32_t *bininfo, const SsProjAux *aux, int32_t *flags, const void *prepass,
+                           void *stream)
 {
     if (!cloud || !cam || !opt || !tile_counts || !flags) return SS_ERR_INVALID;
     if (cam->width <= 0 || cam->height <= 0 || opt->tile <= 0) return SS_ERR_INVALID;
@@ -318,9 +421,32 @@ extern "C" int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const Ss
     SsEnv e = env ? *env : SsEnv{};
     SsProjAux a = aux ? *aux : SsProjAux{};
     int blocks = (cloud->n + 255) / 256;
+    const PreGeom *pg = reinterpret_cast<const PreGeom *>(prepass);
+    // the shading part of the prepass is only written with the float64 maps
+    const PreShade *ps = pg && e.diffuse64 && e.specular64 ? reinterpret_cast<const PreShade *>(pg + cloud->n) : nullptr;
     preprocess_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
         *cloud, cf, *opt, color_source, colors_in, e, reinterpret_cast<SsRecord *>(records), cull,
-        pair_count, tile_counts, reinterpret_cast<uint4 *>(bininfo), a, flags);
+        pair_count, tile_counts, reinterpret_cast<uint4 *>(bininfo), a, flags, pg, ps);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
+}
+
+extern "C" int ss_preprocess(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                             int color_source, const float *colors_in, const SsEnv *env,
+                             float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
+                             uint32_t *bininfo, const SsProjAux *aux, int32_t *flags, void *stream)
+{
+    return preprocess_impl(cloud, cam, opt, color_source, colors_in, env, records, cull, pair_count, tile_counts,
+                           bininfo, aux, flags, nullptr, stream);
+}
+
+extern "C" int ss_preprocess_prepared(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                                      int color_source, const float *colors_in, const SsEnv *env,
+                                      float *records, int8_t *cull, int32_t *pair_count, int32_t *tile_counts,
+                                      uint32_t *bininfo, const SsProjAux *aux, int32_t *flags, const void *prepass,
+                                      void *stream)
+{
+    if (!prepass) return SS_ERR_INVALID;
+    return preprocess_impl(cloud, cam, opt, color_source, colors_in, env, records, cull, pair_count, tile_counts,
+                           bininfo, aux, flags, prepass, stream);
 }

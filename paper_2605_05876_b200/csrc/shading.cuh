@@ -222,9 +222,9 @@ struct ShadeState {
     R dgu[3], dgv[3], sgu[2][3], sgv[2][3], lgu[2], lgv[2];
 };
 
-// Activated materials, float64 normal and view direction of surfel i.
+// Activated materials and normal of surfel i (view independent).
 template <typename R>
-__device__ __forceinline__ void ss_shade_inputs(const SsCloud &cloud, int i, const double cam_pos[3], ShadeIn<R> &in) {
+__device__ __forceinline__ void ss_shade_material(const SsCloud &cloud, int i, ShadeIn<R> &in) {
     in.albedo[0] = ss_act<R>(cloud.albedo_raw[3 * i]);
     in.albedo[1] = ss_act<R>(cloud.albedo_raw[3 * i + 1]);
     in.albedo[2] = ss_act<R>(cloud.albedo_raw[3 * i + 2]);
@@ -234,6 +234,11 @@ __device__ __forceinline__ void ss_shade_inputs(const SsCloud &cloud, int i, con
     R nrm = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
     R w = q0 / nrm, x = q1 / nrm, y = q2 / nrm, z = q3 / nrm;
     in.n[0] = 2 * (x * z + w * y); in.n[1] = 2 * (y * z - w * x); in.n[2] = 1 - 2 * (x * x + y * y);
+}
+
+// View direction of surfel i.
+template <typename R>
+__device__ __forceinline__ void ss_shade_view(const SsCloud &cloud, int i, const double cam_pos[3], ShadeIn<R> &in) {
     R tc[3];
     for (int c = 0; c < 3; ++c) tc[c] = cam_pos[c] - (R)cloud.centers[3 * i + c];
     R dist = sqrt((tc[0] * tc[0] + tc[1] * tc[1]) + tc[2] * tc[2]);
@@ -241,23 +246,41 @@ __device__ __forceinline__ void ss_shade_inputs(const SsCloud &cloud, int i, con
     for (int c = 0; c < 3; ++c) in.wo[c] = tc[c] * in.inv_dist;
 }
 
-// shade_surfels body (shading.py:463-488)
+// Activated materials, float64 normal and view direction of surfel i.
 template <typename R>
-__device__ __forceinline__ void ss_shade_forward(const ShadeIn<R> &in, const SsEnv &env, ShadeState<R> &s, R col[3]) {
+__device__ __forceinline__ void ss_shade_inputs(const SsCloud &cloud, int i, const double cam_pos[3], ShadeIn<R> &in) {
+    ss_shade_material(cloud, i, in);
+    ss_shade_view(cloud, i, cam_pos, in);
+}
+
+// The diffuse (irradiance) lookup of shade_surfels (shading.py:469-471):
+// view independent -- TrainStep evaluates it once per step (ss_surfel_prepass).
+template <typename R>
+__device__ __forceinline__ void ss_shade_diffuse(const R n[3], const SsEnv &env, SsBil<R> &bd, R l_d[3]) {
+    const int he = env.he, we = env.we;
+    R fu, fv;
+    ss_dir_coords(n, he, we, fu, fv);
+    bd = ss_bil_prepare<R>(he, we, fu, fv, true);
+    const float4 *d4 = reinterpret_cast<const float4 *>(env.diffuse4);
+    // float64 shading reads the float64 maps (the reference's, shading.py:369-379)
+    const bool m64 = sizeof(R) == 8 && env.diffuse64 && env.specular64;
+    if (m64) ss_bil_lookup<3>(env.diffuse64, we, bd, l_d);
+    else if (d4) ss_bil_lookup4(d4, we, bd, l_d);
+    else ss_bil_lookup<3>(env.diffuse, we, bd, l_d);
+}
+
+// shade_surfels body (shading.py:463-488) after the diffuse lookup (s.bd,
+// s.l_d set): reflection, specular levels, LUT, colour.
+template <typename R>
+__device__ __forceinline__ void ss_shade_forward_view(const ShadeIn<R> &in, const SsEnv &env, ShadeState<R> &s,
+                                                      R col[3]) {
     const int he = env.he, we = env.we, L = env.levels, LR = env.lut_res;
     s.ndv_raw = (in.n[0] * in.wo[0] + in.n[1] * in.wo[1]) + in.n[2] * in.wo[2];
     R ndv = ss_clip<R>(s.ndv_raw, R(0.0), R(1.0));
     for (int c = 0; c < 3; ++c) s.refl[c] = R(2.0) * s.ndv_raw * in.n[c] - in.wo[c];
     R fu, fv;
-    ss_dir_coords(in.n, he, we, fu, fv);
-    s.bd = ss_bil_prepare<R>(he, we, fu, fv, true);
-    const float4 *d4 = reinterpret_cast<const float4 *>(env.diffuse4);
     const float4 *s4 = reinterpret_cast<const float4 *>(env.specular4);
-    // float64 shading reads the float64 maps (the reference's, shading.py:369-379)
     const bool m64 = sizeof(R) == 8 && env.diffuse64 && env.specular64;
-    if (m64) ss_bil_lookup<3>(env.diffuse64, we, s.bd, s.l_d);
-    else if (d4) ss_bil_lookup4(d4, we, s.bd, s.l_d);
-    else ss_bil_lookup<3>(env.diffuse, we, s.bd, s.l_d);
     R lvl = ss_clip<R>(in.r, R(0.0), R(1.0)) * (L - 1);
     int cap = L - 2 > 0 ? L - 2 : 0;
     R fl = floor(lvl);
@@ -287,6 +310,13 @@ __device__ __forceinline__ void ss_shade_forward(const ShadeIn<R> &in, const SsE
         s.k_d[c] = (R(1.0) - s.f0[c]) * (R(1.0) - in.m);
         col[c] = s.k_d[c] * in.albedo[c] * s.l_d[c] + s.l_s[c] * (s.f0[c] * s.b1 + s.b2);
     }
+}
+
+// shade_surfels body (shading.py:463-488)
+template <typename R>
+__device__ __forceinline__ void ss_shade_forward(const ShadeIn<R> &in, const SsEnv &env, ShadeState<R> &s, R col[3]) {
+    ss_shade_diffuse(in.n, env, s.bd, s.l_d);
+    ss_shade_forward_view(in, env, s, col);
 }
 
 // Narrow a float64 forward state to float32: the backward then runs in

@@ -77,7 +77,7 @@ struct SplatParams {
 constexpr int kBigW = SS_ACC64_WIDTH;  // float64 channels per big-record slot (>= NCHC)
 static_assert(kBigW >= 18, "float64 row holds every channel");
 
-constexpr int kHeadWords = 8 + 2 * 64;  // see the scratch layout below
+constexpr int kHeadWords = 8 + 2 * 256;  // see the scratch layout below
 
 __global__ void pixel_ndc_kernel(int W, int H, float *xs, float *ys, int32_t *big_count) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -314,7 +314,7 @@ __device__ __forceinline__ void load_record(const SsRecord *recs, int rec, SsRec
 constexpr int kBigChunk = 1024;
 constexpr int kHugeArea = 8 * kBigChunk;  // big rects above this are spread over the grid
 constexpr int kBigArea = 512;  // rects above this go to the CTA-chunked kernel (~0.1% of records)
-constexpr int kNB = 64;        // area classes of the other records
+constexpr int kNB = 256;       // (area class, coverage-fraction bucket) classes of the other records
 constexpr int kGL = 8;         // lanes per record group (4 records per warp)
 constexpr int kGCap = 128;     // rect pixels compacted per group pass
 #ifndef SS_SPLAT_WARPS
@@ -332,7 +332,7 @@ constexpr int kNdcSmem = 4096;  // W + H up to this: pixel-centre tables staged 
 #define SS_SCAT_ITEMS 8
 #endif
 constexpr int kScatItems = SS_SCAT_ITEMS;  // records per thread of the class scatter
-constexpr int kHeavyClass = 32;  // area >= 64 px: one round per work-counter ticket (else 8)
+constexpr int kHeavyClass = 32 * 4;  // area >= 64 px: one round per work-counter ticket (else 8)
 
 // Scratch layout (32-bit words after the two NDC tables), see
 // ss_train_backward_scratch_words: 8 counters (medium / huge queue sizes,
@@ -350,6 +350,23 @@ __device__ __forceinline__ int area_class(int a) {
 
 __device__ __forceinline__ int rect_area(const int4 &r) {
     return (r.z > r.x && r.w > r.y) ? (r.z - r.x) * (r.w - r.y) : 0;
+}
+
+// Covered fraction of the rect, estimated from the record (the support
+// ellipse rho^2 < 9 has area 9 pi / sqrt(det Sigma^-1) in the tangent plane,
+// mapped by the projection's Jacobian at the centre), in 4 buckets: records
+// of a round then have similar covered counts as well as similar areas
+// (pass 2 runs to the round's largest covered count).
+__device__ __forceinline__ int cover_bucket(const SsRecord &R, int area, int W, int H) {
+    const float t1x = R.a.x, t1y = R.a.y, t1z = R.a.z, t2x = R.a.w, t2y = R.b.x, t2z = R.b.y;
+    const float t4x = R.b.z, t4y = R.b.w, t4z = R.c.x;
+    const float i2 = 1.f / (t4z * t4z);
+    const float jxu = (t1x * t4z - t1z * t4x) * i2, jxv = (t1y * t4z - t1z * t4y) * i2;
+    const float jyu = (t2x * t4z - t2z * t4x) * i2, jyv = (t2y * t4z - t2z * t4y) * i2;
+    const float dets = R.c.y * R.c.w - R.c.z * R.c.z;
+    const float est = 28.274333882f * rsqrtf(fmaxf(dets, 1e-30f)) * fabsf(jxu * jyv - jxv * jyu) * (0.25f * W * H);
+    const float fr = est / (float)max(area, 1);
+    return (fr >= 0.56f) + (fr >= 0.70f) + (fr >= 0.785f);  // (NaN: bucket 0)
 }
 
 // Class every kept record by rect area.  Big rects are queued for
@@ -375,7 +392,10 @@ __global__ void __launch_bounds__(256) area_class_kernel(SplatParams P, uint8_t 
 #pragma unroll
                 for (int i = 0; i < kBigW / 2; ++i) row[i] = make_double2(0.0, 0.0);
             } else {
-                c = (uint8_t)area_class(area);
+                SsRecord R;
+                const float4 *src = reinterpret_cast<const float4 *>(P.records + r);
+                R.a = __ldg(src); R.b = __ldg(src + 1); R.c = __ldg(src + 2);
+                c = (uint8_t)(area_class(area) * 4 + cover_bucket(R, area, P.W, P.H));
                 atomicAdd(&s_hist[c], 1);
             }
         }
@@ -393,7 +413,7 @@ __global__ void __launch_bounds__(256) area_scatter_kernel(int n, const uint8_t 
 {
     __shared__ int s_cnt[kNB], s_base[kNB];
     const int t = threadIdx.x;
-    if (t < kNB) s_cnt[t] = 0;
+    for (int k = t; k < kNB; k += 256) s_cnt[k] = 0;
     __syncthreads();
     const int base = blockIdx.x * 256 * kScatItems;
     int rank[kScatItems], c[kScatItems];
@@ -401,24 +421,31 @@ __global__ void __launch_bounds__(256) area_scatter_kernel(int n, const uint8_t 
     for (int j = 0; j < kScatItems; ++j) {
         const int r = base + j * 256 + t;
         c[j] = r < n ? cls[r] : 0xff;
-        rank[j] = c[j] < kNB ? atomicAdd(&s_cnt[c[j]], 1) : 0;
+        rank[j] = c[j] != 0xff ? atomicAdd(&s_cnt[c[j]], 1) : 0;
     }
     __syncthreads();
     if (t < 32) {
-        // positions 2t, 2t+1 of the descending order are classes 63-2t, 62-2t
-        const int ca = kNB - 1 - 2 * t, cb = ca - 1;
-        const int ha = __ldg(hist + ca), hb = __ldg(hist + cb);
-        int incl = ha + hb;
+        // positions kCpl t .. kCpl t + kCpl - 1 of the descending order are
+        // classes kNB - 1 - kCpl t - j
+        constexpr int kCpl = kNB / 32;
+        int h[kCpl], loc = 0;
+#pragma unroll
+        for (int j = 0; j < kCpl; ++j) { h[j] = __ldg(hist + kNB - 1 - kCpl * t - j); loc += h[j]; }
+        int incl = loc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, o);
             if (t >= o) incl += v;
         }
-        const int excl = incl - ha - hb;
-        s_base[ca] = excl + (s_cnt[ca] ? atomicAdd(cursor + ca, s_cnt[ca]) : 0);
-        s_base[cb] = excl + ha + (s_cnt[cb] ? atomicAdd(cursor + cb, s_cnt[cb]) : 0);
-        // records of class >= kHeavyClass (positions before 2 * 16) are handed out one round at a time
-        const int nheavy = __shfl_sync(0xffffffffu, incl, kNB / 2 - kHeavyClass / 2 - 1);
+        int run = incl - loc;
+#pragma unroll
+        for (int j = 0; j < kCpl; ++j) {
+            const int cj = kNB - 1 - kCpl * t - j;
+            s_base[cj] = run + (s_cnt[cj] ? atomicAdd(cursor + cj, s_cnt[cj]) : 0);
+            run += h[j];
+        }
+        // records of class >= kHeavyClass (the first kNB - kHeavyClass positions) are handed out one round at a time
+        const int nheavy = __shfl_sync(0xffffffffu, incl, (kNB - kHeavyClass) / kCpl - 1);
         if (blockIdx.x == 0 && t == 31) {
             nsmall[0] = incl;
             nsmall[1] = nheavy;
@@ -427,7 +454,7 @@ __global__ void __launch_bounds__(256) area_scatter_kernel(int n, const uint8_t 
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kScatItems; ++j)
-        if (c[j] < kNB) order[s_base[c[j]] + rank[j]] = base + j * 256 + t;
+        if (c[j] != 0xff) order[s_base[c[j]] + rank[j]] = base + j * 256 + t;
 }
 
 struct GroupSmem {

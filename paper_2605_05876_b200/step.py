@@ -281,6 +281,9 @@ class TrainStep:
         self.loss_f = self.pack.loss
         self.view_count = self.pack.view_count
         self._cl = _lib.make_cloud(cloud)
+        # the step's view-independent per-surfel state (ss_surfel_prepass)
+        self._prepass = torch.empty(int(self.lib.ss_surfel_prepass_bytes(self.n)), device=dev, dtype=torch.uint8)
+        self._prepared = False
         for b in self.bufs:
             b.gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
                                 None, _lib.ptr(b.d_diffuse64), _lib.ptr(b.d_spec64),
@@ -340,11 +343,14 @@ class TrainStep:
     def _preprocess(self, cam, b):
         b.tile_counts.zero_()
         camst = _lib.make_camera(cam)
-        rc = self.lib.ss_preprocess(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
-                                    self.color_source, None, ctypes.byref(self._envs), _lib.ptr(b.records),
-                                    _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts), _lib.ptr(b.bininfo),
-                                    ctypes.byref(b.aux) if self.color_source == _lib.SS_COLOR_IBL else None,
-                                    _lib.ptr(b.flags), _lib.stream_ptr())
+        args = (ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po), self.color_source, None,
+                ctypes.byref(self._envs), _lib.ptr(b.records), _lib.ptr(b.cull), None, _lib.ptr(b.tile_counts),
+                _lib.ptr(b.bininfo), ctypes.byref(b.aux) if self.color_source == _lib.SS_COLOR_IBL else None,
+                _lib.ptr(b.flags))
+        if self._prepared:  # inside a step: this step's prepass
+            rc = self.lib.ss_preprocess_prepared(*args, _lib.ptr(self._prepass), _lib.stream_ptr())
+        else:
+            rc = self.lib.ss_preprocess(*args, _lib.stream_ptr())
         _lib.check(rc, "ss_preprocess")
         return camst
 
@@ -471,21 +477,28 @@ class TrainStep:
         """Issue every view, alternating the worker streams (view i uses stream
         and buffers i % S); the streams are independent until the join."""
         main = torch.cuda.current_stream()
+        # the view-independent per-surfel state, once for the step's views
+        _lib.check(self.lib.ss_surfel_prepass(ctypes.byref(self._cl), ctypes.byref(self._envs),
+                                              _lib.ptr(self._prepass), _lib.stream_ptr()), "ss_surfel_prepass")
+        self._prepared = True
         for st in self.streams:
             st.wait_stream(main)
         nst = min(len(self.streams), self.active_streams or len(self.streams))
-        for i, cam in enumerate(cameras):
-            k = i % nst
-            with torch.cuda.stream(self.streams[k]):
-                tgt = targets_for(i, self.streams[k])
-                self.view(cam, tgt, self.bufs[k],
-                                 target_done=None if target_done is None else target_done[i % len(target_done)],
-                                 mask=None if masks is None else masks[i])
-                if self.collect_stats:
-                    b = self.bufs[k]
-                    self._pairs.append(int(b.offsets[-1].item()))
-                    self._kept.append(int((b.cull == 0).sum().item()))
-                    self._layer_px.append(self._view_layer_pixels(b))
+        try:
+            for i, cam in enumerate(cameras):
+                k = i % nst
+                with torch.cuda.stream(self.streams[k]):
+                    tgt = targets_for(i, self.streams[k])
+                    self.view(cam, tgt, self.bufs[k],
+                              target_done=None if target_done is None else target_done[i % len(target_done)],
+                              mask=None if masks is None else masks[i])
+                    if self.collect_stats:
+                        b = self.bufs[k]
+                        self._pairs.append(int(b.offsets[-1].item()))
+                        self._kept.append(int((b.cull == 0).sum().item()))
+                        self._layer_px.append(self._view_layer_pixels(b))
+        finally:
+            self._prepared = False
         for st in self.streams:
             main.wait_stream(st)
         for b in self.bufs[1:nst]:  # the other sets' derived-map sums into the step's
