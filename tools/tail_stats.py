@@ -25,7 +25,7 @@ ts = TrainStep(ss.SurfelCloud(**init), ss.EnvironmentLight(np.log(env_base)), 80
 ts.size_pairs(cams)
 ts.step(cams, targets)
 lib = _lib.load()
-fb = torch.zeros(3 * 50 * 50 * 2, device="cuda", dtype=torch.int64)
+fb = torch.zeros(3 * 50 * 50 * 4, device="cuda", dtype=torch.int64)
 bb = torch.zeros(3 * 148 * 3 * 8 * 2, device="cuda", dtype=torch.int64)
 _lib.check(lib.ss_debug_set_fwd_timing(_lib.ptr(fb)), "set_fwd_timing")
 _lib.check(lib.ss_debug_set_bwd_timing(_lib.ptr(bb)), "set_bwd_timing")
