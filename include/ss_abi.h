@@ -454,6 +454,16 @@ int ss_adam_step_f64(int64_t count, float *param, const float *grad, double *m, 
 int ss_adam_multi_f64(int ntensors, float *const *params, const float *const *grads, double *const *m,
                       double *const *v, const int64_t *counts, const int *steps, const float *lrs,
                       const int *quat_flags, float beta1, float beta2, float eps, void *stream);
+/* ss_adam_multi_master: the same multi-tensor step on float64 MASTER
+ * parameters `masters` (the reference's fit keeps its parameters in float64,
+ * train.py:168-174): the reference's numpy update operation by operation
+ * (adam.py:31-41; c1s / c2s = 1 - beta^t per tensor, lrs in float64),
+ * quaternion segments renormalised in float64 (surfels.py:31-37); `params`
+ * receives the float32 rounding of each updated master value. */
+int ss_adam_multi_master(int ntensors, float *const *params, double *const *masters, const float *const *grads,
+                         double *const *m, double *const *v, const int64_t *counts, const double *c1s,
+                         const double *c2s, const double *lrs, const int *quat_flags, double beta1, double beta2,
+                         double eps, void *stream);
 /* q <- q / |q| after the step (train.py:246). */
 int ss_normalize_quats(int n, float *quats, void *stream);
 
@@ -499,7 +509,7 @@ int ss_split_children(int nsplit, const int32_t *parents, const float *centers, 
  * active, candidates, then the threshold's float64 bits.  workspace:
  * ss_refine_workspace_bytes(n).  No host synchronisation; a fixed launch
  * sequence (order statistics by an 8-bit radix select on the float64 bits).
- * ss_refine_apply: the new rows of up to 20 row-major tensors (src[t] n
+ * ss_refine_apply: the new rows of up to 32 row-major tensors (src[t] n
  * rows, dst[t] capacity >= n_out rows, row_bytes[t] a multiple of 4) by
  * role: 0 children copy the parent row, 1 children zero (Adam moments),
  * 2 centres (children +-(s_max / 2) along the longer tangent axis), 3 log

@@ -74,6 +74,8 @@ _SIGNATURES = {
     "ss_preprocess": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_preprocess_prepared": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_surfel_prepass_bytes": [ctypes.c_int],
+    "ss_adam_multi_master": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_double,
+                             ctypes.c_double, ctypes.c_double, c_p],
     "ss_surfel_prepass": [c_p, c_p, c_p, c_p],
     "ss_pack_records": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int, ctypes.c_int,
                         ctypes.c_int, c_p, c_p, c_p, c_p],

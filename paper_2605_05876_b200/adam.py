@@ -6,6 +6,13 @@ read and written once.  The moments are float64 by default, like the
 reference's numpy state (adam.py:26-28), so checkpoints carry the same
 dtypes; state_dtype=torch.float32 halves their memory and traffic.  The
 update itself is evaluated in float64 per element either way.
+
+master_params=True keeps a float64 master copy of every parameter it steps
+(`p64`), like the reference's fit, which promotes the cloud to float64
+(train.py:168-174): step_multi then runs the reference's numpy update
+operation by operation on the masters (ss_adam_multi_master, float64
+hyper-parameters) and writes the float32 rounding into the tensors the
+kernels read.
 """
 
 from __future__ import annotations
@@ -17,16 +24,22 @@ from . import _lib
 
 
 class Adam:
-    def __init__(self, beta1=0.9, beta2=0.999, eps=1e-15, state_dtype=torch.float64):
+    def __init__(self, beta1=0.9, beta2=0.999, eps=1e-15, state_dtype=torch.float64, master_params=False):
         if state_dtype not in (torch.float64, torch.float32):
             raise ValueError("state_dtype must be torch.float64 or torch.float32")
+        if master_params and state_dtype != torch.float64:
+            raise ValueError("master parameters need float64 moments")
         self.beta1, self.beta2, self.eps = float(beta1), float(beta2), float(eps)
         self.state_dtype = state_dtype
+        self.master_params = bool(master_params)
         self.m: dict[str, torch.Tensor] = {}
         self.v: dict[str, torch.Tensor] = {}
         self.t: dict[str, int] = {}
+        self.p64: dict[str, torch.Tensor] = {}  # float64 masters (master_params)
 
     def step(self, name, param, grad, lr):
+        if self.master_params:
+            return self.step_multi([(name, param, grad, lr)])[0]
         if tuple(grad.shape) != tuple(param.shape):
             raise ValueError(f"gradient shape {tuple(grad.shape)} != param shape {tuple(param.shape)}")
         self._init_state(name, param)
@@ -46,6 +59,15 @@ class Adam:
             self.t[name] = 0
         elif self.m[name].dtype != self.state_dtype:
             raise ValueError(f"optimizer state {name!r} is {self.m[name].dtype}, not {self.state_dtype}")
+        if self.master_params:
+            p = self.p64.get(name)
+            if p is None or p.shape != param.shape:  # first use, or the tensor was replaced
+                self.p64[name] = param.detach().to(torch.float64).contiguous()
+
+    def set_master(self, name, values):
+        """Replace the float64 master of `name` (e.g. a loaded float64
+        checkpoint); the float32 tensor the kernels read is the caller's."""
+        self.p64[name] = torch.as_tensor(values, device="cuda", dtype=torch.float64).contiguous()
 
     def step_multi(self, items, renorm_quats=None):
         """Adam on several tensors in ONE fused launch (csrc/optim.cu
@@ -71,6 +93,17 @@ class Adam:
         k = len(items)
         ptrs = {c: (ctypes.c_void_p * k)(*cols[c]) for c in ("p", "g", "m", "v")}
         lib = _lib.load()
+        if self.master_params:
+            masters = (ctypes.c_void_p * k)(*[self.p64[it[0]].data_ptr() for it in items])
+            # bias corrections exactly as the reference's Python (1.0 - beta ** t)
+            c1 = (ctypes.c_double * k)(*[1.0 - self.beta1 ** t for t in cols["t"]])
+            c2 = (ctypes.c_double * k)(*[1.0 - self.beta2 ** t for t in cols["t"]])
+            rc = lib.ss_adam_multi_master(k, ptrs["p"], masters, ptrs["g"], ptrs["m"], ptrs["v"],
+                                          (ctypes.c_int64 * k)(*cols["n"]), c1, c2, (ctypes.c_double * k)(*cols["lr"]),
+                                          (ctypes.c_int * k)(*cols["q"]), self.beta1, self.beta2, self.eps,
+                                          _lib.stream_ptr())
+            _lib.check(rc, "ss_adam_multi_master")
+            return [it[1] for it in items]
         fn = lib.ss_adam_multi_f64 if self.state_dtype == torch.float64 else lib.ss_adam_multi
         rc = fn(k, ptrs["p"], ptrs["g"], ptrs["m"], ptrs["v"], (ctypes.c_int64 * k)(*cols["n"]),
                 (ctypes.c_int * k)(*cols["t"]), (ctypes.c_float * k)(*cols["lr"]), (ctypes.c_int * k)(*cols["q"]),
@@ -78,8 +111,11 @@ class Adam:
         _lib.check(rc, "ss_adam_multi")
         return [it[1] for it in items]
 
-    def remap(self, name, index):
-        """adam.py:43-58: reindex rows; index -1 rows start from zero."""
+    def remap(self, name, index, param=None):
+        """adam.py:43-58: reindex rows; index -1 rows start from zero.  A float64
+        master (master_params) is reindexed too, its new rows taken from
+        `param` (the float32 tensor after the topology change); without
+        `param` the master is re-seeded from the tensor at the next step."""
         if name not in self.m:
             return
         idx = torch.as_tensor(index, device=self.m[name].device, dtype=torch.int64)
@@ -89,10 +125,17 @@ class Adam:
             new = store[name][src].clone()
             new[~keep] = 0.0
             store[name] = new.contiguous()
+        if name in self.p64:
+            if param is None:
+                del self.p64[name]
+            else:
+                new = self.p64[name][src].clone()
+                new[~keep] = param[~keep].to(torch.float64)
+                self.p64[name] = new.contiguous()
 
-    def remap_all(self, index):
+    def remap_all(self, index, params=None):
         for name in list(self.m):
-            self.remap(name, index)
+            self.remap(name, index, None if params is None else params.get(name))
 
     def state_arrays(self):
         out = {}

@@ -20,8 +20,14 @@ constexpr int kScanThreads = 1024;
 // kSmallCap keys are sorted by a light CTA so several tiles share an SM; the
 // heavier ones by a second launch with a large buffer (each launch skips the
 // other's tiles); beyond kHeavyCap a bitonic network runs in global memory.
-constexpr int kSmallThreads = 256;
-constexpr int kSmallCap = 2048;
+#ifndef SS_SORT_SMALL_THREADS
+#define SS_SORT_SMALL_THREADS 256
+#endif
+#ifndef SS_SORT_SMALL_CAP
+#define SS_SORT_SMALL_CAP 2048
+#endif
+constexpr int kSmallThreads = SS_SORT_SMALL_THREADS;
+constexpr int kSmallCap = SS_SORT_SMALL_CAP;
 constexpr int kHeavyThreads = 1024;
 constexpr int kHeavyCap = 12288;
 
@@ -304,6 +310,7 @@ extern "C" int ss_bin_sort(int n, const uint32_t *bininfo, const int8_t *cull, i
         return SS_ERR_INVALID;
     if (width > 65535 || height > 65535) return SS_ERR_INVALID;  // rects are packed as uint16
     ss_func_smem((const void *)tile_sort_kernel<kHeavyThreads, kHeavyCap, true>, 2 * kHeavyCap * (int)sizeof(uint64_t));
+    ss_func_smem((const void *)tile_sort_kernel<kSmallThreads, kSmallCap, false>, 2 * kSmallCap * (int)sizeof(uint64_t));
     cudaStream_t st = (cudaStream_t)stream;
     const int ntx = (width + tile - 1) / tile, nty = (height + tile - 1) / tile;
     const int ntiles = ntx * nty;

@@ -92,6 +92,65 @@ __global__ void adam_multi_kernel(AdamMulti<S> A) {
     }
 }
 
+// Multi-tensor Adam on float64 MASTER parameters (the reference's fit keeps
+// its parameters in float64, train.py:168-174): the update is the
+// reference's numpy sequence operation by operation (adam.py:31-41, no
+// contraction), quaternions are renormalised in float64 like
+// normalize_quats (surfels.py:31-37, train.py:246), and the kernels' float32
+// copy is the rounded master value.
+struct MasterSeg {
+    float *p;
+    double *p64;
+    const float *g;
+    double *m, *v;
+    int64_t count, first;
+    double lr, c1, c2;
+    int quat;
+};
+struct MasterMulti {
+    MasterSeg seg[kMaxTensors];
+    int nseg;
+    int64_t items;
+    double b1, b2, eps;
+};
+
+__device__ __forceinline__ double adam_master_one(double p, float g, double *m, double *v, const MasterSeg &s,
+                                                  const MasterMulti &A) {
+    const double gg = g;
+    // m *= b1; m += (1 - b1) g;  v *= b2; v += (1 - b2) g g
+    const double mm = __dadd_rn(__dmul_rn(*m, A.b1), __dmul_rn(__dsub_rn(1.0, A.b1), gg));
+    const double vv = __dadd_rn(__dmul_rn(*v, A.b2), __dmul_rn(__dmul_rn(__dsub_rn(1.0, A.b2), gg), gg));
+    *m = mm;
+    *v = vv;
+    const double mh = __ddiv_rn(mm, s.c1), vh = __ddiv_rn(vv, s.c2);
+    return __dsub_rn(p, __ddiv_rn(__dmul_rn(s.lr, mh), __dadd_rn(__dsqrt_rn(vh), A.eps)));
+}
+
+__global__ void adam_master_kernel(MasterMulti A) {
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < A.items;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (k + 1 < A.nseg && it >= A.seg[k + 1].first) ++k;
+        const MasterSeg &s = A.seg[k];
+        const int64_t j = it - s.first;
+        if (s.quat) {
+            double q[4];
+            for (int c = 0; c < 4; ++c) q[c] = adam_master_one(s.p64[4 * j + c], s.g[4 * j + c], s.m + 4 * j + c,
+                                                               s.v + 4 * j + c, s, A);
+            const double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q[0], q[0]), __dmul_rn(q[1], q[1])),
+                                                              __dmul_rn(q[2], q[2])),
+                                                    __dmul_rn(q[3], q[3])));
+            if (nrm > 0.0)  // (zero norms are reported by the next preprocess, as the reference raises)
+                for (int c = 0; c < 4; ++c) q[c] = __ddiv_rn(q[c], nrm);
+            for (int c = 0; c < 4; ++c) { s.p64[4 * j + c] = q[c]; s.p[4 * j + c] = (float)q[c]; }
+        } else {
+            const double p = adam_master_one(s.p64[j], s.g[j], s.m + j, s.v + j, s, A);
+            s.p64[j] = p;
+            s.p[j] = (float)p;
+        }
+    }
+}
+
 struct Grid { float ox, oy, oz, cell; int dim; };
 
 __device__ __forceinline__ int axis_cell(float c, float o, float cell, int dim) {
@@ -298,6 +357,37 @@ extern "C" int ss_adam_multi_f64(int ntensors, float *const *params, const float
                                  const int *quat_flags, float beta1, float beta2, float eps, void *stream) {
     return adam_multi<double>(ntensors, params, grads, m, v, counts, steps, lrs, quat_flags, beta1, beta2, eps,
                               stream);
+}
+
+extern "C" int ss_adam_multi_master(int ntensors, float *const *params, double *const *masters,
+                                    const float *const *grads, double *const *m, double *const *v,
+                                    const int64_t *counts, const double *c1s, const double *c2s, const double *lrs,
+                                    const int *quat_flags, double beta1, double beta2, double eps, void *stream) {
+    if (ntensors < 1 || ntensors > kMaxTensors || !params || !masters || !grads || !m || !v || !counts || !c1s ||
+        !c2s || !lrs)
+        return SS_ERR_INVALID;
+    MasterMulti A{};
+    A.nseg = ntensors;
+    A.b1 = beta1; A.b2 = beta2; A.eps = eps;
+    int64_t items = 0;
+    for (int k = 0; k < ntensors; ++k) {
+        MasterSeg &sg = A.seg[k];
+        sg.p = params[k]; sg.p64 = masters[k]; sg.g = grads[k]; sg.m = m[k]; sg.v = v[k];
+        sg.count = counts[k];
+        sg.quat = quat_flags ? quat_flags[k] : 0;
+        if (sg.count < 0 || (sg.quat && sg.count % 4)) return SS_ERR_INVALID;
+        if (sg.count > 0 && (!sg.p || !sg.p64 || !sg.g || !sg.m || !sg.v)) return SS_ERR_INVALID;
+        sg.lr = lrs[k]; sg.c1 = c1s[k]; sg.c2 = c2s[k];
+        sg.first = items;
+        items += sg.quat ? sg.count / 4 : sg.count;
+    }
+    A.items = items;
+    if (items == 0) return SS_OK;
+    const int64_t cap = (int64_t)ss_sm_count() * 16;
+    const int blocks = (int)((items + 255) / 256 < cap ? (items + 255) / 256 : cap);
+    adam_master_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(A);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
 }
 
 extern "C" int ss_normalize_quats(int n, float *quats, void *stream) {

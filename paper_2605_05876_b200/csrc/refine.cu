@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kThreads) scan_apply_kernel(int n, uint8_t *__
 }
 
 // ---- apply: the new rows ---------------------------------------------------
-constexpr int kMaxRemap = 20;
+constexpr int kMaxRemap = 32;
 struct RemapSet {
     const void *src[kMaxRemap];
     void *dst[kMaxRemap];

@@ -177,14 +177,16 @@ def refine_topology(cloud, stats, mean_neighbor_dist, max_surfels, quantile=SPLI
         for name in list(optimizer.m):
             if name not in FIELDS:  # per-surfel state only (not the env)
                 continue
-            for store in (optimizer.m, optimizer.v):
+            for store in (optimizer.m, optimizer.v, getattr(optimizer, "p64", {})):
+                if name not in store:
+                    continue
                 t = store[name]
                 if t.shape[0] != n:
                     raise ValueError(f"optimizer state {name!r} has {t.shape[0]} rows, the cloud {n}")
                 out = torch.empty((cap,) + tuple(t.shape[1:]), device=dev, dtype=t.dtype)
                 tensors.append((t, out, 1))
                 opt_new[(id(store), name)] = out
-    if len(tensors) > 20:
+    if len(tensors) > 32:
         raise ValueError("too many tensors to remap in one pass")
     index_map = torch.empty(cap, device=dev, dtype=torch.int64)
     m = len(tensors)
@@ -199,11 +201,17 @@ def refine_topology(cloud, stats, mean_neighbor_dist, max_surfels, quantile=SPLI
     n_out = int(c[0])
     new = SurfelCloud(*(tensors[i][1][:n_out] for i in range(len(FIELDS))))
     if optimizer is not None:
+        p64 = getattr(optimizer, "p64", {})
         for name in list(optimizer.m):
-            for store in (optimizer.m, optimizer.v):
+            for store in (optimizer.m, optimizer.v, p64):
                 key = (id(store), name)
                 if key in opt_new:
                     store[name] = opt_new[key][:n_out]
+            if name in p64 and (id(p64), name) in opt_new:
+                # float64 masters: survivors keep theirs, new rows (zeroed
+                # like the moments) take the new float32 parameters
+                fresh = index_map[:n_out] < 0
+                p64[name][fresh] = getattr(new, name)[fresh].to(torch.float64)
     reasons = {"stale": int(c[3]), "isolated": int(c[4]), "floater": int(c[5]), "split": int(c[2])}
     LAST_REFINE.update(kept=int(c[1]), active=int(c[6]), candidates=int(c[7]),
                        threshold=float(np.array([c[8]], dtype=np.int64).view(np.float64)[0]))

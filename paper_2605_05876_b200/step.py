@@ -174,7 +174,8 @@ class ViewBuffers:
 class TrainStep:
     def __init__(self, cloud, env, width, height, k_max=16, tile=16, background=(0.0, 0.0, 0.0),
                  lrs=None, pair_capacity=None, process_group=None, options=None, streams=2, loss="l1",
-                 tone="hdr-loss", lambda_ssim=0.2, lambda_sil=0.1, cons_scale=0.0, surfel_capacity=None):
+                 tone="hdr-loss", lambda_ssim=0.2, lambda_sil=0.1, cons_scale=0.0, surfel_capacity=None,
+                 master_params=True):
         """loss="l1": the BASELINE config loss (mean |rgb - target| in linear
         space), fused into the forward kernel.  loss="photometric": the
         reference fit loss (train.py:194-206): tone_map(tone) then
@@ -231,7 +232,8 @@ class TrainStep:
             b.d_diffuse64 = self.d_diffuse if k == 0 else torch.zeros_like(self.d_diffuse)
             b.d_spec64 = self.d_spec if k == 0 else torch.zeros_like(self.d_spec)
         self.d_base = torch.empty(env.base.shape, device=dev, dtype=torch.float64)
-        self.adam = Adam()
+        # float64 master parameters like the reference's fit (train.py:168-174)
+        self.adam = Adam(master_params=master_params)
         self._po = make_opts(self.opts, tile)
         self._envs = _lib.make_env(env)
         self._bind_cloud(cloud)

@@ -47,6 +47,59 @@ def test_adam_state_precision(state):
         assert torch.equal(back.m["x"], opt.m["x"]) and back.t["x"] == 3
 
 
+def test_adam_master_params_match_reference_update_exactly():
+    """Adam(master_params=True): float64 masters stepped with the reference's
+    numpy update operation by operation (adam.py:31-41) and quaternions
+    renormalised in float64 (surfels.py:31-37, train.py:246) -- bit-equal to
+    the oracle's float64 restatement given the same (float32) gradients; the
+    kernels' float32 tensors hold the rounded masters."""
+    rng = np.random.default_rng(11)
+    n = 1000
+    p0 = rng.normal(size=(n, 3))
+    q0 = rng.normal(size=(n, 4))
+    q0 /= np.linalg.norm(q0, axis=-1, keepdims=True)
+    opt = ss.Adam(master_params=True)
+    p = torch.tensor(p0, device="cuda", dtype=torch.float32)
+    q = torch.tensor(q0, device="cuda", dtype=torch.float32)
+    opt.set_master("x", p0)
+    opt.set_master("q", q0)
+    rp, rq = p0.copy(), q0.copy()
+    mp, vp, mq, vq = (np.zeros_like(a) for a in (p0, p0, q0, q0))
+    for t in range(1, 4):
+        gp = rng.normal(size=p0.shape).astype(np.float32)
+        gq = rng.normal(size=q0.shape).astype(np.float32)
+        opt.step_multi([("x", p, torch.tensor(gp, device="cuda"), 0.01),
+                        ("q", q, torch.tensor(gq, device="cuda"), 0.005)], renorm_quats="q")
+        O.adam_step(rp, gp, mp, vp, t, 0.01)
+        O.adam_step(rq, gq, mq, vq, t, 0.005)
+        rq /= np.linalg.norm(rq, axis=-1, keepdims=True)
+        assert np.array_equal(host(opt.p64["x"]), rp)
+        assert np.array_equal(host(opt.p64["q"]), rq)
+        assert np.array_equal(host(opt.m["x"]), mp) and np.array_equal(host(opt.v["q"]), vq)
+        assert np.array_equal(host(p), rp.astype(np.float32)) and np.array_equal(host(q), rq.astype(np.float32))
+    # the reference's own 3-step trace (float64 gradients, rounded to float32 here)
+    d = load("optim_refine")
+    opt = ss.Adam(master_params=True)
+    x = torch.tensor(d["adam_p0"], device="cuda")
+    for k in range(3):
+        opt.step_multi([("x", x, torch.tensor(d["adam_grads"][k], device="cuda", dtype=torch.float32), 0.01)])
+        np.testing.assert_allclose(host(opt.p64["x"]), d["adam_traj"][k], rtol=1e-6, atol=1e-7)
+
+
+def test_adam_master_remap_keeps_survivors():
+    opt = ss.Adam(master_params=True)
+    p = torch.arange(12, device="cuda", dtype=torch.float32).view(4, 3)
+    opt.set_master("x", p.double() + 1e-9)
+    opt.step_multi([("x", p, torch.ones_like(p), 0.1)])
+    before = opt.p64["x"].clone()
+    new = torch.full((5, 3), 7.0, device="cuda")
+    opt.remap("x", torch.tensor([2, 0, -1, 3, -1], device="cuda"), param=new)
+    got = opt.p64["x"]
+    assert torch.equal(got[0], before[2]) and torch.equal(got[1], before[0]) and torch.equal(got[3], before[3])
+    assert torch.equal(got[2], new[2].double()) and torch.equal(got[4], new[4].double())
+    assert float(opt.m["x"][2].abs().sum()) == 0.0
+
+
 def test_adam_remap_semantics():
     opt = ss.Adam()
     p = torch.zeros(4, 2, device="cuda")
