@@ -413,6 +413,11 @@ int ss_env_rowsums(int he, int we, const double *khat, double *rowsum, double *w
 int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log, const SsEnvOps *ops,
                    float *base, float *diffuse, float *specular, double *base64, double *diffuse64,
                    double *specular64, void *stream);
+/* ss_env_refresh64: ss_env_refresh from a float64 base_log (the optimiser's
+ * float64 master of the environment, like the reference's float64 env). */
+int ss_env_refresh64(int he, int we, int levels, int samples, const double *base_log, const SsEnvOps *ops,
+                     float *base, float *diffuse, float *specular, double *base64, double *diffuse64,
+                     double *specular64, void *stream);
 int ss_env_adjoint(int he, int we, int levels, int samples, const double *base64, const SsEnvOps *ops,
                    const double *d_diffuse, const double *d_specular, double *d_base, float *d_base_log,
                    void *stream);

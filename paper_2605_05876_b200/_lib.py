@@ -92,6 +92,8 @@ _SIGNATURES = {
     "ss_env_rowsums": [ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],
     "ss_env_refresh": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
                        c_p],
+    "ss_env_refresh64": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p,
+                         c_p, c_p],
     "ss_env_adjoint": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
     "ss_spec_op_count": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p],
     "ss_spec_op_fill": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p],

@@ -21,15 +21,18 @@ constexpr int kScanThreads = 1024;
 // heavier ones by a second launch with a large buffer (each launch skips the
 // other's tiles); beyond kHeavyCap a bitonic network runs in global memory.
 #ifndef SS_SORT_SMALL_THREADS
-#define SS_SORT_SMALL_THREADS 256
+#define SS_SORT_SMALL_THREADS 512
 #endif
 #ifndef SS_SORT_SMALL_CAP
-#define SS_SORT_SMALL_CAP 2048
+#define SS_SORT_SMALL_CAP 4096
 #endif
 constexpr int kSmallThreads = SS_SORT_SMALL_THREADS;
 constexpr int kSmallCap = SS_SORT_SMALL_CAP;
+#ifndef SS_SORT_HEAVY_CAP
+#define SS_SORT_HEAVY_CAP 12288
+#endif
 constexpr int kHeavyThreads = 1024;
-constexpr int kHeavyCap = 12288;
+constexpr int kHeavyCap = SS_SORT_HEAVY_CAP;
 
 
 __device__ void tile_order(const int32_t *__restrict__ counts, int ntiles, int32_t *__restrict__ order);

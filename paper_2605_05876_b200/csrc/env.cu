@@ -570,7 +570,8 @@ __global__ void __launch_bounds__(256) spec_apply_t_kernel(int T, int levels, co
 
 // base = exp(base_log) in float64 (the reference's base, shading.py:373)
 // and its float copies; level 0 of the specular chain is the base itself
-__global__ void exp_kernel(int n, const float *__restrict__ lg, float *__restrict__ base, float *__restrict__ spec0,
+template <typename T>
+__global__ void exp_kernel(int n, const T *__restrict__ lg, float *__restrict__ base, float *__restrict__ spec0,
                            double *__restrict__ base64, double *__restrict__ spec0_64) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -628,15 +629,16 @@ extern "C" int ss_env_khat(int he, int we, double *khat, void *stream) {
     return SS_OK;
 }
 
-extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log, const SsEnvOps *ops,
-                              float *base, float *diffuse, float *specular, double *base64, double *diffuse64,
-                              double *specular64, void *stream) {
+template <typename TL>
+static int env_refresh(int he, int we, int levels, int samples, const TL *base_log, const SsEnvOps *ops,
+                       float *base, float *diffuse, float *specular, double *base64, double *diffuse64,
+                       double *specular64, void *stream) {
     if (he < 2 || we < 2 || levels < 1 || !base_log || !ops || !ops->rowsum || !ops->work || !base || !diffuse ||
         !specular || !base64 || !diffuse64 || !specular64)
         return SS_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     const int T = he * we;
-    exp_kernel<<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular, base64, specular64);
+    exp_kernel<TL><<<(3 * T + 255) / 256, 256, 0, st>>>(3 * T, base_log, base, specular, base64, specular64);
     SS_CUDA_CHECK_LAUNCH();
     {
         const int rc = run_diffuse<1, double, double>(he, we, base64, ops->rowsum, diffuse64, ops->work, ops->khat, st);
@@ -656,6 +658,20 @@ extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const flo
         SS_CUDA_CHECK_LAUNCH();
     }
     return SS_OK;
+}
+
+extern "C" int ss_env_refresh(int he, int we, int levels, int samples, const float *base_log, const SsEnvOps *ops,
+                              float *base, float *diffuse, float *specular, double *base64, double *diffuse64,
+                              double *specular64, void *stream) {
+    return env_refresh<float>(he, we, levels, samples, base_log, ops, base, diffuse, specular, base64, diffuse64,
+                              specular64, stream);
+}
+
+extern "C" int ss_env_refresh64(int he, int we, int levels, int samples, const double *base_log,
+                                const SsEnvOps *ops, float *base, float *diffuse, float *specular, double *base64,
+                                double *diffuse64, double *specular64, void *stream) {
+    return env_refresh<double>(he, we, levels, samples, base_log, ops, base, diffuse, specular, base64, diffuse64,
+                               specular64, stream);
 }
 
 extern "C" int ss_env_adjoint(int he, int we, int levels, int samples, const double *base, const SsEnvOps *ops,

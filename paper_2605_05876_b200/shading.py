@@ -133,11 +133,18 @@ class EnvironmentLight:
             return np.zeros(1)
         return np.arange(self.levels) / (self.levels - 1.0)
 
-    def refresh(self):
+    def refresh(self, base_log64=None):
+        """Derived maps from base_log (shading.py:369-379); base_log64: a float64
+        master of it (Adam(master_params=True)) to refresh from instead."""
         lib = _lib.load()
         he, we = self.shape
         ops = env_ops(he, we, self.levels, self.spec_samples)
-        _lib.check(lib.ss_env_refresh(he, we, self.levels, self.spec_samples, _lib.ptr(self.base_log), ops.ref(),
+        fn, src = lib.ss_env_refresh, self.base_log
+        if base_log64 is not None:
+            if tuple(base_log64.shape) != tuple(self.base_log.shape) or base_log64.dtype != torch.float64:
+                raise ValueError("base_log64 must be a float64 tensor shaped like base_log")
+            fn, src = lib.ss_env_refresh64, base_log64
+        _lib.check(fn(he, we, self.levels, self.spec_samples, _lib.ptr(src), ops.ref(),
                                       _lib.ptr(self.base), _lib.ptr(self.diffuse), _lib.ptr(self.specular),
                                       _lib.ptr(self.base64), _lib.ptr(self.diffuse64), _lib.ptr(self.specular64),
                                       _lib.stream_ptr()), "ss_env_refresh")

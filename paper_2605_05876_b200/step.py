@@ -655,7 +655,7 @@ class TrainStep:
         items = [(k, getattr(self.cloud, k), self.grads[k], self.lrs[k] * lr_scale) for k in PARAMS]
         items.append(("env_base_log", self.env.base_log, self.g_env_log, self.lrs["env_base_log"] * lr_scale))
         self.adam.step_multi(items, renorm_quats="quats")  # one launch, quaternions renormalised in it
-        self.env.refresh()
+        self.env.refresh(self.adam.p64.get("env_base_log"))
 
     # -- CUDA-graph replay ----------------------------------------------------
     MAX_GRAPHS = 8

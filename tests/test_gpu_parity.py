@@ -116,6 +116,19 @@ def test_env_refresh_and_adjoint_match_reference():
     assert bad == 0, err
 
 
+def test_env_refresh_from_float64_master():
+    """refresh(base_log64=...) (the optimiser's float64 master, like the
+    reference's float64 env): the float64 maps follow the reference's own
+    float64 computation from the unrounded log radiance."""
+    d = load("env_ops")
+    env = ss.EnvironmentLight(d["base_log"], levels=int(d["levels"]))
+    env.refresh(base_log64=torch.tensor(d["base_log"], device="cuda", dtype=torch.float64))
+    for k, k64 in (("base", "base64"), ("diffuse", "diffuse64"), ("specular", "specular64")):
+        got, ref = host(getattr(env, k64)), np.asarray(d[k], dtype=np.float64)
+        err = np.abs(got - ref).max() / np.abs(ref).max()
+        assert err < 1e-9, (k, err)
+
+
 def test_empty_and_all_culled():
     cam = ss.Camera.perspective(16, 16, 45.0, (0.0, -3.0, 0.0), (0.0, 0.0, 0.0))
     empty = ss.SurfelCloud(np.zeros((0, 3)), np.zeros((0, 4)), np.zeros((0, 2)), np.zeros((0, 3)),
