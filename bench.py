@@ -91,6 +91,21 @@ def _self_launch(argv, nproc):
     return subprocess.call(cmd, env=env)
 
 
+class _stdout_to_stderr:
+    """fd-level redirect of stdout to stderr (C libraries included)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
+
+
 def _check_world(args):
     rank, world, _ = _dist_env()
     if world != args.gpus:
@@ -409,8 +424,16 @@ def run_ours(args):
     rank, world = _check_world(args)
     local = _dist_env()[2]
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # SS_COLLECTIVES=force under torchrun with one rank: the NCCL path (process
+    # group, all-reduces, max-over-ranks timing) on a single GPU (self-test)
+    multi = world > 1 or (os.environ.get("SS_COLLECTIVES") == "force" and "WORLD_SIZE" in os.environ)
+    if multi:
+        # NCCL prints its version line on stdout at communicator creation
+        # (NCCL_DEBUG=VERSION in this image): create it with fd 1 on stderr,
+        # so stdout carries only the JSON line
+        with _stdout_to_stderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
     from paper_2605_05876_b200.step import shard_views
     my_views = shard_views(VIEWS_PER_STEP, world, rank)
 
@@ -445,7 +468,7 @@ def run_ours(args):
 
     # ---- timed region: inputs resident in HBM ----
     clocks = Clocks(local) if rank == 0 else None
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -456,7 +479,7 @@ def run_ours(args):
         one_step()
     ev1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     step_ms = ev0.elapsed_time(ev1) / args.steps
     clk = clocks.stop() if clocks else None
@@ -468,7 +491,7 @@ def run_ours(args):
     kev = ts.kernel_events
     ts.kernel_events = None
     t = torch.tensor([step_ms], device="cuda", dtype=torch.float64)
-    if world > 1:
+    if multi:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms = float(t.item())
     value = VIEWS_PER_STEP / (step_ms / 1e3)
@@ -522,7 +545,7 @@ def run_ours(args):
     for _ in range(2):
         ts.step_host(cams, host_targets).item()
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     e0 = time.perf_counter()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -533,7 +556,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e_ms = ea.elapsed_time(eb) / args.steps
     et = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
-    if world > 1:
+    if multi:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
     e_ms = float(et.item())
     h2d = sum(h.numel() * h.element_size() for h in host_targets) * world
@@ -551,7 +574,7 @@ def run_ours(args):
     for _ in range(2):
         tp.step(cams, targets)
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     pa.record(stream)
@@ -561,7 +584,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     p_ms = pa.elapsed_time(pb) / args.steps
     pt = torch.tensor([p_ms], device="cuda", dtype=torch.float64)
-    if world > 1:
+    if multi:
         dist.all_reduce(pt, op=dist.ReduceOp.MAX)
     photometric = {"value": VIEWS_PER_STEP / (float(pt.item()) / 1e3), "unit": UNIT,
                    "loss": "tone_map hdr-loss, 0.8 L1 + 0.2 (1 - SSIM 11x11) (train.py:194-199)",
@@ -573,7 +596,7 @@ def run_ours(args):
     for _ in range(2):
         tp.step(cams, targets)
     torch.cuda.synchronize()
-    if world > 1:
+    if multi:
         dist.barrier()
     pa.record(stream)
     for _ in range(args.steps):
@@ -581,7 +604,7 @@ def run_ours(args):
     pb.record(stream)
     torch.cuda.synchronize()
     pt = torch.tensor([pa.elapsed_time(pb) / args.steps], device="cuda", dtype=torch.float64)
-    if world > 1:
+    if multi:
         dist.all_reduce(pt, op=dist.ReduceOp.MAX)
     photometric_cons = {"value": VIEWS_PER_STEP / (float(pt.item()) / 1e3), "unit": UNIT,
                         "loss": "the above + depth consolidation, cons_scale = 100 / (1 * 800 * 800) "
@@ -589,7 +612,7 @@ def run_ours(args):
     del tp
 
     if rank != 0:
-        if world > 1:
+        if multi:
             dist.destroy_process_group()
         return
 
@@ -625,7 +648,9 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": _config({"parallelism": f"dp{world} over views", "pairs_per_view": P, "kept_per_view": Nk,
-                                 "layer_pixels_per_view": LP}),
+                                 "layer_pixels_per_view": LP,
+                                 "collective": (f"NCCL all-reduce, {dist.get_world_size()} rank(s), 2 buckets per step"
+                                                if multi else "none (one process)")}),
         "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src, "kernel": "record backward (ss_train_backward_records: area classes, splat_bwd, big rects)",
@@ -651,7 +676,7 @@ def run_ours(args):
         "loss": last_loss,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
 
 

@@ -220,11 +220,9 @@ int ss_raster_backward(int width, int height, int tile, const int32_t *tile_offs
  * float64 layer sums; A = A_hi + A_lo is formed from the float-rounded
  * dL/dC_raw so that the backward's g_w = A + dL/dC_raw . colour keeps the
  * record colour - layer mean colour difference exactly), per pixel a packed header `pix_hdr` (H*W x 8
- * int32: number of closed layers | layer count << 8, then the depths at which
- * layers 0..2 closed, as float bits -- words past the closed count are not
- * written; then layer 0's float4 (A_hi, dL/dC_raw rgb) again, so the record
- * backward reads header and layer-0 coefficients with one 32-byte load) and
- * the closing depths of layers >= 3 into `thr` (k_max*H*W floats, plane j), and adds sum|rgb - target| into loss_sum (1 double).
+ * int32: number of closed layers, then the depths at which layers 0..6
+ * closed, as float bits; words past the closed count are not written) and
+ * the closing depths of layers >= 7 into `thr` (k_max*H*W floats, plane j), and adds sum|rgb - target| into loss_sum (1 double).
  * rgb (H,W,3) is nullable.
  * ss_train_backward_records: pass 2 of backward.py:240-320 without the walk:
  * a covering record with interval start zs belongs to layer
@@ -244,13 +242,12 @@ int ss_train_forward(int width, int height, int tile, const int32_t *tile_offset
  * (required), alpha (nullable) and, per pixel and layer, the raw layer sums
  * (W, C rgb) into coef; after the loss has produced g_rgb (and g_alpha),
  * ss_train_coefs turns them into the backward coefficients in place (suffix
- * recursion of backward.py:201-238 incl. the coverage term) and stores layer
- * 0's coefficients into pix_hdr words 4..7.  pix_hdr.x = closed layers |
- * layer count << 8. */
+ * recursion of backward.py:201-238 incl. the coverage term).  pix_hdr.x =
+ * closed layers | layer count << 8. */
 /* g_rgb64 (nullable): the same image gradient in float64 (ss_photometric_loss
  * grad64), used instead of g_rgb -- the layer coefficients' colour terms
  * cancel, so a float32-rounded gradient biases them by ~1e-5 */
-int ss_train_coefs(int width, int height, int k_max, int32_t *pix_hdr, float *coef, const float *g_rgb,
+int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef, const float *g_rgb,
                    const double *g_rgb64, const float *g_alpha, const float *background, void *stream);
 /* The same three steps with the consolidation penalty (backward.py:160-320
  * with cons_scale > 0): ss_train_forward_zstats is the deferred forward that
@@ -265,7 +262,7 @@ int ss_train_forward_zstats(int width, int height, int tile, const int32_t *tile
                             const int32_t *pair_rec, const uint32_t *pair_rect, const float *records,
                             const float *background, int k_max, float *coef, float *thr, int32_t *pix_hdr,
                             float *rgb, float *alpha, const int32_t *tile_order, float *zstats, void *stream);
-int ss_train_coefs_cons(int width, int height, int k_max, int32_t *pix_hdr, float *coef, float *zstats,
+int ss_train_coefs_cons(int width, int height, int k_max, const int32_t *pix_hdr, float *coef, float *zstats,
                         const float *g_rgb, const double *g_rgb64, const float *g_alpha, const float *background,
                         double cons_scale, double *cons_loss, void *stream);
 int ss_train_backward_records_cons(int n, const int8_t *cull, const float *records, int width, int height,

@@ -53,8 +53,8 @@ struct FwdParams {
     const float *target;   // (H,W,3)
     float inv_count;       // 1 / (3 H W): mean over all image entries
     float4 *coef;          // (k_max, H*W) float4
-    float *thr;            // (k_max, H*W) depth at which layer j >= 3 closed (planes 0..2 unused)
-    int4 *hdr;             // (H*W, 2) packed (closed-layer count, closing depths of layers 0..2), layer-0 coefficients
+    float *thr;            // (k_max, H*W) depth at which layer j >= 3 closed
+    int4 *hdr;             // (H*W, 2) packed (closed-layer count, closing depths of layers 0..2), (depths 3..6)
     double *loss;          // sum of |rgb - target| (1 double)
     float4 *zst;           // kCons: (k_max, H*W) per layer (z0, sum w dz, sum w dz^2, 0), dz = view_z - z0
 };
@@ -66,18 +66,13 @@ struct FwdParams {
 // ROUNDED G_c (then g_w = g_am (1 - a) + sum_c G_c (c_c - c_hat_c) exactly)
 // and stored as float hi + lo (the lo plane follows the k_max float4 planes
 // in `coef`).  The backward evaluates g_w in float64.
-// Returns the float4 it stored: layer 0's is also kept next to the pixel
-// header (hdr[2 pix + 1]), so the record backward reads header and layer-0
-// coefficients with one 32-byte load.
-__device__ __forceinline__ float4 store_coef(float4 *coef, size_t o, size_t lo_off, double base, double gh0, double gh1,
-                                             double gh2, double inv, double ch0, double ch1, double ch2) {
+__device__ __forceinline__ void store_coef(float4 *coef, size_t o, size_t lo_off, double base, double gh0, double gh1,
+                                           double gh2, double inv, double ch0, double ch1, double ch2) {
     const float g0 = (float)(gh0 * inv), g1 = (float)(gh1 * inv), g2 = (float)(gh2 * inv);
     const double A = base - ((double)g0 * ch0 + (double)g1 * ch1 + (double)g2 * ch2);
     const float hi = (float)A;
-    const float4 c = make_float4(hi, g0, g1, g2);
-    coef[o] = c;
+    coef[o] = make_float4(hi, g0, g1, g2);
     reinterpret_cast<float *>(coef + lo_off)[o] = (float)(A - (double)hi);
-    return c;
 }
 
 // CTAs of kFwdWarps warps (a tile is split over tile*tile/32/kFwdWarps
@@ -187,6 +182,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
                     if (ncl == 0) th0 = zmax;
                     else if (ncl == 1) th1 = zmax;
                     else if (ncl == 2) th2 = zmax;
+                    else if (ncl < 7) reinterpret_cast<float *>(P.hdr)[8 * pix + 1 + ncl] = zmax;
                     else P.thr[(size_t)ncl * P.W * P.H + pix] = zmax;
                 }
                 ++ncl;
@@ -266,9 +262,8 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
                 const double g_am = tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2));
                 const double ta = tb[m] * a;
                 const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
-                const float4 c = store_coef(P.coef, (size_t)m * HW + pix, (size_t)P.k_max * HW, g_am * (1.0 - a), gh0,
-                                            gh1, gh2, inv, ch0, ch1, ch2);
-                if (m == 0) reinterpret_cast<float4 *>(P.hdr)[2 * pix + 1] = c;
+                store_coef(P.coef, (size_t)m * HW + pix, (size_t)P.k_max * HW, g_am * (1.0 - a), gh0, gh1, gh2, inv,
+                           ch0, ch1, ch2);
                 sf0 = a * ch0 + (1.0 - a) * sf0;
                 sf1 = a * ch1 + (1.0 - a) * sf1;
                 sf2 = a * ch2 + (1.0 - a) * sf2;
@@ -299,7 +294,7 @@ __global__ void __launch_bounds__(32 * kFwdWarps) raster_fwd_kernel(FwdParams P)
 // the per-layer backward coefficients (A, dL/dC_raw) once the image-space
 // gradients g_rgb (and g_alpha) are known -- the suffix recursion of
 // backward.py:201-238 including the coverage term (g_alpha * prod(1 - a)).
-__global__ void __launch_bounds__(256) train_coef_kernel(int HW, int k_max, int4 *__restrict__ hdr, float4 *coef,
+__global__ void __launch_bounds__(256) train_coef_kernel(int HW, int k_max, const int4 *__restrict__ hdr, float4 *coef,
                                                          const float *__restrict__ g_rgb, const double *__restrict__ g64,
                                                          const float *__restrict__ g_alpha, float bg0, float bg1,
                                                          float bg2)
@@ -335,9 +330,8 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, int k_max, int4
         const double g_am = tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2) + ga * q);
         const double ta = tb[m] * a[m];
         const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
-        const float4 c = store_coef(coef, (size_t)m * HW + pix, (size_t)k_max * HW, g_am * (1.0 - a[m]), gh0, gh1, gh2,
-                                    inv, ch0, ch1, ch2);
-        if (m == 0) reinterpret_cast<float4 *>(hdr)[2 * pix + 1] = c;
+        store_coef(coef, (size_t)m * HW + pix, (size_t)k_max * HW, g_am * (1.0 - a[m]), gh0, gh1, gh2, inv, ch0, ch1,
+                   ch2);
         sf0 = a[m] * ch0 + (1.0 - a[m]) * sf0;
         sf1 = a[m] * ch1 + (1.0 - a[m]) * sf1;
         sf2 = a[m] * ch2 + (1.0 - a[m]) * sf2;
@@ -351,7 +345,7 @@ __global__ void __launch_bounds__(256) train_coef_kernel(int HW, int k_max, int4
 // zst in place as the per-layer (B, Q, z_bar, var) of the record gradient
 //     g_w += B dz + Q (dz^2 - var),  g_vz = w (B + 2 Q dz),  dz = view_z - z_bar;
 // the penalty value is block-reduced into cons_loss.
-__global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, int k_max, int4 *__restrict__ hdr, float4 *coef,
+__global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, int k_max, const int4 *__restrict__ hdr, float4 *coef,
                                                               float4 *zst, const float *__restrict__ g_rgb,
                                                               const double *__restrict__ g64,
                                                               const float *__restrict__ g_alpha, float bg0,
@@ -413,9 +407,8 @@ __global__ void __launch_bounds__(256) train_coef_cons_kernel(int HW, int k_max,
                 tb[m] * (gc0 * (ch0 - sf0) + gc1 * (ch1 - sf1) + gc2 * (ch2 - sf2) + ga * q + gw_c[m] - rw);
             const double ta = tb[m] * a[m];
             const double gh0 = gc0 * ta, gh1 = gc1 * ta, gh2 = gc2 * ta;
-            const float4 c = store_coef(coef, (size_t)m * HW + pix, (size_t)k_max * HW, g_am * (1.0 - a[m]), gh0, gh1,
-                                        gh2, inv, ch0, ch1, ch2);
-            if (m == 0) reinterpret_cast<float4 *>(hdr)[2 * pix + 1] = c;
+            store_coef(coef, (size_t)m * HW + pix, (size_t)k_max * HW, g_am * (1.0 - a[m]), gh0, gh1, gh2, inv, ch0,
+                       ch1, ch2);
             zst[(size_t)m * HW + pix] = make_float4((float)(gz_c[m] * inv), (float)(gv_c[m] * inv), (float)zb[m],
                                                     (float)vr[m]);
             sf0 = a[m] * ch0 + (1.0 - a[m]) * sf0;
@@ -527,7 +520,7 @@ extern "C" int ss_train_forward_zstats(int width, int height, int tile, const in
                          coef, thr, pix_hdr, nullptr, rgb, alpha, tile_order, zstats, stream);
 }
 
-extern "C" int ss_train_coefs(int width, int height, int k_max, int32_t *pix_hdr, float *coef,
+extern "C" int ss_train_coefs(int width, int height, int k_max, const int32_t *pix_hdr, float *coef,
                               const float *g_rgb, const double *g_rgb64, const float *g_alpha,
                               const float *background, void *stream)
 {
@@ -535,13 +528,13 @@ extern "C" int ss_train_coefs(int width, int height, int k_max, int32_t *pix_hdr
         return SS_ERR_INVALID;
     const int HW = width * height;
     train_coef_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-        HW, k_max, reinterpret_cast<int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef), g_rgb, g_rgb64, g_alpha,
+        HW, k_max, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef), g_rgb, g_rgb64, g_alpha,
         background[0], background[1], background[2]);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }
 
-extern "C" int ss_train_coefs_cons(int width, int height, int k_max, int32_t *pix_hdr, float *coef,
+extern "C" int ss_train_coefs_cons(int width, int height, int k_max, const int32_t *pix_hdr, float *coef,
                                    float *zstats, const float *g_rgb, const double *g_rgb64, const float *g_alpha,
                                    const float *background, double cons_scale, double *cons_loss, void *stream)
 {
@@ -550,7 +543,7 @@ extern "C" int ss_train_coefs_cons(int width, int height, int k_max, int32_t *pi
         return SS_ERR_INVALID;
     const int HW = width * height;
     train_coef_cons_kernel<<<(HW + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-        HW, k_max, reinterpret_cast<int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef),
+        HW, k_max, reinterpret_cast<const int4 *>(pix_hdr), reinterpret_cast<float4 *>(coef),
         reinterpret_cast<float4 *>(zstats), g_rgb, g_rgb64, g_alpha, background[0], background[1], background[2],
         cons_scale, cons_loss);
     SS_CUDA_CHECK_LAUNCH();

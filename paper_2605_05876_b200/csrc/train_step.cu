@@ -68,7 +68,7 @@ struct SplatParams {
     const float4 *coef;     // (k_max, HW) per-layer (A hi, dL/dC_raw)
     const float *coef_lo;   // (k_max, HW) low part of A (follows the float4 planes)
     const float *thr;       // (k_max, HW) closing depths of layers >= 3
-    const int4 *hdr;        // (HW, 2) (closed-layer count, closing depths of layers 0..2), layer-0 coefficients
+    const int4 *hdr;        // (HW, 2) (closed-layer count, closing depths of layers 0..2), (depths 3..6)
     const float4 *zc;       // kCons: (k_max, HW) per layer (B, Q, z_bar, var) of the consolidation penalty
     float *acc;             // (n, 20)
     const int32_t *big_list;  // big-record queue (medium from the front, huge from the back)
@@ -84,16 +84,6 @@ __global__ void pixel_ndc_kernel(int W, int H, float *xs, float *ys, int32_t *bi
     if (k < W) xs[k] = ss_ndc_x(k, W);
     if (k < H) ys[k] = ss_ndc_y(k, H);
     if (k < kHeadWords) big_count[k] = 0;  // counters, class histogram and cursors
-}
-
-// The pixel's header (closed-layer count, closing depths 0..2) and its
-// layer-0 coefficients: one 32-byte load (LDG.256, read-only path).
-__device__ __forceinline__ void ldg_hdr(const int4 *p, int4 &h, float4 &cf0) {
-    float a, b, c, d;
-    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=r"(h.x), "=r"(h.y), "=r"(h.z), "=r"(h.w), "=f"(a), "=f"(b), "=f"(c), "=f"(d)
-        : "l"(p));
-    cf0 = make_float4(a, b, c, d);
 }
 
 // Gradient of the covered item (pixel ix, iy of record R) with the coverage
@@ -121,9 +111,8 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const size_t pix = (size_t)iy * P.W + ix;
     // the packed header and the (most common) layer-0 coefficients are loaded
     // together, before the geometry below, so their latency hides behind it
-    int4 h;
-    float4 cf0;
-    ldg_hdr(P.hdr + 2 * pix, h, cf0);
+    const int4 h = __ldg(P.hdr + 2 * pix);
+    const float4 cf0 = __ldg(P.coef + pix);
     // ray / tangent-plane quantities with the reference's own float32
     // sequence (rasterizer.py:197-207, bit-identical k, l, den; u, v within
     // ~2 ulp): the certified fast form decided coverage in pass 1, but its
@@ -150,11 +139,16 @@ __device__ __forceinline__ int item_grad(const SplatParams &P, const SsRecord &R
     const int nc = h.x & 0xff;  // closed layers (the layer count sits in bits 8+)
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
             (nc > 2 && __int_as_float(h.w) < zs);
-    // the closing depths increase strictly with j: the planes of layers >= 3
-    // only when zs lies beyond the first three
+    // the closing depths increase strictly with j: the second header half
+    // (same 32-byte sector) only when zs lies beyond the first three
     if (m == 3 && nc > 3) {
-        const int jn = min(nc, P.k_max);
-        for (int j = 3; j < jn && __ldg(P.thr + j * HW + pix) < zs; ++j) ++m;
+        const int4 h2 = __ldg(P.hdr + 2 * pix + 1);
+        m += (__int_as_float(h2.x) < zs) + (nc > 4 && __int_as_float(h2.y) < zs) +
+             (nc > 5 && __int_as_float(h2.z) < zs) + (nc > 6 && __int_as_float(h2.w) < zs);
+        if (m == 7) {
+            const int jn = min(nc, P.k_max);
+            for (int j = 7; j < jn && __ldg(P.thr + j * HW + pix) < zs; ++j) ++m;
+        }
     }
     if (m >= P.k_max) return 0;  // beyond the K_MAX stop: discarded
     const float4 cf = m == 0 ? cf0 : __ldg(P.coef + m * HW + pix);
@@ -223,8 +217,13 @@ __device__ __forceinline__ int pixel_layer(const SplatParams &P, size_t pix, flo
     int m = (nc > 0 && __int_as_float(h.y) < zs) + (nc > 1 && __int_as_float(h.z) < zs) +
             (nc > 2 && __int_as_float(h.w) < zs);
     if (m == 3 && nc > 3) {
-        const int jn = min(nc, P.k_max);
-        for (int j = 3; j < jn && __ldg(P.thr + j * HW + pix) < zs; ++j) ++m;
+        const int4 h2 = __ldg(P.hdr + 2 * pix + 1);
+        m += (__int_as_float(h2.x) < zs) + (nc > 4 && __int_as_float(h2.y) < zs) +
+             (nc > 5 && __int_as_float(h2.z) < zs) + (nc > 6 && __int_as_float(h2.w) < zs);
+        if (m == 7) {
+            const int jn = min(nc, P.k_max);
+            for (int j = 7; j < jn && __ldg(P.thr + j * HW + pix) < zs; ++j) ++m;
+        }
     }
     if (m >= P.k_max) return -1;
     cf = __ldg(P.coef + m * HW + pix);

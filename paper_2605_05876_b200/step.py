@@ -25,6 +25,7 @@ the reference's render() does (rasterizer.py:352-353).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -44,6 +45,16 @@ def shard_views(n_views, world, rank):
     base, extra = divmod(n_views, world)
     start = rank * base + min(rank, extra)
     return list(range(start, start + base + (1 if rank < extra else 0)))
+
+
+def collectives_on(group=None):
+    """Whether the step's gradients go through a collective: a process group
+    with more than one rank, or any initialised group when SS_COLLECTIVES=force
+    (the NCCL self-test: one rank, the same calls and stream ordering as a
+    multi-GPU run)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return False
+    return dist.get_world_size(group) > 1 or os.environ.get("SS_COLLECTIVES") == "force"
 
 
 class GradPack:
@@ -90,20 +101,20 @@ class GradPack:
         """Start the all-reduce of bucket A asynchronously (NCCL runs it on its
         own stream after the work queued so far); returns the work handle or
         None when not distributed."""
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if collectives_on(group):
             n = self._bucket_split() // self.flat.element_size()
             return dist.all_reduce(self.flat[:n], group=group, async_op=True)
         return None
 
     def all_reduce_rest(self, group=None):
         """All-reduce bucket B (env gradient, loss, status: ~T*3 + 2 floats)."""
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if collectives_on(group):
             n = self._bucket_split() // self.flat.element_size()
             dist.all_reduce(self.flat[n:], group=group)
 
     def all_reduce(self, group=None, async_op=False):
         """The whole buffer in one collective."""
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if collectives_on(group):
             return dist.all_reduce(self.flat, group=group, async_op=async_op)
         return None
 
@@ -676,7 +687,7 @@ class TrainStep:
         addresses; it is dropped when the pair buffers grow or the cloud is
         rebound.  The status read and the overflow re-run stay as in
         gradients().  Single process only (the NCCL all-reduce is not captured)."""
-        if self.pg is not None or (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+        if self.pg is not None or collectives_on():
             return self.gradients(cameras, targets, masks)
         if self.kernel_events is not None or self.collect_stats or self.captured_rgb is not None:
             return self.gradients(cameras, targets, masks)
