@@ -16,6 +16,7 @@ struct ChainParams {
     double view[16], proj[16], cam_pos[3];
     float viewf[16], projf[16];
     int W, H, mip, color_source;
+    SsPixelSteps px;
     double sigma;
     float r_cut, sigma_f;
     SsEnv env;
@@ -35,18 +36,18 @@ __device__ __forceinline__ float dot_gemv(float a0, float a1, float a2, float v0
 
 // T rows of surfel i, bit-identical to the preprocess kernel (explicit
 // round-to-nearest ops so this file's FMA contraction cannot change them).
-__device__ __forceinline__ void rows_of(const ChainParams &P, int i, double su_d, double sv_d, float t1[3], float t2[3],
-                                        float t4[3]) {
+__device__ __forceinline__ void rows_of(const ChainParams &P, int i, float t1[3], float t2[3], float t4[3]) {
     const SsCloud &c = P.cloud;
     const float c0 = c.centers[3 * i], c1 = c.centers[3 * i + 1], c2 = c.centers[3 * i + 2];
     const float4 q = reinterpret_cast<const float4 *>(c.quats)[i];
+    const float2 ls = reinterpret_cast<const float2 *>(c.log_scales)[i];
     const float nrm = __fsqrt_rn(fa(fa(fa(fm(q.x, q.x), fm(q.y, q.y)), fm(q.z, q.z)), fm(q.w, q.w)));
     const float w = fd(q.x, nrm), x = fd(q.y, nrm), y = fd(q.z, nrm), z = fd(q.w, nrm);
     const float uh0 = fs(1.f, fm(2.f, fa(fm(y, y), fm(z, z)))), uh1 = fm(2.f, fa(fm(x, y), fm(w, z))),
                 uh2 = fm(2.f, fs(fm(x, z), fm(w, y)));
     const float vh0 = fm(2.f, fs(fm(x, y), fm(w, z))), vh1 = fs(1.f, fm(2.f, fa(fm(x, x), fm(z, z)))),
                 vh2 = fm(2.f, fa(fm(y, z), fm(w, x)));
-    const float su = (float)su_d, sv = (float)sv_d;  // exp of the log-scales, float64 (the tail's too)
+    const float su = (float)exp((double)ls.x), sv = (float)exp((double)ls.y);
     const float su0 = fm(su, uh0), su1 = fm(su, uh1), su2 = fm(su, uh2);
     const float sv0 = fm(sv, vh0), sv1 = fm(sv, vh1), sv2 = fm(sv, vh2);
     float cc[3], tu[3], tv[3];
@@ -167,10 +168,8 @@ __global__ void __launch_bounds__(128, SS_CHAIN_MINB) chain_kernel(ChainParams P
         gs0 = r[9]; gs1 = r[10]; gs2 = r[11]; gnf = r[12]; gz = r[17];
     }
 
-    const float2 lsv = reinterpret_cast<const float2 *>(P.cloud.log_scales)[i];
-    const double su_d = exp((double)lsv.x), sv_d = exp((double)lsv.y);
     float t1f[3], t2f[3], t4f[3];
-    rows_of(P, i, su_d, sv_d, t1f, t2f, t4f);
+    rows_of(P, i, t1f, t2f, t4f);
     if (a4.w == SS_ACC_MOMENTS) {
         // moments of the ray-plane gradient (train_step.cu item_grad) about
         // the projected centre (cx, cy): Sx = Sx' + cx S, Sy = Sy' + cy S in
@@ -198,7 +197,7 @@ __global__ void __launch_bounds__(128, SS_CHAIN_MINB) chain_kernel(ChainParams P
 #endif
         // _mip_chain_backward (backward.py:473-548)
         float jf[4];
-        const bool ok = ss_center_jacobian(t1f, t2f, t4f, P.W, P.H, jf);
+        const bool ok = ss_center_jacobian(t1f, t2f, t4f, P.px.dxp, P.px.dyp, jf);
         const double j00 = jf[0], j01 = jf[1], j10 = jf[2], j11 = jf[3];
         const double sg = P.sigma;
         const double s00 = 1.0 + sg * (j00 * j00 + j01 * j01);
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(128, SS_CHAIN_MINB) chain_kernel(ChainParams P
             const double gj10 = ts * (ga01 * j00 + ga11 * j10), gj11 = ts * (ga01 * j01 + ga11 * j11);
             const double T1[3] = {t1f[0], t1f[1], t1f[2]}, T2[3] = {t2f[0], t2f[1], t2f[2]}, T4[3] = {t4f[0], t4f[1], t4f[2]};
             const double d4 = T4[2], id4 = 1.0 / d4, cx = T1[2] * id4, cy = T2[2] * id4;
-            const double dx = 1.0 / P.W, dy = 1.0 / P.H;
+            const double dx = P.px.inv_w, dy = P.px.inv_h;
             const double pr[4][4] = {{cx + dx, cy, gj00, gj10}, {cx - dx, cy, -gj00, -gj10},
                                      {cx, cy + dy, gj01, gj11}, {cx, cy - dy, -gj01, -gj11}};
             double gcx = 0.0, gcy = 0.0;
@@ -281,7 +280,8 @@ __global__ void __launch_bounds__(128, SS_CHAIN_MINB) chain_kernel(ChainParams P
     const TT w = qv.x * iqn, x = qv.y * iqn, y = qv.z * iqn, z = qv.w * iqn;
     const TT uh[3] = {1 - 2 * (y * y + z * z), 2 * (x * y + w * z), 2 * (x * z - w * y)};
     const TT vh[3] = {2 * (x * y - w * z), 1 - 2 * (x * x + z * z), 2 * (y * z + w * x)};
-    const TT su = (TT)su_d, sv = (TT)sv_d;
+    const float2 lsv = reinterpret_cast<const float2 *>(cl.log_scales)[i];
+    const TT su = (TT)exp((double)lsv.x), sv = (TT)exp((double)lsv.y);
     const TT gsu = (guw[0] * uh[0] + guw[1] * uh[1]) + guw[2] * uh[2];
     const TT gsv = (gvw[0] * vh[0] + gvw[1] * vh[1]) + gvw[2] * vh[2];
     TT gU[3], gV[3], gN[3] = {0, 0, 0};
@@ -419,6 +419,7 @@ extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, cons
     for (int k = 0; k < 3; ++k)
         P.cam_pos[k] = -(cam->view[k] * cam->view[3] + cam->view[4 + k] * cam->view[7] + cam->view[8 + k] * cam->view[11]);
     P.W = cam->width; P.H = cam->height; P.mip = opt->mip_enabled; P.color_source = color_source;
+    P.px = ss_pixel_steps(P.W, P.H);
     P.sigma = (double)opt->mip_sigma;
     P.r_cut = opt->r_cut; P.sigma_f = opt->mip_sigma;
     P.env = env ? *env : SsEnv{};

@@ -84,12 +84,13 @@ __device__ __forceinline__ int fast_cover(const FastCov &f, float s0, float s1, 
 // first-order propagation plus both rho^2 evaluation roundings.  +inf when
 // den may change sign over the rect or the bound is not small.
 __device__ __forceinline__ float coverage_margin(const float t1[3], const float t2[3], const float t4[3], float s0,
-                                                 float s1, float s2, int x0, int y0, int x1, int y1, int W, int H) {
+                                                 float s1, float s2, int x0, int y0, int x1, int y1, double two_w,
+                                                 double two_h) {
     const double e = 5.9604644775390625e-08;  // 2^-24, float32 unit roundoff
     const float INF = __int_as_float(0x7f800000);
     const double T1[3] = {t1[0], t1[1], t1[2]}, T2[3] = {t2[0], t2[1], t2[2]}, T4[3] = {t4[0], t4[1], t4[2]};
-    const double xs[2] = {(double)ss_ndc_x(x0, W), (double)ss_ndc_x(x1 - 1, W)};
-    const double ys[2] = {(double)ss_ndc_y(y0, H), (double)ss_ndc_y(y1 - 1, H)};
+    const double xs[2] = {(double)ss_ndc_xs(x0, two_w), (double)ss_ndc_xs(x1 - 1, two_w)};
+    const double ys[2] = {(double)ss_ndc_ys(y0, two_h), (double)ss_ndc_ys(y1 - 1, two_h)};
     // den is linear in (x, y): its extremes over the rect are at the corners
     double dmin = 1e300, dmax = -1e300;
     for (int i = 0; i < 2; ++i)

@@ -31,6 +31,7 @@ struct CamF {
     float view[16], proj[16];
     double cam_pos[3];
     int W, H;
+    SsPixelSteps px;
 };
 
 // View-independent per-surfel state of one optimisation step
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
     float tb[3][3];
     if (opt.mip_enabled) {
         float jj[4];
-        ok = ss_center_jacobian(t1, t2, t4, cam.W, cam.H, jj);
+        ok = ss_center_jacobian(t1, t2, t4, cam.px.dxp, cam.px.dyp, jj);
         if (ok && alive) { j00 = jj[0]; j01 = jj[1]; j10 = jj[2]; j11 = jj[3]; }
         const float s = opt.mip_sigma;
         float jjt00 = j00 * j00 + j01 * j01;
@@ -275,7 +276,8 @@ __global__ void __launch_bounds__(256, SS_PRE_MINB) preprocess_kernel(
 #ifdef SS_EXP_NO_MARGIN
     const float cm = alive ? 1.f
 #else
-    const float cm = alive ? coverage_margin(t1, t2, t4, m00, m01, m11, (int)x0, (int)y0, (int)x1, (int)y1, cam.W, cam.H)
+    const float cm = alive ? coverage_margin(t1, t2, t4, m00, m01, m11, (int)x0, (int)y0, (int)x1, (int)y1, cam.px.two_w,
+                                            cam.px.two_h)
 #endif
                            : 0.f;
     rec.e = make_float4(col[0], col[1], col[2], cm);
@@ -347,7 +349,7 @@ __global__ void pack_kernel(int k, const float *__restrict__ t1, const float *__
     rec.c = make_float4(a4[2], m00, m01, m11);
     rec.d = make_float4(n_f[j], vz, zs, ze);
     const bool alive = x1 > x0 && y1 > y0;
-    const float cm = alive ? coverage_margin(a1, a2, a4, m00, m01, m11, x0, y0, x1, y1, W, H) : 0.f;
+    const float cm = alive ? coverage_margin(a1, a2, a4, m00, m01, m11, x0, y0, x1, y1, 2.0 / W, 2.0 / H) : 0.f;
     const float c0 = colors ? colors[3 * i] : 0.f, c1 = colors ? colors[3 * i + 1] : 0.f,
                 c2 = colors ? colors[3 * i + 2] : 0.f;
     rec.e = make_float4(c0, c1, c2, cm);
@@ -418,6 +420,7 @@ static int preprocess_impl(const SsCloud *cloud, const SsCamera *cam, const SsPr
     for (int k = 0; k < 3; ++k)
         cf.cam_pos[k] = -(cam->view[k] * cam->view[3] + cam->view[4 + k] * cam->view[7] + cam->view[8 + k] * cam->view[11]);
     cf.W = cam->width; cf.H = cam->height;
+    cf.px = ss_pixel_steps(cf.W, cf.H);
     SsEnv e = env ? *env : SsEnv{};
     SsProjAux a = aux ? *aux : SsProjAux{};
     int blocks = (cloud->n + 255) / 256;
