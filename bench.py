@@ -53,6 +53,22 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _ncu_instructions():
+    """Executed warp instructions per launch of the rasterisers from the latest
+    committed ncu --set full summary (profiles/*_ncu_full.txt): (dict, file)."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.txt")))
+    if not files:
+        return {}, None
+    out = {}
+    for line in open(files[-1]):
+        m = re.match(r"\s*(?:void )?<unnamed>::(\w+).*\| Executed Instructions = ([0-9.]+) inst", line)
+        if m and m.group(1) not in out:
+            out[m.group(1)] = float(m.group(2))
+    return out, os.path.relpath(files[-1], ROOT)
+
+
 def _traffic():
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     --set full capture (profiles/), or None."""
@@ -638,6 +654,24 @@ def run_ours(args):
     bwd_bytes = 96.0 * Nk + 80.0 * Nk + 32.0 * HW + 16.0 * LP
     achieved = bwd_bytes / (bwd_ms / 1e3) / 1e9
     view_bytes = 176.0 * N_SURFELS + 352.0 * Nk + 236.0 * P + 40.0 * HW
+    # issue-slot roofline of the two rasterisers (issue-bound: nothing on the
+    # path is a contraction, so the SM's instruction issue rate -- 4 warp
+    # instructions per clock per SM -- is their ceiling, not HBM)
+    instr, instr_src = _ncu_instructions()
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    issue_peak = sms * 4 * mhz * 1e6
+    issue = {"unit": "warp instructions/s", "peak": issue_peak,
+             "peak_basis": f"{sms} SMs x 4 issue slots x {mhz:.0f} MHz (median SM clock under load)",
+             "instructions_source": instr_src, "kernels": {}}
+    for name, kern, ms in (("train_forward", ("raster_fwd_kernel",), iso.get("train_forward")),
+                           ("train_backward", ("splat_bwd_kernel", "big_bwd_kernel"), iso.get("train_backward"))):
+        n_instr = sum(instr.get(k, 0.0) for k in kern)
+        if n_instr and ms:
+            t = float(np.mean(ms)) / 1e3
+            issue["kernels"][name] = {"warp_instructions_per_launch": n_instr, "launch_ms": t * 1e3,
+                                      "achieved": n_instr / t, "frac": n_instr / t / issue_peak,
+                                      "ncu_kernels": list(kern)}
     cpu = None
     if world == 1 and not args.no_cpu:
         dt, cores, sample = cpu_oracle_view()
@@ -663,6 +697,7 @@ def run_ours(args):
                                "step with the views serialised (avg_launch_ms); in the timed 3-stream step the "
                                "same events also span the other streams' kernels (avg_launch_ms_in_step)",
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json)"},
+        "issue_roofline": issue,
         "view_roofline": {"bytes_per_view": view_bytes,
                           "achieved_gbs": view_bytes * VIEWS_PER_STEP / world / (step_ms / 1e3) / 1e9,
                           "frac": view_bytes * VIEWS_PER_STEP / world / (step_ms / 1e3) / 1e9 / peak},
