@@ -329,7 +329,7 @@ constexpr int kNdcSmem = 4096;  // W + H up to this: pixel-centre tables staged 
 #define SS_SPLAT_GRID SS_SPLAT_MINB  // persistent CTAs launched per SM
 #endif
 #ifndef SS_SCAT_ITEMS
-#define SS_SCAT_ITEMS 8
+#define SS_SCAT_ITEMS 16
 #endif
 constexpr int kScatItems = SS_SCAT_ITEMS;  // records per thread of the class scatter
 constexpr int kHeavyClass = 32 * 4;  // area >= 64 px: one round per work-counter ticket (else 8)
