@@ -369,6 +369,21 @@ int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreproc
                       int color_source, const SsEnv *env, const int8_t *cull,
                       const float *rec_acc, const double *rec_acc64, const uint32_t *shade_cells,
                       const SsGrads *grads, void *stream);
+/* ss_chain_backward inside a training step whose prepass (ss_surfel_prepass,
+ * this step's parameters and env) is given: the shading adjoint takes the
+ * normal's diffuse lookup, texel derivatives and coord_grad_to_dir map from
+ * the prepass, and instead of scattering the diffuse-lookup upstream into
+ * grads->d_diffuse4 through the four bilinear taps per view it adds it per
+ * surfel into g_ld (n x 4 floats, rgb + pad; zero before the step's first
+ * view); ss_diffuse_scatter then applies the (view independent) taps once per
+ * step into d_diffuse (He x We x 3 doubles, +=) and zeroes g_ld.  Same result
+ * as the per-view scatter up to float summation order
+ * (bilinear_scatter, shading.py:248-260, 583-597). */
+int ss_chain_backward_prepared(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                               int color_source, const SsEnv *env, const int8_t *cull,
+                               const float *rec_acc, const double *rec_acc64, const uint32_t *shade_cells,
+                               const SsGrads *grads, const void *prepass, float *g_ld, void *stream);
+int ss_diffuse_scatter(int n, const SsEnv *env, const void *prepass, float *g_ld, double *d_diffuse, void *stream);
 
 /* ss_env_grad_merge: dst[3 t + c] += src4[4 t + c] (float64 += float32) for
  * t < texels, c < 3, and zeroes src4 (the per-view derived-map accumulators

@@ -86,6 +86,8 @@ _SIGNATURES = {
     "ss_raster_backward": [ctypes.c_int, ctypes.c_int, ctypes.c_int, c_p, c_p, c_p, c_p,
                            ctypes.POINTER(ctypes.c_float), ctypes.c_int, c_p, c_p, ctypes.c_float, c_p, c_p, c_p],
     "ss_chain_backward": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_chain_backward_prepared": [c_p, c_p, c_p, ctypes.c_int, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p],
+    "ss_diffuse_scatter": [ctypes.c_int, c_p, c_p, c_p, c_p, c_p],
     "ss_brdf_lut": [ctypes.c_int, ctypes.c_int, c_p, c_p],
     "ss_env_khat_words": [ctypes.c_int, ctypes.c_int],
     "ss_env_khat": [ctypes.c_int, ctypes.c_int, c_p, c_p],

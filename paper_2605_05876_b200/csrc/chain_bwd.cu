@@ -8,6 +8,7 @@
 // gradients + stats (multi-view steps accumulate in place, no extra pass).
 #include "ss_common.cuh"
 #include "shading.cuh"
+#include "prepass.cuh"
 
 namespace {
 
@@ -24,6 +25,9 @@ struct ChainParams {
     const float *acc;
     const double *acc64;  // float64 rows of the big records (SS_ACC_F64)
     const uint4 *cells;   // nullable: the forward's packed shading branch state
+    const PreDiff *pre_diff;  // nullable: the step's float32 diffuse state (ss_chain_backward_prepared)
+    float4 *g_ld;             // with pre_diff: per-surfel sum of the diffuse-lookup upstream (the taps
+                              // are view independent: ss_diffuse_scatter applies them once per step)
     SsGrads g;
 };
 
@@ -154,6 +158,10 @@ typedef double TT;
 #ifndef SS_CHAIN_MINB
 #define SS_CHAIN_MINB 4
 #endif
+// kPre: the step's prepass diffuse state and per-surfel diffuse upstream
+// (ss_chain_backward_prepared); a separate instantiation, so the per-view
+// path keeps its register allocation
+template <bool kPre>
 __global__ void __launch_bounds__(128, SS_CHAIN_MINB) chain_kernel(ChainParams P)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -314,7 +322,8 @@ __global__ void __launch_bounds__(128, SS_CHAIN_MINB) chain_kernel(ChainParams P
             // the preprocess kernel's float64 branch decisions, float32 state
             // with the texel derivatives read together with the values
             ss_shade_inputs(cl, i, P.cam_pos, in);
-            ss_shade_forward_cells(in, P.env, __ldg(P.cells + i), st);
+            ss_shade_forward_cells(in, P.env, __ldg(P.cells + i), st,
+                                   kPre ? reinterpret_cast<const float *>(P.pre_diff + i) : nullptr);
             ss_shade_backward<float, true>(in, st, P.env, gcf, sg);
         } else {
             ShadeIn<double> in64;
@@ -352,9 +361,13 @@ __global__ void __launch_bounds__(128, SS_CHAIN_MINB) chain_kernel(ChainParams P
                     scatter_rgb4<false>(P.g.d_specular4, lvs[h] * T + sidx[k], sg.g_ls[0] * f, sg.g_ls[1] * f,
                                         sg.g_ls[2] * f);
                 }
-            for (int k = 0; k < 4; ++k) {
-                const float f = (float)dcw[k];
-                scatter_rgb4<true>(P.g.d_diffuse4, didx[k], sg.g_ld[0] * f, sg.g_ld[1] * f, sg.g_ld[2] * f);
+            if (kPre) {  // per surfel; the step's one diffuse scatter applies the taps
+                red_add4(reinterpret_cast<float *>(P.g_ld + i), sg.g_ld[0], sg.g_ld[1], sg.g_ld[2], 0.f);
+            } else {
+                for (int k = 0; k < 4; ++k) {
+                    const float f = (float)dcw[k];
+                    scatter_rgb4<true>(P.g.d_diffuse4, didx[k], sg.g_ld[0] * f, sg.g_ld[1] * f, sg.g_ld[2] * f);
+                }
             }
         } else if (!P.g.d_specular4) {
             for (int h = 0; h < 2; ++h)  // level lvs[h] texel sidx[k] = element 3 * (lvs[h] * T + sidx[k])
@@ -409,10 +422,10 @@ extern "C" int ss_env_grad_merge(int64_t texels, float *src4, double *dst, void 
     return SS_OK;
 }
 
-extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
-                                 int color_source, const SsEnv *env, const int8_t *cull,
-                                 const float *rec_acc, const double *rec_acc64, const uint32_t *shade_cells,
-                                 const SsGrads *grads, void *stream)
+static int chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt, int color_source,
+                          const SsEnv *env, const int8_t *cull, const float *rec_acc, const double *rec_acc64,
+                          const uint32_t *shade_cells, const SsGrads *grads, const void *prepass, float *g_ld,
+                          void *stream)
 {
     if (!cloud || !cam || !opt || !grads) return SS_ERR_INVALID;
     if (cloud->n == 0) return SS_OK;
@@ -434,7 +447,65 @@ extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, cons
     P.env = env ? *env : SsEnv{};
     P.cull = cull; P.acc = rec_acc; P.acc64 = rec_acc64; P.g = *grads;
     P.cells = reinterpret_cast<const uint4 *>(shade_cells);
-    chain_kernel<<<(cloud->n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P);
+    const bool pre = prepass && g_ld && shade_cells && color_source == SS_COLOR_IBL && env && env->diffuse4;
+    P.pre_diff = pre ? prepass_diff(prepass, cloud->n) : nullptr;
+    P.g_ld = pre ? reinterpret_cast<float4 *>(g_ld) : nullptr;
+    if (pre) chain_kernel<true><<<(cloud->n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P);
+    else chain_kernel<false><<<(cloud->n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(P);
+    SS_CUDA_CHECK_LAUNCH();
+    return SS_OK;
+}
+
+extern "C" int ss_chain_backward(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                                 int color_source, const SsEnv *env, const int8_t *cull,
+                                 const float *rec_acc, const double *rec_acc64, const uint32_t *shade_cells,
+                                 const SsGrads *grads, void *stream)
+{
+    return chain_backward(cloud, cam, opt, color_source, env, cull, rec_acc, rec_acc64, shade_cells, grads, nullptr,
+                          nullptr, stream);
+}
+
+extern "C" int ss_chain_backward_prepared(const SsCloud *cloud, const SsCamera *cam, const SsPreprocessOpts *opt,
+                                          int color_source, const SsEnv *env, const int8_t *cull,
+                                          const float *rec_acc, const double *rec_acc64,
+                                          const uint32_t *shade_cells, const SsGrads *grads, const void *prepass,
+                                          float *g_ld, void *stream)
+{
+    if (!prepass || !g_ld) return SS_ERR_INVALID;
+    return chain_backward(cloud, cam, opt, color_source, env, cull, rec_acc, rec_acc64, shade_cells, grads, prepass,
+                          g_ld, stream);
+}
+
+namespace {
+// d_diffuse += the step's diffuse-lookup upstream of every surfel through its
+// four bilinear taps (bilinear_scatter, shading.py:248-260, 583-597): the
+// cell and fractions are the normal's, so the per-view scatter folds into one
+// per step; g_ld is zeroed for the next step.
+__global__ void diffuse_scatter_kernel(int n, int we, const PreShade *__restrict__ sh, const PreDiff *__restrict__ pd,
+                                       float4 *__restrict__ g_ld, double *__restrict__ d_diffuse) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 g = g_ld[i];
+    if (g.x == 0.f && g.y == 0.f && g.z == 0.f) return;
+    g_ld[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const unsigned cell = sh[i].cell;
+    const int i0 = (int)(cell & 0xffffu), j0 = (int)(cell >> 16);
+    const int i1 = i0 + 1 == we ? 0 : i0 + 1, j1 = j0 + 1;
+    const double tu = pd[i].tu, tv = pd[i].tv;
+    const int idx[4] = {j0 * we + i0, j0 * we + i1, j1 * we + i0, j1 * we + i1};
+    const double w[4] = {(1.0 - tu) * (1.0 - tv), tu * (1.0 - tv), (1.0 - tu) * tv, tu * tv};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) scatter_rgb(d_diffuse, idx[k], g.x * w[k], g.y * w[k], g.z * w[k]);
+}
+}  // namespace
+
+extern "C" int ss_diffuse_scatter(int n, const SsEnv *env, const void *prepass, float *g_ld, double *d_diffuse,
+                                  void *stream)
+{
+    if (n < 0 || !env || !prepass || !g_ld || !d_diffuse) return SS_ERR_INVALID;
+    if (n == 0) return SS_OK;
+    diffuse_scatter_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        n, env->we, prepass_shade(prepass, n), prepass_diff(prepass, n), reinterpret_cast<float4 *>(g_ld), d_diffuse);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

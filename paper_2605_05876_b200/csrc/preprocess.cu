@@ -12,6 +12,7 @@
 #include "ss_common.cuh"
 #include "shading.cuh"
 #include "coverage.cuh"
+#include "prepass.cuh"
 
 namespace {
 
@@ -39,19 +40,7 @@ struct CamF {
 // shading inputs plus the diffuse lookup, computed once per step instead of
 // once per view, with exactly the preprocess kernel's operations (this file
 // is compiled with -fmad=false), so the records are bit-identical.
-struct PreGeom {
-    float su0, su1, su2, sv0;
-    float sv1, sv2;
-    int finite, zero_norm;
-};
-struct PreShade {
-    double n[3], l_d[3];
-    float alb[3], m, r;
-    uint32_t cell;   // diffuse cell i0 | j0 << 16
-    uint32_t dv_ok;  // diffuse dv_ok
-    uint32_t pad;
-};
-static_assert(sizeof(PreGeom) == 32 && sizeof(PreShade) == 80, "prepass layout");
+// (PreGeom, PreShade, PreDiff: prepass.cuh)
 
 // quat_to_frame + exp(log_scales) in float32 (surfels.py:40-51), the
 // preprocess kernel's expressions
@@ -69,7 +58,7 @@ __device__ __forceinline__ void scaled_frame(float4 q, float2 ls, float &nrm, fl
 
 __global__ void __launch_bounds__(256) surfel_prepass_kernel(SsCloud cloud, SsEnv env, int shade,
                                                              PreGeom *__restrict__ geom,
-                                                             PreShade *__restrict__ sh) {
+                                                             PreShade *__restrict__ sh, PreDiff *__restrict__ pd) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cloud.n) return;
     const float4 q = reinterpret_cast<const float4 *>(cloud.quats)[i];
@@ -98,6 +87,23 @@ __global__ void __launch_bounds__(256) surfel_prepass_kernel(SsCloud cloud, SsEn
     o.dv_ok = bd.dv_ok;
     o.pad = 0;
     sh[i] = o;
+    if (!env.diffuse4) return;
+    // the chain kernel's float32 diffuse state on this cell (its
+    // ss_shade_forward_cells / ss_shade_backward diffuse part, once per step)
+    ShadeIn<float> inf;
+    ss_shade_material(cloud, i, inf);
+    float fu, fv;
+    ss_dir_coords(inf.n, env.he, env.we, fu, fv);
+    const SsBil<float> b = ss_bil_forced(env.he, env.we, fu, fv, true, o.cell, true, bd.dv_ok);
+    PreDiff d;
+    ss_bil_lookup_grads4(reinterpret_cast<const float4 *>(env.diffuse4), env.we, b, d.l_d, d.gu, d.gv);
+    float ga[3], gb[3];
+    ss_coord_grad_to_dir(inf.n, env.he, env.we, 1.f, 0.f, ga);
+    ss_coord_grad_to_dir(inf.n, env.he, env.we, 0.f, 1.f, gb);
+    d.a0 = ga[0]; d.a1 = ga[1]; d.b2 = gb[2];
+    d.tu = b.tu; d.tv = b.tv;
+    d.pad[0] = d.pad[1] = 0.f;
+    pd[i] = d;
 }
 
 #ifndef SS_PRE_MINB
@@ -383,7 +389,7 @@ extern "C" int ss_pack_records(int k, const float *t1, const float *t2, const fl
 }
 
 extern "C" size_t ss_surfel_prepass_bytes(int n) {
-    return n < 0 ? 0 : (sizeof(PreGeom) + sizeof(PreShade)) * (size_t)n;
+    return n < 0 ? 0 : (sizeof(PreGeom) + sizeof(PreShade) + sizeof(PreDiff)) * (size_t)n;
 }
 
 extern "C" int ss_surfel_prepass(const SsCloud *cloud, const SsEnv *env, void *prepass, void *stream)
@@ -393,8 +399,9 @@ extern "C" int ss_surfel_prepass(const SsCloud *cloud, const SsEnv *env, void *p
     const bool shade = env && env->diffuse && env->diffuse64 && env->specular64;
     PreGeom *g = reinterpret_cast<PreGeom *>(prepass);
     PreShade *sh = reinterpret_cast<PreShade *>(g + cloud->n);
+    PreDiff *pd = reinterpret_cast<PreDiff *>(sh + cloud->n);
     surfel_prepass_kernel<<<(cloud->n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(*cloud, env ? *env : SsEnv{},
-                                                                                     shade ? 1 : 0, g, sh);
+                                                                                     shade ? 1 : 0, g, sh, pd);
     SS_CUDA_CHECK_LAUNCH();
     return SS_OK;
 }

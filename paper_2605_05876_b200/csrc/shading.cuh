@@ -220,6 +220,9 @@ struct ShadeState {
     // texel derivatives of the lookups, when the forward kept them
     // (ss_shade_forward_cells): diffuse, specular lo / hi, LUT
     R dgu[3], dgv[3], sgu[2][3], sgv[2][3], lgu[2], lgv[2];
+    // the step's diffuse normal map (PreDiff): dL/dn = (gfu a0, gfu a1, gfv b2)
+    bool dpre;
+    R da0, da1, db2;
 };
 
 // Activated materials and normal of surfel i (view independent).
@@ -384,8 +387,11 @@ __device__ __forceinline__ SsBil<float> ss_bil_forced(int h, int w, float fu, fl
 // shade_surfels body in float32 on the branch state of the float64 forward
 // (ss_shade_pack): the state the adjoint needs, without re-deriving the
 // cells in float64.
+// pd (nullable): the step's float32 diffuse state (prepass.cuh PreDiff: l_d,
+// texel derivatives and the coord_grad_to_dir map of the normal), which the
+// lookup and its adjoint then take instead of re-deriving them per view.
 __device__ __forceinline__ void ss_shade_forward_cells(const ShadeIn<float> &in, const SsEnv &env, uint4 cells,
-                                                       ShadeState<float> &s) {
+                                                       ShadeState<float> &s, const float *pd = nullptr) {
     const int he = env.he, we = env.we, L = env.levels, LR = env.lut_res;
     const unsigned fl = cells.w >> 8;
     s.ndv_raw = (in.n[0] * in.wo[0] + in.n[1] * in.wo[1]) + in.n[2] * in.wo[2];
@@ -395,11 +401,23 @@ __device__ __forceinline__ void ss_shade_forward_cells(const ShadeIn<float> &in,
     const float ndv = ss_clip<float>(s.ndv_raw, 0.f, 1.f);
     for (int c = 0; c < 3; ++c) s.refl[c] = 2.f * s.ndv_raw * in.n[c] - in.wo[c];
     float fu, fv;
-    ss_dir_coords(in.n, he, we, fu, fv);
-    s.bd = ss_bil_forced(he, we, fu, fv, true, cells.x, true, (fl & 1u) != 0);
-    const float4 *d4 = reinterpret_cast<const float4 *>(env.diffuse4);
+    s.dpre = pd != nullptr;
+    if (pd) {  // PreDiff: l_d[3] gu[3] gv[3] a0 a1 b2 tu tv
+        const float4 p0 = reinterpret_cast<const float4 *>(pd)[0], p1 = reinterpret_cast<const float4 *>(pd)[1];
+        const float4 p2 = reinterpret_cast<const float4 *>(pd)[2], p3 = reinterpret_cast<const float4 *>(pd)[3];
+        s.l_d[0] = p0.x; s.l_d[1] = p0.y; s.l_d[2] = p0.z;
+        s.dgu[0] = p0.w; s.dgu[1] = p1.x; s.dgu[2] = p1.y;
+        s.dgv[0] = p1.z; s.dgv[1] = p1.w; s.dgv[2] = p2.x;
+        s.da0 = p2.y; s.da1 = p2.z; s.db2 = p2.w;
+        s.bd.i0 = (int)(cells.x & 0xffffu); s.bd.j0 = (int)(cells.x >> 16);
+        s.bd.i1 = s.bd.i0 + 1 == we ? 0 : s.bd.i0 + 1; s.bd.j1 = s.bd.j0 + 1;
+        s.bd.tu = p3.x; s.bd.tv = p3.y; s.bd.du_ok = true; s.bd.dv_ok = (fl & 1u) != 0;
+    } else {
+        ss_dir_coords(in.n, he, we, fu, fv);
+        s.bd = ss_bil_forced(he, we, fu, fv, true, cells.x, true, (fl & 1u) != 0);
+        ss_bil_lookup_grads4(reinterpret_cast<const float4 *>(env.diffuse4), we, s.bd, s.l_d, s.dgu, s.dgv);
+    }
     const float4 *s4 = reinterpret_cast<const float4 *>(env.specular4);
-    ss_bil_lookup_grads4(d4, we, s.bd, s.l_d, s.dgu, s.dgv);
     const float lvl = ss_clip<float>(in.r, 0.f, 1.f) * (L - 1);
     s.lvl0 = (int)(cells.w & 0xffu);
     s.frac = L > 1 ? lvl - (float)s.lvl0 : 0.f;
@@ -502,7 +520,11 @@ __device__ __forceinline__ void ss_shade_backward(const ShadeIn<R> &in, const Sh
     R gfu = (o.g_ld[0] * gu[0] + o.g_ld[1] * gu[1]) + o.g_ld[2] * gu[2];
     R gfv = (o.g_ld[0] * gv[0] + o.g_ld[1] * gv[1]) + o.g_ld[2] * gv[2];
     R g_n[3];
-    ss_coord_grad_to_dir(in.n, he, we, gfu, gfv, g_n);
+    if (kStored && s.dpre) {
+        g_n[0] = gfu * s.da0; g_n[1] = gfu * s.da1; g_n[2] = gfv * s.db2;
+    } else {
+        ss_coord_grad_to_dir(in.n, he, we, gfu, gfv, g_n);
+    }
     R grn = (g_refl[0] * in.n[0] + g_refl[1] * in.n[1]) + g_refl[2] * in.n[2];
     R g_wo[3];
     for (int c = 0; c < 3; ++c) {

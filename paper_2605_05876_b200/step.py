@@ -296,6 +296,9 @@ class TrainStep:
         self._cl = _lib.make_cloud(cloud)
         # the step's view-independent per-surfel state (ss_surfel_prepass)
         self._prepass = torch.empty(int(self.lib.ss_surfel_prepass_bytes(self.n)), device=dev, dtype=torch.uint8)
+        # per-surfel diffuse-lookup upstream of the step's views (ss_chain_backward_prepared);
+        # ss_diffuse_scatter applies the taps once per step and re-zeroes it
+        self._g_ld = torch.zeros(4 * self.n, device=dev, dtype=torch.float32)
         self._prepared = False
         for b in self.bufs:
             b.gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
@@ -472,19 +475,30 @@ class TrainStep:
         # the chain kernels of concurrent views may overlap: their parameter
         # gradients are vector reductions (atomic), the derived-map sums go to
         # this buffer set's own float32 maps
-        _lib.check(lib.ss_chain_backward(ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po),
-                                         _lib.SS_COLOR_IBL, ctypes.byref(self._envs), _lib.ptr(b.cull),
-                                         _lib.ptr(b.acc), _lib.ptr(b.acc64),
-                                         _lib.ptr(b.cells) if self.color_source == _lib.SS_COLOR_IBL else None,
-                                         ctypes.byref(b.gs), s),
-                   "ss_chain_backward")
-        # fold this view's float32 derived-map sums into the buffer set's
-        # float64 ones (same stream: no ordering with the other sets)
-        _lib.check(lib.ss_env_grad_merge(b.d_diff4.numel() // 4, _lib.ptr(b.d_diff4), _lib.ptr(b.d_diffuse64), s),
-                   "ss_env_grad_merge")
+        args = (ctypes.byref(self._cl), ctypes.byref(camst), ctypes.byref(self._po), _lib.SS_COLOR_IBL,
+                ctypes.byref(self._envs), _lib.ptr(b.cull), _lib.ptr(b.acc), _lib.ptr(b.acc64),
+                _lib.ptr(b.cells) if self.color_source == _lib.SS_COLOR_IBL else None, ctypes.byref(b.gs))
+        if self._diffuse_per_step():
+            # the diffuse taps are applied once per step (ss_diffuse_scatter at the join)
+            _lib.check(lib.ss_chain_backward_prepared(*args, _lib.ptr(self._prepass), _lib.ptr(self._g_ld), s),
+                       "ss_chain_backward_prepared")
+        else:
+            _lib.check(lib.ss_chain_backward(*args, s), "ss_chain_backward")
+            # fold this view's float32 derived-map sums into the buffer set's
+            # float64 ones (same stream: no ordering with the other sets)
+            _lib.check(lib.ss_env_grad_merge(b.d_diff4.numel() // 4, _lib.ptr(b.d_diff4), _lib.ptr(b.d_diffuse64),
+                                             s), "ss_env_grad_merge")
         _lib.check(lib.ss_env_grad_merge(b.d_spec4.numel() // 4, _lib.ptr(b.d_spec4), _lib.ptr(b.d_spec64), s),
                    "ss_env_grad_merge")
         self._ev_end(ev)
+
+    def _diffuse_per_step(self):
+        """Inside a step with the IBL prepass (float32 and float64 maps): the
+        chain's diffuse lookup state comes from the prepass and its env taps are
+        applied once per step (ss_diffuse_scatter at the join)."""
+        e = self._envs
+        return (self._prepared and self.color_source == _lib.SS_COLOR_IBL and e is not None and
+                bool(e.diffuse4) and bool(e.diffuse) and bool(e.diffuse64) and bool(e.specular64))
 
     def _run_views(self, cameras, targets_for, target_done=None, masks=None):
         """Issue every view, alternating the worker streams (view i uses stream
@@ -494,6 +508,7 @@ class TrainStep:
         _lib.check(self.lib.ss_surfel_prepass(ctypes.byref(self._cl), ctypes.byref(self._envs),
                                               _lib.ptr(self._prepass), _lib.stream_ptr()), "ss_surfel_prepass")
         self._prepared = True
+        diffuse_per_step = self._diffuse_per_step()
         for st in self.streams:
             st.wait_stream(main)
         nst = min(len(self.streams), self.active_streams or len(self.streams))
@@ -514,6 +529,10 @@ class TrainStep:
             self._prepared = False
         for st in self.streams:
             main.wait_stream(st)
+        if diffuse_per_step:
+            _lib.check(self.lib.ss_diffuse_scatter(self.n, ctypes.byref(self._envs), _lib.ptr(self._prepass),
+                                                   _lib.ptr(self._g_ld), _lib.ptr(self.d_diffuse),
+                                                   _lib.stream_ptr()), "ss_diffuse_scatter")
         for b in self.bufs[1:nst]:  # the other sets' derived-map sums into the step's
             self.d_diffuse.add_(b.d_diffuse64)
             self.d_spec.add_(b.d_spec64)
