@@ -267,9 +267,13 @@ class TrainStep:
         self.active_streams = None     # None: all worker streams; 1: views serialised (isolated kernel timing)
         self._stage = None
         # preprocess, scan + order, scatter, tile sort x2, train fwd, ndc, area class, class scatter,
-        # record bwd, big-rect bwd, big-rect finish, chain, env merge x2
-        self.launches_per_view = 15
-        self.launches_per_step_fixed = 4 + 1 + 4  # env adjoint, fused Adam (+ quat renorm), env refresh
+        # record bwd, big-rect bwd, big-rect finish, chain, env merge (specular; + diffuse when the
+        # diffuse taps are scattered per view)
+        self.launches_per_view = 14
+        # prepass, diffuse scatter, env adjoint (spectral diffuse 3, specular SpMV, finish), fused
+        # Adam (+ quat renorm), env refresh (exp, narrow, spectral diffuse 3, specular SpMV) --
+        # the ncu launch list of profiles/r2j_launches.txt
+        self.launches_per_step_fixed = 1 + 1 + 5 + 1 + 6
 
     # -- buffers -----------------------------------------------------------
     def _bind_cloud(self, cloud):
