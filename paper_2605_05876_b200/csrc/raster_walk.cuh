@@ -84,7 +84,7 @@ struct RecGeo {
 };
 
 #ifndef SS_PACK_SLOTS
-#define SS_PACK_SLOTS 16
+#define SS_PACK_SLOTS 20
 #endif
 constexpr int kSlots = SS_PACK_SLOTS;  // overlapping records per chunk (<= 32)
 
