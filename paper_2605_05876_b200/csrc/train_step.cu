@@ -316,7 +316,10 @@ constexpr int kHugeArea = 8 * kBigChunk;  // big rects above this are spread ove
 constexpr int kBigArea = 512;  // rects above this go to the CTA-chunked kernel (~0.1% of records)
 constexpr int kNB = 256;       // (area class, coverage-fraction bucket) classes of the other records
 constexpr int kGL = 8;         // lanes per record group (4 records per warp)
-constexpr int kGCap = 128;     // rect pixels compacted per group pass
+#ifndef SS_GCAP
+#define SS_GCAP 128
+#endif
+constexpr int kGCap = SS_GCAP;  // rect pixels compacted per group pass
 #ifndef SS_SPLAT_WARPS
 #define SS_SPLAT_WARPS 8
 #endif
