@@ -335,7 +335,14 @@ constexpr int kNdcSmem = 4096;  // W + H up to this: pixel-centre tables staged 
 #define SS_SCAT_ITEMS 16
 #endif
 constexpr int kScatItems = SS_SCAT_ITEMS;  // records per thread of the class scatter
-constexpr int kHeavyClass = 32 * 4;  // area >= 64 px: one round per work-counter ticket (else 8)
+#ifndef SS_HEAVY_CLASS
+#define SS_HEAVY_CLASS (32 * 4)
+#endif
+#ifndef SS_LIGHT_ROUNDS
+#define SS_LIGHT_ROUNDS 8
+#endif
+constexpr int kHeavyClass = SS_HEAVY_CLASS;  // area >= 64 px: one round per work-counter ticket
+constexpr int kLightRounds = SS_LIGHT_ROUNDS;  // rounds per ticket of the lighter classes
 
 // Scratch layout (32-bit words after the two NDC tables), see
 // ss_train_backward_scratch_words: 8 counters (medium / huge queue sizes,
@@ -512,12 +519,12 @@ __global__ void __launch_bounds__(32 * kSplatWarps, SS_SPLAT_MINB) splat_bwd_ker
     const int nrounds = (nsmall + 3) >> 2, hrounds = (counters[5] + 3) >> 2;
     int32_t *work = counters + 2;
     int rend = 0;
-    auto grab = [&]() {  // ticket -> first round: heavy rounds one by one, then blocks of 8
+    auto grab = [&]() {  // ticket -> first round: heavy rounds one by one, then blocks of kLightRounds
         int t = 0;
         if (lane == 0) t = atomicAdd(work, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
-        const int b = t < hrounds ? t : hrounds + (t - hrounds) * 8;
-        rend = t < hrounds ? b + 1 : b + 8;
+        const int b = t < hrounds ? t : hrounds + (t - hrounds) * kLightRounds;
+        rend = t < hrounds ? b + 1 : b + kLightRounds;
         return b;
     };
     auto issue = [&](int r, int buf) {  // cp.async of round r's records into slot buf
