@@ -298,11 +298,17 @@ class TrainStep:
         self.loss_f = self.pack.loss
         self.view_count = self.pack.view_count
         self._cl = _lib.make_cloud(cloud)
-        # the step's view-independent per-surfel state (ss_surfel_prepass)
-        self._prepass = torch.empty(int(self.lib.ss_surfel_prepass_bytes(self.n)), device=dev, dtype=torch.uint8)
-        # per-surfel diffuse-lookup upstream of the step's views (ss_chain_backward_prepared);
-        # ss_diffuse_scatter applies the taps once per step and re-zeroes it
-        self._g_ld = torch.zeros(4 * self.n, device=dev, dtype=torch.float32)
+        # the step's view-independent per-surfel state (ss_surfel_prepass) and the
+        # per-surfel diffuse-lookup upstream of its views (ss_chain_backward_prepared;
+        # ss_diffuse_scatter applies the taps once per step and re-zeroes it): sized
+        # for the surfel capacity, so a refinement step's rebinding does not reallocate
+        cap = self.surfel_capacity
+        if getattr(self, "_prepass_cap", 0) < cap:
+            self._prepass = torch.empty(int(self.lib.ss_surfel_prepass_bytes(cap)), device=dev, dtype=torch.uint8)
+            self._g_ld = torch.zeros(4 * cap, device=dev, dtype=torch.float32)
+            self._prepass_cap = cap
+        else:
+            self._g_ld[:4 * self.n].zero_()
         self._prepared = False
         for b in self.bufs:
             b.gs = _lib.SsGrads(*(_lib.ptr(self.grads[k]) for k in PARAMS), None, _lib.ptr(self.grads["ss_grad"]),
