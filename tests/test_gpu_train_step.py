@@ -324,3 +324,30 @@ def test_graph_replay_matches_eager():
     ts.gradients(cams[:1], targets[:1])
     for k in PARAMS:
         torch.testing.assert_close(want[k], ts.grads[k], rtol=1e-5, atol=1e-6 * float(ts.grads[k].abs().max()))
+
+
+def test_diffuse_taps_per_step_equal_per_view():
+    """ss_chain_backward_prepared + ss_diffuse_scatter (the normal's diffuse
+    lookup from the step prepass, its bilinear taps applied once per step) vs
+    the per-view scatter of ss_chain_backward: the same derived-map gradient
+    and parameter gradients up to float summation order."""
+    init, env_base, cams, targets = _scene()
+    out = {}
+    for per_step in (True, False):
+        ts = TrainStep(ss.SurfelCloud(**init), ss.EnvironmentLight.from_base(env_base), 96, 96, streams=1)
+        if not per_step:
+            ts._diffuse_per_step = lambda: False
+        ts.gradients(cams, targets)
+        torch.cuda.synchronize()
+        out[per_step] = ({k: ts.grads[k].clone() for k in PARAMS}, ts.d_diffuse.clone(), ts.g_env_log.clone())
+    (ga, da, ea), (gb, db, eb) = out[True], out[False]
+    assert float(da.abs().max()) > 0
+    # the float32 per-view maps vs the float32 per-surfel view sums: texels whose
+    # contributions cancel differ beyond 1e-5 of themselves, so the bar is the
+    # gradient tolerance of every parity test (rel 1e-3, floor 1e-5 x max)
+    assert grad_close(da, db)[0] == 0, grad_outliers(da, db)
+    assert grad_close(ea, eb)[0] == 0, grad_outliers(ea, eb)
+    for k in PARAMS:
+        assert grad_close(ga[k], gb[k])[0] == 0, (k, grad_outliers(ga[k], gb[k]))
+    # and far inside it in aggregate
+    assert float((da - db).abs().max()) <= 1e-4 * float(db.abs().max())
